@@ -1,0 +1,207 @@
+/*
+ * gsim_gpu.h — C ABI of the B200-native multi-camera RGB-D Gaussian-splat renderer.
+ *
+ * This is the drop-in boundary for the reference's render path
+ * (/root/reference/proj/core/include/gsim/raster.hpp:54-67):
+ *
+ *   std::vector<ProjectedSplat> project(const GaussianField&, const std::vector<SceneNode>&,
+ *                                       const CameraModel&);                 raster.hpp:54-56
+ *   RenderTarget rasterize(const std::vector<ProjectedSplat>&, const CameraModel&,
+ *                          const RasterOptions& = {});                       raster.hpp:59-60
+ *   std::vector<RenderTarget> render(const GaussianField&, const std::vector<SceneNode>&,
+ *                                    const std::vector<CameraModel>&,
+ *                                    const RasterOptions& = {});             raster.hpp:64-67
+ *   void transform_primitives(GaussianField&, const IndexRange&,
+ *                             const RigidTransform&);                        gaussian.hpp:76-77
+ *
+ * Plain C: pointers, sizes and POD structs only, no C++ or torch types. Every entry point
+ * returns a status that mirrors the reference CLI contract (tools/gsim.cpp:366-375,
+ * errors.hpp:12-25): 0 = ok, 1 = io/runtime (CUDA) failure, 2 = validation error.
+ * The message of the last failure on a context is available from gsim_gpu_last_error().
+ *
+ * Ownership: inputs are read during the call and never retained (the scene upload copies
+ * the field into device memory). Host outputs are written by the time a host-output call
+ * returns. Calls on one context are serialised by an internal mutex; different contexts
+ * (one per device) run concurrently.
+ */
+#ifndef GSIM_GPU_H
+#define GSIM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSIM_OK 0
+#define GSIM_ERR_IO 1
+#define GSIM_ERR_VALIDATION 2
+
+#define GSIM_NODE_BACKGROUND 0  /* NodeKind::background, gaussian.hpp:64 */
+#define GSIM_NODE_INTERACTIVE 1 /* NodeKind::interactive */
+#define GSIM_ENV_ALL (-1)       /* node visible to every camera (the reference's only mode) */
+
+/* RigidTransform (math.hpp:217-239): x -> R(q) x + t, q stored (w, x, y, z). */
+typedef struct gsim_rigid {
+    double rotation[4];
+    double translation[3];
+} gsim_rigid;
+
+/* GaussianField (gaussian.hpp:53-60) as strided double views. A stride is the distance,
+ * in doubles, between consecutive primitives, so the reference's AoS GaussianPrimitive
+ * array (stride 59) and SoA numpy arrays (strides 3, 3, 4, 1, 48) are both valid views.
+ * sh holds 48 coefficients per primitive, channel-major sh[c*16 + k] (gaussian.hpp:16-19). */
+typedef struct gsim_field_view {
+    uint64_t count;
+    int32_t sh_degree; /* 0..3, global across the field (scene.cpp:92) */
+    int32_t reserved;
+    const double* means;
+    uint64_t means_stride;
+    const double* scales; /* linear, > 0 */
+    uint64_t scales_stride;
+    const double* rotations; /* unit quaternion (w, x, y, z) */
+    uint64_t rotations_stride;
+    const double* opacities; /* post-sigmoid, (0, 1) */
+    uint64_t opacities_stride;
+    const double* sh;
+    uint64_t sh_stride;
+} gsim_field_view;
+
+/* SceneNode (gaussian.hpp:66-71) plus an environment tag for batched rendering.
+ * env == GSIM_ENV_ALL reproduces the reference exactly; env >= 0 restricts the node to the
+ * cameras whose env equals it (BASELINE configs 2 and 4: shared background, per-env objects). */
+typedef struct gsim_node {
+    uint64_t begin; /* IndexRange, end exclusive */
+    uint64_t end;
+    gsim_rigid pose;
+    int32_t kind;
+    int32_t env;
+} gsim_node;
+
+/* CameraModel (camera.hpp:14-33): pose maps world -> camera (x right, y down, z forward). */
+typedef struct gsim_camera {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    gsim_rigid pose;
+    double near_plane, far_plane;
+    int32_t env; /* which environment's nodes this camera sees (ignored for GSIM_ENV_ALL nodes) */
+    int32_t reserved;
+} gsim_camera;
+
+/* RasterOptions (raster.hpp:31-36). */
+typedef struct gsim_raster_options {
+    int32_t normalize_depth;
+    int32_t reserved;
+    double transmittance_cutoff;
+} gsim_raster_options;
+
+/* ProjectedSplat (raster.hpp:20-29), identical memory layout (120 bytes). */
+typedef struct gsim_projected_splat {
+    double pixel_center[2];
+    double cov_xx, cov_xy, cov_yy;
+    double inv_xx, inv_xy, inv_yy;
+    double view_depth;
+    double alpha_peak;
+    double rgb[3];
+    double radius;
+    uint32_t prim_index;
+    uint32_t reserved;
+} gsim_projected_splat;
+
+/* RenderTarget (image.hpp:38-45): row-major float images, rgb interleaved (W*H*3). */
+typedef struct gsim_target {
+    float* rgb;
+    float* depth;
+    float* accum_alpha;
+} gsim_target;
+
+/* Counters and per-stage device times (ms) of the last render on a context. */
+typedef struct gsim_render_stats {
+    uint64_t slots;        /* (camera, primitive) candidates */
+    uint64_t visible;      /* records that touch at least one tile (V) */
+    uint64_t pairs;        /* (tile, record) pairs (P) */
+    uint64_t tiles;        /* total tiles over all cameras */
+    uint64_t launches;     /* kernels launched by the last render */
+    uint64_t launches_total; /* kernels launched on this context since creation */
+    uint32_t depth_passes; /* radix passes over the depth digits (pre-duplication) */
+    uint32_t tile_passes;  /* radix passes over the camera|tile digits (post-duplication) */
+    /* per-stage device milliseconds, filled when profiling is on (gsim_gpu_set_profiling) */
+    float ms_preprocess;
+    float ms_depth_sort;
+    float ms_duplicate;
+    float ms_tile_sort;
+    float ms_ranges;
+    float ms_raster;
+    float ms_total;
+    float reserved;
+} gsim_render_stats;
+
+typedef struct gsim_gpu_context gsim_gpu_context;
+typedef struct gsim_gpu_scene gsim_gpu_scene;
+
+const char* gsim_gpu_version(void);
+
+/* One context per device: a CUDA stream plus grow-only device workspaces. */
+int gsim_gpu_context_create(int device, gsim_gpu_context** out);
+int gsim_gpu_context_destroy(gsim_gpu_context* ctx);
+/* Message of the last failure on ctx (ctx may be NULL for a failed create). */
+const char* gsim_gpu_last_error(const gsim_gpu_context* ctx);
+/* The context's cudaStream_t, for callers that time or order work around it. */
+void* gsim_gpu_stream(gsim_gpu_context* ctx);
+int gsim_gpu_synchronize(gsim_gpu_context* ctx);
+int gsim_gpu_set_profiling(gsim_gpu_context* ctx, int enable);
+int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out);
+
+/* Device-resident scene: the field is validated (gaussian.cpp:13-30 rules on sh_degree) and
+ * copied once; renders then read it from HBM. Replaces re-reading the AoS double field on
+ * every render() call. */
+int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* field,
+                          gsim_gpu_scene** out);
+int gsim_gpu_scene_destroy(gsim_gpu_scene* scene);
+uint64_t gsim_gpu_scene_size(const gsim_gpu_scene* scene);
+/* transform_primitives (gaussian.cpp:65-79) in place on the device-resident field (K1). */
+int gsim_gpu_transform_primitives(gsim_gpu_context* ctx, gsim_gpu_scene* scene, uint64_t begin,
+                                  uint64_t end, const gsim_rigid* transform);
+/* Copies the device field's means (count*3) and rotations (count*4) back; either may be NULL. */
+int gsim_gpu_scene_download(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, double* means,
+                            double* rotations);
+
+/* project (raster.cpp:135-232): visible splats in primitive order. Writes at most
+ * capacity splats to out and the visible count to *count (count may exceed capacity). */
+int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                     uint64_t n_nodes, const gsim_camera* camera, gsim_projected_splat* out,
+                     uint64_t capacity, uint64_t* count);
+
+/* rasterize (raster.cpp:234-323) of host splats into a host target. */
+int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats, uint64_t n,
+                       const gsim_camera* camera, const gsim_raster_options* options,
+                       gsim_target* out);
+
+/* render (raster.cpp:325-334): one host target per camera; returns after the copies land. */
+int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                    uint64_t n_nodes, const gsim_camera* cameras, uint64_t n_cameras,
+                    const gsim_raster_options* options, gsim_target* outs);
+
+/* render into device memory, asynchronous on the context stream. device_out holds, per
+ * camera in order, [rgb W*H*3 | depth W*H | accum_alpha W*H] floats (20 B per pixel);
+ * NULL renders into an internal buffer (see gsim_gpu_device_output). */
+int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                           const gsim_node* nodes, uint64_t n_nodes, const gsim_camera* cameras,
+                           uint64_t n_cameras, const gsim_raster_options* options,
+                           float* device_out);
+/* Device pointer of the internal output buffer of the last render_device(NULL) call. */
+float* gsim_gpu_device_output(gsim_gpu_context* ctx);
+
+/* Sorted tile lists of one camera of the last render/rasterize on ctx (test hook for the
+ * reference's pair sort, raster.cpp:243-271): tile_begin gets tiles_x*tiles_y+1 offsets,
+ * values gets the primitive index (render) or splat index (rasterize) of each pair in
+ * sorted order. *count = number of pairs of that camera (values may be NULL to query). */
+int gsim_gpu_tile_lists(gsim_gpu_context* ctx, uint32_t camera, uint32_t* tile_begin,
+                        uint32_t* values, uint64_t capacity, uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GSIM_GPU_H */

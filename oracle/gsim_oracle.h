@@ -1,0 +1,88 @@
+/*
+ * gsim_oracle.h — CPU restatement of the reference render path. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+ * load this library, and only as the checker (or the timed CPU baseline). The product path
+ * (paper_2507_21981_b200, libgsim_gpu.so) never links or calls it.
+ *
+ * Restates in plain C, in double precision and in the reference's operation order:
+ *   project            raster.cpp:135-232      rasterize           raster.cpp:234-323
+ *   reference_rasterize reference_raster.cpp:12-67   render        raster.cpp:325-334
+ *   shade_sh           sh.cpp:10-51            transform_primitives gaussian.cpp:65-79
+ *   CameraModel::look_at raster.cpp:94-111     Quat::from_matrix   math.hpp:158-187
+ *   oracle::random_field tests/support/test_oracles.cpp:144-168 (std::mt19937_64 and
+ *       libstdc++'s uniform_real_distribution<double> restated bit-exactly)
+ *   hash_target (FNV-1a)  hash.hpp:16-44
+ *
+ * Parity pin: tests/test_oracle_pin.py checks every function against the reference itself
+ * (oracle/_ref/libgsim_ref.so, compiled from /root/reference sources by oracle/Makefile) and
+ * against the committed golden fixtures in tests/golden/ (made by tests/golden/make_golden.py
+ * from the reference).
+ */
+#ifndef GSIM_ORACLE_H
+#define GSIM_ORACLE_H
+
+#include <stdint.h>
+
+#include "../include/gsim_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- math / sensors --------------------------------------------------------------------- */
+void gso_shade_sh(const double* sh48, int degree, const double view_dir[3], double rgb[3]);
+void gso_look_at(const double eye[3], const double target[3], double fx, double fy, int width,
+                 int height, const double up[3], gsim_camera* out);
+/* camera.pose.inverse().translation (camera.hpp:23) */
+void gso_camera_center(const gsim_camera* cam, double out[3]);
+void gso_rigid_compose(const gsim_rigid* a, const gsim_rigid* b, gsim_rigid* out); /* a*b */
+void gso_rigid_inverse(const gsim_rigid* a, gsim_rigid* out);
+void gso_quat_from_axis_angle(const double axis[3], double angle, double q[4]);
+
+/* ---- the render path -------------------------------------------------------------------- */
+/* Returns GSIM_OK or GSIM_ERR_VALIDATION (bad camera / node range). Nodes with env >= 0 are
+ * seen only by cameras of that env (batched-env extension; env = -1 is the reference). */
+int gso_project(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+                const gsim_camera* camera, gsim_projected_splat* out, uint64_t capacity,
+                uint64_t* count);
+int gso_rasterize(const gsim_projected_splat* splats, uint64_t n, const gsim_camera* camera,
+                  const gsim_raster_options* options, float* rgb, float* depth, float* alpha);
+/* The sorted (tile, depth, splat) pair list of rasterize (raster.cpp:243-271): tile_begin
+ * gets tiles+1 offsets, values the splat index of each pair (NULL to query *count). */
+int gso_rasterize_lists(const gsim_projected_splat* splats, uint64_t n,
+                        const gsim_camera* camera, uint32_t* tile_begin, uint32_t* values,
+                        uint64_t capacity, uint64_t* count);
+int gso_reference_rasterize(const gsim_projected_splat* splats, uint64_t n,
+                            const gsim_camera* camera, const gsim_raster_options* options,
+                            float* rgb, float* depth, float* alpha);
+int gso_render(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+               const gsim_camera* cameras, uint64_t n_cameras,
+               const gsim_raster_options* options, gsim_target* outs);
+/* In place on means (stride 3) and rotations (stride 4). */
+int gso_transform_primitives(double* means, double* rotations, uint64_t count, uint64_t begin,
+                             uint64_t end, const gsim_rigid* transform);
+
+/* ---- deterministic fixtures ------------------------------------------------------------- */
+typedef struct gso_mt19937_64 {
+    uint64_t mt[312];
+    int index;
+} gso_mt19937_64;
+void gso_mt_seed(gso_mt19937_64* rng, uint64_t seed);
+uint64_t gso_mt_next(gso_mt19937_64* rng);
+double gso_uniform_real(gso_mt19937_64* rng, double a, double b);
+/* Arrays are SoA: means count*3, scales count*3, rotations count*4, opacities count,
+ * sh count*48 (zero beyond the degree). */
+void gso_random_field(uint64_t seed, uint64_t count, double box_extent, double scale_lo,
+                      double scale_hi, int sh_degree, double* means, double* scales,
+                      double* rotations, double* opacities, double* sh);
+
+uint64_t gso_hash_bytes(const void* data, uint64_t size, uint64_t seed);
+uint64_t gso_hash_target(const float* rgb, const float* depth, const float* alpha, int width,
+                         int height, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,329 @@
+"""ctypes front-end of the CPU checker. TEST INFRASTRUCTURE ONLY.
+
+    Oracle  -> oracle/liboracle.so        our plain-C restatement (gsim_oracle.c)
+    Ref     -> oracle/_ref/libgsim_ref.so the unmodified reference, compiled from its sources
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) may use
+this module, and only as the checker or the timed CPU baseline — never as a product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_2507_21981_b200 import abi
+from paper_2507_21981_b200.api import (CameraModel, GaussianField, RasterOptions, RenderTarget,
+                                       SceneNode)
+
+HERE = Path(__file__).resolve().parent
+ORACLE_LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libgsim_ref.so"
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+_vp = C.c_void_p
+
+
+def build_oracle(with_ref: bool = True) -> None:
+    """make -C oracle (liboracle.so always; _ref only where /root/reference exists)."""
+    target = "all" if with_ref else str(ORACLE_LIB)
+    subprocess.run(["make", "-s", "-C", str(HERE), "-f", str(HERE / "Makefile"), target], check=True)
+
+
+def _cams(cameras):
+    arr = (abi.gsim_camera * max(len(cameras), 1))()
+    for k, c in enumerate(cameras):
+        arr[k] = c.to_c() if isinstance(c, CameraModel) else c
+    return arr
+
+
+def _nodes(nodes):
+    arr = (abi.gsim_node * max(len(nodes), 1))()
+    for k, n in enumerate(nodes):
+        arr[k] = n.to_c() if isinstance(n, SceneNode) else n
+    return arr
+
+
+def _target(width, height):
+    return RenderTarget.empty(width, height)
+
+
+class Oracle:
+    """Our C restatement of the reference path (liboracle.so)."""
+
+    def __init__(self, path: Path | None = None):
+        p = Path(path) if path else ORACLE_LIB
+        if not p.exists():
+            build_oracle(with_ref=False)
+        self.lib = C.CDLL(str(p))
+        L = self.lib
+        L.gso_project.argtypes = [C.POINTER(abi.gsim_field_view), C.POINTER(abi.gsim_node), C.c_uint64,
+                                  C.POINTER(abi.gsim_camera), _vp, C.c_uint64, _u64p]
+        L.gso_rasterize.argtypes = [_vp, C.c_uint64, C.POINTER(abi.gsim_camera),
+                                    C.POINTER(abi.gsim_raster_options), _fp, _fp, _fp]
+        L.gso_reference_rasterize.argtypes = L.gso_rasterize.argtypes
+        L.gso_rasterize_lists.argtypes = [_vp, C.c_uint64, C.POINTER(abi.gsim_camera), _u32p, _u32p,
+                                          C.c_uint64, _u64p]
+        L.gso_render.argtypes = [C.POINTER(abi.gsim_field_view), C.POINTER(abi.gsim_node), C.c_uint64,
+                                 C.POINTER(abi.gsim_camera), C.c_uint64,
+                                 C.POINTER(abi.gsim_raster_options), C.POINTER(abi.gsim_target)]
+        L.gso_transform_primitives.argtypes = [_dp, _dp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                               C.POINTER(abi.gsim_rigid)]
+        L.gso_random_field.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                       C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.gso_hash_target.argtypes = [_fp, _fp, _fp, C.c_int, C.c_int, C.c_uint64]
+        L.gso_hash_target.restype = C.c_uint64
+        L.gso_look_at.argtypes = [_dp, _dp, C.c_double, C.c_double, C.c_int, C.c_int, _dp,
+                                  C.POINTER(abi.gsim_camera)]
+        L.gso_shade_sh.argtypes = [_dp, C.c_int, _dp, _dp]
+        L.gso_mt_seed.argtypes = [_vp, C.c_uint64]
+        L.gso_mt_next.argtypes = [_vp]
+        L.gso_mt_next.restype = C.c_uint64
+
+    # -- fixtures ----------------------------------------------------------------------------
+    def random_field(self, seed, count, box_extent, scale_lo, scale_hi, sh_degree) -> GaussianField:
+        """oracle::random_field (tests/support/test_oracles.cpp:144-168), bit-exact."""
+        m = np.zeros((count, 3)); s = np.zeros((count, 3)); q = np.zeros((count, 4))
+        o = np.zeros(count); sh = np.zeros((count, 48))
+        self.lib.gso_random_field(seed, count, box_extent, scale_lo, scale_hi, sh_degree,
+                                  m.ctypes.data_as(_dp), s.ctypes.data_as(_dp), q.ctypes.data_as(_dp),
+                                  o.ctypes.data_as(_dp), sh.ctypes.data_as(_dp))
+        return GaussianField(m, s, q, o, sh, sh_degree)
+
+    def mt19937_64(self, seed: int, n: int) -> np.ndarray:
+        state = C.create_string_buffer(312 * 8 + 16)
+        self.lib.gso_mt_seed(state, seed)
+        return np.array([self.lib.gso_mt_next(state) for _ in range(n)], dtype=np.uint64)
+
+    def look_at(self, eye, target, fx, fy, width, height, up=(0.0, 0.0, 1.0)) -> abi.gsim_camera:
+        cam = abi.gsim_camera()
+        e = (C.c_double * 3)(*eye); t = (C.c_double * 3)(*target); u = (C.c_double * 3)(*up)
+        self.lib.gso_look_at(e, t, fx, fy, width, height, u, C.byref(cam))
+        return cam
+
+    def shade_sh(self, sh48, degree, view_dir):
+        sh = (C.c_double * 48)(*sh48); d = (C.c_double * 3)(*view_dir); out = (C.c_double * 3)()
+        self.lib.gso_shade_sh(sh, degree, d, out)
+        return tuple(out)
+
+    # -- the path ----------------------------------------------------------------------------
+    def project(self, field: GaussianField, nodes, camera) -> np.ndarray:
+        v = field.view()
+        na = _nodes(nodes)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        out = np.zeros(max(field.size(), 1), dtype=abi.SPLAT_DTYPE)
+        count = C.c_uint64(0)
+        st = self.lib.gso_project(C.byref(v), na, len(nodes), C.byref(cam), out.ctypes.data_as(_vp),
+                                  field.size(), C.byref(count))
+        if st != abi.GSIM_OK:
+            raise ValueError("oracle project: validation error")
+        return out[: count.value].copy()
+
+    def rasterize(self, splats, camera, options: RasterOptions | None = None) -> RenderTarget:
+        splats = np.ascontiguousarray(splats, dtype=abi.SPLAT_DTYPE)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        opt = (options or RasterOptions()).to_c()
+        t = _target(cam.width, cam.height)
+        self.lib.gso_rasterize(splats.ctypes.data_as(_vp), len(splats), C.byref(cam), C.byref(opt),
+                               t.rgb.ctypes.data_as(_fp), t.depth.ctypes.data_as(_fp),
+                               t.accum_alpha.ctypes.data_as(_fp))
+        return t
+
+    def reference_rasterize(self, splats, camera, options: RasterOptions | None = None) -> RenderTarget:
+        splats = np.ascontiguousarray(splats, dtype=abi.SPLAT_DTYPE)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        opt = (options or RasterOptions()).to_c()
+        t = _target(cam.width, cam.height)
+        self.lib.gso_reference_rasterize(splats.ctypes.data_as(_vp), len(splats), C.byref(cam),
+                                         C.byref(opt), t.rgb.ctypes.data_as(_fp),
+                                         t.depth.ctypes.data_as(_fp), t.accum_alpha.ctypes.data_as(_fp))
+        return t
+
+    def rasterize_lists(self, splats, camera):
+        """(tile_begin[tiles+1], splat index per sorted pair) of raster.cpp:243-271."""
+        splats = np.ascontiguousarray(splats, dtype=abi.SPLAT_DTYPE)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+        count = C.c_uint64(0)
+        self.lib.gso_rasterize_lists(splats.ctypes.data_as(_vp), len(splats), C.byref(cam), None,
+                                     None, 0, C.byref(count))
+        tb = np.zeros(tiles + 1, np.uint32)
+        vals = np.zeros(max(count.value, 1), np.uint32)
+        self.lib.gso_rasterize_lists(splats.ctypes.data_as(_vp), len(splats), C.byref(cam),
+                                     tb.ctypes.data_as(_u32p), vals.ctypes.data_as(_u32p),
+                                     count.value, C.byref(count))
+        return tb, vals[: count.value]
+
+    def render(self, field: GaussianField, nodes, cameras, options: RasterOptions | None = None):
+        v = field.view()
+        na = _nodes(nodes)
+        ca = _cams(cameras)
+        opt = (options or RasterOptions()).to_c()
+        targets = [_target(ca[k].width, ca[k].height) for k in range(len(cameras))]
+        ta = (abi.gsim_target * max(len(cameras), 1))()
+        for k, t in enumerate(targets):
+            ta[k] = t.to_c()
+        st = self.lib.gso_render(C.byref(v), na, len(nodes), ca, len(cameras), C.byref(opt), ta)
+        if st != abi.GSIM_OK:
+            raise ValueError("oracle render: validation error")
+        return targets
+
+    def transform_primitives(self, means, rotations, begin, end, rigid) -> int:
+        r = rigid.to_c() if hasattr(rigid, "to_c") else rigid
+        return self.lib.gso_transform_primitives(means.ctypes.data_as(_dp), rotations.ctypes.data_as(_dp),
+                                                 len(means), begin, end, C.byref(r))
+
+    def hash_target(self, t: RenderTarget, seed: int = 1469598103934665603) -> int:
+        h, w = t.depth.shape
+        return int(self.lib.gso_hash_target(t.rgb.ctypes.data_as(_fp), t.depth.ctypes.data_as(_fp),
+                                            t.accum_alpha.ctypes.data_as(_fp), w, h, seed))
+
+
+class Ref:
+    """The unmodified reference (oracle/_ref/libgsim_ref.so). Raises if it was never built."""
+
+    def __init__(self, path: Path | None = None):
+        p = Path(path) if path else REF_LIB
+        if not p.exists():
+            if Path("/root/reference/proj").exists():
+                build_oracle(with_ref=True)
+            if not p.exists():
+                raise FileNotFoundError(f"{p} not built (needs /root/reference at build time)")
+        self.lib = C.CDLL(str(p))
+        L = self.lib
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_field_create.argtypes = [C.POINTER(abi.gsim_field_view)]
+        L.ref_field_create.restype = _vp
+        L.ref_field_destroy.argtypes = [_vp]
+        L.ref_project.argtypes = [_vp, C.POINTER(abi.gsim_node), C.c_uint64, C.POINTER(abi.gsim_camera),
+                                  _vp, C.c_uint64, _u64p]
+        L.ref_rasterize.argtypes = [_vp, C.c_uint64, C.POINTER(abi.gsim_camera),
+                                    C.POINTER(abi.gsim_raster_options), _fp, _fp, _fp]
+        L.ref_reference_rasterize.argtypes = L.ref_rasterize.argtypes
+        L.ref_render.argtypes = [_vp, C.POINTER(abi.gsim_node), C.c_uint64, C.POINTER(abi.gsim_camera),
+                                 C.c_uint64, C.POINTER(abi.gsim_raster_options), C.POINTER(abi.gsim_target)]
+        L.ref_transform_primitives.argtypes = [_dp, _dp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                               C.POINTER(abi.gsim_rigid)]
+        L.ref_look_at.argtypes = [_dp, _dp, C.c_double, C.c_double, C.c_int, C.c_int, _dp,
+                                  C.POINTER(abi.gsim_camera)]
+        L.ref_random_field.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                       C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_thread_count.restype = C.c_int
+        L.ref_rigid_compose.argtypes = [C.POINTER(abi.gsim_rigid)] * 3
+
+    def set_threads(self, n: int) -> None:
+        self.lib.ref_set_threads(n)
+
+    def thread_count(self) -> int:
+        return self.lib.ref_thread_count()
+
+    def random_field(self, seed, count, box_extent, scale_lo, scale_hi, sh_degree) -> GaussianField:
+        m = np.zeros((count, 3)); s = np.zeros((count, 3)); q = np.zeros((count, 4))
+        o = np.zeros(count); sh = np.zeros((count, 48))
+        self.lib.ref_random_field(seed, count, box_extent, scale_lo, scale_hi, sh_degree,
+                                  m.ctypes.data_as(_dp), s.ctypes.data_as(_dp), q.ctypes.data_as(_dp),
+                                  o.ctypes.data_as(_dp), sh.ctypes.data_as(_dp))
+        return GaussianField(m, s, q, o, sh, sh_degree)
+
+    def field(self, field: GaussianField):
+        v = field.view()
+        return RefField(self, self.lib.ref_field_create(C.byref(v)), field.size())
+
+    def project(self, field: GaussianField, nodes, camera) -> np.ndarray:
+        with_field = self.field(field)
+        try:
+            return with_field.project(nodes, camera)
+        finally:
+            with_field.close()
+
+    def rasterize(self, splats, camera, options=None) -> RenderTarget:
+        return self._raster(self.lib.ref_rasterize, splats, camera, options)
+
+    def reference_rasterize(self, splats, camera, options=None) -> RenderTarget:
+        return self._raster(self.lib.ref_reference_rasterize, splats, camera, options)
+
+    def _raster(self, fn, splats, camera, options):
+        splats = np.ascontiguousarray(splats, dtype=abi.SPLAT_DTYPE)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        opt = (options or RasterOptions()).to_c()
+        t = _target(cam.width, cam.height)
+        st = fn(splats.ctypes.data_as(_vp), len(splats), C.byref(cam), C.byref(opt),
+                t.rgb.ctypes.data_as(_fp), t.depth.ctypes.data_as(_fp), t.accum_alpha.ctypes.data_as(_fp))
+        if st != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return t
+
+    def render(self, field: GaussianField, nodes, cameras, options=None):
+        with_field = self.field(field)
+        try:
+            return with_field.render(nodes, cameras, options)
+        finally:
+            with_field.close()
+
+    def transform_primitives(self, means, rotations, begin, end, rigid) -> int:
+        r = rigid.to_c() if hasattr(rigid, "to_c") else rigid
+        return self.lib.ref_transform_primitives(means.ctypes.data_as(_dp), rotations.ctypes.data_as(_dp),
+                                                 len(means), begin, end, C.byref(r))
+
+    def look_at(self, eye, target, fx, fy, width, height, up=(0.0, 0.0, 1.0)) -> abi.gsim_camera:
+        cam = abi.gsim_camera()
+        e = (C.c_double * 3)(*eye); t = (C.c_double * 3)(*target); u = (C.c_double * 3)(*up)
+        self.lib.ref_look_at(e, t, fx, fy, width, height, u, C.byref(cam))
+        return cam
+
+
+class RefField:
+    """A reference GaussianField built once (outside timed regions)."""
+
+    def __init__(self, ref: Ref, handle, size: int):
+        self.ref = ref
+        self.handle = handle
+        self.size = size
+
+    def project(self, nodes, camera) -> np.ndarray:
+        na = _nodes(nodes)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        out = np.zeros(max(self.size, 1), dtype=abi.SPLAT_DTYPE)
+        count = C.c_uint64(0)
+        st = self.ref.lib.ref_project(self.handle, na, len(nodes), C.byref(cam), out.ctypes.data_as(_vp),
+                                      self.size, C.byref(count))
+        if st != 0:
+            raise ValueError(self.ref.lib.ref_last_error().decode())
+        return out[: count.value].copy()
+
+    def render(self, nodes, cameras, options=None, targets=None):
+        na = _nodes(nodes)
+        ca = _cams(cameras)
+        opt = (options or RasterOptions()).to_c()
+        if targets is None:
+            targets = [_target(ca[k].width, ca[k].height) for k in range(len(cameras))]
+        ta = (abi.gsim_target * max(len(cameras), 1))()
+        for k, t in enumerate(targets):
+            ta[k] = t.to_c()
+        st = self.ref.lib.ref_render(self.handle, na, len(nodes), ca, len(cameras), C.byref(opt), ta)
+        if st != 0:
+            raise ValueError(self.ref.lib.ref_last_error().decode())
+        return targets
+
+    def close(self) -> None:
+        if self.handle:
+            self.ref.lib.ref_field_destroy(self.handle)
+            self.handle = None
+
+
+def ref_available() -> bool:
+    return REF_LIB.exists() or Path("/root/reference/proj").exists()
+
+
+def cpu_count() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1

@@ -1,0 +1,144 @@
+"""ctypes mirror of include/gsim_gpu.h and the loader of libgsim_gpu.so.
+
+There is no fallback: if the CUDA library is missing or fails to load, every entry point
+raises. Build it with ``python -m paper_2507_21981_b200.build`` (or __graft_entry__.build()).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libgsim_gpu.so"
+
+GSIM_OK = 0
+GSIM_ERR_IO = 1
+GSIM_ERR_VALIDATION = 2
+GSIM_NODE_BACKGROUND = 0
+GSIM_NODE_INTERACTIVE = 1
+GSIM_ENV_ALL = -1
+
+
+class gsim_rigid(C.Structure):
+    _fields_ = [("rotation", C.c_double * 4), ("translation", C.c_double * 3)]
+
+
+class gsim_field_view(C.Structure):
+    _fields_ = [
+        ("count", C.c_uint64), ("sh_degree", C.c_int32), ("reserved", C.c_int32),
+        ("means", C.POINTER(C.c_double)), ("means_stride", C.c_uint64),
+        ("scales", C.POINTER(C.c_double)), ("scales_stride", C.c_uint64),
+        ("rotations", C.POINTER(C.c_double)), ("rotations_stride", C.c_uint64),
+        ("opacities", C.POINTER(C.c_double)), ("opacities_stride", C.c_uint64),
+        ("sh", C.POINTER(C.c_double)), ("sh_stride", C.c_uint64),
+    ]
+
+
+class gsim_node(C.Structure):
+    _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64), ("pose", gsim_rigid),
+                ("kind", C.c_int32), ("env", C.c_int32)]
+
+
+class gsim_camera(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32), ("pose", gsim_rigid),
+                ("near_plane", C.c_double), ("far_plane", C.c_double),
+                ("env", C.c_int32), ("reserved", C.c_int32)]
+
+
+class gsim_raster_options(C.Structure):
+    _fields_ = [("normalize_depth", C.c_int32), ("reserved", C.c_int32),
+                ("transmittance_cutoff", C.c_double)]
+
+
+class gsim_projected_splat(C.Structure):
+    _fields_ = [("pixel_center", C.c_double * 2), ("cov_xx", C.c_double), ("cov_xy", C.c_double),
+                ("cov_yy", C.c_double), ("inv_xx", C.c_double), ("inv_xy", C.c_double),
+                ("inv_yy", C.c_double), ("view_depth", C.c_double), ("alpha_peak", C.c_double),
+                ("rgb", C.c_double * 3), ("radius", C.c_double), ("prim_index", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class gsim_target(C.Structure):
+    _fields_ = [("rgb", C.POINTER(C.c_float)), ("depth", C.POINTER(C.c_float)),
+                ("accum_alpha", C.POINTER(C.c_float))]
+
+
+class gsim_render_stats(C.Structure):
+    _fields_ = [("slots", C.c_uint64), ("visible", C.c_uint64), ("pairs", C.c_uint64),
+                ("tiles", C.c_uint64), ("launches", C.c_uint64), ("launches_total", C.c_uint64),
+                ("depth_passes", C.c_uint32), ("tile_passes", C.c_uint32),
+                ("ms_preprocess", C.c_float), ("ms_depth_sort", C.c_float),
+                ("ms_duplicate", C.c_float), ("ms_tile_sort", C.c_float),
+                ("ms_ranges", C.c_float), ("ms_raster", C.c_float), ("ms_total", C.c_float),
+                ("reserved", C.c_float)]
+
+
+# numpy view of gsim_projected_splat (ProjectedSplat, raster.hpp:20-29), 120 bytes
+SPLAT_DTYPE = np.dtype([
+    ("pixel_center", "<f8", (2,)), ("cov_xx", "<f8"), ("cov_xy", "<f8"), ("cov_yy", "<f8"),
+    ("inv_xx", "<f8"), ("inv_xy", "<f8"), ("inv_yy", "<f8"), ("view_depth", "<f8"),
+    ("alpha_peak", "<f8"), ("rgb", "<f8", (3,)), ("radius", "<f8"), ("prim_index", "<u4"),
+    ("reserved", "<u4"),
+])
+assert SPLAT_DTYPE.itemsize == C.sizeof(gsim_projected_splat) == 120
+
+# Every symbol include/gsim_gpu.h declares: (name, restype, argtypes)
+_P = C.c_void_p
+SIGNATURES = [
+    ("gsim_gpu_version", C.c_char_p, []),
+    ("gsim_gpu_context_create", C.c_int, [C.c_int, C.POINTER(_P)]),
+    ("gsim_gpu_context_destroy", C.c_int, [_P]),
+    ("gsim_gpu_last_error", C.c_char_p, [_P]),
+    ("gsim_gpu_stream", _P, [_P]),
+    ("gsim_gpu_synchronize", C.c_int, [_P]),
+    ("gsim_gpu_set_profiling", C.c_int, [_P, C.c_int]),
+    ("gsim_gpu_get_stats", C.c_int, [_P, C.POINTER(gsim_render_stats)]),
+    ("gsim_gpu_scene_upload", C.c_int, [_P, C.POINTER(gsim_field_view), C.POINTER(_P)]),
+    ("gsim_gpu_scene_destroy", C.c_int, [_P]),
+    ("gsim_gpu_scene_size", C.c_uint64, [_P]),
+    ("gsim_gpu_transform_primitives", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(gsim_rigid)]),
+    ("gsim_gpu_scene_download", C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("gsim_gpu_project", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64, C.POINTER(gsim_camera),
+                                   _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("gsim_gpu_rasterize", C.c_int, [_P, _P, C.c_uint64, C.POINTER(gsim_camera),
+                                     C.POINTER(gsim_raster_options), C.POINTER(gsim_target)]),
+    ("gsim_gpu_render", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64, C.POINTER(gsim_camera),
+                                  C.c_uint64, C.POINTER(gsim_raster_options), C.POINTER(gsim_target)]),
+    ("gsim_gpu_render_device", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64,
+                                         C.POINTER(gsim_camera), C.c_uint64,
+                                         C.POINTER(gsim_raster_options), _P]),
+    ("gsim_gpu_device_output", _P, [_P]),
+    ("gsim_gpu_tile_lists", C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                      C.c_uint64, C.POINTER(C.c_uint64)]),
+]
+
+_lib = None
+
+
+def load_library(path: Path | None = None) -> C.CDLL:
+    """Load libgsim_gpu.so (raises if it is missing: there is no CPU fallback)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA extension first "
+            "(python -m paper_2507_21981_b200.build); there is no CPU fallback")
+    lib = C.CDLL(str(p))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/gsim_gpu.h (parsed, for the ABI test)."""
+    import re
+    text = (Path(__file__).resolve().parent.parent / "include" / "gsim_gpu.h").read_text()
+    return sorted(set(re.findall(r"\b(gsim_gpu_[a-z_]+)\s*\(", text)))

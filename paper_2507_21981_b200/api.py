@@ -1,0 +1,487 @@
+"""Python host mirror of the reference render API, backed by the sm_100a C ABI.
+
+Names, argument meaning and error behaviour follow the reference gsim library:
+    GaussianField, SceneNode, NodeKind    gaussian.hpp:19-71
+    RigidTransform                        math.hpp:217-239
+    CameraModel (+ look_at)               camera.hpp:14-33, raster.cpp:94-111
+    RasterOptions, ProjectedSplat         raster.hpp:20-36
+    RenderTarget                          image.hpp:38-45
+    project / rasterize / render          raster.hpp:54-67
+    transform_primitives                  gaussian.hpp:76-77
+    io_error / validation_error           errors.hpp:12-25
+Every compute call goes through libgsim_gpu.so; there is no CPU path here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass, field as dc_field
+from typing import Sequence
+
+import numpy as np
+
+from . import abi
+
+
+class IoError(RuntimeError):
+    """io_error (errors.hpp:12-15): runtime / CUDA failure, CLI exit code 1."""
+
+
+class ValidationError(ValueError):
+    """validation_error (errors.hpp:18-21): bad input, CLI exit code 2."""
+
+
+io_error = IoError
+validation_error = ValidationError
+
+
+def _check(status: int, ctx_ptr) -> None:
+    if status == abi.GSIM_OK:
+        return
+    lib = abi.load_library()
+    msg = lib.gsim_gpu_last_error(ctx_ptr)
+    msg = msg.decode() if msg else ""
+    if status == abi.GSIM_ERR_VALIDATION:
+        raise ValidationError(msg)
+    raise IoError(msg)
+
+
+# ---- math.hpp (host-side helpers for building poses and cameras) -------------------------
+
+def quat_mul(a, b):
+    aw, ax, ay, az = a
+    bw, bx, by, bz = b
+    return (aw * bw - ax * bx - ay * by - az * bz,
+            aw * bx + ax * bw + ay * bz - az * by,
+            aw * by - ax * bz + ay * bw + az * bx,
+            aw * bz + ax * by - ay * bx + az * bw)
+
+
+def quat_rotate(q, v):
+    w, x, y, z = q
+    vx, vy, vz = v
+    tx, ty, tz = 2.0 * (y * vz - z * vy), 2.0 * (z * vx - x * vz), 2.0 * (x * vy - y * vx)
+    return (vx + tx * w + (y * tz - z * ty),
+            vy + ty * w + (z * tx - x * tz),
+            vz + tz * w + (x * ty - y * tx))
+
+
+def quat_normalized(q):
+    n = math.sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3])
+    return tuple(c / n for c in q) if n > 0.0 else (1.0, 0.0, 0.0, 0.0)
+
+
+def quat_from_axis_angle(axis, angle):
+    n = math.sqrt(sum(a * a for a in axis))
+    a = [c / n for c in axis] if n > 0 else [0.0, 0.0, 0.0]
+    s = math.sin(0.5 * angle)
+    return (math.cos(0.5 * angle), a[0] * s, a[1] * s, a[2] * s)
+
+
+def quat_from_matrix(m):
+    """Shepperd's method, math.hpp:158-187 (m row-major 3x3 nested)."""
+    tr = m[0][0] + m[1][1] + m[2][2]
+    if tr > 0.0:
+        s = math.sqrt(tr + 1.0) * 2.0
+        q = (0.25 * s, (m[2][1] - m[1][2]) / s, (m[0][2] - m[2][0]) / s, (m[1][0] - m[0][1]) / s)
+    elif m[0][0] > m[1][1] and m[0][0] > m[2][2]:
+        s = math.sqrt(1.0 + m[0][0] - m[1][1] - m[2][2]) * 2.0
+        q = ((m[2][1] - m[1][2]) / s, 0.25 * s, (m[0][1] + m[1][0]) / s, (m[0][2] + m[2][0]) / s)
+    elif m[1][1] > m[2][2]:
+        s = math.sqrt(1.0 + m[1][1] - m[0][0] - m[2][2]) * 2.0
+        q = ((m[0][2] - m[2][0]) / s, (m[0][1] + m[1][0]) / s, 0.25 * s, (m[1][2] + m[2][1]) / s)
+    else:
+        s = math.sqrt(1.0 + m[2][2] - m[0][0] - m[1][1]) * 2.0
+        q = ((m[1][0] - m[0][1]) / s, (m[0][2] + m[2][0]) / s, (m[1][2] + m[2][1]) / s, 0.25 * s)
+    return quat_normalized(q)
+
+
+@dataclass
+class RigidTransform:
+    """SE(3) pose x -> R(q) x + t, q = (w, x, y, z) (math.hpp:217-239)."""
+    rotation: tuple = (1.0, 0.0, 0.0, 0.0)
+    translation: tuple = (0.0, 0.0, 0.0)
+
+    @staticmethod
+    def identity() -> "RigidTransform":
+        return RigidTransform()
+
+    def transform_point(self, p):
+        r = quat_rotate(self.rotation, p)
+        return (r[0] + self.translation[0], r[1] + self.translation[1], r[2] + self.translation[2])
+
+    def __mul__(self, o: "RigidTransform") -> "RigidTransform":
+        return RigidTransform(quat_normalized(quat_mul(self.rotation, o.rotation)),
+                              self.transform_point(o.translation))
+
+    def inverse(self) -> "RigidTransform":
+        inv = (self.rotation[0], -self.rotation[1], -self.rotation[2], -self.rotation[3])
+        t = quat_rotate(inv, self.translation)
+        return RigidTransform(inv, (-t[0], -t[1], -t[2]))
+
+    def to_c(self) -> abi.gsim_rigid:
+        r = abi.gsim_rigid()
+        for k in range(4):
+            r.rotation[k] = float(self.rotation[k])
+        for k in range(3):
+            r.translation[k] = float(self.translation[k])
+        return r
+
+
+class NodeKind:
+    background = abi.GSIM_NODE_BACKGROUND
+    interactive = abi.GSIM_NODE_INTERACTIVE
+
+
+@dataclass
+class SceneNode:
+    """Background or interactive entity driving a contiguous primitive range (gaussian.hpp:66-71).
+    env = -1 (default) is the reference's semantics; env >= 0 limits the node to that env's
+    cameras for batched multi-environment rendering."""
+    id: str = ""
+    kind: int = NodeKind.background
+    pose: RigidTransform = dc_field(default_factory=RigidTransform)
+    range: tuple = (0, 0)
+    env: int = abi.GSIM_ENV_ALL
+
+    def to_c(self) -> abi.gsim_node:
+        n = abi.gsim_node()
+        n.begin, n.end = int(self.range[0]), int(self.range[1])
+        n.pose = self.pose.to_c()
+        n.kind = int(self.kind)
+        n.env = int(self.env)
+        return n
+
+
+@dataclass
+class CameraModel:
+    """Pinhole camera; pose maps world -> camera (x right, y down, z forward) (camera.hpp)."""
+    id: str = ""
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    width: int = 0
+    height: int = 0
+    pose: RigidTransform = dc_field(default_factory=RigidTransform)
+    near: float = 0.05
+    far: float = 100.0
+    env: int = 0
+
+    def camera_center(self):
+        return self.pose.inverse().translation
+
+    @staticmethod
+    def look_at(eye, target, fx, fy, width, height, up=(0.0, 0.0, 1.0)) -> "CameraModel":
+        """CameraModel::look_at (raster.cpp:94-111)."""
+        def sub(a, b): return (a[0] - b[0], a[1] - b[1], a[2] - b[2])
+        def cross(a, b): return (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
+        def normalized(a):
+            n = math.sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2])
+            return (a[0] / n, a[1] / n, a[2] / n) if n > 0 else (0.0, 0.0, 0.0)
+        forward = normalized(sub(target, eye))
+        right = normalized(cross(forward, up))
+        if right[0] ** 2 + right[1] ** 2 + right[2] ** 2 < 1e-20:
+            right = normalized(cross(forward, (0.0, 1.0, 0.0)))
+        down = cross(forward, right)
+        q = quat_from_matrix([list(right), list(down), list(forward)])
+        t = quat_rotate(q, eye)
+        return CameraModel(fx=fx, fy=fy, cx=width * 0.5, cy=height * 0.5, width=width,
+                           height=height, pose=RigidTransform(q, (-t[0], -t[1], -t[2])))
+
+    def to_c(self) -> abi.gsim_camera:
+        c = abi.gsim_camera()
+        c.fx, c.fy, c.cx, c.cy = float(self.fx), float(self.fy), float(self.cx), float(self.cy)
+        c.width, c.height = int(self.width), int(self.height)
+        c.pose = self.pose.to_c()
+        c.near_plane, c.far_plane = float(self.near), float(self.far)
+        c.env = int(self.env)
+        return c
+
+
+@dataclass
+class RasterOptions:
+    """raster.hpp:31-36."""
+    normalize_depth: bool = False
+    transmittance_cutoff: float = 1e-4
+
+    def to_c(self) -> abi.gsim_raster_options:
+        o = abi.gsim_raster_options()
+        o.normalize_depth = 1 if self.normalize_depth else 0
+        o.transmittance_cutoff = float(self.transmittance_cutoff)
+        return o
+
+
+@dataclass
+class RenderTarget:
+    """RGB + alpha-composited depth + accumulated alpha (image.hpp:38-45)."""
+    rgb: np.ndarray
+    depth: np.ndarray
+    accum_alpha: np.ndarray
+
+    @staticmethod
+    def empty(width: int, height: int) -> "RenderTarget":
+        return RenderTarget(np.zeros((height, width, 3), np.float32),
+                            np.zeros((height, width), np.float32),
+                            np.zeros((height, width), np.float32))
+
+    def to_c(self) -> abi.gsim_target:
+        t = abi.gsim_target()
+        fp = C.POINTER(C.c_float)
+        t.rgb = self.rgb.ctypes.data_as(fp)
+        t.depth = self.depth.ctypes.data_as(fp)
+        t.accum_alpha = self.accum_alpha.ctypes.data_as(fp)
+        return t
+
+
+class GaussianField:
+    """Indexed Gaussian collection (gaussian.hpp:53-60) held as SoA float64 arrays:
+    means (N,3), scales (N,3) linear, rotations (N,4) unit (w,x,y,z), opacities (N,)
+    post-sigmoid, sh (N,48) channel-major sh[c*16+k]; sh_degree global."""
+
+    def __init__(self, means, scales, rotations, opacities, sh, sh_degree: int):
+        self.means = np.ascontiguousarray(means, dtype=np.float64).reshape(-1, 3)
+        n = self.means.shape[0]
+        self.scales = np.ascontiguousarray(scales, dtype=np.float64).reshape(n, 3)
+        self.rotations = np.ascontiguousarray(rotations, dtype=np.float64).reshape(n, 4)
+        self.opacities = np.ascontiguousarray(opacities, dtype=np.float64).reshape(n)
+        sh = np.asarray(sh, dtype=np.float64)
+        if sh.shape != (n, 48):
+            full = np.zeros((n, 48))
+            full[:, : sh.shape[1]] = sh.reshape(n, -1)
+            sh = full
+        self.sh = np.ascontiguousarray(sh)
+        self.sh_degree = int(sh_degree)
+        self.generation = 0  # bump after in-place edits so cached uploads are refreshed
+
+    def size(self) -> int:
+        return self.means.shape[0]
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def touch(self) -> None:
+        self.generation += 1
+
+    def view(self) -> abi.gsim_field_view:
+        v = abi.gsim_field_view()
+        dp = C.POINTER(C.c_double)
+        v.count = self.size()
+        v.sh_degree = self.sh_degree
+        v.means, v.means_stride = self.means.ctypes.data_as(dp), 3
+        v.scales, v.scales_stride = self.scales.ctypes.data_as(dp), 3
+        v.rotations, v.rotations_stride = self.rotations.ctypes.data_as(dp), 4
+        v.opacities, v.opacities_stride = self.opacities.ctypes.data_as(dp), 1
+        v.sh, v.sh_stride = self.sh.ctypes.data_as(dp), 48
+        return v
+
+
+def _nodes_array(nodes: Sequence[SceneNode]):
+    arr = (abi.gsim_node * max(len(nodes), 1))()
+    for k, n in enumerate(nodes):
+        arr[k] = n.to_c() if isinstance(n, SceneNode) else n
+    return arr
+
+
+def _cams_array(cameras: Sequence[CameraModel]):
+    arr = (abi.gsim_camera * max(len(cameras), 1))()
+    for k, c in enumerate(cameras):
+        arr[k] = c.to_c() if isinstance(c, CameraModel) else c
+    return arr
+
+
+class Scene:
+    """A GaussianField resident in HBM on one context's device."""
+
+    def __init__(self, ctx: "Context", handle: C.c_void_p, size: int):
+        self.ctx = ctx
+        self.handle = handle
+        self.size = size
+
+    def transform_primitives(self, begin: int, end: int, transform: RigidTransform) -> None:
+        """transform_primitives (gaussian.cpp:65-79) on the device copy (K1)."""
+        t = transform.to_c()
+        _check(self.ctx.lib.gsim_gpu_transform_primitives(self.ctx.ptr, self.handle, begin, end,
+                                                          C.byref(t)), self.ctx.ptr)
+
+    def download(self):
+        means = np.zeros((self.size, 3))
+        rots = np.zeros((self.size, 4))
+        dp = C.POINTER(C.c_double)
+        _check(self.ctx.lib.gsim_gpu_scene_download(self.ctx.ptr, self.handle, means.ctypes.data_as(dp),
+                                                    rots.ctypes.data_as(dp)), self.ctx.ptr)
+        return means, rots
+
+    def close(self) -> None:
+        if self.handle:
+            self.ctx.lib.gsim_gpu_scene_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """One device: a CUDA stream and grow-only HBM workspaces (gsim_gpu_context)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = abi.load_library()
+        p = C.c_void_p()
+        st = self.lib.gsim_gpu_context_create(device, C.byref(p))
+        if st != abi.GSIM_OK:
+            msg = (self.lib.gsim_gpu_last_error(None) or b"").decode()
+            raise (ValidationError if st == abi.GSIM_ERR_VALIDATION else IoError)(msg)
+        self.ptr = p
+        self.device = device
+        self.lock = threading.Lock()
+
+    def close(self) -> None:
+        if self.ptr:
+            self.lib.gsim_gpu_context_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.gsim_gpu_stream(self.ptr) or 0)
+
+    def synchronize(self) -> None:
+        _check(self.lib.gsim_gpu_synchronize(self.ptr), self.ptr)
+
+    def set_profiling(self, enable: bool) -> None:
+        _check(self.lib.gsim_gpu_set_profiling(self.ptr, 1 if enable else 0), self.ptr)
+
+    def stats(self) -> dict:
+        s = abi.gsim_render_stats()
+        _check(self.lib.gsim_gpu_get_stats(self.ptr, C.byref(s)), self.ptr)
+        return {name: getattr(s, name) for name, _ in s._fields_ if name != "reserved"}
+
+    def upload(self, field: GaussianField) -> Scene:
+        v = field.view()
+        h = C.c_void_p()
+        _check(self.lib.gsim_gpu_scene_upload(self.ptr, C.byref(v), C.byref(h)), self.ptr)
+        return Scene(self, h, field.size())
+
+    def project(self, scene: Scene, nodes: Sequence[SceneNode], camera: CameraModel) -> np.ndarray:
+        na = _nodes_array(nodes)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        count = C.c_uint64(0)
+        out = np.zeros(scene.size, dtype=abi.SPLAT_DTYPE)
+        _check(self.lib.gsim_gpu_project(self.ptr, scene.handle, na, len(nodes), C.byref(cam),
+                                         out.ctypes.data_as(C.c_void_p), scene.size, C.byref(count)),
+               self.ptr)
+        return out[: count.value].copy()
+
+    def rasterize(self, splats: np.ndarray, camera: CameraModel,
+                  options: RasterOptions | None = None) -> RenderTarget:
+        splats = np.ascontiguousarray(splats, dtype=abi.SPLAT_DTYPE)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        opt = (options or RasterOptions()).to_c()
+        t = RenderTarget.empty(cam.width, cam.height)
+        tc = t.to_c()
+        _check(self.lib.gsim_gpu_rasterize(self.ptr, splats.ctypes.data_as(C.c_void_p), len(splats),
+                                           C.byref(cam), C.byref(opt), C.byref(tc)), self.ptr)
+        return t
+
+    def render(self, scene: Scene, nodes: Sequence[SceneNode], cameras: Sequence[CameraModel],
+               options: RasterOptions | None = None,
+               targets: Sequence[RenderTarget] | None = None) -> list[RenderTarget]:
+        na = _nodes_array(nodes)
+        ca = _cams_array(cameras)
+        opt = (options or RasterOptions()).to_c()
+        if targets is None:
+            targets = [RenderTarget.empty(ca[k].width, ca[k].height) for k in range(len(cameras))]
+        ta = (abi.gsim_target * max(len(cameras), 1))()
+        for k, t in enumerate(targets):
+            ta[k] = t.to_c()
+        _check(self.lib.gsim_gpu_render(self.ptr, scene.handle, na, len(nodes), ca, len(cameras),
+                                        C.byref(opt), ta), self.ptr)
+        return list(targets)
+
+    def render_device(self, scene: Scene, nodes, cameras, options: RasterOptions | None = None,
+                      device_out: int | None = None) -> int:
+        """Asynchronous render into device memory; returns the output device pointer."""
+        na = _nodes_array(nodes)
+        ca = _cams_array(cameras)
+        opt = (options or RasterOptions()).to_c()
+        _check(self.lib.gsim_gpu_render_device(self.ptr, scene.handle, na, len(nodes), ca,
+                                               len(cameras), C.byref(opt),
+                                               C.c_void_p(device_out) if device_out else None),
+               self.ptr)
+        return device_out if device_out else int(self.lib.gsim_gpu_device_output(self.ptr))
+
+    def tile_lists(self, camera: int):
+        """Sorted per-tile lists of `camera` from the last render (tile offsets, indices)."""
+        count = C.c_uint64(0)
+        _check(self.lib.gsim_gpu_tile_lists(self.ptr, camera, None, None, 0, C.byref(count)), self.ptr)
+        # tiles of that camera are needed to size the offsets array: ask with a big buffer
+        offsets = np.zeros(256 * 256 + 1, dtype=np.uint32)
+        values = np.zeros(max(count.value, 1), dtype=np.uint32)
+        _check(self.lib.gsim_gpu_tile_lists(self.ptr, camera, offsets.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                            values.ctypes.data_as(C.POINTER(C.c_uint32)), count.value,
+                                            C.byref(count)), self.ptr)
+        return offsets, values[: count.value]
+
+
+# ---- free functions with the reference's signatures ---------------------------------------
+
+_default = {"ctx": None, "scene": None, "key": None}
+_default_lock = threading.Lock()
+
+
+def default_context() -> Context:
+    with _default_lock:
+        if _default["ctx"] is None:
+            _default["ctx"] = Context(0)
+        return _default["ctx"]
+
+
+def _scene_for(field: GaussianField) -> Scene:
+    ctx = default_context()
+    key = (id(field), field.size(), field.generation, field.means.ctypes.data)
+    with _default_lock:
+        if _default["key"] != key:
+            _default["scene"] = None
+            _default["scene"] = ctx.upload(field)
+            _default["key"] = key
+        return _default["scene"]
+
+
+def project(field: GaussianField, nodes: Sequence[SceneNode], camera: CameraModel) -> np.ndarray:
+    """raster.hpp:54-56 — visible splats (ProjectedSplat records) in primitive order."""
+    return default_context().project(_scene_for(field), nodes, camera)
+
+
+def rasterize(splats: np.ndarray, camera: CameraModel, options: RasterOptions | None = None) -> RenderTarget:
+    """raster.hpp:59-60."""
+    return default_context().rasterize(splats, camera, options)
+
+
+def render(field: GaussianField, nodes: Sequence[SceneNode], cameras: Sequence[CameraModel],
+           options: RasterOptions | None = None) -> list[RenderTarget]:
+    """raster.hpp:64-67 — one target per camera."""
+    return default_context().render(_scene_for(field), nodes, cameras, options)
+
+
+def transform_primitives(field: GaussianField, rng: tuple, transform: RigidTransform) -> None:
+    """gaussian.hpp:76-77 — in place; runs K1 on the device copy and writes the result back."""
+    begin, end = int(rng[0]), int(rng[1])
+    if begin > end or end > field.size():
+        raise ValidationError(f"transform_primitives: range [{begin},{end}) outside field of size {field.size()}")
+    scene = _scene_for(field)
+    scene.transform_primitives(begin, end, transform)
+    means, rots = scene.download()
+    field.means[:] = means
+    field.rotations[:] = rots
+    field.touch()
+    with _default_lock:  # the device copy already holds the transformed field
+        _default["key"] = (id(field), field.size(), field.generation, field.means.ctypes.data)

@@ -1,0 +1,1015 @@
+// host.cu — C-ABI implementation: contexts, device-resident scenes, frame plans and the
+// render pipeline orchestration (one CUDA stream per context, grow-only HBM workspaces).
+//
+// Reference behaviour mirrored here:
+//   validate_camera          raster.cpp:16-23   (status 2, same rules)
+//   PoseTable                raster.cpp:47-62   (node painting, later nodes win, range check)
+//   render / rasterize       raster.cpp:234-334 (pipeline: K2 -> K3 -> K4)
+//   transform_primitives     gaussian.cpp:65-79 (K1, range check)
+//   validate_field sh_degree gaussian.cpp:15-17
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/gsim_gpu.h"
+#include "common.cuh"
+#include "kernels.hpp"
+
+using namespace gsim_gpu;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaError {
+    std::string msg;
+};
+struct ValidationError {
+    std::string msg;
+};
+
+#define GSIM_CK(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            throw CudaError{std::string(#expr) + ": " + cudaGetErrorString(_e)};        \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;  // elements
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (ptr) GSIM_CK(cudaFree(ptr));
+        ptr = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 1);
+        GSIM_CK(cudaMalloc(&ptr, want * sizeof(T)));
+        cap = want;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+struct PinnedBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void reserve(size_t bytes) {
+        if (bytes <= cap) return;
+        if (ptr) GSIM_CK(cudaFreeHost(ptr));
+        ptr = nullptr;
+        cap = 0;
+        GSIM_CK(cudaMallocHost(&ptr, std::max<size_t>(bytes, 64)));
+        cap = std::max<size_t>(bytes, 64);
+    }
+    void release() {
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+// Everything a frame needs that is a pure function of (nodes, cameras, field size).
+struct Plan {
+    std::vector<DevCamera> cams;
+    std::vector<uint64_t> slot_base;   // C + 1
+    std::vector<uint32_t> tile_base;   // C + 1
+    std::vector<int> tiles_x;          // C
+    std::vector<DevSegment> segs;
+    std::vector<SegEntry> entries;
+    uint64_t slots = 0;
+    uint32_t tiles = 0;
+    uint64_t out_floats = 0;
+};
+
+// profiling events: start, after K2, after depth sort, after dup, after tile sort, after ranges, after raster
+enum Stage { kEvStart = 0, kEvPre, kEvDepth, kEvDup, kEvTile, kEvRanges, kEvRaster, kNumStages };
+
+}  // namespace
+
+struct gsim_gpu_context {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    std::string err;
+    bool profiling = false;
+    cudaEvent_t ev[kNumStages] = {};
+
+    int occ_pre = 1, occ_sort = 1, occ_dup = 1;
+
+    DevBuf<Record> records;
+    DevBuf<uint32_t> keys;
+    DevBuf<uint32_t> dk[2], dv[2];   // depth sort ping-pong
+    DevBuf<uint32_t> pk[2], pv[2];   // tile sort ping-pong
+    DevBuf<uint64_t> status;
+    // zero block: [0,1024) depth hist, [1024, 2048) tile hist, [2048, 2048+32) tickets
+    DevBuf<uint32_t> zero_block;
+    DevBuf<unsigned long long> counts;  // [0] visible, [1] pairs
+    DevBuf<uint32_t> tile_begin, tile_end;
+    DevBuf<DevCamera> cams;
+    DevBuf<uint64_t> cam_slot_base;
+    DevBuf<uint32_t> cam_tile_base;
+    DevBuf<int> cam_tiles_x;
+    DevBuf<DevSegment> segs;
+    DevBuf<SegEntry> entries;
+    DevBuf<float> out;
+    DevBuf<gsim_projected_splat> full;
+    DevBuf<uint8_t> full_vis;
+    DevBuf<gsim_projected_splat> splats_in;
+    PinnedBuf staging;
+    PinnedBuf readback;
+
+    uint32_t epoch = 0;
+    uint64_t pair_capacity = 0;
+    uint64_t launches_total = 0;
+
+    // last frame, for stats and the tile-list hook
+    gsim_render_stats stats{};
+    Plan last_plan;
+    const uint32_t* final_vals = nullptr;
+    uint64_t last_pairs = 0;
+
+    uint32_t next_epoch() {
+        epoch = (epoch + 1) & kEpochMask;
+        if (epoch == 0) {
+            if (status.ptr) GSIM_CK(cudaMemsetAsync(status.ptr, 0, status.cap * sizeof(uint64_t), stream));
+            epoch = 1;
+        }
+        return epoch;
+    }
+};
+
+struct gsim_gpu_scene {
+    gsim_gpu_context* ctx = nullptr;
+    DevField f{};
+    void* mem = nullptr;
+};
+
+namespace {
+
+uint32_t ceil_log2_bits(uint64_t n) {  // bits needed to represent values in [0, n)
+    uint32_t b = 0;
+    while ((uint64_t(1) << b) < n) ++b;
+    return b;
+}
+
+void validate_camera(const gsim_camera& c, uint64_t index) {  // raster.cpp:16-23
+    const std::string who = "camera " + std::to_string(index);
+    if (!(c.fx > 0.0) || !(c.fy > 0.0)) throw ValidationError{who + ": fx, fy must be positive"};
+    if (!(c.near_plane > 0.0) || !(c.far_plane > c.near_plane))
+        throw ValidationError{who + ": need 0 < near < far"};
+    if (c.width < 16 || c.height < 16) throw ValidationError{who + ": resolution below 16x16"};
+    if (c.width > kMaxTilesPerAxis * kTileSize || c.height > kMaxTilesPerAxis * kTileSize)
+        throw ValidationError{who + ": resolution above 4096x4096 (GPU tile-rect limit)"};
+}
+
+DevCamera make_dev_camera(const gsim_camera& c) {
+    DevCamera d{};
+    const dq q{c.pose.rotation[0], c.pose.rotation[1], c.pose.rotation[2], c.pose.rotation[3]};
+    const dm3 r = qmatrix(q);  // raster.cpp:141
+    for (int k = 0; k < 9; ++k) d.r[k] = r.m[k];
+    for (int k = 0; k < 4; ++k) d.q[k] = c.pose.rotation[k];
+    for (int k = 0; k < 3; ++k) d.t[k] = c.pose.translation[k];
+    // camera_center() = pose.inverse().translation = -(conj(q).rotate(t))  (camera.hpp:23)
+    const dq conj{q.w, -q.x, -q.y, -q.z};
+    const dv3 ct = qrotate(conj, mk3(c.pose.translation[0], c.pose.translation[1], c.pose.translation[2]));
+    d.center[0] = -ct.x;
+    d.center[1] = -ct.y;
+    d.center[2] = -ct.z;
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    d.near_p = c.near_plane;
+    d.far_p = c.far_plane;
+    const double tan_fovx = c.width / (2.0 * c.fx);  // raster.cpp:143-146
+    const double tan_fovy = c.height / (2.0 * c.fy);
+    d.limx = 1.3 * tan_fovx;
+    d.limy = 1.3 * tan_fovy;
+    d.width = c.width;
+    d.height = c.height;
+    d.tiles_x = (c.width + kTileSize - 1) / kTileSize;
+    d.tiles_y = (c.height + kTileSize - 1) / kTileSize;
+    return d;
+}
+
+// Paint node ranges like PoseTable (raster.cpp:47-62) into maximal segments and assign each
+// (camera, primitive) a record slot; cameras' slot lists keep primitive order.
+Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
+                const gsim_camera* cameras, uint64_t n_cams) {
+    Plan p;
+    for (uint64_t c = 0; c < n_cams; ++c) validate_camera(cameras[c], c);
+    for (uint64_t k = 0; k < n_nodes; ++k)
+        if (nodes[k].end > n_prims)
+            throw ValidationError{"node " + std::to_string(k) + " range exceeds field size"};
+
+    // elementary intervals
+    std::vector<uint64_t> pts{0, n_prims};
+    for (uint64_t k = 0; k < n_nodes; ++k)
+        if (nodes[k].begin < nodes[k].end) {
+            pts.push_back(nodes[k].begin);
+            pts.push_back(nodes[k].end);
+        }
+    std::sort(pts.begin(), pts.end());
+    pts.erase(std::unique(pts.begin(), pts.end()), pts.end());
+    struct Iv { uint64_t b, e; int64_t owner; };
+    std::vector<Iv> ivs;
+    for (size_t k = 0; k + 1 < pts.size(); ++k)
+        if (pts[k] < pts[k + 1]) ivs.push_back({pts[k], pts[k + 1], -1});
+    for (uint64_t k = 0; k < n_nodes; ++k) {
+        if (!(nodes[k].begin < nodes[k].end)) continue;
+        auto it = std::lower_bound(ivs.begin(), ivs.end(), nodes[k].begin,
+                                   [](const Iv& iv, uint64_t v) { return iv.b < v; });
+        for (; it != ivs.end() && it->b < nodes[k].end; ++it) it->owner = int64_t(k);
+    }
+    // merge equal owners
+    std::vector<Iv> merged;
+    for (const auto& iv : ivs) {
+        if (!merged.empty() && merged.back().owner == iv.owner && merged.back().e == iv.b)
+            merged.back().e = iv.e;
+        else
+            merged.push_back(iv);
+    }
+    if (merged.empty()) merged.push_back({0, 0, -1});
+
+    auto visible = [&](const Iv& iv, uint64_t c) {
+        if (iv.owner < 0) return true;
+        const int env = nodes[iv.owner].env;
+        return env < 0 || env == cameras[c].env;
+    };
+    // slots per camera
+    p.slot_base.assign(n_cams + 1, 0);
+    for (uint64_t c = 0; c < n_cams; ++c) {
+        uint64_t s = 0;
+        for (const auto& iv : merged)
+            if (visible(iv, c)) s += iv.e - iv.b;
+        p.slot_base[c + 1] = p.slot_base[c] + s;
+    }
+    p.slots = p.slot_base[n_cams];
+    if (p.slots >= 0xFFFFFFFFull)
+        throw ValidationError{"batch has " + std::to_string(p.slots) +
+                              " (camera, primitive) slots; split it below 2^32"};
+    std::vector<uint64_t> running(n_cams, 0);
+    for (const auto& iv : merged) {
+        DevSegment s{};
+        s.begin = iv.b;
+        s.end = iv.e;
+        if (iv.owner < 0) {
+            s.q[0] = 1.0;  // RigidTransform::identity()
+        } else {
+            for (int k = 0; k < 4; ++k) s.q[k] = nodes[iv.owner].pose.rotation[k];
+            for (int k = 0; k < 3; ++k) s.t[k] = nodes[iv.owner].pose.translation[k];
+        }
+        s.entry_begin = uint32_t(p.entries.size());
+        for (uint64_t c = 0; c < n_cams; ++c) {
+            if (!visible(iv, c)) continue;
+            SegEntry e{};
+            e.cam = uint32_t(c);
+            e.slot_base = p.slot_base[c] + running[c];
+            running[c] += iv.e - iv.b;
+            p.entries.push_back(e);
+        }
+        s.entry_count = uint32_t(p.entries.size()) - s.entry_begin;
+        p.segs.push_back(s);
+    }
+    // cameras, tiles, output offsets
+    p.tile_base.assign(n_cams + 1, 0);
+    uint64_t out_off = 0;
+    for (uint64_t c = 0; c < n_cams; ++c) {
+        DevCamera d = make_dev_camera(cameras[c]);
+        d.slot_base = p.slot_base[c];
+        d.tile_base = p.tile_base[c];
+        d.out_offset = out_off;
+        out_off += uint64_t(5) * d.width * d.height;
+        p.tile_base[c + 1] = p.tile_base[c] + uint32_t(d.tiles_x * d.tiles_y);
+        p.tiles_x.push_back(d.tiles_x);
+        p.cams.push_back(d);
+    }
+    p.tiles = p.tile_base[n_cams];
+    p.out_floats = out_off;
+    return p;
+}
+
+// Camera plan for rasterize(splats): one camera, slot = splat index, no validation
+// (rasterize does not call validate_camera in the reference).
+Plan build_splat_plan(uint64_t n, const gsim_camera& cam) {
+    if (cam.width < 1 || cam.height < 1 || cam.width > kMaxTilesPerAxis * kTileSize ||
+        cam.height > kMaxTilesPerAxis * kTileSize)
+        throw ValidationError{"rasterize: resolution outside 1..4096"};
+    Plan p;
+    DevCamera d = make_dev_camera(cam);
+    p.slot_base = {0, n};
+    p.slots = n;
+    p.tile_base = {0, uint32_t(d.tiles_x * d.tiles_y)};
+    p.tiles_x = {d.tiles_x};
+    p.tiles = p.tile_base[1];
+    p.out_floats = uint64_t(5) * d.width * d.height;
+    p.cams.push_back(d);
+    return p;
+}
+
+template <class T>
+size_t append_bytes(std::vector<char>& blob, const std::vector<T>& v) {
+    const size_t off = (blob.size() + 15) & ~size_t(15);
+    blob.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+}
+
+void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
+    ctx->cams.reserve(p.cams.size());
+    ctx->cam_slot_base.reserve(p.slot_base.size());
+    ctx->cam_tile_base.reserve(p.tile_base.size());
+    ctx->cam_tiles_x.reserve(std::max<size_t>(p.tiles_x.size(), 1));
+    ctx->segs.reserve(std::max<size_t>(p.segs.size(), 1));
+    ctx->entries.reserve(std::max<size_t>(p.entries.size(), 1));
+    std::vector<char> blob;
+    const size_t o_cams = append_bytes(blob, p.cams);
+    const size_t o_sb = append_bytes(blob, p.slot_base);
+    const size_t o_tb = append_bytes(blob, p.tile_base);
+    const size_t o_tx = append_bytes(blob, p.tiles_x);
+    const size_t o_seg = append_bytes(blob, p.segs);
+    const size_t o_ent = append_bytes(blob, p.entries);
+    // The previous frame's copies out of the staging buffer must have landed.
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->staging.reserve(blob.size());
+    std::memcpy(ctx->staging.ptr, blob.data(), blob.size());
+    const char* h = static_cast<const char*>(ctx->staging.ptr);
+    auto cp = [&](void* dst, size_t off, size_t bytes) {
+        if (bytes) GSIM_CK(cudaMemcpyAsync(dst, h + off, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    };
+    cp(ctx->cams.ptr, o_cams, p.cams.size() * sizeof(DevCamera));
+    cp(ctx->cam_slot_base.ptr, o_sb, p.slot_base.size() * sizeof(uint64_t));
+    cp(ctx->cam_tile_base.ptr, o_tb, p.tile_base.size() * sizeof(uint32_t));
+    cp(ctx->cam_tiles_x.ptr, o_tx, p.tiles_x.size() * sizeof(int));
+    cp(ctx->segs.ptr, o_seg, p.segs.size() * sizeof(DevSegment));
+    cp(ctx->entries.ptr, o_ent, p.entries.size() * sizeof(SegEntry));
+}
+
+void record_stage(gsim_gpu_context* ctx, int stage) {
+    if (ctx->profiling) GSIM_CK(cudaEventRecord(ctx->ev[stage], ctx->stream));
+}
+
+void check_launch() { GSIM_CK(cudaGetLastError()); }
+
+// Workspaces sized for a plan (grow-only).
+void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
+    const uint64_t S = std::max<uint64_t>(p.slots, 1);
+    ctx->records.reserve(S);
+    ctx->keys.reserve(S);
+    for (int k = 0; k < 2; ++k) {
+        ctx->dk[k].reserve(S);
+        ctx->dv[k].reserve(S);
+    }
+    if (ctx->pair_capacity < 4 * S + (1u << 20)) ctx->pair_capacity = 4 * S + (1u << 20);
+    for (int k = 0; k < 2; ++k) {
+        ctx->pk[k].reserve(ctx->pair_capacity);
+        ctx->pv[k].reserve(ctx->pair_capacity);
+    }
+    const uint64_t chunks = std::max((S + kOnesweepTile - 1) / kOnesweepTile,
+                                     (ctx->pair_capacity + kOnesweepTile - 1) / kOnesweepTile);
+    const uint64_t words = std::max<uint64_t>(chunks * 256, (S + kDupTile - 1) / kDupTile);
+    if (words > ctx->status.cap) {
+        ctx->status.reserve(words);
+        GSIM_CK(cudaMemsetAsync(ctx->status.ptr, 0, ctx->status.cap * sizeof(uint64_t), ctx->stream));
+    }
+    ctx->zero_block.reserve(2048 + 64);
+    ctx->counts.reserve(4);
+    ctx->tile_begin.reserve(std::max<uint32_t>(p.tiles, 1));
+    ctx->tile_end.reserve(std::max<uint32_t>(p.tiles, 1));
+}
+
+uint32_t* depth_hist(gsim_gpu_context* c) { return c->zero_block.ptr; }
+uint32_t* tile_hist(gsim_gpu_context* c) { return c->zero_block.ptr + 1024; }
+uint32_t* ticket(gsim_gpu_context* c, int i) { return c->zero_block.ptr + 2048 + i; }
+
+float smallest_float_geq(double x) {
+    float f = float(x);
+    if (double(f) < x) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+// K3 + K4 over records/keys already produced for `p` (by K2 or the splat converter).
+void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
+                         float* out, uint64_t& launches) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t S = p.slots;
+    const int sort_grid_cap = ctx->num_sms * ctx->occ_sort;
+    auto grid_for = [&](uint64_t n, int tile, int cap) {
+        uint64_t g = (n + tile - 1) / tile;
+        if (g < 1) g = 1;
+        return int(std::min<uint64_t>(g, uint64_t(cap)));
+    };
+    // Depth digits: 4 onesweep passes over the visible records (pass 1 compacts).
+    OnesweepArgs oa{};
+    oa.n_dev = ctx->counts.ptr + 0;
+    oa.status = ctx->status.ptr;
+    const int dgrid = grid_for(S, kOnesweepTile, sort_grid_cap);
+    const uint32_t* kin = ctx->keys.ptr;
+    const uint32_t* vin = nullptr;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int o = pass & 1;
+        oa.keys_in = kin;
+        oa.vals_in = vin;
+        oa.keys_out = ctx->dk[o].ptr;
+        oa.vals_out = ctx->dv[o].ptr;
+        oa.n_host = S;
+        oa.hist = depth_hist(ctx) + 256 * pass;
+        oa.ticket = ticket(ctx, pass);
+        oa.epoch = ctx->next_epoch();
+        oa.shift = 8 * pass;
+        launch_onesweep(oa, pass == 0, pass < 3, dgrid, s);
+        check_launch();
+        ++launches;
+        kin = ctx->dk[o].ptr;
+        vin = ctx->dv[o].ptr;
+    }
+    const uint32_t* depth_sorted_slots = ctx->dv[1].ptr;
+    record_stage(ctx, kEvDepth);
+
+    const uint32_t tile_bits = std::max<uint32_t>(1, ceil_log2_bits(p.tiles));
+    const int tile_passes = int((tile_bits + 7) / 8);
+    DupArgs da{};
+    da.slots = depth_sorted_slots;
+    da.n_dev = ctx->counts.ptr + 0;
+    da.records = ctx->records.ptr;
+    da.cam_slot_base = ctx->cam_slot_base.ptr;
+    da.cam_tile_base = ctx->cam_tile_base.ptr;
+    da.cam_tiles_x = ctx->cam_tiles_x.ptr;
+    da.n_cams = int(p.cams.size());
+    da.tile_passes = tile_passes;
+    da.hist = tile_hist(ctx);
+    da.status = ctx->status.ptr;
+    da.pairs_out = ctx->counts.ptr + 1;
+    const int dup_grid = grid_for(S, kDupTile, ctx->num_sms * ctx->occ_dup);
+    uint64_t P = 0;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        da.keys_out = ctx->pk[0].ptr;
+        da.vals_out = ctx->pv[0].ptr;
+        da.capacity = ctx->pair_capacity;
+        da.ticket = ticket(ctx, 8);
+        da.epoch = ctx->next_epoch();
+        launch_scan_dup(da, dup_grid, s);
+        check_launch();
+        ++launches;
+        // The pair count decides the tile-sort grid and the buffer capacity.
+        ctx->readback.reserve(64);
+        GSIM_CK(cudaMemcpyAsync(ctx->readback.ptr, ctx->counts.ptr, 2 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+        const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
+        ctx->stats.visible = rb[0];
+        P = rb[1];
+        if (P <= ctx->pair_capacity) break;
+        // Grow and redo the duplication (the depth order is still valid).
+        ctx->pair_capacity = P + P / 4 + (1u << 20);
+        for (int k = 0; k < 2; ++k) {
+            ctx->pk[k].reserve(ctx->pair_capacity);
+            ctx->pv[k].reserve(ctx->pair_capacity);
+        }
+        const uint64_t words = (ctx->pair_capacity + kOnesweepTile - 1) / kOnesweepTile * 256;
+        if (words > ctx->status.cap) {
+            ctx->status.reserve(words);
+            GSIM_CK(cudaMemsetAsync(ctx->status.ptr, 0, ctx->status.cap * sizeof(uint64_t), s));
+            da.status = ctx->status.ptr;
+        }
+        GSIM_CK(cudaMemsetAsync(tile_hist(ctx), 0, 1024 * sizeof(uint32_t), s));
+        GSIM_CK(cudaMemsetAsync(ticket(ctx, 8), 0, sizeof(uint32_t), s));
+    }
+    if (P > ctx->pair_capacity) throw CudaError{"pair buffer overflow after regrowth"};
+    ctx->last_pairs = P;
+    record_stage(ctx, kEvDup);
+
+    // camera|tile digits: stable onesweep passes over the pairs.
+    const int tgrid = grid_for(P, kOnesweepTile, sort_grid_cap);
+    int cur = 0;
+    for (int pass = 0; pass < tile_passes; ++pass) {
+        OnesweepArgs ta{};
+        ta.keys_in = ctx->pk[cur].ptr;
+        ta.vals_in = ctx->pv[cur].ptr;
+        ta.keys_out = ctx->pk[cur ^ 1].ptr;
+        ta.vals_out = ctx->pv[cur ^ 1].ptr;
+        ta.n_dev = ctx->counts.ptr + 1;
+        ta.hist = tile_hist(ctx) + 256 * pass;
+        ta.status = ctx->status.ptr;
+        ta.ticket = ticket(ctx, 4 + pass);
+        ta.epoch = ctx->next_epoch();
+        ta.shift = 8 * pass;
+        launch_onesweep(ta, false, true, tgrid, s);
+        check_launch();
+        ++launches;
+        cur ^= 1;
+    }
+    record_stage(ctx, kEvTile);
+
+    GSIM_CK(cudaMemsetAsync(ctx->tile_begin.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
+    GSIM_CK(cudaMemsetAsync(ctx->tile_end.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
+    RangesArgs ra{};
+    ra.keys = ctx->pk[cur].ptr;
+    ra.n_dev = ctx->counts.ptr + 1;
+    ra.capacity = ctx->pair_capacity;
+    ra.tile_begin = ctx->tile_begin.ptr;
+    ra.tile_end = ctx->tile_end.ptr;
+    launch_ranges(ra, grid_for(P, 256 * 8, ctx->num_sms * 8), s);
+    check_launch();
+    ++launches;
+    record_stage(ctx, kEvRanges);
+
+    RasterArgs rr{};
+    rr.records = ctx->records.ptr;
+    rr.values = ctx->pv[cur].ptr;
+    rr.tile_begin = ctx->tile_begin.ptr;
+    rr.tile_end = ctx->tile_end.ptr;
+    rr.cams = ctx->cams.ptr;
+    rr.cam_tile_base = ctx->cam_tile_base.ptr;
+    rr.n_cams = int(p.cams.size());
+    rr.normalize_depth = opt.normalize_depth;
+    rr.cutoff = smallest_float_geq(opt.transmittance_cutoff);
+    rr.out = out;
+    launch_raster(rr, p.tiles, s);
+    check_launch();
+    ++launches;
+    record_stage(ctx, kEvRaster);
+    ctx->final_vals = ctx->pv[cur].ptr;
+    ctx->stats.depth_passes = 4;
+    ctx->stats.tile_passes = uint32_t(tile_passes);
+    ctx->stats.pairs = P;
+}
+
+void begin_frame(gsim_gpu_context* ctx) {
+    GSIM_CK(cudaMemsetAsync(ctx->zero_block.ptr, 0, (2048 + 64) * sizeof(uint32_t), ctx->stream));
+    GSIM_CK(cudaMemsetAsync(ctx->counts.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
+}
+
+void finish_stats(gsim_gpu_context* ctx, const Plan& p, uint64_t launches) {
+    ctx->stats.slots = p.slots;
+    ctx->stats.tiles = p.tiles;
+    ctx->stats.launches = launches;
+    ctx->launches_total += launches;
+    ctx->stats.launches_total = ctx->launches_total;
+}
+
+void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                  uint64_t n_nodes, const gsim_camera* cameras, uint64_t n_cams,
+                  const gsim_raster_options* options, float* device_out, Plan& plan) {
+    plan = build_plan(scene->f.n, nodes, n_nodes, cameras, n_cams);
+    gsim_raster_options opt{0, 0, 1e-4};
+    if (options) opt = *options;
+    reserve_workspace(ctx, plan);
+    upload_plan(ctx, plan);
+    float* out = device_out;
+    if (!out) {
+        ctx->out.reserve(std::max<uint64_t>(plan.out_floats, 1));
+        out = ctx->out.ptr;
+    }
+    record_stage(ctx, kEvStart);
+    begin_frame(ctx);
+    uint64_t launches = 0;
+    PreprocessArgs pa{};
+    pa.field = scene->f;
+    pa.segs = ctx->segs.ptr;
+    pa.n_segs = int(plan.segs.size());
+    pa.entries = ctx->entries.ptr;
+    pa.cams = ctx->cams.ptr;
+    pa.records = ctx->records.ptr;
+    pa.keys = ctx->keys.ptr;
+    pa.hist = depth_hist(ctx);
+    pa.visible_count = ctx->counts.ptr + 0;
+    launch_preprocess(pa, false, ctx->num_sms * ctx->occ_pre, ctx->stream);
+    check_launch();
+    ++launches;
+    record_stage(ctx, kEvPre);
+    run_sort_and_raster(ctx, plan, opt, out, launches);
+    finish_stats(ctx, plan, launches);
+}
+
+struct Guard {
+    gsim_gpu_context* ctx;
+    explicit Guard(gsim_gpu_context* c) : ctx(c) {}
+    template <class F>
+    int run(F&& f) {
+        if (!ctx) return GSIM_ERR_VALIDATION;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        try {
+            GSIM_CK(cudaSetDevice(ctx->device));
+            f();
+            ctx->err.clear();
+            return GSIM_OK;
+        } catch (const ValidationError& e) {
+            ctx->err = e.msg;
+            return GSIM_ERR_VALIDATION;
+        } catch (const CudaError& e) {
+            ctx->err = e.msg;
+            return GSIM_ERR_IO;
+        } catch (const std::exception& e) {
+            ctx->err = e.what();
+            return GSIM_ERR_IO;
+        }
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* gsim_gpu_version(void) { return "gsim_gpu 0.1 (sm_100a)"; }
+
+int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
+    if (!out) return GSIM_ERR_VALIDATION;
+    *out = nullptr;
+    auto* ctx = new gsim_gpu_context();
+    try {
+        int n = 0;
+        GSIM_CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw ValidationError{"no CUDA device " + std::to_string(device)};
+        ctx->device = device;
+        GSIM_CK(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        GSIM_CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw CudaError{std::string("gsim_gpu is built for sm_100a; device is ") + prop.name};
+        ctx->num_sms = prop.multiProcessorCount;
+        GSIM_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->ev) GSIM_CK(cudaEventCreate(&e));
+        ctx->occ_pre = 2;
+        ctx->occ_sort = 3;
+        ctx->occ_dup = 4;
+        ctx->zero_block.reserve(2048 + 64);
+        ctx->counts.reserve(4);
+        ctx->readback.reserve(64);
+        ctx->epoch = 0;
+    } catch (const ValidationError& e) {
+        g_create_error = e.msg;
+        delete ctx;
+        return GSIM_ERR_VALIDATION;
+    } catch (const CudaError& e) {
+        g_create_error = e.msg;
+        delete ctx;
+        return GSIM_ERR_IO;
+    }
+    *out = ctx;
+    return GSIM_OK;
+}
+
+int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
+    if (!ctx) return GSIM_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    ctx->records.release();
+    ctx->keys.release();
+    for (int k = 0; k < 2; ++k) {
+        ctx->dk[k].release();
+        ctx->dv[k].release();
+        ctx->pk[k].release();
+        ctx->pv[k].release();
+    }
+    ctx->status.release();
+    ctx->zero_block.release();
+    ctx->counts.release();
+    ctx->tile_begin.release();
+    ctx->tile_end.release();
+    ctx->cams.release();
+    ctx->cam_slot_base.release();
+    ctx->cam_tile_base.release();
+    ctx->cam_tiles_x.release();
+    ctx->segs.release();
+    ctx->entries.release();
+    ctx->out.release();
+    ctx->full.release();
+    ctx->full_vis.release();
+    ctx->splats_in.release();
+    ctx->staging.release();
+    ctx->readback.release();
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return GSIM_OK;
+}
+
+const char* gsim_gpu_last_error(const gsim_gpu_context* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+void* gsim_gpu_stream(gsim_gpu_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int gsim_gpu_synchronize(gsim_gpu_context* ctx) {
+    return Guard(ctx).run([&] { GSIM_CK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int gsim_gpu_set_profiling(gsim_gpu_context* ctx, int enable) {
+    return Guard(ctx).run([&] { ctx->profiling = enable != 0; });
+}
+
+int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out) {
+    return Guard(ctx).run([&] {
+        if (!out) throw ValidationError{"stats: null output"};
+        gsim_render_stats st = ctx->stats;
+        if (ctx->profiling) {
+            GSIM_CK(cudaEventSynchronize(ctx->ev[kEvRaster]));
+            auto ms = [&](int a, int b) {
+                float v = 0.f;
+                GSIM_CK(cudaEventElapsedTime(&v, ctx->ev[a], ctx->ev[b]));
+                return v;
+            };
+            st.ms_preprocess = ms(kEvStart, kEvPre);
+            st.ms_depth_sort = ms(kEvPre, kEvDepth);
+            st.ms_duplicate = ms(kEvDepth, kEvDup);
+            st.ms_tile_sort = ms(kEvDup, kEvTile);
+            st.ms_ranges = ms(kEvTile, kEvRanges);
+            st.ms_raster = ms(kEvRanges, kEvRaster);
+            st.ms_total = ms(kEvStart, kEvRaster);
+        }
+        *out = st;
+    });
+}
+
+int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_gpu_scene** out) {
+    return Guard(ctx).run([&] {
+        if (!v || !out) throw ValidationError{"scene_upload: null argument"};
+        if (v->sh_degree < 0 || v->sh_degree > 3)  // gaussian.cpp:15-17
+            throw ValidationError{"sh_degree " + std::to_string(v->sh_degree) + " outside [0,3]"};
+        const uint64_t n = v->count;
+        if (n >= 0xFFFFFFFFull) throw ValidationError{"field larger than 2^32 - 1 primitives"};
+        if (n && (!v->means || !v->scales || !v->rotations || !v->opacities || !v->sh))
+            throw ValidationError{"scene_upload: null field array"};
+        const int K = (v->sh_degree + 1) * (v->sh_degree + 1);
+        const int planes = (3 * K + 3) / 4;
+        const uint64_t nn = std::max<uint64_t>(n, 1);
+        const size_t geo_bytes = 11 * nn * sizeof(double);
+        const size_t sh_bytes = size_t(planes) * nn * sizeof(float4);
+        std::vector<double> geo(11 * nn, 0.0);
+        std::vector<float4> sh(size_t(planes) * nn, make_float4(0, 0, 0, 0));
+        for (uint64_t i = 0; i < n; ++i) {
+            const double* m = v->means + i * v->means_stride;
+            const double* s = v->scales + i * v->scales_stride;
+            const double* q = v->rotations + i * v->rotations_stride;
+            geo[0 * nn + i] = m[0];
+            geo[1 * nn + i] = m[1];
+            geo[2 * nn + i] = m[2];
+            geo[3 * nn + i] = s[0];
+            geo[4 * nn + i] = s[1];
+            geo[5 * nn + i] = s[2];
+            geo[6 * nn + i] = q[0];
+            geo[7 * nn + i] = q[1];
+            geo[8 * nn + i] = q[2];
+            geo[9 * nn + i] = q[3];
+            geo[10 * nn + i] = v->opacities[i * v->opacities_stride];
+            const double* c = v->sh + i * v->sh_stride;
+            float tmp[48 + 4] = {0};
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < K; ++k) tmp[ch * K + k] = float(c[ch * 16 + k]);
+            for (int p = 0; p < planes; ++p)
+                sh[size_t(p) * nn + i] = make_float4(tmp[4 * p], tmp[4 * p + 1], tmp[4 * p + 2], tmp[4 * p + 3]);
+        }
+        auto* sc = new gsim_gpu_scene();
+        sc->ctx = ctx;
+        try {
+            GSIM_CK(cudaMalloc(&sc->mem, geo_bytes + sh_bytes));
+            GSIM_CK(cudaMemcpy(sc->mem, geo.data(), geo_bytes, cudaMemcpyHostToDevice));
+            GSIM_CK(cudaMemcpy(static_cast<char*>(sc->mem) + geo_bytes, sh.data(), sh_bytes,
+                               cudaMemcpyHostToDevice));
+        } catch (...) {
+            if (sc->mem) cudaFree(sc->mem);
+            delete sc;
+            throw;
+        }
+        double* g = static_cast<double*>(sc->mem);
+        sc->f.n = n;
+        sc->f.sh_degree = v->sh_degree;
+        sc->f.sh_planes = planes;
+        sc->f.mx = g + 0 * nn; sc->f.my = g + 1 * nn; sc->f.mz = g + 2 * nn;
+        sc->f.sx = g + 3 * nn; sc->f.sy = g + 4 * nn; sc->f.sz = g + 5 * nn;
+        sc->f.qw = g + 6 * nn; sc->f.qx = g + 7 * nn; sc->f.qy = g + 8 * nn; sc->f.qz = g + 9 * nn;
+        sc->f.opacity = g + 10 * nn;
+        sc->f.sh = reinterpret_cast<float4*>(static_cast<char*>(sc->mem) + geo_bytes);
+        *out = sc;
+    });
+}
+
+int gsim_gpu_scene_destroy(gsim_gpu_scene* scene) {
+    if (!scene) return GSIM_OK;
+    if (scene->ctx) {
+        std::lock_guard<std::mutex> lk(scene->ctx->mu);
+        cudaSetDevice(scene->ctx->device);
+        cudaStreamSynchronize(scene->ctx->stream);
+    }
+    if (scene->mem) cudaFree(scene->mem);
+    delete scene;
+    return GSIM_OK;
+}
+
+uint64_t gsim_gpu_scene_size(const gsim_gpu_scene* scene) { return scene ? scene->f.n : 0; }
+
+int gsim_gpu_transform_primitives(gsim_gpu_context* ctx, gsim_gpu_scene* scene, uint64_t begin,
+                                  uint64_t end, const gsim_rigid* t) {
+    return Guard(ctx).run([&] {
+        if (!scene || !t) throw ValidationError{"transform_primitives: null argument"};
+        if (begin > end || end > scene->f.n)  // gaussian.cpp:67-71
+            throw ValidationError{"transform_primitives: range [" + std::to_string(begin) + "," +
+                                  std::to_string(end) + ") outside field of size " +
+                                  std::to_string(scene->f.n)};
+        launch_pose(scene->f, begin, end, *t, ctx->num_sms * 8, ctx->stream);
+        check_launch();
+        ctx->launches_total += (end > begin) ? 1 : 0;
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsim_gpu_scene_download(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, double* means,
+                            double* rotations) {
+    return Guard(ctx).run([&] {
+        if (!scene) throw ValidationError{"scene_download: null scene"};
+        const uint64_t n = scene->f.n;
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        std::vector<double> plane(std::max<uint64_t>(n, 1));
+        auto fetch = [&](const double* src, double* dst, int comp, int ncomp) {
+            GSIM_CK(cudaMemcpy(plane.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < n; ++i) dst[i * ncomp + comp] = plane[i];
+        };
+        if (means) {
+            fetch(scene->f.mx, means, 0, 3);
+            fetch(scene->f.my, means, 1, 3);
+            fetch(scene->f.mz, means, 2, 3);
+        }
+        if (rotations) {
+            fetch(scene->f.qw, rotations, 0, 4);
+            fetch(scene->f.qx, rotations, 1, 4);
+            fetch(scene->f.qy, rotations, 2, 4);
+            fetch(scene->f.qz, rotations, 3, 4);
+        }
+    });
+}
+
+int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                     uint64_t n_nodes, const gsim_camera* camera, gsim_projected_splat* out,
+                     uint64_t capacity, uint64_t* count) {
+    return Guard(ctx).run([&] {
+        if (!scene || !camera || !count) throw ValidationError{"project: null argument"};
+        Plan plan = build_plan(scene->f.n, nodes, n_nodes, camera, 1);
+        reserve_workspace(ctx, plan);
+        upload_plan(ctx, plan);
+        const uint64_t S = std::max<uint64_t>(plan.slots, 1);
+        ctx->full.reserve(S);
+        ctx->full_vis.reserve(S);
+        begin_frame(ctx);
+        PreprocessArgs pa{};
+        pa.field = scene->f;
+        pa.segs = ctx->segs.ptr;
+        pa.n_segs = int(plan.segs.size());
+        pa.entries = ctx->entries.ptr;
+        pa.cams = ctx->cams.ptr;
+        pa.records = ctx->records.ptr;
+        pa.keys = ctx->keys.ptr;
+        pa.hist = depth_hist(ctx);
+        pa.visible_count = ctx->counts.ptr;
+        pa.full = ctx->full.ptr;
+        pa.full_visible = ctx->full_vis.ptr;
+        if (plan.slots) {
+            launch_preprocess(pa, true, ctx->num_sms * ctx->occ_pre, ctx->stream);
+            check_launch();
+            ctx->launches_total += 1;
+        }
+        std::vector<uint8_t> vis(plan.slots);
+        std::vector<gsim_projected_splat> all(plan.slots);
+        if (plan.slots) {
+            GSIM_CK(cudaMemcpyAsync(vis.data(), ctx->full_vis.ptr, plan.slots, cudaMemcpyDeviceToHost, ctx->stream));
+            GSIM_CK(cudaMemcpyAsync(all.data(), ctx->full.ptr, plan.slots * sizeof(gsim_projected_splat),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        uint64_t k = 0;
+        for (uint64_t s = 0; s < plan.slots; ++s) {
+            if (!vis[s]) continue;
+            if (out && k < capacity) out[k] = all[s];
+            ++k;
+        }
+        *count = k;
+    });
+}
+
+int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats, uint64_t n,
+                       const gsim_camera* camera, const gsim_raster_options* options,
+                       gsim_target* out) {
+    return Guard(ctx).run([&] {
+        if (!camera || !out || (n && !splats)) throw ValidationError{"rasterize: null argument"};
+        if (n >= 0xFFFFFFFFull) throw ValidationError{"rasterize: too many splats"};
+        Plan plan = build_splat_plan(n, *camera);
+        gsim_raster_options opt{0, 0, 1e-4};
+        if (options) opt = *options;
+        reserve_workspace(ctx, plan);
+        upload_plan(ctx, plan);
+        ctx->splats_in.reserve(std::max<uint64_t>(n, 1));
+        ctx->out.reserve(plan.out_floats);
+        if (n)
+            GSIM_CK(cudaMemcpyAsync(ctx->splats_in.ptr, splats, n * sizeof(gsim_projected_splat),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+        record_stage(ctx, kEvStart);
+        begin_frame(ctx);
+        uint64_t launches = 0;
+        SplatArgs sa{};
+        sa.splats = ctx->splats_in.ptr;
+        sa.n = n;
+        sa.cam = ctx->cams.ptr;
+        sa.records = ctx->records.ptr;
+        sa.keys = ctx->keys.ptr;
+        sa.hist = depth_hist(ctx);
+        sa.visible_count = ctx->counts.ptr;
+        if (n) {
+            launch_splats_to_records(sa, ctx->num_sms * 8, ctx->stream);
+            check_launch();
+            ++launches;
+        }
+        record_stage(ctx, kEvPre);
+        run_sort_and_raster(ctx, plan, opt, ctx->out.ptr, launches);
+        finish_stats(ctx, plan, launches);
+        const DevCamera& c = plan.cams[0];
+        const size_t npx = size_t(c.width) * c.height;
+        GSIM_CK(cudaMemcpyAsync(out->rgb, ctx->out.ptr, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaMemcpyAsync(out->depth, ctx->out.ptr + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaMemcpyAsync(out->accum_alpha, ctx->out.ptr + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        ctx->last_plan = std::move(plan);
+    });
+}
+
+int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                           const gsim_node* nodes, uint64_t n_nodes, const gsim_camera* cameras,
+                           uint64_t n_cameras, const gsim_raster_options* options,
+                           float* device_out) {
+    return Guard(ctx).run([&] {
+        if (!scene || (n_cameras && !cameras) || (n_nodes && !nodes))
+            throw ValidationError{"render: null argument"};
+        Plan plan;
+        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, device_out, plan);
+        ctx->last_plan = std::move(plan);
+    });
+}
+
+float* gsim_gpu_device_output(gsim_gpu_context* ctx) { return ctx ? ctx->out.ptr : nullptr; }
+
+int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                    uint64_t n_nodes, const gsim_camera* cameras, uint64_t n_cameras,
+                    const gsim_raster_options* options, gsim_target* outs) {
+    return Guard(ctx).run([&] {
+        if (!scene || (n_cameras && (!cameras || !outs)) || (n_nodes && !nodes))
+            throw ValidationError{"render: null argument"};
+        Plan plan;
+        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, plan);
+        for (uint64_t c = 0; c < n_cameras; ++c) {
+            const DevCamera& d = plan.cams[c];
+            const size_t npx = size_t(d.width) * d.height;
+            const float* base = ctx->out.ptr + d.out_offset;
+            GSIM_CK(cudaMemcpyAsync(outs[c].rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+            GSIM_CK(cudaMemcpyAsync(outs[c].depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+            GSIM_CK(cudaMemcpyAsync(outs[c].accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        ctx->last_plan = std::move(plan);
+    });
+}
+
+int gsim_gpu_tile_lists(gsim_gpu_context* ctx, uint32_t camera, uint32_t* tile_begin,
+                        uint32_t* values, uint64_t capacity, uint64_t* count) {
+    return Guard(ctx).run([&] {
+        const Plan& p = ctx->last_plan;
+        if (camera >= p.cams.size()) throw ValidationError{"tile_lists: no such camera in the last render"};
+        if (!count) throw ValidationError{"tile_lists: null count"};
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        const uint32_t t0 = p.tile_base[camera], nt = p.tile_base[camera + 1] - t0;
+        std::vector<uint32_t> b(nt), e(nt);
+        if (nt) {
+            GSIM_CK(cudaMemcpy(b.data(), ctx->tile_begin.ptr + t0, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            GSIM_CK(cudaMemcpy(e.data(), ctx->tile_end.ptr + t0, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        }
+        uint64_t first = UINT64_MAX, total = 0;
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (tile_begin) tile_begin[t] = uint32_t(total);
+            if (e[t] > b[t]) {
+                if (first == UINT64_MAX) first = b[t];
+                total += e[t] - b[t];
+            }
+        }
+        if (tile_begin) tile_begin[nt] = uint32_t(total);
+        *count = total;
+        if (values && total) {
+            std::vector<uint32_t> v(total);
+            GSIM_CK(cudaMemcpy(v.data(), ctx->final_vals + first, total * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            const uint64_t sb = p.slot_base[camera];
+            for (uint64_t k = 0; k < total && k < capacity; ++k) values[k] = uint32_t(v[k] - sb);
+        }
+    });
+}
+
+}  // extern "C"
