@@ -124,6 +124,9 @@ typedef struct gsim_render_stats {
     uint64_t tiles;        /* total tiles over all cameras */
     uint64_t launches;     /* kernels launched by the last render */
     uint64_t launches_total; /* kernels launched on this context since creation */
+    uint64_t consumed;     /* pair-list entries the rasterizer fetched before saturating (K) */
+    uint64_t h2d_bytes;    /* host->device bytes copied by the last call */
+    uint64_t d2h_bytes;    /* device->host bytes copied by the last call */
     uint32_t depth_passes; /* radix passes over the depth digits (pre-duplication) */
     uint32_t tile_passes;  /* radix passes over the camera|tile digits (post-duplication) */
     /* per-stage device milliseconds, filled when profiling is on (gsim_gpu_set_profiling) */

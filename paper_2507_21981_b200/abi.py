@@ -68,6 +68,7 @@ class gsim_target(C.Structure):
 class gsim_render_stats(C.Structure):
     _fields_ = [("slots", C.c_uint64), ("visible", C.c_uint64), ("pairs", C.c_uint64),
                 ("tiles", C.c_uint64), ("launches", C.c_uint64), ("launches_total", C.c_uint64),
+                ("consumed", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("depth_passes", C.c_uint32), ("tile_passes", C.c_uint32),
                 ("ms_preprocess", C.c_float), ("ms_depth_sort", C.c_float),
                 ("ms_duplicate", C.c_float), ("ms_tile_sort", C.c_float),

@@ -345,6 +345,8 @@ void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
     GSIM_CK(cudaStreamSynchronize(ctx->stream));
     ctx->staging.reserve(blob.size());
     std::memcpy(ctx->staging.ptr, blob.data(), blob.size());
+    ctx->stats.h2d_bytes = blob.size();
+    ctx->stats.d2h_bytes = 0;
     const char* h = static_cast<const char*>(ctx->staging.ptr);
     auto cp = [&](void* dst, size_t off, size_t bytes) {
         if (bytes) GSIM_CK(cudaMemcpyAsync(dst, h + off, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -537,6 +539,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.normalize_depth = opt.normalize_depth;
     rr.cutoff = smallest_float_geq(opt.transmittance_cutoff);
     rr.out = out;
+    rr.consumed = ctx->counts.ptr + 2;
     launch_raster(rr, p.tiles, s);
     check_launch();
     ++launches;
@@ -716,6 +719,12 @@ int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out) {
     return Guard(ctx).run([&] {
         if (!out) throw ValidationError{"stats: null output"};
         gsim_render_stats st = ctx->stats;
+        {
+            unsigned long long c[4] = {0, 0, 0, 0};
+            GSIM_CK(cudaMemcpyAsync(c, ctx->counts.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+            GSIM_CK(cudaStreamSynchronize(ctx->stream));
+            st.consumed = c[2];
+        }
         if (ctx->profiling) {
             GSIM_CK(cudaEventSynchronize(ctx->ev[kEvRaster]));
             auto ms = [&](int a, int b) {
@@ -915,6 +924,7 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
         if (n)
             GSIM_CK(cudaMemcpyAsync(ctx->splats_in.ptr, splats, n * sizeof(gsim_projected_splat),
                                     cudaMemcpyHostToDevice, ctx->stream));
+        ctx->stats.h2d_bytes += n * sizeof(gsim_projected_splat);
         record_stage(ctx, kEvStart);
         begin_frame(ctx);
         uint64_t launches = 0;
@@ -939,6 +949,7 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
         GSIM_CK(cudaMemcpyAsync(out->rgb, ctx->out.ptr, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
         GSIM_CK(cudaMemcpyAsync(out->depth, ctx->out.ptr + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
         GSIM_CK(cudaMemcpyAsync(out->accum_alpha, ctx->out.ptr + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->stats.d2h_bytes += 5 * npx * sizeof(float);
         GSIM_CK(cudaStreamSynchronize(ctx->stream));
         ctx->last_plan = std::move(plan);
     });
@@ -974,6 +985,7 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
             GSIM_CK(cudaMemcpyAsync(outs[c].rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
             GSIM_CK(cudaMemcpyAsync(outs[c].depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
             GSIM_CK(cudaMemcpyAsync(outs[c].accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->stats.d2h_bytes += 5 * npx * sizeof(float);
         }
         GSIM_CK(cudaStreamSynchronize(ctx->stream));
         ctx->last_plan = std::move(plan);

@@ -92,6 +92,7 @@ struct RasterArgs {
     float cutoff;                    // smallest float >= transmittance_cutoff
     float reserved;
     float* out;                      // per camera [rgb W*H*3 | depth W*H | alpha W*H]
+    unsigned long long* consumed;    // += list entries fetched before the tile saturated
 };
 
 void launch_pose(const DevField& f, uint64_t begin, uint64_t end, const gsim_rigid& t,

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) pose_kernel(DevField f, uint64_t begin, u
 
 // ---- K2: project + shade_sh (raster.cpp:135-232, sh.cpp:10-51) ---------------------------
 template <int DEG, bool kFull>
-__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs args) {
+__global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args) {
     __shared__ uint32_t s_hist[4][256];
     __shared__ uint64_t s_seg_begin[kMaxSmemSegments];
     const DevField f = args.field;

@@ -50,8 +50,10 @@ __global__ void __launch_bounds__(kThreads) raster_kernel(RasterArgs a) {
     // Warp-rectangle pixel-centre bounds used by the mask test: x columns (2) and y rows (4).
     const float tile_x0 = float(tx * kTileSize) + 0.5f, tile_y0 = float(ty * kTileSize) + 0.5f;
 
+    uint32_t fetched = 0;
     for (uint32_t b0 = begin; b0 < end; b0 += kBatch) {
         const uint32_t n_b = (end - b0) < uint32_t(kBatch) ? (end - b0) : uint32_t(kBatch);
+        fetched += n_b;
         uint8_t mask = 0;
         if (uint32_t(tid) < n_b) {
             const uint32_t slot = a.values[b0 + tid];
@@ -125,6 +127,7 @@ __global__ void __launch_bounds__(kThreads) raster_kernel(RasterArgs a) {
         if (__syncthreads_count(done ? 0 : 1) == 0) break;
     }
 
+    if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
     if (x < cam.width && y < cam.height) {
         float* base = a.out + cam.out_offset;
         const size_t npx = size_t(cam.width) * cam.height;

@@ -1,0 +1,304 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the pinned CPU oracle.
+
+Bars (BASELINE.json north star): per-pixel RGB max-abs <= 2e-3 on >= 99.9% of pixels, depth
+within 1e-3 relative (1e-4 m absolute floor below 0.1 m) on >= 99.9% of pixels; the
+projected geometry, visibility set, depth keys and per-tile index lists bit-exact (K2 runs the
+reference's double-precision operation order). Plus the reference's own raster invariants
+(test_raster.cpp) on the GPU.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2507_21981_b200 import ValidationError
+from paper_2507_21981_b200.api import (NodeKind, RasterOptions, RigidTransform, SceneNode,
+                                       quat_from_axis_angle, quat_normalized)
+from tests.helpers import flat_splat, max_diff, parity_stats, ref_camera, single_prim_field
+
+pytestmark = pytest.mark.gpu
+
+GEOM_FIELDS = ("pixel_center", "cov_xx", "cov_xy", "cov_yy", "inv_xx", "inv_xy", "inv_yy",
+               "view_depth", "alpha_peak", "radius", "prim_index")
+
+
+def two_nodes(n, q=(0.9, 0.1, 0.3, 0.2), t=(0.1, -0.2, 0.3)):
+    return [SceneNode("bg", NodeKind.background, RigidTransform(), (0, n // 2)),
+            SceneNode("obj", NodeKind.interactive, RigidTransform(quat_normalized(q), t), (n // 2, n))]
+
+
+def acceptance_scenes(oracle, k, seed0=9000):
+    """acceptance.cpp:47-82 family: <= 2000 prims, 128x128, random SH degree."""
+    rng = np.random.Generator(np.random.PCG64(2024))
+    for scene in range(k):
+        count = int(50 + rng.integers(0, 1951))
+        deg = int(rng.integers(0, 4))
+        field = oracle.random_field(seed0 + scene, count, 3.0, 0.01, 0.05 + (scene % 5) * 0.06, deg)
+        field.means[:, 2] += 3.2
+        nodes = two_nodes(count) if scene % 3 == 0 else []
+        yield scene, field, nodes
+
+
+def assert_parity(gpu, ref, what=""):
+    st = parity_stats(gpu, ref)
+    assert st["rgb_ok"] >= 0.999, (what, st)
+    assert st["depth_ok"] >= 0.999, (what, st)
+    return st
+
+
+# ---- K2: projection ---------------------------------------------------------------------------
+
+def test_project_geometry_bit_exact(ctx, oracle):
+    cam = ref_camera()
+    for scene, field, nodes in acceptance_scenes(oracle, 12):
+        s = ctx.upload(field)
+        g = ctx.project(s, nodes, cam)
+        o = oracle.project(field, nodes, cam)
+        assert len(g) == len(o), scene
+        for name in GEOM_FIELDS:
+            assert np.array_equal(g[name], o[name]), (scene, name)
+        assert np.max(np.abs(g["rgb"] - o["rgb"]), initial=0.0) < 2e-5
+
+
+def test_project_oblique_camera_and_culls(ctx, oracle):
+    """Off-centre camera with frustum-clamped Jacobians, near/far culls and off-screen culls."""
+    field = oracle.random_field(4711, 4000, 12.0, 0.01, 0.4, 3)
+    cam = ref_camera(200, 120, 80.0)
+    cam.pose = RigidTransform(quat_normalized((0.95, 0.1, -0.2, 0.05)), (0.3, -0.1, 2.0))
+    cam.near, cam.far = 0.3, 9.0
+    s = ctx.upload(field)
+    nodes = two_nodes(field.size(), q=(0.2, 0.9, -0.1, 0.3), t=(0.5, 0.0, 1.0))
+    g, o = ctx.project(s, nodes, cam), oracle.project(field, nodes, cam)
+    assert len(g) == len(o) and len(o) > 100
+    for name in GEOM_FIELDS:
+        assert np.array_equal(g[name], o[name]), name
+
+
+# ---- K3: tile lists ---------------------------------------------------------------------------
+
+def test_tile_lists_bit_exact(ctx, oracle):
+    cam = ref_camera(160, 112, 110.0)
+    for scene, field, nodes in acceptance_scenes(oracle, 8, seed0=7000):
+        s = ctx.upload(field)
+        ctx.render(s, nodes, [cam])
+        offsets, values = ctx.tile_lists(0)
+        splats = oracle.project(field, nodes, cam)
+        tb, vals = oracle.rasterize_lists(splats, cam)
+        tiles = len(tb) - 1
+        assert np.array_equal(offsets[: tiles + 1], tb), scene
+        assert np.array_equal(values, splats["prim_index"][vals]), scene
+
+
+# ---- K4 / end to end ----------------------------------------------------------------------------
+
+def test_render_parity_acceptance_scenes(ctx, oracle):
+    cam = ref_camera()
+    worst = 0.0
+    for scene, field, nodes in acceptance_scenes(oracle, 40):
+        s = ctx.upload(field)
+        g = ctx.render(s, nodes, [cam])[0]
+        o = oracle.render(field, nodes, [cam])[0]
+        st = assert_parity(g, o, scene)
+        worst = max(worst, st["rgb_max"])
+        assert st["alpha_max"] < 5e-3, (scene, st)
+    assert worst < 0.02
+
+
+def test_rasterize_splats_parity(ctx, oracle):
+    cam = ref_camera(128, 96, 100.0)
+    for scene, field, nodes in acceptance_scenes(oracle, 10, seed0=8000):
+        splats = oracle.project(field, nodes, cam)
+        g = ctx.rasterize(splats, cam)
+        o = oracle.rasterize(splats, cam)
+        assert_parity(g, o, scene)
+        opt = RasterOptions(normalize_depth=True, transmittance_cutoff=1e-3)
+        assert_parity(ctx.rasterize(splats, cam, opt), oracle.rasterize(splats, cam, opt), scene)
+
+
+def test_two_splat_recurrence(ctx):  # test_raster.cpp:119-133
+    cam = ref_camera(32, 32, 50.0)
+    c1, c2 = (1.0, 0.0, 0.2), (0.0, 1.0, 0.6)
+    splats = np.concatenate([flat_splat(16, 16, 1.0, 0.5, c1), flat_splat(16, 16, 2.0, 0.5, c2)])
+    t = ctx.rasterize(splats, cam)
+    assert t.accum_alpha[9, 7] == pytest.approx(0.75, abs=1e-6)
+    assert t.depth[9, 7] == pytest.approx(1.0, abs=1e-6)
+    for ch in range(3):
+        assert t.rgb[9, 7, ch] == pytest.approx(0.5 * c1[ch] + 0.25 * c2[ch], abs=1e-6)
+    # same everywhere (flat splats cover the image)
+    assert np.allclose(t.accum_alpha, 0.75, atol=1e-6)
+
+
+def test_empty_renders_zeros(ctx):  # test_raster.cpp:135-140
+    t = ctx.rasterize(flat_splat(0, 0, 1, 1, (0, 0, 0))[:0], ref_camera(32, 32))
+    assert not t.rgb.any() and not t.depth.any() and not t.accum_alpha.any()
+    field = single_prim_field((0, 0, -1), (1, 1, 1), 0.5)  # fully culled scene
+    t = ctx.render(ctx.upload(field), [], [ref_camera(48, 32)])[0]
+    assert not t.rgb.any() and not t.depth.any() and not t.accum_alpha.any()
+
+
+@pytest.mark.parametrize("opacity", [0.3, 0.7, 0.995])
+def test_single_splat_peak_alpha(ctx, opacity):  # test_raster.cpp:159-177
+    field = single_prim_field((0, 0, 2), (0.05, 0.05, 0.05), opacity)
+    cam = ref_camera(129, 129)
+    cam.cx = cam.cy = 64.5
+    t = ctx.render(ctx.upload(field), [], [cam])[0]
+    assert t.accum_alpha[64, 64] == pytest.approx(min(opacity, 0.99), rel=1e-5)
+
+
+def test_on_axis_footprint(ctx):  # test_raster.cpp:58-78
+    field = single_prim_field((0, 0, 2), (0.1, 0.1, 0.1), 0.7)
+    cam = ref_camera()
+    s = ctx.project(ctx.upload(field), [], cam)
+    assert len(s) == 1
+    assert s[0]["cov_xx"] == pytest.approx(25.3, rel=1e-9)
+    assert s[0]["pixel_center"][0] == pytest.approx(64.0)
+
+
+def test_deterministic_and_batch_equals_single(ctx, oracle):  # test_raster.cpp:179-211
+    field = oracle.random_field(78, 3000, 3.0, 0.01, 0.3, 1)
+    field.means[:, 2] += 3.0
+    s = ctx.upload(field)
+    cam_a = ref_camera()
+    cam_b = ref_camera()
+    cam_b.pose = RigidTransform((1.0, 0.0, 0.0, 0.0), (0.2, 0.0, 0.0))
+    single = ctx.render(s, [], [cam_a])
+    again = ctx.render(s, [], [cam_a])
+    batch = ctx.render(s, [], [cam_a, cam_b, cam_a])
+    for t in (again[0], batch[0], batch[2]):
+        assert np.array_equal(single[0].rgb, t.rgb)
+        assert np.array_equal(single[0].depth, t.depth)
+        assert np.array_equal(single[0].accum_alpha, t.accum_alpha)
+    assert not np.array_equal(batch[0].rgb, batch[1].rgb)
+
+
+def test_monotone_alpha_without_cutoff(ctx, oracle):  # test_raster.cpp:213-229
+    cam = ref_camera(64, 64)
+    opt = RasterOptions(transmittance_cutoff=0.0)
+    for rnd in range(10):
+        field = oracle.random_field(3000 + rnd, 60, 2.0, 0.02, 0.3, 0)
+        field.means[:, 2] += 2.5
+        splats = oracle.project(field, [], cam)
+        if len(splats) < 2:
+            continue
+        a = ctx.rasterize(splats, cam, opt).accum_alpha
+        b = ctx.rasterize(splats[:-1], cam, opt).accum_alpha
+        assert np.all(a >= b - 1e-6)
+
+
+def test_rigid_equivariance(ctx, oracle):  # test_raster.cpp:231-253
+    field = oracle.random_field(79, 200, 2.0, 0.02, 0.3, 2)
+    s = ctx.upload(field)
+    nodes = [SceneNode("bg", NodeKind.background, RigidTransform(), (0, field.size()))]
+    cam = ref_camera()
+    cam.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.2), (0.1, -0.2, 4.0))
+    before = ctx.render(s, nodes, [cam])[0]
+    motion = RigidTransform(quat_from_axis_angle((1, 2, 3), 0.8), (5.0, -2.0, 1.0))
+    moved = [SceneNode("bg", NodeKind.interactive, motion, (0, field.size()))]
+    cam2 = ref_camera()
+    cam2.pose = cam.pose * motion.inverse()
+    after = ctx.render(s, moved, [cam2])[0]
+    rgb, depth = max_diff(before, after)
+    assert rgb <= 1e-4 and depth <= 1e-3
+
+
+# ---- K1 --------------------------------------------------------------------------------------
+
+def test_transform_primitives_bit_exact(ctx, oracle):  # gaussian.cpp:65-79, test_core_types.cpp
+    field = oracle.random_field(12, 5000, 2.0, 0.01, 0.3, 1)
+    s = ctx.upload(field)
+    m, q = field.means.copy(), field.rotations.copy()
+    rt = RigidTransform(quat_normalized((0.3, 0.5, -0.2, 0.7)), (0.5, -1.25, 2.0))
+    s.transform_primitives(100, 4000, rt)
+    oracle.transform_primitives(m, q, 100, 4000, rt)
+    gm, gq = s.download()
+    assert np.array_equal(gm, m) and np.array_equal(gq, q)
+    s.transform_primitives(0, 5000, RigidTransform())  # identity: bit-exact no-op
+    gm2, gq2 = s.download()
+    assert np.array_equal(gm2, gm) and np.array_equal(gq2, gq)
+    with pytest.raises(ValidationError):
+        s.transform_primitives(10, 5001, rt)
+
+
+def test_validation_errors(ctx, oracle):
+    field = oracle.random_field(5, 100, 2.0, 0.01, 0.3, 0)
+    s = ctx.upload(field)
+    bad = ref_camera()
+    bad.fx = 0.0
+    with pytest.raises(ValidationError, match="fx, fy"):
+        ctx.render(s, [], [bad])
+    small = ref_camera(8, 8)
+    with pytest.raises(ValidationError, match="16x16"):
+        ctx.render(s, [], [small])
+    nf = ref_camera()
+    nf.near, nf.far = 1.0, 0.5
+    with pytest.raises(ValidationError, match="near"):
+        ctx.render(s, [], [nf])
+    with pytest.raises(ValidationError, match="exceeds field size"):
+        ctx.render(s, [SceneNode("x", NodeKind.background, RigidTransform(), (0, 101))], [ref_camera()])
+
+
+# ---- batched environments (BASELINE configs 2 and 4) -------------------------------------------
+
+def test_env_batch_equals_separate_renders(ctx, oracle):
+    bg = oracle.random_field(1, 3000, 3.0, 0.01, 0.2, 2)
+    objs = [oracle.random_field(10 + e, 500, 1.0, 0.01, 0.1, 2) for e in range(3)]
+    from paper_2507_21981_b200.api import GaussianField
+    field = GaussianField(np.concatenate([bg.means] + [o.means for o in objs]),
+                          np.concatenate([bg.scales] + [o.scales for o in objs]),
+                          np.concatenate([bg.rotations] + [o.rotations for o in objs]),
+                          np.concatenate([bg.opacities] + [o.opacities for o in objs]),
+                          np.concatenate([bg.sh] + [o.sh for o in objs]), 2)
+    field.means[:, 2] += 3.0
+    s = ctx.upload(field)
+    nodes = [SceneNode("bg", NodeKind.background, RigidTransform(), (0, 3000))]
+    for e in range(3):
+        nodes.append(SceneNode(f"o{e}", NodeKind.interactive,
+                               RigidTransform(quat_from_axis_angle((0, 0, 1), 0.3 * e + 0.1), (0.1 * e, 0, 0.2)),
+                               (3000 + 500 * e, 3500 + 500 * e), env=e))
+    cams = []
+    for e in range(3):
+        for k in range(2):
+            c = ref_camera(96, 64, 80.0)
+            c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.05 * k - 0.02 * e), (0.1 * k, 0.05 * e, 0.0))
+            c.env = e
+            cams.append(c)
+    batch = ctx.render(s, nodes, cams)
+    for e in range(3):
+        sep = ctx.render(s, nodes, cams[2 * e: 2 * e + 2])
+        for k in range(2):
+            assert np.array_equal(batch[2 * e + k].rgb, sep[k].rgb)
+            assert np.array_equal(batch[2 * e + k].depth, sep[k].depth)
+        o = oracle.render(field, nodes, cams[2 * e: 2 * e + 2])
+        for k in range(2):
+            assert_parity(batch[2 * e + k], o[k], (e, k))
+
+
+# ---- BASELINE-shaped parity ----------------------------------------------------------------
+
+def test_config0_parity(ctx, oracle):
+    from paper_2507_21981_b200.scenes import config0
+    w = config0(seed=3, n=100_000)
+    g = ctx.render(ctx.upload(w.field), w.nodes, w.cameras)[0]
+    o = oracle.render(w.field, w.nodes, w.cameras)[0]
+    st = assert_parity(g, o, "cfg0")
+    print("cfg0 parity", st)
+
+
+@pytest.mark.slow
+def test_config1_one_camera_parity(ctx, oracle):
+    """Full 1.08M-Gaussian SH3 config-1 scene with posed objects, one of the five cameras
+    against the oracle, plus the pair count and the tile lists of that camera."""
+    from paper_2507_21981_b200.scenes import config1
+    w = config1(seed=1)
+    nodes = w.frame_nodes(0)
+    cam = w.cameras[2]
+    s = ctx.upload(w.field)
+    g = ctx.render(s, nodes, [cam])[0]
+    offsets, values = ctx.tile_lists(0)
+    splats = oracle.project(w.field, nodes, cam)
+    o = oracle.rasterize(splats, cam)
+    st = assert_parity(g, o, "cfg1")
+    print("cfg1 parity", st)
+    tb, vals = oracle.rasterize_lists(splats, cam)
+    assert np.array_equal(offsets[: len(tb)], tb)
+    assert np.array_equal(values, splats["prim_index"][vals])
