@@ -756,7 +756,8 @@ int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_
         const int K = (v->sh_degree + 1) * (v->sh_degree + 1);
         const int planes = (3 * K + 3) / 4;
         const uint64_t nn = std::max<uint64_t>(n, 1);
-        const size_t geo_bytes = 11 * nn * sizeof(double);
+        // SH planes are float4: keep their base 256-byte aligned whatever n is
+        const size_t geo_bytes = (11 * nn * sizeof(double) + 255) & ~size_t(255);
         const size_t sh_bytes = size_t(planes) * nn * sizeof(float4);
         std::vector<double> geo(11 * nn, 0.0);
         std::vector<float4> sh(size_t(planes) * nn, make_float4(0, 0, 0, 0));
@@ -786,7 +787,7 @@ int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_
         sc->ctx = ctx;
         try {
             GSIM_CK(cudaMalloc(&sc->mem, geo_bytes + sh_bytes));
-            GSIM_CK(cudaMemcpy(sc->mem, geo.data(), geo_bytes, cudaMemcpyHostToDevice));
+            GSIM_CK(cudaMemcpy(sc->mem, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
             GSIM_CK(cudaMemcpy(static_cast<char*>(sc->mem) + geo_bytes, sh.data(), sh_bytes,
                                cudaMemcpyHostToDevice));
         } catch (...) {
