@@ -110,6 +110,7 @@ struct gsim_gpu_context {
 
     DevBuf<Record> records;
     DevBuf<uint32_t> keys;
+    DevBuf<uint32_t> rects;
     DevBuf<uint32_t> dk[2], dv[2];   // depth sort ping-pong
     DevBuf<uint32_t> pk[2], pv[2];   // tile sort ping-pong
     DevBuf<uint64_t> status;
@@ -370,6 +371,7 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     const uint64_t S = std::max<uint64_t>(p.slots, 1);
     ctx->records.reserve(S);
     ctx->keys.reserve(S);
+    ctx->rects.reserve(S);
     for (int k = 0; k < 2; ++k) {
         ctx->dk[k].reserve(S);
         ctx->dv[k].reserve(S);
@@ -445,7 +447,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     DupArgs da{};
     da.slots = depth_sorted_slots;
     da.n_dev = ctx->counts.ptr + 0;
-    da.records = ctx->records.ptr;
+    da.rects = ctx->rects.ptr;
     da.cam_slot_base = ctx->cam_slot_base.ptr;
     da.cam_tile_base = ctx->cam_tile_base.ptr;
     da.cam_tiles_x = ctx->cam_tiles_x.ptr;
@@ -586,6 +588,7 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     pa.entries = ctx->entries.ptr;
     pa.cams = ctx->cams.ptr;
     pa.records = ctx->records.ptr;
+    pa.rects = ctx->rects.ptr;
     pa.keys = ctx->keys.ptr;
     pa.hist = depth_hist(ctx);
     pa.visible_count = ctx->counts.ptr + 0;
@@ -671,6 +674,7 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->records.release();
     ctx->keys.release();
+    ctx->rects.release();
     for (int k = 0; k < 2; ++k) {
         ctx->dk[k].release();
         ctx->dv[k].release();
@@ -881,6 +885,7 @@ int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const g
         pa.entries = ctx->entries.ptr;
         pa.cams = ctx->cams.ptr;
         pa.records = ctx->records.ptr;
+    pa.rects = ctx->rects.ptr;
         pa.keys = ctx->keys.ptr;
         pa.hist = depth_hist(ctx);
         pa.visible_count = ctx->counts.ptr;
@@ -934,6 +939,7 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
         sa.n = n;
         sa.cam = ctx->cams.ptr;
         sa.records = ctx->records.ptr;
+        sa.rects = ctx->rects.ptr;
         sa.keys = ctx->keys.ptr;
         sa.hist = depth_hist(ctx);
         sa.visible_count = ctx->counts.ptr;

@@ -20,6 +20,7 @@ struct PreprocessArgs {
     const SegEntry* entries;
     const DevCamera* cams;
     Record* records;                 // [slots]
+    uint32_t* rects;                 // [slots] packed tile rect (dup reads this, L2-resident)
     uint32_t* keys;                  // [slots], kInvalidKey when culled / no tile
     uint32_t* hist;                  // [4][256] digit histograms of valid keys
     unsigned long long* visible_count;
@@ -32,6 +33,7 @@ struct SplatArgs {
     uint64_t n;
     const DevCamera* cam;
     Record* records;
+    uint32_t* rects;
     uint32_t* keys;
     uint32_t* hist;
     unsigned long long* visible_count;
@@ -56,7 +58,7 @@ struct OnesweepArgs {
 struct DupArgs {
     const uint32_t* slots;           // [V] record slots in depth order
     const unsigned long long* n_dev; // V
-    const Record* records;
+    const uint32_t* rects;           // [slots] packed tile rects
     const uint64_t* cam_slot_base;   // [n_cams + 1]
     const uint32_t* cam_tile_base;   // [n_cams + 1]
     const int* cam_tiles_x;          // [n_cams]

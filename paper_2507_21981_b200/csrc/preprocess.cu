@@ -264,9 +264,10 @@ __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args)
             rec.b = make_float4(__double2float_rn(cov_yy * inv_det),
                                 __double2float_rn(-cov_xy * inv_det),
                                 __double2float_rn(cov_xx * inv_det), __double2float_rn(opacity));
-            rec.c = make_float4(rgb[0], rgb[1], rgb[2],
-                                __uint_as_float(pack_rect(tx0, ty0, tx1, ty1)));
+            const uint32_t rec_rect = pack_rect(tx0, ty0, tx1, ty1);
+            rec.c = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(rec_rect));
             args.records[slot] = rec;
+            args.rects[slot] = rec_rect;
             const uint32_t key = __float_as_uint(fz);  // depth_sort_key, raster.hpp:45-47
             args.keys[slot] = key;
             atomicAdd(&s_hist[0][key & 255], 1u);
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(256) splats_to_records_kernel(SplatArgs args) 
                             __double2float_rn(sp.rgb[2]),
                             __uint_as_float(pack_rect(tx0, ty0, tx1, ty1)));
         args.records[i] = rec;
+        args.rects[i] = pack_rect(tx0, ty0, tx1, ty1);
         uint32_t key = __float_as_uint(fz);
         if (key == kInvalidKey) key = kInvalidKey - 1;  // reserved sentinel (a NaN payload)
         args.keys[i] = key;

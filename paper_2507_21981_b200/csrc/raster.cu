@@ -1,13 +1,18 @@
 // raster.cu — K4: per-tile front-to-back compositing (raster.cpp:273-320).
 //
 // One 256-thread CTA per (camera, 16x16 tile); thread = pixel. The 8 warps own 8x4 pixel
-// sub-rectangles so a splat's footprint test can be made per warp. The tile's depth-sorted
-// list is consumed in batches of 256 records: each thread gathers one 48-byte record into
-// shared memory and computes an 8-bit mask of the warp rectangles the splat can reach
-// (its 3-sigma box intersected with the alpha >= 1/255 ellipse bound, conservatively
-// widened). Each warp then walks only the splats whose bit it owns (ballot + ffs keeps the
-// depth order), and drops out as soon as all its pixels are saturated; the CTA leaves when
-// __syncthreads_count says every pixel is done.
+// sub-rectangles. The tile's depth-sorted list is consumed in batches of 256 records:
+//   1. each thread gathers one 48-byte record into shared memory and computes an 8-bit mask
+//      of the warp rectangles the splat can reach (its 3-sigma box intersected with the
+//      alpha >= 1/255 ellipse bound, conservatively widened, so no contributing splat is
+//      ever dropped);
+//   2. each warp compacts the indices of the splats whose bit it owns into a private list
+//      (ballot + popc keeps the depth order);
+//   3. each warp walks its list with a branch-free blend: a splat that fails the box test or
+//      the 1/255 skip gets alpha 0, which leaves C, D, A and T bit-for-bit unchanged, so the
+//      result equals the reference's skip-with-continue loop;
+//   4. a warp stops when all its pixels are saturated; the CTA leaves when
+//      __syncthreads_count says every pixel is done.
 //
 // Per-pixel contract (raster.cpp:284-318): box test |dx|>r || |dy|>r, q with 2*inv_xy,
 // alpha = min(o*exp(-q/2), 0.99), skip alpha < 1/255, accumulate, T *= 1-alpha, stop after
@@ -22,104 +27,149 @@ namespace gsim_gpu {
 
 namespace {
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kBatch = 256;
 constexpr float kLog2e = 1.4426950408889634f;
+
+struct alignas(16) SmemSplat {
+    float4 p0;  // u, v, radius, log2(opacity)
+    float4 p1;  // inv_xx, 2*inv_xy, inv_yy, depth
+    float4 p2;  // r, g, b, -
+};
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads) raster_kernel(RasterArgs a) {
-    __shared__ float4 s_p0[kBatch];  // u, v, radius, log2(opacity)
-    __shared__ float4 s_p1[kBatch];  // inv_xx, 2*inv_xy, inv_yy, depth
-    __shared__ float4 s_p2[kBatch];  // r, g, b, -
+__global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
+    __shared__ SmemSplat s_spl[kBatch];
     __shared__ uint8_t s_mask[kBatch];
+    __shared__ uint8_t s_list[kWarps][kBatch];
 
     const uint32_t g = blockIdx.x;
     const int cam_idx = upper_index(a.cam_tile_base, a.n_cams, g);
     const DevCamera& cam = a.cams[cam_idx];
     const uint32_t tile = g - a.cam_tile_base[cam_idx];
-    const int tx = int(tile % uint32_t(cam.tiles_x)), ty = int(tile / uint32_t(cam.tiles_x));
+    const int tiles_x = cam.tiles_x;
+    const int tx = int(tile % uint32_t(tiles_x)), ty = int(tile / uint32_t(tiles_x));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // warp w owns the 8x4 block (w % 2, w / 2) of the tile; lane = (lane % 8, lane / 8)
-    const int wx0 = tx * kTileSize + (warp & 1) * 8, wy0 = ty * kTileSize + (warp >> 1) * 4;
-    const int x = wx0 + (lane & 7), y = wy0 + (lane >> 3);
+    const int x = tx * kTileSize + (warp & 1) * 8 + (lane & 7);
+    const int y = ty * kTileSize + (warp >> 1) * 4 + (lane >> 3);
     const float px = float(x) + 0.5f, py = float(y) + 0.5f;
 
     const uint32_t begin = a.tile_begin[g], end = a.tile_end[g];
+    const float cutoff = a.cutoff;
     float cr = 0.f, cg = 0.f, cb = 0.f, d = 0.f, acc = 0.f, T = 1.f;
     bool done = false;
 
-    // Warp-rectangle pixel-centre bounds used by the mask test: x columns (2) and y rows (4).
+    const uint32_t spl_base = uint32_t(__cvta_generic_to_shared(&s_spl[0]));
+    const uint32_t mask_base = uint32_t(__cvta_generic_to_shared(&s_mask[0]));
+    const uint32_t list_base = uint32_t(__cvta_generic_to_shared(&s_list[warp][0]));
+    // Pixel-centre bounds of the 2 warp columns and 4 warp rows of this tile.
     const float tile_x0 = float(tx * kTileSize) + 0.5f, tile_y0 = float(ty * kTileSize) + 0.5f;
 
     uint32_t fetched = 0;
     for (uint32_t b0 = begin; b0 < end; b0 += kBatch) {
         const uint32_t n_b = (end - b0) < uint32_t(kBatch) ? (end - b0) : uint32_t(kBatch);
         fetched += n_b;
-        uint8_t mask = 0;
+        uint32_t mask = 0;
         if (uint32_t(tid) < n_b) {
-            const uint32_t slot = a.values[b0 + tid];
-            const Record r = a.records[slot];
-            const float u = r.a.x, v = r.a.y, rad = r.a.w, op = r.b.w;
-            const float ia = r.b.x, ib = r.b.y, ic = r.b.z;
-            s_p0[tid] = make_float4(u, v, rad, __log2f(op));
-            s_p1[tid] = make_float4(ia, 2.0f * ib, ic, r.a.z);
-            s_p2[tid] = make_float4(r.c.x, r.c.y, r.c.z, 0.f);
+            const uint32_t slot = __ldg(a.values + b0 + tid);
+            const float4 ra = __ldg(&a.records[slot].a);
+            const float4 rb = __ldg(&a.records[slot].b);
+            const float4 rc = __ldg(&a.records[slot].c);
+            const float u = ra.x, v = ra.y, rad = ra.w, op = rb.w;
+            const float ia = rb.x, ib = rb.y, ic = rb.z;
+            s_spl[tid].p0 = make_float4(u, v, rad, __log2f(op));
+            s_spl[tid].p1 = make_float4(ia, 2.0f * ib, ic, ra.z);
+            s_spl[tid].p2 = make_float4(rc.x, rc.y, rc.z, 0.f);
             // Reachable half-extents: the box test bounds |dx|,|dy| <= r; alpha >= 1/255 needs
             // q <= qc = 2 ln(255 o), whose ellipse has half-extents sqrt(qc * cov_xx/yy).
             float ex = rad, ey = rad;
             if (op * 255.0f < 1.0f) {
                 ex = -1.0f;  // can never reach alpha 1/255
             } else {
-                const float qc = 2.0f * logf(op * 255.0f);
+                const float qc = 2.0f * __logf(op * 255.0f);
                 const float det = ia * ic - ib * ib;
                 if (det > 0.0f) {
-                    const float cxx = ic / det, cyy = ia / det;  // covariance from the conic
-                    const float bx = sqrtf(qc * cxx) * 1.01f + 0.05f;
-                    const float by = sqrtf(qc * cyy) * 1.01f + 0.05f;
+                    const float inv = 1.0f / det;
+                    const float bx = sqrtf(qc * ic * inv) * 1.01f + 0.05f;
+                    const float by = sqrtf(qc * ia * inv) * 1.01f + 0.05f;
                     ex = fminf(ex, bx);
                     ey = fminf(ey, by);
                 }
             }
             if (ex >= 0.0f) {
-                // column c covers pixel centres [tile_x0 + 8c, tile_x0 + 8c + 7]
+                uint32_t cols = 0, rows = 0;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    const float lo = tile_x0 + 8.0f * c, hi = lo + 7.0f;
-                    if (u + ex < lo || u - ex > hi) continue;
-#pragma unroll
-                    for (int rr = 0; rr < 4; ++rr) {
-                        const float ylo = tile_y0 + 4.0f * rr, yhi = ylo + 3.0f;
-                        if (v + ey < ylo || v - ey > yhi) continue;
-                        mask |= uint8_t(1u << (rr * 2 + c));
-                    }
+                    const float lo = tile_x0 + 8.0f * c;
+                    cols |= (u + ex >= lo && u - ex <= lo + 7.0f) ? (1u << c) : 0u;
                 }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float lo = tile_y0 + 4.0f * r;
+                    rows |= (v + ey >= lo && v - ey <= lo + 3.0f) ? (1u << r) : 0u;
+                }
+                // bit (row * 2 + col) for every reachable (col, row)
+                const uint32_t colmask = (cols & 1u) * 0x55u | ((cols >> 1) & 1u) * 0xAAu;
+                const uint32_t rowmask = (rows & 1u) * 0x03u | ((rows >> 1) & 1u) * 0x0Cu |
+                                         ((rows >> 2) & 1u) * 0x30u | ((rows >> 3) & 1u) * 0xC0u;
+                mask = colmask & rowmask;
             }
         }
-        s_mask[tid] = mask;
+        s_mask[tid] = uint8_t(mask);
         __syncthreads();
 
         if (!__all_sync(0xffffffffu, done)) {
-            for (int j = 0; j < int(n_b); j += 32) {
-                uint32_t m = __ballot_sync(0xffffffffu, (s_mask[j + lane] >> warp) & 1u);
-                while (m) {
-                    const int s = j + __ffs(m) - 1;
-                    m &= m - 1;
-                    if (done) continue;
-                    const float4 p0 = s_p0[s];
+            // Compact this warp's splats (depth order preserved).
+            uint32_t count = 0;
+            for (uint32_t j = 0; j < n_b; j += 32) {
+                const uint32_t idx = j + lane;
+                const bool mine = idx < n_b && ((lds8(mask_base + idx) >> warp) & 1u);
+                const uint32_t bits = __ballot_sync(0xffffffffu, mine);
+                if (mine) s_list[warp][count + __popc(bits & lanemask_lt())] = uint8_t(idx);
+                count += __popc(bits);
+            }
+            __syncwarp();
+            for (uint32_t k0 = 0; k0 < count; k0 += 32) {
+                const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
+#pragma unroll 2
+                for (uint32_t k = k0; k < k1; ++k) {
+                    const uint32_t s = lds8(list_base + k);
+                    const uint32_t sa = spl_base + s * uint32_t(sizeof(SmemSplat));
+                    const float4 p0 = lds128(sa);
+                    const float4 p1 = lds128(sa + 16);
+                    const float4 p2 = lds128(sa + 32);
                     const float dx = p0.x - px, dy = p0.y - py;
-                    if (fabsf(dx) > p0.z || fabsf(dy) > p0.z) continue;
-                    const float4 p1 = s_p1[s];
                     const float q = p1.x * dx * dx + p1.y * dx * dy + p1.z * dy * dy;
-                    const float alpha = fminf(exp2f(fmaf(q, -0.5f * kLog2e, p0.w)), 0.99f);
-                    if (alpha < float(kAlphaSkip)) continue;
-                    const float4 p2 = s_p2[s];
+                    const float e = fminf(ex2_approx(fmaf(q, -0.5f * kLog2e, p0.w)), 0.99f);
+                    const bool ok = !done && fmaxf(fabsf(dx), fabsf(dy)) <= p0.z &&
+                                    e >= float(kAlphaSkip);
+                    const float alpha = ok ? e : 0.0f;
                     const float w = alpha * T;
-                    cr += p2.x * w;
-                    cg += p2.y * w;
-                    cb += p2.z * w;
-                    d += p1.w * w;
+                    cr = fmaf(p2.x, w, cr);
+                    cg = fmaf(p2.y, w, cg);
+                    cb = fmaf(p2.z, w, cb);
+                    d = fmaf(p1.w, w, d);
                     acc += w;
                     T *= 1.0f - alpha;
-                    if (T < a.cutoff) done = true;
+                    done = done || (ok && T < cutoff);
                 }
                 if (__all_sync(0xffffffffu, done)) break;
             }

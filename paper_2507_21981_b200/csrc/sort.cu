@@ -65,7 +65,7 @@ __device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoc
 }  // namespace
 
 template <bool kFirst, bool kWriteKeys>
-__global__ void __launch_bounds__(kThreads) onesweep_kernel(OnesweepArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     __shared__ uint32_t s_keys[kOnesweepTile];
     __shared__ uint32_t s_vals[kOnesweepTile];
     __shared__ uint32_t s_warp_hist[kWarps][kRadix];
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads) scan_dup_kernel(DupArgs a) {
             cnt[j] = 0;
             if (e < n_here) {
                 const uint32_t slot = a.slots[base + e];
-                const uint32_t rect = __float_as_uint(__ldg(&a.records[slot].c.w));
+                const uint32_t rect = __ldg(a.rects + slot);
                 // camera of this slot: last camera whose slot_base <= slot
                 int lo = 0, hi = a.n_cams - 1;
                 while (lo < hi) {
