@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -118,21 +119,30 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> zero_block;
     DevBuf<unsigned long long> counts;  // [0] visible, [1] pairs
     DevBuf<uint32_t> tile_begin, tile_end;
-    DevBuf<DevCamera> cams;
-    DevBuf<uint64_t> cam_slot_base;
-    DevBuf<uint32_t> cam_tile_base;
-    DevBuf<int> cam_tiles_x;
-    DevBuf<DevSegment> segs;
-    DevBuf<SegEntry> entries;
+    // plan tables of the current frame: pointers into plan_dev
+    DevBuf<char> plan_dev;
+    DevCamera* cams = nullptr;
+    uint64_t* cam_slot_base = nullptr;
+    uint32_t* cam_tile_base = nullptr;
+    int* cam_tiles_x = nullptr;
+    DevSegment* segs = nullptr;
+    SegEntry* entries = nullptr;
+    std::vector<char> blob_host;
+    PinnedBuf staging[2];
+    cudaEvent_t staging_ev[2] = {};
+    int staging_index = 0;
     DevBuf<float> out;
     DevBuf<gsim_projected_splat> full;
     DevBuf<uint8_t> full_vis;
     DevBuf<gsim_projected_splat> splats_in;
-    PinnedBuf staging;
     PinnedBuf readback;
+    cudaEvent_t dup_ev = nullptr;
 
     uint32_t epoch = 0;
     uint64_t pair_capacity = 0;
+    // GSIM_GPU_INITIAL_PAIR_CAPACITY (tests): start from this capacity instead of 4 x slots,
+    // to exercise the overflow -> regrow -> re-run path.
+    uint64_t fixed_initial_capacity = 0;
     uint64_t launches_total = 0;
 
     // last frame, for stats and the tile-list hook
@@ -328,36 +338,36 @@ size_t append_bytes(std::vector<char>& blob, const std::vector<T>& v) {
     return off;
 }
 
+// One H2D copy per frame: the plan tables are packed into a pinned blob (double-buffered, so
+// building frame k+1 never waits for frame k) and copied into one device blob; the kernels read
+// them through pointers into that blob. Stream order keeps frame k's kernels ahead of the copy.
 void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
-    ctx->cams.reserve(p.cams.size());
-    ctx->cam_slot_base.reserve(p.slot_base.size());
-    ctx->cam_tile_base.reserve(p.tile_base.size());
-    ctx->cam_tiles_x.reserve(std::max<size_t>(p.tiles_x.size(), 1));
-    ctx->segs.reserve(std::max<size_t>(p.segs.size(), 1));
-    ctx->entries.reserve(std::max<size_t>(p.entries.size(), 1));
-    std::vector<char> blob;
+    std::vector<char>& blob = ctx->blob_host;
+    blob.clear();
     const size_t o_cams = append_bytes(blob, p.cams);
     const size_t o_sb = append_bytes(blob, p.slot_base);
     const size_t o_tb = append_bytes(blob, p.tile_base);
     const size_t o_tx = append_bytes(blob, p.tiles_x);
     const size_t o_seg = append_bytes(blob, p.segs);
     const size_t o_ent = append_bytes(blob, p.entries);
-    // The previous frame's copies out of the staging buffer must have landed.
-    GSIM_CK(cudaStreamSynchronize(ctx->stream));
-    ctx->staging.reserve(blob.size());
-    std::memcpy(ctx->staging.ptr, blob.data(), blob.size());
+    const int k = ctx->staging_index;
+    ctx->staging_index ^= 1;
+    GSIM_CK(cudaEventSynchronize(ctx->staging_ev[k]));  // its copy (two frames ago) landed
+    ctx->staging[k].reserve(blob.size());
+    std::memcpy(ctx->staging[k].ptr, blob.data(), blob.size());
+    ctx->plan_dev.reserve(blob.size());
+    GSIM_CK(cudaMemcpyAsync(ctx->plan_dev.ptr, ctx->staging[k].ptr, blob.size(),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    GSIM_CK(cudaEventRecord(ctx->staging_ev[k], ctx->stream));
     ctx->stats.h2d_bytes = blob.size();
     ctx->stats.d2h_bytes = 0;
-    const char* h = static_cast<const char*>(ctx->staging.ptr);
-    auto cp = [&](void* dst, size_t off, size_t bytes) {
-        if (bytes) GSIM_CK(cudaMemcpyAsync(dst, h + off, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    };
-    cp(ctx->cams.ptr, o_cams, p.cams.size() * sizeof(DevCamera));
-    cp(ctx->cam_slot_base.ptr, o_sb, p.slot_base.size() * sizeof(uint64_t));
-    cp(ctx->cam_tile_base.ptr, o_tb, p.tile_base.size() * sizeof(uint32_t));
-    cp(ctx->cam_tiles_x.ptr, o_tx, p.tiles_x.size() * sizeof(int));
-    cp(ctx->segs.ptr, o_seg, p.segs.size() * sizeof(DevSegment));
-    cp(ctx->entries.ptr, o_ent, p.entries.size() * sizeof(SegEntry));
+    char* d = ctx->plan_dev.ptr;
+    ctx->cams = reinterpret_cast<DevCamera*>(d + o_cams);
+    ctx->cam_slot_base = reinterpret_cast<uint64_t*>(d + o_sb);
+    ctx->cam_tile_base = reinterpret_cast<uint32_t*>(d + o_tb);
+    ctx->cam_tiles_x = reinterpret_cast<int*>(d + o_tx);
+    ctx->segs = reinterpret_cast<DevSegment*>(d + o_seg);
+    ctx->entries = reinterpret_cast<SegEntry*>(d + o_ent);
 }
 
 void record_stage(gsim_gpu_context* ctx, int stage) {
@@ -376,7 +386,8 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
         ctx->dk[k].reserve(S);
         ctx->dv[k].reserve(S);
     }
-    if (ctx->pair_capacity < 4 * S + (1u << 20)) ctx->pair_capacity = 4 * S + (1u << 20);
+    if (ctx->fixed_initial_capacity == 0 && ctx->pair_capacity < 4 * S + (1u << 20))
+        ctx->pair_capacity = 4 * S + (1u << 20);
     for (int k = 0; k < 2; ++k) {
         ctx->pk[k].reserve(ctx->pair_capacity);
         ctx->pv[k].reserve(ctx->pair_capacity);
@@ -403,6 +414,9 @@ float smallest_float_geq(double x) {
     if (double(f) < x) f = std::nextafter(f, INFINITY);
     return f;
 }
+
+void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
+                         float* out, int cur);
 
 // K3 + K4 over records/keys already produced for `p` (by K2 or the splat converter).
 void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
@@ -448,16 +462,21 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     da.slots = depth_sorted_slots;
     da.n_dev = ctx->counts.ptr + 0;
     da.rects = ctx->rects.ptr;
-    da.cam_slot_base = ctx->cam_slot_base.ptr;
-    da.cam_tile_base = ctx->cam_tile_base.ptr;
-    da.cam_tiles_x = ctx->cam_tiles_x.ptr;
+    da.cam_slot_base = ctx->cam_slot_base;
+    da.cam_tile_base = ctx->cam_tile_base;
+    da.cam_tiles_x = ctx->cam_tiles_x;
     da.n_cams = int(p.cams.size());
     da.tile_passes = tile_passes;
     da.hist = tile_hist(ctx);
     da.status = ctx->status.ptr;
     da.pairs_out = ctx->counts.ptr + 1;
     const int dup_grid = grid_for(S, kDupTile, ctx->num_sms * ctx->occ_dup);
+    int cur = 0;
     uint64_t P = 0;
+    // The tail (dup -> tile sort -> ranges -> raster) is enqueued without waiting for the pair
+    // count: every kernel reads P from device memory and clamps it to the pair capacity. The
+    // host checks P once dup has finished (while the GPU keeps sorting); on overflow it grows
+    // the buffers and enqueues the tail again, overwriting the clamped frame.
     for (int attempt = 0; attempt < 3; ++attempt) {
         da.keys_out = ctx->pk[0].ptr;
         da.vals_out = ctx->pv[0].ptr;
@@ -467,16 +486,56 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         launch_scan_dup(da, dup_grid, s);
         check_launch();
         ++launches;
-        // The pair count decides the tile-sort grid and the buffer capacity.
         ctx->readback.reserve(64);
         GSIM_CK(cudaMemcpyAsync(ctx->readback.ptr, ctx->counts.ptr, 2 * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, s));
-        GSIM_CK(cudaStreamSynchronize(s));
+        GSIM_CK(cudaEventRecord(ctx->dup_ev, s));
+        record_stage(ctx, kEvDup);
+
+        // camera|tile digits: stable onesweep passes over the pairs (persistent grids).
+        cur = 0;
+        for (int pass = 0; pass < tile_passes; ++pass) {
+            OnesweepArgs ta{};
+            ta.keys_in = ctx->pk[cur].ptr;
+            ta.vals_in = ctx->pv[cur].ptr;
+            ta.keys_out = ctx->pk[cur ^ 1].ptr;
+            ta.vals_out = ctx->pv[cur ^ 1].ptr;
+            ta.n_dev = ctx->counts.ptr + 1;
+            ta.capacity = ctx->pair_capacity;
+            ta.hist = tile_hist(ctx) + 256 * pass;
+            ta.status = ctx->status.ptr;
+            ta.ticket = ticket(ctx, 4 + pass);
+            ta.epoch = ctx->next_epoch();
+            ta.shift = 8 * pass;
+            launch_onesweep(ta, false, true, sort_grid_cap, s);
+            check_launch();
+            ++launches;
+            cur ^= 1;
+        }
+        record_stage(ctx, kEvTile);
+
+        GSIM_CK(cudaMemsetAsync(ctx->tile_begin.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
+        GSIM_CK(cudaMemsetAsync(ctx->tile_end.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
+        RangesArgs ra{};
+        ra.keys = ctx->pk[cur].ptr;
+        ra.n_dev = ctx->counts.ptr + 1;
+        ra.capacity = ctx->pair_capacity;
+        ra.tile_begin = ctx->tile_begin.ptr;
+        ra.tile_end = ctx->tile_end.ptr;
+        launch_ranges(ra, ctx->num_sms * 8, s);
+        check_launch();
+        ++launches;
+        record_stage(ctx, kEvRanges);
+        launch_raster_stage(ctx, p, opt, out, cur);
+        ++launches;
+
+        GSIM_CK(cudaEventSynchronize(ctx->dup_ev));
         const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
         ctx->stats.visible = rb[0];
         P = rb[1];
         if (P <= ctx->pair_capacity) break;
-        // Grow and redo the duplication (the depth order is still valid).
+        // Grow, reset the tail's counters and run the tail again (the depth order is valid).
+        GSIM_CK(cudaStreamSynchronize(s));
         ctx->pair_capacity = P + P / 4 + (1u << 20);
         for (int k = 0; k < 2; ++k) {
             ctx->pk[k].reserve(ctx->pair_capacity);
@@ -489,67 +548,34 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
             da.status = ctx->status.ptr;
         }
         GSIM_CK(cudaMemsetAsync(tile_hist(ctx), 0, 1024 * sizeof(uint32_t), s));
-        GSIM_CK(cudaMemsetAsync(ticket(ctx, 8), 0, sizeof(uint32_t), s));
+        GSIM_CK(cudaMemsetAsync(ticket(ctx, 4), 0, 5 * sizeof(uint32_t), s));
+        GSIM_CK(cudaMemsetAsync(ctx->counts.ptr + 2, 0, sizeof(unsigned long long), s));
     }
     if (P > ctx->pair_capacity) throw CudaError{"pair buffer overflow after regrowth"};
     ctx->last_pairs = P;
-    record_stage(ctx, kEvDup);
+    ctx->final_vals = ctx->pv[cur].ptr;
+    ctx->stats.depth_passes = 4;
+    ctx->stats.tile_passes = uint32_t(tile_passes);
+    ctx->stats.pairs = P;
+}
 
-    // camera|tile digits: stable onesweep passes over the pairs.
-    const int tgrid = grid_for(P, kOnesweepTile, sort_grid_cap);
-    int cur = 0;
-    for (int pass = 0; pass < tile_passes; ++pass) {
-        OnesweepArgs ta{};
-        ta.keys_in = ctx->pk[cur].ptr;
-        ta.vals_in = ctx->pv[cur].ptr;
-        ta.keys_out = ctx->pk[cur ^ 1].ptr;
-        ta.vals_out = ctx->pv[cur ^ 1].ptr;
-        ta.n_dev = ctx->counts.ptr + 1;
-        ta.hist = tile_hist(ctx) + 256 * pass;
-        ta.status = ctx->status.ptr;
-        ta.ticket = ticket(ctx, 4 + pass);
-        ta.epoch = ctx->next_epoch();
-        ta.shift = 8 * pass;
-        launch_onesweep(ta, false, true, tgrid, s);
-        check_launch();
-        ++launches;
-        cur ^= 1;
-    }
-    record_stage(ctx, kEvTile);
-
-    GSIM_CK(cudaMemsetAsync(ctx->tile_begin.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
-    GSIM_CK(cudaMemsetAsync(ctx->tile_end.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
-    RangesArgs ra{};
-    ra.keys = ctx->pk[cur].ptr;
-    ra.n_dev = ctx->counts.ptr + 1;
-    ra.capacity = ctx->pair_capacity;
-    ra.tile_begin = ctx->tile_begin.ptr;
-    ra.tile_end = ctx->tile_end.ptr;
-    launch_ranges(ra, grid_for(P, 256 * 8, ctx->num_sms * 8), s);
-    check_launch();
-    ++launches;
-    record_stage(ctx, kEvRanges);
-
+void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
+                         float* out, int cur) {
     RasterArgs rr{};
     rr.records = ctx->records.ptr;
     rr.values = ctx->pv[cur].ptr;
     rr.tile_begin = ctx->tile_begin.ptr;
     rr.tile_end = ctx->tile_end.ptr;
-    rr.cams = ctx->cams.ptr;
-    rr.cam_tile_base = ctx->cam_tile_base.ptr;
+    rr.cams = ctx->cams;
+    rr.cam_tile_base = ctx->cam_tile_base;
     rr.n_cams = int(p.cams.size());
     rr.normalize_depth = opt.normalize_depth;
     rr.cutoff = smallest_float_geq(opt.transmittance_cutoff);
     rr.out = out;
     rr.consumed = ctx->counts.ptr + 2;
-    launch_raster(rr, p.tiles, s);
+    launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
-    ++launches;
     record_stage(ctx, kEvRaster);
-    ctx->final_vals = ctx->pv[cur].ptr;
-    ctx->stats.depth_passes = 4;
-    ctx->stats.tile_passes = uint32_t(tile_passes);
-    ctx->stats.pairs = P;
 }
 
 void begin_frame(gsim_gpu_context* ctx) {
@@ -583,10 +609,10 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     uint64_t launches = 0;
     PreprocessArgs pa{};
     pa.field = scene->f;
-    pa.segs = ctx->segs.ptr;
+    pa.segs = ctx->segs;
     pa.n_segs = int(plan.segs.size());
-    pa.entries = ctx->entries.ptr;
-    pa.cams = ctx->cams.ptr;
+    pa.entries = ctx->entries;
+    pa.cams = ctx->cams;
     pa.records = ctx->records.ptr;
     pa.rects = ctx->rects.ptr;
     pa.keys = ctx->keys.ptr;
@@ -648,6 +674,8 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         ctx->num_sms = prop.multiProcessorCount;
         GSIM_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) GSIM_CK(cudaEventCreate(&e));
+        for (auto& e : ctx->staging_ev) GSIM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        GSIM_CK(cudaEventCreateWithFlags(&ctx->dup_ev, cudaEventDisableTiming));
         ctx->occ_pre = 2;
         ctx->occ_sort = 3;
         ctx->occ_dup = 4;
@@ -655,6 +683,10 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         ctx->counts.reserve(4);
         ctx->readback.reserve(64);
         ctx->epoch = 0;
+        if (const char* e = std::getenv("GSIM_GPU_INITIAL_PAIR_CAPACITY")) {
+            ctx->fixed_initial_capacity = std::strtoull(e, nullptr, 10);
+            ctx->pair_capacity = ctx->fixed_initial_capacity;
+        }
     } catch (const ValidationError& e) {
         g_create_error = e.msg;
         delete ctx;
@@ -686,18 +718,17 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->counts.release();
     ctx->tile_begin.release();
     ctx->tile_end.release();
-    ctx->cams.release();
-    ctx->cam_slot_base.release();
-    ctx->cam_tile_base.release();
-    ctx->cam_tiles_x.release();
-    ctx->segs.release();
-    ctx->entries.release();
+    ctx->plan_dev.release();
     ctx->out.release();
     ctx->full.release();
     ctx->full_vis.release();
     ctx->splats_in.release();
-    ctx->staging.release();
+    ctx->staging[0].release();
+    ctx->staging[1].release();
     ctx->readback.release();
+    for (auto& e : ctx->staging_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->dup_ev) cudaEventDestroy(ctx->dup_ev);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -880,10 +911,10 @@ int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const g
         begin_frame(ctx);
         PreprocessArgs pa{};
         pa.field = scene->f;
-        pa.segs = ctx->segs.ptr;
+        pa.segs = ctx->segs;
         pa.n_segs = int(plan.segs.size());
-        pa.entries = ctx->entries.ptr;
-        pa.cams = ctx->cams.ptr;
+        pa.entries = ctx->entries;
+        pa.cams = ctx->cams;
         pa.records = ctx->records.ptr;
     pa.rects = ctx->rects.ptr;
         pa.keys = ctx->keys.ptr;
@@ -937,7 +968,7 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
         SplatArgs sa{};
         sa.splats = ctx->splats_in.ptr;
         sa.n = n;
-        sa.cam = ctx->cams.ptr;
+        sa.cam = ctx->cams;
         sa.records = ctx->records.ptr;
         sa.rects = ctx->rects.ptr;
         sa.keys = ctx->keys.ptr;

@@ -47,6 +47,7 @@ struct OnesweepArgs {
     uint32_t* vals_out;
     const unsigned long long* n_dev; // element count on device (ignored when n_host used)
     uint64_t n_host;
+    uint64_t capacity;               // n_dev is clamped to this (0 = no clamp)
     const uint32_t* hist;            // [256] digit histogram of this pass
     uint64_t* status;                // decoupled-lookback words, [chunks][256]
     uint32_t* ticket;                // zeroed per pass

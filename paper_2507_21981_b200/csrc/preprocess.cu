@@ -29,6 +29,18 @@ __device__ __forceinline__ int x86_trunc_int(double x) {
 
 __device__ __forceinline__ dq seg_q(const DevSegment& s) { return dq{s.q[0], s.q[1], s.q[2], s.q[3]}; }
 
+// Correctly rounded x / b from a correctly rounded reciprocal rb = RN(1/b) (Markstein): the
+// first quotient is within 1 ulp, one fma residual step rounds it exactly like IEEE division
+// (no overflow/underflow in range; out-of-range numerators take the real division). Replaces
+// eight double divisions per (camera, primitive) by two reciprocals and multiply-adds.
+__device__ __forceinline__ double div_rn(double x, double b, double rb) {
+    const double ax = fabs(x);
+    if (!(ax < 0x1p900) || (ax < 0x1p-900 && x != 0.0)) return x / b;
+    const double q0 = x * rb;
+    const double r = fma(-q0, b, x);
+    return fma(r, rb, q0);
+}
+
 constexpr float kSh0 = 0.28209479177387814f;  // sh.hpp:12-20
 constexpr float kSh1 = 0.4886025119029199f;
 constexpr float kSh2_0 = 1.0925484305920792f, kSh2_1 = -1.0925484305920792f,
@@ -166,8 +178,9 @@ __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args)
             bool alive = (z > cam.near_p) && (z < cam.far_p);
             double u = 0, v = 0, cov_xx = 0, cov_xy = 0, cov_yy = 0, det = 1, radius = 0;
             if (alive) {
-                u = cam.fx * mean_cam.x / z + cam.cx;
-                v = cam.fy * mean_cam.y / z + cam.cy;
+                const double rz = __drcp_rn(z);
+                u = div_rn(cam.fx * mean_cam.x, z, rz) + cam.cx;
+                v = div_rn(cam.fy * mean_cam.y, z, rz) + cam.cy;
                 dm3 rwc;
 #pragma unroll
                 for (int k = 0; k < 9; ++k) rwc.m[k] = cam.r[k];
@@ -178,12 +191,14 @@ __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args)
                              c02 = mm_entry(t1, rwct, 0, 2), c11 = mm_entry(t1, rwct, 1, 1),
                              c12 = mm_entry(t1, rwct, 1, 2), c20 = mm_entry(t1, rwct, 2, 0),
                              c21 = mm_entry(t1, rwct, 2, 1), c22 = mm_entry(t1, rwct, 2, 2);
-                const double tx = clampd(mean_cam.x / z, -cam.limx, cam.limx) * z;
-                const double ty = clampd(mean_cam.y / z, -cam.limy, cam.limy) * z;
-                const double j00 = cam.fx / z;
-                const double j02 = -cam.fx * tx / (z * z);
-                const double j11 = cam.fy / z;
-                const double j12 = -cam.fy * ty / (z * z);
+                const double tx = clampd(div_rn(mean_cam.x, z, rz), -cam.limx, cam.limx) * z;
+                const double ty = clampd(div_rn(mean_cam.y, z, rz), -cam.limy, cam.limy) * z;
+                const double zz = z * z;
+                const double rzz = __drcp_rn(zz);
+                const double j00 = div_rn(cam.fx, z, rz);
+                const double j02 = div_rn(-cam.fx * tx, zz, rzz);
+                const double j11 = div_rn(cam.fy, z, rz);
+                const double j12 = div_rn(-cam.fy * ty, zz, rzz);
                 const double a = j00 * (j00 * c00 + j02 * c20) + j02 * (j00 * c02 + j02 * c22);
                 const double b = j00 * (j11 * c01 + j12 * c02) + j02 * (j11 * c21 + j12 * c22);
                 const double c = j11 * (j11 * c11 + j12 * c21) + j12 * (j11 * c12 + j12 * c22);

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     __shared__ uint32_t s_total;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t n = kFirst ? a.n_host : uint64_t(*a.n_dev);
+    uint64_t n = kFirst ? a.n_host : uint64_t(*a.n_dev);
+    if (a.capacity && n > a.capacity) n = a.capacity;
     const uint64_t chunks = (n + kOnesweepTile - 1) / kOnesweepTile;
 
     // Global start of each digit: exclusive scan of the pass histogram.
@@ -169,13 +170,25 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 
 // ---- scan + duplicate ----------------------------------------------------------------------
 constexpr int kDupItems = kDupTile / kThreads;  // 8 consecutive records per thread
+constexpr int kMaxSmemCams = 2048;
 
+__device__ __forceinline__ int camera_of_slot(uint32_t slot, const uint32_t* cam_slot, int n_cams) {
+    int lo = 0, hi = n_cams - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cam_slot[mid] <= slot) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Each thread owns 8 consecutive depth-sorted records; the block scans their tile counts,
+// gets its global offset by decoupled lookback, and every thread then writes its own records'
+// pairs (row-major per record, raster.cpp:259-263) — tile counts are small and the sum over
+// 8 records evens them out, so no cross-thread load balancing is needed.
 __global__ void __launch_bounds__(kThreads) scan_dup_kernel(DupArgs a) {
-    __shared__ uint32_t s_off[kDupTile];
-    __shared__ uint32_t s_rect[kDupTile];
-    __shared__ uint32_t s_slot[kDupTile];
-    __shared__ uint32_t s_tbase[kDupTile];
-    __shared__ uint32_t s_tx[kDupTile];
+    __shared__ uint32_t s_cam_slot[kMaxSmemCams + 1];
+    __shared__ uint32_t s_cam_tile[kMaxSmemCams + 1];
+    __shared__ uint32_t s_cam_tx[kMaxSmemCams];
     __shared__ uint32_t s_hist[kMaxTilePasses][kRadix];
     __shared__ uint32_t s_tmp[kWarps];
     __shared__ uint32_t s_ticket;
@@ -184,40 +197,44 @@ __global__ void __launch_bounds__(kThreads) scan_dup_kernel(DupArgs a) {
     const int tid = threadIdx.x;
     const uint64_t n = uint64_t(*a.n_dev);
     const uint64_t chunks = (n + kDupTile - 1) / kDupTile;
+    const bool smem_cams = a.n_cams <= kMaxSmemCams;
     for (int k = tid; k < kMaxTilePasses * kRadix; k += kThreads) (&s_hist[0][0])[k] = 0;
+    if (smem_cams)
+        for (int k = tid; k < a.n_cams; k += kThreads) {
+            s_cam_slot[k] = uint32_t(a.cam_slot_base[k]);
+            s_cam_tile[k] = a.cam_tile_base[k];
+            s_cam_tx[k] = uint32_t(a.cam_tiles_x[k]);
+        }
 
     while (true) {
         if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
         __syncthreads();
         const uint32_t t = s_ticket;
         if (t >= chunks) break;
-        const uint64_t base = uint64_t(t) * kDupTile;
-        const uint32_t n_here = uint32_t((n - base) < uint64_t(kDupTile) ? (n - base) : kDupTile);
+        const uint64_t base = uint64_t(t) * kDupTile + uint64_t(tid) * kDupItems;
 
-        uint32_t cnt[kDupItems];
+        uint32_t slot[kDupItems], rect[kDupItems];
+        if (base + kDupItems <= n) {
+            const uint4 s0 = __ldcs(reinterpret_cast<const uint4*>(a.slots + base));
+            const uint4 s1 = __ldcs(reinterpret_cast<const uint4*>(a.slots + base) + 1);
+            slot[0] = s0.x; slot[1] = s0.y; slot[2] = s0.z; slot[3] = s0.w;
+            slot[4] = s1.x; slot[5] = s1.y; slot[6] = s1.z; slot[7] = s1.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kDupItems; ++j)
+                slot[j] = (base + j < n) ? a.slots[base + j] : 0xFFFFFFFFu;
+        }
         uint32_t thread_sum = 0;
 #pragma unroll
         for (int j = 0; j < kDupItems; ++j) {
-            const uint32_t e = tid * kDupItems + j;
-            cnt[j] = 0;
-            if (e < n_here) {
-                const uint32_t slot = a.slots[base + e];
-                const uint32_t rect = __ldg(a.rects + slot);
-                // camera of this slot: last camera whose slot_base <= slot
-                int lo = 0, hi = a.n_cams - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (__ldg(a.cam_slot_base + mid) <= uint64_t(slot)) lo = mid; else hi = mid - 1;
-                }
-                const uint32_t tx0 = rect & 255u, ty0 = (rect >> 8) & 255u;
-                const uint32_t tx1 = (rect >> 16) & 255u, ty1 = rect >> 24;
-                cnt[j] = (tx1 - tx0 + 1u) * (ty1 - ty0 + 1u);
-                s_rect[e] = rect;
-                s_slot[e] = slot;
-                s_tbase[e] = __ldg(a.cam_tile_base + lo);
-                s_tx[e] = uint32_t(__ldg(a.cam_tiles_x + lo));
-            }
-            thread_sum += cnt[j];
+            rect[j] = 0xFFFFFFFFu;
+            if (slot[j] != 0xFFFFFFFFu) rect[j] = __ldg(a.rects + slot[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kDupItems; ++j) {
+            if (slot[j] == 0xFFFFFFFFu) continue;
+            const uint32_t r = rect[j];
+            thread_sum += (((r >> 16) & 255u) - (r & 255u) + 1u) * ((r >> 24) - ((r >> 8) & 255u) + 1u);
         }
         uint32_t block_total;
         const uint32_t thread_excl = block_exclusive_scan(thread_sum, s_tmp, &block_total);
@@ -241,31 +258,32 @@ __global__ void __launch_bounds__(kThreads) scan_dup_kernel(DupArgs a) {
             s_prefix = prefix;
             if (t == chunks - 1) *a.pairs_out = prefix + block_total;
         }
-        uint32_t run = thread_excl;
+        __syncthreads();
+        uint64_t out = s_prefix + thread_excl;
 #pragma unroll
         for (int j = 0; j < kDupItems; ++j) {
-            const uint32_t e = tid * kDupItems + j;
-            if (e < kDupTile) s_off[e] = (e < n_here) ? run : block_total;
-            run += cnt[j];
-        }
-        __syncthreads();
-        const uint64_t prefix = s_prefix;
-        // Load-balanced emission: output j of this chunk belongs to the last record e with
-        // s_off[e] <= j. Pairs of one record come out row-major (raster.cpp:259-263).
-        for (uint32_t j = tid; j < block_total; j += kThreads) {
-            const int e = upper_index(s_off, int(n_here), j);
-            const uint32_t k = j - s_off[e];
-            const uint32_t rect = s_rect[e];
-            const uint32_t tx0 = rect & 255u, ty0 = (rect >> 8) & 255u, tx1 = (rect >> 16) & 255u;
-            const uint32_t w = tx1 - tx0 + 1u;
-            const uint32_t ty = ty0 + k / w, tx = tx0 + k % w;
-            const uint32_t key = s_tbase[e] + ty * s_tx[e] + tx;
-            const uint64_t out = prefix + j;
-            if (out < a.capacity) {
-                a.keys_out[out] = key;
-                a.vals_out[out] = s_slot[e];
+            if (slot[j] == 0xFFFFFFFFu) continue;
+            int cam = 0;
+            if (a.n_cams > 1)
+                cam = smem_cams ? camera_of_slot(slot[j], s_cam_slot, a.n_cams)
+                                : upper_index(a.cam_slot_base, a.n_cams, uint64_t(slot[j]));
+            const uint32_t tbase = smem_cams ? s_cam_tile[cam] : a.cam_tile_base[cam];
+            const uint32_t tw = smem_cams ? s_cam_tx[cam] : uint32_t(a.cam_tiles_x[cam]);
+            const uint32_t r = rect[j];
+            const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u, ty1 = r >> 24;
+            for (uint32_t ty = ty0; ty <= ty1; ++ty) {
+                const uint32_t row = tbase + ty * tw;
+                for (uint32_t tx = tx0; tx <= tx1; ++tx) {
+                    const uint32_t key = row + tx;
+                    if (out < a.capacity) {
+                        a.keys_out[out] = key;
+                        a.vals_out[out] = slot[j];
+                    }
+                    ++out;
+                    for (int p = 0; p < a.tile_passes; ++p)
+                        atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+                }
             }
-            for (int p = 0; p < a.tile_passes; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
         }
         __syncthreads();
     }

@@ -201,6 +201,23 @@ def test_rigid_equivariance(ctx, oracle):  # test_raster.cpp:231-253
     assert rgb <= 1e-4 and depth <= 1e-3
 
 
+def test_pair_capacity_overflow_regrows(ctx, oracle, monkeypatch):
+    """Start a context with a tiny pair buffer: the tail overflows, regrows and re-runs, and the
+    result is bit-identical to a context that never overflowed."""
+    from paper_2507_21981_b200 import Context
+    field = oracle.random_field(99, 4000, 3.0, 0.01, 0.3, 2)
+    field.means[:, 2] += 3.0
+    cams = [ref_camera(160, 128, 110.0), ref_camera(96, 64, 70.0)]
+    want = ctx.render(ctx.upload(field), [], cams)
+    monkeypatch.setenv("GSIM_GPU_INITIAL_PAIR_CAPACITY", "1000")
+    small = Context(0)
+    got = small.render(small.upload(field), [], cams)
+    assert small.stats()["pairs"] > 1000
+    for g, w in zip(got, want):
+        assert np.array_equal(g.rgb, w.rgb) and np.array_equal(g.depth, w.depth)
+        assert np.array_equal(g.accum_alpha, w.accum_alpha)
+
+
 # ---- K1 --------------------------------------------------------------------------------------
 
 def test_transform_primitives_bit_exact(ctx, oracle):  # gaussian.cpp:65-79, test_core_types.cpp
