@@ -102,19 +102,22 @@ class ClockSampler:
 
 # ---- algorithmic byte model ----------------------------------------
 
-def stage_bytes(stats: dict, n_prims: int, sh_degree: int, pixels: int) -> dict:
+def stage_bytes(stats: dict, n_prims: int, sh_degree: int, pixels: int, n_cams: int) -> dict:
     """Minimum HBM bytes each stage of OUR pipeline must move for one step."""
     S, V, P, K = stats["slots"], stats["visible"], stats["pairs"], stats["consumed"]
     sh_bytes = 12 * (sh_degree + 1) ** 2
+    M = stats["tiles"] // max(1, n_cams) * stats["chunks"]  # count-matrix entries
     return {
-        # scene read once per batch (f64 geometry 88 B + fp32 SH) + 48 B record + 4 B key per slot
-        "preprocess": (88 + sh_bytes) * n_prims + 48 * V + 4 * S,
-        # pass 1 reads S keys, writes V (key, slot); passes 2-3 read+write 8 B; pass 4 writes 4 B
-        "depth_sort": 4 * S + 8 * V + 2 * 16 * V + 8 * V + 4 * V,
-        # read V slots + one 32 B sector of each record, write P (key, slot)
-        "duplicate": 4 * V + 32 * V + 8 * P,
-        "tile_sort": stats["tile_passes"] * 16 * P,
-        "ranges": 4 * P + 8 * stats["tiles"],
+        # scene read once per batch (f64 geometry 88 B + fp32 SH) + 48 B record, 4 B key and
+        # 4 B rect per visible slot, 4 B key per culled slot
+        "preprocess": (88 + sh_bytes) * n_prims + 52 * V + 4 * S,
+        # histogram reads S keys; pass 1 reads S keys, writes V (key, slot); passes 2-3 read
+        # and write 8 B; pass 4 reads 8 B, writes the 4 B slot
+        "depth_sort": 4 * S + 4 * S + 8 * V + 2 * 16 * V + 12 * V,
+        # count: V slots + V rects; column scan reads and writes the count matrix
+        "binning": 8 * V + 12 * M,
+        # scatter: V slots + V rects again, column prefixes, P record slots written
+        "scatter": 8 * V + 4 * M + 4 * P,
         # K list entries + 48 B records (2 sectors: 64 B) + 20 B/px outputs
         "raster": 4 * K + 64 * K + 20 * pixels,
     }
@@ -149,7 +152,7 @@ def run_ours(args, rank, world, local):
 
     # ---- timed region: device-resident inputs and outputs -------------------------------
     ctx.set_profiling(True)
-    stage_ms = {k: 0.0 for k in ("preprocess", "depth_sort", "duplicate", "tile_sort", "ranges", "raster")}
+    stage_ms = {k: 0.0 for k in ("preprocess", "depth_sort", "binning", "scatter", "raster")}
     launches = 0
     stats = None
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -219,7 +222,7 @@ def run_ours(args, rank, world, local):
 
     pk, pk_kind = peaks()
     per_step_ms = {k: v / args.steps for k, v in stage_ms.items()}
-    bytes_ = stage_bytes(stats, w.field.size(), w.field.sh_degree, pixels)
+    bytes_ = stage_bytes(stats, w.field.size(), w.field.sh_degree, pixels, n_cams)
     dominant = max(per_step_ms, key=per_step_ms.get)
     achieved = bytes_[dominant] / (per_step_ms[dominant] / 1e3) / 1e9 if per_step_ms[dominant] > 0 else 0.0
     total_ms = sum(per_step_ms.values())
@@ -251,7 +254,7 @@ def run_ours(args, rank, world, local):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "stats_last_step": {k: stats[k] for k in ("slots", "visible", "pairs", "consumed", "tiles",
-                                                  "depth_passes", "tile_passes")},
+                                                  "depth_passes", "chunks")},
         "roofline": roofline,
         "clocks": clocks,
         "wall_s_timed": round(wall, 4),

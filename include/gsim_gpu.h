@@ -127,17 +127,16 @@ typedef struct gsim_render_stats {
     uint64_t consumed;     /* pair-list entries the rasterizer fetched before saturating (K) */
     uint64_t h2d_bytes;    /* host->device bytes copied by the last call */
     uint64_t d2h_bytes;    /* device->host bytes copied by the last call */
-    uint32_t depth_passes; /* radix passes over the depth digits (pre-duplication) */
-    uint32_t tile_passes;  /* radix passes over the camera|tile digits (post-duplication) */
+    uint32_t depth_passes; /* onesweep passes over the (camera | depth) record keys */
+    uint32_t chunks;       /* binning chunks (runs of depth-sorted records of one camera) */
     /* per-stage device milliseconds, filled when profiling is on (gsim_gpu_set_profiling) */
-    float ms_preprocess;
-    float ms_depth_sort;
-    float ms_duplicate;
-    float ms_tile_sort;
-    float ms_ranges;
-    float ms_raster;
+    float ms_preprocess;   /* K2 projection + SH */
+    float ms_depth_sort;   /* key histograms + chunk table + onesweep passes */
+    float ms_binning;      /* per-chunk tile counts + column/tile/camera scans */
+    float ms_scatter;      /* pair placement in final (camera, tile, depth) order */
+    float ms_raster;       /* K4 */
     float ms_total;
-    float reserved;
+    float reserved[2];
 } gsim_render_stats;
 
 typedef struct gsim_gpu_context gsim_gpu_context;

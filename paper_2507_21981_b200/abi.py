@@ -69,11 +69,11 @@ class gsim_render_stats(C.Structure):
     _fields_ = [("slots", C.c_uint64), ("visible", C.c_uint64), ("pairs", C.c_uint64),
                 ("tiles", C.c_uint64), ("launches", C.c_uint64), ("launches_total", C.c_uint64),
                 ("consumed", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("depth_passes", C.c_uint32), ("tile_passes", C.c_uint32),
+                ("depth_passes", C.c_uint32), ("chunks", C.c_uint32),
                 ("ms_preprocess", C.c_float), ("ms_depth_sort", C.c_float),
-                ("ms_duplicate", C.c_float), ("ms_tile_sort", C.c_float),
-                ("ms_ranges", C.c_float), ("ms_raster", C.c_float), ("ms_total", C.c_float),
-                ("reserved", C.c_float)]
+                ("ms_binning", C.c_float), ("ms_scatter", C.c_float),
+                ("ms_raster", C.c_float), ("ms_total", C.c_float),
+                ("reserved", C.c_float * 2)]
 
 
 # numpy view of gsim_projected_splat (ProjectedSplat, raster.hpp:20-29), 120 bytes

@@ -25,6 +25,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
 SOURCES = {
     "preprocess.cu": ["-fmad=false"],
     "sort.cu": [],
+    "bin.cu": [],
     "raster.cu": [],
     "host.cu": [],
 }

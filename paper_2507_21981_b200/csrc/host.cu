@@ -4,9 +4,15 @@
 // Reference behaviour mirrored here:
 //   validate_camera          raster.cpp:16-23   (status 2, same rules)
 //   PoseTable                raster.cpp:47-62   (node painting, later nodes win, range check)
-//   render / rasterize       raster.cpp:234-334 (pipeline: K2 -> K3 -> K4)
+//   render / rasterize       raster.cpp:234-334 (pipeline K2 -> K3 -> K4)
 //   transform_primitives     gaussian.cpp:65-79 (K1, range check)
 //   validate_field sh_degree gaussian.cpp:15-17
+//
+// Frame pipeline (all on the context stream, no host round trip before the raster):
+//   K2 preprocess -> key_hist -> chunk_table -> 4 x onesweep (camera | depth)
+//   -> bin_count -> bin_colscan -> bin_tilescan -> bin_campre -> bin_scatter -> K4 raster
+// The host waits only for the small (V, P) readback behind bin_campre, while the GPU runs the
+// scatter and the raster, to catch a pair-buffer overflow (then it grows and re-runs the tail).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -51,7 +57,7 @@ struct DevBuf {
         if (ptr) GSIM_CK(cudaFree(ptr));
         ptr = nullptr;
         cap = 0;
-        size_t want = std::max<size_t>(n, 1);
+        const size_t want = std::max<size_t>(n, 1);
         GSIM_CK(cudaMalloc(&ptr, want * sizeof(T)));
         cap = want;
     }
@@ -90,11 +96,18 @@ struct Plan {
     std::vector<SegEntry> entries;
     uint64_t slots = 0;
     uint32_t tiles = 0;
+    uint32_t max_tc = 0;
     uint64_t out_floats = 0;
+    uint32_t key_base = 0;
+    int depth_bits = 32;
 };
 
-// profiling events: start, after K2, after depth sort, after dup, after tile sort, after ranges, after raster
-enum Stage { kEvStart = 0, kEvPre, kEvDepth, kEvDup, kEvTile, kEvRanges, kEvRaster, kNumStages };
+// profiling events
+enum Ev { kEvStart = 0, kEvPre, kEvDepth, kEvBin, kEvScatter, kEvRaster, kNumEv };
+
+constexpr int kZeroHist = 0;       // [4][256] depth digit histograms
+constexpr int kZeroTickets = 1024; // 16 onesweep tickets
+constexpr int kZeroCams = 1040;    // per-camera visible counts
 
 }  // namespace
 
@@ -105,20 +118,27 @@ struct gsim_gpu_context {
     std::mutex mu;
     std::string err;
     bool profiling = false;
-    cudaEvent_t ev[kNumStages] = {};
+    cudaEvent_t ev[kNumEv] = {};
 
-    int occ_pre = 1, occ_sort = 1, occ_dup = 1;
-
+    // per-slot planes
     DevBuf<Record> records;
     DevBuf<uint32_t> keys;
     DevBuf<uint32_t> rects;
-    DevBuf<uint32_t> dk[2], dv[2];   // depth sort ping-pong
-    DevBuf<uint32_t> pk[2], pv[2];   // tile sort ping-pong
-    DevBuf<uint64_t> status;
-    // zero block: [0,1024) depth hist, [1024, 2048) tile hist, [2048, 2048+32) tickets
+    DevBuf<uint32_t> dk[2], dv[2];   // depth-sort ping-pong
+    DevBuf<uint64_t> status;         // onesweep lookback words
+    // per-pair plane (final per-tile order)
+    DevBuf<uint32_t> vals;
+    uint64_t pair_capacity = 0;
+    // GSIM_GPU_INITIAL_PAIR_CAPACITY (tests): start from this capacity instead of 4 x slots,
+    // to exercise the overflow -> regrow -> re-run path.
+    uint64_t fixed_initial_capacity = 0;
+    // zeroed per frame: histograms, tickets, per-camera visible counts
     DevBuf<uint32_t> zero_block;
-    DevBuf<unsigned long long> counts;  // [0] visible, [1] pairs
-    DevBuf<uint32_t> tile_begin, tile_end;
+    DevBuf<unsigned long long> counts;  // [0] V, [1] P, [2] consumed
+    // binning scratch
+    DevBuf<uint32_t> cam_vbase, cam_chunk_base, cam_pairs, chunk_cam, n_chunks;
+    DevBuf<uint64_t> cam_mbase, cam_pair_base;
+    DevBuf<uint32_t> count_matrix, tile_count, tile_rel;
     // plan tables of the current frame: pointers into plan_dev
     DevBuf<char> plan_dev;
     DevCamera* cams = nullptr;
@@ -131,25 +151,20 @@ struct gsim_gpu_context {
     PinnedBuf staging[2];
     cudaEvent_t staging_ev[2] = {};
     int staging_index = 0;
+    PinnedBuf readback;
+    cudaEvent_t bin_ev = nullptr;
+    // outputs / API scratch
     DevBuf<float> out;
     DevBuf<gsim_projected_splat> full;
     DevBuf<uint8_t> full_vis;
     DevBuf<gsim_projected_splat> splats_in;
-    PinnedBuf readback;
-    cudaEvent_t dup_ev = nullptr;
 
     uint32_t epoch = 0;
-    uint64_t pair_capacity = 0;
-    // GSIM_GPU_INITIAL_PAIR_CAPACITY (tests): start from this capacity instead of 4 x slots,
-    // to exercise the overflow -> regrow -> re-run path.
-    uint64_t fixed_initial_capacity = 0;
     uint64_t launches_total = 0;
 
     // last frame, for stats and the tile-list hook
     gsim_render_stats stats{};
     Plan last_plan;
-    const uint32_t* final_vals = nullptr;
-    uint64_t last_pairs = 0;
 
     uint32_t next_epoch() {
         epoch = (epoch + 1) & kEpochMask;
@@ -173,6 +188,13 @@ uint32_t ceil_log2_bits(uint64_t n) {  // bits needed to represent values in [0,
     uint32_t b = 0;
     while ((uint64_t(1) << b) < n) ++b;
     return b;
+}
+
+uint32_t float_bits(double x) {
+    const float f = float(x);
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
 }
 
 void validate_camera(const gsim_camera& c, uint64_t index) {  // raster.cpp:16-23
@@ -215,6 +237,25 @@ DevCamera make_dev_camera(const gsim_camera& c) {
     return d;
 }
 
+void finish_cameras(Plan& p, const gsim_camera* cameras, uint64_t n_cams) {
+    p.tile_base.assign(n_cams + 1, 0);
+    uint64_t out_off = 0;
+    for (uint64_t c = 0; c < n_cams; ++c) {
+        DevCamera d = make_dev_camera(cameras[c]);
+        d.slot_base = p.slot_base[c];
+        d.tile_base = p.tile_base[c];
+        d.out_offset = out_off;
+        out_off += uint64_t(5) * d.width * d.height;
+        const uint32_t tc = uint32_t(d.tiles_x * d.tiles_y);
+        p.tile_base[c + 1] = p.tile_base[c] + tc;
+        p.max_tc = std::max(p.max_tc, tc);
+        p.tiles_x.push_back(d.tiles_x);
+        p.cams.push_back(d);
+    }
+    p.tiles = p.tile_base[n_cams];
+    p.out_floats = out_off;
+}
+
 // Paint node ranges like PoseTable (raster.cpp:47-62) into maximal segments and assign each
 // (camera, primitive) a record slot; cameras' slot lists keep primitive order.
 Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
@@ -225,7 +266,6 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         if (nodes[k].end > n_prims)
             throw ValidationError{"node " + std::to_string(k) + " range exceeds field size"};
 
-    // elementary intervals
     std::vector<uint64_t> pts{0, n_prims};
     for (uint64_t k = 0; k < n_nodes; ++k)
         if (nodes[k].begin < nodes[k].end) {
@@ -244,7 +284,6 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
                                    [](const Iv& iv, uint64_t v) { return iv.b < v; });
         for (; it != ivs.end() && it->b < nodes[k].end; ++it) it->owner = int64_t(k);
     }
-    // merge equal owners
     std::vector<Iv> merged;
     for (const auto& iv : ivs) {
         if (!merged.empty() && merged.back().owner == iv.owner && merged.back().e == iv.b)
@@ -259,7 +298,6 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         const int env = nodes[iv.owner].env;
         return env < 0 || env == cameras[c].env;
     };
-    // slots per camera
     p.slot_base.assign(n_cams + 1, 0);
     for (uint64_t c = 0; c < n_cams; ++c) {
         uint64_t s = 0;
@@ -294,39 +332,40 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         s.entry_count = uint32_t(p.entries.size()) - s.entry_begin;
         p.segs.push_back(s);
     }
-    // cameras, tiles, output offsets
-    p.tile_base.assign(n_cams + 1, 0);
-    uint64_t out_off = 0;
-    for (uint64_t c = 0; c < n_cams; ++c) {
-        DevCamera d = make_dev_camera(cameras[c]);
-        d.slot_base = p.slot_base[c];
-        d.tile_base = p.tile_base[c];
-        d.out_offset = out_off;
-        out_off += uint64_t(5) * d.width * d.height;
-        p.tile_base[c + 1] = p.tile_base[c] + uint32_t(d.tiles_x * d.tiles_y);
-        p.tiles_x.push_back(d.tiles_x);
-        p.cams.push_back(d);
+    finish_cameras(p, cameras, n_cams);
+    // Record key = camera index above the float32 depth bits rebased to [near_min, far_max]:
+    // near < z < far implies RN(near) <= RN(z) <= RN(far), and positive floats order like
+    // their bit patterns, so the rebased key keeps the reference's depth_sort_key order.
+    if (n_cams) {
+        double near_min = cameras[0].near_plane, far_max = cameras[0].far_plane;
+        for (uint64_t c = 1; c < n_cams; ++c) {
+            near_min = std::min(near_min, cameras[c].near_plane);
+            far_max = std::max(far_max, cameras[c].far_plane);
+        }
+        p.key_base = float_bits(near_min);
+        const uint64_t span = uint64_t(float_bits(far_max)) - p.key_base;
+        p.depth_bits = int(ceil_log2_bits(span + 2));  // keeps kInvalidKey unreachable
+        const int cam_bits = int(ceil_log2_bits(n_cams));
+        if (p.depth_bits + cam_bits > 32)
+            throw ValidationError{"batch of " + std::to_string(n_cams) + " cameras with near/far span " +
+                                  "needs " + std::to_string(p.depth_bits + cam_bits) +
+                                  " key bits (> 32); split the batch"};
     }
-    p.tiles = p.tile_base[n_cams];
-    p.out_floats = out_off;
     return p;
 }
 
-// Camera plan for rasterize(splats): one camera, slot = splat index, no validation
-// (rasterize does not call validate_camera in the reference).
+// Camera plan for rasterize(splats): one camera, slot = splat index, full 32-bit depth keys,
+// no validation (rasterize does not call validate_camera in the reference).
 Plan build_splat_plan(uint64_t n, const gsim_camera& cam) {
     if (cam.width < 1 || cam.height < 1 || cam.width > kMaxTilesPerAxis * kTileSize ||
         cam.height > kMaxTilesPerAxis * kTileSize)
         throw ValidationError{"rasterize: resolution outside 1..4096"};
     Plan p;
-    DevCamera d = make_dev_camera(cam);
     p.slot_base = {0, n};
     p.slots = n;
-    p.tile_base = {0, uint32_t(d.tiles_x * d.tiles_y)};
-    p.tiles_x = {d.tiles_x};
-    p.tiles = p.tile_base[1];
-    p.out_floats = uint64_t(5) * d.width * d.height;
-    p.cams.push_back(d);
+    finish_cameras(p, &cam, 1);
+    p.key_base = 0;
+    p.depth_bits = 32;
     return p;
 }
 
@@ -370,15 +409,26 @@ void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
     ctx->entries = reinterpret_cast<SegEntry*>(d + o_ent);
 }
 
-void record_stage(gsim_gpu_context* ctx, int stage) {
-    if (ctx->profiling) GSIM_CK(cudaEventRecord(ctx->ev[stage], ctx->stream));
+void record_ev(gsim_gpu_context* ctx, int e) {
+    if (ctx->profiling) GSIM_CK(cudaEventRecord(ctx->ev[e], ctx->stream));
 }
 
 void check_launch() { GSIM_CK(cudaGetLastError()); }
 
+int bin_warps_for(uint32_t max_tc) {
+    const size_t per_warp = size_t(max_tc) * sizeof(uint32_t);
+    const size_t budget = 200 * 1024;
+    const int w = int(std::min<size_t>(8, budget / std::max<size_t>(per_warp, 1)));
+    if (w < 1)
+        throw ValidationError{"camera with " + std::to_string(max_tc) +
+                              " tiles exceeds the binning shared-memory budget (51200 tiles)"};
+    return w;
+}
+
 // Workspaces sized for a plan (grow-only).
 void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     const uint64_t S = std::max<uint64_t>(p.slots, 1);
+    const uint64_t C = std::max<uint64_t>(p.cams.size(), 1);
     ctx->records.reserve(S);
     ctx->keys.reserve(S);
     ctx->rects.reserve(S);
@@ -388,26 +438,26 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     }
     if (ctx->fixed_initial_capacity == 0 && ctx->pair_capacity < 4 * S + (1u << 20))
         ctx->pair_capacity = 4 * S + (1u << 20);
-    for (int k = 0; k < 2; ++k) {
-        ctx->pk[k].reserve(ctx->pair_capacity);
-        ctx->pv[k].reserve(ctx->pair_capacity);
-    }
-    const uint64_t chunks = std::max((S + kOnesweepTile - 1) / kOnesweepTile,
-                                     (ctx->pair_capacity + kOnesweepTile - 1) / kOnesweepTile);
-    const uint64_t words = std::max<uint64_t>(chunks * 256, (S + kDupTile - 1) / kDupTile);
+    ctx->vals.reserve(std::max<uint64_t>(ctx->pair_capacity, 1));
+    const uint64_t words = (S + kOnesweepTile - 1) / kOnesweepTile * 256;
     if (words > ctx->status.cap) {
         ctx->status.reserve(words);
         GSIM_CK(cudaMemsetAsync(ctx->status.ptr, 0, ctx->status.cap * sizeof(uint64_t), ctx->stream));
     }
-    ctx->zero_block.reserve(2048 + 64);
+    ctx->zero_block.reserve(kZeroCams + C);
     ctx->counts.reserve(4);
-    ctx->tile_begin.reserve(std::max<uint32_t>(p.tiles, 1));
-    ctx->tile_end.reserve(std::max<uint32_t>(p.tiles, 1));
+    const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + C;
+    ctx->cam_vbase.reserve(C + 1);
+    ctx->cam_chunk_base.reserve(C + 1);
+    ctx->cam_pairs.reserve(C);
+    ctx->cam_mbase.reserve(C + 1);
+    ctx->cam_pair_base.reserve(C + 1);
+    ctx->chunk_cam.reserve(kmax);
+    ctx->n_chunks.reserve(1);
+    ctx->count_matrix.reserve(uint64_t(std::max<uint32_t>(p.max_tc, 1)) * kmax);
+    ctx->tile_count.reserve(std::max<uint32_t>(p.tiles, 1));
+    ctx->tile_rel.reserve(std::max<uint32_t>(p.tiles, 1));
 }
-
-uint32_t* depth_hist(gsim_gpu_context* c) { return c->zero_block.ptr; }
-uint32_t* tile_hist(gsim_gpu_context* c) { return c->zero_block.ptr + 1024; }
-uint32_t* ticket(gsim_gpu_context* c, int i) { return c->zero_block.ptr + 2048 + i; }
 
 float smallest_float_geq(double x) {
     float f = float(x);
@@ -415,157 +465,45 @@ float smallest_float_geq(double x) {
     return f;
 }
 
-void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
-                         float* out, int cur);
-
-// K3 + K4 over records/keys already produced for `p` (by K2 or the splat converter).
-void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
-                         float* out, uint64_t& launches) {
-    cudaStream_t s = ctx->stream;
-    const uint64_t S = p.slots;
-    const int sort_grid_cap = ctx->num_sms * ctx->occ_sort;
-    auto grid_for = [&](uint64_t n, int tile, int cap) {
-        uint64_t g = (n + tile - 1) / tile;
-        if (g < 1) g = 1;
-        return int(std::min<uint64_t>(g, uint64_t(cap)));
-    };
-    // Depth digits: 4 onesweep passes over the visible records (pass 1 compacts).
-    OnesweepArgs oa{};
-    oa.n_dev = ctx->counts.ptr + 0;
-    oa.status = ctx->status.ptr;
-    const int dgrid = grid_for(S, kOnesweepTile, sort_grid_cap);
-    const uint32_t* kin = ctx->keys.ptr;
-    const uint32_t* vin = nullptr;
-    for (int pass = 0; pass < 4; ++pass) {
-        const int o = pass & 1;
-        oa.keys_in = kin;
-        oa.vals_in = vin;
-        oa.keys_out = ctx->dk[o].ptr;
-        oa.vals_out = ctx->dv[o].ptr;
-        oa.n_host = S;
-        oa.hist = depth_hist(ctx) + 256 * pass;
-        oa.ticket = ticket(ctx, pass);
-        oa.epoch = ctx->next_epoch();
-        oa.shift = 8 * pass;
-        launch_onesweep(oa, pass == 0, pass < 3, dgrid, s);
-        check_launch();
-        ++launches;
-        kin = ctx->dk[o].ptr;
-        vin = ctx->dv[o].ptr;
-    }
-    const uint32_t* depth_sorted_slots = ctx->dv[1].ptr;
-    record_stage(ctx, kEvDepth);
-
-    const uint32_t tile_bits = std::max<uint32_t>(1, ceil_log2_bits(p.tiles));
-    const int tile_passes = int((tile_bits + 7) / 8);
-    DupArgs da{};
-    da.slots = depth_sorted_slots;
-    da.n_dev = ctx->counts.ptr + 0;
-    da.rects = ctx->rects.ptr;
-    da.cam_slot_base = ctx->cam_slot_base;
-    da.cam_tile_base = ctx->cam_tile_base;
-    da.cam_tiles_x = ctx->cam_tiles_x;
-    da.n_cams = int(p.cams.size());
-    da.tile_passes = tile_passes;
-    da.hist = tile_hist(ctx);
-    da.status = ctx->status.ptr;
-    da.pairs_out = ctx->counts.ptr + 1;
-    const int dup_grid = grid_for(S, kDupTile, ctx->num_sms * ctx->occ_dup);
-    int cur = 0;
-    uint64_t P = 0;
-    // The tail (dup -> tile sort -> ranges -> raster) is enqueued without waiting for the pair
-    // count: every kernel reads P from device memory and clamps it to the pair capacity. The
-    // host checks P once dup has finished (while the GPU keeps sorting); on overflow it grows
-    // the buffers and enqueues the tail again, overwriting the clamped frame.
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        da.keys_out = ctx->pk[0].ptr;
-        da.vals_out = ctx->pv[0].ptr;
-        da.capacity = ctx->pair_capacity;
-        da.ticket = ticket(ctx, 8);
-        da.epoch = ctx->next_epoch();
-        launch_scan_dup(da, dup_grid, s);
-        check_launch();
-        ++launches;
-        ctx->readback.reserve(64);
-        GSIM_CK(cudaMemcpyAsync(ctx->readback.ptr, ctx->counts.ptr, 2 * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToHost, s));
-        GSIM_CK(cudaEventRecord(ctx->dup_ev, s));
-        record_stage(ctx, kEvDup);
-
-        // camera|tile digits: stable onesweep passes over the pairs (persistent grids).
-        cur = 0;
-        for (int pass = 0; pass < tile_passes; ++pass) {
-            OnesweepArgs ta{};
-            ta.keys_in = ctx->pk[cur].ptr;
-            ta.vals_in = ctx->pv[cur].ptr;
-            ta.keys_out = ctx->pk[cur ^ 1].ptr;
-            ta.vals_out = ctx->pv[cur ^ 1].ptr;
-            ta.n_dev = ctx->counts.ptr + 1;
-            ta.capacity = ctx->pair_capacity;
-            ta.hist = tile_hist(ctx) + 256 * pass;
-            ta.status = ctx->status.ptr;
-            ta.ticket = ticket(ctx, 4 + pass);
-            ta.epoch = ctx->next_epoch();
-            ta.shift = 8 * pass;
-            launch_onesweep(ta, false, true, sort_grid_cap, s);
-            check_launch();
-            ++launches;
-            cur ^= 1;
-        }
-        record_stage(ctx, kEvTile);
-
-        GSIM_CK(cudaMemsetAsync(ctx->tile_begin.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
-        GSIM_CK(cudaMemsetAsync(ctx->tile_end.ptr, 0, sizeof(uint32_t) * std::max<uint32_t>(p.tiles, 1), s));
-        RangesArgs ra{};
-        ra.keys = ctx->pk[cur].ptr;
-        ra.n_dev = ctx->counts.ptr + 1;
-        ra.capacity = ctx->pair_capacity;
-        ra.tile_begin = ctx->tile_begin.ptr;
-        ra.tile_end = ctx->tile_end.ptr;
-        launch_ranges(ra, ctx->num_sms * 8, s);
-        check_launch();
-        ++launches;
-        record_stage(ctx, kEvRanges);
-        launch_raster_stage(ctx, p, opt, out, cur);
-        ++launches;
-
-        GSIM_CK(cudaEventSynchronize(ctx->dup_ev));
-        const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
-        ctx->stats.visible = rb[0];
-        P = rb[1];
-        if (P <= ctx->pair_capacity) break;
-        // Grow, reset the tail's counters and run the tail again (the depth order is valid).
-        GSIM_CK(cudaStreamSynchronize(s));
-        ctx->pair_capacity = P + P / 4 + (1u << 20);
-        for (int k = 0; k < 2; ++k) {
-            ctx->pk[k].reserve(ctx->pair_capacity);
-            ctx->pv[k].reserve(ctx->pair_capacity);
-        }
-        const uint64_t words = (ctx->pair_capacity + kOnesweepTile - 1) / kOnesweepTile * 256;
-        if (words > ctx->status.cap) {
-            ctx->status.reserve(words);
-            GSIM_CK(cudaMemsetAsync(ctx->status.ptr, 0, ctx->status.cap * sizeof(uint64_t), s));
-            da.status = ctx->status.ptr;
-        }
-        GSIM_CK(cudaMemsetAsync(tile_hist(ctx), 0, 1024 * sizeof(uint32_t), s));
-        GSIM_CK(cudaMemsetAsync(ticket(ctx, 4), 0, 5 * sizeof(uint32_t), s));
-        GSIM_CK(cudaMemsetAsync(ctx->counts.ptr + 2, 0, sizeof(unsigned long long), s));
-    }
-    if (P > ctx->pair_capacity) throw CudaError{"pair buffer overflow after regrowth"};
-    ctx->last_pairs = P;
-    ctx->final_vals = ctx->pv[cur].ptr;
-    ctx->stats.depth_passes = 4;
-    ctx->stats.tile_passes = uint32_t(tile_passes);
-    ctx->stats.pairs = P;
+BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sorted_slots) {
+    BinArgs b{};
+    b.keys = ctx->keys.ptr;
+    b.n_slots = p.slots;
+    b.depth_bits = p.depth_bits;
+    b.n_cams = int(p.cams.size());
+    b.sorted_slots = sorted_slots;
+    b.rects = ctx->rects.ptr;
+    b.cam_tile_base = ctx->cam_tile_base;
+    b.cam_tiles_x = ctx->cam_tiles_x;
+    b.cam_visible = ctx->zero_block.ptr + kZeroCams;
+    b.cam_vbase = ctx->cam_vbase.ptr;
+    b.cam_chunk_base = ctx->cam_chunk_base.ptr;
+    b.cam_mbase = ctx->cam_mbase.ptr;
+    b.cam_pairs = ctx->cam_pairs.ptr;
+    b.cam_pair_base = ctx->cam_pair_base.ptr;
+    b.chunk_cam = ctx->chunk_cam.ptr;
+    b.n_chunks = ctx->n_chunks.ptr;
+    b.counts = ctx->count_matrix.ptr;
+    b.tile_count = ctx->tile_count.ptr;
+    b.tile_rel = ctx->tile_rel.ptr;
+    b.hist = ctx->zero_block.ptr + kZeroHist;
+    b.totals = ctx->counts.ptr;
+    b.vals_out = ctx->vals.ptr;
+    b.capacity = ctx->pair_capacity;
+    b.max_tc = int(p.max_tc);
+    b.chunk_records = kChunkRecords;
+    b.bin_warps = bin_warps_for(p.max_tc);
+    return b;
 }
 
 void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
-                         float* out, int cur) {
+                         float* out) {
     RasterArgs rr{};
     rr.records = ctx->records.ptr;
-    rr.values = ctx->pv[cur].ptr;
-    rr.tile_begin = ctx->tile_begin.ptr;
-    rr.tile_end = ctx->tile_end.ptr;
+    rr.values = ctx->vals.ptr;
+    rr.tile_rel = ctx->tile_rel.ptr;
+    rr.tile_count = ctx->tile_count.ptr;
+    rr.cam_pair_base = ctx->cam_pair_base.ptr;
     rr.cams = ctx->cams;
     rr.cam_tile_base = ctx->cam_tile_base;
     rr.n_cams = int(p.cams.size());
@@ -575,11 +513,96 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.consumed = ctx->counts.ptr + 2;
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
-    record_stage(ctx, kEvRaster);
 }
 
-void begin_frame(gsim_gpu_context* ctx) {
-    GSIM_CK(cudaMemsetAsync(ctx->zero_block.ptr, 0, (2048 + 64) * sizeof(uint32_t), ctx->stream));
+// K3 + K4 over records/keys/rects already produced for `p` (by K2 or the splat converter).
+void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
+                         float* out, uint64_t& launches) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t S = p.slots;
+    const int n_sms = ctx->num_sms;
+
+    // key histograms + per-camera counts, then the chunk table (needs only the counts)
+    BinArgs b = make_bin_args(ctx, p, ctx->dv[1].ptr);
+    launch_key_hist(b, n_sms * 4, s);
+    check_launch();
+    launch_chunk_table(b, s);
+    check_launch();
+    launches += 2;
+
+    // 4 onesweep passes over (camera | depth) keys; pass 1 compacts the culled slots away.
+    OnesweepArgs oa{};
+    oa.n_dev = ctx->counts.ptr + 0;
+    oa.status = ctx->status.ptr;
+    uint64_t dgrid = (S + kOnesweepTile - 1) / kOnesweepTile;
+    dgrid = std::max<uint64_t>(1, std::min<uint64_t>(dgrid, uint64_t(n_sms) * 3));
+    const uint32_t* kin = ctx->keys.ptr;
+    const uint32_t* vin = nullptr;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int o = pass & 1;
+        oa.keys_in = kin;
+        oa.vals_in = vin;
+        oa.keys_out = ctx->dk[o].ptr;
+        oa.vals_out = ctx->dv[o].ptr;
+        oa.n_host = S;
+        oa.hist = b.hist + 256 * pass;
+        oa.ticket = ctx->zero_block.ptr + kZeroTickets + pass;
+        oa.epoch = ctx->next_epoch();
+        oa.shift = 8 * pass;
+        launch_onesweep(oa, pass == 0, pass < 3, int(dgrid), s);
+        check_launch();
+        ++launches;
+        kin = ctx->dk[o].ptr;
+        vin = ctx->dv[o].ptr;
+    }
+    record_ev(ctx, kEvDepth);
+
+    // tile binning: counts, scans, camera bases
+    const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + p.cams.size();
+    const int chunk_grid = int(std::max<uint64_t>(1, std::min<uint64_t>(kmax, uint64_t(n_sms) * 2)));
+    launch_bin_count(b, chunk_grid, s);
+    check_launch();
+    const uint64_t col_warps = p.tiles;
+    launch_bin_colscan(b, int(std::max<uint64_t>(1, std::min<uint64_t>((col_warps + 7) / 8, uint64_t(n_sms) * 8))), s);
+    check_launch();
+    launch_bin_tilescan(b, int(std::min<uint64_t>(p.cams.size(), uint64_t(n_sms) * 2)), s);
+    check_launch();
+    launch_bin_campre(b, s);
+    check_launch();
+    launches += 4;
+    ctx->readback.reserve(64);
+    GSIM_CK(cudaMemcpyAsync(ctx->readback.ptr, ctx->counts.ptr, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    GSIM_CK(cudaEventRecord(ctx->bin_ev, s));
+    record_ev(ctx, kEvBin);
+
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        b.vals_out = ctx->vals.ptr;
+        b.capacity = ctx->pair_capacity;
+        launch_bin_scatter(b, chunk_grid, s);
+        check_launch();
+        record_ev(ctx, kEvScatter);
+        launch_raster_stage(ctx, p, opt, out);
+        record_ev(ctx, kEvRaster);
+        launches += 2;
+        GSIM_CK(cudaEventSynchronize(ctx->bin_ev));
+        const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
+        ctx->stats.visible = rb[0];
+        ctx->stats.pairs = rb[1];
+        if (rb[1] <= ctx->pair_capacity) break;
+        // Pair buffer too small: grow and place + raster again (counts and scans stay valid).
+        GSIM_CK(cudaStreamSynchronize(s));
+        ctx->pair_capacity = rb[1] + rb[1] / 4 + (1u << 20);
+        ctx->vals.reserve(ctx->pair_capacity);
+        GSIM_CK(cudaMemsetAsync(ctx->counts.ptr + 2, 0, sizeof(unsigned long long), s));
+    }
+    if (ctx->stats.pairs > ctx->pair_capacity) throw CudaError{"pair buffer overflow after regrowth"};
+    ctx->stats.depth_passes = 4;
+}
+
+void begin_frame(gsim_gpu_context* ctx, const Plan& p) {
+    GSIM_CK(cudaMemsetAsync(ctx->zero_block.ptr, 0, (kZeroCams + std::max<size_t>(p.cams.size(), 1)) * sizeof(uint32_t),
+                            ctx->stream));
     GSIM_CK(cudaMemsetAsync(ctx->counts.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
 }
 
@@ -587,8 +610,24 @@ void finish_stats(gsim_gpu_context* ctx, const Plan& p, uint64_t launches) {
     ctx->stats.slots = p.slots;
     ctx->stats.tiles = p.tiles;
     ctx->stats.launches = launches;
+    ctx->stats.chunks = 0;
     ctx->launches_total += launches;
     ctx->stats.launches_total = ctx->launches_total;
+}
+
+PreprocessArgs make_pre_args(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const Plan& p) {
+    PreprocessArgs pa{};
+    pa.field = scene->f;
+    pa.segs = ctx->segs;
+    pa.n_segs = int(p.segs.size());
+    pa.depth_bits = p.depth_bits;
+    pa.entries = ctx->entries;
+    pa.cams = ctx->cams;
+    pa.records = ctx->records.ptr;
+    pa.rects = ctx->rects.ptr;
+    pa.keys = ctx->keys.ptr;
+    pa.key_base = p.key_base;
+    return pa;
 }
 
 void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
@@ -604,24 +643,16 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
         ctx->out.reserve(std::max<uint64_t>(plan.out_floats, 1));
         out = ctx->out.ptr;
     }
-    record_stage(ctx, kEvStart);
-    begin_frame(ctx);
+    record_ev(ctx, kEvStart);
+    begin_frame(ctx, plan);
     uint64_t launches = 0;
-    PreprocessArgs pa{};
-    pa.field = scene->f;
-    pa.segs = ctx->segs;
-    pa.n_segs = int(plan.segs.size());
-    pa.entries = ctx->entries;
-    pa.cams = ctx->cams;
-    pa.records = ctx->records.ptr;
-    pa.rects = ctx->rects.ptr;
-    pa.keys = ctx->keys.ptr;
-    pa.hist = depth_hist(ctx);
-    pa.visible_count = ctx->counts.ptr + 0;
-    launch_preprocess(pa, false, ctx->num_sms * ctx->occ_pre, ctx->stream);
-    check_launch();
-    ++launches;
-    record_stage(ctx, kEvPre);
+    PreprocessArgs pa = make_pre_args(ctx, scene, plan);
+    if (plan.slots) {
+        launch_preprocess(pa, false, ctx->num_sms * 2, ctx->stream);
+        check_launch();
+        ++launches;
+    }
+    record_ev(ctx, kEvPre);
     run_sort_and_raster(ctx, plan, opt, out, launches);
     finish_stats(ctx, plan, launches);
 }
@@ -655,7 +686,7 @@ struct Guard {
 
 extern "C" {
 
-const char* gsim_gpu_version(void) { return "gsim_gpu 0.1 (sm_100a)"; }
+const char* gsim_gpu_version(void) { return "gsim_gpu 0.2 (sm_100a)"; }
 
 int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
     if (!out) return GSIM_ERR_VALIDATION;
@@ -675,14 +706,10 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         GSIM_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (auto& e : ctx->ev) GSIM_CK(cudaEventCreate(&e));
         for (auto& e : ctx->staging_ev) GSIM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        GSIM_CK(cudaEventCreateWithFlags(&ctx->dup_ev, cudaEventDisableTiming));
-        ctx->occ_pre = 2;
-        ctx->occ_sort = 3;
-        ctx->occ_dup = 4;
-        ctx->zero_block.reserve(2048 + 64);
+        GSIM_CK(cudaEventCreateWithFlags(&ctx->bin_ev, cudaEventDisableTiming));
+        ctx->zero_block.reserve(kZeroCams + 64);
         ctx->counts.reserve(4);
         ctx->readback.reserve(64);
-        ctx->epoch = 0;
         if (const char* e = std::getenv("GSIM_GPU_INITIAL_PAIR_CAPACITY")) {
             ctx->fixed_initial_capacity = std::strtoull(e, nullptr, 10);
             ctx->pair_capacity = ctx->fixed_initial_capacity;
@@ -710,27 +737,33 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     for (int k = 0; k < 2; ++k) {
         ctx->dk[k].release();
         ctx->dv[k].release();
-        ctx->pk[k].release();
-        ctx->pv[k].release();
+        ctx->staging[k].release();
     }
     ctx->status.release();
+    ctx->vals.release();
     ctx->zero_block.release();
     ctx->counts.release();
-    ctx->tile_begin.release();
-    ctx->tile_end.release();
+    ctx->cam_vbase.release();
+    ctx->cam_chunk_base.release();
+    ctx->cam_pairs.release();
+    ctx->chunk_cam.release();
+    ctx->n_chunks.release();
+    ctx->cam_mbase.release();
+    ctx->cam_pair_base.release();
+    ctx->count_matrix.release();
+    ctx->tile_count.release();
+    ctx->tile_rel.release();
     ctx->plan_dev.release();
     ctx->out.release();
     ctx->full.release();
     ctx->full_vis.release();
     ctx->splats_in.release();
-    ctx->staging[0].release();
-    ctx->staging[1].release();
     ctx->readback.release();
-    for (auto& e : ctx->staging_ev)
-        if (e) cudaEventDestroy(e);
-    if (ctx->dup_ev) cudaEventDestroy(ctx->dup_ev);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->staging_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->bin_ev) cudaEventDestroy(ctx->bin_ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GSIM_OK;
@@ -754,14 +787,15 @@ int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out) {
     return Guard(ctx).run([&] {
         if (!out) throw ValidationError{"stats: null output"};
         gsim_render_stats st = ctx->stats;
-        {
-            unsigned long long c[4] = {0, 0, 0, 0};
-            GSIM_CK(cudaMemcpyAsync(c, ctx->counts.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
-            GSIM_CK(cudaStreamSynchronize(ctx->stream));
-            st.consumed = c[2];
-        }
+        unsigned long long c[4] = {0, 0, 0, 0};
+        uint32_t chunks = 0;
+        GSIM_CK(cudaMemcpyAsync(c, ctx->counts.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+        if (ctx->n_chunks.ptr)
+            GSIM_CK(cudaMemcpyAsync(&chunks, ctx->n_chunks.ptr, sizeof(chunks), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        st.consumed = c[2];
+        st.chunks = chunks;
         if (ctx->profiling) {
-            GSIM_CK(cudaEventSynchronize(ctx->ev[kEvRaster]));
             auto ms = [&](int a, int b) {
                 float v = 0.f;
                 GSIM_CK(cudaEventElapsedTime(&v, ctx->ev[a], ctx->ev[b]));
@@ -769,10 +803,9 @@ int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out) {
             };
             st.ms_preprocess = ms(kEvStart, kEvPre);
             st.ms_depth_sort = ms(kEvPre, kEvDepth);
-            st.ms_duplicate = ms(kEvDepth, kEvDup);
-            st.ms_tile_sort = ms(kEvDup, kEvTile);
-            st.ms_ranges = ms(kEvTile, kEvRanges);
-            st.ms_raster = ms(kEvRanges, kEvRaster);
+            st.ms_binning = ms(kEvDepth, kEvBin);
+            st.ms_scatter = ms(kEvBin, kEvScatter);
+            st.ms_raster = ms(kEvScatter, kEvRaster);
             st.ms_total = ms(kEvStart, kEvRaster);
         }
         *out = st;
@@ -908,22 +941,12 @@ int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const g
         const uint64_t S = std::max<uint64_t>(plan.slots, 1);
         ctx->full.reserve(S);
         ctx->full_vis.reserve(S);
-        begin_frame(ctx);
-        PreprocessArgs pa{};
-        pa.field = scene->f;
-        pa.segs = ctx->segs;
-        pa.n_segs = int(plan.segs.size());
-        pa.entries = ctx->entries;
-        pa.cams = ctx->cams;
-        pa.records = ctx->records.ptr;
-    pa.rects = ctx->rects.ptr;
-        pa.keys = ctx->keys.ptr;
-        pa.hist = depth_hist(ctx);
-        pa.visible_count = ctx->counts.ptr;
+        begin_frame(ctx, plan);
+        PreprocessArgs pa = make_pre_args(ctx, scene, plan);
         pa.full = ctx->full.ptr;
         pa.full_visible = ctx->full_vis.ptr;
         if (plan.slots) {
-            launch_preprocess(pa, true, ctx->num_sms * ctx->occ_pre, ctx->stream);
+            launch_preprocess(pa, true, ctx->num_sms * 2, ctx->stream);
             check_launch();
             ctx->launches_total += 1;
         }
@@ -962,8 +985,8 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
             GSIM_CK(cudaMemcpyAsync(ctx->splats_in.ptr, splats, n * sizeof(gsim_projected_splat),
                                     cudaMemcpyHostToDevice, ctx->stream));
         ctx->stats.h2d_bytes += n * sizeof(gsim_projected_splat);
-        record_stage(ctx, kEvStart);
-        begin_frame(ctx);
+        record_ev(ctx, kEvStart);
+        begin_frame(ctx, plan);
         uint64_t launches = 0;
         SplatArgs sa{};
         sa.splats = ctx->splats_in.ptr;
@@ -972,14 +995,12 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
         sa.records = ctx->records.ptr;
         sa.rects = ctx->rects.ptr;
         sa.keys = ctx->keys.ptr;
-        sa.hist = depth_hist(ctx);
-        sa.visible_count = ctx->counts.ptr;
         if (n) {
             launch_splats_to_records(sa, ctx->num_sms * 8, ctx->stream);
             check_launch();
             ++launches;
         }
-        record_stage(ctx, kEvPre);
+        record_ev(ctx, kEvPre);
         run_sort_and_raster(ctx, plan, opt, ctx->out.ptr, launches);
         finish_stats(ctx, plan, launches);
         const DevCamera& c = plan.cams[0];
@@ -1038,24 +1059,24 @@ int gsim_gpu_tile_lists(gsim_gpu_context* ctx, uint32_t camera, uint32_t* tile_b
         if (!count) throw ValidationError{"tile_lists: null count"};
         GSIM_CK(cudaStreamSynchronize(ctx->stream));
         const uint32_t t0 = p.tile_base[camera], nt = p.tile_base[camera + 1] - t0;
-        std::vector<uint32_t> b(nt), e(nt);
+        std::vector<uint32_t> rel(nt), cnt(nt);
+        uint64_t pbase = 0;
         if (nt) {
-            GSIM_CK(cudaMemcpy(b.data(), ctx->tile_begin.ptr + t0, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-            GSIM_CK(cudaMemcpy(e.data(), ctx->tile_end.ptr + t0, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            GSIM_CK(cudaMemcpy(rel.data(), ctx->tile_rel.ptr + t0, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            GSIM_CK(cudaMemcpy(cnt.data(), ctx->tile_count.ptr + t0, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            GSIM_CK(cudaMemcpy(&pbase, ctx->cam_pair_base.ptr + camera, sizeof(uint64_t), cudaMemcpyDeviceToHost));
         }
-        uint64_t first = UINT64_MAX, total = 0;
+        uint64_t total = 0;
         for (uint32_t t = 0; t < nt; ++t) {
             if (tile_begin) tile_begin[t] = uint32_t(total);
-            if (e[t] > b[t]) {
-                if (first == UINT64_MAX) first = b[t];
-                total += e[t] - b[t];
-            }
+            if (rel[t] != total) throw CudaError{"tile_lists: inconsistent tile offsets"};
+            total += cnt[t];
         }
         if (tile_begin) tile_begin[nt] = uint32_t(total);
         *count = total;
         if (values && total) {
             std::vector<uint32_t> v(total);
-            GSIM_CK(cudaMemcpy(v.data(), ctx->final_vals + first, total * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            GSIM_CK(cudaMemcpy(v.data(), ctx->vals.ptr + pbase, total * sizeof(uint32_t), cudaMemcpyDeviceToHost));
             const uint64_t sb = p.slot_base[camera];
             for (uint64_t k = 0; k < total && k < capacity; ++k) values[k] = uint32_t(v[k] - sb);
         }

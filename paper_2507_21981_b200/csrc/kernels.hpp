@@ -1,6 +1,7 @@
 // kernels.hpp — argument blocks and host launchers of the sm_100a kernels.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -10,20 +11,21 @@
 namespace gsim_gpu {
 
 constexpr int kMaxSmemSegments = 1024;
-constexpr int kMaxTilePasses = 4;
+constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
+constexpr int kChunkRecords = 8192;     // depth-sorted records per binning chunk
 
 struct PreprocessArgs {
     DevField field;
     const DevSegment* segs;
     int n_segs;
-    int reserved;
+    int depth_bits;                  // camera index sits above this many key bits
     const SegEntry* entries;
     const DevCamera* cams;
     Record* records;                 // [slots]
-    uint32_t* rects;                 // [slots] packed tile rect (dup reads this, L2-resident)
+    uint32_t* rects;                 // [slots] packed tile rect (binning reads this plane)
     uint32_t* keys;                  // [slots], kInvalidKey when culled / no tile
-    uint32_t* hist;                  // [4][256] digit histograms of valid keys
-    unsigned long long* visible_count;
+    uint32_t key_base;               // float bits of the batch's smallest near plane
+    uint32_t reserved;
     gsim_projected_splat* full;      // project() API only: double splat per slot
     uint8_t* full_visible;           // project() API only
 };
@@ -35,8 +37,6 @@ struct SplatArgs {
     Record* records;
     uint32_t* rects;
     uint32_t* keys;
-    uint32_t* hist;
-    unsigned long long* visible_count;
 };
 
 // One onesweep LSD pass over (u32 key, u32 value) pairs, 8-bit digit at `shift`.
@@ -55,39 +55,43 @@ struct OnesweepArgs {
     int shift;
 };
 
-// Exclusive scan of tiles-touched over depth-sorted records + pair emission.
-struct DupArgs {
-    const uint32_t* slots;           // [V] record slots in depth order
-    const unsigned long long* n_dev; // V
-    const uint32_t* rects;           // [slots] packed tile rects
-    const uint64_t* cam_slot_base;   // [n_cams + 1]
-    const uint32_t* cam_tile_base;   // [n_cams + 1]
-    const int* cam_tiles_x;          // [n_cams]
+// Tile binning of the camera-major depth-sorted records (bin.cu).
+struct BinArgs {
+    const uint32_t* keys;            // [S] packed keys (key_hist)
+    uint64_t n_slots;
+    int depth_bits;
     int n_cams;
-    int tile_passes;
-    uint32_t* keys_out;              // [P] global tile id (camera tile_base + tile)
-    uint32_t* vals_out;              // [P] record slot
+    const uint32_t* sorted_slots;    // [V] record slots, camera-major depth order
+    const uint32_t* rects;           // [S]
+    const uint32_t* cam_tile_base;   // [C+1]
+    const int* cam_tiles_x;          // [C]
+    uint32_t* cam_visible;           // [C]   V_c (zeroed per frame)
+    uint32_t* cam_vbase;             // [C+1]
+    uint32_t* cam_chunk_base;        // [C+1]
+    uint64_t* cam_mbase;             // [C+1] count-matrix base, column-major [tile][chunk]
+    uint32_t* cam_pairs;             // [C]
+    uint64_t* cam_pair_base;         // [C+1]
+    uint32_t* chunk_cam;             // [K_max]
+    uint32_t* n_chunks;              // [1]
+    uint32_t* counts;                // count matrix / column prefixes
+    uint32_t* tile_count;            // [tiles]
+    uint32_t* tile_rel;              // [tiles] first pair of the tile within its camera
+    uint32_t* hist;                  // [4][256] depth digit histograms (zeroed per frame)
+    unsigned long long* totals;      // [0] V, [1] P
+    uint32_t* vals_out;              // [capacity] record slot of every pair, final order
     uint64_t capacity;
-    uint32_t* hist;                  // [tile_passes][256]
-    uint64_t* status;                // [chunks]
-    uint32_t* ticket;
-    uint32_t epoch;
-    unsigned long long* pairs_out;   // P (total, may exceed capacity)
-};
-
-struct RangesArgs {
-    const uint32_t* keys;            // [P] sorted global tile ids
-    const unsigned long long* n_dev; // P
-    uint64_t capacity;
-    uint32_t* tile_begin;            // [tiles]
-    uint32_t* tile_end;              // [tiles]
+    int max_tc;                      // largest tile count of a camera in the batch
+    int chunk_records;
+    int bin_warps;                   // warps per block that own a counter array
+    int reserved;
 };
 
 struct RasterArgs {
     const Record* records;
-    const uint32_t* values;          // [P] sorted record slots
-    const uint32_t* tile_begin;
-    const uint32_t* tile_end;
+    const uint32_t* values;          // [P] record slots in (camera, tile, depth) order
+    const uint32_t* tile_rel;        // [tiles]
+    const uint32_t* tile_count;      // [tiles]
+    const uint64_t* cam_pair_base;   // [C+1]
     const DevCamera* cams;
     const uint32_t* cam_tile_base;   // [n_cams + 1]
     int n_cams;
@@ -104,11 +108,14 @@ void launch_preprocess(const PreprocessArgs& a, bool full, int grid_cap, cudaStr
 void launch_splats_to_records(const SplatArgs& a, int grid_cap, cudaStream_t stream);
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream);
-void launch_scan_dup(const DupArgs& a, int grid, cudaStream_t stream);
-void launch_ranges(const RangesArgs& a, int grid, cudaStream_t stream);
+void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s);
+void launch_chunk_table(const BinArgs& a, cudaStream_t s);
+size_t bin_smem_bytes(const BinArgs& a);
+void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s);
+void launch_bin_colscan(const BinArgs& a, int grid, cudaStream_t s);
+void launch_bin_tilescan(const BinArgs& a, int grid, cudaStream_t s);
+void launch_bin_campre(const BinArgs& a, cudaStream_t s);
+void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s);
 void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream);
-
-constexpr int kOnesweepTile = 4096;  // keys per onesweep chunk (256 threads x 16)
-constexpr int kDupTile = 2048;       // records per scan/duplicate chunk (256 threads x 8)
 
 }  // namespace gsim_gpu

@@ -126,15 +126,12 @@ __global__ void __launch_bounds__(256) pose_kernel(DevField f, uint64_t begin, u
 // ---- K2: project + shade_sh (raster.cpp:135-232, sh.cpp:10-51) ---------------------------
 template <int DEG, bool kFull>
 __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args) {
-    __shared__ uint32_t s_hist[4][256];
     __shared__ uint64_t s_seg_begin[kMaxSmemSegments];
     const DevField f = args.field;
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
     const int n_seg_smem = args.n_segs < kMaxSmemSegments ? args.n_segs : kMaxSmemSegments;
     for (int k = threadIdx.x; k < n_seg_smem; k += blockDim.x) s_seg_begin[k] = args.segs[k].begin;
     __syncthreads();
 
-    uint32_t local_visible = 0;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < f.n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         int si;
@@ -283,33 +280,17 @@ __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args)
             rec.c = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(rec_rect));
             args.records[slot] = rec;
             args.rects[slot] = rec_rect;
-            const uint32_t key = __float_as_uint(fz);  // depth_sort_key, raster.hpp:45-47
-            args.keys[slot] = key;
-            atomicAdd(&s_hist[0][key & 255], 1u);
-            atomicAdd(&s_hist[1][(key >> 8) & 255], 1u);
-            atomicAdd(&s_hist[2][(key >> 16) & 255], 1u);
-            atomicAdd(&s_hist[3][key >> 24], 1u);
-            ++local_visible;
+            // Camera-major sort key: camera index above the float32 depth bits
+            // (depth_sort_key, raster.hpp:45-47) rebased to the batch's [near, far) range;
+            // positive floats order like their bit patterns, so the order is unchanged.
+            args.keys[slot] = (ent.cam << args.depth_bits) | (__float_as_uint(fz) - args.key_base);
         }
-    }
-    // Flush the block's digit histograms and visible count.
-    for (int w = 16; w >= 1; w >>= 1) local_visible += __shfl_xor_sync(0xffffffffu, local_visible, w);
-    if ((threadIdx.x & 31) == 0 && local_visible)
-        atomicAdd(args.visible_count, (unsigned long long)local_visible);
-    __syncthreads();
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
-        const uint32_t v = (&s_hist[0][0])[k];
-        if (v) atomicAdd(args.hist + k, v);
     }
 }
 
 // ---- rasterize(splats) entry: host ProjectedSplats -> records + keys -----------------------
 __global__ void __launch_bounds__(256) splats_to_records_kernel(SplatArgs args) {
-    __shared__ uint32_t s_hist[4][256];
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
-    __syncthreads();
     const DevCamera cam = args.cam[0];
-    uint32_t local_visible = 0;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < args.n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const gsim_projected_splat sp = args.splats[i];
@@ -336,22 +317,10 @@ __global__ void __launch_bounds__(256) splats_to_records_kernel(SplatArgs args) 
                             __uint_as_float(pack_rect(tx0, ty0, tx1, ty1)));
         args.records[i] = rec;
         args.rects[i] = pack_rect(tx0, ty0, tx1, ty1);
+        // Full 32-bit depth_sort_key (raster.hpp:45-47): hand-made splats may carry any depth.
         uint32_t key = __float_as_uint(fz);
         if (key == kInvalidKey) key = kInvalidKey - 1;  // reserved sentinel (a NaN payload)
         args.keys[i] = key;
-        atomicAdd(&s_hist[0][key & 255], 1u);
-        atomicAdd(&s_hist[1][(key >> 8) & 255], 1u);
-        atomicAdd(&s_hist[2][(key >> 16) & 255], 1u);
-        atomicAdd(&s_hist[3][key >> 24], 1u);
-        ++local_visible;
-    }
-    for (int w = 16; w >= 1; w >>= 1) local_visible += __shfl_xor_sync(0xffffffffu, local_visible, w);
-    if ((threadIdx.x & 31) == 0 && local_visible)
-        atomicAdd(args.visible_count, (unsigned long long)local_visible);
-    __syncthreads();
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
-        const uint32_t v = (&s_hist[0][0])[k];
-        if (v) atomicAdd(args.hist + k, v);
     }
 }
 

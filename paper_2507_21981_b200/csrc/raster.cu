@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
     const int y = ty * kTileSize + (warp >> 1) * 4 + (lane >> 3);
     const float px = float(x) + 0.5f, py = float(y) + 0.5f;
 
-    const uint32_t begin = a.tile_begin[g], end = a.tile_end[g];
+    const uint32_t begin = uint32_t(a.cam_pair_base[cam_idx]) + a.tile_rel[g];
+    const uint32_t end = begin + a.tile_count[g];
     const float cutoff = a.cutoff;
     float cr = 0.f, cg = 0.f, cb = 0.f, d = 0.f, acc = 0.f, T = 1.f;
     bool done = false;

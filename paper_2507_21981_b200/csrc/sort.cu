@@ -1,4 +1,4 @@
-// sort.cu — K3: onesweep LSD radix sort, fused scan + tile duplication, tile ranges.
+// sort.cu — K3a: onesweep LSD radix sort of the (camera | depth) record keys.
 //
 // The reference bins splats into (tile << 32 | float32 depth bits) keys and std::sorts
 // (key, splat index) pairs (raster.cpp:243-271). We produce the same order with an LSD radix
@@ -7,10 +7,10 @@
 //   pass 1..4  onesweep over the 32-bit depth key of every (camera, primitive) slot; pass 1
 //              also compacts (drops culled slots). Input order = (camera, primitive) order,
 //              so the stable sort leaves ties in primitive order, as the reference does.
-//   scan+dup   decoupled-lookback exclusive scan of tiles-touched over the depth-sorted
-//              records, then load-balanced emission of (camera|tile, slot) pairs.
-//   pass 5..   onesweep over the camera|tile digits (stable), giving (camera, tile, depth,
-//              primitive) order: exactly the reference's per-camera pair order.
+//   The key carries the camera index above the rebased depth bits, so the result is in
+//   (camera, depth, primitive) order; bin.cu then places every (tile, record) pair directly
+//   at its final position, which gives the reference's per-camera pair order without
+//   sorting the P ~ 3.5 V pairs.
 // Every pass is single-sweep: chunks are claimed through an atomic ticket (so predecessors
 // are always resident) and per-digit prefixes come from decoupled lookback over epoch-tagged
 // status words (no clearing between passes).
@@ -168,144 +168,6 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     }
 }
 
-// ---- scan + duplicate ----------------------------------------------------------------------
-constexpr int kDupItems = kDupTile / kThreads;  // 8 consecutive records per thread
-constexpr int kMaxSmemCams = 2048;
-
-__device__ __forceinline__ int camera_of_slot(uint32_t slot, const uint32_t* cam_slot, int n_cams) {
-    int lo = 0, hi = n_cams - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (cam_slot[mid] <= slot) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-// Each thread owns 8 consecutive depth-sorted records; the block scans their tile counts,
-// gets its global offset by decoupled lookback, and every thread then writes its own records'
-// pairs (row-major per record, raster.cpp:259-263) — tile counts are small and the sum over
-// 8 records evens them out, so no cross-thread load balancing is needed.
-__global__ void __launch_bounds__(kThreads) scan_dup_kernel(DupArgs a) {
-    __shared__ uint32_t s_cam_slot[kMaxSmemCams + 1];
-    __shared__ uint32_t s_cam_tile[kMaxSmemCams + 1];
-    __shared__ uint32_t s_cam_tx[kMaxSmemCams];
-    __shared__ uint32_t s_hist[kMaxTilePasses][kRadix];
-    __shared__ uint32_t s_tmp[kWarps];
-    __shared__ uint32_t s_ticket;
-    __shared__ unsigned long long s_prefix;
-
-    const int tid = threadIdx.x;
-    const uint64_t n = uint64_t(*a.n_dev);
-    const uint64_t chunks = (n + kDupTile - 1) / kDupTile;
-    const bool smem_cams = a.n_cams <= kMaxSmemCams;
-    for (int k = tid; k < kMaxTilePasses * kRadix; k += kThreads) (&s_hist[0][0])[k] = 0;
-    if (smem_cams)
-        for (int k = tid; k < a.n_cams; k += kThreads) {
-            s_cam_slot[k] = uint32_t(a.cam_slot_base[k]);
-            s_cam_tile[k] = a.cam_tile_base[k];
-            s_cam_tx[k] = uint32_t(a.cam_tiles_x[k]);
-        }
-
-    while (true) {
-        if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
-        __syncthreads();
-        const uint32_t t = s_ticket;
-        if (t >= chunks) break;
-        const uint64_t base = uint64_t(t) * kDupTile + uint64_t(tid) * kDupItems;
-
-        uint32_t slot[kDupItems], rect[kDupItems];
-        if (base + kDupItems <= n) {
-            const uint4 s0 = __ldcs(reinterpret_cast<const uint4*>(a.slots + base));
-            const uint4 s1 = __ldcs(reinterpret_cast<const uint4*>(a.slots + base) + 1);
-            slot[0] = s0.x; slot[1] = s0.y; slot[2] = s0.z; slot[3] = s0.w;
-            slot[4] = s1.x; slot[5] = s1.y; slot[6] = s1.z; slot[7] = s1.w;
-        } else {
-#pragma unroll
-            for (int j = 0; j < kDupItems; ++j)
-                slot[j] = (base + j < n) ? a.slots[base + j] : 0xFFFFFFFFu;
-        }
-        uint32_t thread_sum = 0;
-#pragma unroll
-        for (int j = 0; j < kDupItems; ++j) {
-            rect[j] = 0xFFFFFFFFu;
-            if (slot[j] != 0xFFFFFFFFu) rect[j] = __ldg(a.rects + slot[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < kDupItems; ++j) {
-            if (slot[j] == 0xFFFFFFFFu) continue;
-            const uint32_t r = rect[j];
-            thread_sum += (((r >> 16) & 255u) - (r & 255u) + 1u) * ((r >> 24) - ((r >> 8) & 255u) + 1u);
-        }
-        uint32_t block_total;
-        const uint32_t thread_excl = block_exclusive_scan(thread_sum, s_tmp, &block_total);
-        // Publish + lookback (one chain per pass).
-        if (tid == 0) {
-            uint64_t* my = a.status + t;
-            uint64_t prefix = 0;
-            if (t == 0) {
-                st_volatile_u64(my, make_status(kFlagInclusive, a.epoch, block_total));
-            } else {
-                st_volatile_u64(my, make_status(kFlagAggregate, a.epoch, block_total));
-                int64_t j = int64_t(t) - 1;
-                while (true) {
-                    const uint64_t s = wait_status(a.status + j, a.epoch);
-                    prefix += s & kCountMask;
-                    if ((s >> 62) == kFlagInclusive) break;
-                    --j;
-                }
-                st_volatile_u64(my, make_status(kFlagInclusive, a.epoch, prefix + block_total));
-            }
-            s_prefix = prefix;
-            if (t == chunks - 1) *a.pairs_out = prefix + block_total;
-        }
-        __syncthreads();
-        uint64_t out = s_prefix + thread_excl;
-#pragma unroll
-        for (int j = 0; j < kDupItems; ++j) {
-            if (slot[j] == 0xFFFFFFFFu) continue;
-            int cam = 0;
-            if (a.n_cams > 1)
-                cam = smem_cams ? camera_of_slot(slot[j], s_cam_slot, a.n_cams)
-                                : upper_index(a.cam_slot_base, a.n_cams, uint64_t(slot[j]));
-            const uint32_t tbase = smem_cams ? s_cam_tile[cam] : a.cam_tile_base[cam];
-            const uint32_t tw = smem_cams ? s_cam_tx[cam] : uint32_t(a.cam_tiles_x[cam]);
-            const uint32_t r = rect[j];
-            const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u, ty1 = r >> 24;
-            for (uint32_t ty = ty0; ty <= ty1; ++ty) {
-                const uint32_t row = tbase + ty * tw;
-                for (uint32_t tx = tx0; tx <= tx1; ++tx) {
-                    const uint32_t key = row + tx;
-                    if (out < a.capacity) {
-                        a.keys_out[out] = key;
-                        a.vals_out[out] = slot[j];
-                    }
-                    ++out;
-                    for (int p = 0; p < a.tile_passes; ++p)
-                        atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
-                }
-            }
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    for (int k = tid; k < a.tile_passes * kRadix; k += kThreads) {
-        const uint32_t v = (&s_hist[0][0])[k];
-        if (v) atomicAdd(a.hist + k, v);
-    }
-}
-
-// ---- tile ranges (raster.cpp:267-271) ------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) ranges_kernel(RangesArgs a) {
-    uint64_t n = uint64_t(*a.n_dev);
-    if (n > a.capacity) n = a.capacity;
-    for (uint64_t i = blockIdx.x * uint64_t(kThreads) + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * kThreads) {
-        const uint32_t k = a.keys[i];
-        if (i == 0 || a.keys[i - 1] != k) a.tile_begin[k] = uint32_t(i);
-        if (i + 1 == n || a.keys[i + 1] != k) a.tile_end[k] = uint32_t(i + 1);
-    }
-}
-
 // ---- launchers -----------------------------------------------------------------------------
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream) {
@@ -316,14 +178,6 @@ void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int gri
         if (write_keys) onesweep_kernel<false, true><<<grid, kThreads, 0, stream>>>(a);
         else onesweep_kernel<false, false><<<grid, kThreads, 0, stream>>>(a);
     }
-}
-
-void launch_scan_dup(const DupArgs& a, int grid, cudaStream_t stream) {
-    scan_dup_kernel<<<grid, kThreads, 0, stream>>>(a);
-}
-
-void launch_ranges(const RangesArgs& a, int grid, cudaStream_t stream) {
-    ranges_kernel<<<grid, kThreads, 0, stream>>>(a);
 }
 
 }  // namespace gsim_gpu
