@@ -84,6 +84,7 @@ struct ChunkInfo {
     int tiles_x;
     uint32_t tc;                  // tiles of the camera
     uint32_t tile_base;
+    int tbits;                    // bits of a camera-local tile id
 };
 
 __device__ __forceinline__ ChunkInfo chunk_info(const BinArgs& a, uint32_t k) {
@@ -99,6 +100,7 @@ __device__ __forceinline__ ChunkInfo chunk_info(const BinArgs& a, uint32_t k) {
     ci.tiles_x = a.cam_tiles_x[ci.cam];
     ci.tile_base = a.cam_tile_base[ci.cam];
     ci.tc = a.cam_tile_base[ci.cam + 1] - ci.tile_base;
+    ci.tbits = ci.tc > 1 ? 32 - __clz(int(ci.tc - 1)) : 0;
     return ci;
 }
 
@@ -117,10 +119,8 @@ __device__ __forceinline__ void count_chunk(const BinArgs& a, const ChunkInfo& c
         const uint32_t rect = valid ? __ldg(a.rects + slot) : 0u;
         for_each_pair(slot, rect, valid, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t) {
             const uint32_t m = __ballot_sync(kFull, in);
-            if (in) {
-                const uint32_t peers = __match_any_sync(m, tile);
-                if ((peers & lanemask_lt()) == 0) cnt_w[tile] += __popc(peers);
-            }
+            const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
+            if (in && (peers & lanemask_lt()) == 0) cnt_w[tile] += __popc(peers);
             __syncwarp();
         });
     }
@@ -140,15 +140,23 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
         const uint64_t i = base + lane;
         const uint32_t key = i < n ? __ldcs(a.keys + i) : kInvalidKey;
         const bool valid = key != kInvalidKey;
+        const uint32_t vmask = __ballot_sync(kFull, valid);
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            const uint32_t d = valid ? ((key >> (8 * p)) & 255u) : 256u;
-            const uint32_t peers = __match_any_sync(kFull, d);
+            const uint32_t d = (key >> (8 * p)) & 255u;
+            const uint32_t peers = peers_of<8>(kFull, d) & vmask;
             if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][p][d] += __popc(peers);
         }
-        const uint32_t cam = valid ? key_camera(key, a.depth_bits) : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(kFull, cam);
-        if (valid && (peers & lanemask_lt()) == 0) atomicAdd(a.cam_visible + cam, __popc(peers));
+        // per-camera counts: one round per distinct camera in the warp (usually one)
+        const uint32_t cam = key_camera(key, a.depth_bits);
+        uint32_t rem = vmask;
+        while (rem) {
+            const int leader = __ffs(rem) - 1;
+            const uint32_t c = __shfl_sync(kFull, cam, leader);
+            const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
+            if (lane == leader) atomicAdd(a.cam_visible + c, __popc(same));
+            rem &= ~same;
+        }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < 4 * 256; k += kThreads) {
@@ -389,11 +397,11 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                 const uint32_t rect = valid ? __ldg(a.rects + slot) : 0u;
                 for_each_pair(slot, rect, valid, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t sl) {
                     const uint32_t m = __ballot_sync(kFull, in);
+                    const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
+                    const uint32_t below = peers & lanemask_lt();
+                    const uint32_t pre = in ? pos_w[tile] : 0u;
+                    __syncwarp();
                     if (in) {
-                        const uint32_t peers = __match_any_sync(m, tile);
-                        const uint32_t below = peers & lanemask_lt();
-                        const uint32_t pre = pos_w[tile];
-                        __syncwarp(m);
                         if (below == 0) pos_w[tile] = pre + __popc(peers);
                         const uint32_t p = pre + __popc(below);
                         if (p < a.capacity) a.vals_out[p] = sl;

@@ -511,6 +511,8 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.cutoff = smallest_float_geq(opt.transmittance_cutoff);
     rr.out = out;
     rr.consumed = ctx->counts.ptr + 2;
+    rr.capacity = ctx->pair_capacity;
+    rr.n_slots = std::max<uint64_t>(p.slots, 1);
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
 }

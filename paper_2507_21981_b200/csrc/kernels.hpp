@@ -100,6 +100,8 @@ struct RasterArgs {
     float reserved;
     float* out;                      // per camera [rgb W*H*3 | depth W*H | alpha W*H]
     unsigned long long* consumed;    // += list entries fetched before the tile saturated
+    uint64_t capacity;               // pair-buffer capacity (reads are clamped to it)
+    uint64_t n_slots;                // record slots (stale values are clamped to a valid slot)
 };
 
 void launch_pose(const DevField& f, uint64_t begin, uint64_t end, const gsim_rigid& t,

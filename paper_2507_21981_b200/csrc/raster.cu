@@ -72,8 +72,12 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
     const int y = ty * kTileSize + (warp >> 1) * 4 + (lane >> 3);
     const float px = float(x) + 0.5f, py = float(y) + 0.5f;
 
-    const uint32_t begin = uint32_t(a.cam_pair_base[cam_idx]) + a.tile_rel[g];
-    const uint32_t end = begin + a.tile_count[g];
+    // On a pair-buffer overflow the host re-runs scatter + raster; until then keep every read
+    // in bounds (the clamped frame is discarded).
+    const uint64_t b64 = a.cam_pair_base[cam_idx] + a.tile_rel[g];
+    const uint32_t begin = uint32_t(b64 < a.capacity ? b64 : a.capacity);
+    const uint64_t e64 = b64 + a.tile_count[g];
+    const uint32_t end = uint32_t(e64 < a.capacity ? e64 : a.capacity);
     const float cutoff = a.cutoff;
     float cr = 0.f, cg = 0.f, cb = 0.f, d = 0.f, acc = 0.f, T = 1.f;
     bool done = false;
@@ -90,7 +94,8 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
         fetched += n_b;
         uint32_t mask = 0;
         if (uint32_t(tid) < n_b) {
-            const uint32_t slot = __ldg(a.values + b0 + tid);
+            uint32_t slot = __ldg(a.values + b0 + tid);
+            if (slot >= a.n_slots) slot = 0;  // only possible in a clamped (overflowed) frame
             const float4 ra = __ldg(&a.records[slot].a);
             const float4 rb = __ldg(&a.records[slot].b);
             const float4 rc = __ldg(&a.records[slot].c);

@@ -108,8 +108,9 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const bool valid = rank[i] != 0u;
-            const uint32_t d = valid ? ((keys[i] >> a.shift) & 255u) : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t d = (keys[i] >> a.shift) & 255u;
+            const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+            const uint32_t peers = peers_of<8>(0xffffffffu, d) & vmask;
             const uint32_t below = peers & lanemask_lt();
             uint32_t pre = 0;
             if (valid) pre = s_warp_hist[warp][d];
