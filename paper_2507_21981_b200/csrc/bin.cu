@@ -54,6 +54,10 @@ __device__ __forceinline__ void for_each_pair(uint32_t slot, uint32_t rect, bool
     }
     const uint32_t excl = incl - cnt;
     const uint32_t total = __shfl_sync(kFull, incl, 31);
+    // row-major position -> (row, column) with a per-record magic reciprocal: for kk < 2^16
+    // and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
+    const uint32_t w_own = ((rect >> 16) & 255u) - (rect & 255u) + 1u;
+    const uint32_t magic = w_own > 1u ? 0xFFFFFFFFu / w_own + 1u : 0u;
     for (uint32_t k0 = 0; k0 < total; k0 += 32) {
         const uint32_t j = k0 + lane;
         // owner = last lane whose exclusive offset <= j (valid lanes have cnt >= 1)
@@ -66,13 +70,41 @@ __device__ __forceinline__ void for_each_pair(uint32_t slot, uint32_t rect, bool
         const uint32_t o_own = __shfl_sync(kFull, excl, lo);
         const uint32_t r = __shfl_sync(kFull, rect, lo);
         const uint32_t sl = __shfl_sync(kFull, slot, lo);
+        const uint32_t mg = __shfl_sync(kFull, magic, lo);
         const bool in = j < total;
         const uint32_t kk = j - o_own;
         const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u;
         const uint32_t w = tx1 - tx0 + 1u;
-        const uint32_t q = in ? kk / w : 0u;
+        const uint32_t q = mg ? __umulhi(kk, mg) : kk;
         const uint32_t tile = (ty0 + q) * uint32_t(tiles_x) + tx0 + (kk - q * w);
         fn(in, tile, sl);
+    }
+}
+
+// Walk records [wb, we) of the depth-sorted list in order, 32 per group, with the slot and
+// rect loads of kG groups issued together (latency hiding), calling for_each_pair per group.
+template <class F>
+__device__ __forceinline__ void walk_records(const BinArgs& a, uint32_t wb, uint32_t we,
+                                             int tiles_x, F&& fn) {
+    constexpr int kG = 4;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t g0 = wb; g0 < we; g0 += 32 * kG) {
+        uint32_t slot[kG], rect[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const uint32_t e = g0 + q * 32 + lane;
+            slot[q] = e < we ? __ldcs(a.sorted_slots + e) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const uint32_t e = g0 + q * 32 + lane;
+            rect[q] = e < we ? __ldg(a.rects + slot[q]) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            if (g0 + q * 32 >= we) break;
+            for_each_pair(slot[q], rect[q], g0 + q * 32 + lane < we, tiles_x, fn);
+        }
     }
 }
 
@@ -112,18 +144,13 @@ __device__ __forceinline__ void count_chunk(const BinArgs& a, const ChunkInfo& c
     const uint32_t per_warp = (n + n_warps - 1) / n_warps;
     const uint32_t wb = ci.rec_begin + min(n, per_warp * warp);
     const uint32_t we = ci.rec_begin + min(n, per_warp * (warp + 1));
-    for (uint32_t g0 = wb; g0 < we; g0 += 32) {
-        const uint32_t e = g0 + lane;
-        const bool valid = e < we;
-        const uint32_t slot = valid ? a.sorted_slots[e] : 0u;
-        const uint32_t rect = valid ? __ldg(a.rects + slot) : 0u;
-        for_each_pair(slot, rect, valid, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t) {
-            const uint32_t m = __ballot_sync(kFull, in);
-            const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
-            if (in && (peers & lanemask_lt()) == 0) cnt_w[tile] += __popc(peers);
-            __syncwarp();
-        });
-    }
+    walk_records(a, wb, we, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t) {
+        const uint32_t m = __ballot_sync(kFull, in);
+        const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
+        if (in && (peers & lanemask_lt()) == 0) cnt_w[tile] += __popc(peers);
+        __syncwarp();
+    });
+    (void)lane;
 }
 
 }  // namespace
@@ -135,28 +162,45 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
     for (int k = threadIdx.x; k < kWarps * 4 * 256; k += kThreads) (&s_hist[0][0][0])[k] = 0;
     __syncthreads();
     const uint64_t n = a.n_slots;
-    const uint64_t stride = uint64_t(gridDim.x) * kThreads;
-    for (uint64_t base = uint64_t(blockIdx.x) * kThreads + (threadIdx.x & ~31u); base < n; base += stride) {
-        const uint64_t i = base + lane;
-        const uint32_t key = i < n ? __ldcs(a.keys + i) : kInvalidKey;
-        const bool valid = key != kInvalidKey;
-        const uint32_t vmask = __ballot_sync(kFull, valid);
+    constexpr int kKeys = 16;  // keys per lane in flight: memory-level parallelism
+    const uint64_t stride = uint64_t(gridDim.x) * kThreads * kKeys;
+    for (uint64_t base = (uint64_t(blockIdx.x) * kWarps + warp) * 32 * kKeys; base < n; base += stride) {
+        uint32_t keys[kKeys];
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const uint32_t d = (key >> (8 * p)) & 255u;
-            const uint32_t peers = peers_of<8>(kFull, d) & vmask;
-            if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][p][d] += __popc(peers);
+        for (int i = 0; i < kKeys; ++i) {
+            const uint64_t idx = base + uint64_t(i) * 32 + lane;
+            keys[i] = idx < n ? __ldcs(a.keys + idx) : kInvalidKey;
         }
-        // per-camera counts: one round per distinct camera in the warp (usually one)
-        const uint32_t cam = key_camera(key, a.depth_bits);
-        uint32_t rem = vmask;
-        while (rem) {
-            const int leader = __ffs(rem) - 1;
-            const uint32_t c = __shfl_sync(kFull, cam, leader);
-            const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
-            if (lane == leader) atomicAdd(a.cam_visible + c, __popc(same));
-            rem &= ~same;
+        uint32_t cam_run = 0xFFFFFFFFu, cam_cnt = 0;  // lane 0 accumulates runs of one camera
+#pragma unroll
+        for (int i = 0; i < kKeys; ++i) {
+            const uint32_t key = keys[i];
+            const bool valid = key != kInvalidKey;
+            const uint32_t vmask = __ballot_sync(kFull, valid);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const uint32_t d = (key >> (8 * p)) & 255u;
+                const uint32_t peers = peers_of<8>(kFull, d) & vmask;
+                if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][p][d] += __popc(peers);
+            }
+            // per-camera counts: one round per distinct camera in the group (usually one)
+            const uint32_t cam = key_camera(key, a.depth_bits);
+            uint32_t rem = vmask;
+            while (rem) {
+                const int leader = __ffs(rem) - 1;
+                const uint32_t c = __shfl_sync(kFull, cam, leader);
+                const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
+                if (c == cam_run) {
+                    cam_cnt += __popc(same);
+                } else {
+                    if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
+                    cam_run = c;
+                    cam_cnt = __popc(same);
+                }
+                rem &= ~same;
+            }
         }
+        if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < 4 * 256; k += kThreads) {
@@ -390,25 +434,20 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
             const uint32_t per_warp = (n + n_warps - 1) / n_warps;
             const uint32_t wb = ci.rec_begin + min(n, per_warp * warp);
             const uint32_t we = ci.rec_begin + min(n, per_warp * (warp + 1));
-            for (uint32_t g0 = wb; g0 < we; g0 += 32) {
-                const uint32_t e = g0 + lane;
-                const bool valid = e < we;
-                const uint32_t slot = valid ? a.sorted_slots[e] : 0u;
-                const uint32_t rect = valid ? __ldg(a.rects + slot) : 0u;
-                for_each_pair(slot, rect, valid, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t sl) {
-                    const uint32_t m = __ballot_sync(kFull, in);
-                    const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
-                    const uint32_t below = peers & lanemask_lt();
-                    const uint32_t pre = in ? pos_w[tile] : 0u;
-                    __syncwarp();
-                    if (in) {
-                        if (below == 0) pos_w[tile] = pre + __popc(peers);
-                        const uint32_t p = pre + __popc(below);
-                        if (p < a.capacity) a.vals_out[p] = sl;
-                    }
-                    __syncwarp();
-                });
-            }
+            walk_records(a, wb, we, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t sl) {
+                const uint32_t m = __ballot_sync(kFull, in);
+                const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
+                const uint32_t below = peers & lanemask_lt();
+                const uint32_t pre = in ? pos_w[tile] : 0u;
+                __syncwarp();
+                if (in) {
+                    if (below == 0) pos_w[tile] = pre + __popc(peers);
+                    const uint32_t p = pre + __popc(below);
+                    if (p < a.capacity) a.vals_out[p] = sl;
+                }
+                __syncwarp();
+            });
+            (void)lane;
         }
         __syncthreads();
     }

@@ -561,7 +561,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
 
     // tile binning: counts, scans, camera bases
     const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + p.cams.size();
-    const int chunk_grid = int(std::max<uint64_t>(1, std::min<uint64_t>(kmax, uint64_t(n_sms) * 2)));
+    const int chunk_grid = int(std::max<uint64_t>(1, std::min<uint64_t>(kmax, uint64_t(n_sms) * 6)));
     launch_bin_count(b, chunk_grid, s);
     check_launch();
     const uint64_t col_warps = p.tiles;

@@ -12,7 +12,7 @@ namespace gsim_gpu {
 
 constexpr int kMaxSmemSegments = 1024;
 constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
-constexpr int kChunkRecords = 8192;     // depth-sorted records per binning chunk
+constexpr int kChunkRecords = 2048;     // depth-sorted records per binning chunk
 
 struct PreprocessArgs {
     DevField field;
