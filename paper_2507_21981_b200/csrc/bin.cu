@@ -3,18 +3,22 @@
 // The reference emits (tile << 32 | depth, splat) pairs and std::sorts them
 // (raster.cpp:243-271). After the camera-major depth sort of the V visible records
 // (sort.cu), the pair order we need is simply "by (camera, tile), then by record order".
-// Instead of radix-sorting the P ~ 3.5 V pairs by tile, we place every pair directly:
-//   count    per chunk of R depth-sorted records of one camera, count pairs per tile
-//            (pairs are enumerated warp-cooperatively; lanes with the same tile are merged
-//            with match.any and the leader bumps a warp-private counter — no shared atomics,
-//            which cost 2 cycles per lane on this part);
-//   colscan  per (camera, tile): exclusive scan of the counts over the camera's chunks;
-//   tilescan per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:267-271);
-//   campre   per batch: pair base of every camera;
-//   scatter  per chunk: recount per warp, turn counts into base positions, then walk the
-//            records again in order and write each pair's record slot at base + rank, where
-//            rank comes from match.any in lane order = emission order (raster.cpp:259-263).
-// The result equals the reference's stable (tile, depth, primitive) order bit for bit.
+// Instead of radix-sorting the P ~ 3.5 V pairs by tile, every pair is placed directly:
+//   units     the depth-sorted records of each camera are cut into units of R records; one
+//             warp owns one unit (no block-level cooperation, no barriers);
+//   count     per unit, count pairs per tile into a warp-private counter array and store the
+//             row into a per-camera [tile][unit] count matrix;
+//   colscan   per (camera, tile): exclusive scan over the camera's units;
+//   tilescan  per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:267-271);
+//   campre    per batch: pair base of every camera;
+//   scatter   per unit: load the unit's first position of every tile, walk the records again
+//             in order and write each pair's record slot at its position.
+// Pairs are enumerated warp-cooperatively, 32 consecutive pairs per step in emission order
+// (record order, row-major tiles inside a record, raster.cpp:259-263). Two lanes of a step
+// hitting the same tile is detected with a shared-memory "last writer" probe; only then are
+// the tile's lanes ranked with ballots (match.any issues at ~1 per 40 SM cycles on sm_100,
+// shared atomics at 2 cycles per lane: both measured, both avoided). The result equals the
+// reference's stable (tile, depth, primitive) order bit for bit.
 #include <cstdint>
 
 #include "common.cuh"
@@ -31,16 +35,12 @@ __device__ __forceinline__ uint32_t key_camera(uint32_t key, int depth_bits) {
     return depth_bits >= 32 ? 0u : (key >> depth_bits);
 }
 
-__device__ __forceinline__ int cam_of_tile(const uint32_t* tile_base, int n_cams, uint32_t g) {
-    return upper_index(tile_base, n_cams, g);
-}
-
 __device__ __forceinline__ uint32_t rect_area(uint32_t r) {
     return (((r >> 16) & 255u) - (r & 255u) + 1u) * ((r >> 24) - ((r >> 8) & 255u) + 1u);
 }
 
 // Warp-cooperative enumeration of the pairs of 32 records (one per lane): calls
-// fn(j_valid, tile, slot) once per output step with consecutive pair indices per lane.
+// fn(in, tile, slot) once per step; lane j of a step holds the step's j-th pair.
 template <class F>
 __device__ __forceinline__ void for_each_pair(uint32_t slot, uint32_t rect, bool valid,
                                               int tiles_x, F&& fn) {
@@ -108,49 +108,53 @@ __device__ __forceinline__ void walk_records(const BinArgs& a, uint32_t wb, uint
     }
 }
 
-struct ChunkInfo {
+// Lanes of `in_mask` whose tile equals this lane's, ordered by lane = emission order.
+// Fast path: every lane writes its lane id to probe[tile], then reads it back; if no lane
+// lost the write, all tiles in the step are distinct and each lane is its own only peer.
+__device__ __forceinline__ uint32_t tile_peers(uint8_t* probe, uint32_t tile, bool in,
+                                               uint32_t in_mask, int tbits) {
+    const int lane = threadIdx.x & 31;
+    if (in) probe[tile] = uint8_t(lane);
+    __syncwarp();
+    const bool lost = in && probe[tile] != uint8_t(lane);
+    const bool any_conflict = __any_sync(kFull, lost);
+    __syncwarp();
+    if (!any_conflict) return in ? (1u << lane) : 0u;
+    return peers_of_bits(kFull, tile, tbits) & in_mask;
+}
+
+struct Unit {
     int cam;
     uint32_t rec_begin, rec_end;  // depth-sorted record range
-    uint32_t chunk_in_cam, chunks_in_cam;
-    uint64_t mbase;               // count-matrix base of the camera
+    uint32_t unit_in_cam, units_in_cam;
+    uint64_t mbase;               // count-matrix base of the camera ([tile][unit])
     int tiles_x;
     uint32_t tc;                  // tiles of the camera
     uint32_t tile_base;
     int tbits;                    // bits of a camera-local tile id
 };
 
-__device__ __forceinline__ ChunkInfo chunk_info(const BinArgs& a, uint32_t k) {
-    ChunkInfo ci;
-    ci.cam = int(a.chunk_cam[k]);
-    const uint32_t cb = a.cam_chunk_base[ci.cam];
-    ci.chunk_in_cam = k - cb;
-    ci.chunks_in_cam = a.cam_chunk_base[ci.cam + 1] - cb;
-    const uint32_t vb = a.cam_vbase[ci.cam], ve = a.cam_vbase[ci.cam + 1];
-    ci.rec_begin = vb + ci.chunk_in_cam * uint32_t(a.chunk_records);
-    ci.rec_end = min(ci.rec_begin + uint32_t(a.chunk_records), ve);
-    ci.mbase = a.cam_mbase[ci.cam];
-    ci.tiles_x = a.cam_tiles_x[ci.cam];
-    ci.tile_base = a.cam_tile_base[ci.cam];
-    ci.tc = a.cam_tile_base[ci.cam + 1] - ci.tile_base;
-    ci.tbits = ci.tc > 1 ? 32 - __clz(int(ci.tc - 1)) : 0;
-    return ci;
+__device__ __forceinline__ Unit unit_info(const BinArgs& a, uint32_t k) {
+    Unit u;
+    u.cam = int(a.chunk_cam[k]);
+    const uint32_t cb = a.cam_chunk_base[u.cam];
+    u.unit_in_cam = k - cb;
+    u.units_in_cam = a.cam_chunk_base[u.cam + 1] - cb;
+    const uint32_t vb = a.cam_vbase[u.cam], ve = a.cam_vbase[u.cam + 1];
+    u.rec_begin = vb + u.unit_in_cam * uint32_t(a.chunk_records);
+    u.rec_end = min(u.rec_begin + uint32_t(a.chunk_records), ve);
+    u.mbase = a.cam_mbase[u.cam];
+    u.tiles_x = a.cam_tiles_x[u.cam];
+    u.tile_base = a.cam_tile_base[u.cam];
+    u.tc = a.cam_tile_base[u.cam + 1] - u.tile_base;
+    u.tbits = u.tc > 1 ? 32 - __clz(int(u.tc - 1)) : 0;
+    return u;
 }
 
-// Per-warp counts of a chunk into cnt[warp][tile] (counters zeroed by the caller).
-__device__ __forceinline__ void count_chunk(const BinArgs& a, const ChunkInfo& ci, uint32_t* cnt_w,
-                                            int n_warps) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t n = ci.rec_end - ci.rec_begin;
-    const uint32_t per_warp = (n + n_warps - 1) / n_warps;
-    const uint32_t wb = ci.rec_begin + min(n, per_warp * warp);
-    const uint32_t we = ci.rec_begin + min(n, per_warp * (warp + 1));
-    walk_records(a, wb, we, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t) {
-        const uint32_t m = __ballot_sync(kFull, in);
-        const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
-        if (in && (peers & lanemask_lt()) == 0) cnt_w[tile] += __popc(peers);
-        __syncwarp();
-    });
-    (void)lane;
+// Warp w of the block works in s_bin + w * per_warp_bytes: [max_tc] u32 + [max_tc] u8 probe.
+__device__ __forceinline__ uint32_t* warp_counters(char* s_bin, int max_tc) {
+    const size_t per_warp = (size_t(max_tc) * 5 + 15) & ~size_t(15);
+    return reinterpret_cast<uint32_t*>(s_bin + (threadIdx.x >> 5) * per_warp);
 }
 
 }  // namespace
@@ -211,103 +215,82 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
     }
 }
 
-// ---- per-camera chunk tables (one block) ----------------------------------------------------
+// ---- per-camera unit tables (one block) -----------------------------------------------------
 __global__ void __launch_bounds__(1024) chunk_table_kernel(BinArgs a) {
-    __shared__ uint32_t s_scan[1024];
-    __shared__ uint32_t s_carry_v, s_carry_k;
-    __shared__ unsigned long long s_carry_m;
+    __shared__ unsigned long long s_scan[1024];
+    __shared__ unsigned long long s_carry[3];
     const int tid = threadIdx.x;
-    if (tid == 0) { s_carry_v = 0; s_carry_k = 0; s_carry_m = 0; }
+    if (tid < 3) s_carry[tid] = 0;
     __syncthreads();
     const uint32_t R = uint32_t(a.chunk_records);
+    auto scan = [&](unsigned long long v) {  // inclusive block scan
+        s_scan[tid] = v;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            const unsigned long long t = tid >= o ? s_scan[tid - o] : 0ull;
+            __syncthreads();
+            s_scan[tid] += t;
+            __syncthreads();
+        }
+        const unsigned long long r = s_scan[tid];
+        __syncthreads();
+        return r;
+    };
     for (int c0 = 0; c0 < a.n_cams; c0 += 1024) {
         const int c = c0 + tid;
         const uint32_t v = c < a.n_cams ? a.cam_visible[c] : 0u;
         const uint32_t k = (v + R - 1) / R;
         const uint32_t tc = c < a.n_cams ? a.cam_tile_base[c + 1] - a.cam_tile_base[c] : 0u;
         const unsigned long long m = (unsigned long long)k * tc;
-        // three inclusive block scans (v, k, m) via smem Hillis-Steele
-        uint32_t sv = v;
-        s_scan[tid] = sv;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const uint32_t t = tid >= o ? s_scan[tid - o] : 0u;
-            __syncthreads();
-            s_scan[tid] += t;
-            __syncthreads();
-        }
-        const uint32_t incl_v = s_scan[tid];
-        __syncthreads();
-        s_scan[tid] = k;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const uint32_t t = tid >= o ? s_scan[tid - o] : 0u;
-            __syncthreads();
-            s_scan[tid] += t;
-            __syncthreads();
-        }
-        const uint32_t incl_k = s_scan[tid];
-        __syncthreads();
-        // m can exceed 32 bits only for absurd batches; scan it in 64-bit via two passes of hi/lo
-        unsigned long long incl_m = m;
-        {
-            __shared__ unsigned long long s_m[1024];
-            s_m[tid] = m;
-            __syncthreads();
-            for (int o = 1; o < 1024; o <<= 1) {
-                const unsigned long long t = tid >= o ? s_m[tid - o] : 0ull;
-                __syncthreads();
-                s_m[tid] += t;
-                __syncthreads();
-            }
-            incl_m = s_m[tid];
-            __syncthreads();
-        }
+        const unsigned long long iv = scan(v), ik = scan(k), im = scan(m);
         if (c < a.n_cams) {
-            a.cam_vbase[c] = s_carry_v + incl_v - v;
-            a.cam_chunk_base[c] = s_carry_k + incl_k - k;
-            a.cam_mbase[c] = s_carry_m + incl_m - m;
+            a.cam_vbase[c] = uint32_t(s_carry[0] + iv - v);
+            a.cam_chunk_base[c] = uint32_t(s_carry[1] + ik - k);
+            a.cam_mbase[c] = s_carry[2] + im - m;
         }
         __syncthreads();
         if (tid == 1023) {
-            s_carry_v += incl_v;
-            s_carry_k += incl_k;
-            s_carry_m += incl_m;
+            s_carry[0] += iv;
+            s_carry[1] += ik;
+            s_carry[2] += im;
         }
         __syncthreads();
     }
     if (tid == 0) {
-        a.cam_vbase[a.n_cams] = s_carry_v;
-        a.cam_chunk_base[a.n_cams] = s_carry_k;
-        a.cam_mbase[a.n_cams] = s_carry_m;
-        *a.n_chunks = s_carry_k;
-        a.totals[0] = s_carry_v;  // V
+        a.cam_vbase[a.n_cams] = uint32_t(s_carry[0]);
+        a.cam_chunk_base[a.n_cams] = uint32_t(s_carry[1]);
+        a.cam_mbase[a.n_cams] = s_carry[2];
+        *a.n_chunks = uint32_t(s_carry[1]);
+        a.totals[0] = s_carry[0];  // V
     }
     __syncthreads();
-    const uint32_t K = s_carry_k;
+    const uint32_t K = uint32_t(s_carry[1]);
     for (uint32_t k = tid; k < K; k += 1024)
         a.chunk_cam[k] = uint32_t(upper_index(a.cam_chunk_base, a.n_cams, k));
 }
 
-// ---- count -------------------------------------------------------------------------------
+// ---- count: one warp per unit ------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinArgs a) {
-    extern __shared__ uint32_t s_cnt[];  // [n_warps][max_tc]
-    const int n_warps = a.bin_warps;
+    extern __shared__ __align__(16) char s_bin[];
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) >= a.bin_warps) return;
+    uint32_t* cnt = warp_counters(s_bin, a.max_tc);
+    uint8_t* probe = reinterpret_cast<uint8_t*>(cnt + a.max_tc);
     const uint32_t K = *a.n_chunks;
-    for (uint32_t k = blockIdx.x; k < K; k += gridDim.x) {
-        const ChunkInfo ci = chunk_info(a, k);
-        for (uint32_t i = threadIdx.x; i < uint32_t(n_warps) * ci.tc; i += blockDim.x) s_cnt[i] = 0;
-        __syncthreads();
-        if (int(threadIdx.x >> 5) < n_warps)
-            count_chunk(a, ci, s_cnt + (threadIdx.x >> 5) * ci.tc, n_warps);
-        __syncthreads();
-        uint32_t* col = a.counts + ci.mbase + ci.chunk_in_cam;
-        for (uint32_t t = threadIdx.x; t < ci.tc; t += blockDim.x) {
-            uint32_t s = 0;
-            for (int w = 0; w < n_warps; ++w) s += s_cnt[w * ci.tc + t];
-            col[uint64_t(t) * ci.chunks_in_cam] = s;
-        }
-        __syncthreads();
+    const uint32_t n_warps = gridDim.x * uint32_t(a.bin_warps);
+    for (uint32_t k = blockIdx.x * a.bin_warps + (threadIdx.x >> 5); k < K; k += n_warps) {
+        const Unit u = unit_info(a, k);
+        for (uint32_t t = lane; t < u.tc; t += 32) cnt[t] = 0;
+        __syncwarp();
+        walk_records(a, u.rec_begin, u.rec_end, u.tiles_x, [&](bool in, uint32_t tile, uint32_t) {
+            const uint32_t m = __ballot_sync(kFull, in);
+            const uint32_t peers = tile_peers(probe, tile, in, m, u.tbits);
+            if (in && (peers & lanemask_lt()) == 0) cnt[tile] += __popc(peers);
+            __syncwarp();
+        });
+        uint32_t* col = a.counts + u.mbase + u.unit_in_cam;
+        for (uint32_t t = lane; t < u.tc; t += 32) col[uint64_t(t) * u.units_in_cam] = cnt[t];
+        __syncwarp();
     }
 }
 
@@ -317,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) bin_colscan_kernel(BinArgs a) {
     const uint32_t n_cols = a.cam_tile_base[a.n_cams];
     for (uint32_t g = (blockIdx.x * kThreads + threadIdx.x) >> 5; g < n_cols;
          g += (gridDim.x * kThreads) >> 5) {
-        const int c = cam_of_tile(a.cam_tile_base, a.n_cams, g);
+        const int c = upper_index(a.cam_tile_base, a.n_cams, g);
         const uint32_t t = g - a.cam_tile_base[c];
         const uint32_t nk = a.cam_chunk_base[c + 1] - a.cam_chunk_base[c];
         uint32_t* col = a.counts + a.cam_mbase[c] + uint64_t(t) * nk;
@@ -403,53 +386,36 @@ __global__ void __launch_bounds__(1024) bin_campre_kernel(BinArgs a) {
     }
 }
 
-// ---- scatter -----------------------------------------------------------------------------------
+// ---- scatter: one warp per unit ----------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
-    extern __shared__ uint32_t s_cnt[];  // [n_warps][max_tc]: counts, then running positions
-    const int n_warps = a.bin_warps;
-    const int warp = threadIdx.x >> 5;
+    extern __shared__ __align__(16) char s_bin[];
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) >= a.bin_warps) return;
+    uint32_t* pos = warp_counters(s_bin, a.max_tc);
+    uint8_t* probe = reinterpret_cast<uint8_t*>(pos + a.max_tc);
     const uint32_t K = *a.n_chunks;
-    for (uint32_t k = blockIdx.x; k < K; k += gridDim.x) {
-        const ChunkInfo ci = chunk_info(a, k);
-        for (uint32_t i = threadIdx.x; i < uint32_t(n_warps) * ci.tc; i += blockDim.x) s_cnt[i] = 0;
-        __syncthreads();
-        if (warp < n_warps) count_chunk(a, ci, s_cnt + warp * ci.tc, n_warps);
-        __syncthreads();
-        // counts -> first position of every (warp, tile) in the final list
-        const uint64_t pbase = a.cam_pair_base[ci.cam];
-        const uint32_t* col = a.counts + ci.mbase + ci.chunk_in_cam;
-        for (uint32_t t = threadIdx.x; t < ci.tc; t += blockDim.x) {
-            uint32_t run = uint32_t(pbase) + a.tile_rel[ci.tile_base + t] + col[uint64_t(t) * ci.chunks_in_cam];
-            for (int w = 0; w < n_warps; ++w) {
-                const uint32_t c = s_cnt[w * ci.tc + t];
-                s_cnt[w * ci.tc + t] = run;
-                run += c;
+    const uint32_t n_warps = gridDim.x * uint32_t(a.bin_warps);
+    for (uint32_t k = blockIdx.x * a.bin_warps + (threadIdx.x >> 5); k < K; k += n_warps) {
+        const Unit u = unit_info(a, k);
+        // first position of every tile of this unit in the final list
+        const uint32_t pbase = uint32_t(a.cam_pair_base[u.cam]);
+        const uint32_t* col = a.counts + u.mbase + u.unit_in_cam;
+        for (uint32_t t = lane; t < u.tc; t += 32)
+            pos[t] = pbase + a.tile_rel[u.tile_base + t] + col[uint64_t(t) * u.units_in_cam];
+        __syncwarp();
+        walk_records(a, u.rec_begin, u.rec_end, u.tiles_x, [&](bool in, uint32_t tile, uint32_t sl) {
+            const uint32_t m = __ballot_sync(kFull, in);
+            const uint32_t peers = tile_peers(probe, tile, in, m, u.tbits);
+            const uint32_t below = peers & lanemask_lt();
+            const uint32_t pre = in ? pos[tile] : 0u;
+            __syncwarp();
+            if (in) {
+                if (below == 0) pos[tile] = pre + __popc(peers);
+                const uint32_t p = pre + __popc(below);
+                if (p < a.capacity) a.vals_out[p] = sl;
             }
-        }
-        __syncthreads();
-        if (warp < n_warps) {
-            const int lane = threadIdx.x & 31;
-            uint32_t* pos_w = s_cnt + warp * ci.tc;
-            const uint32_t n = ci.rec_end - ci.rec_begin;
-            const uint32_t per_warp = (n + n_warps - 1) / n_warps;
-            const uint32_t wb = ci.rec_begin + min(n, per_warp * warp);
-            const uint32_t we = ci.rec_begin + min(n, per_warp * (warp + 1));
-            walk_records(a, wb, we, ci.tiles_x, [&](bool in, uint32_t tile, uint32_t sl) {
-                const uint32_t m = __ballot_sync(kFull, in);
-                const uint32_t peers = peers_of_bits(kFull, tile, ci.tbits) & m;
-                const uint32_t below = peers & lanemask_lt();
-                const uint32_t pre = in ? pos_w[tile] : 0u;
-                __syncwarp();
-                if (in) {
-                    if (below == 0) pos_w[tile] = pre + __popc(peers);
-                    const uint32_t p = pre + __popc(below);
-                    if (p < a.capacity) a.vals_out[p] = sl;
-                }
-                __syncwarp();
-            });
-            (void)lane;
-        }
-        __syncthreads();
+            __syncwarp();
+        });
     }
 }
 
@@ -458,11 +424,13 @@ void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
     key_hist_kernel<<<grid, kThreads, 0, s>>>(a);
 }
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 1024, 0, s>>>(a); }
-size_t bin_smem_bytes(const BinArgs& a) { return size_t(a.bin_warps) * a.max_tc * sizeof(uint32_t); }
+size_t bin_smem_bytes(const BinArgs& a) {
+    return size_t(a.bin_warps) * ((size_t(a.max_tc) * 5 + 15) & ~size_t(15));
+}
 void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = bin_smem_bytes(a);
     cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    bin_count_kernel<<<grid, kThreads, smem, s>>>(a);
+    bin_count_kernel<<<grid, 32 * a.bin_warps, smem, s>>>(a);
 }
 void launch_bin_colscan(const BinArgs& a, int grid, cudaStream_t s) {
     bin_colscan_kernel<<<grid, kThreads, 0, s>>>(a);
@@ -474,7 +442,7 @@ void launch_bin_campre(const BinArgs& a, cudaStream_t s) { bin_campre_kernel<<<1
 void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = bin_smem_bytes(a);
     cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    bin_scatter_kernel<<<grid, kThreads, smem, s>>>(a);
+    bin_scatter_kernel<<<grid, 32 * a.bin_warps, smem, s>>>(a);
 }
 
 }  // namespace gsim_gpu

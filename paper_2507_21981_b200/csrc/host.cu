@@ -416,7 +416,7 @@ void record_ev(gsim_gpu_context* ctx, int e) {
 void check_launch() { GSIM_CK(cudaGetLastError()); }
 
 int bin_warps_for(uint32_t max_tc) {
-    const size_t per_warp = size_t(max_tc) * sizeof(uint32_t);
+    const size_t per_warp = (size_t(max_tc) * 5 + 15) & ~size_t(15);  // u32 counters + u8 probe
     const size_t budget = 200 * 1024;
     const int w = int(std::min<size_t>(8, budget / std::max<size_t>(per_warp, 1)));
     if (w < 1)
@@ -561,7 +561,8 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
 
     // tile binning: counts, scans, camera bases
     const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + p.cams.size();
-    const int chunk_grid = int(std::max<uint64_t>(1, std::min<uint64_t>(kmax, uint64_t(n_sms) * 6)));
+    // one warp per unit, bin_warps units per block
+    const int chunk_grid = int(std::max<uint64_t>(1, (kmax + b.bin_warps - 1) / b.bin_warps));
     launch_bin_count(b, chunk_grid, s);
     check_launch();
     const uint64_t col_warps = p.tiles;

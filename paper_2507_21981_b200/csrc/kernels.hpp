@@ -12,7 +12,7 @@ namespace gsim_gpu {
 
 constexpr int kMaxSmemSegments = 1024;
 constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
-constexpr int kChunkRecords = 2048;     // depth-sorted records per binning chunk
+constexpr int kChunkRecords = 1024;     // depth-sorted records per binning unit (one warp)
 
 struct PreprocessArgs {
     DevField field;
