@@ -153,6 +153,11 @@ struct gsim_gpu_context {
     int staging_index = 0;
     PinnedBuf readback;
     cudaEvent_t bin_ev = nullptr;
+    // deferred pair-count check of the last asynchronous render (see check_pending)
+    bool pending = false;
+    float* pending_out = nullptr;
+    gsim_raster_options pending_opt{0, 0, 1e-4};
+    int pending_grid = 1;
     // outputs / API scratch
     DevBuf<float> out;
     DevBuf<gsim_projected_splat> full;
@@ -436,8 +441,10 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
         ctx->dk[k].reserve(S);
         ctx->dv[k].reserve(S);
     }
-    if (ctx->fixed_initial_capacity == 0 && ctx->pair_capacity < 4 * S + (1u << 20))
-        ctx->pair_capacity = 4 * S + (1u << 20);
+    // P / S is about 3 for the BASELINE scenes; 8 x slots (4 B each) makes an overflow of an
+    // asynchronous frame practically impossible and costs 32 B per slot of HBM.
+    if (ctx->fixed_initial_capacity == 0 && ctx->pair_capacity < 8 * S + (1u << 20))
+        ctx->pair_capacity = 8 * S + (1u << 20);
     ctx->vals.reserve(std::max<uint64_t>(ctx->pair_capacity, 1));
     const uint64_t words = (S + kOnesweepTile - 1) / kOnesweepTile * 256;
     if (words > ctx->status.cap) {
@@ -519,7 +526,7 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
 
 // K3 + K4 over records/keys/rects already produced for `p` (by K2 or the splat converter).
 void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
-                         float* out, uint64_t& launches) {
+                         float* out, uint64_t& launches, bool wait_for_count) {
     cudaStream_t s = ctx->stream;
     const uint64_t S = p.slots;
     const int n_sms = ctx->num_sms;
@@ -588,6 +595,15 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         launch_raster_stage(ctx, p, opt, out);
         record_ev(ctx, kEvRaster);
         launches += 2;
+        if (!wait_for_count) {
+            // Asynchronous frame: the (V, P) readback is checked by the next call on this
+            // context (check_pending), which re-runs scatter + raster on overflow.
+            ctx->pending = true;
+            ctx->pending_out = out;
+            ctx->pending_opt = opt;
+            ctx->pending_grid = chunk_grid;
+            break;
+        }
         GSIM_CK(cudaEventSynchronize(ctx->bin_ev));
         const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
         ctx->stats.visible = rb[0];
@@ -635,7 +651,8 @@ PreprocessArgs make_pre_args(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
 
 void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
                   uint64_t n_nodes, const gsim_camera* cameras, uint64_t n_cams,
-                  const gsim_raster_options* options, float* device_out, Plan& plan) {
+                  const gsim_raster_options* options, float* device_out, Plan& plan,
+                  bool wait_for_count) {
     plan = build_plan(scene->f.n, nodes, n_nodes, cameras, n_cams);
     gsim_raster_options opt{0, 0, 1e-4};
     if (options) opt = *options;
@@ -651,13 +668,35 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     uint64_t launches = 0;
     PreprocessArgs pa = make_pre_args(ctx, scene, plan);
     if (plan.slots) {
-        launch_preprocess(pa, false, ctx->num_sms * 2, ctx->stream);
+        launch_preprocess(pa, false, ctx->num_sms * 3, ctx->stream);
         check_launch();
         ++launches;
     }
     record_ev(ctx, kEvPre);
-    run_sort_and_raster(ctx, plan, opt, out, launches);
+    run_sort_and_raster(ctx, plan, opt, out, launches, wait_for_count);
     finish_stats(ctx, plan, launches);
+}
+
+// Completes the deferred pair-count check of an asynchronous render: by now its readback has
+// long landed; on overflow the buffers of that frame are still intact (nothing new has been
+// enqueued), so scatter + raster are re-run into the same output before anything else.
+void check_pending(gsim_gpu_context* ctx) {
+    if (!ctx->pending) return;
+    ctx->pending = false;
+    GSIM_CK(cudaEventSynchronize(ctx->bin_ev));
+    const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
+    ctx->stats.visible = rb[0];
+    ctx->stats.pairs = rb[1];
+    if (rb[1] <= ctx->pair_capacity) return;
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->pair_capacity = rb[1] + rb[1] / 4 + (1u << 20);
+    ctx->vals.reserve(ctx->pair_capacity);
+    GSIM_CK(cudaMemsetAsync(ctx->counts.ptr + 2, 0, sizeof(unsigned long long), ctx->stream));
+    BinArgs b = make_bin_args(ctx, ctx->last_plan, ctx->dv[1].ptr);
+    launch_bin_scatter(b, ctx->pending_grid, ctx->stream);
+    check_launch();
+    launch_raster_stage(ctx, ctx->last_plan, ctx->pending_opt, ctx->pending_out);
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
 }
 
 struct Guard {
@@ -669,6 +708,7 @@ struct Guard {
         std::lock_guard<std::mutex> lk(ctx->mu);
         try {
             GSIM_CK(cudaSetDevice(ctx->device));
+            check_pending(ctx);
             f();
             ctx->err.clear();
             return GSIM_OK;
@@ -949,7 +989,7 @@ int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const g
         pa.full = ctx->full.ptr;
         pa.full_visible = ctx->full_vis.ptr;
         if (plan.slots) {
-            launch_preprocess(pa, true, ctx->num_sms * 2, ctx->stream);
+            launch_preprocess(pa, true, ctx->num_sms * 3, ctx->stream);
             check_launch();
             ctx->launches_total += 1;
         }
@@ -1004,7 +1044,7 @@ int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats
             ++launches;
         }
         record_ev(ctx, kEvPre);
-        run_sort_and_raster(ctx, plan, opt, ctx->out.ptr, launches);
+        run_sort_and_raster(ctx, plan, opt, ctx->out.ptr, launches, true);
         finish_stats(ctx, plan, launches);
         const DevCamera& c = plan.cams[0];
         const size_t npx = size_t(c.width) * c.height;
@@ -1025,7 +1065,7 @@ int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
         if (!scene || (n_cameras && !cameras) || (n_nodes && !nodes))
             throw ValidationError{"render: null argument"};
         Plan plan;
-        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, device_out, plan);
+        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, device_out, plan, false);
         ctx->last_plan = std::move(plan);
     });
 }
@@ -1039,7 +1079,7 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
         if (!scene || (n_cameras && (!cameras || !outs)) || (n_nodes && !nodes))
             throw ValidationError{"render: null argument"};
         Plan plan;
-        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, plan);
+        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, plan, true);
         for (uint64_t c = 0; c < n_cameras; ++c) {
             const DevCamera& d = plan.cams[c];
             const size_t npx = size_t(d.width) * d.height;

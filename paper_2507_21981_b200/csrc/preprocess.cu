@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) pose_kernel(DevField f, uint64_t begin, u
 
 // ---- K2: project + shade_sh (raster.cpp:135-232, sh.cpp:10-51) ---------------------------
 template <int DEG, bool kFull>
-__global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args) {
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args) {
     __shared__ uint64_t s_seg_begin[kMaxSmemSegments];
     const DevField f = args.field;
     const int n_seg_smem = args.n_segs < kMaxSmemSegments ? args.n_segs : kMaxSmemSegments;
@@ -159,8 +159,6 @@ __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args)
         const dm3 cov_world = mmul(mmul(r, d), mtransposed(r));
         const double opacity = f.opacity[i];
 
-        ShRegs<DEG> sh;
-        bool sh_loaded = false;
         // View direction in the node frame uses the inverse node rotation (raster.cpp:205-208).
         const float nqw = float(nq.w), nqx = -float(nq.x), nqy = -float(nq.y), nqz = -float(nq.z);
 
@@ -229,10 +227,11 @@ __global__ void __launch_bounds__(256, 2) preprocess_kernel(PreprocessArgs args)
             tx1 = tx1 > cam.tiles_x - 1 ? cam.tiles_x - 1 : tx1;
             ty1 = ty1 > cam.tiles_y - 1 ? cam.tiles_y - 1 : ty1;
 
-            if (!sh_loaded) {
-                sh.load(f.sh, f.n, i);
-                sh_loaded = true;
-            }
+            // Coefficients are (re)loaded per camera: the first camera brings the primitive's
+            // 192 B into L1, later cameras hit it, and the 48 registers are not held across
+            // the camera loop (occupancy).
+            ShRegs<DEG> sh;
+            sh.load(f.sh, f.n, i);
             float vx = float(mean_world.x - cam.center[0]);
             float vy = float(mean_world.y - cam.center[1]);
             float vz = float(mean_world.z - cam.center[2]);

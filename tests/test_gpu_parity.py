@@ -216,6 +216,22 @@ def test_pair_capacity_overflow_regrows(ctx, oracle, monkeypatch):
     for g, w in zip(got, want):
         assert np.array_equal(g.rgb, w.rgb) and np.array_equal(g.depth, w.depth)
         assert np.array_equal(g.accum_alpha, w.accum_alpha)
+    # asynchronous path: the overflow is found by the next call and the frame re-rendered
+    import torch
+    monkeypatch.setenv("GSIM_GPU_INITIAL_PAIR_CAPACITY", "1000")
+    small2 = Context(0)
+    s2 = small2.upload(field)
+    n = sum(5 * c.width * c.height for c in cams)
+    out = torch.zeros(n, dtype=torch.float32, device="cuda:0")
+    small2.render_device(s2, [], cams, None, out.data_ptr())
+    small2.synchronize()
+    flat = out.cpu().numpy()
+    off = 0
+    for c, w in zip(cams, want):
+        npx = c.width * c.height
+        assert np.array_equal(flat[off: off + 3 * npx].reshape(c.height, c.width, 3), w.rgb)
+        assert np.array_equal(flat[off + 3 * npx: off + 4 * npx].reshape(c.height, c.width), w.depth)
+        off += 5 * npx
 
 
 # ---- K1 --------------------------------------------------------------------------------------
