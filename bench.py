@@ -126,15 +126,14 @@ def stage_bytes(stats: dict, n_prims: int, sh_degree: int, pixels: int, n_cams: 
 def run_ours(args, rank, world, local):
     import torch
     from paper_2507_21981_b200 import Context, RenderTarget
-    from paper_2507_21981_b200.scenes import config1, config0, config3
+    from paper_2507_21981_b200.scenes import CONFIGS
 
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    gen = {"cfg1": config1, "cfg0": config0, "cfg3": config3}[args.config]
-    w = gen(seed=1000 + rank)  # each rank renders its own environment
+    w = CONFIGS[args.config](seed=1000 + rank)  # each rank renders its own environment(s)
     # --contexts K: K renderer contexts (each its own stream and workspaces) take frames in
     # turn, so consecutive frames overlap on the GPU.
     ctxs = [Context(local) for _ in range(args.contexts)]
@@ -336,10 +335,9 @@ def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU renderer on this box's host cores."""
     if rank != 0:
         return
-    from paper_2507_21981_b200.scenes import config1, config0, config3
+    from paper_2507_21981_b200.scenes import CONFIGS
     from oracle.oracle import REF_LIB, Oracle, Ref, cpu_count
-    gen = {"cfg1": config1, "cfg0": config0, "cfg3": config3}[args.config]
-    w = gen(seed=1000)
+    w = CONFIGS[args.config](seed=1000)
     cores = cpu_count()
     if REF_LIB.exists():
         ref = Ref()
@@ -388,11 +386,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg0", "cfg1", "cfg3"], default="cfg1")
+    ap.add_argument("--config", choices=["cfg0", "cfg1", "cfg2", "cfg3"], default="cfg1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--contexts", type=int, default=1,
+    ap.add_argument("--contexts", type=int, default=2,
                     help="renderer contexts taking frames in turn (frame-level overlap)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

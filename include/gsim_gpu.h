@@ -136,7 +136,8 @@ typedef struct gsim_render_stats {
     float ms_scatter;      /* pair placement in final (camera, tile, depth) order */
     float ms_raster;       /* K4 */
     float ms_total;
-    float reserved[2];
+    uint32_t groups;       /* camera groups the last batch was split into (32-bit record keys) */
+    float reserved;
 } gsim_render_stats;
 
 typedef struct gsim_gpu_context gsim_gpu_context;

@@ -73,7 +73,7 @@ class gsim_render_stats(C.Structure):
                 ("ms_preprocess", C.c_float), ("ms_depth_sort", C.c_float),
                 ("ms_binning", C.c_float), ("ms_scatter", C.c_float),
                 ("ms_raster", C.c_float), ("ms_total", C.c_float),
-                ("reserved", C.c_float * 2)]
+                ("groups", C.c_uint32), ("reserved", C.c_float)]
 
 
 # numpy view of gsim_projected_splat (ProjectedSplat, raster.hpp:20-29), 120 bytes

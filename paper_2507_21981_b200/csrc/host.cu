@@ -677,6 +677,59 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     finish_stats(ctx, plan, launches);
 }
 
+void check_pending(gsim_gpu_context* ctx);
+
+// A camera batch is rendered in groups whose (camera | depth) record keys fit 32 bits and whose
+// (camera, primitive) slots stay below 2^31: e.g. BASELINE config 2 (320 cameras, near/far
+// 0.05/100 -> 27 depth bits) runs as 10 groups of 32 cameras. Every group re-reads the shared
+// background once (a few microseconds per camera); outputs keep the batch's camera order.
+// Returns the float offset of every camera's block in the output.
+std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                                     const gsim_node* nodes, uint64_t n_nodes,
+                                     const gsim_camera* cameras, uint64_t n_cams,
+                                     const gsim_raster_options* options, float* device_out,
+                                     bool wait_for_count) {
+    std::vector<uint64_t> offsets(n_cams + 1, 0);
+    for (uint64_t c = 0; c < n_cams; ++c) {
+        validate_camera(cameras[c], c);
+        offsets[c + 1] = offsets[c] + uint64_t(5) * cameras[c].width * cameras[c].height;
+    }
+    float* out = device_out;
+    if (!out) {
+        ctx->out.reserve(std::max<uint64_t>(offsets[n_cams], 1));
+        out = ctx->out.ptr;
+    }
+    uint64_t group = n_cams ? n_cams : 1;
+    if (n_cams) {
+        double near_min = cameras[0].near_plane, far_max = cameras[0].far_plane;
+        for (uint64_t c = 1; c < n_cams; ++c) {
+            near_min = std::min(near_min, cameras[c].near_plane);
+            far_max = std::max(far_max, cameras[c].far_plane);
+        }
+        const uint64_t span = uint64_t(float_bits(far_max)) - float_bits(near_min);
+        const int depth_bits = int(ceil_log2_bits(span + 2));
+        group = std::min<uint64_t>(group, uint64_t(1) << (32 - std::min(depth_bits, 32)));
+        const uint64_t n = std::max<uint64_t>(scene->f.n, 1);
+        group = std::max<uint64_t>(1, std::min<uint64_t>(group, (uint64_t(1) << 31) / n));
+    }
+    uint64_t launches = 0, h2d = 0;
+    for (uint64_t c0 = 0; c0 < n_cams || (n_cams == 0 && c0 == 0); c0 += group) {
+        const uint64_t g = n_cams ? std::min(group, n_cams - c0) : 0;
+        if (c0 > 0 && !wait_for_count) check_pending(ctx);
+        Plan plan;
+        render_frame(ctx, scene, nodes, n_nodes, cameras + c0, g, options, out + offsets[c0], plan,
+                     wait_for_count);
+        launches += ctx->stats.launches;
+        h2d += ctx->stats.h2d_bytes;
+        ctx->last_plan = std::move(plan);
+        if (n_cams == 0) break;
+    }
+    ctx->stats.launches = launches;
+    ctx->stats.h2d_bytes = h2d;
+    ctx->stats.groups = uint32_t((n_cams + group - 1) / std::max<uint64_t>(group, 1));
+    return offsets;
+}
+
 // Completes the deferred pair-count check of an asynchronous render: by now its readback has
 // long landed; on overflow the buffers of that frame are still intact (nothing new has been
 // enqueued), so scatter + raster are re-run into the same output before anything else.
@@ -1064,9 +1117,7 @@ int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
     return Guard(ctx).run([&] {
         if (!scene || (n_cameras && !cameras) || (n_nodes && !nodes))
             throw ValidationError{"render: null argument"};
-        Plan plan;
-        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, device_out, plan, false);
-        ctx->last_plan = std::move(plan);
+        render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, device_out, false);
     });
 }
 
@@ -1078,19 +1129,17 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
     return Guard(ctx).run([&] {
         if (!scene || (n_cameras && (!cameras || !outs)) || (n_nodes && !nodes))
             throw ValidationError{"render: null argument"};
-        Plan plan;
-        render_frame(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, plan, true);
+        const std::vector<uint64_t> off =
+            render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, true);
         for (uint64_t c = 0; c < n_cameras; ++c) {
-            const DevCamera& d = plan.cams[c];
-            const size_t npx = size_t(d.width) * d.height;
-            const float* base = ctx->out.ptr + d.out_offset;
+            const size_t npx = size_t(cameras[c].width) * cameras[c].height;
+            const float* base = ctx->out.ptr + off[c];
             GSIM_CK(cudaMemcpyAsync(outs[c].rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
             GSIM_CK(cudaMemcpyAsync(outs[c].depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
             GSIM_CK(cudaMemcpyAsync(outs[c].accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
             ctx->stats.d2h_bytes += 5 * npx * sizeof(float);
         }
         GSIM_CK(cudaStreamSynchronize(ctx->stream));
-        ctx->last_plan = std::move(plan);
     });
 }
 
