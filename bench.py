@@ -147,8 +147,15 @@ def run_ours(args, rank, world, local):
 
     def step(i):
         k = i % len(ctxs)
-        return ctxs[k].render_device(scenes[k], w.frame_nodes(i, seed=rank), w.cameras, None,
-                                     outs[k].data_ptr())
+        ptr = ctxs[k].render_device(scenes[k], w.frame_nodes(i, seed=rank), w.cameras, None,
+                                    outs[k].data_ptr())
+        if args.gather and dist:
+            # BASELINE config 4: the frame (every rank's environment) goes to rank 0 over NCCL
+            from paper_2507_21981_b200.shard import gather_frames
+            torch.cuda.current_stream().wait_stream(streams[k])
+            gather_frames(outs[k], world, outs[k].numel(), dst=0)
+            streams[k].wait_stream(torch.cuda.current_stream())
+        return ptr
 
     for i in range(args.warmup):
         step(i)
@@ -268,7 +275,9 @@ def run_ours(args, rank, world, local):
         "config": {"workload": f"{args.config}: {w.description}", "gaussians": w.field.size(),
                    "sh_degree": w.field.sh_degree, "cameras_per_rank": n_cams,
                    "resolution": f"{w.cameras[0].width}x{w.cameras[0].height}",
-                   "parallelism": f"env-sharded x{world} (replicated background, no data-path collective)",
+                   "parallelism": (f"env-sharded x{world} (replicated background, "
+                                   + ("frames gathered to rank 0 over NCCL each step)" if args.gather and world > 1
+                                      else "no data-path collective)")),
                    "l2": "inputs larger than L2 (scene 300 MB, per-frame working set > 500 MB); no flush",
                    "seed": "1000+rank", "contexts_per_gpu": len(ctxs)},
         "five_camera_frames_per_s": round(value / n_cams, 2),
@@ -392,6 +401,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--contexts", type=int, default=2,
                     help="renderer contexts taking frames in turn (frame-level overlap)")
+    ap.add_argument("--gather", action="store_true",
+                    help="N > 1: gather every step's frames to rank 0 (config 4) inside the timed step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

@@ -68,7 +68,8 @@ def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) 
             sys.stdout.write(res.stderr)
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
+        # static CUDA runtime: the library needs only the driver, whoever loads it
+        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         res = subprocess.run(cmd, capture_output=True, text=True)

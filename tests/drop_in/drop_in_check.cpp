@@ -1,0 +1,110 @@
+// drop_in_check.cpp — one C++ binary that links the UNMODIFIED reference library (oracle/_ref,
+// the checker) and the GPU library through include/gsim_gpu.hpp, and compares them on the same
+// GaussianField with the reference's own types. TEST CODE (built by oracle/Makefile `drop_in`,
+// run by tests/test_gpu_dropin.py on a GPU box).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "gsim/gaussian.hpp"
+#include "gsim/raster.hpp"
+#include "gsim_gpu.hpp"
+#include "test_oracles.hpp"
+
+using namespace gsim;
+
+static double frac_within(const RenderTarget& a, const RenderTarget& b, double rgb_tol,
+                          double depth_rel) {
+    const std::size_t n = a.depth.data.size();
+    std::size_t ok = 0;
+    for (std::size_t p = 0; p < n; ++p) {
+        double d = 0.0;
+        for (int c = 0; c < 3; ++c)
+            d = std::fmax(d, std::fabs(double(a.rgb.data[3 * p + c]) - b.rgb.data[3 * p + c]));
+        const double dd = std::fabs(double(a.depth.data[p]) - b.depth.data[p]);
+        const double rel = dd / std::fmax(std::fabs(double(b.depth.data[p])), 0.1);
+        if (d <= rgb_tol && (rel <= depth_rel || dd <= 1e-4)) ++ok;
+    }
+    return double(ok) / double(n);
+}
+
+int main() {
+    GaussianField field = oracle::random_field(2024, 3000, 3.0, 0.01, 0.2, 3);
+    for (auto& p : field.primitives) p.mean.z += 3.0;
+    std::vector<SceneNode> nodes(2);
+    nodes[0] = {"bg", NodeKind::background, RigidTransform::identity(), {0, 2000}};
+    nodes[1] = {"obj", NodeKind::interactive,
+                RigidTransform{Quat::from_axis_angle({0, 0, 1}, 0.4), {0.1, 0.0, 0.2}}, {2000, 3000}};
+    std::vector<CameraModel> cams(2);
+    for (int k = 0; k < 2; ++k) {
+        cams[k].fx = cams[k].fy = 120.0;
+        cams[k].cx = 80.0;
+        cams[k].cy = 60.0;
+        cams[k].width = 160;
+        cams[k].height = 120;
+        cams[k].pose = RigidTransform{Quat::from_axis_angle({0, 1, 0}, 0.1 * k), {0.2 * k, 0.0, 0.0}};
+    }
+    int failures = 0;
+
+    // render: same signature, reference types
+    const auto ref = render(field, nodes, cams);
+    const auto gpu = gpu::render(field, nodes, cams);
+    for (int k = 0; k < 2; ++k) {
+        const double f = frac_within(gpu[k], ref[k], 2e-3, 1e-3);
+        std::printf("render camera %d: %.5f of pixels within tolerance\n", k, f);
+        if (f < 0.999) ++failures;
+    }
+
+    // project: geometry bit-exact (double), rgb close
+    const auto sp_ref = project(field, nodes, cams[0]);
+    const auto sp_gpu = gpu::project(field, nodes, cams[0]);
+    std::size_t geo_mismatch = sp_ref.size() == sp_gpu.size() ? 0 : 1;
+    double rgb_err = 0.0;
+    for (std::size_t i = 0; i < sp_ref.size() && i < sp_gpu.size(); ++i) {
+        const auto& a = sp_ref[i];
+        const auto& b = sp_gpu[i];
+        if (a.prim_index != b.prim_index || a.pixel_center.x != b.pixel_center.x ||
+            a.pixel_center.y != b.pixel_center.y || a.inv_xx != b.inv_xx || a.inv_xy != b.inv_xy ||
+            a.inv_yy != b.inv_yy || a.view_depth != b.view_depth || a.radius != b.radius)
+            ++geo_mismatch;
+        rgb_err = std::fmax(rgb_err, std::fabs(a.rgb.x - b.rgb.x));
+    }
+    std::printf("project: %zu splats, %zu geometry mismatches, max rgb err %.2e\n", sp_ref.size(),
+                geo_mismatch, rgb_err);
+    if (geo_mismatch || rgb_err > 2e-5) ++failures;
+
+    // rasterize of the reference's own splats
+    const RenderTarget r_ref = rasterize(sp_ref, cams[0]);
+    const RenderTarget r_gpu = gpu::rasterize(sp_ref, cams[0]);
+    const double fr = frac_within(r_gpu, r_ref, 2e-3, 1e-3);
+    std::printf("rasterize: %.5f of pixels within tolerance\n", fr);
+    if (fr < 0.999) ++failures;
+
+    // transform_primitives: bit-exact
+    GaussianField a = field, b = field;
+    const RigidTransform t{Quat::from_axis_angle({1, 2, 3}, 0.7), {0.5, -1.0, 2.0}};
+    transform_primitives(a, {100, 2500}, t);
+    gpu::transform_primitives(b, {100, 2500}, t);
+    std::size_t tf_mismatch = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        const auto& pa = a.primitives[i];
+        const auto& pb = b.primitives[i];
+        if (pa.mean.x != pb.mean.x || pa.mean.y != pb.mean.y || pa.mean.z != pb.mean.z ||
+            pa.rotation.w != pb.rotation.w || pa.rotation.x != pb.rotation.x)
+            ++tf_mismatch;
+    }
+    std::printf("transform_primitives: %zu mismatches\n", tf_mismatch);
+    if (tf_mismatch) ++failures;
+
+    // error mapping: a bad camera is a validation_error from both
+    CameraModel bad = cams[0];
+    bad.fx = 0.0;
+    bool ref_threw = false, gpu_threw = false;
+    try { render(field, nodes, {bad}); } catch (const validation_error&) { ref_threw = true; }
+    try { gpu::render(field, nodes, {bad}); } catch (const validation_error&) { gpu_threw = true; }
+    std::printf("validation_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
+    if (!ref_threw || !gpu_threw) ++failures;
+
+    std::printf(failures ? "DROP-IN FAILED\n" : "DROP-IN OK\n");
+    return failures ? 1 : 0;
+}
