@@ -152,9 +152,60 @@ __device__ __forceinline__ Unit unit_info(const BinArgs& a, uint32_t k) {
 }
 
 // Warp w of the block works in s_bin + w * per_warp_bytes: [max_tc] u32 + [max_tc] u8 probe.
-__device__ __forceinline__ uint32_t* warp_counters(char* s_bin, int max_tc) {
-    const size_t per_warp = (size_t(max_tc) * 5 + 15) & ~size_t(15);
-    return reinterpret_cast<uint32_t*>(s_bin + (threadIdx.x >> 5) * per_warp);
+constexpr int kTab = 512;  // pairs of one 32-record group held in a shared-memory table
+
+__host__ __device__ inline size_t bin_warp_bytes(int max_cells) {
+    return (size_t(max_cells) * 5 + size_t(kTab) * 3 + 15) & ~size_t(15);
+}
+
+// Warp w of the block works in s_bin + w * bin_warp_bytes: [max_cells] u32 counters,
+// [max_cells] u8 probe, [kTab] u16 tile table, [kTab] u8 owner table.
+__device__ __forceinline__ uint32_t* warp_counters(char* s_bin, int max_cells) {
+    return reinterpret_cast<uint32_t*>(s_bin + (threadIdx.x >> 5) * bin_warp_bytes(max_cells));
+}
+
+// Walk records [wb, we) in order, 32 per group (lane = record), loads of kG groups in flight.
+template <class F>
+__device__ __forceinline__ void walk_groups(const BinArgs& a, uint32_t wb, uint32_t we, F&& fn) {
+    constexpr int kG = 4;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t g0 = wb; g0 < we; g0 += 32 * kG) {
+        uint32_t slot[kG], rect[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const uint32_t e = g0 + q * 32 + lane;
+            slot[q] = e < we ? __ldcs(a.sorted_slots + e) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const uint32_t e = g0 + q * 32 + lane;
+            rect[q] = e < we ? __ldg(a.rects + slot[q]) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            if (g0 + q * 32 >= we) break;
+            fn(slot[q], rect[q], g0 + q * 32 + lane < we);
+        }
+    }
+}
+
+// D[cell] += delta for every active lane; lanes that share a cell in the same call are
+// applied in rounds (a shared-memory last-writer probe picks one winner per cell per round).
+__device__ __forceinline__ void add_cells(int* D, uint8_t* probe, uint32_t cell, int delta,
+                                          bool active) {
+    const int lane = threadIdx.x & 31;
+    bool pending = active;
+    while (__any_sync(kFull, pending)) {
+        if (pending) probe[cell] = uint8_t(lane);
+        __syncwarp();
+        const bool win = pending && probe[cell] == uint8_t(lane);
+        __syncwarp();
+        if (win) {
+            D[cell] += delta;
+            pending = false;
+        }
+        __syncwarp();
+    }
 }
 
 }  // namespace
@@ -274,22 +325,47 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinArgs a) {
     extern __shared__ __align__(16) char s_bin[];
     const int lane = threadIdx.x & 31;
     if ((threadIdx.x >> 5) >= a.bin_warps) return;
-    uint32_t* cnt = warp_counters(s_bin, a.max_tc);
-    uint8_t* probe = reinterpret_cast<uint8_t*>(cnt + a.max_tc);
+    // Pairs per tile of a unit without enumerating pairs: every record adds +1 over its tile
+    // rectangle, written as 4 corner updates of a 2-D difference array, then a 2-D prefix sum.
+    int* D = reinterpret_cast<int*>(warp_counters(s_bin, a.max_tc));
+    uint8_t* probe = reinterpret_cast<uint8_t*>(D + a.max_tc);
     const uint32_t K = *a.n_chunks;
     const uint32_t n_warps = gridDim.x * uint32_t(a.bin_warps);
     for (uint32_t k = blockIdx.x * a.bin_warps + (threadIdx.x >> 5); k < K; k += n_warps) {
         const Unit u = unit_info(a, k);
-        for (uint32_t t = lane; t < u.tc; t += 32) cnt[t] = 0;
+        const uint32_t W = uint32_t(u.tiles_x) + 1u, tiles_y = u.tc / uint32_t(u.tiles_x);
+        const uint32_t H = tiles_y + 1u;
+        for (uint32_t t = lane; t < W * H; t += 32) D[t] = 0;
         __syncwarp();
-        walk_records(a, u.rec_begin, u.rec_end, u.tiles_x, [&](bool in, uint32_t tile, uint32_t) {
-            const uint32_t m = __ballot_sync(kFull, in);
-            const uint32_t peers = tile_peers(probe, tile, in, m, u.tbits);
-            if (in && (peers & lanemask_lt()) == 0) cnt[tile] += __popc(peers);
-            __syncwarp();
+        walk_groups(a, u.rec_begin, u.rec_end, [&](uint32_t, uint32_t r, bool valid) {
+            const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u;
+            const uint32_t tx1 = ((r >> 16) & 255u) + 1u, ty1 = (r >> 24) + 1u;
+            add_cells(D, probe, ty0 * W + tx0, 1, valid);
+            add_cells(D, probe, ty0 * W + tx1, -1, valid);
+            add_cells(D, probe, ty1 * W + tx0, -1, valid);
+            add_cells(D, probe, ty1 * W + tx1, 1, valid);
         });
+        for (uint32_t y = lane; y < H; y += 32) {
+            int run = 0;
+            for (uint32_t x = 0; x < W; ++x) {
+                run += D[y * W + x];
+                D[y * W + x] = run;
+            }
+        }
+        __syncwarp();
+        for (uint32_t x = lane; x < W; x += 32) {
+            int run = 0;
+            for (uint32_t y = 0; y < H; ++y) {
+                run += D[y * W + x];
+                D[y * W + x] = run;
+            }
+        }
+        __syncwarp();
         uint32_t* col = a.counts + u.mbase + u.unit_in_cam;
-        for (uint32_t t = lane; t < u.tc; t += 32) col[uint64_t(t) * u.units_in_cam] = cnt[t];
+        for (uint32_t t = lane; t < u.tc; t += 32) {
+            const uint32_t ty = t / uint32_t(u.tiles_x), tx = t - ty * uint32_t(u.tiles_x);
+            col[uint64_t(t) * u.units_in_cam] = uint32_t(D[ty * W + tx]);
+        }
         __syncwarp();
     }
 }
@@ -393,6 +469,8 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     if ((threadIdx.x >> 5) >= a.bin_warps) return;
     uint32_t* pos = warp_counters(s_bin, a.max_tc);
     uint8_t* probe = reinterpret_cast<uint8_t*>(pos + a.max_tc);
+    uint16_t* tab_tile = reinterpret_cast<uint16_t*>(probe + ((a.max_tc + 1) & ~1));
+    uint8_t* tab_own = reinterpret_cast<uint8_t*>(tab_tile + kTab);
     const uint32_t K = *a.n_chunks;
     const uint32_t n_warps = gridDim.x * uint32_t(a.bin_warps);
     for (uint32_t k = blockIdx.x * a.bin_warps + (threadIdx.x >> 5); k < K; k += n_warps) {
@@ -403,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         for (uint32_t t = lane; t < u.tc; t += 32)
             pos[t] = pbase + a.tile_rel[u.tile_base + t] + col[uint64_t(t) * u.units_in_cam];
         __syncwarp();
-        walk_records(a, u.rec_begin, u.rec_end, u.tiles_x, [&](bool in, uint32_t tile, uint32_t sl) {
+        auto place = [&](bool in, uint32_t tile, uint32_t sl) {
             const uint32_t m = __ballot_sync(kFull, in);
             const uint32_t peers = tile_peers(probe, tile, in, m, u.tbits);
             const uint32_t below = peers & lanemask_lt();
@@ -415,6 +493,39 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                 if (p < a.capacity) a.vals_out[p] = sl;
             }
             __syncwarp();
+        };
+        walk_groups(a, u.rec_begin, u.rec_end, [&](uint32_t slot, uint32_t r, bool valid) {
+            // exclusive offsets of the group's pairs in emission order
+            const uint32_t cnt = valid ? rect_area(r) : 0u;
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t total = __shfl_sync(kFull, incl, 31);
+            if (total > uint32_t(kTab)) {  // rare: huge splats; enumerate with the owner search
+                for_each_pair(slot, r, valid, u.tiles_x, place);
+                return;
+            }
+            // each lane writes its record's tiles (row-major) and its lane id into the tables
+            const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u, ty1 = r >> 24;
+            uint32_t k = incl - cnt;
+            if (valid)
+                for (uint32_t ty = ty0; ty <= ty1; ++ty)
+                    for (uint32_t tx = tx0; tx <= tx1; ++tx, ++k) {
+                        tab_tile[k] = uint16_t(ty * uint32_t(u.tiles_x) + tx);
+                        tab_own[k] = uint8_t(lane);
+                    }
+            __syncwarp();
+            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+                const uint32_t j = k0 + lane;
+                const bool in = j < total;
+                const uint32_t tile = in ? tab_tile[j] : 0u;
+                const uint32_t own = in ? tab_own[j] : 0u;
+                const uint32_t sl = __shfl_sync(kFull, slot, own);
+                place(in, tile, sl);
+            }
         });
     }
 }
@@ -424,9 +535,7 @@ void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
     key_hist_kernel<<<grid, kThreads, 0, s>>>(a);
 }
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 1024, 0, s>>>(a); }
-size_t bin_smem_bytes(const BinArgs& a) {
-    return size_t(a.bin_warps) * ((size_t(a.max_tc) * 5 + 15) & ~size_t(15));
-}
+size_t bin_smem_bytes(const BinArgs& a) { return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc); }
 void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = bin_smem_bytes(a);
     cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

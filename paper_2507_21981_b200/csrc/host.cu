@@ -253,7 +253,9 @@ void finish_cameras(Plan& p, const gsim_camera* cameras, uint64_t n_cams) {
         out_off += uint64_t(5) * d.width * d.height;
         const uint32_t tc = uint32_t(d.tiles_x * d.tiles_y);
         p.tile_base[c + 1] = p.tile_base[c] + tc;
-        p.max_tc = std::max(p.max_tc, tc);
+        // binning works on a (tiles_x + 1) x (tiles_y + 1) difference grid per camera
+        p.max_tc = std::max(p.max_tc, uint32_t((d.tiles_x + 1) * (d.tiles_y + 1)));
+        (void)tc;
         p.tiles_x.push_back(d.tiles_x);
         p.cams.push_back(d);
     }
@@ -421,7 +423,8 @@ void record_ev(gsim_gpu_context* ctx, int e) {
 void check_launch() { GSIM_CK(cudaGetLastError()); }
 
 int bin_warps_for(uint32_t max_tc) {
-    const size_t per_warp = (size_t(max_tc) * 5 + 15) & ~size_t(15);  // u32 counters + u8 probe
+    // u32 counters + u8 probe per grid cell, u16 + u8 table of 512 pairs (bin.cu bin_warp_bytes)
+    const size_t per_warp = (size_t(max_tc) * 5 + 512 * 3 + 15) & ~size_t(15);
     const size_t budget = 200 * 1024;
     const int w = int(std::min<size_t>(8, budget / std::max<size_t>(per_warp, 1)));
     if (w < 1)
