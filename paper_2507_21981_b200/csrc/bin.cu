@@ -232,11 +232,13 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
             const uint32_t key = keys[i];
             const bool valid = key != kInvalidKey;
             const uint32_t vmask = __ballot_sync(kFull, valid);
+            if (a.hist) {  // digit histograms (only the onesweep variant needs them)
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const uint32_t d = (key >> (8 * p)) & 255u;
-                const uint32_t peers = peers_of<8>(kFull, d) & vmask;
-                if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][p][d] += __popc(peers);
+                for (int p = 0; p < 4; ++p) {
+                    const uint32_t d = (key >> (8 * p)) & 255u;
+                    const uint32_t peers = peers_of<8>(kFull, d) & vmask;
+                    if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][p][d] += __popc(peers);
+                }
             }
             // per-camera counts: one round per distinct camera in the group (usually one)
             const uint32_t cam = key_camera(key, a.depth_bits);
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
         uint32_t s = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
-        if (s) atomicAdd(a.hist + k, s);
+        if (s && a.hist) atomicAdd(a.hist + k, s);
     }
 }
 

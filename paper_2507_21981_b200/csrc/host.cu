@@ -126,6 +126,9 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> rects;
     DevBuf<uint32_t> dk[2], dv[2];   // depth-sort ping-pong
     DevBuf<uint64_t> status;         // onesweep lookback words
+    DevBuf<uint32_t> radix_counts;   // [256][chunks] per-chunk digit counts (reduce-then-scan)
+    DevBuf<uint32_t> radix_totals;   // [256]
+    bool use_onesweep = false;       // GSIM_GPU_ONESWEEP=1: decoupled look-back passes instead
     // per-pair plane (final per-tile order)
     DevBuf<uint32_t> vals;
     uint64_t pair_capacity = 0;
@@ -536,12 +539,44 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
 
     // key histograms + per-camera counts, then the chunk table (needs only the counts)
     BinArgs b = make_bin_args(ctx, p, ctx->dv[1].ptr);
+    if (!ctx->use_onesweep) b.hist = nullptr;  // the reduce-then-scan passes count their own digits
     launch_key_hist(b, n_sms * 4, s);
+    b.hist = ctx->zero_block.ptr + kZeroHist;
     check_launch();
     launch_chunk_table(b, s);
     check_launch();
     launches += 2;
 
+    if (!ctx->use_onesweep) {
+        // 4 reduce-then-scan LSD passes over (camera | depth) keys; pass 1 drops culled slots.
+        const uint32_t max_chunks = uint32_t(std::max<uint64_t>(1, (S + kOnesweepTile - 1) / kOnesweepTile));
+        ctx->radix_counts.reserve(uint64_t(256) * max_chunks);
+        ctx->radix_totals.reserve(256);
+        const uint32_t* kin = ctx->keys.ptr;
+        const uint32_t* vin = nullptr;
+        for (int pass = 0; pass < 4; ++pass) {
+            const int o = pass & 1;
+            RadixArgs ra{};
+            ra.keys_in = kin;
+            ra.vals_in = vin;
+            ra.keys_out = ctx->dk[o].ptr;
+            ra.vals_out = ctx->dv[o].ptr;
+            ra.n_dev = ctx->counts.ptr + 0;
+            ra.n_host = S;
+            ra.counts = ctx->radix_counts.ptr;
+            ra.totals = ctx->radix_totals.ptr;
+            ra.max_chunks = max_chunks;
+            ra.shift = 8 * pass;
+            ra.first = pass == 0;
+            ra.write_keys = pass < 3;
+            launch_radix_pass(ra, s);
+            check_launch();
+            launches += 3;
+            kin = ctx->dk[o].ptr;
+            vin = ctx->dv[o].ptr;
+        }
+        record_ev(ctx, kEvDepth);
+    } else {
     // 4 onesweep passes over (camera | depth) keys; pass 1 compacts the culled slots away.
     OnesweepArgs oa{};
     oa.n_dev = ctx->counts.ptr + 0;
@@ -568,6 +603,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         vin = ctx->dv[o].ptr;
     }
     record_ev(ctx, kEvDepth);
+    }
 
     // tile binning: counts, scans, camera bases
     const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + p.cams.size();
@@ -809,6 +845,7 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         ctx->zero_block.reserve(kZeroCams + 64);
         ctx->counts.reserve(4);
         ctx->readback.reserve(64);
+        if (const char* e = std::getenv("GSIM_GPU_ONESWEEP")) ctx->use_onesweep = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_INITIAL_PAIR_CAPACITY")) {
             ctx->fixed_initial_capacity = std::strtoull(e, nullptr, 10);
             ctx->pair_capacity = ctx->fixed_initial_capacity;
@@ -839,6 +876,8 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
         ctx->staging[k].release();
     }
     ctx->status.release();
+    ctx->radix_counts.release();
+    ctx->radix_totals.release();
     ctx->vals.release();
     ctx->zero_block.release();
     ctx->counts.release();

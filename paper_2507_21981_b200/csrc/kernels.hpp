@@ -55,6 +55,23 @@ struct OnesweepArgs {
     int shift;
 };
 
+// One reduce-then-scan LSD pass (sort.cu): upsweep counts per (digit, chunk), a per-digit scan
+// over chunks, then a downsweep that ranks and scatters. No decoupled look-back.
+struct RadixArgs {
+    const uint32_t* keys_in;
+    const uint32_t* vals_in;         // nullptr on the first pass: value = input index
+    uint32_t* keys_out;
+    uint32_t* vals_out;
+    const unsigned long long* n_dev; // element count on device (first pass: n_host)
+    uint64_t n_host;
+    uint32_t* counts;                // [256][max_chunks] digit-major per-chunk counts -> prefixes
+    uint32_t* totals;                // [256] digit totals of the pass
+    uint32_t max_chunks;
+    int shift;
+    int first;                       // input is the per-slot key plane (drop kInvalidKey)
+    int write_keys;
+};
+
 // Tile binning of the camera-major depth-sorted records (bin.cu).
 struct BinArgs {
     const uint32_t* keys;            // [S] packed keys (key_hist)
@@ -110,6 +127,7 @@ void launch_preprocess(const PreprocessArgs& a, bool full, int grid_cap, cudaStr
 void launch_splats_to_records(const SplatArgs& a, int grid_cap, cudaStream_t stream);
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream);
+void launch_radix_pass(const RadixArgs& a, cudaStream_t stream);
 void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s);
 void launch_chunk_table(const BinArgs& a, cudaStream_t s);
 size_t bin_smem_bytes(const BinArgs& a);
