@@ -112,11 +112,10 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
             const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
             const uint32_t peers = peers_of<8>(0xffffffffu, d) & vmask;
             const uint32_t below = peers & lanemask_lt();
+            const int leader = peers ? __ffs(peers) - 1 : lane;
             uint32_t pre = 0;
-            if (valid) pre = s_warp_hist[warp][d];
-            __syncwarp();
-            if (valid && below == 0) s_warp_hist[warp][d] = pre + __popc(peers);
-            __syncwarp();
+            if (valid && below == 0) pre = atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
+            pre = __shfl_sync(0xffffffffu, pre, leader);
             rank[i] = valid ? (pre + __popc(below)) : 0xFFFFFFFFu;
         }
         __syncthreads();
@@ -216,8 +215,7 @@ __global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(RadixArgs a) {
         const bool valid = (valid_bits >> i) & 1u;
         const uint32_t d = (keys[i] >> a.shift) & 255u;
         const uint32_t peers = peers_of<8>(0xffffffffu, d) & __ballot_sync(0xffffffffu, valid);
-        if (valid && (peers & lanemask_lt()) == 0) s_warp_hist[warp][d] += __popc(peers);
-        __syncwarp();
+        if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
     }
     __syncthreads();
     uint32_t s = 0;
@@ -283,17 +281,21 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(RadixArgs 
     uint32_t keys[kItems], vals[kItems], rank[kItems], valid_bits;
     radix_load(a, n, uint64_t(c) * kOnesweepTile, keys, vals, valid_bits, true);
     __syncthreads();
-    // warp-level stable ranking: item order (i, lane) = memory order
+    // Warp-level stable ranking, item order (i, lane) = memory order. The lowest lane of each
+    // digit group bumps the warp's counter with an atomic that returns the running count; the
+    // atomics of consecutive items are ordered by the hardware, so no item waits on another
+    // in registers and the 16 items pipeline (shared atomics are cheap on this part, measured
+    // in tools/microbench.cu; match.any is not).
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const bool valid = (valid_bits >> i) & 1u;
         const uint32_t d = (keys[i] >> a.shift) & 255u;
         const uint32_t peers = peers_of<8>(0xffffffffu, d) & __ballot_sync(0xffffffffu, valid);
         const uint32_t below = peers & lanemask_lt();
-        const uint32_t pre = valid ? s_warp_hist[warp][d] : 0u;
-        __syncwarp();
-        if (valid && below == 0) s_warp_hist[warp][d] = pre + __popc(peers);
-        __syncwarp();
+        const int leader = peers ? __ffs(peers) - 1 : lane;
+        uint32_t pre = 0;
+        if (valid && below == 0) pre = atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
+        pre = __shfl_sync(0xffffffffu, pre, leader);
         rank[i] = pre + __popc(below);
     }
     __syncthreads();
