@@ -128,7 +128,7 @@ struct gsim_gpu_context {
     DevBuf<uint64_t> status;         // onesweep lookback words
     DevBuf<uint32_t> radix_counts;   // [256][chunks] per-chunk digit counts (reduce-then-scan)
     DevBuf<uint32_t> radix_totals;   // [256]
-    bool use_onesweep = false;       // GSIM_GPU_ONESWEEP=1: decoupled look-back passes instead
+    bool use_onesweep = true;        // GSIM_GPU_ONESWEEP=0: reduce-then-scan passes instead
     // per-pair plane (final per-tile order)
     DevBuf<uint32_t> vals;
     uint64_t pair_capacity = 0;

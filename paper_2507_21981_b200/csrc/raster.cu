@@ -11,8 +11,9 @@
 //   3. each warp walks its list with a branch-free blend: a splat that fails the box test or
 //      the 1/255 skip gets alpha 0, which leaves C, D, A and T bit-for-bit unchanged, so the
 //      result equals the reference's skip-with-continue loop;
-//   4. a warp stops when all its pixels are saturated; the CTA leaves when
-//      __syncthreads_count says every pixel is done.
+//   4. a pixel that saturates (T < cutoff after accumulating) parks at T = 0, so later
+//      weights are exactly zero; a warp stops when all its pixels are parked and the CTA
+//      leaves when __syncthreads_count says every pixel is.
 //
 // Per-pixel contract (raster.cpp:284-318): box test |dx|>r || |dy|>r, q with 2*inv_xy,
 // alpha = min(o*exp(-q/2), 0.99), skip alpha < 1/255, accumulate, T *= 1-alpha, stop after
@@ -31,23 +32,14 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kBatch = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 
+// The conic is stored prescaled by -log2(e)/2 so the exponent of ex2 is
+// lop + dx*(A*dx + B*dy) + C*dy*dy: five FP32 ops per pixel and splat.
 struct alignas(16) SmemSplat {
     float4 p0;  // u, v, radius, log2(opacity)
-    float4 p1;  // inv_xx, 2*inv_xy, inv_yy, depth
+    float4 p1;  // A = -inv_xx*log2e/2, B = -inv_xy*log2e, C = -inv_yy*log2e/2, depth
     float4 p2;  // r, g, b, -
 };
 
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds8(uint32_t addr) {
-    uint16_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
-    return v;
-}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -58,7 +50,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
     __shared__ SmemSplat s_spl[kBatch];
     __shared__ uint8_t s_mask[kBatch];
-    __shared__ uint8_t s_list[kWarps][kBatch];
+    __shared__ uint16_t s_list[kWarps][kBatch];
 
     const uint32_t g = blockIdx.x;
     const int cam_idx = upper_index(a.cam_tile_base, a.n_cams, g);
@@ -80,11 +72,7 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
     const uint32_t end = uint32_t(e64 < a.capacity ? e64 : a.capacity);
     const float cutoff = a.cutoff;
     float cr = 0.f, cg = 0.f, cb = 0.f, d = 0.f, acc = 0.f, T = 1.f;
-    bool done = false;
 
-    const uint32_t spl_base = uint32_t(__cvta_generic_to_shared(&s_spl[0]));
-    const uint32_t mask_base = uint32_t(__cvta_generic_to_shared(&s_mask[0]));
-    const uint32_t list_base = uint32_t(__cvta_generic_to_shared(&s_list[warp][0]));
     // Pixel-centre bounds of the 2 warp columns and 4 warp rows of this tile.
     const float tile_x0 = float(tx * kTileSize) + 0.5f, tile_y0 = float(ty * kTileSize) + 0.5f;
 
@@ -102,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
             const float u = ra.x, v = ra.y, rad = ra.w, op = rb.w;
             const float ia = rb.x, ib = rb.y, ic = rb.z;
             s_spl[tid].p0 = make_float4(u, v, rad, __log2f(op));
-            s_spl[tid].p1 = make_float4(ia, 2.0f * ib, ic, ra.z);
+            s_spl[tid].p1 = make_float4(ia * (-0.5f * kLog2e), ib * -kLog2e, ic * (-0.5f * kLog2e), ra.z);
             s_spl[tid].p2 = make_float4(rc.x, rc.y, rc.z, 0.f);
             // Reachable half-extents: the box test bounds |dx|,|dy| <= r; alpha >= 1/255 needs
             // q <= qc = 2 ln(255 o), whose ellipse has half-extents sqrt(qc * cov_xx/yy).
@@ -142,45 +130,46 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
         s_mask[tid] = uint8_t(mask);
         __syncthreads();
 
-        if (!__all_sync(0xffffffffu, done)) {
-            // Compact this warp's splats (depth order preserved).
+        if (!__all_sync(0xffffffffu, T == 0.0f)) {
+            // Compact this warp's splats (depth order preserved) as byte offsets into s_spl.
             uint32_t count = 0;
             for (uint32_t j = 0; j < n_b; j += 32) {
                 const uint32_t idx = j + lane;
-                const bool mine = idx < n_b && ((lds8(mask_base + idx) >> warp) & 1u);
+                const bool mine = idx < n_b && ((s_mask[idx] >> warp) & 1u);
                 const uint32_t bits = __ballot_sync(0xffffffffu, mine);
-                if (mine) s_list[warp][count + __popc(bits & lanemask_lt())] = uint8_t(idx);
+                if (mine)
+                    s_list[warp][count + __popc(bits & lanemask_lt())] =
+                        uint16_t(idx * sizeof(SmemSplat));
                 count += __popc(bits);
             }
             __syncwarp();
+            const char* spl = reinterpret_cast<const char*>(s_spl);
             for (uint32_t k0 = 0; k0 < count; k0 += 32) {
                 const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
-#pragma unroll 2
+#pragma unroll 4
                 for (uint32_t k = k0; k < k1; ++k) {
-                    const uint32_t s = lds8(list_base + k);
-                    const uint32_t sa = spl_base + s * uint32_t(sizeof(SmemSplat));
-                    const float4 p0 = lds128(sa);
-                    const float4 p1 = lds128(sa + 16);
-                    const float4 p2 = lds128(sa + 32);
+                    const SmemSplat& sp = *reinterpret_cast<const SmemSplat*>(spl + s_list[warp][k]);
+                    const float4 p0 = sp.p0, p1 = sp.p1, p2 = sp.p2;
                     const float dx = p0.x - px, dy = p0.y - py;
-                    const float q = p1.x * dx * dx + p1.y * dx * dy + p1.z * dy * dy;
-                    const float e = fminf(ex2_approx(fmaf(q, -0.5f * kLog2e, p0.w)), 0.99f);
-                    const bool ok = !done && fmaxf(fabsf(dx), fabsf(dy)) <= p0.z &&
-                                    e >= float(kAlphaSkip);
-                    const float alpha = ok ? e : 0.0f;
-                    const float w = alpha * T;
+                    const float t = fmaf(p1.y, dy, p1.x * dx);
+                    const float E = fmaf(p1.z * dy, dy, fmaf(t, dx, p0.w));
+                    const float e = fminf(ex2_approx(E), 0.99f);
+                    const bool ok = fmaxf(fabsf(dx), fabsf(dy)) <= p0.z && e >= float(kAlphaSkip);
+                    const float w = (ok ? e : 0.0f) * T;
                     cr = fmaf(p2.x, w, cr);
                     cg = fmaf(p2.y, w, cg);
                     cb = fmaf(p2.z, w, cb);
                     d = fmaf(p1.w, w, d);
                     acc += w;
-                    T *= 1.0f - alpha;
-                    done = done || (ok && T < cutoff);
+                    // T * (1 - alpha) == T - w up to rounding; a saturated pixel parks at T = 0,
+                    // where every later weight is exactly zero (the reference's break).
+                    const float Tn = T - w;
+                    T = (ok && Tn < cutoff) ? 0.0f : Tn;
                 }
-                if (__all_sync(0xffffffffu, done)) break;
+                if (__all_sync(0xffffffffu, T == 0.0f)) break;
             }
         }
-        if (__syncthreads_count(done ? 0 : 1) == 0) break;
+        if (__syncthreads_count(T == 0.0f ? 0 : 1) == 0) break;
     }
 
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
