@@ -203,6 +203,58 @@ float* gsim_gpu_device_output(gsim_gpu_context* ctx);
 int gsim_gpu_tile_lists(gsim_gpu_context* ctx, uint32_t camera, uint32_t* tile_begin,
                         uint32_t* values, uint64_t capacity, uint64_t* count);
 
+/* ---- Output encoding: the byte images the reference's writers produce ----
+ * image_io.cpp:75-86  write_png_rgb8  -> GSIM_ENCODE_RGB8    interleaved RGB u8, rows top-down,
+ *                     value quantize8(srgb ? linear_to_srgb(v) : clamp(v, 0, 1)) (:19-22, :43-45)
+ * image_io.cpp:88-97  write_png_gray8 -> GSIM_ENCODE_ALPHA8  accum_alpha as u8, quantize8(clamp)
+ * image_io.cpp:99-111 write_png_gray16-> GSIM_ENCODE_DEPTH16 depth as big-endian u16 of
+ *                     clamp(lround(depth * depth_scale), 0, 65535)  (scale 1000: metres -> mm)
+ * image_io.cpp:166-178 write_pfm      -> GSIM_ENCODE_DEPTH_PFM f32 depth rows bottom-up (the PFM
+ *                     body; the "Pf\n%d %d\n-1.0\n" header is the caller's)
+ * The per-camera block is the enabled parts in that order (RGB8, ALPHA8, DEPTH16, DEPTH_PFM),
+ * packed; cameras follow each other. The bytes are those the reference hands to libpng / fwrite
+ * for the same float images, bit for bit (tools/gsim.cpp:57-66 is the caller being replaced). */
+#define GSIM_ENCODE_RGB8 1u
+#define GSIM_ENCODE_ALPHA8 2u
+#define GSIM_ENCODE_DEPTH16 4u
+#define GSIM_ENCODE_DEPTH_PFM 8u
+
+typedef struct gsim_encode_options {
+    uint32_t flags;      /* GSIM_ENCODE_* bits */
+    int32_t srgb;        /* write_png_rgb8's srgb_encode (tools/gsim.cpp:60 passes true) */
+    double depth_scale;  /* write_png_gray16's scale (tools/gsim.cpp:64 passes 1000.0) */
+} gsim_encode_options;
+
+/* Encoded bytes of one width x height camera under `flags` (0 for unknown bits). */
+uint64_t gsim_gpu_encoded_bytes(uint32_t flags, int32_t width, int32_t height);
+
+/* The 256 sRGB code thresholds the kernels use: thresholds[k] is the smallest float v with
+ * quantize8(linear_to_srgb(v)) >= k (thresholds[0] = -inf). Built on the host from the
+ * reference's transfer function; needs no GPU (test hook). */
+void gsim_gpu_srgb_thresholds(float* thresholds);
+
+/* Encode one host RenderTarget (rgb H*W*3, depth H*W, accum_alpha H*W floats) into `out`
+ * (host, gsim_gpu_encoded_bytes(flags, width, height) bytes). Unused planes may be NULL. */
+int gsim_gpu_encode_host(gsim_gpu_context* ctx, int32_t width, int32_t height, const float* rgb,
+                         const float* depth, const float* accum_alpha,
+                         const gsim_encode_options* options, uint8_t* out);
+
+/* Encode render_device output (device, per camera [rgb|depth|alpha] f32) of `cameras` into
+ * `out` (device pointer if out_is_device, else host; synchronous for host). */
+int gsim_gpu_encode(gsim_gpu_context* ctx, const float* device_targets, const gsim_camera* cameras,
+                    uint64_t n_cameras, const gsim_encode_options* options, uint8_t* out,
+                    int32_t out_is_device);
+
+/* render + encode fused in the compositing kernel's epilogue: the float images never reach
+ * HBM and only the encoded bytes cross to the host (6-11 B per pixel instead of 20).
+ * out_is_device selects a device (asynchronous, like render_device) or host (synchronous)
+ * destination. */
+int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                            const gsim_node* nodes, uint64_t n_nodes, const gsim_camera* cameras,
+                            uint64_t n_cameras, const gsim_raster_options* raster_options,
+                            const gsim_encode_options* options, uint8_t* out,
+                            int32_t out_is_device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -674,3 +674,127 @@ uint64_t gso_hash_target(const float* rgb, const float* depth, const float* alph
     h = hash_image(depth, width, height, 1, h);
     return hash_image(alpha, width, height, 1, h);
 }
+
+/* ---- output encoding ------------------------------------------------------------------------ */
+
+double gso_linear_to_srgb(double v) { /* image_io.cpp:19-22 */
+    v = clampd(v, 0.0, 1.0);
+    return v <= 0.0031308 ? 12.92 * v : 1.055 * pow(v, 1.0 / 2.4) - 0.055;
+}
+
+static uint8_t quantize8(double v) { /* image_io.cpp:43-45 */
+    const long r = lround(v * 255.0);
+    return (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
+}
+
+uint64_t gso_encoded_bytes(uint32_t flags, int width, int height) {
+    const uint64_t bpp = ((flags & GSIM_ENCODE_RGB8) ? 3u : 0u) + ((flags & GSIM_ENCODE_ALPHA8) ? 1u : 0u) +
+                         ((flags & GSIM_ENCODE_DEPTH16) ? 2u : 0u) + ((flags & GSIM_ENCODE_DEPTH_PFM) ? 4u : 0u);
+    return bpp * (uint64_t)width * (uint64_t)height;
+}
+
+int gso_encode(uint32_t flags, int srgb, double depth_scale, int width, int height,
+               const float* rgb, const float* depth, const float* alpha, uint8_t* out) {
+    if (width <= 0 || height <= 0) return GSIM_ERR_VALIDATION; /* "empty image" */
+    const size_t npx = (size_t)width * (size_t)height;
+    uint8_t* part = out;
+    if (flags & GSIM_ENCODE_RGB8) { /* write_png_rgb8, image_io.cpp:75-86 */
+        for (size_t i = 0; i < 3 * npx; ++i) {
+            const double v = rgb[i];
+            part[i] = quantize8(srgb ? gso_linear_to_srgb(v) : clampd(v, 0.0, 1.0));
+        }
+        part += 3 * npx;
+    }
+    if (flags & GSIM_ENCODE_ALPHA8) { /* write_png_gray8, image_io.cpp:88-97 */
+        for (size_t i = 0; i < npx; ++i) part[i] = quantize8(clampd((double)alpha[i], 0.0, 1.0));
+        part += npx;
+    }
+    if (flags & GSIM_ENCODE_DEPTH16) { /* write_png_gray16, image_io.cpp:99-111 */
+        for (size_t i = 0; i < npx; ++i) {
+            long v = lround(depth[i] * depth_scale);
+            v = v < 0 ? 0 : (v > 65535 ? 65535 : v);
+            part[2 * i] = (uint8_t)(v >> 8);
+            part[2 * i + 1] = (uint8_t)(v & 0xff);
+        }
+        part += 2 * npx;
+    }
+    if (flags & GSIM_ENCODE_DEPTH_PFM) { /* write_pfm body, image_io.cpp:166-178 */
+        for (int y = height - 1, r = 0; y >= 0; --y, ++r)
+            memcpy(part + (size_t)r * width * 4, depth + (size_t)y * width, (size_t)width * 4);
+    }
+    return GSIM_OK;
+}
+
+/* ---- pose playback -------------------------------------------------------------------------- */
+
+static quat slerp_q(quat a, quat b, double t) { /* math.hpp:195-214 */
+    double cos_half = a.w * b.w + a.x * b.x + a.y * b.y + a.z * b.z;
+    if (cos_half < 0.0) {
+        b = q_make(-b.w, -b.x, -b.y, -b.z);
+        cos_half = -cos_half;
+    }
+    if (cos_half > 1.0 - 1e-12) {
+        const quat q = q_make(a.w + t * (b.w - a.w), a.x + t * (b.x - a.x), a.y + t * (b.y - a.y),
+                              a.z + t * (b.z - a.z));
+        return q_normalized(q);
+    }
+    const double half = acos(cos_half);
+    const double s = sin(half);
+    const double wa = sin((1.0 - t) * half) / s;
+    const double wb = sin(t * half) / s;
+    const quat q = q_make(wa * a.w + wb * b.w, wa * a.x + wb * b.x, wa * a.y + wb * b.y,
+                          wa * a.z + wb * b.z);
+    return q_normalized(q);
+}
+
+void gso_slerp(const double a[4], const double b[4], double t, double out[4]) {
+    const quat q = slerp_q(q_make(a[0], a[1], a[2], a[3]), q_make(b[0], b[1], b[2], b[3]), t);
+    out[0] = q.w;
+    out[1] = q.x;
+    out[2] = q.y;
+    out[3] = q.z;
+}
+
+int gso_pose_sample(const double* rec_t, const double* rec_p, const double* rec_q, uint64_t n_rec,
+                    const gsim_rigid* initial, const double* ts, uint64_t n_t, gsim_rigid* out) {
+    /* PoseStream::append (pose_stream.cpp:31-40): finite checks, non-decreasing times,
+     * rotation normalised on append. */
+    for (uint64_t i = 0; i < n_rec; ++i) {
+        if (!isfinite(rec_t[i])) return GSIM_ERR_VALIDATION;
+        for (int k = 0; k < 3; ++k) if (!isfinite(rec_p[3 * i + k])) return GSIM_ERR_VALIDATION;
+        for (int k = 0; k < 4; ++k) if (!isfinite(rec_q[4 * i + k])) return GSIM_ERR_VALIDATION;
+        if (i && rec_t[i] < rec_t[i - 1]) return GSIM_ERR_VALIDATION;
+    }
+    for (uint64_t k = 0; k < n_t; ++k) { /* PoseStream::sample, pose_stream.cpp:117-136 */
+        const double t = ts[k];
+        gsim_rigid* o = &out[k];
+        if (n_rec == 0 || t < rec_t[0]) { *o = *initial; continue; }
+        const uint64_t last = n_rec - 1;
+        const quat ql = q_normalized(q_make(rec_q[4 * last], rec_q[4 * last + 1], rec_q[4 * last + 2],
+                                            rec_q[4 * last + 3]));
+        if (t >= rec_t[last]) {
+            o->rotation[0] = ql.w; o->rotation[1] = ql.x; o->rotation[2] = ql.y; o->rotation[3] = ql.z;
+            for (int c = 0; c < 3; ++c) o->translation[c] = rec_p[3 * last + c];
+            continue;
+        }
+        uint64_t lo_i = 0, hi_i = n_rec; /* first record with time > t (upper_bound) */
+        while (lo_i < hi_i) {
+            const uint64_t mid = lo_i + (hi_i - lo_i) / 2;
+            if (t < rec_t[mid]) hi_i = mid; else lo_i = mid + 1;
+        }
+        const uint64_t hi = lo_i, lo = hi - 1;
+        const quat qh = q_normalized(q_make(rec_q[4 * hi], rec_q[4 * hi + 1], rec_q[4 * hi + 2], rec_q[4 * hi + 3]));
+        const double span = rec_t[hi] - rec_t[lo];
+        if (span <= 0.0) {
+            o->rotation[0] = qh.w; o->rotation[1] = qh.x; o->rotation[2] = qh.y; o->rotation[3] = qh.z;
+            for (int c = 0; c < 3; ++c) o->translation[c] = rec_p[3 * hi + c];
+            continue;
+        }
+        const double u = (t - rec_t[lo]) / span;
+        for (int c = 0; c < 3; ++c) o->translation[c] = rec_p[3 * lo + c] * (1.0 - u) + rec_p[3 * hi + c] * u;
+        const quat qlo = q_normalized(q_make(rec_q[4 * lo], rec_q[4 * lo + 1], rec_q[4 * lo + 2], rec_q[4 * lo + 3]));
+        const quat q = slerp_q(qlo, qh, u);
+        o->rotation[0] = q.w; o->rotation[1] = q.x; o->rotation[2] = q.y; o->rotation[3] = q.z;
+    }
+    return GSIM_OK;
+}

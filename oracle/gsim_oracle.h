@@ -13,6 +13,10 @@
  *   oracle::random_field tests/support/test_oracles.cpp:144-168 (std::mt19937_64 and
  *       libstdc++'s uniform_real_distribution<double> restated bit-exactly)
  *   hash_target (FNV-1a)  hash.hpp:16-44
+ *   encode: write_png_rgb8 / gray8 / gray16 row bytes, write_pfm body, linear_to_srgb
+ *       image_io.cpp:19-22, 43-45, 75-111, 166-178
+ *   pose playback: PoseStream::append / sample  pose_stream.cpp:31-40, 117-136;
+ *       slerp  math.hpp:195-214
  *
  * Parity pin: tests/test_oracle_pin.py checks every function against the reference itself
  * (oracle/_ref/libgsim_ref.so, compiled from /root/reference sources by oracle/Makefile) and
@@ -76,6 +80,19 @@ double gso_uniform_real(gso_mt19937_64* rng, double a, double b);
 void gso_random_field(uint64_t seed, uint64_t count, double box_extent, double scale_lo,
                       double scale_hi, int sh_degree, double* means, double* scales,
                       double* rotations, double* opacities, double* sh);
+
+/* ---- output encoding (gsim_gpu.h GSIM_ENCODE_* layout) -------------------------------- */
+double gso_linear_to_srgb(double v);
+uint64_t gso_encoded_bytes(uint32_t flags, int width, int height);
+int gso_encode(uint32_t flags, int srgb, double depth_scale, int width, int height,
+               const float* rgb, const float* depth, const float* alpha, uint8_t* out);
+
+/* ---- pose playback ----------------------------------------------------------------------- */
+void gso_slerp(const double a[4], const double b[4], double t, double out[4]);
+/* One node's track (records appended in order: validation error on non-finite values or
+ * decreasing times), sampled at n_t times with the given initial pose. */
+int gso_pose_sample(const double* rec_t, const double* rec_p, const double* rec_q, uint64_t n_rec,
+                    const gsim_rigid* initial, const double* ts, uint64_t n_t, gsim_rigid* out);
 
 uint64_t gso_hash_bytes(const void* data, uint64_t size, uint64_t seed);
 uint64_t gso_hash_target(const float* rgb, const float* depth, const float* alpha, int width,

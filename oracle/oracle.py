@@ -85,6 +85,15 @@ class Oracle:
         L.gso_mt_seed.argtypes = [_vp, C.c_uint64]
         L.gso_mt_next.argtypes = [_vp]
         L.gso_mt_next.restype = C.c_uint64
+        L.gso_linear_to_srgb.argtypes = [C.c_double]
+        L.gso_linear_to_srgb.restype = C.c_double
+        L.gso_encoded_bytes.argtypes = [C.c_uint32, C.c_int, C.c_int]
+        L.gso_encoded_bytes.restype = C.c_uint64
+        L.gso_encode.argtypes = [C.c_uint32, C.c_int, C.c_double, C.c_int, C.c_int, _fp, _fp, _fp,
+                                 C.POINTER(C.c_uint8)]
+        L.gso_slerp.argtypes = [_dp, _dp, C.c_double, _dp]
+        L.gso_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
+                                      C.c_uint64, C.POINTER(abi.gsim_rigid)]
 
     # -- fixtures ----------------------------------------------------------------------------
     def random_field(self, seed, count, box_extent, scale_lo, scale_hi, sh_degree) -> GaussianField:
@@ -185,6 +194,54 @@ class Oracle:
                                             t.accum_alpha.ctypes.data_as(_fp), w, h, seed))
 
 
+    # -- output encoding / pose playback ------------------------------------------------------
+    def linear_to_srgb(self, v: float) -> float:
+        return self.lib.gso_linear_to_srgb(v)
+
+    def encode(self, flags, srgb, depth_scale, width, height, rgb=None, depth=None, alpha=None):
+        """GSIM_ENCODE_* blob of one target (image_io.cpp writers' bytes)."""
+        n = int(self.lib.gso_encoded_bytes(flags, width, height))
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        planes = [_plane(rgb, width * height * 3), _plane(depth, width * height), _plane(alpha, width * height)]
+        rc = self.lib.gso_encode(flags, int(srgb), float(depth_scale), width, height,
+                                 *[p.ctypes.data_as(_fp) for p in planes],
+                                 out.ctypes.data_as(C.POINTER(C.c_uint8)))
+        if rc != 0:
+            raise ValueError(f"gso_encode rc={rc}")
+        return out[:n]
+
+    def slerp(self, a, b, t):
+        o = np.zeros(4)
+        self.lib.gso_slerp(np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(_dp),
+                           np.ascontiguousarray(b, dtype=np.float64).ctypes.data_as(_dp), float(t),
+                           o.ctypes.data_as(_dp))
+        return o
+
+    def pose_sample(self, rec_t, rec_p, rec_q, initial, ts):
+        """(rc, [n_t] gsim_rigid) of one node's track sampled at ts (PoseStream::sample)."""
+        return _pose_sample(self.lib.gso_pose_sample, rec_t, rec_p, rec_q, initial, ts)
+
+
+def _plane(a, n):
+    if a is None:
+        return np.zeros(max(n, 1), dtype=np.float32)
+    return np.ascontiguousarray(a, dtype=np.float32).reshape(-1)
+
+
+def _pose_sample(fn, rec_t, rec_p, rec_q, initial, ts):
+    rt = np.ascontiguousarray(rec_t, dtype=np.float64).reshape(-1)
+    rp = np.ascontiguousarray(rec_p, dtype=np.float64).reshape(-1)
+    rq = np.ascontiguousarray(rec_q, dtype=np.float64).reshape(-1)
+    tt = np.ascontiguousarray(ts, dtype=np.float64).reshape(-1)
+    out = (abi.gsim_rigid * max(len(tt), 1))()
+    init = initial.to_c() if hasattr(initial, "to_c") else initial
+    rc = fn(rt.ctypes.data_as(_dp), rp.ctypes.data_as(_dp), rq.ctypes.data_as(_dp), len(rt),
+            C.byref(init), tt.ctypes.data_as(_dp), len(tt), out)
+    poses = np.array([list(out[k].rotation) + list(out[k].translation) for k in range(len(tt))],
+                     dtype=np.float64).reshape(-1, 7)
+    return rc, poses
+
+
 class Ref:
     """The unmodified reference (oracle/_ref/libgsim_ref.so). Raises if it was never built."""
 
@@ -217,6 +274,16 @@ class Ref:
         L.ref_set_threads.argtypes = [C.c_int]
         L.ref_thread_count.restype = C.c_int
         L.ref_rigid_compose.argtypes = [C.POINTER(abi.gsim_rigid)] * 3
+        u8p = C.POINTER(C.c_uint8)
+        L.ref_linear_to_srgb.argtypes = [C.c_double]
+        L.ref_linear_to_srgb.restype = C.c_double
+        L.ref_png_rgb8.argtypes = [_fp, C.c_int, C.c_int, C.c_int, u8p, C.c_uint64, _u64p]
+        L.ref_png_gray8.argtypes = [_fp, C.c_int, C.c_int, u8p, C.c_uint64, _u64p]
+        L.ref_png_gray16.argtypes = [_fp, C.c_int, C.c_int, C.c_double, u8p, C.c_uint64, _u64p]
+        L.ref_write_pfm.argtypes = [C.c_char_p, _fp, C.c_int, C.c_int]
+        L.ref_slerp.argtypes = [_dp, _dp, C.c_double, _dp]
+        L.ref_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
+                                      C.c_uint64, C.POINTER(abi.gsim_rigid)]
 
     def set_threads(self, n: int) -> None:
         self.lib.ref_set_threads(n)
@@ -277,6 +344,70 @@ class Ref:
         e = (C.c_double * 3)(*eye); t = (C.c_double * 3)(*target); u = (C.c_double * 3)(*up)
         self.lib.ref_look_at(e, t, fx, fy, width, height, u, C.byref(cam))
         return cam
+
+
+    # -- image_io.cpp writers (row bytes captured at the libpng boundary) / pose playback -----
+    def linear_to_srgb(self, v: float) -> float:
+        return self.lib.ref_linear_to_srgb(v)
+
+    def _capture(self, fn, *args, n):
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        size = C.c_uint64(0)
+        rc = fn(*args, out.ctypes.data_as(C.POINTER(C.c_uint8)), len(out), C.byref(size))
+        if rc != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return out[: size.value]
+
+    def png_rgb8(self, rgb, width, height, srgb):
+        a = _plane(rgb, width * height * 3)
+        return self._capture(self.lib.ref_png_rgb8, a.ctypes.data_as(_fp), width, height, int(srgb),
+                             n=3 * width * height)
+
+    def png_gray8(self, v, width, height):
+        a = _plane(v, width * height)
+        return self._capture(self.lib.ref_png_gray8, a.ctypes.data_as(_fp), width, height,
+                             n=width * height)
+
+    def png_gray16(self, v, width, height, scale):
+        a = _plane(v, width * height)
+        return self._capture(self.lib.ref_png_gray16, a.ctypes.data_as(_fp), width, height,
+                             float(scale), n=2 * width * height)
+
+    def write_pfm(self, path, v, width, height) -> bytes:
+        a = _plane(v, width * height)
+        rc = self.lib.ref_write_pfm(str(path).encode(), a.ctypes.data_as(_fp), width, height)
+        if rc != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return Path(path).read_bytes()
+
+    def encode(self, flags, srgb, depth_scale, width, height, rgb=None, depth=None, alpha=None,
+               tmpdir=None):
+        """The GSIM_ENCODE_* blob assembled from the reference writers' own bytes."""
+        import tempfile
+        parts = []
+        if flags & abi.GSIM_ENCODE_RGB8:
+            parts.append(self.png_rgb8(rgb, width, height, srgb))
+        if flags & abi.GSIM_ENCODE_ALPHA8:
+            parts.append(self.png_gray8(alpha, width, height))
+        if flags & abi.GSIM_ENCODE_DEPTH16:
+            parts.append(self.png_gray16(depth, width, height, depth_scale))
+        if flags & abi.GSIM_ENCODE_DEPTH_PFM:
+            with tempfile.TemporaryDirectory(dir=tmpdir) as d:
+                raw = self.write_pfm(Path(d) / "d.pfm", depth, width, height)
+            header = f"Pf\n{width} {height}\n-1.0\n".encode()
+            assert raw.startswith(header)
+            parts.append(np.frombuffer(raw[len(header):], dtype=np.uint8))
+        return np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8)
+
+    def slerp(self, a, b, t):
+        o = np.zeros(4)
+        self.lib.ref_slerp(np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(_dp),
+                           np.ascontiguousarray(b, dtype=np.float64).ctypes.data_as(_dp), float(t),
+                           o.ctypes.data_as(_dp))
+        return o
+
+    def pose_sample(self, rec_t, rec_p, rec_q, initial, ts):
+        return _pose_sample(self.lib.ref_pose_sample, rec_t, rec_p, rec_q, initial, ts)
 
 
 class RefField:

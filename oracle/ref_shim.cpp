@@ -11,6 +11,10 @@
 //   gsim::CameraModel::look_at                   camera.hpp:31-32
 //   gsim::set_thread_count                       parallel.hpp:13
 //   oracle::random_field                         tests/support/test_oracles.hpp:34-35
+//   gsim::write_png_rgb8 / gray8 / gray16 / write_pfm / linear_to_srgb   image_io.hpp:12-33
+//     (image_io.cpp compiled against oracle/png_capture, which records the row bytes handed
+//     to libpng instead of compressing them)
+//   gsim::PoseStream::append / sample, gsim::slerp          pose_stream.hpp:28-45, math.hpp:196
 // Used by tests/test_oracle_pin.py (pin the C restatement), tests/golden/make_golden.py and
 // bench.py --impl reference (the reference's CPU renderer timed on the host cores).
 #include <cstring>
@@ -20,6 +24,9 @@
 
 #include "gsim/errors.hpp"
 #include "gsim/gaussian.hpp"
+#include "gsim/image_io.hpp"
+#include "gsim/pose_stream.hpp"
+#include "png.h"
 #include "gsim/parallel.hpp"
 #include "gsim/raster.hpp"
 #include "gsim/reference_raster.hpp"
@@ -273,6 +280,89 @@ void ref_random_field(std::uint64_t seed, std::uint64_t count, double box_extent
         opacities[i] = p.opacity;
         std::memcpy(sh + 48 * i, p.sh.data(), 48 * sizeof(double));
     }
+}
+
+// ---- image_io.cpp writers: the bytes each hands to libpng (captured), and the PFM file ----
+namespace {
+int copy_capture(std::uint8_t* out, std::uint64_t capacity, std::uint64_t* size) {
+    std::size_t n = 0;
+    const unsigned char* b = png_capture_last(nullptr, nullptr, nullptr, nullptr, &n);
+    if (size) *size = n;
+    if (n > capacity) {
+        g_error = "capture larger than the output buffer";
+        return GSIM_ERR_VALIDATION;
+    }
+    std::memcpy(out, b, n);
+    return GSIM_OK;
+}
+}  // namespace
+
+double ref_linear_to_srgb(double v) { return linear_to_srgb(v); }
+
+int ref_png_rgb8(const float* rgb, int width, int height, int srgb, std::uint8_t* out,
+                 std::uint64_t capacity, std::uint64_t* size) {
+    const int rc = guarded([&] {
+        Image3 img(width, height);
+        std::memcpy(img.data.data(), rgb, img.data.size() * sizeof(float));
+        write_png_rgb8("/dev/null", img, srgb != 0);
+    });
+    return rc != GSIM_OK ? rc : copy_capture(out, capacity, size);
+}
+
+int ref_png_gray8(const float* v, int width, int height, std::uint8_t* out, std::uint64_t capacity,
+                  std::uint64_t* size) {
+    const int rc = guarded([&] {
+        Image1 img(width, height);
+        std::memcpy(img.data.data(), v, img.data.size() * sizeof(float));
+        write_png_gray8("/dev/null", img);
+    });
+    return rc != GSIM_OK ? rc : copy_capture(out, capacity, size);
+}
+
+int ref_png_gray16(const float* v, int width, int height, double scale, std::uint8_t* out,
+                   std::uint64_t capacity, std::uint64_t* size) {
+    const int rc = guarded([&] {
+        Image1 img(width, height);
+        std::memcpy(img.data.data(), v, img.data.size() * sizeof(float));
+        write_png_gray16("/dev/null", img, scale);
+    });
+    return rc != GSIM_OK ? rc : copy_capture(out, capacity, size);
+}
+
+int ref_write_pfm(const char* path, const float* v, int width, int height) {
+    return guarded([&] {
+        Image1 img(width, height);
+        std::memcpy(img.data.data(), v, img.data.size() * sizeof(float));
+        write_pfm(path, img);
+    });
+}
+
+// ---- pose playback: one node's track through PoseStream (pose_stream.cpp:31-40, 117-136) ----
+// Records are (t, p[3], q[4] as w,x,y,z); queries sample the track at times ts[k] with the
+// given initial pose. Returns validation errors for non-finite or decreasing records.
+int ref_pose_sample(const double* rec_t, const double* rec_p, const double* rec_q,
+                    std::uint64_t n_rec, const gsim_rigid* initial, const double* ts,
+                    std::uint64_t n_t, gsim_rigid* out) {
+    return guarded([&] {
+        PoseStream stream;
+        for (std::uint64_t i = 0; i < n_rec; ++i) {
+            PoseRecord r;
+            r.t = rec_t[i];
+            r.node = "node";
+            r.pose = RigidTransform(to_quat(rec_q + 4 * i), to_vec(rec_p + 3 * i));
+            stream.append(r);
+        }
+        const RigidTransform init = to_rigid(*initial);
+        for (std::uint64_t k = 0; k < n_t; ++k) from_rigid(stream.sample("node", ts[k], init), &out[k]);
+    });
+}
+
+void ref_slerp(const double* a, const double* b, double t, double* out) {
+    const Quat q = slerp(to_quat(a), to_quat(b), t);
+    out[0] = q.w;
+    out[1] = q.x;
+    out[2] = q.y;
+    out[3] = q.z;
 }
 
 }  // extern "C"

@@ -7,6 +7,7 @@ include/gsim_gpu.h). See DESIGN.md.
 from .api import (  # noqa: F401
     CameraModel,
     Context,
+    EncodeOptions,
     GaussianField,
     IoError,
     NodeKind,
@@ -28,7 +29,7 @@ from .api import (  # noqa: F401
 from .abi import SPLAT_DTYPE, load_library  # noqa: F401
 
 __all__ = [
-    "CameraModel", "Context", "GaussianField", "IoError", "NodeKind", "RasterOptions",
+    "CameraModel", "Context", "EncodeOptions", "GaussianField", "IoError", "NodeKind", "RasterOptions",
     "RenderTarget", "RigidTransform", "Scene", "SceneNode", "ValidationError", "SPLAT_DTYPE",
     "default_context", "io_error", "load_library", "project", "quat_from_axis_angle",
     "rasterize", "render", "transform_primitives", "validation_error",

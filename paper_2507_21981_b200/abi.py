@@ -18,6 +18,10 @@ GSIM_ERR_VALIDATION = 2
 GSIM_NODE_BACKGROUND = 0
 GSIM_NODE_INTERACTIVE = 1
 GSIM_ENV_ALL = -1
+GSIM_ENCODE_RGB8 = 1
+GSIM_ENCODE_ALPHA8 = 2
+GSIM_ENCODE_DEPTH16 = 4
+GSIM_ENCODE_DEPTH_PFM = 8
 
 
 class gsim_rigid(C.Structure):
@@ -50,6 +54,10 @@ class gsim_camera(C.Structure):
 class gsim_raster_options(C.Structure):
     _fields_ = [("normalize_depth", C.c_int32), ("reserved", C.c_int32),
                 ("transmittance_cutoff", C.c_double)]
+
+
+class gsim_encode_options(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("srgb", C.c_int32), ("depth_scale", C.c_double)]
 
 
 class gsim_projected_splat(C.Structure):
@@ -113,6 +121,17 @@ SIGNATURES = [
     ("gsim_gpu_device_output", _P, [_P]),
     ("gsim_gpu_tile_lists", C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                       C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("gsim_gpu_encoded_bytes", C.c_uint64, [C.c_uint32, C.c_int32, C.c_int32]),
+    ("gsim_gpu_srgb_thresholds", None, [C.POINTER(C.c_float)]),
+    ("gsim_gpu_encode_host", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_float),
+                                       C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                       C.POINTER(gsim_encode_options), C.POINTER(C.c_uint8)]),
+    ("gsim_gpu_encode", C.c_int, [_P, _P, C.POINTER(gsim_camera), C.c_uint64,
+                                  C.POINTER(gsim_encode_options), _P, C.c_int32]),
+    ("gsim_gpu_render_encoded", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64,
+                                          C.POINTER(gsim_camera), C.c_uint64,
+                                          C.POINTER(gsim_raster_options),
+                                          C.POINTER(gsim_encode_options), _P, C.c_int32]),
 ]
 
 _lib = None

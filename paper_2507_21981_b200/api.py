@@ -213,6 +213,48 @@ class RasterOptions:
         return o
 
 
+class EncodeOptions:
+    """Which writer bytes to produce (include/gsim_gpu.h GSIM_ENCODE_*); defaults follow the
+    reference CLI's render command (tools/gsim.cpp:57-66): sRGB 8-bit RGB, 8-bit alpha, PFM
+    depth, and 16-bit millimetre depth."""
+
+    RGB8 = abi.GSIM_ENCODE_RGB8
+    ALPHA8 = abi.GSIM_ENCODE_ALPHA8
+    DEPTH16 = abi.GSIM_ENCODE_DEPTH16
+    DEPTH_PFM = abi.GSIM_ENCODE_DEPTH_PFM
+
+    def __init__(self, flags: int = RGB8 | ALPHA8 | DEPTH16 | DEPTH_PFM, srgb: bool = True,
+                 depth_scale: float = 1000.0):
+        self.flags = int(flags)
+        self.srgb = bool(srgb)
+        self.depth_scale = float(depth_scale)
+
+    def to_c(self) -> abi.gsim_encode_options:
+        return abi.gsim_encode_options(self.flags, int(self.srgb), self.depth_scale)
+
+    def bytes_per_camera(self, width: int, height: int) -> int:
+        return int(abi.load_library().gsim_gpu_encoded_bytes(self.flags, width, height))
+
+    def split(self, blob: np.ndarray, cameras) -> list[dict]:
+        """Per-camera views of an encoded blob: rgb8 (H,W,3) u8, alpha8 (H,W) u8, depth16 (H,W)
+        u16 (decoded from big-endian), depth_pfm (H,W) f32 rows bottom-up."""
+        out, off = [], 0
+        for c in cameras:
+            w, h = c.width, c.height
+            n = w * h
+            d = {}
+            if self.flags & self.RGB8:
+                d["rgb8"] = blob[off:off + 3 * n].reshape(h, w, 3); off += 3 * n
+            if self.flags & self.ALPHA8:
+                d["alpha8"] = blob[off:off + n].reshape(h, w); off += n
+            if self.flags & self.DEPTH16:
+                d["depth16"] = blob[off:off + 2 * n].view(">u2").reshape(h, w).astype(np.uint16); off += 2 * n
+            if self.flags & self.DEPTH_PFM:
+                d["depth_pfm"] = blob[off:off + 4 * n].copy().view("<f4").reshape(h, w); off += 4 * n
+            out.append(d)
+        return out
+
+
 @dataclass
 class RenderTarget:
     """RGB + alpha-composited depth + accumulated alpha (image.hpp:38-45)."""
@@ -418,6 +460,60 @@ class Context:
                                                C.c_void_p(device_out) if device_out else None),
                self.ptr)
         return device_out if device_out else int(self.lib.gsim_gpu_device_output(self.ptr))
+
+    # -- output encoding (image_io.cpp writers' bytes) -----------------------------------------
+    def encode_target(self, target: "RenderTarget", options: EncodeOptions | None = None) -> np.ndarray:
+        """Encode one host RenderTarget on the GPU (gsim_gpu_encode_host)."""
+        o = options or EncodeOptions()
+        h, w = target.depth.shape
+        out = np.zeros(max(o.bytes_per_camera(w, h), 1), dtype=np.uint8)
+        planes = [np.ascontiguousarray(a, dtype=np.float32) for a in (target.rgb, target.depth,
+                                                                      target.accum_alpha)]
+        fp = C.POINTER(C.c_float)
+        oc = o.to_c()
+        _check(self.lib.gsim_gpu_encode_host(self.ptr, w, h, *[a.ctypes.data_as(fp) for a in planes],
+                                             C.byref(oc), out.ctypes.data_as(C.POINTER(C.c_uint8))),
+               self.ptr)
+        return out[: o.bytes_per_camera(w, h)]
+
+    def encode(self, device_targets: int, cameras: Sequence[CameraModel],
+               options: EncodeOptions | None = None, device_out: int | None = None):
+        """Encode render_device output; returns a host blob, or device_out when given."""
+        o = options or EncodeOptions()
+        ca = _cams_array(cameras)
+        oc = o.to_c()
+        if device_out:
+            _check(self.lib.gsim_gpu_encode(self.ptr, C.c_void_p(device_targets), ca, len(cameras),
+                                            C.byref(oc), C.c_void_p(device_out), 1), self.ptr)
+            return device_out
+        n = sum(o.bytes_per_camera(c.width, c.height) for c in cameras)
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        _check(self.lib.gsim_gpu_encode(self.ptr, C.c_void_p(device_targets), ca, len(cameras),
+                                        C.byref(oc), out.ctypes.data_as(C.c_void_p), 0), self.ptr)
+        return out[:n]
+
+    def render_encoded(self, scene: Scene, nodes, cameras, options: RasterOptions | None = None,
+                       encode: EncodeOptions | None = None, out: np.ndarray | None = None,
+                       device_out: int | None = None):
+        """render + encode fused in the compositing kernel (gsim_gpu_render_encoded). Host blob
+        (synchronous) unless device_out is given (asynchronous, like render_device)."""
+        o = encode or EncodeOptions()
+        na = _nodes_array(nodes)
+        ca = _cams_array(cameras)
+        opt = (options or RasterOptions()).to_c()
+        oc = o.to_c()
+        if device_out:
+            _check(self.lib.gsim_gpu_render_encoded(self.ptr, scene.handle, na, len(nodes), ca,
+                                                    len(cameras), C.byref(opt), C.byref(oc),
+                                                    C.c_void_p(device_out), 1), self.ptr)
+            return device_out
+        n = sum(o.bytes_per_camera(c.width, c.height) for c in cameras)
+        if out is None:
+            out = np.zeros(max(n, 1), dtype=np.uint8)
+        _check(self.lib.gsim_gpu_render_encoded(self.ptr, scene.handle, na, len(nodes), ca,
+                                                len(cameras), C.byref(opt), C.byref(oc),
+                                                out.ctypes.data_as(C.c_void_p), 0), self.ptr)
+        return out[:n]
 
     def tile_lists(self, camera: int):
         """Sorted per-tile lists of `camera` from the last render (tile offsets, indices)."""

@@ -27,9 +27,10 @@ SOURCES = {
     "sort.cu": [],
     "bin.cu": [],
     "raster.cu": [],
+    "encode.cu": [],
     "host.cu": [],
 }
-DEPS = ["common.cuh", "kernels.hpp"]
+DEPS = ["common.cuh", "kernels.hpp", "encode.cuh"]
 
 
 def nvcc() -> str:

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -161,6 +162,17 @@ struct gsim_gpu_context {
     float* pending_out = nullptr;
     gsim_raster_options pending_opt{0, 0, 1e-4};
     int pending_grid = 1;
+    // output encoding (encode.cuh): thresholds uploaded on first use; frame_enc is the fused
+    // raster epilogue's encoding of the render in flight (flags 0 = float targets only)
+    DevBuf<float> srgb_thr;
+    bool srgb_ready = false;
+    EncodeParams frame_enc{};
+    bool frame_enc_only = false;     // encoded bytes only, no float targets
+    EncodeParams pending_enc{};
+    bool pending_enc_only = false;
+    DevBuf<uint8_t> enc_buf;
+    DevBuf<float> enc_src;
+    DevBuf<EncodeCam> enc_cams;
     // outputs / API scratch
     DevBuf<float> out;
     DevBuf<gsim_projected_splat> full;
@@ -526,6 +538,8 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.consumed = ctx->counts.ptr + 2;
     rr.capacity = ctx->pair_capacity;
     rr.n_slots = std::max<uint64_t>(p.slots, 1);
+    rr.enc = ctx->frame_enc;
+    if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
 }
@@ -641,6 +655,8 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
             ctx->pending_out = out;
             ctx->pending_opt = opt;
             ctx->pending_grid = chunk_grid;
+            ctx->pending_enc = ctx->frame_enc;
+            ctx->pending_enc_only = ctx->frame_enc_only;
             break;
         }
         GSIM_CK(cudaEventSynchronize(ctx->bin_ev));
@@ -756,8 +772,11 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
         const uint64_t g = n_cams ? std::min(group, n_cams - c0) : 0;
         if (c0 > 0 && !wait_for_count) check_pending(ctx);
         Plan plan;
+        const EncodeParams enc_batch = ctx->frame_enc;
+        if (enc_batch.flags) ctx->frame_enc.dst += offsets[c0] / 5 * encoded_bpp(enc_batch.flags);
         render_frame(ctx, scene, nodes, n_nodes, cameras + c0, g, options, out + offsets[c0], plan,
                      wait_for_count);
+        ctx->frame_enc = enc_batch;
         launches += ctx->stats.launches;
         h2d += ctx->stats.h2d_bytes;
         ctx->last_plan = std::move(plan);
@@ -787,8 +806,88 @@ void check_pending(gsim_gpu_context* ctx) {
     BinArgs b = make_bin_args(ctx, ctx->last_plan, ctx->dv[1].ptr);
     launch_bin_scatter(b, ctx->pending_grid, ctx->stream);
     check_launch();
+    const EncodeParams enc = ctx->frame_enc;
+    const bool enc_only = ctx->frame_enc_only;
+    ctx->frame_enc = ctx->pending_enc;
+    ctx->frame_enc_only = ctx->pending_enc_only;
     launch_raster_stage(ctx, ctx->last_plan, ctx->pending_opt, ctx->pending_out);
+    ctx->frame_enc = enc;
+    ctx->frame_enc_only = enc_only;
     GSIM_CK(cudaStreamSynchronize(ctx->stream));
+}
+
+// ---- output encoding (image_io.cpp) ---------------------------------------------------------
+
+// quantize8(linear_to_srgb(v)) of the reference (image_io.cpp:19-22, :43-45), restated for the
+// threshold table only; the device never evaluates pow.
+uint32_t srgb_code(float f) {
+    double v = std::clamp(double(f), 0.0, 1.0);
+    v = v <= 0.0031308 ? 12.92 * v : 1.055 * std::pow(v, 1.0 / 2.4) - 0.055;
+    return uint32_t(std::clamp(std::lround(v * 255.0), 0l, 255l));
+}
+
+// thr[k] = smallest float in [0, 1] whose code is >= k (binary search over the float bit
+// patterns of [0, 1], on which the code is monotone non-decreasing); thr[0] = -inf.
+void build_srgb_thresholds(float* thr) {
+    thr[0] = -std::numeric_limits<float>::infinity();
+    for (uint32_t k = 1; k < 256; ++k) {
+        uint32_t lo = 0, hi = 0x3f800000u;  // code(as_float(hi)) = 255 >= k
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            float f;
+            std::memcpy(&f, &mid, 4);
+            if (srgb_code(f) >= k) hi = mid; else lo = mid + 1;
+        }
+        std::memcpy(&thr[k], &lo, 4);
+    }
+}
+
+EncodeParams make_encode_params(gsim_gpu_context* ctx, const gsim_encode_options* o, uint8_t* dst) {
+    if (!o) throw ValidationError{"encode: options must not be NULL"};
+    if (o->flags == 0 || (o->flags & ~uint32_t(GSIM_ENCODE_RGB8 | GSIM_ENCODE_ALPHA8 |
+                                               GSIM_ENCODE_DEPTH16 | GSIM_ENCODE_DEPTH_PFM)))
+        throw ValidationError{"encode: flags must be a non-empty set of GSIM_ENCODE_* bits"};
+    if ((o->flags & GSIM_ENCODE_DEPTH16) && !std::isfinite(o->depth_scale))
+        throw ValidationError{"encode: depth_scale must be finite"};
+    if (o->srgb && (o->flags & GSIM_ENCODE_RGB8) && !ctx->srgb_ready) {
+        float thr[256];
+        build_srgb_thresholds(thr);
+        ctx->srgb_thr.reserve(256);
+        GSIM_CK(cudaMemcpy(ctx->srgb_thr.ptr, thr, sizeof(thr), cudaMemcpyHostToDevice));
+        ctx->srgb_ready = true;
+    }
+    EncodeParams e{};
+    e.dst = dst;
+    e.srgb_thr = ctx->srgb_thr.ptr;
+    e.depth_scale = o->depth_scale;
+    e.flags = o->flags;
+    e.srgb = (o->srgb && (o->flags & GSIM_ENCODE_RGB8)) ? 1 : 0;
+    return e;
+}
+
+// Encode float targets already on the device ([rgb|depth|alpha] per camera, consecutive).
+void encode_device(gsim_gpu_context* ctx, const float* src, const uint32_t* widths,
+                   const uint32_t* heights, uint64_t n, const EncodeParams& e) {
+    std::vector<EncodeCam> cams(n);
+    uint64_t src_off = 0, dst_off = 0;
+    uint32_t max_px = 0;
+    const uint32_t bpp = encoded_bpp(e.flags);
+    for (uint64_t c = 0; c < n; ++c) {
+        cams[c] = EncodeCam{widths[c], heights[c], src_off, dst_off};
+        const uint64_t npx = uint64_t(widths[c]) * heights[c];
+        src_off += 5 * npx;
+        dst_off += bpp * npx;
+        max_px = std::max<uint32_t>(max_px, uint32_t(npx));
+    }
+    ctx->enc_cams.reserve(std::max<uint64_t>(n, 1));
+    GSIM_CK(cudaMemcpyAsync(ctx->enc_cams.ptr, cams.data(), n * sizeof(EncodeCam),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    EncodeKernelArgs a{src, ctx->enc_cams.ptr, e};
+    for (uint64_t c0 = 0; c0 < n; c0 += 65535) {  // grid.y limit
+        a.cams = ctx->enc_cams.ptr + c0;
+        launch_encode(a, uint32_t(std::min<uint64_t>(65535, n - c0)), max_px, ctx->stream);
+        check_launch();
+    }
 }
 
 struct Guard {
@@ -1182,6 +1281,123 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
             ctx->stats.d2h_bytes += 5 * npx * sizeof(float);
         }
         GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uint64_t gsim_gpu_encoded_bytes(uint32_t flags, int32_t width, int32_t height) {
+    if (flags & ~uint32_t(GSIM_ENCODE_RGB8 | GSIM_ENCODE_ALPHA8 | GSIM_ENCODE_DEPTH16 |
+                          GSIM_ENCODE_DEPTH_PFM))
+        return 0;
+    if (width <= 0 || height <= 0) return 0;
+    return uint64_t(encoded_bpp(flags)) * uint64_t(width) * uint64_t(height);
+}
+
+void gsim_gpu_srgb_thresholds(float* thresholds) {
+    if (thresholds) build_srgb_thresholds(thresholds);
+}
+
+int gsim_gpu_encode_host(gsim_gpu_context* ctx, int32_t width, int32_t height, const float* rgb,
+                         const float* depth, const float* accum_alpha,
+                         const gsim_encode_options* options, uint8_t* out) {
+    return Guard(ctx).run([&] {
+        const EncodeParams e0 = make_encode_params(ctx, options, nullptr);
+        if (width <= 0 || height <= 0) throw ValidationError{"encode: empty image"};
+        if (!out) throw ValidationError{"encode: out must not be NULL"};
+        if ((e0.flags & GSIM_ENCODE_RGB8) && !rgb) throw ValidationError{"encode: rgb is NULL"};
+        if ((e0.flags & (GSIM_ENCODE_DEPTH16 | GSIM_ENCODE_DEPTH_PFM)) && !depth)
+            throw ValidationError{"encode: depth is NULL"};
+        if ((e0.flags & GSIM_ENCODE_ALPHA8) && !accum_alpha)
+            throw ValidationError{"encode: accum_alpha is NULL"};
+        const uint64_t npx = uint64_t(width) * uint64_t(height);
+        const uint64_t bytes = encoded_bpp(e0.flags) * npx;
+        ctx->enc_src.reserve(5 * npx);
+        ctx->enc_buf.reserve(bytes);
+        cudaStream_t s = ctx->stream;
+        if (rgb) GSIM_CK(cudaMemcpyAsync(ctx->enc_src.ptr, rgb, 12 * npx, cudaMemcpyHostToDevice, s));
+        if (depth)
+            GSIM_CK(cudaMemcpyAsync(ctx->enc_src.ptr + 3 * npx, depth, 4 * npx, cudaMemcpyHostToDevice, s));
+        if (accum_alpha)
+            GSIM_CK(cudaMemcpyAsync(ctx->enc_src.ptr + 4 * npx, accum_alpha, 4 * npx,
+                                    cudaMemcpyHostToDevice, s));
+        EncodeParams e = e0;
+        e.dst = ctx->enc_buf.ptr;
+        const uint32_t w = uint32_t(width), h = uint32_t(height);
+        encode_device(ctx, ctx->enc_src.ptr, &w, &h, 1, e);
+        GSIM_CK(cudaMemcpyAsync(out, ctx->enc_buf.ptr, bytes, cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+        ctx->stats.launches = 1;
+        ctx->launches_total += 1;
+        ctx->stats.launches_total = ctx->launches_total;
+    });
+}
+
+int gsim_gpu_encode(gsim_gpu_context* ctx, const float* device_targets, const gsim_camera* cameras,
+                    uint64_t n_cameras, const gsim_encode_options* options, uint8_t* out,
+                    int32_t out_is_device) {
+    return Guard(ctx).run([&] {
+        EncodeParams e = make_encode_params(ctx, options, nullptr);
+        if (n_cameras && (!device_targets || !cameras || !out))
+            throw ValidationError{"encode: NULL targets, cameras or out"};
+        std::vector<uint32_t> w(n_cameras), h(n_cameras);
+        uint64_t bytes = 0;
+        for (uint64_t c = 0; c < n_cameras; ++c) {
+            validate_camera(cameras[c], c);
+            w[c] = uint32_t(cameras[c].width);
+            h[c] = uint32_t(cameras[c].height);
+            bytes += uint64_t(encoded_bpp(e.flags)) * w[c] * h[c];
+        }
+        if (!n_cameras) return;
+        if (out_is_device) {
+            e.dst = out;
+        } else {
+            ctx->enc_buf.reserve(bytes);
+            e.dst = ctx->enc_buf.ptr;
+        }
+        encode_device(ctx, device_targets, w.data(), h.data(), n_cameras, e);
+        if (!out_is_device) {
+            GSIM_CK(cudaMemcpyAsync(out, ctx->enc_buf.ptr, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        }
+        const uint64_t launches = (n_cameras + 65534) / 65535;
+        ctx->stats.launches = launches;
+        ctx->launches_total += launches;
+        ctx->stats.launches_total = ctx->launches_total;
+    });
+}
+
+int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                            const gsim_node* nodes, uint64_t n_nodes, const gsim_camera* cameras,
+                            uint64_t n_cameras, const gsim_raster_options* raster_options,
+                            const gsim_encode_options* options, uint8_t* out,
+                            int32_t out_is_device) {
+    return Guard(ctx).run([&] {
+        if (!scene || (n_nodes && !nodes)) throw ValidationError{"render: null argument"};
+        EncodeParams e = make_encode_params(ctx, options, nullptr);
+        if (n_cameras && (!cameras || !out)) throw ValidationError{"render: NULL cameras or out"};
+        uint64_t bytes = 0;
+        for (uint64_t c = 0; c < n_cameras; ++c) {
+            validate_camera(cameras[c], c);
+            bytes += uint64_t(encoded_bpp(e.flags)) * cameras[c].width * cameras[c].height;
+        }
+        if (out_is_device) {
+            e.dst = out;
+        } else {
+            ctx->enc_buf.reserve(std::max<uint64_t>(bytes, 1));
+            e.dst = ctx->enc_buf.ptr;
+        }
+        struct Reset {  // the fused encoding applies to this call only
+            gsim_gpu_context* c;
+            ~Reset() { c->frame_enc = EncodeParams{}; c->frame_enc_only = false; }
+        } reset{ctx};
+        ctx->frame_enc = e;
+        ctx->frame_enc_only = true;
+        render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, raster_options, nullptr,
+                       !out_is_device);
+        if (!out_is_device && bytes) {
+            GSIM_CK(cudaMemcpyAsync(out, ctx->enc_buf.ptr, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            GSIM_CK(cudaStreamSynchronize(ctx->stream));
+            ctx->stats.d2h_bytes = bytes;
+        }
     });
 }
 

@@ -7,6 +7,7 @@
 
 #include "../../include/gsim_gpu.h"
 #include "common.cuh"
+#include "encode.cuh"
 
 namespace gsim_gpu {
 
@@ -119,6 +120,21 @@ struct RasterArgs {
     unsigned long long* consumed;    // += list entries fetched before the tile saturated
     uint64_t capacity;               // pair-buffer capacity (reads are clamped to it)
     uint64_t n_slots;                // record slots (stale values are clamped to a valid slot)
+    EncodeParams enc;                // fused encoding when enc.flags != 0; camera c's block
+                                     // starts at enc.dst + out_offset / 5 * encoded_bpp
+};
+
+// Standalone encoder (encode.cu): one grid row per camera.
+struct EncodeCam {
+    uint32_t width, height;
+    uint64_t src_offset;             // float offset of the camera's [rgb|depth|alpha] block
+    uint64_t dst_offset;             // byte offset of its encoded block
+};
+
+struct EncodeKernelArgs {
+    const float* src;
+    const EncodeCam* cams;
+    EncodeParams enc;
 };
 
 void launch_pose(const DevField& f, uint64_t begin, uint64_t end, const gsim_rigid& t,
@@ -137,5 +153,7 @@ void launch_bin_tilescan(const BinArgs& a, int grid, cudaStream_t s);
 void launch_bin_campre(const BinArgs& a, cudaStream_t s);
 void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s);
 void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream);
+void launch_encode(const EncodeKernelArgs& a, uint32_t n_cams, uint32_t max_pixels,
+                   cudaStream_t stream);
 
 }  // namespace gsim_gpu

@@ -174,14 +174,24 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
 
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
     if (x < cam.width && y < cam.height) {
-        float* base = a.out + cam.out_offset;
-        const size_t npx = size_t(cam.width) * cam.height;
-        const size_t p = size_t(y) * cam.width + x;
-        base[3 * p + 0] = fminf(fmaxf(cr, 0.f), 1.f);
-        base[3 * p + 1] = fminf(fmaxf(cg, 0.f), 1.f);
-        base[3 * p + 2] = fminf(fmaxf(cb, 0.f), 1.f);
-        base[3 * npx + p] = a.normalize_depth ? (acc > 1e-12f ? d / acc : 0.f) : d;
-        base[4 * npx + p] = acc;
+        const float r = fminf(fmaxf(cr, 0.f), 1.f), gg = fminf(fmaxf(cg, 0.f), 1.f),
+                    bb = fminf(fmaxf(cb, 0.f), 1.f);
+        const float depth = a.normalize_depth ? (acc > 1e-12f ? d / acc : 0.f) : d;
+        if (a.out) {
+            float* base = a.out + cam.out_offset;
+            const size_t npx = size_t(cam.width) * cam.height;
+            const size_t p = size_t(y) * cam.width + x;
+            base[3 * p + 0] = r;
+            base[3 * p + 1] = gg;
+            base[3 * p + 2] = bb;
+            base[3 * npx + p] = depth;
+            base[4 * npx + p] = acc;
+        }
+        if (a.enc.flags) {
+            uint8_t* blk = a.enc.dst + cam.out_offset / 5 * encoded_bpp(a.enc.flags);
+            encode_pixel(a.enc, a.enc.srgb_thr, blk, uint32_t(cam.width), uint32_t(cam.height),
+                         uint32_t(x), uint32_t(y), r, gg, bb, depth, acc);
+        }
     }
 }
 
