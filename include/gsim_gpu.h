@@ -169,6 +169,23 @@ int gsim_gpu_transform_primitives(gsim_gpu_context* ctx, gsim_gpu_scene* scene, 
 /* Copies the device field's means (count*3) and rotations (count*4) back; either may be NULL. */
 int gsim_gpu_scene_download(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, double* means,
                             double* rotations);
+/* Copies every plane of the device field back in the reference's per-primitive layout:
+ * means n*3, scales n*3, rotations n*4 (w,x,y,z), opacities n, sh n*48 (sh[c*16+k],
+ * gaussian.hpp:16-19; coefficients above the field's degree are 0). Any pointer may be NULL. */
+int gsim_gpu_scene_download_field(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                                  double* means, double* scales, double* rotations,
+                                  double* opacities, double* sh);
+int32_t gsim_gpu_scene_sh_degree(const gsim_gpu_scene* scene);
+
+/* load_splat_ply (splat_ply.cpp:40-162) straight into a device-resident field (SURVEY.md 8f
+ * row 1): the header is parsed on the host with the reference's rules and messages; the float
+ * payload is streamed through pinned chunks to the device and converted by a kernel
+ * (sigmoid opacity, exp scales, 1e-6 rotation renormalisation, per-primitive validation in
+ * the reference's order). Status 1 when the file cannot be opened, 2 for format/validation
+ * errors (format_error derives from validation_error, errors.hpp:22-24). Means, rotations and
+ * SH are bit-exact with the reference loader; scale and opacity go through CUDA's double exp
+ * (scale <= 1 ulp from glibc, opacity = 1 / (1 + exp(-x)) <= 2 ulp). */
+int gsim_gpu_scene_load_ply(gsim_gpu_context* ctx, const char* path, gsim_gpu_scene** out);
 
 /* project (raster.cpp:135-232): visible splats in primitive order. Writes at most
  * capacity splats to out and the visible count to *count (count may exceed capacity). */
@@ -254,6 +271,38 @@ int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
                             uint64_t n_cameras, const gsim_raster_options* raster_options,
                             const gsim_encode_options* options, uint8_t* out,
                             int32_t out_is_device);
+
+/* ---- Pose playback on the device ---------------------------------------
+ * Replaces PoseStream (pose_stream.hpp:22-49; append pose_stream.cpp:31-40, sample :117-136)
+ * and Scene::step_to (scene.cpp:176-190) for batches of nodes: the tracks live in HBM and the
+ * node poses of a frame are sampled by a kernel straight into the frame's pose table. */
+typedef struct gsim_gpu_tracks gsim_gpu_tracks;
+
+/* Upload n_tracks tracks. Records of track k are track_begin[k] .. track_begin[k+1]-1 of the
+ * arrays times[R], translations[R*3], rotations[R*4] (w, x, y, z). PoseStream::append rules:
+ * validation error on non-finite values or times that decrease within a track; rotations are
+ * normalised on upload. */
+int gsim_gpu_tracks_upload(gsim_gpu_context* ctx, const double* times, const double* translations,
+                           const double* rotations, const uint64_t* track_begin, uint64_t n_tracks,
+                           gsim_gpu_tracks** out);
+int gsim_gpu_tracks_destroy(gsim_gpu_tracks* tracks);
+uint64_t gsim_gpu_tracks_count(const gsim_gpu_tracks* tracks);
+
+/* PoseStream::sample for n queries (track[i], time[i], initial[i]) -> out[i] (host arrays). */
+int gsim_gpu_tracks_sample(gsim_gpu_context* ctx, const gsim_gpu_tracks* tracks,
+                           const uint32_t* track, const double* time, const gsim_rigid* initial,
+                           uint64_t n, gsim_rigid* out);
+
+/* render at time t: nodes with node_track[k] >= 0 take track node_track[k] sampled at t (their
+ * pose in `nodes` is the initial pose, scene.cpp:186-188), the rest keep their pose. A
+ * background node driven by a track is a validation error (scene.cpp:180-184). Output as
+ * gsim_gpu_render (outs != NULL, synchronous, host targets) or gsim_gpu_render_device
+ * (outs == NULL: asynchronous into device_out, or the internal buffer when it is NULL). */
+int gsim_gpu_render_at(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                       const gsim_gpu_tracks* tracks, double time, const gsim_node* nodes,
+                       const int64_t* node_track, uint64_t n_nodes, const gsim_camera* cameras,
+                       uint64_t n_cameras, const gsim_raster_options* options, float* device_out,
+                       gsim_target* outs);
 
 #ifdef __cplusplus
 }

@@ -798,3 +798,108 @@ int gso_pose_sample(const double* rec_t, const double* rec_p, const double* rec_
     }
     return GSIM_OK;
 }
+
+/* ---- splat PLY (splat_ply.cpp:40-162) -------------------------------------------------------- */
+
+static int read_line(FILE* f, char* buf, size_t cap) { /* std::getline: up to '\n' */
+    size_t n = 0;
+    int ch;
+    while ((ch = fgetc(f)) != EOF && ch != '\n')
+        if (n + 1 < cap) buf[n++] = (char)ch;
+    buf[n] = 0;
+    return !(ch == EOF && n == 0);
+}
+
+int gso_load_splat_ply(const char* path, uint64_t capacity, uint64_t* count_out, int* degree_out,
+                       double* means, double* scales, double* rotations, double* opacities,
+                       double* sh) {
+    FILE* f = fopen(path, "rb");
+    if (!f) return GSIM_ERR_IO;
+    char line[512];
+    int rc = GSIM_ERR_VALIDATION;
+    char props[80][32];
+    int n_props = 0, format_seen = 0, element_seen = 0, closed = 0;
+    unsigned long long count = 0;
+    float* payload = NULL;
+    if (!read_line(f, line, sizeof line) || strcmp(line, "ply") != 0) goto done;
+    while (read_line(f, line, sizeof line)) {
+        size_t L = strlen(line);
+        if (L && line[L - 1] == '\r') line[--L] = 0;
+        if (strcmp(line, "end_header") == 0) { closed = 1; break; }
+        char tok[64] = "", a[64] = "", b[64] = "";
+        sscanf(line, "%63s %63s %63s", tok, a, b);
+        if (strcmp(tok, "comment") == 0) continue;
+        if (strcmp(tok, "format") == 0) {
+            if (strcmp(a, "binary_little_endian") != 0) goto done;
+            format_seen = 1;
+        } else if (strcmp(tok, "element") == 0) {
+            if (strcmp(a, "vertex") != 0) goto done;
+            count = strtoull(b, NULL, 10);
+            element_seen = 1;
+        } else if (strcmp(tok, "property") == 0) {
+            if (strcmp(a, "float") != 0 || n_props >= 80) goto done;
+            snprintf(props[n_props++], sizeof props[0], "%s", b);
+        } else if (tok[0]) {
+            goto done;
+        }
+    }
+    if (!closed || !format_seen || !element_seen) goto done;
+    int rest = 0;
+    for (int i = 0; i < n_props; ++i) if (strncmp(props[i], "f_rest_", 7) == 0) ++rest;
+    int degree = -1;
+    for (int d = 0; d <= 3; ++d) if (rest == 3 * ((d + 1) * (d + 1) - 1)) degree = d;
+    if (degree < 0) goto done;
+    const int K = (degree + 1) * (degree + 1), rpc = K - 1;
+    const int stride = 17 + 3 * rpc;
+    if (n_props != stride) goto done;
+    { /* expected property names and order */
+        static const char* head[9] = {"x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"};
+        static const char* tail[8] = {"opacity", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"};
+        char want[32];
+        for (int i = 0; i < stride; ++i) {
+            if (i < 9) snprintf(want, sizeof want, "%s", head[i]);
+            else if (i < 9 + 3 * rpc) snprintf(want, sizeof want, "f_rest_%d", i - 9);
+            else snprintf(want, sizeof want, "%s", tail[i - 9 - 3 * rpc]);
+            if (strcmp(props[i], want) != 0) goto done;
+        }
+    }
+    const size_t nfl = (size_t)count * (size_t)stride;
+    if (count) {
+        payload = (float*)malloc(nfl * sizeof(float));
+        if (!payload) { rc = GSIM_ERR_IO; goto done; }
+        if (fread(payload, sizeof(float), nfl, f) != nfl) goto done; /* truncated */
+    }
+    for (uint64_t i = 0; i < count; ++i) {
+        const float* row = payload + i * (size_t)stride;
+        for (int k = 0; k < stride; ++k) if (!isfinite(row[k])) goto done;
+        const float* t = row + 9 + 3 * rpc;
+        const double op = 1.0 / (1.0 + exp(-(double)t[0]));
+        if (op <= 0.0 || op >= 1.0) goto done;
+        const double s0 = exp((double)t[1]), s1 = exp((double)t[2]), s2 = exp((double)t[3]);
+        if (!isfinite(s0) || !isfinite(s1) || !isfinite(s2)) goto done;
+        quat q = q_make(t[4], t[5], t[6], t[7]);
+        const double n = q_norm(q);
+        if (!(n > 0.0) || !isfinite(n)) goto done;
+        if (fabs(n - 1.0) > 1e-6) q = q_normalized(q);
+        if (count <= capacity) {
+            for (int c = 0; c < 3; ++c) means[3 * i + c] = row[c];
+            scales[3 * i] = s0; scales[3 * i + 1] = s1; scales[3 * i + 2] = s2;
+            rotations[4 * i] = q.w; rotations[4 * i + 1] = q.x;
+            rotations[4 * i + 2] = q.y; rotations[4 * i + 3] = q.z;
+            opacities[i] = op;
+            double* o = sh + 48 * i;
+            for (int k = 0; k < 48; ++k) o[k] = 0.0;
+            for (int c = 0; c < 3; ++c) {
+                o[c * 16] = row[6 + c];
+                for (int k = 0; k < rpc; ++k) o[c * 16 + k + 1] = row[9 + c * rpc + k];
+            }
+        }
+    }
+    *count_out = count;
+    *degree_out = degree;
+    rc = GSIM_OK;
+done:
+    free(payload);
+    fclose(f);
+    return rc;
+}

@@ -17,6 +17,7 @@
  *       image_io.cpp:19-22, 43-45, 75-111, 166-178
  *   pose playback: PoseStream::append / sample  pose_stream.cpp:31-40, 117-136;
  *       slerp  math.hpp:195-214
+ *   load_splat_ply   splat_ply.cpp:40-162 (status only: 1 io, 2 format/validation)
  *
  * Parity pin: tests/test_oracle_pin.py checks every function against the reference itself
  * (oracle/_ref/libgsim_ref.so, compiled from /root/reference sources by oracle/Makefile) and
@@ -93,6 +94,13 @@ void gso_slerp(const double a[4], const double b[4], double t, double out[4]);
  * decreasing times), sampled at n_t times with the given initial pose. */
 int gso_pose_sample(const double* rec_t, const double* rec_p, const double* rec_q, uint64_t n_rec,
                     const gsim_rigid* initial, const double* ts, uint64_t n_t, gsim_rigid* out);
+
+/* ---- splat PLY ------------------------------------------------------------------------------
+ * Two-call: *count / *degree are always set on success; arrays are written when
+ * count <= capacity (sh is 48 per primitive, sh[c*16+k]). */
+int gso_load_splat_ply(const char* path, uint64_t capacity, uint64_t* count, int* degree,
+                       double* means, double* scales, double* rotations, double* opacities,
+                       double* sh);
 
 uint64_t gso_hash_bytes(const void* data, uint64_t size, uint64_t seed);
 uint64_t gso_hash_target(const float* rgb, const float* depth, const float* alpha, int width,

@@ -91,6 +91,8 @@ class Oracle:
         L.gso_encoded_bytes.restype = C.c_uint64
         L.gso_encode.argtypes = [C.c_uint32, C.c_int, C.c_double, C.c_int, C.c_int, _fp, _fp, _fp,
                                  C.POINTER(C.c_uint8)]
+        L.gso_load_splat_ply.argtypes = [C.c_char_p, C.c_uint64, _u64p, C.POINTER(C.c_int), _dp, _dp,
+                                         _dp, _dp, _dp]
         L.gso_slerp.argtypes = [_dp, _dp, C.c_double, _dp]
         L.gso_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
                                       C.c_uint64, C.POINTER(abi.gsim_rigid)]
@@ -210,6 +212,9 @@ class Oracle:
             raise ValueError(f"gso_encode rc={rc}")
         return out[:n]
 
+    def load_splat_ply(self, path):
+        return _load_ply(self.lib.gso_load_splat_ply, path)
+
     def slerp(self, a, b, t):
         o = np.zeros(4)
         self.lib.gso_slerp(np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(_dp),
@@ -220,6 +225,24 @@ class Oracle:
     def pose_sample(self, rec_t, rec_p, rec_q, initial, ts):
         """(rc, [n_t] gsim_rigid) of one node's track sampled at ts (PoseStream::sample)."""
         return _pose_sample(self.lib.gso_pose_sample, rec_t, rec_p, rec_q, initial, ts)
+
+
+def _load_ply(fn, path):
+    """(status, GaussianField | None) through a two-call C loader."""
+    count = C.c_uint64(0)
+    degree = C.c_int(0)
+    z = np.zeros(1)
+    rc = fn(str(path).encode(), 0, C.byref(count), C.byref(degree), *[z.ctypes.data_as(_dp)] * 5)
+    if rc != 0:
+        return rc, None
+    n = count.value
+    m = np.zeros((max(n, 1), 3)); s = np.zeros((max(n, 1), 3)); q = np.zeros((max(n, 1), 4))
+    o = np.zeros(max(n, 1)); sh = np.zeros((max(n, 1), 48))
+    rc = fn(str(path).encode(), n, C.byref(count), C.byref(degree),
+            *[a.ctypes.data_as(_dp) for a in (m, s, q, o, sh)])
+    if rc != 0:
+        return rc, None
+    return 0, GaussianField(m[:n], s[:n], q[:n], o[:n], sh[:n], degree.value)
 
 
 def _plane(a, n):
@@ -252,6 +275,9 @@ class Ref:
                 build_oracle(with_ref=True)
             if not p.exists():
                 raise FileNotFoundError(f"{p} not built (needs /root/reference at build time)")
+        # The reference's iostream users (save_splat_ply, write_pfm) need libstdc++'s unique
+        # locale-facet symbols resolved globally; a RTLD_LOCAL-only load crashes in ofstream.
+        C.CDLL("libstdc++.so.6", mode=C.RTLD_GLOBAL)
         self.lib = C.CDLL(str(p))
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
@@ -281,6 +307,9 @@ class Ref:
         L.ref_png_gray8.argtypes = [_fp, C.c_int, C.c_int, u8p, C.c_uint64, _u64p]
         L.ref_png_gray16.argtypes = [_fp, C.c_int, C.c_int, C.c_double, u8p, C.c_uint64, _u64p]
         L.ref_write_pfm.argtypes = [C.c_char_p, _fp, C.c_int, C.c_int]
+        L.ref_load_splat_ply.argtypes = [C.c_char_p, C.c_uint64, _u64p, C.POINTER(C.c_int), _dp, _dp,
+                                         _dp, _dp, _dp]
+        L.ref_save_splat_ply.argtypes = [C.c_char_p, C.POINTER(abi.gsim_field_view)]
         L.ref_slerp.argtypes = [_dp, _dp, C.c_double, _dp]
         L.ref_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
                                       C.c_uint64, C.POINTER(abi.gsim_rigid)]
@@ -398,6 +427,13 @@ class Ref:
             assert raw.startswith(header)
             parts.append(np.frombuffer(raw[len(header):], dtype=np.uint8))
         return np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8)
+
+    def load_splat_ply(self, path):
+        return _load_ply(self.lib.ref_load_splat_ply, path)
+
+    def save_splat_ply(self, path, field: GaussianField) -> int:
+        v = field.view()
+        return self.lib.ref_save_splat_ply(str(path).encode(), C.byref(v))
 
     def slerp(self, a, b, t):
         o = np.zeros(4)

@@ -15,6 +15,7 @@
 //     (image_io.cpp compiled against oracle/png_capture, which records the row bytes handed
 //     to libpng instead of compressing them)
 //   gsim::PoseStream::append / sample, gsim::slerp          pose_stream.hpp:28-45, math.hpp:196
+//   gsim::load_splat_ply / save_splat_ply                   splat_ply.hpp:20-24
 // Used by tests/test_oracle_pin.py (pin the C restatement), tests/golden/make_golden.py and
 // bench.py --impl reference (the reference's CPU renderer timed on the host cores).
 #include <cstring>
@@ -26,6 +27,7 @@
 #include "gsim/gaussian.hpp"
 #include "gsim/image_io.hpp"
 #include "gsim/pose_stream.hpp"
+#include "gsim/splat_ply.hpp"
 #include "png.h"
 #include "gsim/parallel.hpp"
 #include "gsim/raster.hpp"
@@ -363,6 +365,34 @@ void ref_slerp(const double* a, const double* b, double t, double* out) {
     out[1] = q.x;
     out[2] = q.y;
     out[3] = q.z;
+}
+
+// ---- splat PLY ------------------------------------------------------------------------------
+// Two-call load: the field is (re)loaded each call; arrays are written when count <= capacity.
+int ref_load_splat_ply(const char* path, std::uint64_t capacity, std::uint64_t* count, int* degree,
+                       double* means, double* scales, double* rotations, double* opacities,
+                       double* sh) {
+    return guarded([&] {
+        const GaussianField f = load_splat_ply(path);
+        *count = f.size();
+        *degree = f.sh_degree;
+        if (f.size() > capacity) return;
+        for (std::size_t i = 0; i < f.size(); ++i) {
+            const auto& p = f.primitives[i];
+            std::memcpy(means + 3 * i, &p.mean.x, 3 * sizeof(double));
+            std::memcpy(scales + 3 * i, &p.scale.x, 3 * sizeof(double));
+            rotations[4 * i + 0] = p.rotation.w;
+            rotations[4 * i + 1] = p.rotation.x;
+            rotations[4 * i + 2] = p.rotation.y;
+            rotations[4 * i + 3] = p.rotation.z;
+            opacities[i] = p.opacity;
+            std::memcpy(sh + 48 * i, p.sh.data(), 48 * sizeof(double));
+        }
+    });
+}
+
+int ref_save_splat_ply(const char* path, const gsim_field_view* view) {
+    return guarded([&] { save_splat_ply(to_field(view), path); });
 }
 
 }  // extern "C"

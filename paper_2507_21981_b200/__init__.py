@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     GaussianField,
     IoError,
     NodeKind,
+    PoseTracks,
     RasterOptions,
     RenderTarget,
     RigidTransform,
@@ -29,7 +30,7 @@ from .api import (  # noqa: F401
 from .abi import SPLAT_DTYPE, load_library  # noqa: F401
 
 __all__ = [
-    "CameraModel", "Context", "EncodeOptions", "GaussianField", "IoError", "NodeKind", "RasterOptions",
+    "CameraModel", "Context", "EncodeOptions", "GaussianField", "IoError", "NodeKind", "PoseTracks", "RasterOptions",
     "RenderTarget", "RigidTransform", "Scene", "SceneNode", "ValidationError", "SPLAT_DTYPE",
     "default_context", "io_error", "load_library", "project", "quat_from_axis_angle",
     "rasterize", "render", "transform_primitives", "validation_error",

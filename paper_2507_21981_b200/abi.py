@@ -109,6 +109,9 @@ SIGNATURES = [
     ("gsim_gpu_scene_size", C.c_uint64, [_P]),
     ("gsim_gpu_transform_primitives", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(gsim_rigid)]),
     ("gsim_gpu_scene_download", C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("gsim_gpu_scene_download_field", C.c_int, [_P, _P] + [C.POINTER(C.c_double)] * 5),
+    ("gsim_gpu_scene_sh_degree", C.c_int32, [_P]),
+    ("gsim_gpu_scene_load_ply", C.c_int, [_P, C.c_char_p, C.POINTER(_P)]),
     ("gsim_gpu_project", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64, C.POINTER(gsim_camera),
                                    _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     ("gsim_gpu_rasterize", C.c_int, [_P, _P, C.c_uint64, C.POINTER(gsim_camera),
@@ -121,6 +124,17 @@ SIGNATURES = [
     ("gsim_gpu_device_output", _P, [_P]),
     ("gsim_gpu_tile_lists", C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                       C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("gsim_gpu_tracks_upload", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_uint64,
+                                         C.POINTER(_P)]),
+    ("gsim_gpu_tracks_destroy", C.c_int, [_P]),
+    ("gsim_gpu_tracks_count", C.c_uint64, [_P]),
+    ("gsim_gpu_tracks_sample", C.c_int, [_P, _P, C.POINTER(C.c_uint32), C.POINTER(C.c_double),
+                                         C.POINTER(gsim_rigid), C.c_uint64, C.POINTER(gsim_rigid)]),
+    ("gsim_gpu_render_at", C.c_int, [_P, _P, _P, C.c_double, C.POINTER(gsim_node),
+                                     C.POINTER(C.c_int64), C.c_uint64, C.POINTER(gsim_camera),
+                                     C.c_uint64, C.POINTER(gsim_raster_options), _P,
+                                     C.POINTER(gsim_target)]),
     ("gsim_gpu_encoded_bytes", C.c_uint64, [C.c_uint32, C.c_int32, C.c_int32]),
     ("gsim_gpu_srgb_thresholds", None, [C.POINTER(C.c_float)]),
     ("gsim_gpu_encode_host", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_float),

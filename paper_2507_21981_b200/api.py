@@ -355,9 +355,58 @@ class Scene:
                                                     rots.ctypes.data_as(dp)), self.ctx.ptr)
         return means, rots
 
+    @property
+    def sh_degree(self) -> int:
+        return int(self.ctx.lib.gsim_gpu_scene_sh_degree(self.handle))
+
+    def download_field(self) -> "GaussianField":
+        """Every plane of the device field, in the reference's per-primitive layout."""
+        n = self.size
+        arrs = [np.zeros((max(n, 1), w)) for w in (3, 3, 4, 1, 48)]
+        dp = C.POINTER(C.c_double)
+        _check(self.ctx.lib.gsim_gpu_scene_download_field(self.ctx.ptr, self.handle,
+                                                          *[a.ctypes.data_as(dp) for a in arrs]),
+               self.ctx.ptr)
+        m, s, q, o, sh = (a[:n] for a in arrs)
+        return GaussianField(m, s, q, o.reshape(-1), sh, self.sh_degree)
+
     def close(self) -> None:
         if self.handle:
             self.ctx.lib.gsim_gpu_scene_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PoseTracks:
+    """Device-resident pose tracks (PoseStream, pose_stream.hpp:22-49), one per driven node."""
+
+    def __init__(self, ctx: "Context", handle: C.c_void_p, count: int):
+        self.ctx, self.handle, self.count = ctx, handle, count
+
+    def sample(self, track, time, initial) -> np.ndarray:
+        """PoseStream::sample for queries (track[i], time[i], initial[i]); returns (n, 7) rows
+        (qw, qx, qy, qz, tx, ty, tz)."""
+        tr = np.ascontiguousarray(np.broadcast_to(track, np.shape(time)), dtype=np.uint32).reshape(-1)
+        tt = np.ascontiguousarray(time, dtype=np.float64).reshape(-1)
+        n = len(tt)
+        inits = initial if isinstance(initial, (list, tuple)) else [initial] * n
+        ia = (abi.gsim_rigid * max(n, 1))(*[r.to_c() for r in inits])
+        out = (abi.gsim_rigid * max(n, 1))()
+        _check(self.ctx.lib.gsim_gpu_tracks_sample(self.ctx.ptr, self.handle,
+                                                   tr.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                   tt.ctypes.data_as(C.POINTER(C.c_double)), ia, n,
+                                                   out), self.ctx.ptr)
+        return np.array([list(out[k].rotation) + list(out[k].translation) for k in range(n)],
+                        dtype=np.float64).reshape(-1, 7)
+
+    def close(self) -> None:
+        if self.handle:
+            self.ctx.lib.gsim_gpu_tracks_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -413,6 +462,12 @@ class Context:
         _check(self.lib.gsim_gpu_scene_upload(self.ptr, C.byref(v), C.byref(h)), self.ptr)
         return Scene(self, h, field.size())
 
+    def load_ply(self, path) -> Scene:
+        """load_splat_ply (splat_ply.cpp:40-162) straight into a device-resident field."""
+        h = C.c_void_p()
+        _check(self.lib.gsim_gpu_scene_load_ply(self.ptr, str(path).encode(), C.byref(h)), self.ptr)
+        return Scene(self, h, int(self.lib.gsim_gpu_scene_size(h)))
+
     def project(self, scene: Scene, nodes: Sequence[SceneNode], camera: CameraModel) -> np.ndarray:
         na = _nodes_array(nodes)
         cam = camera.to_c() if isinstance(camera, CameraModel) else camera
@@ -460,6 +515,49 @@ class Context:
                                                C.c_void_p(device_out) if device_out else None),
                self.ptr)
         return device_out if device_out else int(self.lib.gsim_gpu_device_output(self.ptr))
+
+    # -- pose playback (pose_stream.cpp / scene.cpp step_to) ----------------------------------
+    def upload_tracks(self, tracks) -> PoseTracks:
+        """tracks: list of (times[R], translations[R,3], rotations[R,4] as w,x,y,z) per node."""
+        times = [np.asarray(t, dtype=np.float64).reshape(-1) for t, _, _ in tracks]
+        begin = np.zeros(len(tracks) + 1, dtype=np.uint64)
+        begin[1:] = np.cumsum([len(t) for t in times])
+        cat = lambda xs, w: (np.ascontiguousarray(np.concatenate(xs), dtype=np.float64)
+                             if xs and sum(len(x) for x in xs) else np.zeros(w))
+        tt = cat(times, 1)
+        pp = cat([np.asarray(p, dtype=np.float64).reshape(-1, 3) for _, p, _ in tracks], 3).reshape(-1)
+        qq = cat([np.asarray(q, dtype=np.float64).reshape(-1, 4) for _, _, q in tracks], 4).reshape(-1)
+        handle = C.c_void_p()
+        dp = C.POINTER(C.c_double)
+        _check(self.lib.gsim_gpu_tracks_upload(self.ptr, tt.ctypes.data_as(dp), pp.ctypes.data_as(dp),
+                                               qq.ctypes.data_as(dp),
+                                               begin.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                               len(tracks), C.byref(handle)), self.ptr)
+        return PoseTracks(self, handle, len(tracks))
+
+    def render_at(self, scene: Scene, tracks: PoseTracks, time: float, nodes, node_track,
+                  cameras, options: RasterOptions | None = None, targets=None,
+                  device_out: int | None = None):
+        """Render with node poses sampled on the GPU at `time` (Scene::step_to + render_all).
+        Host targets (synchronous) unless device_out is given."""
+        na = _nodes_array(nodes)
+        nt = np.ascontiguousarray(node_track, dtype=np.int64).reshape(-1)
+        if len(nt) != len(nodes):
+            raise ValidationError("render_at: node_track needs one entry per node")
+        ca = _cams_array(cameras)
+        opt = (options or RasterOptions()).to_c()
+        if device_out:
+            _check(self.lib.gsim_gpu_render_at(self.ptr, scene.handle, tracks.handle, float(time), na,
+                                               nt.ctypes.data_as(C.POINTER(C.c_int64)), len(nodes),
+                                               ca, len(cameras), C.byref(opt),
+                                               C.c_void_p(device_out), None), self.ptr)
+            return device_out
+        targets = targets or [RenderTarget.empty(c.width, c.height) for c in cameras]
+        ta = (abi.gsim_target * max(len(cameras), 1))(*[t.to_c() for t in targets])
+        _check(self.lib.gsim_gpu_render_at(self.ptr, scene.handle, tracks.handle, float(time), na,
+                                           nt.ctypes.data_as(C.POINTER(C.c_int64)), len(nodes), ca,
+                                           len(cameras), C.byref(opt), None, ta), self.ptr)
+        return targets
 
     # -- output encoding (image_io.cpp writers' bytes) -----------------------------------------
     def encode_target(self, target: "RenderTarget", options: EncodeOptions | None = None) -> np.ndarray:

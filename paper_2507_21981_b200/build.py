@@ -28,6 +28,8 @@ SOURCES = {
     "bin.cu": [],
     "raster.cu": [],
     "encode.cu": [],
+    "tracks.cu": ["-fmad=false"],
+    "ply.cu": ["-fmad=false"],
     "host.cu": [],
 }
 DEPS = ["common.cuh", "kernels.hpp", "encode.cuh"]

@@ -19,7 +19,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <cctype>
+#include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -95,6 +98,8 @@ struct Plan {
     std::vector<int> tiles_x;          // C
     std::vector<DevSegment> segs;
     std::vector<SegEntry> entries;
+    std::vector<int32_t> seg_owner;    // node index painting each segment, -1 = none
+    std::vector<int32_t> seg_track;    // render_at only: track driving each segment, -1 = none
     uint64_t slots = 0;
     uint32_t tiles = 0;
     uint32_t max_tc = 0;
@@ -151,6 +156,7 @@ struct gsim_gpu_context {
     int* cam_tiles_x = nullptr;
     DevSegment* segs = nullptr;
     SegEntry* entries = nullptr;
+    int32_t* seg_track = nullptr;
     std::vector<char> blob_host;
     PinnedBuf staging[2];
     cudaEvent_t staging_ev[2] = {};
@@ -171,6 +177,11 @@ struct gsim_gpu_context {
     EncodeParams pending_enc{};
     bool pending_enc_only = false;
     DevBuf<uint8_t> enc_buf;
+    // render_at: device pose playback of the frame in flight (tracks.cu)
+    const gsim_gpu_tracks* frame_tracks = nullptr;
+    double frame_time = 0.0;
+    const int64_t* frame_node_track = nullptr;
+    DevBuf<char> query_buf;
     DevBuf<float> enc_src;
     DevBuf<EncodeCam> enc_cams;
     // outputs / API scratch
@@ -181,6 +192,12 @@ struct gsim_gpu_context {
 
     uint32_t epoch = 0;
     uint64_t launches_total = 0;
+
+    // scenes and tracks created on this context: destroying the context orphans them (their
+    // ctx becomes null and only their own memory is freed later), so handle lifetimes may end
+    // in any order
+    std::set<gsim_gpu_scene*> scenes;
+    std::set<gsim_gpu_tracks*> tracks;
 
     // last frame, for stats and the tile-list hook
     gsim_render_stats stats{};
@@ -200,6 +217,13 @@ struct gsim_gpu_scene {
     gsim_gpu_context* ctx = nullptr;
     DevField f{};
     void* mem = nullptr;
+};
+
+struct gsim_gpu_tracks {
+    gsim_gpu_context* ctx = nullptr;
+    void* mem = nullptr;
+    DevTracks d{};
+    uint64_t n_tracks = 0, n_records = 0;
 };
 
 namespace {
@@ -353,6 +377,7 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         }
         s.entry_count = uint32_t(p.entries.size()) - s.entry_begin;
         p.segs.push_back(s);
+        p.seg_owner.push_back(int32_t(iv.owner));
     }
     finish_cameras(p, cameras, n_cams);
     // Record key = camera index above the float32 depth bits rebased to [near_min, far_max]:
@@ -411,6 +436,7 @@ void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
     const size_t o_tx = append_bytes(blob, p.tiles_x);
     const size_t o_seg = append_bytes(blob, p.segs);
     const size_t o_ent = append_bytes(blob, p.entries);
+    const size_t o_st = append_bytes(blob, p.seg_track);
     const int k = ctx->staging_index;
     ctx->staging_index ^= 1;
     GSIM_CK(cudaEventSynchronize(ctx->staging_ev[k]));  // its copy (two frames ago) landed
@@ -429,6 +455,7 @@ void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
     ctx->cam_tiles_x = reinterpret_cast<int*>(d + o_tx);
     ctx->segs = reinterpret_cast<DevSegment*>(d + o_seg);
     ctx->entries = reinterpret_cast<SegEntry*>(d + o_ent);
+    ctx->seg_track = p.seg_track.empty() ? nullptr : reinterpret_cast<int32_t*>(d + o_st);
 }
 
 void record_ev(gsim_gpu_context* ctx, int e) {
@@ -711,8 +738,25 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     plan = build_plan(scene->f.n, nodes, n_nodes, cameras, n_cams);
     gsim_raster_options opt{0, 0, 1e-4};
     if (options) opt = *options;
+    bool posed = false;
+    if (ctx->frame_tracks) {  // render_at: which segments a track drives
+        plan.seg_track.resize(plan.segs.size(), -1);
+        for (size_t k = 0; k < plan.segs.size(); ++k) {
+            const int32_t owner = plan.seg_owner[k];
+            if (owner >= 0 && ctx->frame_node_track[owner] >= 0) {
+                plan.seg_track[k] = int32_t(ctx->frame_node_track[owner]);
+                posed = true;
+            }
+        }
+        if (!posed) plan.seg_track.clear();
+    }
     reserve_workspace(ctx, plan);
     upload_plan(ctx, plan);
+    if (posed) {
+        launch_pose_segments(ctx->frame_tracks->d, ctx->segs, ctx->seg_track,
+                             uint32_t(plan.segs.size()), ctx->frame_time, ctx->stream);
+        check_launch();
+    }
     float* out = device_out;
     if (!out) {
         ctx->out.reserve(std::max<uint64_t>(plan.out_floats, 1));
@@ -720,7 +764,7 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     }
     record_ev(ctx, kEvStart);
     begin_frame(ctx, plan);
-    uint64_t launches = 0;
+    uint64_t launches = posed ? 1 : 0;
     PreprocessArgs pa = make_pre_args(ctx, scene, plan);
     if (plan.slots) {
         launch_preprocess(pa, false, ctx->num_sms * 3, ctx->stream);
@@ -890,6 +934,220 @@ void encode_device(gsim_gpu_context* ctx, const float* src, const uint32_t* widt
     }
 }
 
+// Device field of n primitives: 11 double planes, then ceil(3K/4) float4 SH planes whose base
+// stays 256-byte aligned for any n.
+gsim_gpu_scene* alloc_scene(gsim_gpu_context* ctx, uint64_t n, int degree) {
+    const int K = (degree + 1) * (degree + 1);
+    const int planes = (3 * K + 3) / 4;
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    const size_t geo_bytes = (11 * nn * sizeof(double) + 255) & ~size_t(255);
+    const size_t sh_bytes = size_t(planes) * nn * sizeof(float4);
+    auto* sc = new gsim_gpu_scene();
+    sc->ctx = ctx;
+    if (cudaMalloc(&sc->mem, geo_bytes + sh_bytes) != cudaSuccess) {
+        delete sc;
+        throw CudaError{"scene: device allocation of " + std::to_string(geo_bytes + sh_bytes) +
+                        " bytes failed"};
+    }
+    double* g = static_cast<double*>(sc->mem);
+    sc->f.n = n;
+    sc->f.sh_degree = degree;
+    sc->f.sh_planes = planes;
+    sc->f.mx = g + 0 * nn; sc->f.my = g + 1 * nn; sc->f.mz = g + 2 * nn;
+    sc->f.sx = g + 3 * nn; sc->f.sy = g + 4 * nn; sc->f.sz = g + 5 * nn;
+    sc->f.qw = g + 6 * nn; sc->f.qx = g + 7 * nn; sc->f.qy = g + 8 * nn; sc->f.qz = g + 9 * nn;
+    sc->f.opacity = g + 10 * nn;
+    sc->f.sh = reinterpret_cast<float4*>(static_cast<char*>(sc->mem) + geo_bytes);
+    ctx->scenes.insert(sc);  // callers hold ctx->mu (Guard)
+    return sc;
+}
+
+void discard_scene(gsim_gpu_context* ctx, gsim_gpu_scene* sc) {  // failed load / upload
+    ctx->scenes.erase(sc);
+    cudaFree(sc->mem);
+    delete sc;
+}
+
+// ---- splat PLY (splat_ply.cpp:40-162) ----------------------------------------------------------
+
+int sh_coeff_count(int degree) { return (degree + 1) * (degree + 1); }  // sh.hpp
+
+std::vector<std::string> ply_expected_properties(int degree) {  // splat_ply.cpp:19-28
+    std::vector<std::string> props = {"x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"};
+    const int rest = 3 * (sh_coeff_count(degree) - 1);
+    for (int i = 0; i < rest; ++i) props.push_back("f_rest_" + std::to_string(i));
+    props.push_back("opacity");
+    for (int i = 0; i < 3; ++i) props.push_back("scale_" + std::to_string(i));
+    for (int i = 0; i < 4; ++i) props.push_back("rot_" + std::to_string(i));
+    return props;
+}
+
+struct FileCloser {
+    void operator()(std::FILE* f) const { if (f) std::fclose(f); }
+};
+
+gsim_gpu_scene* load_ply(gsim_gpu_context* ctx, const std::string& path) {
+    std::unique_ptr<std::FILE, FileCloser> fp(std::fopen(path.c_str(), "rb"));
+    if (!fp) throw CudaError{"cannot open splat PLY '" + path + "'"};  // io_error -> status 1
+    const std::string who = "'" + path + "'";
+    auto getline = [&](std::string& line) {
+        line.clear();
+        int ch;
+        while ((ch = std::fgetc(fp.get())) != EOF && ch != '\n') line.push_back(char(ch));
+        return !(ch == EOF && line.empty());
+    };
+    std::string line;
+    if (!getline(line) || line != "ply") throw ValidationError{who + ": missing 'ply' magic"};
+    bool format_seen = false, element_seen = false, header_closed = false;
+    uint64_t count = 0;
+    std::vector<std::string> props;
+    while (getline(line)) {
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (line == "end_header") {
+            header_closed = true;
+            break;
+        }
+        // whitespace tokens, as operator>> on an istringstream would split the line
+        std::vector<std::string> words;
+        for (size_t i = 0; i < line.size();) {
+            while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+            size_t j = i;
+            while (j < line.size() && !std::isspace(static_cast<unsigned char>(line[j]))) ++j;
+            if (j > i) words.emplace_back(line, i, j - i);
+            i = j;
+        }
+        auto word = [&](size_t k) { return k < words.size() ? words[k] : std::string(); };
+        const std::string tok = word(0);
+        if (tok == "comment") continue;
+        if (tok == "format") {
+            const std::string fmt = word(1);
+            if (fmt != "binary_little_endian")
+                throw ValidationError{who + ": format must be binary_little_endian, got '" + fmt + "'"};
+            format_seen = true;
+        } else if (tok == "element") {
+            const std::string name = word(1);
+            count = std::strtoull(word(2).c_str(), nullptr, 10);
+            if (name != "vertex") throw ValidationError{who + ": unexpected element '" + name + "'"};
+            element_seen = true;
+        } else if (tok == "property") {
+            const std::string type = word(1), name = word(2);
+            if (type != "float")
+                throw ValidationError{who + ": property '" + name + "' must be float, got '" + type + "'"};
+            props.push_back(name);
+        } else if (!tok.empty()) {
+            throw ValidationError{who + ": unexpected header token '" + tok + "'"};
+        }
+    }
+    if (!header_closed) throw ValidationError{who + ": header missing end_header"};
+    if (!format_seen) throw ValidationError{who + ": header missing format line"};
+    if (!element_seen) throw ValidationError{who + ": header missing element vertex line"};
+    size_t rest_count = 0;
+    for (const auto& p : props)
+        if (p.rfind("f_rest_", 0) == 0) ++rest_count;
+    int degree = -1;
+    for (int d = 0; d <= 3; ++d)
+        if (rest_count == size_t(3 * (sh_coeff_count(d) - 1))) degree = d;
+    if (degree < 0)
+        throw ValidationError{who + ": f_rest property count " + std::to_string(rest_count) +
+                              " does not match any SH degree in [0,3]"};
+    const std::vector<std::string> expected = ply_expected_properties(degree);
+    for (size_t i = 0; i < expected.size(); ++i) {
+        if (i >= props.size()) throw ValidationError{who + ": missing property '" + expected[i] + "'"};
+        if (props[i] != expected[i])
+            throw ValidationError{who + ": expected property '" + expected[i] + "' at position " +
+                                  std::to_string(i) + ", found '" + props[i] + "'"};
+    }
+    if (props.size() > expected.size())
+        throw ValidationError{who + ": unexpected extra property '" + props[expected.size()] + "'"};
+    if (count >= 0xFFFFFFFFull) throw ValidationError{who + ": more than 2^32 - 1 primitives"};
+
+    // Payload: pinned double-buffered chunks, disk read of chunk k+1 overlapping the H2D of k.
+    const int stride = int(expected.size());
+    const uint64_t bytes = count * uint64_t(stride) * sizeof(float);
+    DevBuf<char> raw;
+    PinnedBuf stage[2];
+    struct Release {  // scratch of this call only, released on every path
+        DevBuf<char>& raw;
+        PinnedBuf* stage;
+        ~Release() { raw.release(); stage[0].release(); stage[1].release(); }
+    } release{raw, stage};
+    raw.reserve(std::max<uint64_t>(bytes, 4));
+    constexpr size_t kChunk = size_t(32) << 20;
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() { for (int k = 0; k < 2; ++k) if (e[k]) cudaEventDestroy(e[k]); }
+    } evg{done};
+    for (int k = 0; k < 2; ++k) {
+        stage[k].reserve(std::min<uint64_t>(std::max<uint64_t>(bytes, 64), kChunk));
+        GSIM_CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    }
+    uint64_t off = 0;
+    int k = 0;
+    bool truncated = false;
+    while (off < bytes) {
+        const size_t want = size_t(std::min<uint64_t>(kChunk, bytes - off));
+        GSIM_CK(cudaEventSynchronize(done[k]));
+        const size_t got = std::fread(stage[k].ptr, 1, want, fp.get());
+        if (got) {
+            GSIM_CK(cudaMemcpyAsync(raw.ptr + off, stage[k].ptr, got, cudaMemcpyHostToDevice, ctx->stream));
+            GSIM_CK(cudaEventRecord(done[k], ctx->stream));
+        }
+        off += got;
+        if (got != want) {
+            truncated = true;
+            break;
+        }
+        k ^= 1;
+    }
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    if (truncated) throw ValidationError{who + ": payload truncated"};
+    gsim_gpu_scene* sc = alloc_scene(ctx, count, degree);
+    ctx->counts.reserve(4);
+    unsigned long long* err = ctx->counts.ptr + 3;
+    GSIM_CK(cudaMemsetAsync(err, 0xFF, sizeof(unsigned long long), ctx->stream));
+    PlyArgs a{};
+    a.rows = reinterpret_cast<const float*>(raw.ptr);
+    a.n = count;
+    a.stride = stride;
+    a.degree = degree;
+    a.field = sc->f;
+    a.plane_stride = std::max<uint64_t>(count, 1);
+    a.err = err;
+    launch_ply_convert(a, ctx->num_sms * 8, ctx->stream);
+    unsigned long long e = ~0ull;
+    try {
+        check_launch();
+        GSIM_CK(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        discard_scene(ctx, sc);
+        throw;
+    }
+    if (e != ~0ull) {
+        discard_scene(ctx, sc);
+        static const char* what[] = {"", "non-finite value", "opacity saturates", "scale overflows",
+                                     "zero-norm rotation"};
+        throw ValidationError{who + ": " + what[e & 7] + " in primitive " + std::to_string(e >> 3)};
+    }
+    ctx->launches_total += 1;
+    return sc;
+}
+
+// D2H of the internal output buffer into host RenderTargets (the drop-in's by-value return).
+void copy_targets(gsim_gpu_context* ctx, const gsim_camera* cameras, uint64_t n,
+                  const std::vector<uint64_t>& off, gsim_target* outs) {
+    for (uint64_t c = 0; c < n; ++c) {
+        const size_t npx = size_t(cameras[c].width) * cameras[c].height;
+        const float* base = ctx->out.ptr + off[c];
+        GSIM_CK(cudaMemcpyAsync(outs[c].rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaMemcpyAsync(outs[c].depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaMemcpyAsync(outs[c].accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->stats.d2h_bytes += 5 * npx * sizeof(float);
+    }
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
+}
+
 struct Guard {
     gsim_gpu_context* ctx;
     explicit Guard(gsim_gpu_context* c) : ctx(c) {}
@@ -996,6 +1254,16 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->full_vis.release();
     ctx->splats_in.release();
     ctx->readback.release();
+    ctx->srgb_thr.release();
+    ctx->enc_buf.release();
+    ctx->enc_src.release();
+    ctx->enc_cams.release();
+    ctx->query_buf.release();
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        for (auto* sc : ctx->scenes) sc->ctx = nullptr;
+        for (auto* tr : ctx->tracks) tr->ctx = nullptr;
+    }
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->staging_ev)
@@ -1061,9 +1329,6 @@ int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_
         const int K = (v->sh_degree + 1) * (v->sh_degree + 1);
         const int planes = (3 * K + 3) / 4;
         const uint64_t nn = std::max<uint64_t>(n, 1);
-        // SH planes are float4: keep their base 256-byte aligned whatever n is
-        const size_t geo_bytes = (11 * nn * sizeof(double) + 255) & ~size_t(255);
-        const size_t sh_bytes = size_t(planes) * nn * sizeof(float4);
         std::vector<double> geo(11 * nn, 0.0);
         std::vector<float4> sh(size_t(planes) * nn, make_float4(0, 0, 0, 0));
         for (uint64_t i = 0; i < n; ++i) {
@@ -1088,28 +1353,58 @@ int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_
             for (int p = 0; p < planes; ++p)
                 sh[size_t(p) * nn + i] = make_float4(tmp[4 * p], tmp[4 * p + 1], tmp[4 * p + 2], tmp[4 * p + 3]);
         }
-        auto* sc = new gsim_gpu_scene();
-        sc->ctx = ctx;
+        gsim_gpu_scene* sc = alloc_scene(ctx, n, v->sh_degree);
         try {
-            GSIM_CK(cudaMalloc(&sc->mem, geo_bytes + sh_bytes));
-            GSIM_CK(cudaMemcpy(sc->mem, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
-            GSIM_CK(cudaMemcpy(static_cast<char*>(sc->mem) + geo_bytes, sh.data(), sh_bytes,
-                               cudaMemcpyHostToDevice));
+            GSIM_CK(cudaMemcpy(sc->f.mx, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
+            GSIM_CK(cudaMemcpy(sc->f.sh, sh.data(), sh.size() * sizeof(float4), cudaMemcpyHostToDevice));
         } catch (...) {
-            if (sc->mem) cudaFree(sc->mem);
-            delete sc;
+            discard_scene(ctx, sc);
             throw;
         }
-        double* g = static_cast<double*>(sc->mem);
-        sc->f.n = n;
-        sc->f.sh_degree = v->sh_degree;
-        sc->f.sh_planes = planes;
-        sc->f.mx = g + 0 * nn; sc->f.my = g + 1 * nn; sc->f.mz = g + 2 * nn;
-        sc->f.sx = g + 3 * nn; sc->f.sy = g + 4 * nn; sc->f.sz = g + 5 * nn;
-        sc->f.qw = g + 6 * nn; sc->f.qx = g + 7 * nn; sc->f.qy = g + 8 * nn; sc->f.qz = g + 9 * nn;
-        sc->f.opacity = g + 10 * nn;
-        sc->f.sh = reinterpret_cast<float4*>(static_cast<char*>(sc->mem) + geo_bytes);
         *out = sc;
+    });
+}
+
+int32_t gsim_gpu_scene_sh_degree(const gsim_gpu_scene* scene) { return scene ? scene->f.sh_degree : -1; }
+
+int gsim_gpu_scene_download_field(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                                  double* means, double* scales, double* rotations,
+                                  double* opacities, double* sh) {
+    return Guard(ctx).run([&] {
+        if (!scene) throw ValidationError{"scene_download_field: null scene"};
+        const uint64_t n = scene->f.n, nn = std::max<uint64_t>(n, 1);
+        const int K = (scene->f.sh_degree + 1) * (scene->f.sh_degree + 1);
+        std::vector<double> geo(11 * nn);
+        std::vector<float4> shp(size_t(scene->f.sh_planes) * nn);
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        GSIM_CK(cudaMemcpy(geo.data(), scene->f.mx, geo.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        GSIM_CK(cudaMemcpy(shp.data(), scene->f.sh, shp.size() * sizeof(float4), cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < n; ++i) {
+            for (int c = 0; c < 3; ++c) {
+                if (means) means[3 * i + c] = geo[c * nn + i];
+                if (scales) scales[3 * i + c] = geo[(3 + c) * nn + i];
+            }
+            for (int c = 0; c < 4; ++c)
+                if (rotations) rotations[4 * i + c] = geo[(6 + c) * nn + i];
+            if (opacities) opacities[i] = geo[10 * nn + i];
+            if (sh) {
+                double* o = sh + 48 * i;
+                for (int k = 0; k < 48; ++k) o[k] = 0.0;
+                for (int j = 0; j < 3 * K; ++j) {
+                    const float4 v = shp[size_t(j / 4) * nn + i];
+                    const float comp[4] = {v.x, v.y, v.z, v.w};
+                    o[(j / K) * 16 + (j % K)] = comp[j % 4];
+                }
+            }
+        }
+    });
+}
+
+int gsim_gpu_scene_load_ply(gsim_gpu_context* ctx, const char* path, gsim_gpu_scene** out) {
+    if (out) *out = nullptr;
+    return Guard(ctx).run([&] {
+        if (!path || !out) throw ValidationError{"scene_load_ply: null argument"};
+        *out = load_ply(ctx, path);
     });
 }
 
@@ -1119,6 +1414,7 @@ int gsim_gpu_scene_destroy(gsim_gpu_scene* scene) {
         std::lock_guard<std::mutex> lk(scene->ctx->mu);
         cudaSetDevice(scene->ctx->device);
         cudaStreamSynchronize(scene->ctx->stream);
+        scene->ctx->scenes.erase(scene);
     }
     if (scene->mem) cudaFree(scene->mem);
     delete scene;
@@ -1272,15 +1568,7 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
             throw ValidationError{"render: null argument"};
         const std::vector<uint64_t> off =
             render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, true);
-        for (uint64_t c = 0; c < n_cameras; ++c) {
-            const size_t npx = size_t(cameras[c].width) * cameras[c].height;
-            const float* base = ctx->out.ptr + off[c];
-            GSIM_CK(cudaMemcpyAsync(outs[c].rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-            GSIM_CK(cudaMemcpyAsync(outs[c].depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-            GSIM_CK(cudaMemcpyAsync(outs[c].accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-            ctx->stats.d2h_bytes += 5 * npx * sizeof(float);
-        }
-        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        copy_targets(ctx, cameras, n_cameras, off, outs);
     });
 }
 
@@ -1398,6 +1686,141 @@ int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
             GSIM_CK(cudaStreamSynchronize(ctx->stream));
             ctx->stats.d2h_bytes = bytes;
         }
+    });
+}
+
+int gsim_gpu_tracks_upload(gsim_gpu_context* ctx, const double* times, const double* translations,
+                           const double* rotations, const uint64_t* track_begin, uint64_t n_tracks,
+                           gsim_gpu_tracks** out) {
+    if (out) *out = nullptr;
+    return Guard(ctx).run([&] {
+        if (!out || (n_tracks && !track_begin)) throw ValidationError{"tracks: null argument"};
+        if (n_tracks >= (uint64_t(1) << 31)) throw ValidationError{"tracks: too many tracks"};
+        const uint64_t R = n_tracks ? track_begin[n_tracks] : 0;
+        if (n_tracks && track_begin[0] != 0) throw ValidationError{"tracks: track_begin[0] must be 0"};
+        if (R && (!times || !translations || !rotations)) throw ValidationError{"tracks: null record array"};
+        std::vector<double> q(4 * R);
+        for (uint64_t k = 0; k < n_tracks; ++k) {
+            if (track_begin[k + 1] < track_begin[k]) throw ValidationError{"tracks: track_begin decreases"};
+            for (uint64_t i = track_begin[k]; i < track_begin[k + 1]; ++i) {
+                // PoseStream::append (pose_stream.cpp:20-40)
+                const std::string who = "pose stream: track " + std::to_string(k);
+                if (!std::isfinite(times[i])) throw ValidationError{who + ": non-finite timestamp"};
+                for (int c = 0; c < 3; ++c)
+                    if (!std::isfinite(translations[3 * i + c])) throw ValidationError{who + ": non-finite pose"};
+                for (int c = 0; c < 4; ++c)
+                    if (!std::isfinite(rotations[4 * i + c])) throw ValidationError{who + ": non-finite pose"};
+                if (i > track_begin[k] && times[i] < times[i - 1])
+                    throw ValidationError{who + ": timestamps decrease"};
+                const dq n = qnormalized(dq{rotations[4 * i], rotations[4 * i + 1], rotations[4 * i + 2],
+                                            rotations[4 * i + 3]});
+                q[4 * i] = n.w; q[4 * i + 1] = n.x; q[4 * i + 2] = n.y; q[4 * i + 3] = n.z;
+            }
+        }
+        auto* tr = new gsim_gpu_tracks;
+        tr->ctx = ctx;
+        tr->n_tracks = n_tracks;
+        tr->n_records = R;
+        const size_t bt = 8 * R, bp = 24 * R, bq = 32 * R, bb = 8 * (n_tracks + 1);
+        if (cudaMalloc(&tr->mem, std::max<size_t>(bt + bp + bq + bb, 64)) != cudaSuccess) {
+            delete tr;
+            throw CudaError{"tracks: device allocation failed"};
+        }
+        char* m = static_cast<char*>(tr->mem);
+        std::vector<uint64_t> begin(n_tracks + 1, 0);
+        for (uint64_t k = 0; k <= n_tracks && n_tracks; ++k) begin[k] = track_begin[k];
+        if (R) {
+            GSIM_CK(cudaMemcpy(m, times, bt, cudaMemcpyHostToDevice));
+            GSIM_CK(cudaMemcpy(m + bt, translations, bp, cudaMemcpyHostToDevice));
+            GSIM_CK(cudaMemcpy(m + bt + bp, q.data(), bq, cudaMemcpyHostToDevice));
+        }
+        GSIM_CK(cudaMemcpy(m + bt + bp + bq, begin.data(), bb, cudaMemcpyHostToDevice));
+        tr->d.t = reinterpret_cast<const double*>(m);
+        tr->d.p = reinterpret_cast<const double*>(m + bt);
+        tr->d.q = reinterpret_cast<const double*>(m + bt + bp);
+        tr->d.begin = reinterpret_cast<const uint64_t*>(m + bt + bp + bq);
+        tr->d.n_tracks = uint32_t(n_tracks);
+        ctx->tracks.insert(tr);
+        *out = tr;
+    });
+}
+
+int gsim_gpu_tracks_destroy(gsim_gpu_tracks* tracks) {
+    if (!tracks) return GSIM_OK;
+    if (tracks->ctx) {
+        std::lock_guard<std::mutex> lk(tracks->ctx->mu);
+        cudaSetDevice(tracks->ctx->device);
+        cudaStreamSynchronize(tracks->ctx->stream);
+        tracks->ctx->tracks.erase(tracks);
+    }
+    if (tracks->mem) cudaFree(tracks->mem);
+    delete tracks;
+    return GSIM_OK;
+}
+
+uint64_t gsim_gpu_tracks_count(const gsim_gpu_tracks* tracks) { return tracks ? tracks->n_tracks : 0; }
+
+int gsim_gpu_tracks_sample(gsim_gpu_context* ctx, const gsim_gpu_tracks* tracks,
+                           const uint32_t* track, const double* time, const gsim_rigid* initial,
+                           uint64_t n, gsim_rigid* out) {
+    return Guard(ctx).run([&] {
+        if (!tracks || (n && (!track || !time || !initial || !out)))
+            throw ValidationError{"tracks_sample: null argument"};
+        for (uint64_t i = 0; i < n; ++i)
+            if (track[i] >= tracks->n_tracks)
+                throw ValidationError{"tracks_sample: query " + std::to_string(i) + " names track " +
+                                      std::to_string(track[i]) + " of " + std::to_string(tracks->n_tracks)};
+        if (!n) return;
+        const size_t b_tr = (4 * n + 15) & ~size_t(15), b_t = 8 * n, b_r = sizeof(gsim_rigid) * n;
+        ctx->query_buf.reserve(b_tr + b_t + 2 * b_r);
+        char* m = ctx->query_buf.ptr;
+        cudaStream_t s = ctx->stream;
+        GSIM_CK(cudaMemcpyAsync(m, track, 4 * n, cudaMemcpyHostToDevice, s));
+        GSIM_CK(cudaMemcpyAsync(m + b_tr, time, b_t, cudaMemcpyHostToDevice, s));
+        GSIM_CK(cudaMemcpyAsync(m + b_tr + b_t, initial, b_r, cudaMemcpyHostToDevice, s));
+        gsim_rigid* dout = reinterpret_cast<gsim_rigid*>(m + b_tr + b_t + b_r);
+        launch_track_query(tracks->d, reinterpret_cast<const uint32_t*>(m),
+                           reinterpret_cast<const double*>(m + b_tr),
+                           reinterpret_cast<const gsim_rigid*>(m + b_tr + b_t), dout, n,
+                           ctx->num_sms * 8, s);
+        check_launch();
+        GSIM_CK(cudaMemcpyAsync(out, dout, b_r, cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+        ctx->stats.launches = 1;
+        ctx->launches_total += 1;
+        ctx->stats.launches_total = ctx->launches_total;
+    });
+}
+
+int gsim_gpu_render_at(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                       const gsim_gpu_tracks* tracks, double time, const gsim_node* nodes,
+                       const int64_t* node_track, uint64_t n_nodes, const gsim_camera* cameras,
+                       uint64_t n_cameras, const gsim_raster_options* options, float* device_out,
+                       gsim_target* outs) {
+    return Guard(ctx).run([&] {
+        if (!scene || !tracks || (n_nodes && (!nodes || !node_track)) || (n_cameras && !cameras))
+            throw ValidationError{"render_at: null argument"};
+        if (!std::isfinite(time)) throw ValidationError{"render_at: non-finite time"};
+        for (uint64_t k = 0; k < n_nodes; ++k) {
+            if (node_track[k] < 0) continue;
+            if (uint64_t(node_track[k]) >= tracks->n_tracks)
+                throw ValidationError{"render_at: node " + std::to_string(k) + " names track " +
+                                      std::to_string(node_track[k]) + " of " +
+                                      std::to_string(tracks->n_tracks)};
+            if (nodes[k].kind == GSIM_NODE_BACKGROUND)  // scene.cpp:180-184
+                throw ValidationError{"pose stream drives background node " + std::to_string(k)};
+        }
+        struct Reset {
+            gsim_gpu_context* c;
+            ~Reset() { c->frame_tracks = nullptr; c->frame_node_track = nullptr; }
+        } reset{ctx};
+        ctx->frame_tracks = tracks;
+        ctx->frame_time = time;
+        ctx->frame_node_track = node_track;
+        const bool host = outs != nullptr;
+        const std::vector<uint64_t> off = render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras,
+                                                         options, host ? nullptr : device_out, host);
+        if (host) copy_targets(ctx, cameras, n_cameras, off, outs);
     });
 }
 

@@ -124,6 +124,27 @@ struct RasterArgs {
                                      // starts at enc.dst + out_offset / 5 * encoded_bpp
 };
 
+// Device pose tracks (tracks.cu): records of track k are begin[k] .. begin[k+1]-1.
+struct DevTracks {
+    const double* t;                 // [R] times, non-decreasing per track
+    const double* p;                 // [R][3] translations
+    const double* q;                 // [R][4] normalised rotations (w, x, y, z)
+    const uint64_t* begin;           // [n_tracks + 1]
+    uint32_t n_tracks;
+    uint32_t reserved;
+};
+
+// Splat PLY payload -> field planes (ply.cu).
+struct PlyArgs {
+    const float* rows;               // [n][stride] little-endian floats as on disk
+    uint64_t n;
+    int stride;
+    int degree;
+    DevField field;
+    uint64_t plane_stride;           // SH plane pitch (max(n, 1))
+    unsigned long long* err;         // min(i << 3 | code), ~0 when the file is valid
+};
+
 // Standalone encoder (encode.cu): one grid row per camera.
 struct EncodeCam {
     uint32_t width, height;
@@ -155,5 +176,11 @@ void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s);
 void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream);
 void launch_encode(const EncodeKernelArgs& a, uint32_t n_cams, uint32_t max_pixels,
                    cudaStream_t stream);
+void launch_track_query(const DevTracks& tr, const uint32_t* track, const double* time,
+                        const gsim_rigid* initial, gsim_rigid* out, uint64_t n, int grid_cap,
+                        cudaStream_t stream);
+void launch_ply_convert(const PlyArgs& a, int grid_cap, cudaStream_t stream);
+void launch_pose_segments(const DevTracks& tr, DevSegment* segs, const int32_t* seg_track,
+                          uint32_t n_segs, double t, cudaStream_t stream);
 
 }  // namespace gsim_gpu

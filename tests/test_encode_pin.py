@@ -160,3 +160,99 @@ def test_pose_sample_validation_matches_reference(oracle, ref):
     # empty track -> initial pose everywhere
     rc, o = oracle.pose_sample(np.zeros(0), np.zeros((0, 3)), np.zeros((0, 4)), init, [0.0, 5.0])
     assert rc == 0 and np.array_equal(o[0], [1, 0, 0, 0, 0, 0, 0])
+
+
+# ---- splat PLY (splat_ply.cpp:40-162) ------------------------------------------------------
+
+PLY_FIELDS = ("means", "scales", "rotations", "opacities", "sh")
+
+
+def ply_bytes(n, degree, rows=None, header_edit=None, payload_floats=None, seed=0):
+    """A splat PLY in the reference's layout (header + float rows), editable for error cases."""
+    K = (degree + 1) ** 2
+    props = ["x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"]
+    props += [f"f_rest_{i}" for i in range(3 * (K - 1))]
+    props += ["opacity", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"]
+    lines = ["ply", "format binary_little_endian 1.0", f"element vertex {n}"]
+    lines += [f"property float {p}" for p in props] + ["end_header"]
+    if header_edit:
+        lines = header_edit(lines)
+    if rows is None:
+        rng = np.random.default_rng(seed)
+        rows = rng.normal(size=(n, len(props))).astype(np.float32)
+        rows[:, -4:] = rng.normal(size=(n, 4))  # unnormalised rotations
+        rows[: n // 3, -4:] /= np.linalg.norm(rows[: n // 3, -4:], axis=1, keepdims=True)
+        rows[:, -7:-4] = rng.uniform(-6, -1, (n, 3))  # log scales
+    data = np.asarray(rows, dtype=np.float32).tobytes()
+    if payload_floats is not None:
+        data = data[: 4 * payload_floats]
+    return ("\n".join(lines) + "\n").encode() + data
+
+
+def test_ply_loader_matches_reference(oracle, ref, tmp_path):
+    for degree in range(4):
+        for n in (0, 1, 257):
+            p = tmp_path / f"f{degree}_{n}.ply"
+            p.write_bytes(ply_bytes(n, degree, seed=degree * 10 + n))
+            rc_o, fo = oracle.load_splat_ply(p)
+            rc_r, fr = ref.load_splat_ply(p)
+            assert rc_o == rc_r == 0, (degree, n)
+            assert fo.sh_degree == fr.sh_degree == degree
+            for k in PLY_FIELDS:
+                assert np.array_equal(getattr(fo, k), getattr(fr, k)), (degree, n, k)
+    # the reference's own writer -> both loaders (save->load is exact, splat_ply.hpp:22-24)
+    field = oracle.random_field(77, 300, 2.0, 0.01, 0.3, 3)
+    p = tmp_path / "saved.ply"
+    assert ref.save_splat_ply(p, field) == 0
+    rc_o, fo = oracle.load_splat_ply(p)
+    rc_r, fr = ref.load_splat_ply(p)
+    assert rc_o == rc_r == 0
+    for k in PLY_FIELDS:
+        assert np.array_equal(getattr(fo, k), getattr(fr, k)), k
+
+
+def ply_error_cases(n=20, degree=1):
+    K = (degree + 1) ** 2
+    stride = 17 + 3 * (K - 1)
+    rng = np.random.default_rng(3)
+    good = np.frombuffer(ply_bytes(n, degree, seed=3).split(b"end_header\n", 1)[1], np.float32).reshape(n, stride)
+
+    def rows_with(i, col, v):
+        r = good.copy()
+        r[i, col] = v
+        return r
+
+    def edit(fn):
+        return lambda lines: fn(list(lines))
+
+    return {
+        "magic": ply_bytes(n, degree, header_edit=edit(lambda l: ["plyx"] + l[1:])),
+        "ascii": ply_bytes(n, degree, header_edit=edit(lambda l: [l[0], "format ascii 1.0"] + l[2:])),
+        "no_end": ply_bytes(0, degree, header_edit=edit(lambda l: l[:-1])),
+        "no_format": ply_bytes(n, degree, header_edit=edit(lambda l: [l[0]] + l[2:])),
+        "face": ply_bytes(n, degree, header_edit=edit(lambda l: l[:2] + ["element face 3"] + l[3:])),
+        "double": ply_bytes(n, degree, header_edit=edit(lambda l: l[:3] + ["property double x"] + l[4:])),
+        "order": ply_bytes(n, degree, header_edit=edit(lambda l: l[:3] + [l[4], l[3]] + l[5:])),
+        "extra": ply_bytes(n, degree, header_edit=edit(lambda l: l[:-1] + ["property float extra", l[-1]])),
+        "rest5": ply_bytes(n, degree, header_edit=edit(lambda l: [x for x in l if x != "property float f_rest_8"])),
+        "token": ply_bytes(n, degree, header_edit=edit(lambda l: l[:2] + ["bogus"] + l[2:])),
+        "truncated": ply_bytes(n, degree, payload_floats=n * stride - 1),
+        "nonfinite": ply_bytes(n, degree, rows=rows_with(7, 4, np.nan)),
+        "saturated": ply_bytes(n, degree, rows=rows_with(5, stride - 8, 60.0)),
+        "scale_inf": ply_bytes(n, degree, rows=rows_with(9, stride - 6, 800.0)),
+        "zero_rot": ply_bytes(n, degree, rows=np.concatenate([good[:4], np.hstack([good[4:5, :-4], np.zeros((1, 4), np.float32)]), good[5:]])),
+        "comment_crlf": ply_bytes(n, degree, header_edit=edit(lambda l: [l[0], "comment hi\r"] + [x + "\r" for x in l[1:]])),
+    }
+
+
+def test_ply_loader_errors_match_reference(oracle, ref, tmp_path):
+    for name, data in ply_error_cases().items():
+        p = tmp_path / f"{name}.ply"
+        p.write_bytes(data)
+        rc_o, _ = oracle.load_splat_ply(p)
+        rc_r, _ = ref.load_splat_ply(p)
+        assert rc_o == rc_r, (name, rc_o, rc_r)
+        assert rc_r == (0 if name == "comment_crlf" else 2), (name, rc_r)
+    rc_o, _ = oracle.load_splat_ply(tmp_path / "missing.ply")
+    rc_r, _ = ref.load_splat_ply(tmp_path / "missing.ply")
+    assert rc_o == rc_r == 1
