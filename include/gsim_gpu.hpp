@@ -8,19 +8,29 @@
 //   gsim::gpu::rasterize(splats, camera, options)       gsim::rasterize (raster.hpp:59-60)
 //   gsim::gpu::transform_primitives(field, range, t)    gsim::transform_primitives
 //                                                       (gaussian.hpp:76-77)
+//   gsim::gpu::encode(target, options)                  the bytes write_png_rgb8 / gray8 /
+//                                                       gray16 / write_pfm produce
+//                                                       (image_io.hpp:16-33)
+//   Renderer::load_ply(path)                            load_splat_ply (splat_ply.hpp:20)
+//   PoseTracks + Renderer::render_at(tracks, t, ...)    PoseStream::sample + Scene::step_to
+//                                                       (pose_stream.hpp:41-45, scene.cpp:176)
+//   Renderer::render_encoded(...)                       render + encode fused on the GPU
 //
 // Errors are rethrown as the reference's gsim::validation_error (status 2) and gsim::io_error
 // (status 1). The free functions upload the field on every call (a pure function of their
 // inputs, like the reference); gsim::gpu::Renderer keeps it resident in HBM for the fast path.
 #pragma once
 
+#include <cstdint>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "gsim/errors.hpp"
 #include "gsim/gaussian.hpp"
+#include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
 #include "gsim_gpu.h"
 
@@ -80,6 +90,35 @@ inline gsim_raster_options options(const RasterOptions& o) {
 }
 
 }  // namespace detail
+
+// Which writer outputs to produce (gsim_gpu.h GSIM_ENCODE_*); the defaults are the reference
+// CLI's render outputs (tools/gsim.cpp:60-65).
+struct EncodeOptions {
+    uint32_t flags = GSIM_ENCODE_RGB8 | GSIM_ENCODE_ALPHA8 | GSIM_ENCODE_DEPTH16 | GSIM_ENCODE_DEPTH_PFM;
+    bool srgb = true;
+    double depth_scale = 1000.0;
+    gsim_encode_options c() const { return gsim_encode_options{flags, srgb ? 1 : 0, depth_scale}; }
+};
+
+class Renderer;
+
+// Device-resident pose tracks built from PoseStream records (the PoseStream(records)
+// constructor's input, pose_stream.hpp:28): one track per node id, records in input order.
+class PoseTracks {
+public:
+    PoseTracks(Renderer& r, const std::vector<PoseRecord>& records);
+    // index of the node's track, -1 when the stream does not drive it
+    int64_t track_of(const std::string& node) const {
+        const auto it = index_.find(node);
+        return it == index_.end() ? -1 : int64_t(it->second);
+    }
+    const gsim_gpu_tracks* handle() const { return tracks_.get(); }
+
+private:
+    struct Del { void operator()(gsim_gpu_tracks* t) const { gsim_gpu_tracks_destroy(t); } };
+    std::unique_ptr<gsim_gpu_tracks, Del> tracks_;
+    std::map<std::string, std::size_t> index_;
+};
 
 // One device context plus (optionally) a resident scene.
 class Renderer {
@@ -144,6 +183,71 @@ public:
         return t;
     }
 
+    // load_splat_ply straight into HBM (replaces a previously uploaded field).
+    void load_ply(const std::string& path) {
+        gsim_gpu_scene* s = nullptr;
+        detail::check(gsim_gpu_scene_load_ply(ctx_.get(), path.c_str(), &s), ctx_.get());
+        scene_.reset(s);
+    }
+
+    // render + the writers' bytes, fused on the GPU; per camera the enabled parts in
+    // GSIM_ENCODE_* order.
+    std::vector<uint8_t> render_encoded(const std::vector<SceneNode>& nodes,
+                                        const std::vector<CameraModel>& cameras,
+                                        const RasterOptions& options = {},
+                                        const EncodeOptions& encode = {}) {
+        const auto ns = detail::nodes(nodes);
+        std::vector<gsim_camera> cs;
+        uint64_t bytes = 0;
+        for (const auto& c : cameras) {
+            cs.push_back(detail::camera(c));
+            bytes += gsim_gpu_encoded_bytes(encode.flags, c.width, c.height);
+        }
+        std::vector<uint8_t> out(bytes);
+        const gsim_raster_options o = detail::options(options);
+        const gsim_encode_options e = encode.c();
+        detail::check(gsim_gpu_render_encoded(ctx_.get(), scene_.get(), ns.data(), ns.size(), cs.data(),
+                                              cs.size(), &o, &e, out.data(), 0),
+                      ctx_.get());
+        return out;
+    }
+
+    // Scene::step_to(stream, t) + render_all: nodes named in the tracks take their pose at t
+    // (their pose in `nodes` is the initial pose), sampled on the GPU.
+    std::vector<RenderTarget> render_at(const PoseTracks& tracks, double t,
+                                        const std::vector<SceneNode>& nodes,
+                                        const std::vector<CameraModel>& cameras,
+                                        const RasterOptions& options = {}) {
+        const auto ns = detail::nodes(nodes);
+        std::vector<int64_t> node_track;
+        for (const auto& n : nodes) node_track.push_back(tracks.track_of(n.id));
+        std::vector<gsim_camera> cs;
+        for (const auto& c : cameras) cs.push_back(detail::camera(c));
+        std::vector<RenderTarget> targets;
+        std::vector<gsim_target> outs;
+        targets.reserve(cameras.size());
+        for (const auto& c : cameras) targets.emplace_back(c.width, c.height);
+        for (auto& tg : targets)
+            outs.push_back(gsim_target{tg.rgb.data.data(), tg.depth.data.data(), tg.accum_alpha.data.data()});
+        const gsim_raster_options o = detail::options(options);
+        detail::check(gsim_gpu_render_at(ctx_.get(), scene_.get(), tracks.handle(), t, ns.data(),
+                                         node_track.data(), ns.size(), cs.data(), cs.size(), &o,
+                                         nullptr, outs.data()),
+                      ctx_.get());
+        return targets;
+    }
+
+    // The writers' bytes of one RenderTarget.
+    std::vector<uint8_t> encode(const RenderTarget& t, const EncodeOptions& encode = {}) {
+        std::vector<uint8_t> out(gsim_gpu_encoded_bytes(encode.flags, t.depth.width, t.depth.height));
+        const gsim_encode_options e = encode.c();
+        detail::check(gsim_gpu_encode_host(ctx_.get(), t.depth.width, t.depth.height, t.rgb.data.data(),
+                                           t.depth.data.data(), t.accum_alpha.data.data(), &e,
+                                           out.data()),
+                      ctx_.get());
+        return out;
+    }
+
     gsim_gpu_context* context() { return ctx_.get(); }
     gsim_gpu_scene* scene() { return scene_.get(); }
 
@@ -153,6 +257,34 @@ private:
     std::unique_ptr<gsim_gpu_context, CtxDel> ctx_;
     std::unique_ptr<gsim_gpu_scene, SceneDel> scene_;
 };
+
+inline PoseTracks::PoseTracks(Renderer& r, const std::vector<PoseRecord>& records) {
+    std::vector<std::vector<const PoseRecord*>> per;
+    for (const auto& rec : records) {
+        auto it = index_.find(rec.node);
+        if (it == index_.end()) {
+            it = index_.emplace(rec.node, per.size()).first;
+            per.emplace_back();
+        }
+        per[it->second].push_back(&rec);
+    }
+    std::vector<double> t, p, q;
+    std::vector<uint64_t> begin{0};
+    for (const auto& track : per) {
+        for (const PoseRecord* rec : track) {
+            t.push_back(rec->t);
+            p.insert(p.end(), {rec->pose.translation.x, rec->pose.translation.y, rec->pose.translation.z});
+            q.insert(q.end(), {rec->pose.rotation.w, rec->pose.rotation.x, rec->pose.rotation.y,
+                               rec->pose.rotation.z});
+        }
+        begin.push_back(t.size());
+    }
+    gsim_gpu_tracks* h = nullptr;
+    detail::check(gsim_gpu_tracks_upload(r.context(), t.data(), p.data(), q.data(), begin.data(),
+                                         per.size(), &h),
+                  r.context());
+    tracks_.reset(h);
+}
 
 inline Renderer& default_renderer() {
     static Renderer r(0);
@@ -196,6 +328,12 @@ inline void transform_primitives(GaussianField& field, const IndexRange& range,
         p.mean = Vec3(means[3 * i], means[3 * i + 1], means[3 * i + 2]);
         p.rotation = Quat(rots[4 * i], rots[4 * i + 1], rots[4 * i + 2], rots[4 * i + 3]);
     }
+}
+
+// The bytes gsim::write_png_rgb8 (srgb), write_png_gray8, write_png_gray16 (scale) and write_pfm
+// would write for `t` (GSIM_ENCODE_* order), encoded on the GPU.
+inline std::vector<uint8_t> encode(const RenderTarget& t, const EncodeOptions& options = {}) {
+    return default_renderer().encode(t, options);
 }
 
 }  // namespace gsim::gpu

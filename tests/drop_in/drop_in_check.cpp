@@ -4,11 +4,18 @@
 // run by tests/test_gpu_dropin.py on a GPU box).
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <iterator>
+#include <string>
 #include <vector>
 
 #include "gsim/gaussian.hpp"
+#include "gsim/image_io.hpp"
+#include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
+#include "gsim/splat_ply.hpp"
 #include "gsim_gpu.hpp"
+#include "png.h"  // oracle/png_capture: the row bytes the reference writers hand to libpng
 #include "test_oracles.hpp"
 
 using namespace gsim;
@@ -104,6 +111,93 @@ int main() {
     try { gpu::render(field, nodes, {bad}); } catch (const validation_error&) { gpu_threw = true; }
     std::printf("validation_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
     if (!ref_threw || !gpu_threw) ++failures;
+
+    // encode: gsim::gpu::encode bytes == what write_png_rgb8(srgb) / gray8 / gray16(1000) /
+    // write_pfm write for the reference's own render target
+    {
+        const RenderTarget& t = ref[0];
+        const std::vector<uint8_t> enc = gpu::encode(t);
+        std::vector<uint8_t> want;
+        auto capture = [&]() {
+            std::size_t n = 0;
+            const unsigned char* b = png_capture_last(nullptr, nullptr, nullptr, nullptr, &n);
+            want.insert(want.end(), b, b + n);
+        };
+        write_png_rgb8("/dev/null", t.rgb, true);
+        capture();
+        write_png_gray8("/dev/null", t.accum_alpha);
+        capture();
+        write_png_gray16("/dev/null", t.depth, 1000.0);
+        capture();
+        const std::string pfm = "/tmp/drop_in_check_depth.pfm";
+        write_pfm(pfm, t.depth);
+        std::ifstream in(pfm, std::ios::binary);
+        std::vector<uint8_t> file((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        const std::string head = "Pf\n" + std::to_string(t.depth.width) + " " +
+                                 std::to_string(t.depth.height) + "\n-1.0\n";
+        want.insert(want.end(), file.begin() + head.size(), file.end());
+        std::size_t diff = enc.size() == want.size() ? 0 : 1;
+        for (std::size_t i = 0; i < enc.size() && i < want.size(); ++i) diff += enc[i] != want[i];
+        std::printf("encode: %zu bytes, %zu differ from the reference writers\n", enc.size(), diff);
+        if (diff) ++failures;
+        // fused render + encode == encode of the GPU's float render
+        gpu::Renderer r(field);
+        const std::vector<uint8_t> fused = r.render_encoded(nodes, {cams[0]});
+        const std::vector<uint8_t> sep = r.encode(r.render(nodes, {cams[0]})[0]);
+        std::printf("render_encoded: %s\n", fused == sep ? "equal" : "DIFFERENT");
+        if (fused != sep) ++failures;
+    }
+
+    // splat PLY: the reference writes the field, both load it and render
+    {
+        const std::string ply = "/tmp/drop_in_check_field.ply";
+        save_splat_ply(field, ply);
+        const GaussianField loaded = load_splat_ply(ply);
+        gpu::Renderer r;
+        r.load_ply(ply);
+        const auto a = render(loaded, nodes, cams);
+        const auto b = r.render(nodes, cams);
+        for (int k = 0; k < 2; ++k) {
+            const double f = frac_within(b[k], a[k], 2e-3, 1e-3);
+            std::printf("load_ply + render camera %d: %.5f of pixels within tolerance\n", k, f);
+            if (f < 0.999) ++failures;
+        }
+        bool ref_threw = false, gpu_threw = false;
+        try { load_splat_ply("/tmp/does_not_exist.ply"); } catch (const io_error&) { ref_threw = true; }
+        try { r.load_ply("/tmp/does_not_exist.ply"); } catch (const io_error&) { gpu_threw = true; }
+        std::printf("load_ply io_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
+        if (!ref_threw || !gpu_threw) ++failures;
+    }
+
+    // pose playback: PoseStream::sample on the host vs render_at sampling on the GPU
+    {
+        std::vector<PoseRecord> recs;
+        for (int i = 0; i < 6; ++i) {
+            PoseRecord rec;
+            rec.t = 0.25 * i;
+            rec.node = "obj";
+            rec.pose = RigidTransform{Quat::from_axis_angle({0.2, 1, 0.3}, 0.5 * i),
+                                      {0.1 * i, -0.05 * i, 0.02 * i}};
+            recs.push_back(rec);
+        }
+        const PoseStream stream(recs);
+        gpu::Renderer r(field);
+        const gpu::PoseTracks tracks(r, recs);
+        for (double t : {-1.0, 0.3, 0.8, 9.0}) {
+            std::vector<SceneNode> posed = nodes;
+            posed[1].pose = stream.sample("obj", t, nodes[1].pose);
+            const auto a = render(field, posed, cams);
+            const auto b = r.render_at(tracks, t, nodes, cams);
+            for (int k = 0; k < 2; ++k) {
+                const double f = frac_within(b[k], a[k], 2e-3, 1e-3);
+                if (f < 0.999) {
+                    std::printf("render_at t=%.2f camera %d: %.5f within tolerance\n", t, k, f);
+                    ++failures;
+                }
+            }
+        }
+        std::printf("render_at: 4 times x 2 cameras checked against PoseStream::sample + render\n");
+    }
 
     std::printf(failures ? "DROP-IN FAILED\n" : "DROP-IN OK\n");
     return failures ? 1 : 0;
