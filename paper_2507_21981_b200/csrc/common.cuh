@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace gsim_gpu {
@@ -66,12 +67,50 @@ struct SegEntry {
     uint64_t slot_base;
 };
 
-// 48-byte splat record, one per (camera, primitive) slot, read by duplication and raster.
+// 48-byte splat record, one per (camera, primitive) slot, in the form K4 consumes it (it is
+// copied global -> shared with three 16-byte cp.async and used as is):
 struct alignas(16) Record {
-    float4 a;  // u, v, view_depth, radius
-    float4 b;  // inv_xx, inv_xy, inv_yy, alpha_peak
-    float4 c;  // r, g, b, tile rect (tx0 | ty0 << 8 | tx1 << 16 | ty1 << 24) as bits
+    float4 a;  // u, v, radius, log2(alpha_peak)
+    float4 b;  // conic prescaled for ex2: -inv_xx*log2(e)/2, -inv_xy*log2(e), -inv_yy*log2(e)/2,
+               // view_depth
+    float4 c;  // r, g, b, reach: half2 (ex, ey) rounded up = half-extents of the region where
+               // the splat can pass the raster's box test AND reach alpha >= 1/255; -inf if
+               // it can reach it nowhere
 };
+
+constexpr float kLog2eF = 1.4426950408889634f;
+
+// Builds the raster record from the fp32 projection (u, v, depth, radius, inverse covariance,
+// peak alpha, rgb). The exponent of ex2 is then log2(o) + dx*(A*dx + B*dy) + C*dy*dy, i.e.
+// log2(o * exp(-q/2)) with q = inv_xx dx^2 + 2 inv_xy dx dy + inv_yy dy^2 (raster.cpp:291-293).
+__device__ inline Record make_record(float u, float v, float z, float rad, float ia, float ib,
+                                     float ic, float op, float r, float g, float b) {
+    Record rec;
+    rec.a = make_float4(u, v, rad, __log2f(op));
+    rec.b = make_float4(ia * (-0.5f * kLog2eF), ib * -kLog2eF, ic * (-0.5f * kLog2eF), z);
+    // Reachable half-extents: the box test bounds |dx|,|dy| <= r; alpha >= 1/255 needs
+    // q <= qc = 2 ln(255 o), whose ellipse has half-extents sqrt(qc * cov_xx/yy) (conservatively
+    // widened), so no contributing splat is ever culled by them.
+    float ex = rad, ey = rad;
+    if (!(op * 255.0f >= 1.0f)) {
+        ex = ey = -INFINITY;  // can never reach alpha 1/255
+    } else {
+        // approximate MUFU ops are fine here: the bound is widened by 1% + 0.05 px
+        const float qc = 2.0f * __logf(op * 255.0f);
+        const float det = ia * ic - ib * ib;
+        if (det > 0.0f) {
+            float inv, sx, sy;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(det));
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sx) : "f"(qc * ic * inv));
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sy) : "f"(qc * ia * inv));
+            ex = fminf(ex, sx * 1.01f + 0.05f);
+            ey = fminf(ey, sy * 1.01f + 0.05f);
+        }
+    }
+    const __half2 reach = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
+    rec.c = make_float4(r, g, b, *reinterpret_cast<const float*>(&reach));
+    return rec;
+}
 
 __host__ __device__ inline uint32_t pack_rect(int tx0, int ty0, int tx1, int ty1) {
     return uint32_t(tx0) | (uint32_t(ty0) << 8) | (uint32_t(tx1) << 16) | (uint32_t(ty1) << 24);

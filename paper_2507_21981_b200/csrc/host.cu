@@ -135,6 +135,9 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> radix_counts;   // [256][chunks] per-chunk digit counts (reduce-then-scan)
     DevBuf<uint32_t> radix_totals;   // [256]
     bool use_onesweep = true;        // GSIM_GPU_ONESWEEP=0: reduce-then-scan passes instead
+    int raster_rect_w = 8;           // GSIM_GPU_RASTER_RECT=16: 16x4 warp bands in K4 (default 8x8)
+    int raster_exact_cull = 1;       // GSIM_GPU_RASTER_EXACT=0: bounding-box warp culling only
+    int raster_batch = 128;          // GSIM_GPU_RASTER_BATCH=256: larger K4 batches, fewer CTAs/SM
     // per-pair plane (final per-tile order)
     DevBuf<uint32_t> vals;
     uint64_t pair_capacity = 0;
@@ -566,6 +569,9 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.capacity = ctx->pair_capacity;
     rr.n_slots = std::max<uint64_t>(p.slots, 1);
     rr.enc = ctx->frame_enc;
+    rr.rect_w = ctx->raster_rect_w;
+    rr.batch = ctx->raster_batch;
+    rr.exact_cull = ctx->raster_exact_cull;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
@@ -1203,6 +1209,9 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         ctx->counts.reserve(4);
         ctx->readback.reserve(64);
         if (const char* e = std::getenv("GSIM_GPU_ONESWEEP")) ctx->use_onesweep = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GSIM_GPU_RASTER_RECT")) ctx->raster_rect_w = std::atoi(e) == 16 ? 16 : 8;
+        if (const char* e = std::getenv("GSIM_GPU_RASTER_EXACT")) ctx->raster_exact_cull = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
         if (const char* e = std::getenv("GSIM_GPU_INITIAL_PAIR_CAPACITY")) {
             ctx->fixed_initial_capacity = std::strtoull(e, nullptr, 10);
             ctx->pair_capacity = ctx->fixed_initial_capacity;

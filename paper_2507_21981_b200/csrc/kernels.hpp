@@ -115,7 +115,10 @@ struct RasterArgs {
     int n_cams;
     int normalize_depth;
     float cutoff;                    // smallest float >= transmittance_cutoff
-    float reserved;
+    int rect_w;                      // warp-rectangle width: 16 (16x4 bands) or 8 (8x8)
+    int batch;                       // records per shared-memory batch: 128 or 256
+    int exact_cull;                  // exact ellipse-vs-warp-rectangle test in the compaction
+    int reserved2;
     float* out;                      // per camera [rgb W*H*3 | depth W*H | alpha W*H]
     unsigned long long* consumed;    // += list entries fetched before the tile saturated
     uint64_t capacity;               // pair-buffer capacity (reads are clamped to it)

@@ -269,15 +269,12 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args)
                 continue;
             }
             const double inv_det = 1.0 / det;
-            Record rec;
-            rec.a = make_float4(__double2float_rn(u), __double2float_rn(v), fz,
-                                __double2float_rn(radius));
-            rec.b = make_float4(__double2float_rn(cov_yy * inv_det),
-                                __double2float_rn(-cov_xy * inv_det),
-                                __double2float_rn(cov_xx * inv_det), __double2float_rn(opacity));
+            args.records[slot] = make_record(
+                __double2float_rn(u), __double2float_rn(v), fz, __double2float_rn(radius),
+                __double2float_rn(cov_yy * inv_det), __double2float_rn(-cov_xy * inv_det),
+                __double2float_rn(cov_xx * inv_det), __double2float_rn(opacity), rgb[0], rgb[1],
+                rgb[2]);
             const uint32_t rec_rect = pack_rect(tx0, ty0, tx1, ty1);
-            rec.c = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(rec_rect));
-            args.records[slot] = rec;
             args.rects[slot] = rec_rect;
             // Camera-major sort key: camera index above the float32 depth bits
             // (depth_sort_key, raster.hpp:45-47) rebased to the batch's [near, far) range;
@@ -307,14 +304,12 @@ __global__ void __launch_bounds__(256) splats_to_records_kernel(SplatArgs args) 
         tx1 = tx1 > cam.tiles_x - 1 ? cam.tiles_x - 1 : tx1;
         ty1 = ty1 > cam.tiles_y - 1 ? cam.tiles_y - 1 : ty1;
         const float fz = __double2float_rn(sp.view_depth);
-        Record rec;
-        rec.a = make_float4(__double2float_rn(u), __double2float_rn(v), fz, __double2float_rn(r));
-        rec.b = make_float4(__double2float_rn(sp.inv_xx), __double2float_rn(sp.inv_xy),
-                            __double2float_rn(sp.inv_yy), __double2float_rn(sp.alpha_peak));
-        rec.c = make_float4(__double2float_rn(sp.rgb[0]), __double2float_rn(sp.rgb[1]),
-                            __double2float_rn(sp.rgb[2]),
-                            __uint_as_float(pack_rect(tx0, ty0, tx1, ty1)));
-        args.records[i] = rec;
+        args.records[i] = make_record(
+            __double2float_rn(u), __double2float_rn(v), fz, __double2float_rn(r),
+            __double2float_rn(sp.inv_xx), __double2float_rn(sp.inv_xy),
+            __double2float_rn(sp.inv_yy), __double2float_rn(sp.alpha_peak),
+            __double2float_rn(sp.rgb[0]), __double2float_rn(sp.rgb[1]),
+            __double2float_rn(sp.rgb[2]));
         args.rects[i] = pack_rect(tx0, ty0, tx1, ty1);
         // Full 32-bit depth_sort_key (raster.hpp:45-47): hand-made splats may carry any depth.
         uint32_t key = __float_as_uint(fz);

@@ -1,19 +1,24 @@
 // raster.cu — K4: per-tile front-to-back compositing (raster.cpp:273-320).
 //
-// One 256-thread CTA per (camera, 16x16 tile); thread = pixel. The 8 warps own 8x4 pixel
-// sub-rectangles. The tile's depth-sorted list is consumed in batches of 256 records:
-//   1. each thread gathers one 48-byte record into shared memory and computes an 8-bit mask
-//      of the warp rectangles the splat can reach (its 3-sigma box intersected with the
+// One 128-thread CTA per (camera, 16x16 tile); each thread owns TWO horizontally adjacent
+// pixels, so every per-splat quantity that depends only on the row (dy, the dy terms of the
+// quadratic form, the |dy| box test) is computed once for both, and the per-pixel arithmetic
+// runs on Blackwell's packed FP32 pipe (FFMA2 / FMUL2 / FADD2 on float2 registers). The 4
+// warps own 64-pixel warp rectangles (16x4 bands or 8x8 quadrants, template RW). The tile's
+// depth-sorted list is consumed in batches of 256 records:
+//   1. each thread gathers two 48-byte records into shared memory and computes a 4-bit mask
+//      of the warp rectangles each splat can reach (its 3-sigma box intersected with the
 //      alpha >= 1/255 ellipse bound, conservatively widened, so no contributing splat is
 //      ever dropped);
 //   2. each warp compacts the indices of the splats whose bit it owns into a private list
 //      (ballot + popc keeps the depth order);
 //   3. each warp walks its list with a branch-free blend: a splat that fails the box test or
-//      the 1/255 skip gets alpha 0, which leaves C, D, A and T bit-for-bit unchanged, so the
+//      the 1/255 skip gets weight 0, which leaves C, D, A and T bit-for-bit unchanged, so the
 //      result equals the reference's skip-with-continue loop;
 //   4. a pixel that saturates (T < cutoff after accumulating) parks at T = 0, so later
-//      weights are exactly zero; a warp stops when all its pixels are parked and the CTA
-//      leaves when __syncthreads_count says every pixel is.
+//      weights are exactly zero; T is therefore always 0 or >= cutoff, which makes the park
+//      test independent of the skip test. A warp stops when all its pixels are parked and the
+//      CTA leaves when __syncthreads_count says every pixel is.
 //
 // Per-pixel contract (raster.cpp:284-318): box test |dx|>r || |dy|>r, q with 2*inv_xy,
 // alpha = min(o*exp(-q/2), 0.99), skip alpha < 1/255, accumulate, T *= 1-alpha, stop after
@@ -27,29 +32,90 @@
 namespace gsim_gpu {
 
 namespace {
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBatch = 256;
-constexpr float kLog2e = 1.4426950408889634f;
-
-// The conic is stored prescaled by -log2(e)/2 so the exponent of ex2 is
-// lop + dx*(A*dx + B*dy) + C*dy*dy: five FP32 ops per pixel and splat.
-struct alignas(16) SmemSplat {
-    float4 p0;  // u, v, radius, log2(opacity)
-    float4 p1;  // A = -inv_xx*log2e/2, B = -inv_xy*log2e, C = -inv_yy*log2e/2, depth
-    float4 p2;  // r, g, b, -
-};
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
+
+// (e0, e1) with each lane zeroed unless |dx_i| <= r, |dy| <= r and e_i >= 1/255: the chained
+// setp.and form gives one compare per condition and one select per pixel.
+__device__ __forceinline__ float2 gate(float e0, float e1, float adx0, float adx1, float ady,
+                                       float r) {
+    static_assert(float(kAlphaSkip) == 0x1.010102p-8f, "skip constant below");
+    float2 o;
+    asm("{\n\t.reg .pred py, p0, p1;\n\t"
+        "setp.le.f32 py, %4, %5;\n\t"
+        "setp.le.and.f32 p0, %2, %5, py;\n\t"
+        "setp.le.and.f32 p1, %3, %5, py;\n\t"
+        "setp.ge.and.f32 p0, %6, 0f3B808081, p0;\n\t"
+        "setp.ge.and.f32 p1, %7, 0f3B808081, p1;\n\t"
+        "selp.f32 %0, %6, 0f00000000, p0;\n\t"
+        "selp.f32 %1, %7, 0f00000000, p1;\n\t}"
+        : "=f"(o.x), "=f"(o.y)
+        : "f"(adx0), "f"(adx1), "f"(ady), "f"(r), "f"(e0), "f"(e1));
+    return o;
+}
+
+// Can the splat reach alpha >= 1/255 at any point of the rectangle [x_lo, x_hi] x [y_lo, y_hi]
+// of pixel centres? The ex2 exponent E(dx, dy) = lop + dx (A dx + B dy) + C dy^2 (dx = u - px,
+// dy = v - py) is concave; its maximum over the rectangle is at (0, 0) when the centre is
+// inside, else on an edge facing the centre. Each candidate fixes one coordinate at the
+// clamped centre offset and maximises the other in closed form (clamped to the range), so
+// max(E1, E2) is the exact rectangle maximum (the approximate division only moves the
+// candidate along the edge, which lowers E by a second-order amount). The threshold keeps a
+// 0.02 margin below log2(1/255) so rounding can never drop a contributing splat.
+__device__ __forceinline__ bool reaches_rect(float4 p0, float4 p1, float x_lo, float x_hi,
+                                             float y_lo, float y_hi) {
+    const float A = p1.x, B = p1.y, C = p1.z;
+    const float dx_lo = p0.x - x_hi, dx_hi = p0.x - x_lo;  // range of dx over the rectangle
+    const float dy_lo = p0.y - y_hi, dy_hi = p0.y - y_lo;
+    const float dx1 = fminf(fmaxf(0.0f, dx_lo), dx_hi);
+    const float dy1 = fminf(fmaxf(dx1 * __fdividef(B, -2.0f * C), dy_lo), dy_hi);
+    const float dy2 = fminf(fmaxf(0.0f, dy_lo), dy_hi);
+    const float dx2 = fminf(fmaxf(dy2 * __fdividef(B, -2.0f * A), dx_lo), dx_hi);
+    const float e1 = p0.w + dx1 * (A * dx1 + B * dy1) + C * dy1 * dy1;
+    const float e2 = p0.w + dx2 * (A * dx2 + B * dy2) + C * dy2 * dy2;
+    return !(fmaxf(e1, e2) < -7.9943534f - 0.02f);  // NaN-safe: keep on doubt
+}
+
+__device__ __forceinline__ void write_pixel(const RasterArgs& a, const DevCamera& cam, int x, int y,
+                                            float cr, float cg, float cb, float d, float acc) {
+    if (x >= cam.width || y >= cam.height) return;
+    const float r = fminf(fmaxf(cr, 0.f), 1.f), gg = fminf(fmaxf(cg, 0.f), 1.f),
+                bb = fminf(fmaxf(cb, 0.f), 1.f);
+    const float depth = a.normalize_depth ? (acc > 1e-12f ? d / acc : 0.f) : d;
+    if (a.out) {
+        float* base = a.out + cam.out_offset;
+        const size_t npx = size_t(cam.width) * cam.height;
+        const size_t p = size_t(y) * cam.width + x;
+        base[3 * p + 0] = r;
+        base[3 * p + 1] = gg;
+        base[3 * p + 2] = bb;
+        base[3 * npx + p] = depth;
+        base[4 * npx + p] = acc;
+    }
+    if (a.enc.flags) {
+        uint8_t* blk = a.enc.dst + cam.out_offset / 5 * encoded_bpp(a.enc.flags);
+        encode_pixel(a.enc, a.enc.srgb_thr, blk, uint32_t(cam.width), uint32_t(cam.height),
+                     uint32_t(x), uint32_t(y), r, gg, bb, depth, acc);
+    }
+}
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
-    __shared__ SmemSplat s_spl[kBatch];
-    __shared__ uint8_t s_mask[kBatch];
+// RW = warp-rectangle width in pixels (16: 16x4 bands, 8: 8x8 quadrants); kBatch = records
+// per batch (two buffers of kBatch * 48 bytes of shared memory).
+template <int RW, int kBatch>
+__global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kernel(RasterArgs a) {
+    constexpr int kPerThread = kBatch / kThreads;
+    constexpr int RH = 64 / RW;  // warp-rectangle height
+    constexpr int PC = RW / 2;   // pixel-pair columns of a warp rectangle
+    constexpr int WX = 16 / RW;  // warp rectangles per tile row
+    __shared__ Record s_spl[2][kBatch];
     __shared__ uint16_t s_list[kWarps][kBatch];
 
     const uint32_t g = blockIdx.x;
@@ -59,10 +125,14 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
     const int tiles_x = cam.tiles_x;
     const int tx = int(tile % uint32_t(tiles_x)), ty = int(tile / uint32_t(tiles_x));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // warp w owns the 8x4 block (w % 2, w / 2) of the tile; lane = (lane % 8, lane / 8)
-    const int x = tx * kTileSize + (warp & 1) * 8 + (lane & 7);
-    const int y = ty * kTileSize + (warp >> 1) * 4 + (lane >> 3);
-    const float px = float(x) + 0.5f, py = float(y) + 0.5f;
+    const int rx0 = tx * kTileSize + (warp % WX) * RW, ry0 = ty * kTileSize + (warp / WX) * RH;
+    const int x = rx0 + 2 * (lane % PC);  // first pixel of the pair
+    const int y = ry0 + lane / PC;
+    const float2 npx = make_float2(-(float(x) + 0.5f), -(float(x) + 1.5f));
+    const float py = float(y) + 0.5f;
+    // pixel-centre bounds of this warp's rectangle
+    const float wx_lo = float(rx0) + 0.5f, wx_hi = wx_lo + float(RW - 1);
+    const float wy_lo = float(ry0) + 0.5f, wy_hi = wy_lo + float(RH - 1);
 
     // On a pair-buffer overflow the host re-runs scatter + raster; until then keep every read
     // in bounds (the clamped frame is discarded).
@@ -71,133 +141,129 @@ __global__ void __launch_bounds__(kThreads, 5) raster_kernel(RasterArgs a) {
     const uint64_t e64 = b64 + a.tile_count[g];
     const uint32_t end = uint32_t(e64 < a.capacity ? e64 : a.capacity);
     const float cutoff = a.cutoff;
-    float cr = 0.f, cg = 0.f, cb = 0.f, d = 0.f, acc = 0.f, T = 1.f;
+    float2 cr = bc(0.f), cg = bc(0.f), cb = bc(0.f), d = bc(0.f), acc = bc(0.f), T = bc(1.f);
 
-    // Pixel-centre bounds of the 2 warp columns and 4 warp rows of this tile.
-    const float tile_x0 = float(tx * kTileSize) + 0.5f, tile_y0 = float(ty * kTileSize) + 0.5f;
-
-    uint32_t fetched = 0;
-    for (uint32_t b0 = begin; b0 < end; b0 += kBatch) {
-        const uint32_t n_b = (end - b0) < uint32_t(kBatch) ? (end - b0) : uint32_t(kBatch);
-        fetched += n_b;
-        uint32_t mask = 0;
-        if (uint32_t(tid) < n_b) {
-            uint32_t slot = __ldg(a.values + b0 + tid);
-            if (slot >= a.n_slots) slot = 0;  // only possible in a clamped (overflowed) frame
-            const float4 ra = __ldg(&a.records[slot].a);
-            const float4 rb = __ldg(&a.records[slot].b);
-            const float4 rc = __ldg(&a.records[slot].c);
-            const float u = ra.x, v = ra.y, rad = ra.w, op = rb.w;
-            const float ia = rb.x, ib = rb.y, ic = rb.z;
-            s_spl[tid].p0 = make_float4(u, v, rad, __log2f(op));
-            s_spl[tid].p1 = make_float4(ia * (-0.5f * kLog2e), ib * -kLog2e, ic * (-0.5f * kLog2e), ra.z);
-            s_spl[tid].p2 = make_float4(rc.x, rc.y, rc.z, 0.f);
-            // Reachable half-extents: the box test bounds |dx|,|dy| <= r; alpha >= 1/255 needs
-            // q <= qc = 2 ln(255 o), whose ellipse has half-extents sqrt(qc * cov_xx/yy).
-            float ex = rad, ey = rad;
-            if (op * 255.0f < 1.0f) {
-                ex = -1.0f;  // can never reach alpha 1/255
-            } else {
-                const float qc = 2.0f * __logf(op * 255.0f);
-                const float det = ia * ic - ib * ib;
-                if (det > 0.0f) {
-                    const float inv = 1.0f / det;
-                    const float bx = sqrtf(qc * ic * inv) * 1.01f + 0.05f;
-                    const float by = sqrtf(qc * ia * inv) * 1.01f + 0.05f;
-                    ex = fminf(ex, bx);
-                    ey = fminf(ey, by);
-                }
-            }
-            if (ex >= 0.0f) {
-                uint32_t cols = 0, rows = 0;
+    // Batches are double-buffered: the records of batch i+1 are copied global -> shared with
+    // cp.async while batch i is blended; the list entries of batch i+2 are loaded meanwhile.
+    uint32_t slot_next[kPerThread];
+    auto load_slots = [&](uint32_t b) {
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const float lo = tile_x0 + 8.0f * c;
-                    cols |= (u + ex >= lo && u - ex <= lo + 7.0f) ? (1u << c) : 0u;
-                }
+        for (int h = 0; h < kPerThread; ++h) {
+            const uint32_t i = b + uint32_t(tid + h * kThreads);
+            uint32_t sl = i < end ? __ldg(a.values + i) : 0xFFFFFFFFu;
+            // a stale slot is only possible in a clamped (overflowed) frame
+            if (i < end && sl >= a.n_slots) sl = 0;
+            slot_next[h] = sl;
+        }
+    };
+    auto issue_copy = [&](int buf) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const float lo = tile_y0 + 4.0f * r;
-                    rows |= (v + ey >= lo && v - ey <= lo + 3.0f) ? (1u << r) : 0u;
-                }
-                // bit (row * 2 + col) for every reachable (col, row)
-                const uint32_t colmask = (cols & 1u) * 0x55u | ((cols >> 1) & 1u) * 0xAAu;
-                const uint32_t rowmask = (rows & 1u) * 0x03u | ((rows >> 1) & 1u) * 0x0Cu |
-                                         ((rows >> 2) & 1u) * 0x30u | ((rows >> 3) & 1u) * 0xC0u;
-                mask = colmask & rowmask;
+        for (int h = 0; h < kPerThread; ++h) {
+            if (slot_next[h] != 0xFFFFFFFFu) {
+                const char* src = reinterpret_cast<const char*>(a.records + slot_next[h]);
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(&s_spl[buf][tid + h * kThreads]));
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q),
+                                 "l"(src + 16 * q) : "memory");
             }
         }
-        s_mask[tid] = uint8_t(mask);
-        __syncthreads();
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 
-        if (!__all_sync(0xffffffffu, T == 0.0f)) {
-            // Compact this warp's splats (depth order preserved) as byte offsets into s_spl.
+    uint32_t fetched = 0;
+    if (begin < end) {
+        load_slots(begin);
+        issue_copy(0);
+        load_slots(begin + kBatch);
+    }
+    int buf = 0;
+    for (uint32_t b0 = begin; b0 < end; b0 += kBatch, buf ^= 1) {
+        const uint32_t n_b = (end - b0) < uint32_t(kBatch) ? (end - b0) : uint32_t(kBatch);
+        fetched += n_b;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        // every warp has left batch i-1, so its buffer takes batch i+1
+        if (b0 + kBatch < end) {
+            issue_copy(buf ^ 1);
+            load_slots(b0 + 2 * kBatch);
+        }
+
+        if (!__all_sync(0xffffffffu, T.x == 0.0f && T.y == 0.0f)) {
+            // Compact the splats that can reach this warp's rectangle (depth order preserved)
+            // as byte offsets into s_spl.
+            const Record* spl_buf = s_spl[buf];
             uint32_t count = 0;
             for (uint32_t j = 0; j < n_b; j += 32) {
                 const uint32_t idx = j + lane;
-                const bool mine = idx < n_b && ((s_mask[idx] >> warp) & 1u);
+                bool mine = false;
+                if (idx < n_b) {
+                    const float4 p0 = spl_buf[idx].a;
+                    const float rw = spl_buf[idx].c.w;
+                    const __half2 reach = *reinterpret_cast<const __half2*>(&rw);
+                    const float ex = __low2float(reach), ey = __high2float(reach);
+                    mine = p0.x + ex >= wx_lo && p0.x - ex <= wx_hi && p0.y + ey >= wy_lo &&
+                           p0.y - ey <= wy_hi;
+                    if (a.exact_cull) mine = mine && reaches_rect(p0, spl_buf[idx].b, wx_lo, wx_hi, wy_lo, wy_hi);
+                }
                 const uint32_t bits = __ballot_sync(0xffffffffu, mine);
                 if (mine)
                     s_list[warp][count + __popc(bits & lanemask_lt())] =
-                        uint16_t(idx * sizeof(SmemSplat));
+                        uint16_t(idx * sizeof(Record));
                 count += __popc(bits);
             }
             __syncwarp();
-            const char* spl = reinterpret_cast<const char*>(s_spl);
+            const char* spl = reinterpret_cast<const char*>(spl_buf);
             for (uint32_t k0 = 0; k0 < count; k0 += 32) {
                 const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
 #pragma unroll 4
                 for (uint32_t k = k0; k < k1; ++k) {
-                    const SmemSplat& sp = *reinterpret_cast<const SmemSplat*>(spl + s_list[warp][k]);
-                    const float4 p0 = sp.p0, p1 = sp.p1, p2 = sp.p2;
-                    const float dx = p0.x - px, dy = p0.y - py;
-                    const float t = fmaf(p1.y, dy, p1.x * dx);
-                    const float E = fmaf(p1.z * dy, dy, fmaf(t, dx, p0.w));
-                    const float e = fminf(ex2_approx(E), 0.99f);
-                    const bool ok = fmaxf(fabsf(dx), fabsf(dy)) <= p0.z && e >= float(kAlphaSkip);
-                    const float w = (ok ? e : 0.0f) * T;
-                    cr = fmaf(p2.x, w, cr);
-                    cg = fmaf(p2.y, w, cg);
-                    cb = fmaf(p2.z, w, cb);
-                    d = fmaf(p1.w, w, d);
-                    acc += w;
+                    const Record& sp = *reinterpret_cast<const Record*>(spl + s_list[warp][k]);
+                    const float4 p0 = sp.a, p1 = sp.b, p2 = sp.c;
+                    // row terms, shared by the pair
+                    const float dy = p0.y - py;
+                    const float kq = fmaf(p1.z * dy, dy, p0.w);
+                    // pair terms on the packed pipe
+                    const float2 dx = __fadd2_rn(bc(p0.x), npx);
+                    const float2 t = __ffma2_rn(bc(p1.x), dx, bc(p1.y * dy));
+                    const float2 E = __ffma2_rn(t, dx, bc(kq));
+                    const float e0 = fminf(ex2_approx(E.x), 0.99f);
+                    const float e1 = fminf(ex2_approx(E.y), 0.99f);
+                    const float2 w = __fmul2_rn(gate(e0, e1, fabsf(dx.x), fabsf(dx.y), fabsf(dy), p0.z), T);
+                    cr = __ffma2_rn(bc(p2.x), w, cr);
+                    cg = __ffma2_rn(bc(p2.y), w, cg);
+                    cb = __ffma2_rn(bc(p2.z), w, cb);
+                    d = __ffma2_rn(bc(p1.w), w, d);
+                    acc = __fadd2_rn(acc, w);
                     // T * (1 - alpha) == T - w up to rounding; a saturated pixel parks at T = 0,
                     // where every later weight is exactly zero (the reference's break).
-                    const float Tn = T - w;
-                    T = (ok && Tn < cutoff) ? 0.0f : Tn;
+                    const float2 Tn = __fadd2_rn(T, make_float2(-w.x, -w.y));
+                    T.x = Tn.x < cutoff ? 0.0f : Tn.x;
+                    T.y = Tn.y < cutoff ? 0.0f : Tn.y;
                 }
-                if (__all_sync(0xffffffffu, T == 0.0f)) break;
+                if (__all_sync(0xffffffffu, T.x == 0.0f && T.y == 0.0f)) break;
             }
         }
-        if (__syncthreads_count(T == 0.0f ? 0 : 1) == 0) break;
+        if (__syncthreads_count(T.x == 0.0f && T.y == 0.0f ? 0 : 1) == 0) break;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // no copy may land after the CTA exits
 
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
-    if (x < cam.width && y < cam.height) {
-        const float r = fminf(fmaxf(cr, 0.f), 1.f), gg = fminf(fmaxf(cg, 0.f), 1.f),
-                    bb = fminf(fmaxf(cb, 0.f), 1.f);
-        const float depth = a.normalize_depth ? (acc > 1e-12f ? d / acc : 0.f) : d;
-        if (a.out) {
-            float* base = a.out + cam.out_offset;
-            const size_t npx = size_t(cam.width) * cam.height;
-            const size_t p = size_t(y) * cam.width + x;
-            base[3 * p + 0] = r;
-            base[3 * p + 1] = gg;
-            base[3 * p + 2] = bb;
-            base[3 * npx + p] = depth;
-            base[4 * npx + p] = acc;
-        }
-        if (a.enc.flags) {
-            uint8_t* blk = a.enc.dst + cam.out_offset / 5 * encoded_bpp(a.enc.flags);
-            encode_pixel(a.enc, a.enc.srgb_thr, blk, uint32_t(cam.width), uint32_t(cam.height),
-                         uint32_t(x), uint32_t(y), r, gg, bb, depth, acc);
-        }
-    }
+    write_pixel(a, cam, x, y, cr.x, cg.x, cb.x, d.x, acc.x);
+    write_pixel(a, cam, x + 1, y, cr.y, cg.y, cb.y, d.y, acc.y);
 }
 
 void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream) {
     if (n_tiles == 0) return;
-    raster_kernel<<<n_tiles, kThreads, 0, stream>>>(a);
+    const bool small = a.batch == 128;
+    if (a.rect_w == 8) {
+        if (small) raster_kernel<8, 128><<<n_tiles, kThreads, 0, stream>>>(a);
+        else raster_kernel<8, 256><<<n_tiles, kThreads, 0, stream>>>(a);
+    } else {
+        if (small) raster_kernel<16, 128><<<n_tiles, kThreads, 0, stream>>>(a);
+        else raster_kernel<16, 256><<<n_tiles, kThreads, 0, stream>>>(a);
+    }
 }
 
 }  // namespace gsim_gpu
+
