@@ -2,23 +2,27 @@
 //
 // The reference emits (tile << 32 | depth, splat) pairs and std::sorts them
 // (raster.cpp:243-271). After the camera-major depth sort of the V visible records
-// (sort.cu), the pair order we need is simply "by (camera, tile), then by record order".
-// Instead of radix-sorting the P ~ 3.5 V pairs by tile, every pair is placed directly:
-//   units     the depth-sorted records of each camera are cut into units of R records; one
-//             warp owns one unit (no block-level cooperation, no barriers);
-//   count     per unit, count pairs per tile into a warp-private counter array and store the
-//             row into a per-camera [tile][unit] count matrix;
-//   colscan   per (camera, tile): exclusive scan over the camera's units;
+// (sort.cu, whose last pass also gathers every record's tile rect into depth order), the pair
+// order we need is simply "by (camera, tile), then by record order". Instead of radix-sorting
+// the P ~ 3.5 V pairs by tile, every pair is placed directly:
+//   units     the depth-sorted records of each camera are cut into units of R = 1024 * W
+//             records; one W-warp CTA owns one unit, warp w its w-th 1024-record slice;
+//   count     per unit, pairs per tile: every record adds +1 / -1 at both ends of each of its
+//             rect rows in a shared row-difference array (red.shared), rows are then
+//             prefix-summed by warp scans; the row goes to a per-camera [unit][tile] matrix;
+//   colscan   per (camera, tile): exclusive scan over the camera's units (lanes = tiles);
 //   tilescan  per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:267-271);
 //   campre    per batch: pair base of every camera;
-//   scatter   per unit: load the unit's first position of every tile, walk the records again
-//             in order and write each pair's record slot at its position.
+//   scatter   per unit: each warp recounts its slice the same way, the CTA turns the counts
+//             into per-warp first positions of every tile, and each warp walks its records in
+//             order writing each pair's record slot at its position.
 // Pairs are enumerated warp-cooperatively, 32 consecutive pairs per step in emission order
-// (record order, row-major tiles inside a record, raster.cpp:259-263). Two lanes of a step
-// hitting the same tile is detected with a shared-memory "last writer" probe; only then are
-// the tile's lanes ranked with ballots (match.any issues at ~1 per 40 SM cycles on sm_100,
-// shared atomics at 2 cycles per lane: both measured, both avoided). The result equals the
-// reference's stable (tile, depth, primitive) order bit for bit.
+// (record order, row-major tiles inside a record, raster.cpp:259-263): the owner record of a
+// pair position comes from one redux.sync.or of the records' start bits and a popc. Two lanes
+// of a step hitting the same tile is detected with a shared-memory "last writer" probe; only
+// then are the tile's lanes ranked with ballots (match.any issues at ~1 per 40 SM cycles on
+// sm_100, both measured, and is avoided). The result equals the reference's stable
+// (tile, depth, primitive) order bit for bit.
 #include <cstdint>
 
 #include "common.cuh"
@@ -39,96 +43,16 @@ __device__ __forceinline__ uint32_t rect_area(uint32_t r) {
     return (((r >> 16) & 255u) - (r & 255u) + 1u) * ((r >> 24) - ((r >> 8) & 255u) + 1u);
 }
 
-// Warp-cooperative enumeration of the pairs of 32 records (one per lane): calls
-// fn(in, tile, slot) once per step; lane j of a step holds the step's j-th pair.
-template <class F>
-__device__ __forceinline__ void for_each_pair(uint32_t slot, uint32_t rect, bool valid,
-                                              int tiles_x, F&& fn) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t cnt = valid ? rect_area(rect) : 0u;
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += t;
-    }
-    const uint32_t excl = incl - cnt;
-    const uint32_t total = __shfl_sync(kFull, incl, 31);
-    // row-major position -> (row, column) with a per-record magic reciprocal: for kk < 2^16
-    // and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
-    const uint32_t w_own = ((rect >> 16) & 255u) - (rect & 255u) + 1u;
-    const uint32_t magic = w_own > 1u ? 0xFFFFFFFFu / w_own + 1u : 0u;
-    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-        const uint32_t j = k0 + lane;
-        // owner = last lane whose exclusive offset <= j (valid lanes have cnt >= 1)
-        int lo = 0;
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-            const uint32_t oc = __shfl_sync(kFull, excl, (lo + s) & 31);
-            if (lo + s < 32 && oc <= j) lo += s;
-        }
-        const uint32_t o_own = __shfl_sync(kFull, excl, lo);
-        const uint32_t r = __shfl_sync(kFull, rect, lo);
-        const uint32_t sl = __shfl_sync(kFull, slot, lo);
-        const uint32_t mg = __shfl_sync(kFull, magic, lo);
-        const bool in = j < total;
-        const uint32_t kk = j - o_own;
-        const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u;
-        const uint32_t w = tx1 - tx0 + 1u;
-        const uint32_t q = mg ? __umulhi(kk, mg) : kk;
-        const uint32_t tile = (ty0 + q) * uint32_t(tiles_x) + tx0 + (kk - q * w);
-        fn(in, tile, sl);
-    }
-}
-
-// Walk records [wb, we) of the depth-sorted list in order, 32 per group, with the slot and
-// rect loads of kG groups issued together (latency hiding), calling for_each_pair per group.
-template <class F>
-__device__ __forceinline__ void walk_records(const BinArgs& a, uint32_t wb, uint32_t we,
-                                             int tiles_x, F&& fn) {
-    constexpr int kG = 4;
-    const int lane = threadIdx.x & 31;
-    for (uint32_t g0 = wb; g0 < we; g0 += 32 * kG) {
-        uint32_t slot[kG], rect[kG];
-#pragma unroll
-        for (int q = 0; q < kG; ++q) {
-            const uint32_t e = g0 + q * 32 + lane;
-            slot[q] = e < we ? __ldcs(a.sorted_slots + e) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < kG; ++q) {
-            const uint32_t e = g0 + q * 32 + lane;
-            rect[q] = e < we ? __ldg(a.rects + slot[q]) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < kG; ++q) {
-            if (g0 + q * 32 >= we) break;
-            for_each_pair(slot[q], rect[q], g0 + q * 32 + lane < we, tiles_x, fn);
-        }
-    }
-}
-
-// Lanes of `in_mask` whose tile equals this lane's, ordered by lane = emission order.
-// Fast path: every lane writes its lane id to probe[tile], then reads it back; if no lane
-// lost the write, all tiles in the step are distinct and each lane is its own only peer.
-__device__ __forceinline__ uint32_t tile_peers(uint8_t* probe, uint32_t tile, bool in,
-                                               uint32_t in_mask, int tbits) {
-    const int lane = threadIdx.x & 31;
-    if (in) probe[tile] = uint8_t(lane);
-    __syncwarp();
-    const bool lost = in && probe[tile] != uint8_t(lane);
-    const bool any_conflict = __any_sync(kFull, lost);
-    __syncwarp();
-    if (!any_conflict) return in ? (1u << lane) : 0u;
-    return peers_of_bits(kFull, tile, tbits) & in_mask;
+__host__ __device__ inline size_t bin_warp_bytes(int max_cells) {
+    return (size_t(max_cells) * 5 + 15) & ~size_t(15);
 }
 
 struct Unit {
     int cam;
     uint32_t rec_begin, rec_end;  // depth-sorted record range
     uint32_t unit_in_cam, units_in_cam;
-    uint64_t mbase;               // count-matrix base of the camera ([tile][unit])
-    int tiles_x;
+    uint64_t mbase;               // count-matrix base of the camera ([unit][tile])
+    int tiles_x, tiles_y;
     uint32_t tc;                  // tiles of the camera
     uint32_t tile_base;
     int tbits;                    // bits of a camera-local tile id
@@ -147,25 +71,14 @@ __device__ __forceinline__ Unit unit_info(const BinArgs& a, uint32_t k) {
     u.tiles_x = a.cam_tiles_x[u.cam];
     u.tile_base = a.cam_tile_base[u.cam];
     u.tc = a.cam_tile_base[u.cam + 1] - u.tile_base;
+    u.tiles_y = int(u.tc / uint32_t(u.tiles_x));
     u.tbits = u.tc > 1 ? 32 - __clz(int(u.tc - 1)) : 0;
     return u;
 }
 
-// Warp w of the block works in s_bin + w * per_warp_bytes: [max_tc] u32 + [max_tc] u8 probe.
-constexpr int kTab = 512;  // pairs of one 32-record group held in a shared-memory table
-
-__host__ __device__ inline size_t bin_warp_bytes(int max_cells) {
-    return (size_t(max_cells) * 5 + size_t(kTab) * 3 + 15) & ~size_t(15);
-}
-
-// Warp w of the block works in s_bin + w * bin_warp_bytes: [max_cells] u32 counters,
-// [max_cells] u8 probe, [kTab] u16 tile table, [kTab] u8 owner table.
-__device__ __forceinline__ uint32_t* warp_counters(char* s_bin, int max_cells) {
-    return reinterpret_cast<uint32_t*>(s_bin + (threadIdx.x >> 5) * bin_warp_bytes(max_cells));
-}
-
-// Walk records [wb, we) in order, 32 per group (lane = record), loads of kG groups in flight.
-template <class F>
+// Walk records [wb, we) in order, 32 per group (lane = record), with the coalesced loads of kG
+// groups in flight; fn(slot, rect, valid) per group.
+template <bool kSlots, class F>
 __device__ __forceinline__ void walk_groups(const BinArgs& a, uint32_t wb, uint32_t we, F&& fn) {
     constexpr int kG = 4;
     const int lane = threadIdx.x & 31;
@@ -174,12 +87,8 @@ __device__ __forceinline__ void walk_groups(const BinArgs& a, uint32_t wb, uint3
 #pragma unroll
         for (int q = 0; q < kG; ++q) {
             const uint32_t e = g0 + q * 32 + lane;
-            slot[q] = e < we ? __ldcs(a.sorted_slots + e) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < kG; ++q) {
-            const uint32_t e = g0 + q * 32 + lane;
-            rect[q] = e < we ? __ldg(a.rects + slot[q]) : 0u;
+            rect[q] = e < we ? __ldcs(a.sorted_rects + e) : 0u;
+            slot[q] = (kSlots && e < we) ? __ldcs(a.sorted_slots + e) : 0u;
         }
 #pragma unroll
         for (int q = 0; q < kG; ++q) {
@@ -189,23 +98,41 @@ __device__ __forceinline__ void walk_groups(const BinArgs& a, uint32_t wb, uint3
     }
 }
 
-// D[cell] += delta for every active lane; lanes that share a cell in the same call are
-// applied in rounds (a shared-memory last-writer probe picks one winner per cell per round).
-__device__ __forceinline__ void add_cells(int* D, uint8_t* probe, uint32_t cell, int delta,
-                                          bool active) {
-    const int lane = threadIdx.x & 31;
-    bool pending = active;
-    while (__any_sync(kFull, pending)) {
-        if (pending) probe[cell] = uint8_t(lane);
-        __syncwarp();
-        const bool win = pending && probe[cell] == uint8_t(lane);
-        __syncwarp();
-        if (win) {
-            D[cell] += delta;
-            pending = false;
-        }
-        __syncwarp();
+// Row-difference counting: +1 at (ty, tx0) and -1 at (ty, tx1 + 1) for every rect row of every
+// valid lane's record. D is [tiles_y][tiles_x + 1]; shared atomics (order is irrelevant here).
+__device__ __forceinline__ void add_rect_rows(int* D, int wd, uint32_t r, bool valid) {
+    if (!valid) return;
+    const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u, ty1 = r >> 24;
+    for (uint32_t ty = ty0; ty <= ty1; ++ty) {
+        atomicAdd(D + ty * uint32_t(wd) + tx0, 1);
+        atomicAdd(D + ty * uint32_t(wd) + tx1 + 1u, -1);
     }
+}
+
+// Inclusive prefix of row `row` of D (length n, row stride wd) by one warp; calls
+// out(x, value) for every x < n. Reads before writes within each 32-chunk.
+template <class F>
+__device__ __forceinline__ void scan_row(int* D, int wd, int row, int n, F&& out) {
+    const int lane = threadIdx.x & 31;
+    int carry = 0;
+    for (int x0 = 0; x0 < n; x0 += 32) {
+        const int x = x0 + lane;
+        int v = x < n ? D[row * wd + x] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, v, o);
+            if (lane >= o) v += t;
+        }
+        v += carry;
+        if (x < n) out(x, v);
+        carry = __shfl_sync(kFull, v, 31);
+    }
+}
+
+__device__ __forceinline__ uint32_t reduce_or(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.or.b32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
 }
 
 }  // namespace
@@ -232,13 +159,16 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
             const uint32_t key = keys[i];
             const bool valid = key != kInvalidKey;
             const uint32_t vmask = __ballot_sync(kFull, valid);
-            if (a.hist) {  // digit histograms (only the onesweep variant needs them)
+            // digit histograms: the three low digits are spread over many values, so plain
+            // shared atomics (per-warp sub-histograms) are cheap; the top digit (camera and
+            // exponent bits) repeats within a warp and is aggregated over ballot peers.
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const uint32_t d = (key >> (8 * p)) & 255u;
-                    const uint32_t peers = peers_of<8>(kFull, d) & vmask;
-                    if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][p][d] += __popc(peers);
-                }
+            for (int p = 0; p < 3; ++p)
+                if (valid) atomicAdd(&s_hist[warp][p][(key >> (8 * p)) & 255u], 1u);
+            {
+                const uint32_t d = key >> 24;
+                const uint32_t peers = peers_of<8>(kFull, d) & vmask;
+                if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][3][d] += __popc(peers);
             }
             // per-camera counts: one round per distinct camera in the group (usually one)
             const uint32_t cam = key_camera(key, a.depth_bits);
@@ -264,7 +194,7 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
         uint32_t s = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
-        if (s && a.hist) atomicAdd(a.hist + k, s);
+        if (s) atomicAdd(a.hist + k, s);
     }
 }
 
@@ -322,80 +252,51 @@ __global__ void __launch_bounds__(1024) chunk_table_kernel(BinArgs a) {
         a.chunk_cam[k] = uint32_t(upper_index(a.cam_chunk_base, a.n_cams, k));
 }
 
-// ---- count: one warp per unit ------------------------------------------------------------------
+// ---- count: one CTA per unit ------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinArgs a) {
     extern __shared__ __align__(16) char s_bin[];
-    const int lane = threadIdx.x & 31;
-    if ((threadIdx.x >> 5) >= a.bin_warps) return;
-    // Pairs per tile of a unit without enumerating pairs: every record adds +1 over its tile
-    // rectangle, written as 4 corner updates of a 2-D difference array, then a 2-D prefix sum.
-    int* D = reinterpret_cast<int*>(warp_counters(s_bin, a.max_tc));
-    uint8_t* probe = reinterpret_cast<uint8_t*>(D + a.max_tc);
+    int* D = reinterpret_cast<int*>(s_bin);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t K = *a.n_chunks;
-    const uint32_t n_warps = gridDim.x * uint32_t(a.bin_warps);
-    for (uint32_t k = blockIdx.x * a.bin_warps + (threadIdx.x >> 5); k < K; k += n_warps) {
+    for (uint32_t k = blockIdx.x; k < K; k += gridDim.x) {
         const Unit u = unit_info(a, k);
-        const uint32_t W = uint32_t(u.tiles_x) + 1u, tiles_y = u.tc / uint32_t(u.tiles_x);
-        const uint32_t H = tiles_y + 1u;
-        for (uint32_t t = lane; t < W * H; t += 32) D[t] = 0;
-        __syncwarp();
-        walk_groups(a, u.rec_begin, u.rec_end, [&](uint32_t, uint32_t r, bool valid) {
-            const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u;
-            const uint32_t tx1 = ((r >> 16) & 255u) + 1u, ty1 = (r >> 24) + 1u;
-            add_cells(D, probe, ty0 * W + tx0, 1, valid);
-            add_cells(D, probe, ty0 * W + tx1, -1, valid);
-            add_cells(D, probe, ty1 * W + tx0, -1, valid);
-            add_cells(D, probe, ty1 * W + tx1, 1, valid);
-        });
-        for (uint32_t y = lane; y < H; y += 32) {
-            int run = 0;
-            for (uint32_t x = 0; x < W; ++x) {
-                run += D[y * W + x];
-                D[y * W + x] = run;
-            }
-        }
-        __syncwarp();
-        for (uint32_t x = lane; x < W; x += 32) {
-            int run = 0;
-            for (uint32_t y = 0; y < H; ++y) {
-                run += D[y * W + x];
-                D[y * W + x] = run;
-            }
-        }
-        __syncwarp();
-        uint32_t* col = a.counts + u.mbase + u.unit_in_cam;
-        for (uint32_t t = lane; t < u.tc; t += 32) {
-            const uint32_t ty = t / uint32_t(u.tiles_x), tx = t - ty * uint32_t(u.tiles_x);
-            col[uint64_t(t) * u.units_in_cam] = uint32_t(D[ty * W + tx]);
-        }
-        __syncwarp();
+        const int wd = u.tiles_x + 1;
+        for (int t = threadIdx.x; t < wd * u.tiles_y; t += blockDim.x) D[t] = 0;
+        __syncthreads();
+        const uint32_t wb = u.rec_begin + uint32_t(warp) * kWarpRecords;
+        walk_groups<false>(a, wb, min(wb + kWarpRecords, u.rec_end),
+                           [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
+        __syncthreads();
+        uint32_t* mrow = a.counts + u.mbase + uint64_t(u.unit_in_cam) * u.tc;
+        for (int ty = warp; ty < u.tiles_y; ty += nw)
+            scan_row(D, wd, ty, u.tiles_x, [&](int x, int v) { mrow[ty * u.tiles_x + x] = uint32_t(v); });
+        __syncthreads();
     }
+    (void)lane;
 }
 
-// ---- column scan: one warp per (camera, tile) --------------------------------------------------
+// ---- column scan: one thread per (camera, tile), serial over the camera's units ----------------
 __global__ void __launch_bounds__(kThreads) bin_colscan_kernel(BinArgs a) {
-    const int lane = threadIdx.x & 31;
     const uint32_t n_cols = a.cam_tile_base[a.n_cams];
-    for (uint32_t g = (blockIdx.x * kThreads + threadIdx.x) >> 5; g < n_cols;
-         g += (gridDim.x * kThreads) >> 5) {
+    for (uint32_t g = blockIdx.x * kThreads + threadIdx.x; g < n_cols; g += gridDim.x * kThreads) {
         const int c = upper_index(a.cam_tile_base, a.n_cams, g);
+        const uint32_t tc = a.cam_tile_base[c + 1] - a.cam_tile_base[c];
         const uint32_t t = g - a.cam_tile_base[c];
         const uint32_t nk = a.cam_chunk_base[c + 1] - a.cam_chunk_base[c];
-        uint32_t* col = a.counts + a.cam_mbase[c] + uint64_t(t) * nk;
+        uint32_t* col = a.counts + a.cam_mbase[c] + t;
         uint32_t run = 0;
-        for (uint32_t k0 = 0; k0 < nk; k0 += 32) {
-            const uint32_t k = k0 + lane;
-            const uint32_t v = k < nk ? col[k] : 0u;
-            uint32_t incl = v;
+        constexpr uint32_t kU = 8;  // loads in flight
+        for (uint32_t k0 = 0; k0 < nk; k0 += kU) {
+            uint32_t v[kU];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t s = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += s;
+            for (uint32_t q = 0; q < kU; ++q) v[q] = k0 + q < nk ? col[uint64_t(k0 + q) * tc] : 0u;
+#pragma unroll
+            for (uint32_t q = 0; q < kU; ++q) {
+                if (k0 + q < nk) col[uint64_t(k0 + q) * tc] = run;
+                run += v[q];
             }
-            if (k < nk) col[k] = run + incl - v;
-            run += __shfl_sync(kFull, incl, 31);
         }
-        if (lane == 0) a.tile_count[g] = run;
+        a.tile_count[g] = run;
     }
 }
 
@@ -464,71 +365,112 @@ __global__ void __launch_bounds__(1024) bin_campre_kernel(BinArgs a) {
     }
 }
 
-// ---- scatter: one warp per unit ----------------------------------------------------------------
+// ---- scatter: one CTA per unit ----------------------------------------------------------------
+// Shared memory per warp: [tiles_y][tiles_x + 1] u32 counters, turned into first positions, and
+// a u8 probe per cell (bin_warp_bytes).
 __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     extern __shared__ __align__(16) char s_bin[];
-    const int lane = threadIdx.x & 31;
-    if ((threadIdx.x >> 5) >= a.bin_warps) return;
-    uint32_t* pos = warp_counters(s_bin, a.max_tc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const size_t wbytes = bin_warp_bytes(a.max_tc);
+    uint32_t* pos = reinterpret_cast<uint32_t*>(s_bin + warp * wbytes);
     uint8_t* probe = reinterpret_cast<uint8_t*>(pos + a.max_tc);
-    uint16_t* tab_tile = reinterpret_cast<uint16_t*>(probe + ((a.max_tc + 1) & ~1));
-    uint8_t* tab_own = reinterpret_cast<uint8_t*>(tab_tile + kTab);
+    // row-major position -> (row, column) with a magic reciprocal per rect width: for
+    // kk < 2^16 and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
+    __shared__ uint32_t s_magic[257];
+    for (int w = threadIdx.x; w <= 256; w += blockDim.x) s_magic[w] = w > 1 ? 0xFFFFFFFFu / uint32_t(w) + 1u : 0u;
+    __syncthreads();
     const uint32_t K = *a.n_chunks;
-    const uint32_t n_warps = gridDim.x * uint32_t(a.bin_warps);
-    for (uint32_t k = blockIdx.x * a.bin_warps + (threadIdx.x >> 5); k < K; k += n_warps) {
+    for (uint32_t k = blockIdx.x; k < K; k += gridDim.x) {
         const Unit u = unit_info(a, k);
-        // first position of every tile of this unit in the final list
-        const uint32_t pbase = uint32_t(a.cam_pair_base[u.cam]);
-        const uint32_t* col = a.counts + u.mbase + u.unit_in_cam;
-        for (uint32_t t = lane; t < u.tc; t += 32)
-            pos[t] = pbase + a.tile_rel[u.tile_base + t] + col[uint64_t(t) * u.units_in_cam];
+        const int wd = u.tiles_x + 1;
+        const uint32_t wb = u.rec_begin + uint32_t(warp) * kWarpRecords;
+        const uint32_t we = min(wb + kWarpRecords, u.rec_end);
+        // 1. this warp's pairs per tile (row differences, then row scans in place)
+        int* D = reinterpret_cast<int*>(pos);
+        for (int t = lane; t < wd * u.tiles_y; t += 32) D[t] = 0;
         __syncwarp();
-        auto place = [&](bool in, uint32_t tile, uint32_t sl) {
-            const uint32_t m = __ballot_sync(kFull, in);
-            const uint32_t peers = tile_peers(probe, tile, in, m, u.tbits);
-            const uint32_t below = peers & lanemask_lt();
-            const uint32_t pre = in ? pos[tile] : 0u;
-            __syncwarp();
-            if (in) {
-                if (below == 0) pos[tile] = pre + __popc(peers);
-                const uint32_t p = pre + __popc(below);
-                if (p < a.capacity) a.vals_out[p] = sl;
+        walk_groups<false>(a, wb, we, [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
+        __syncwarp();
+        for (int ty = 0; ty < u.tiles_y; ++ty)
+            scan_row(D, wd, ty, u.tiles_x, [&](int x, int v) { D[ty * wd + x] = v; });
+        __syncthreads();
+        // 2. first position of every tile for every warp: camera base + tile base + units
+        //    before this one + warps before this one
+        const uint32_t pbase = uint32_t(a.cam_pair_base[u.cam]);
+        const uint32_t* mrow = a.counts + u.mbase + uint64_t(u.unit_in_cam) * u.tc;
+        for (uint32_t t = threadIdx.x; t < u.tc; t += blockDim.x) {
+            const uint32_t ty = t / uint32_t(u.tiles_x), tx = t - ty * uint32_t(u.tiles_x);
+            const uint32_t cell = ty * uint32_t(wd) + tx;
+            uint32_t base = pbase + a.tile_rel[u.tile_base + t] + mrow[t];
+            for (int w = 0; w < nw; ++w) {
+                uint32_t* pw = reinterpret_cast<uint32_t*>(s_bin + w * wbytes);
+                const uint32_t c = pw[cell];
+                pw[cell] = base;
+                base += c;
             }
-            __syncwarp();
-        };
-        walk_groups(a, u.rec_begin, u.rec_end, [&](uint32_t slot, uint32_t r, bool valid) {
-            // exclusive offsets of the group's pairs in emission order
-            const uint32_t cnt = valid ? rect_area(r) : 0u;
+        }
+        __syncthreads();
+        // 3. place this warp's pairs in emission order
+        walk_groups<true>(a, wb, we, [&](uint32_t slot, uint32_t r, bool valid) {
+            const uint32_t cnt = valid ? (((r >> 16) & 255u) - (r & 255u) + 1u) *
+                                             ((r >> 24) - ((r >> 8) & 255u) + 1u)
+                                       : 0u;
             uint32_t incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t t = __shfl_up_sync(kFull, incl, o);
                 if (lane >= o) incl += t;
             }
+            const uint32_t excl = incl - cnt;
             const uint32_t total = __shfl_sync(kFull, incl, 31);
-            if (total > uint32_t(kTab)) {  // rare: huge splats; enumerate with the owner search
-                for_each_pair(slot, r, valid, u.tiles_x, place);
-                return;
-            }
-            // each lane writes its record's tiles (row-major) and its lane id into the tables
-            const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u, ty1 = r >> 24;
-            uint32_t k = incl - cnt;
-            if (valid)
-                for (uint32_t ty = ty0; ty <= ty1; ++ty)
-                    for (uint32_t tx = tx0; tx <= tx1; ++tx, ++k) {
-                        tab_tile[k] = uint16_t(ty * uint32_t(u.tiles_x) + tx);
-                        tab_own[k] = uint8_t(lane);
-                    }
-            __syncwarp();
-            for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-                const uint32_t j = k0 + lane;
+            const uint32_t magic = s_magic[((r >> 16) & 255u) - (r & 255u) + 1u];
+            const uint32_t lanemask_le = lanemask_lt() | (1u << lane);
+            int started = 0;  // records whose pair range starts before this step
+            for (uint32_t s0 = 0; s0 < total; s0 += 32) {
+                const bool starts = cnt != 0u && excl >= s0 && excl < s0 + 32u;
+                const uint32_t M = reduce_or(starts ? 1u << (excl - s0) : 0u);
+                const uint32_t j = s0 + uint32_t(lane);
                 const bool in = j < total;
-                const uint32_t tile = in ? tab_tile[j] : 0u;
-                const uint32_t own = in ? tab_own[j] : 0u;
+                int own = started + __popc(M & lanemask_le) - 1;
+                own = own < 0 ? 0 : own;
+                started += __popc(M);
+                const uint32_t o_ex = __shfl_sync(kFull, excl, own);
+                const uint32_t ro = __shfl_sync(kFull, r, own);
                 const uint32_t sl = __shfl_sync(kFull, slot, own);
-                place(in, tile, sl);
+                const uint32_t mg = __shfl_sync(kFull, magic, own);
+                const uint32_t kk = j - o_ex;
+                const uint32_t tx0 = ro & 255u, ty0 = (ro >> 8) & 255u, tx1 = (ro >> 16) & 255u;
+                const uint32_t w = tx1 - tx0 + 1u;
+                const uint32_t q = mg ? __umulhi(kk, mg) : kk;
+                const uint32_t cell = (ty0 + q) * uint32_t(wd) + tx0 + (kk - q * w);
+                // conflict probe: did another lane of this step write the same cell?
+                if (in) probe[cell] = uint8_t(lane);
+                __syncwarp();
+                const bool lost = in && probe[cell] != uint8_t(lane);
+                if (!__any_sync(kFull, lost)) {
+                    if (in) {
+                        const uint32_t p = pos[cell];
+                        pos[cell] = p + 1u;
+                        if (p < a.capacity) a.vals_out[p] = sl;
+                    }
+                } else {
+                    // rank the lanes of each cell by lane (= emission) order
+                    const uint32_t m = __ballot_sync(kFull, in);
+                    const uint32_t tile = (ty0 + q) * uint32_t(u.tiles_x) + tx0 + (kk - q * w);
+                    const uint32_t peers = peers_of_bits(kFull, tile, u.tbits) & m;
+                    const uint32_t below = peers & lanemask_lt();
+                    const uint32_t pre = in ? pos[cell] : 0u;
+                    __syncwarp();
+                    if (in) {
+                        if (below == 0) pos[cell] = pre + __popc(peers);
+                        const uint32_t p = pre + __popc(below);
+                        if (p < a.capacity) a.vals_out[p] = sl;
+                    }
+                }
+                __syncwarp();
             }
         });
+        __syncthreads();
     }
 }
 
@@ -539,7 +481,7 @@ void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 1024, 0, s>>>(a); }
 size_t bin_smem_bytes(const BinArgs& a) { return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc); }
 void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s) {
-    const size_t smem = bin_smem_bytes(a);
+    const size_t smem = size_t(a.max_tc) * sizeof(int);
     cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     bin_count_kernel<<<grid, 32 * a.bin_warps, smem, s>>>(a);
 }

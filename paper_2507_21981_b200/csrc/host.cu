@@ -132,9 +132,6 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> rects;
     DevBuf<uint32_t> dk[2], dv[2];   // depth-sort ping-pong
     DevBuf<uint64_t> status;         // onesweep lookback words
-    DevBuf<uint32_t> radix_counts;   // [256][chunks] per-chunk digit counts (reduce-then-scan)
-    DevBuf<uint32_t> radix_totals;   // [256]
-    bool use_onesweep = true;        // GSIM_GPU_ONESWEEP=0: reduce-then-scan passes instead
     int raster_rect_w = 8;           // GSIM_GPU_RASTER_RECT=16: 16x4 warp bands in K4 (default 8x8)
     int raster_exact_cull = 1;       // GSIM_GPU_RASTER_EXACT=0: bounding-box warp culling only
     int raster_batch = 128;          // GSIM_GPU_RASTER_BATCH=256: larger K4 batches, fewer CTAs/SM
@@ -468,13 +465,13 @@ void record_ev(gsim_gpu_context* ctx, int e) {
 void check_launch() { GSIM_CK(cudaGetLastError()); }
 
 int bin_warps_for(uint32_t max_tc) {
-    // u32 counters + u8 probe per grid cell, u16 + u8 table of 512 pairs (bin.cu bin_warp_bytes)
-    const size_t per_warp = (size_t(max_tc) * 5 + 512 * 3 + 15) & ~size_t(15);
+    // u32 counter + u8 probe per grid cell per warp (bin.cu bin_warp_bytes)
+    const size_t per_warp = (size_t(max_tc) * 5 + 15) & ~size_t(15);
     const size_t budget = 200 * 1024;
     const int w = int(std::min<size_t>(8, budget / std::max<size_t>(per_warp, 1)));
     if (w < 1)
         throw ValidationError{"camera with " + std::to_string(max_tc) +
-                              " tiles exceeds the binning shared-memory budget (51200 tiles)"};
+                              " tiles exceeds the binning shared-memory budget (40960 tiles)"};
     return w;
 }
 
@@ -501,7 +498,8 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     }
     ctx->zero_block.reserve(kZeroCams + C);
     ctx->counts.reserve(4);
-    const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + C;
+    const uint64_t R = uint64_t(kWarpRecords) * bin_warps_for(p.max_tc);
+    const uint64_t kmax = (S + R - 1) / R + C;
     ctx->cam_vbase.reserve(C + 1);
     ctx->cam_chunk_base.reserve(C + 1);
     ctx->cam_pairs.reserve(C);
@@ -527,7 +525,7 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
     b.depth_bits = p.depth_bits;
     b.n_cams = int(p.cams.size());
     b.sorted_slots = sorted_slots;
-    b.rects = ctx->rects.ptr;
+    b.sorted_rects = ctx->dk[1].ptr;  // written by the last depth pass
     b.cam_tile_base = ctx->cam_tile_base;
     b.cam_tiles_x = ctx->cam_tiles_x;
     b.cam_visible = ctx->zero_block.ptr + kZeroCams;
@@ -546,8 +544,8 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
     b.vals_out = ctx->vals.ptr;
     b.capacity = ctx->pair_capacity;
     b.max_tc = int(p.max_tc);
-    b.chunk_records = kChunkRecords;
     b.bin_warps = bin_warps_for(p.max_tc);
+    b.chunk_records = kWarpRecords * b.bin_warps;
     return b;
 }
 
@@ -586,7 +584,6 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
 
     // key histograms + per-camera counts, then the chunk table (needs only the counts)
     BinArgs b = make_bin_args(ctx, p, ctx->dv[1].ptr);
-    if (!ctx->use_onesweep) b.hist = nullptr;  // the reduce-then-scan passes count their own digits
     launch_key_hist(b, n_sms * 4, s);
     b.hist = ctx->zero_block.ptr + kZeroHist;
     check_launch();
@@ -594,36 +591,6 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     check_launch();
     launches += 2;
 
-    if (!ctx->use_onesweep) {
-        // 4 reduce-then-scan LSD passes over (camera | depth) keys; pass 1 drops culled slots.
-        const uint32_t max_chunks = uint32_t(std::max<uint64_t>(1, (S + kOnesweepTile - 1) / kOnesweepTile));
-        ctx->radix_counts.reserve(uint64_t(256) * max_chunks);
-        ctx->radix_totals.reserve(256);
-        const uint32_t* kin = ctx->keys.ptr;
-        const uint32_t* vin = nullptr;
-        for (int pass = 0; pass < 4; ++pass) {
-            const int o = pass & 1;
-            RadixArgs ra{};
-            ra.keys_in = kin;
-            ra.vals_in = vin;
-            ra.keys_out = ctx->dk[o].ptr;
-            ra.vals_out = ctx->dv[o].ptr;
-            ra.n_dev = ctx->counts.ptr + 0;
-            ra.n_host = S;
-            ra.counts = ctx->radix_counts.ptr;
-            ra.totals = ctx->radix_totals.ptr;
-            ra.max_chunks = max_chunks;
-            ra.shift = 8 * pass;
-            ra.first = pass == 0;
-            ra.write_keys = pass < 3;
-            launch_radix_pass(ra, s);
-            check_launch();
-            launches += 3;
-            kin = ctx->dk[o].ptr;
-            vin = ctx->dv[o].ptr;
-        }
-        record_ev(ctx, kEvDepth);
-    } else {
     // 4 onesweep passes over (camera | depth) keys; pass 1 compacts the culled slots away.
     OnesweepArgs oa{};
     oa.n_dev = ctx->counts.ptr + 0;
@@ -643,6 +610,9 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         oa.ticket = ctx->zero_block.ptr + kZeroTickets + pass;
         oa.epoch = ctx->next_epoch();
         oa.shift = 8 * pass;
+        // the last pass also gathers the tile rects into depth order (into dk[1], free by then)
+        oa.rects_in = pass == 3 ? ctx->rects.ptr : nullptr;
+        oa.rects_out = pass == 3 ? ctx->dk[1].ptr : nullptr;
         launch_onesweep(oa, pass == 0, pass < 3, int(dgrid), s);
         check_launch();
         ++launches;
@@ -650,16 +620,14 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         vin = ctx->dv[o].ptr;
     }
     record_ev(ctx, kEvDepth);
-    }
 
     // tile binning: counts, scans, camera bases
-    const uint64_t kmax = (S + kChunkRecords - 1) / kChunkRecords + p.cams.size();
-    // one warp per unit, bin_warps units per block
-    const int chunk_grid = int(std::max<uint64_t>(1, (kmax + b.bin_warps - 1) / b.bin_warps));
+    const uint64_t kmax = (S + b.chunk_records - 1) / b.chunk_records + p.cams.size();
+    // one CTA of bin_warps warps per unit
+    const int chunk_grid = int(std::max<uint64_t>(1, kmax));
     launch_bin_count(b, chunk_grid, s);
     check_launch();
-    const uint64_t col_warps = p.tiles;
-    launch_bin_colscan(b, int(std::max<uint64_t>(1, std::min<uint64_t>((col_warps + 7) / 8, uint64_t(n_sms) * 8))), s);
+    launch_bin_colscan(b, int(std::max<uint64_t>(1, (uint64_t(p.tiles) + 255) / 256)), s);
     check_launch();
     launch_bin_tilescan(b, int(std::min<uint64_t>(p.cams.size(), uint64_t(n_sms) * 2)), s);
     check_launch();
@@ -1208,7 +1176,6 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         ctx->zero_block.reserve(kZeroCams + 64);
         ctx->counts.reserve(4);
         ctx->readback.reserve(64);
-        if (const char* e = std::getenv("GSIM_GPU_ONESWEEP")) ctx->use_onesweep = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_RECT")) ctx->raster_rect_w = std::atoi(e) == 16 ? 16 : 8;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_EXACT")) ctx->raster_exact_cull = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
@@ -1242,8 +1209,6 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
         ctx->staging[k].release();
     }
     ctx->status.release();
-    ctx->radix_counts.release();
-    ctx->radix_totals.release();
     ctx->vals.release();
     ctx->zero_block.release();
     ctx->counts.release();

@@ -13,7 +13,7 @@ namespace gsim_gpu {
 
 constexpr int kMaxSmemSegments = 1024;
 constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
-constexpr int kChunkRecords = 1024;     // depth-sorted records per binning unit (one warp)
+constexpr int kWarpRecords = 1024;      // depth-sorted records per warp of a binning unit
 
 struct PreprocessArgs {
     DevField field;
@@ -54,23 +54,8 @@ struct OnesweepArgs {
     uint32_t* ticket;                // zeroed per pass
     uint32_t epoch;
     int shift;
-};
-
-// One reduce-then-scan LSD pass (sort.cu): upsweep counts per (digit, chunk), a per-digit scan
-// over chunks, then a downsweep that ranks and scatters. No decoupled look-back.
-struct RadixArgs {
-    const uint32_t* keys_in;
-    const uint32_t* vals_in;         // nullptr on the first pass: value = input index
-    uint32_t* keys_out;
-    uint32_t* vals_out;
-    const unsigned long long* n_dev; // element count on device (first pass: n_host)
-    uint64_t n_host;
-    uint32_t* counts;                // [256][max_chunks] digit-major per-chunk counts -> prefixes
-    uint32_t* totals;                // [256] digit totals of the pass
-    uint32_t max_chunks;
-    int shift;
-    int first;                       // input is the per-slot key plane (drop kInvalidKey)
-    int write_keys;
+    const uint32_t* rects_in;        // last pass: gather rects_in[slot] ...
+    uint32_t* rects_out;             // ... into depth order (nullptr on the other passes)
 };
 
 // Tile binning of the camera-major depth-sorted records (bin.cu).
@@ -80,7 +65,7 @@ struct BinArgs {
     int depth_bits;
     int n_cams;
     const uint32_t* sorted_slots;    // [V] record slots, camera-major depth order
-    const uint32_t* rects;           // [S]
+    const uint32_t* sorted_rects;    // [V] tile rects of sorted_slots (gathered by the sort)
     const uint32_t* cam_tile_base;   // [C+1]
     const int* cam_tiles_x;          // [C]
     uint32_t* cam_visible;           // [C]   V_c (zeroed per frame)
@@ -98,9 +83,9 @@ struct BinArgs {
     unsigned long long* totals;      // [0] V, [1] P
     uint32_t* vals_out;              // [capacity] record slot of every pair, final order
     uint64_t capacity;
-    int max_tc;                      // largest tile count of a camera in the batch
-    int chunk_records;
-    int bin_warps;                   // warps per block that own a counter array
+    int max_tc;                      // largest (tiles_x + 1) * (tiles_y + 1) of the batch
+    int chunk_records;               // records per unit = 1024 * bin_warps
+    int bin_warps;                   // warps per unit CTA
     int reserved;
 };
 
@@ -167,7 +152,6 @@ void launch_preprocess(const PreprocessArgs& a, bool full, int grid_cap, cudaStr
 void launch_splats_to_records(const SplatArgs& a, int grid_cap, cudaStream_t stream);
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream);
-void launch_radix_pass(const RadixArgs& a, cudaStream_t stream);
 void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s);
 void launch_chunk_table(const BinArgs& a, cudaStream_t s);
 size_t bin_smem_bytes(const BinArgs& a);

@@ -163,180 +163,10 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
             const uint64_t dst = s_dest[(key >> a.shift) & 255u] + p;
             if (kWriteKeys) a.keys_out[dst] = key;
             a.vals_out[dst] = s_vals[p];
+            if (a.rects_out) a.rects_out[dst] = __ldg(a.rects_in + s_vals[p]);
         }
         __syncthreads();
     }
-}
-
-// ---- reduce-then-scan LSD pass ------------------------------------------------------------
-// The persistent onesweep above starts hundreds of chunks at once, and a chunk's per-digit
-// look-back then walks past every predecessor that has only published its aggregate: on this
-// part that chain (one L2 round trip per step) dominated the pass. The three kernels below
-// need no inter-block waiting at all: chunk counts are written to a digit-major matrix, one
-// block per digit scans its row, and the downsweep reads its offsets directly.
-namespace {
-
-__device__ __forceinline__ uint64_t radix_n(const RadixArgs& a) {
-    return a.first ? a.n_host : uint64_t(*a.n_dev);
-}
-
-// Load the chunk's keys (item i of lane l of warp w at base + w*512 + i*32 + l) and mark valid.
-__device__ __forceinline__ void radix_load(const RadixArgs& a, uint64_t n, uint64_t base,
-                                           uint32_t* keys, uint32_t* vals, uint32_t& valid_bits,
-                                           bool with_vals) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    valid_bits = 0;
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = base + uint64_t(warp) * (kItems * 32) + uint64_t(i) * 32 + lane;
-        const bool in = idx < n;
-        keys[i] = in ? __ldcs(a.keys_in + idx) : kInvalidKey;
-        if (with_vals) vals[i] = a.first ? uint32_t(idx) : (in ? __ldcs(a.vals_in + idx) : 0u);
-        const bool valid = in && !(a.first && keys[i] == kInvalidKey);
-        valid_bits |= valid ? (1u << i) : 0u;
-    }
-}
-
-}  // namespace
-
-__global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(RadixArgs a) {
-    __shared__ uint32_t s_warp_hist[kWarps][kRadix];
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const uint64_t n = radix_n(a);
-    const uint32_t chunks = uint32_t((n + kOnesweepTile - 1) / kOnesweepTile);
-    const uint32_t c = blockIdx.x;
-    if (c >= chunks) return;
-    for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_warp_hist[0][0])[k] = 0;
-    __syncthreads();
-    uint32_t keys[kItems], valid_bits;
-    radix_load(a, n, uint64_t(c) * kOnesweepTile, keys, nullptr, valid_bits, false);
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const bool valid = (valid_bits >> i) & 1u;
-        const uint32_t d = (keys[i] >> a.shift) & 255u;
-        const uint32_t peers = peers_of<8>(0xffffffffu, d) & __ballot_sync(0xffffffffu, valid);
-        if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
-    }
-    __syncthreads();
-    uint32_t s = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += s_warp_hist[w][tid];
-    a.counts[uint64_t(tid) * a.max_chunks + c] = s;
-}
-
-// One block per digit: exclusive scan of the digit's row over the chunks, and its total.
-__global__ void __launch_bounds__(1024) radix_scan_kernel(RadixArgs a) {
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_carry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t n = radix_n(a);
-    const uint32_t chunks = uint32_t((n + kOnesweepTile - 1) / kOnesweepTile);
-    uint32_t* row = a.counts + uint64_t(blockIdx.x) * a.max_chunks;
-    if (tid == 0) s_carry = 0;
-    __syncthreads();
-    for (uint32_t c0 = 0; c0 < chunks; c0 += 1024) {
-        const uint32_t c = c0 + tid;
-        const uint32_t v = c < chunks ? row[c] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        uint32_t wp = 0, tot = 0;
-        for (int w = 0; w < 32; ++w) {
-            const uint32_t t = s_warp[w];
-            if (w < warp) wp += t;
-            tot += t;
-        }
-        if (c < chunks) row[c] = s_carry + wp + incl - v;
-        __syncthreads();
-        if (tid == 0) s_carry += tot;
-        __syncthreads();
-    }
-    if (tid == 0) a.totals[blockIdx.x] = s_carry;
-}
-
-template <bool kWriteKeys>
-__global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(RadixArgs a) {
-    __shared__ uint32_t s_keys[kOnesweepTile];
-    __shared__ uint32_t s_vals[kOnesweepTile];
-    __shared__ uint32_t s_warp_hist[kWarps][kRadix];
-    __shared__ uint32_t s_bstart[kRadix];
-    __shared__ uint32_t s_dest[kRadix];
-    __shared__ uint32_t s_tmp[kWarps];
-    __shared__ uint32_t s_total;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t n = radix_n(a);
-    const uint32_t chunks = uint32_t((n + kOnesweepTile - 1) / kOnesweepTile);
-    const uint32_t c = blockIdx.x;
-    if (c >= chunks) return;
-    for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_warp_hist[0][0])[k] = 0;
-    // global start of every digit: exclusive scan of the pass totals
-    uint32_t digit_total;
-    const uint32_t gbase = block_exclusive_scan(a.totals[tid], s_tmp, &digit_total);
-    const uint32_t chunk_prefix = a.counts[uint64_t(tid) * a.max_chunks + c];
-    uint32_t keys[kItems], vals[kItems], rank[kItems], valid_bits;
-    radix_load(a, n, uint64_t(c) * kOnesweepTile, keys, vals, valid_bits, true);
-    __syncthreads();
-    // Warp-level stable ranking, item order (i, lane) = memory order. The lowest lane of each
-    // digit group bumps the warp's counter with an atomic that returns the running count; the
-    // atomics of consecutive items are ordered by the hardware, so no item waits on another
-    // in registers and the 16 items pipeline (shared atomics are cheap on this part, measured
-    // in tools/microbench.cu; match.any is not).
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const bool valid = (valid_bits >> i) & 1u;
-        const uint32_t d = (keys[i] >> a.shift) & 255u;
-        const uint32_t peers = peers_of<8>(0xffffffffu, d) & __ballot_sync(0xffffffffu, valid);
-        const uint32_t below = peers & lanemask_lt();
-        const int leader = peers ? __ffs(peers) - 1 : lane;
-        uint32_t pre = 0;
-        if (valid && below == 0) pre = atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
-        pre = __shfl_sync(0xffffffffu, pre, leader);
-        rank[i] = pre + __popc(below);
-    }
-    __syncthreads();
-    uint32_t count = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const uint32_t cw = s_warp_hist[w][tid];
-        s_warp_hist[w][tid] = count;
-        count += cw;
-    }
-    uint32_t block_total;
-    const uint32_t bstart = block_exclusive_scan(count, s_tmp, &block_total);
-    s_bstart[tid] = bstart;
-    s_dest[tid] = gbase + chunk_prefix - bstart;  // modular: dest = s_dest[d] + position
-    if (tid == 0) s_total = block_total;
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        if (!((valid_bits >> i) & 1u)) continue;
-        const uint32_t d = (keys[i] >> a.shift) & 255u;
-        const uint32_t pos = s_bstart[d] + s_warp_hist[warp][d] + rank[i];
-        s_keys[pos] = keys[i];
-        s_vals[pos] = vals[i];
-    }
-    __syncthreads();
-    const uint32_t total = s_total;
-    for (uint32_t p = tid; p < total; p += kThreads) {
-        const uint32_t key = s_keys[p];
-        const uint32_t dst = s_dest[(key >> a.shift) & 255u] + p;
-        if (kWriteKeys) a.keys_out[dst] = key;
-        a.vals_out[dst] = s_vals[p];
-    }
-}
-
-void launch_radix_pass(const RadixArgs& a, cudaStream_t stream) {
-    radix_upsweep_kernel<<<a.max_chunks, kThreads, 0, stream>>>(a);
-    radix_scan_kernel<<<kRadix, 1024, 0, stream>>>(a);
-    if (a.write_keys)
-        radix_downsweep_kernel<true><<<a.max_chunks, kThreads, 0, stream>>>(a);
-    else
-        radix_downsweep_kernel<false><<<a.max_chunks, kThreads, 0, stream>>>(a);
 }
 
 // ---- launchers -----------------------------------------------------------------------------

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("report")
 ap.add_argument("kernel")
 ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--by", default="samples", choices=["samples", "inst"])
 a = ap.parse_args()
 
 out = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--kernel-name", a.kernel,
@@ -57,7 +58,7 @@ for r in rows:
 tot_s = sum(v["samples"] for v in agg.values()) or 1
 tot_i = sum(v["inst"] for v in agg.values()) or 1
 print(f"total samples {tot_s:.0f}, warp instructions {tot_i:.3e}")
-for key, v in sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[: a.top]:
+for key, v in sorted(agg.items(), key=lambda kv: -kv[1][a.by])[: a.top]:
     stalls = sorted(((k[6:], x) for k, x in v.items() if k.startswith("stall_")), key=lambda t: -t[1])[:3]
     st = " ".join(f"{k}:{x / max(v['samples'], 1):.0%}" for k, x in stalls if x)
     print(f"{key[0]}:{key[1]:<4} {v['samples'] / tot_s:6.1%} smp {v['inst'] / tot_i:6.1%} inst  "
