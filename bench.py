@@ -456,7 +456,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--contexts", type=int, default=2,
+    ap.add_argument("--contexts", type=int, default=4,
                     help="renderer contexts taking frames in turn (frame-level overlap)")
     ap.add_argument("--gather", action="store_true",
                     help="N > 1: gather every step's frames to rank 0 (config 4) inside the timed step")

@@ -702,6 +702,7 @@ PreprocessArgs make_pre_args(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
     pa.rects = ctx->rects.ptr;
     pa.keys = ctx->keys.ptr;
     pa.key_base = p.key_base;
+    pa.n_cams = uint32_t(p.cams.size());
     return pa;
 }
 
@@ -741,7 +742,7 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     uint64_t launches = posed ? 1 : 0;
     PreprocessArgs pa = make_pre_args(ctx, scene, plan);
     if (plan.slots) {
-        launch_preprocess(pa, false, ctx->num_sms * 3, ctx->stream);
+        launch_preprocess(pa, false, ctx->num_sms, ctx->stream);
         check_launch();
         ++launches;
     }
@@ -1453,7 +1454,7 @@ int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const g
         pa.full = ctx->full.ptr;
         pa.full_visible = ctx->full_vis.ptr;
         if (plan.slots) {
-            launch_preprocess(pa, true, ctx->num_sms * 3, ctx->stream);
+            launch_preprocess(pa, true, ctx->num_sms, ctx->stream);
             check_launch();
             ctx->launches_total += 1;
         }

@@ -12,6 +12,7 @@
 namespace gsim_gpu {
 
 constexpr int kMaxSmemSegments = 1024;
+constexpr int kMaxSmemCams = 32;        // K2 stages up to this many cameras in shared memory
 constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
 constexpr int kWarpRecords = 1024;      // depth-sorted records per warp of a binning unit
 
@@ -26,7 +27,7 @@ struct PreprocessArgs {
     uint32_t* rects;                 // [slots] packed tile rect (binning reads this plane)
     uint32_t* keys;                  // [slots], kInvalidKey when culled / no tile
     uint32_t key_base;               // float bits of the batch's smallest near plane
-    uint32_t reserved;
+    uint32_t n_cams;                 // cameras of the batch (staged in shared memory if few)
     gsim_projected_splat* full;      // project() API only: double splat per slot
     uint8_t* full_visible;           // project() API only
 };
@@ -148,7 +149,7 @@ struct EncodeKernelArgs {
 
 void launch_pose(const DevField& f, uint64_t begin, uint64_t end, const gsim_rigid& t,
                  int grid_cap, cudaStream_t stream);
-void launch_preprocess(const PreprocessArgs& a, bool full, int grid_cap, cudaStream_t stream);
+void launch_preprocess(const PreprocessArgs& a, bool full, int n_sms, cudaStream_t stream);
 void launch_splats_to_records(const SplatArgs& a, int grid_cap, cudaStream_t stream);
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream);

@@ -10,6 +10,7 @@
 // Per (camera, primitive) slot it writes a 48-byte Record and a 32-bit depth key (kInvalidKey
 // when culled or when the splat touches no tile), and accumulates the four 8-bit digit
 // histograms of the keys for the onesweep depth sort.
+#include <algorithm>
 #include <cstdint>
 
 #include "../../include/gsim_gpu.h"
@@ -79,31 +80,33 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float* basis
     }
 }
 
+// rgb_c = max(0, 0.5 + sum_k basis_k * sh[c][k])  (sh.cpp:45-49). Coefficient c*K + k of a
+// primitive is component (c*K + k) % 4 of float4 plane (c*K + k) / 4; the planes are loaded
+// channel by channel, so at most two channels' coefficients are live at once.
 template <int DEG>
-struct ShRegs {
-    static constexpr int K = (DEG + 1) * (DEG + 1);
-    static constexpr int kPlanes = (3 * K + 3) / 4;
-    float c[kPlanes * 4];
-    __device__ __forceinline__ void load(const float4* sh, uint64_t n, uint64_t i) {
+__device__ __forceinline__ void shade_sh(const float4* sh, uint64_t n, uint64_t i, float x,
+                                         float y, float z, float rgb[3]) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    float basis[16];
+    sh_basis<DEG>(x, y, z, basis);
 #pragma unroll
-        for (int p = 0; p < kPlanes; ++p) {
-            const float4 v = __ldg(sh + uint64_t(p) * n + i);
-            c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
+    for (int ch = 0; ch < 3; ++ch) {
+        constexpr int kMaxPl = (K + 3) / 4 + 1;
+        const int p0 = (ch * K) / 4, p1 = (ch * K + K - 1) / 4;
+        float c[kMaxPl * 4];
+#pragma unroll
+        for (int p = 0; p < kMaxPl; ++p) {
+            if (p0 + p <= p1) {
+                const float4 v = __ldg(sh + uint64_t(p0 + p) * n + i);
+                c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
+            }
         }
-    }
-    // rgb_c = max(0, 0.5 + sum_k basis_k * sh[c][k])  (sh.cpp:45-49)
-    __device__ __forceinline__ void shade(float x, float y, float z, float rgb[3]) const {
-        float basis[16];
-        sh_basis<DEG>(x, y, z, basis);
+        float acc = 0.5f;
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            float acc = 0.5f;
-#pragma unroll
-            for (int k = 0; k < K; ++k) acc += basis[k] * c[ch * K + k];
-            rgb[ch] = (acc < 0.0f) ? 0.0f : acc;
-        }
+        for (int k = 0; k < K; ++k) acc += basis[k] * c[ch * K + k - 4 * p0];
+        rgb[ch] = (acc < 0.0f) ? 0.0f : acc;
     }
-};
+}
 
 }  // namespace
 
@@ -124,12 +127,23 @@ __global__ void __launch_bounds__(256) pose_kernel(DevField f, uint64_t begin, u
 }
 
 // ---- K2: project + shade_sh (raster.cpp:135-232, sh.cpp:10-51) ---------------------------
-template <int DEG, bool kFull>
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args) {
+template <int DEG, bool kFull, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs args) {
     __shared__ uint64_t s_seg_begin[kMaxSmemSegments];
+    __shared__ DevCamera s_cams[kMaxSmemCams];
     const DevField f = args.field;
     const int n_seg_smem = args.n_segs < kMaxSmemSegments ? args.n_segs : kMaxSmemSegments;
     for (int k = threadIdx.x; k < n_seg_smem; k += blockDim.x) s_seg_begin[k] = args.segs[k].begin;
+    // Cameras are read in every iteration of the camera loop: shared memory keeps those reads
+    // off the L1 miss path.
+    const bool cams_smem = args.n_cams <= uint32_t(kMaxSmemCams);
+    if (cams_smem) {
+        static_assert(sizeof(DevCamera) % 8 == 0, "DevCamera copy");
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(args.cams);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(s_cams);
+        const uint32_t words = args.n_cams * uint32_t(sizeof(DevCamera) / 8);
+        for (uint32_t k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
+    }
     __syncthreads();
 
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < f.n;
@@ -164,7 +178,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args)
 
         for (uint32_t e = 0; e < seg.entry_count; ++e) {
             const SegEntry ent = args.entries[seg.entry_begin + e];
-            const DevCamera& cam = args.cams[ent.cam];
+            const DevCamera& cam = cams_smem ? s_cams[ent.cam] : args.cams[ent.cam];
             const uint64_t slot = ent.slot_base + (i - seg.begin);
 
             const dq cq{cam.q[0], cam.q[1], cam.q[2], cam.q[3]};
@@ -227,11 +241,17 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args)
             tx1 = tx1 > cam.tiles_x - 1 ? cam.tiles_x - 1 : tx1;
             ty1 = ty1 > cam.tiles_y - 1 ? cam.tiles_y - 1 : ty1;
 
-            // Coefficients are (re)loaded per camera: the first camera brings the primitive's
-            // 192 B into L1, later cameras hit it, and the 48 registers are not held across
-            // the camera loop (occupancy).
-            ShRegs<DEG> sh;
-            sh.load(f.sh, f.n, i);
+            // Record geometry in fp32 first, so the double state is dead before shading.
+            const float fz = __double2float_rn(z);
+            const float fu = __double2float_rn(u), fv = __double2float_rn(v),
+                        frad = __double2float_rn(radius);
+            float fia = 0.f, fib = 0.f, fic = 0.f;
+            if (!off_grid) {
+                const double inv_det = 1.0 / det;
+                fia = __double2float_rn(cov_yy * inv_det);
+                fib = __double2float_rn(-cov_xy * inv_det);
+                fic = __double2float_rn(cov_xx * inv_det);
+            }
             float vx = float(mean_world.x - cam.center[0]);
             float vy = float(mean_world.y - cam.center[1]);
             float vz = float(mean_world.z - cam.center[2]);
@@ -244,10 +264,11 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args)
             const float lx = vx + t0 * nqw + (nqy * t2 - nqz * t1v);
             const float ly = vy + t1v * nqw + (nqz * t0 - nqx * t2);
             const float lz = vz + t2 * nqw + (nqx * t1v - nqy * t0);
+            // Coefficients are (re)loaded per camera: the first camera brings the primitive's
+            // 192 B into L1, later cameras hit it; nothing is held across the camera loop.
             float rgb[3];
-            sh.shade(lx, ly, lz, rgb);
+            shade_sh<DEG>(f.sh, f.n, i, lx, ly, lz, rgb);
 
-            const float fz = __double2float_rn(z);
             if (kFull) {
                 gsim_projected_splat s;
                 s.pixel_center[0] = u;
@@ -268,12 +289,8 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(PreprocessArgs args)
                 args.keys[slot] = kInvalidKey;
                 continue;
             }
-            const double inv_det = 1.0 / det;
-            args.records[slot] = make_record(
-                __double2float_rn(u), __double2float_rn(v), fz, __double2float_rn(radius),
-                __double2float_rn(cov_yy * inv_det), __double2float_rn(-cov_xy * inv_det),
-                __double2float_rn(cov_xx * inv_det), __double2float_rn(opacity), rgb[0], rgb[1],
-                rgb[2]);
+            args.records[slot] = make_record(fu, fv, fz, frad, fia, fib, fic,
+                                             __double2float_rn(opacity), rgb[0], rgb[1], rgb[2]);
             const uint32_t rec_rect = pack_rect(tx0, ty0, tx1, ty1);
             args.rects[slot] = rec_rect;
             // Camera-major sort key: camera index above the float32 depth bits
@@ -328,23 +345,27 @@ void launch_pose(const DevField& f, uint64_t begin, uint64_t end, const gsim_rig
     pose_kernel<<<unsigned(blocks), 256, 0, stream>>>(f, begin, end, t);
 }
 
+// 128-thread blocks at 5 per SM (102 registers): the double-precision camera loop spills
+// little and 20 warps per SM hide its load latency (measured best of 256x2/3, 128x5/6, 192x3).
 template <int DEG>
-static void launch_pre_deg(const PreprocessArgs& a, bool full, unsigned grid, cudaStream_t s) {
+static void launch_pre_deg(const PreprocessArgs& a, bool full, uint64_t n, int n_sms,
+                           cudaStream_t s) {
+    constexpr int kNT = 128, kMinB = 5;
+    const unsigned grid =
+        unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + kNT - 1) / kNT, uint64_t(n_sms) * kMinB)));
     if (full)
-        preprocess_kernel<DEG, true><<<grid, 256, 0, s>>>(a);
+        preprocess_kernel<DEG, true, kNT, kMinB><<<grid, kNT, 0, s>>>(a);
     else
-        preprocess_kernel<DEG, false><<<grid, 256, 0, s>>>(a);
+        preprocess_kernel<DEG, false, kNT, kMinB><<<grid, kNT, 0, s>>>(a);
 }
 
-void launch_preprocess(const PreprocessArgs& a, bool full, int grid_cap, cudaStream_t stream) {
+void launch_preprocess(const PreprocessArgs& a, bool full, int n_sms, cudaStream_t stream) {
     if (a.field.n == 0) return;
-    uint64_t blocks = (a.field.n + 255) / 256;
-    if (blocks > uint64_t(grid_cap)) blocks = grid_cap;
     switch (a.field.sh_degree) {
-        case 0: launch_pre_deg<0>(a, full, unsigned(blocks), stream); break;
-        case 1: launch_pre_deg<1>(a, full, unsigned(blocks), stream); break;
-        case 2: launch_pre_deg<2>(a, full, unsigned(blocks), stream); break;
-        default: launch_pre_deg<3>(a, full, unsigned(blocks), stream); break;
+        case 0: launch_pre_deg<0>(a, full, a.field.n, n_sms, stream); break;
+        case 1: launch_pre_deg<1>(a, full, a.field.n, n_sms, stream); break;
+        case 2: launch_pre_deg<2>(a, full, a.field.n, n_sms, stream); break;
+        default: launch_pre_deg<3>(a, full, a.field.n, n_sms, stream); break;
     }
 }
 
