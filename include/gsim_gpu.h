@@ -187,18 +187,18 @@ int32_t gsim_gpu_scene_sh_degree(const gsim_gpu_scene* scene);
  * (scale <= 1 ulp from glibc, opacity = 1 / (1 + exp(-x)) <= 2 ulp). */
 int gsim_gpu_scene_load_ply(gsim_gpu_context* ctx, const char* path, gsim_gpu_scene** out);
 
-/* project (raster.cpp:135-232): visible splats in primitive order. Writes at most
+/* project (raster.cpp:66-163): visible splats in primitive order. Writes at most
  * capacity splats to out and the visible count to *count (count may exceed capacity). */
 int gsim_gpu_project(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
                      uint64_t n_nodes, const gsim_camera* camera, gsim_projected_splat* out,
                      uint64_t capacity, uint64_t* count);
 
-/* rasterize (raster.cpp:234-323) of host splats into a host target. */
+/* rasterize (raster.cpp:165-254) of host splats into a host target. */
 int gsim_gpu_rasterize(gsim_gpu_context* ctx, const gsim_projected_splat* splats, uint64_t n,
                        const gsim_camera* camera, const gsim_raster_options* options,
                        gsim_target* out);
 
-/* render (raster.cpp:325-334): one host target per camera; returns after the copies land. */
+/* render (raster.cpp:256-265): one host target per camera; returns after the copies land. */
 int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
                     uint64_t n_nodes, const gsim_camera* cameras, uint64_t n_cameras,
                     const gsim_raster_options* options, gsim_target* outs);
@@ -214,7 +214,7 @@ int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
 float* gsim_gpu_device_output(gsim_gpu_context* ctx);
 
 /* Sorted tile lists of one camera of the last render/rasterize on ctx (test hook for the
- * reference's pair sort, raster.cpp:243-271): tile_begin gets tiles_x*tiles_y+1 offsets,
+ * reference's pair sort, raster.cpp:174-202): tile_begin gets tiles_x*tiles_y+1 offsets,
  * values gets the primitive index (render) or splat index (rasterize) of each pair in
  * sorted order. *count = number of pairs of that camera (values may be NULL to query). */
 int gsim_gpu_tile_lists(gsim_gpu_context* ctx, uint32_t camera, uint32_t* tile_begin,

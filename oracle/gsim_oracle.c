@@ -161,7 +161,7 @@ void gso_camera_center(const gsim_camera* cam, double out[3]) { /* camera.hpp:23
 
 void gso_look_at(const double eye_[3], const double target_[3], double fx, double fy, int width,
                  int height, const double up_[3], gsim_camera* cam) {
-    /* CameraModel::look_at, raster.cpp:94-111 */
+    /* CameraModel::look_at, raster.cpp:25-42 */
     memset(cam, 0, sizeof(*cam));
     cam->fx = fx; cam->fy = fy;
     cam->cx = width * 0.5; cam->cy = height * 0.5;
@@ -260,7 +260,7 @@ static double clampd(double v, double lo, double hi) { /* std::clamp */
 int gso_project(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
                 const gsim_camera* camera, gsim_projected_splat* out, uint64_t capacity,
                 uint64_t* count) {
-    /* raster.cpp:135-232 */
+    /* raster.cpp:66-163 */
     if (validate_camera(camera) != GSIM_OK) return GSIM_ERR_VALIDATION;
     const uint64_t n = field->count;
     /* PoseTable (raster.cpp:47-62): index 0 is identity; later nodes overwrite earlier ones. */
@@ -375,7 +375,7 @@ static int cmp_pair(const void* pa, const void* pb) {
     return 0;
 }
 
-/* Pair emission + std::sort + tile ranges, raster.cpp:243-271. */
+/* Pair emission + std::sort + tile ranges, raster.cpp:174-202. */
 static pair_t* build_pairs(const gsim_projected_splat* splats, uint64_t n, int tiles_x,
                            int tiles_y, uint64_t* n_pairs, uint64_t** tile_begin_out) {
     uint64_t cap = 1024, np = 0;
@@ -420,7 +420,7 @@ static void blend_pixel(const gsim_projected_splat* splats, const pair_t* pairs,
                         uint64_t begin, uint64_t end, const uint32_t* order, int x, int y,
                         const gsim_raster_options* options, const double* q_cut, float* rgb,
                         float* depth, float* alpha) {
-    /* raster.cpp:284-318 (pairs != NULL) or reference_raster.cpp:108-143 (order != NULL) */
+    /* raster.cpp:215-249 (pairs != NULL) or reference_raster.cpp:29-65 (order != NULL) */
     const double px = x + 0.5;
     const double py = y + 0.5;
     double cr = 0.0, cg = 0.0, cb = 0.0, d = 0.0, acc = 0.0;
@@ -457,7 +457,7 @@ static void blend_pixel(const gsim_projected_splat* splats, const pair_t* pairs,
 
 int gso_rasterize(const gsim_projected_splat* splats, uint64_t n, const gsim_camera* camera,
                   const gsim_raster_options* options, float* rgb, float* depth, float* alpha) {
-    /* raster.cpp:234-323 (rasterize does not validate the camera) */
+    /* raster.cpp:165-254 (rasterize does not validate the camera) */
     const int width = camera->width, height = camera->height;
     memset(rgb, 0, sizeof(float) * 3 * (size_t)width * height);
     memset(depth, 0, sizeof(float) * (size_t)width * height);
@@ -548,7 +548,7 @@ int gso_reference_rasterize(const gsim_projected_splat* splats, uint64_t n,
 int gso_render(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
                const gsim_camera* cameras, uint64_t n_cameras,
                const gsim_raster_options* options, gsim_target* outs) {
-    /* raster.cpp:325-334: every camera independently; validation before any output. */
+    /* raster.cpp:256-265: every camera independently; validation before any output. */
     for (uint64_t c = 0; c < n_cameras; ++c)
         if (validate_camera(&cameras[c]) != GSIM_OK) return GSIM_ERR_VALIDATION;
     gsim_projected_splat* splats =

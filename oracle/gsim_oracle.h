@@ -6,10 +6,10 @@
  * (paper_2507_21981_b200, libgsim_gpu.so) never links or calls it.
  *
  * Restates in plain C, in double precision and in the reference's operation order:
- *   project            raster.cpp:135-232      rasterize           raster.cpp:234-323
- *   reference_rasterize reference_raster.cpp:12-67   render        raster.cpp:325-334
+ *   project            raster.cpp:66-163      rasterize           raster.cpp:165-254
+ *   reference_rasterize reference_raster.cpp:12-67   render        raster.cpp:256-265
  *   shade_sh           sh.cpp:10-51            transform_primitives gaussian.cpp:65-79
- *   CameraModel::look_at raster.cpp:94-111     Quat::from_matrix   math.hpp:158-187
+ *   CameraModel::look_at raster.cpp:25-42     Quat::from_matrix   math.hpp:158-187
  *   oracle::random_field tests/support/test_oracles.cpp:144-168 (std::mt19937_64 and
  *       libstdc++'s uniform_real_distribution<double> restated bit-exactly)
  *   hash_target (FNV-1a)  hash.hpp:16-44
@@ -53,7 +53,7 @@ int gso_project(const gsim_field_view* field, const gsim_node* nodes, uint64_t n
                 uint64_t* count);
 int gso_rasterize(const gsim_projected_splat* splats, uint64_t n, const gsim_camera* camera,
                   const gsim_raster_options* options, float* rgb, float* depth, float* alpha);
-/* The sorted (tile, depth, splat) pair list of rasterize (raster.cpp:243-271): tile_begin
+/* The sorted (tile, depth, splat) pair list of rasterize (raster.cpp:174-202): tile_begin
  * gets tiles+1 offsets, values the splat index of each pair (NULL to query *count). */
 int gso_rasterize_lists(const gsim_projected_splat* splats, uint64_t n,
                         const gsim_camera* camera, uint32_t* tile_begin, uint32_t* values,

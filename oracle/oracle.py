@@ -157,7 +157,7 @@ class Oracle:
         return t
 
     def rasterize_lists(self, splats, camera):
-        """(tile_begin[tiles+1], splat index per sorted pair) of raster.cpp:243-271."""
+        """(tile_begin[tiles+1], splat index per sorted pair) of raster.cpp:174-202."""
         splats = np.ascontiguousarray(splats, dtype=abi.SPLAT_DTYPE)
         cam = camera.to_c() if isinstance(camera, CameraModel) else camera
         tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)

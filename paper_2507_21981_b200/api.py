@@ -3,7 +3,7 @@
 Names, argument meaning and error behaviour follow the reference gsim library:
     GaussianField, SceneNode, NodeKind    gaussian.hpp:19-71
     RigidTransform                        math.hpp:217-239
-    CameraModel (+ look_at)               camera.hpp:14-33, raster.cpp:94-111
+    CameraModel (+ look_at)               camera.hpp:14-33, raster.cpp:25-42
     RasterOptions, ProjectedSplat         raster.hpp:20-36
     RenderTarget                          image.hpp:38-45
     project / rasterize / render          raster.hpp:54-67
@@ -174,7 +174,7 @@ class CameraModel:
 
     @staticmethod
     def look_at(eye, target, fx, fy, width, height, up=(0.0, 0.0, 1.0)) -> "CameraModel":
-        """CameraModel::look_at (raster.cpp:94-111)."""
+        """CameraModel::look_at (raster.cpp:25-42)."""
         def sub(a, b): return (a[0] - b[0], a[1] - b[1], a[2] - b[2])
         def cross(a, b): return (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
         def normalized(a):

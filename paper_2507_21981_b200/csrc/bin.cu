@@ -1,7 +1,7 @@
 // bin.cu — K3 after the depth sort: deterministic tile binning without a pair sort.
 //
 // The reference emits (tile << 32 | depth, splat) pairs and std::sorts them
-// (raster.cpp:243-271). After the camera-major depth sort of the V visible records
+// (raster.cpp:174-202). After the camera-major depth sort of the V visible records
 // (sort.cu, whose last pass also gathers every record's tile rect into depth order), the pair
 // order we need is simply "by (camera, tile), then by record order". Instead of radix-sorting
 // the P ~ 3.5 V pairs by tile, every pair is placed directly:
@@ -11,13 +11,13 @@
 //             rect rows in a shared row-difference array (red.shared), rows are then
 //             prefix-summed by warp scans; the row goes to a per-camera [unit][tile] matrix;
 //   colscan   per (camera, tile): exclusive scan over the camera's units (lanes = tiles);
-//   tilescan  per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:267-271);
+//   tilescan  per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:198-202);
 //   campre    per batch: pair base of every camera;
 //   scatter   per unit: each warp recounts its slice the same way, the CTA turns the counts
 //             into per-warp first positions of every tile, and each warp walks its records in
 //             order writing each pair's record slot at its position.
 // Pairs are enumerated warp-cooperatively, 32 consecutive pairs per step in emission order
-// (record order, row-major tiles inside a record, raster.cpp:259-263): the owner record of a
+// (record order, row-major tiles inside a record, raster.cpp:190-194): the owner record of a
 // pair position comes from one redux.sync.or of the records' start bits and a popc. Two lanes
 // of a step hitting the same tile is detected with a shared-memory "last writer" probe; only
 // then are the tile's lanes ranked with ballots (match.any issues at ~1 per 40 SM cycles on

@@ -1,7 +1,7 @@
 // common.cuh — device-side data layout and the reference's double-precision math.
 //
 // The geometry half of the preprocess (K2) reproduces /root/reference/proj/core/include/gsim/
-// math.hpp and raster.cpp:135-232 operation by operation in double precision. Files that
+// math.hpp and raster.cpp:66-163 operation by operation in double precision. Files that
 // include the *_exact helpers are compiled with -fmad=false so no multiply-add is contracted,
 // which keeps culls, tile rects and depth keys bit-identical to the reference's x86-64 build.
 #pragma once
@@ -36,7 +36,7 @@ struct DevField {
 };
 
 // One camera of a batch, with everything the reference recomputes per call precomputed on the
-// host in the reference's own operation order (raster.cpp:141-146, camera.hpp:23).
+// host in the reference's own operation order (raster.cpp:72-77, camera.hpp:23).
 struct DevCamera {
     double r[9];            // camera.pose.rotation.to_matrix(), row-major
     double q[4];            // world->camera rotation (w, x, y, z)
@@ -82,7 +82,7 @@ constexpr float kLog2eF = 1.4426950408889634f;
 
 // Builds the raster record from the fp32 projection (u, v, depth, radius, inverse covariance,
 // peak alpha, rgb). The exponent of ex2 is then log2(o) + dx*(A*dx + B*dy) + C*dy*dy, i.e.
-// log2(o * exp(-q/2)) with q = inv_xx dx^2 + 2 inv_xy dx dy + inv_yy dy^2 (raster.cpp:291-293).
+// log2(o * exp(-q/2)) with q = inv_xx dx^2 + 2 inv_xy dx dy + inv_yy dy^2 (raster.cpp:226-229).
 __device__ inline Record make_record(float u, float v, float z, float rad, float ia, float ib,
                                      float ic, float op, float r, float g, float b) {
     Record rec;

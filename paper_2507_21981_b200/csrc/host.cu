@@ -4,7 +4,7 @@
 // Reference behaviour mirrored here:
 //   validate_camera          raster.cpp:16-23   (status 2, same rules)
 //   PoseTable                raster.cpp:47-62   (node painting, later nodes win, range check)
-//   render / rasterize       raster.cpp:234-334 (pipeline K2 -> K3 -> K4)
+//   render / rasterize       raster.cpp:165-265 (pipeline K2 -> K3 -> K4)
 //   transform_primitives     gaussian.cpp:65-79 (K1, range check)
 //   validate_field sh_degree gaussian.cpp:15-17
 //
@@ -254,7 +254,7 @@ void validate_camera(const gsim_camera& c, uint64_t index) {  // raster.cpp:16-2
 DevCamera make_dev_camera(const gsim_camera& c) {
     DevCamera d{};
     const dq q{c.pose.rotation[0], c.pose.rotation[1], c.pose.rotation[2], c.pose.rotation[3]};
-    const dm3 r = qmatrix(q);  // raster.cpp:141
+    const dm3 r = qmatrix(q);  // raster.cpp:72
     for (int k = 0; k < 9; ++k) d.r[k] = r.m[k];
     for (int k = 0; k < 4; ++k) d.q[k] = c.pose.rotation[k];
     for (int k = 0; k < 3; ++k) d.t[k] = c.pose.translation[k];
@@ -270,7 +270,7 @@ DevCamera make_dev_camera(const gsim_camera& c) {
     d.cy = c.cy;
     d.near_p = c.near_plane;
     d.far_p = c.far_plane;
-    const double tan_fovx = c.width / (2.0 * c.fx);  // raster.cpp:143-146
+    const double tan_fovx = c.width / (2.0 * c.fx);  // raster.cpp:74-77
     const double tan_fovy = c.height / (2.0 * c.fy);
     d.limx = 1.3 * tan_fovx;
     d.limy = 1.3 * tan_fovy;

@@ -1,7 +1,7 @@
 // preprocess.cu — K1 (scene-node pose) and K2 (projection + SH) kernels.
 //
 // Compiled with -fmad=false: the double-precision geometry below is the reference's
-// raster.cpp:135-232 / gaussian.cpp:65-79 operation for operation (see common.cuh), so the
+// raster.cpp:66-163 / gaussian.cpp:65-79 operation for operation (see common.cuh), so the
 // visibility set, the 3-sigma tile rects and the float32 depth keys equal the reference's
 // bit for bit. Shading (sh.cpp:10-51) runs in fp32; its outputs only feed the blend.
 //
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) pose_kernel(DevField f, uint64_t begin, u
     }
 }
 
-// ---- K2: project + shade_sh (raster.cpp:135-232, sh.cpp:10-51) ---------------------------
+// ---- K2: project + shade_sh (raster.cpp:66-163, sh.cpp:10-51) ---------------------------
 template <int DEG, bool kFull, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs args) {
     __shared__ uint64_t s_seg_begin[kMaxSmemSegments];
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
         const dq nq = seg_q(seg);
         const dv3 nt = mk3(seg.t[0], seg.t[1], seg.t[2]);
 
-        // Per primitive, camera independent (raster.cpp:156,165-170).
+        // Per primitive, camera independent (raster.cpp:87,165-170).
         const dv3 mean_world = add3(qrotate(nq, mk3(f.mx[i], f.my[i], f.mz[i])), nt);
         const dq rot_world = qmul(nq, dq{f.qw[i], f.qx[i], f.qy[i], f.qz[i]});
         const dm3 r = qmatrix(rot_world);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
         const dm3 cov_world = mmul(mmul(r, d), mtransposed(r));
         const double opacity = f.opacity[i];
 
-        // View direction in the node frame uses the inverse node rotation (raster.cpp:205-208).
+        // View direction in the node frame uses the inverse node rotation (raster.cpp:136-139).
         const float nqw = float(nq.w), nqx = -float(nq.x), nqy = -float(nq.y), nqz = -float(nq.z);
 
         for (uint32_t e = 0; e < seg.entry_count; ++e) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
                 args.keys[slot] = kInvalidKey;
                 continue;
             }
-            // Tile rect (raster.cpp:247-257), floor-inclusive, then clamped.
+            // Tile rect (raster.cpp:178-188), floor-inclusive, then clamped.
             int tx0 = x86_trunc_int(floor((u - radius) / kTileSize));
             int tx1 = x86_trunc_int(floor((u + radius) / kTileSize));
             int ty0 = x86_trunc_int(floor((v - radius) / kTileSize));

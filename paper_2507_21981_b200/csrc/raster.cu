@@ -1,4 +1,4 @@
-// raster.cu — K4: per-tile front-to-back compositing (raster.cpp:273-320).
+// raster.cu — K4: per-tile front-to-back compositing (raster.cpp:204-251).
 //
 // One 128-thread CTA per (camera, 16x16 tile); each thread owns TWO horizontally adjacent
 // pixels, so every per-splat quantity that depends only on the row (dy, the dy terms of the
@@ -20,7 +20,7 @@
 //      test independent of the skip test. A warp stops when all its pixels are parked and the
 //      CTA leaves when __syncthreads_count says every pixel is.
 //
-// Per-pixel contract (raster.cpp:284-318): box test |dx|>r || |dy|>r, q with 2*inv_xy,
+// Per-pixel contract (raster.cpp:215-249): box test |dx|>r || |dy|>r, q with 2*inv_xy,
 // alpha = min(o*exp(-q/2), 0.99), skip alpha < 1/255, accumulate, T *= 1-alpha, stop after
 // accumulating once T < cutoff; rgb clamped to [0,1] at write, depth unnormalised unless
 // asked, accum_alpha = sum of weights. Empty tiles write zeros (image.hpp:44).

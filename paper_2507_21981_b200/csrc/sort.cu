@@ -1,7 +1,7 @@
 // sort.cu — K3a: onesweep LSD radix sort of the (camera | depth) record keys.
 //
 // The reference bins splats into (tile << 32 | float32 depth bits) keys and std::sorts
-// (key, splat index) pairs (raster.cpp:243-271). We produce the same order with an LSD radix
+// (key, splat index) pairs (raster.cpp:174-202). We produce the same order with an LSD radix
 // sort whose depth digits are sorted BEFORE duplication, on the V visible records instead of
 // the P ~ 3.5 V pairs:
 //   pass 1..4  onesweep over the 32-bit depth key of every (camera, primitive) slot; pass 1

@@ -106,7 +106,7 @@ def main() -> None:
     rt = RigidTransform(quat_normalized((0.3, 0.5, -0.2, 0.7)), (0.5, -1.25, 2.0))
     ref.transform_primitives(m, q, 5, 45, rt)
     data["transform"] = dict(seed=12, count=50, begin=5, end=45, means_sha=sha(m), rot_sha=sha(q))
-    # look_at (raster.cpp:94-111) for the BASELINE config-0 camera
+    # look_at (raster.cpp:25-42) for the BASELINE config-0 camera
     cam = ref.look_at((5.0, 0.0, 0.0), (0.0, 0.0, 0.0), 554.2562584220407, 554.2562584220407, 640, 480)
     data["look_at"] = dict(rotation=list(cam.pose.rotation), translation=list(cam.pose.translation))
     OUT.write_text(json.dumps(data, indent=1) + "\n")
