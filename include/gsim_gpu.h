@@ -304,6 +304,69 @@ int gsim_gpu_render_at(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
                        uint64_t n_cameras, const gsim_raster_options* options, float* device_out,
                        gsim_target* outs);
 
+
+/* ---- GS -> TSDF: the renderer's second caller -------------------------
+ * transfer.cpp:27-34    field_bounds: AABB of every primitive's 3-sigma box under the identity
+ *                       pose (pose_primitive, trace.cpp:14-36)
+ * transfer.cpp:81-124   render_depth_ring: n_views azimuths x 3 elevations (-30, 0, +30 deg)
+ *                       looking at the box centre; alpha-normalised depth, 0 where accumulated
+ *                       alpha < 0.5
+ * transfer.cpp:126-141  TsdfVolume::create (validation), transfer.hpp:40-62 layout
+ * transfer.cpp:143-172  tsdf_fuse: projective weight-1 running average per voxel
+ * transfer.cpp:174-201  gaussians_to_mesh up to the fused volume (20 azimuths at 256 x 256,
+ *                       voxel grid over the padded box); marching cubes and decimation
+ *                       (extract_mesh, decimate) stay with the caller.
+ * Volumes live in DEVICE memory: tsdf and weights point at voxel_count doubles each, x fastest
+ * (index = (z * dims[1] + y) * dims[0] + x, transfer.hpp:50-52). */
+typedef struct gsim_tsdf_volume {
+    double origin[3];
+    double voxel_size;
+    int32_t dims[3];
+    int32_t reserved;
+    double truncation;
+    double* tsdf;    /* device, in [-1, 1], 1 where unobserved */
+    double* weights; /* device, >= 0 */
+} gsim_tsdf_volume;
+
+#define GSIM_RING_ELEVATIONS 3
+
+/* field_bounds of a device scene (lo = +inf, hi = -inf for an empty scene). */
+int gsim_gpu_scene_bounds(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, double lo[3],
+                          double hi[3]);
+
+/* The 3 * n_views cameras of render_depth_ring for a field with bounds (lo, hi), elevation-
+ * major as the reference orders its views. Host only (no GPU). Validation as the reference:
+ * n_views < 8, radius not > 0, or a degenerate box. */
+int gsim_gpu_depth_ring_cameras(const double lo[3], const double hi[3], int32_t n_views,
+                                double radius, int32_t resolution, gsim_camera* cameras);
+
+/* render_depth_ring of a device scene: depth gets 3 * n_views images of resolution^2 floats
+ * (device if depth_is_device, else host; synchronous for host); cameras (host, 3 * n_views,
+ * may be NULL) gets the views' cameras. Empty scene -> validation error. */
+int gsim_gpu_render_depth_ring(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                               int32_t n_views, double radius, int32_t resolution,
+                               gsim_camera* cameras, float* depth, int32_t depth_is_device);
+
+/* TsdfVolume::create validation; fills the geometry of *volume (pointers untouched). Host. */
+int gsim_gpu_tsdf_create(const double origin[3], double voxel_size, const int32_t dims[3],
+                         double truncation, gsim_tsdf_volume* volume);
+/* tsdf = 1, weights = 0 over the volume's device buffers. */
+int gsim_gpu_tsdf_reset(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume);
+
+/* tsdf_fuse of n_views depth images in order (view k: cameras[k], cameras[k].width *
+ * cameras[k].height floats, packed one after another; device if depth_is_device). Equivalent to
+ * n_views reference tsdf_fuse calls; the volume is read and written once. */
+int gsim_gpu_tsdf_fuse(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume,
+                       const gsim_camera* cameras, uint64_t n_views, const float* depth,
+                       int32_t depth_is_device);
+
+/* gaussians_to_mesh up to the fused volume. Two calls: with volume->tsdf == NULL only the
+ * geometry (origin, voxel_size, dims, truncation) is written; then, with device buffers of
+ * dims[0] * dims[1] * dims[2] doubles in tsdf and weights, the volume is reset, the depth ring
+ * rendered and fused. */
+int gsim_gpu_gaussians_to_tsdf(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                               double voxel_size, gsim_tsdf_volume* volume);
+
 #ifdef __cplusplus
 }
 #endif

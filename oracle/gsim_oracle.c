@@ -903,3 +903,203 @@ done:
     fclose(f);
     return rc;
 }
+
+
+/* ---- GS -> TSDF (transfer.cpp) ------------------------------------------------------------ */
+
+static const double kPiD = 3.14159265358979323846; /* math.hpp:265-266 */
+static const double kBoundsSigma = 3.0;            /* trace.hpp:25 */
+static const double kDepthValidAlpha = 0.5;        /* transfer.cpp:23 */
+static const double kRingRadiusFactor = 2.5;       /* transfer.cpp:24 */
+static const int kFusionAzimuths = 20;             /* transfer.cpp:25 */
+static const int kFusionResolution = 256;          /* transfer.cpp:26 */
+
+void gso_field_bounds(const gsim_field_view* field, double lo[3], double hi[3]) {
+    /* field_bounds (transfer.cpp:27-34): Aabb::expand (math.hpp:249-250, fmin / fmax) of
+     * pose_primitive(p, identity).bounds (trace.cpp:14-36). The identity pose leaves mean and
+     * rotation bit-exact. */
+    for (int k = 0; k < 3; ++k) { lo[k] = INFINITY; hi[k] = -INFINITY; }
+    for (uint64_t i = 0; i < field->count; ++i) {
+        const double* pm = field->means + i * field->means_stride;
+        const double* ps = field->scales + i * field->scales_stride;
+        const double* pq = field->rotations + i * field->rotations_stride;
+        const quat id = q_make(1.0, 0.0, 0.0, 0.0);
+        const quat rot = q_mul(id, q_make(pq[0], pq[1], pq[2], pq[3]));
+        const mat3 r = q_to_matrix(rot);
+        const mat3 d = m3_diag(ps[0] * ps[0], ps[1] * ps[1], ps[2] * ps[2]);
+        const mat3 rd = m3_mul(&r, &d);
+        const mat3 rt = m3_transposed(&r);
+        const mat3 cov = m3_mul(&rd, &rt);
+        const double half[3] = {kBoundsSigma * sqrt(cov.m[0]), kBoundsSigma * sqrt(cov.m[4]),
+                                kBoundsSigma * sqrt(cov.m[8])};
+        gsim_rigid identity;
+        memset(&identity, 0, sizeof(identity));
+        identity.rotation[0] = 1.0;
+        const v3 mean = rigid_apply(&identity, v3_make(pm[0], pm[1], pm[2]));
+        const double m[3] = {mean.x, mean.y, mean.z};
+        double blo[3], bhi[3];
+        for (int k = 0; k < 3; ++k) { blo[k] = INFINITY; bhi[k] = -INFINITY; }
+        for (int k = 0; k < 3; ++k) { /* bounds.expand(mean - half); bounds.expand(mean + half) */
+            const double a = m[k] - half[k], b = m[k] + half[k];
+            blo[k] = fmin(blo[k], a); bhi[k] = fmax(bhi[k], a);
+            blo[k] = fmin(blo[k], b); bhi[k] = fmax(bhi[k], b);
+        }
+        for (int k = 0; k < 3; ++k) { lo[k] = fmin(lo[k], blo[k]); hi[k] = fmax(hi[k], bhi[k]); }
+    }
+}
+
+int gso_depth_ring_cameras(const double lo_[3], const double hi_[3], int n_views, double radius,
+                           int resolution, gsim_camera* cameras) {
+    /* render_depth_ring camera set-up, transfer.cpp:84-112 */
+    if (n_views < 8) return GSIM_ERR_VALIDATION;
+    if (!(radius > 0.0)) return GSIM_ERR_VALIDATION;
+    const v3 lo = v3_make(lo_[0], lo_[1], lo_[2]), hi = v3_make(hi_[0], hi_[1], hi_[2]);
+    const v3 extent = v3_sub(hi, lo);
+    const double diag = v3_norm(extent);
+    if (!(diag > 0.0)) return GSIM_ERR_VALIDATION;
+    const v3 center = v3_scale(v3_add(lo, hi), 0.5);
+    const double tan_half = 0.65 * diag / radius;
+    const double focal = 0.5 * resolution / tan_half;
+    const double elevations[3] = {-kPiD / 6.0, 0.0, kPiD / 6.0};
+    const double up[3] = {0.0, 0.0, 1.0}; /* camera.hpp:32 default */
+    const double c[3] = {center.x, center.y, center.z};
+    int v = 0;
+    for (int e = 0; e < 3; ++e) {
+        const double elevation = elevations[e];
+        for (int k = 0; k < n_views; ++k, ++v) {
+            const double azimuth = 2.0 * kPiD * k / n_views;
+            const v3 dir = v3_make(cos(elevation) * cos(azimuth), cos(elevation) * sin(azimuth),
+                                   sin(elevation));
+            const v3 eye = v3_add(center, v3_scale(dir, radius));
+            const double ev[3] = {eye.x, eye.y, eye.z};
+            gso_look_at(ev, c, focal, focal, resolution, resolution, up, &cameras[v]);
+            /* std::max(1e-4, radius - diag) */
+            cameras[v].near_plane = (1e-4 < radius - diag) ? radius - diag : 1e-4;
+            cameras[v].far_plane = radius + diag;
+        }
+    }
+    return GSIM_OK;
+}
+
+int gso_render_depth_ring(const gsim_field_view* field, int n_views, double radius,
+                          int resolution, gsim_camera* cameras, float* depth) {
+    /* transfer.cpp:81-124 */
+    if (field->count == 0) return GSIM_ERR_VALIDATION;
+    if (n_views < 8) return GSIM_ERR_VALIDATION;
+    if (!(radius > 0.0)) return GSIM_ERR_VALIDATION;
+    double lo[3], hi[3];
+    gso_field_bounds(field, lo, hi);
+    const int st = gso_depth_ring_cameras(lo, hi, n_views, radius, resolution, cameras);
+    if (st != GSIM_OK) return st;
+    const uint64_t npx = (uint64_t)resolution * resolution;
+    gsim_raster_options opt;
+    memset(&opt, 0, sizeof(opt));
+    opt.normalize_depth = 1;
+    opt.transmittance_cutoff = 1e-4;
+    float* rgb = (float*)malloc(npx * 3 * sizeof(float));
+    float* alpha = (float*)malloc(npx * sizeof(float));
+    for (int v = 0; v < 3 * n_views; ++v) {
+        gsim_target t;
+        memset(&t, 0, sizeof(t));
+        t.rgb = rgb;
+        t.depth = depth + (uint64_t)v * npx;
+        t.accum_alpha = alpha;
+        const int r = gso_render(field, NULL, 0, &cameras[v], 1, &opt, &t);
+        if (r != GSIM_OK) { free(rgb); free(alpha); return r; }
+        for (uint64_t i = 0; i < npx; ++i)
+            if (alpha[i] < kDepthValidAlpha) t.depth[i] = 0.0f;
+    }
+    free(rgb);
+    free(alpha);
+    return GSIM_OK;
+}
+
+int gso_tsdf_create(const double origin[3], double voxel_size, const int32_t dims[3],
+                    double truncation, gsim_tsdf_volume* v) {
+    /* TsdfVolume::create, transfer.cpp:126-141 */
+    if (!(voxel_size > 0.0)) return GSIM_ERR_VALIDATION;
+    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2) return GSIM_ERR_VALIDATION;
+    if (truncation < 2.0 * voxel_size) return GSIM_ERR_VALIDATION;
+    for (int k = 0; k < 3; ++k) { v->origin[k] = origin[k]; v->dims[k] = dims[k]; }
+    v->voxel_size = voxel_size;
+    v->truncation = truncation;
+    const uint64_t n = (uint64_t)dims[0] * dims[1] * dims[2];
+    if (v->tsdf) for (uint64_t i = 0; i < n; ++i) v->tsdf[i] = 1.0;
+    if (v->weights) for (uint64_t i = 0; i < n; ++i) v->weights[i] = 0.0;
+    return GSIM_OK;
+}
+
+static int x86_trunc_int(double x) { /* static_cast<int>(double) as cvttsd2si computes it */
+    if (!(x >= -2147483648.0 && x < 2147483648.0)) return INT32_MIN;
+    return (int)x;
+}
+
+int gso_tsdf_fuse(gsim_tsdf_volume* vol, const gsim_camera* camera, const float* depth,
+                  int width, int height) {
+    /* tsdf_fuse, transfer.cpp:143-172 */
+    if (validate_camera(camera) != GSIM_OK) return GSIM_ERR_VALIDATION;
+    if (width != camera->width || height != camera->height) return GSIM_ERR_VALIDATION;
+    const int dx = vol->dims[0], dy = vol->dims[1], dz = vol->dims[2];
+    uint64_t idx = 0;
+    for (int z = 0; z < dz; ++z) {
+        for (int y = 0; y < dy; ++y) {
+            for (int x = 0; x < dx; ++x, ++idx) {
+                /* voxel_center, transfer.hpp:53-56 */
+                const v3 p = v3_add(v3_make(vol->origin[0], vol->origin[1], vol->origin[2]),
+                                    v3_make((x + 0.5) * vol->voxel_size, (y + 0.5) * vol->voxel_size,
+                                            (z + 0.5) * vol->voxel_size));
+                const v3 cp = rigid_apply(&camera->pose, p);
+                if (cp.z <= 0.0) continue;
+                const int px = x86_trunc_int(floor(camera->fx * cp.x / cp.z + camera->cx));
+                const int py = x86_trunc_int(floor(camera->fy * cp.y / cp.z + camera->cy));
+                if (px < 0 || px >= width || py < 0 || py >= height) continue;
+                const double measured = depth[(uint64_t)py * width + px];
+                if (measured <= 0.0) continue;
+                const double sdf = measured - cp.z;
+                if (sdf <= -vol->truncation) continue;
+                const double clamped = clampd(sdf / vol->truncation, -1.0, 1.0);
+                const double w = vol->weights[idx];
+                vol->tsdf[idx] = (vol->tsdf[idx] * w + clamped) / (w + 1.0);
+                vol->weights[idx] = w + 1.0;
+            }
+        }
+    }
+    return GSIM_OK;
+}
+
+int gso_gaussians_to_tsdf(const gsim_field_view* field, double voxel_size, gsim_tsdf_volume* vol) {
+    /* gaussians_to_mesh up to the fused volume, transfer.cpp:174-198 */
+    if (field->count == 0) return GSIM_ERR_VALIDATION;
+    if (!(voxel_size > 0.0)) return GSIM_ERR_VALIDATION;
+    double blo[3], bhi[3];
+    gso_field_bounds(field, blo, bhi);
+    const v3 bl = v3_make(blo[0], blo[1], blo[2]), bh = v3_make(bhi[0], bhi[1], bhi[2]);
+    const double diag = v3_norm(v3_sub(bh, bl));
+    if (!(diag > 0.0)) return GSIM_ERR_VALIDATION;
+    const double truncation = 3.0 * voxel_size;
+    const double margin = truncation + 2.0 * voxel_size;
+    const v3 lo = v3_sub(bl, v3_make(margin, margin, margin));
+    const v3 hi = v3_add(bh, v3_make(margin, margin, margin));
+    const v3 extent = v3_sub(hi, lo);
+    const double ext[3] = {extent.x, extent.y, extent.z};
+    int32_t dims[3];
+    for (int k = 0; k < 3; ++k) {
+        const int d = x86_trunc_int(ceil(ext[k] / voxel_size)) + 1;
+        dims[k] = d > 2 ? d : 2;
+    }
+    const double origin[3] = {lo.x, lo.y, lo.z};
+    int st = gso_tsdf_create(origin, voxel_size, dims, truncation, vol);
+    if (st != GSIM_OK || !vol->tsdf) return st; /* geometry-only call */
+    const double radius = kRingRadiusFactor * diag;
+    const int nv = 3 * kFusionAzimuths;
+    const uint64_t npx = (uint64_t)kFusionResolution * kFusionResolution;
+    gsim_camera* cams = (gsim_camera*)calloc(nv, sizeof(gsim_camera));
+    float* depth = (float*)malloc(npx * nv * sizeof(float));
+    st = gso_render_depth_ring(field, kFusionAzimuths, radius, kFusionResolution, cams, depth);
+    for (int v = 0; st == GSIM_OK && v < nv; ++v)
+        st = gso_tsdf_fuse(vol, &cams[v], depth + (uint64_t)v * npx, kFusionResolution,
+                           kFusionResolution);
+    free(cams);
+    free(depth);
+    return st;
+}

@@ -18,6 +18,8 @@
  *   pose playback: PoseStream::append / sample  pose_stream.cpp:31-40, 117-136;
  *       slerp  math.hpp:195-214
  *   load_splat_ply   splat_ply.cpp:40-162 (status only: 1 io, 2 format/validation)
+ *   GS -> TSDF: field_bounds, render_depth_ring, TsdfVolume::create, tsdf_fuse,
+ *       gaussians_to_mesh up to the fused volume   transfer.cpp:27-34, 81-198
  *
  * Parity pin: tests/test_oracle_pin.py checks every function against the reference itself
  * (oracle/_ref/libgsim_ref.so, compiled from /root/reference sources by oracle/Makefile) and
@@ -101,6 +103,25 @@ int gso_pose_sample(const double* rec_t, const double* rec_p, const double* rec_
 int gso_load_splat_ply(const char* path, uint64_t capacity, uint64_t* count, int* degree,
                        double* means, double* scales, double* rotations, double* opacities,
                        double* sh);
+
+/* ---- GS -> TSDF (transfer.cpp) -------------------------------------------
+ * field_bounds (transfer.cpp:27-34 over pose_primitive, trace.cpp:14-36); the ring cameras and
+ * render_depth_ring (transfer.cpp:81-124, depth: 3*n_views images of resolution^2 floats);
+ * TsdfVolume::create (transfer.cpp:126-141: tsdf = 1, weights = 0 when the host buffers are
+ * given); tsdf_fuse (transfer.cpp:143-172); gaussians_to_mesh up to the fused volume
+ * (transfer.cpp:174-198; two-call, geometry only when volume->tsdf is NULL). Volumes are HOST
+ * buffers here. */
+void gso_field_bounds(const gsim_field_view* field, double lo[3], double hi[3]);
+int gso_depth_ring_cameras(const double lo[3], const double hi[3], int n_views, double radius,
+                           int resolution, gsim_camera* cameras);
+int gso_render_depth_ring(const gsim_field_view* field, int n_views, double radius,
+                          int resolution, gsim_camera* cameras, float* depth);
+int gso_tsdf_create(const double origin[3], double voxel_size, const int32_t dims[3],
+                    double truncation, gsim_tsdf_volume* volume);
+int gso_tsdf_fuse(gsim_tsdf_volume* volume, const gsim_camera* camera, const float* depth,
+                  int width, int height);
+int gso_gaussians_to_tsdf(const gsim_field_view* field, double voxel_size,
+                          gsim_tsdf_volume* volume);
 
 uint64_t gso_hash_bytes(const void* data, uint64_t size, uint64_t seed);
 uint64_t gso_hash_target(const float* rgb, const float* depth, const float* alpha, int width,

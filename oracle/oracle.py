@@ -17,7 +17,7 @@ import numpy as np
 
 from paper_2507_21981_b200 import abi
 from paper_2507_21981_b200.api import (CameraModel, GaussianField, RasterOptions, RenderTarget,
-                                       SceneNode)
+                                       SceneNode, TsdfVolume)
 
 HERE = Path(__file__).resolve().parent
 ORACLE_LIB = HERE / "liboracle.so"
@@ -48,6 +48,23 @@ def _nodes(nodes):
     for k, n in enumerate(nodes):
         arr[k] = n.to_c() if isinstance(n, SceneNode) else n
     return arr
+
+
+class OracleStatus(ValueError):
+    """Non-zero status (1 io, 2 validation) from the oracle or the reference shim."""
+
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: status {status}")
+        self.status = status
+
+
+def _ok(status: int, what: str) -> None:
+    if status != 0:
+        raise OracleStatus(status, what)
+
+
+def _vec3(v):
+    return (C.c_double * 3)(*[float(x) for x in v])
 
 
 def _target(width, height):
@@ -94,6 +111,15 @@ class Oracle:
         L.gso_load_splat_ply.argtypes = [C.c_char_p, C.c_uint64, _u64p, C.POINTER(C.c_int), _dp, _dp,
                                          _dp, _dp, _dp]
         L.gso_slerp.argtypes = [_dp, _dp, C.c_double, _dp]
+        vol = C.POINTER(abi.gsim_tsdf_volume)
+        L.gso_field_bounds.argtypes = [C.POINTER(abi.gsim_field_view), _dp, _dp]
+        L.gso_depth_ring_cameras.argtypes = [_dp, _dp, C.c_int, C.c_double, C.c_int,
+                                             C.POINTER(abi.gsim_camera)]
+        L.gso_render_depth_ring.argtypes = [C.POINTER(abi.gsim_field_view), C.c_int, C.c_double,
+                                            C.c_int, C.POINTER(abi.gsim_camera), _fp]
+        L.gso_tsdf_create.argtypes = [_dp, C.c_double, C.POINTER(C.c_int32), C.c_double, vol]
+        L.gso_tsdf_fuse.argtypes = [vol, C.POINTER(abi.gsim_camera), _fp, C.c_int, C.c_int]
+        L.gso_gaussians_to_tsdf.argtypes = [C.POINTER(abi.gsim_field_view), C.c_double, vol]
         L.gso_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
                                       C.c_uint64, C.POINTER(abi.gsim_rigid)]
 
@@ -122,6 +148,54 @@ class Oracle:
         sh = (C.c_double * 48)(*sh48); d = (C.c_double * 3)(*view_dir); out = (C.c_double * 3)()
         self.lib.gso_shade_sh(sh, degree, d, out)
         return tuple(out)
+
+    # -- GS -> TSDF (transfer.cpp) -------------------------------------------------------------
+    def field_bounds(self, field: GaussianField):
+        lo = (C.c_double * 3)(); hi = (C.c_double * 3)()
+        v = field.view()
+        self.lib.gso_field_bounds(C.byref(v), lo, hi)
+        return tuple(lo), tuple(hi)
+
+    def depth_ring_cameras(self, lo, hi, n_views: int, radius: float, resolution: int):
+        cams = (abi.gsim_camera * (3 * max(n_views, 1)))()
+        _ok(self.lib.gso_depth_ring_cameras(_vec3(lo), _vec3(hi), n_views, radius, resolution, cams),
+            "depth_ring_cameras")
+        return cams
+
+    def render_depth_ring(self, field: GaussianField, n_views: int, radius: float, resolution: int):
+        """-> (3 * n_views cameras, depth float32 (3 * n_views, resolution, resolution))."""
+        n = 3 * max(n_views, 1)
+        cams = (abi.gsim_camera * n)()
+        depth = np.zeros((n, resolution, resolution), dtype=np.float32)
+        v = field.view()
+        _ok(self.lib.gso_render_depth_ring(C.byref(v), n_views, radius, resolution, cams,
+                                           depth.ctypes.data_as(_fp)), "render_depth_ring")
+        return cams, depth
+
+    def tsdf_create(self, origin, voxel_size, dims, truncation) -> TsdfVolume:
+        vol = TsdfVolume(origin, voxel_size, dims, truncation)
+        if min(vol.dims) >= 2:
+            vol.allocate()
+        c = vol.to_c()
+        _ok(self.lib.gso_tsdf_create(_vec3(origin), voxel_size, (C.c_int32 * 3)(*vol.dims),
+                                     truncation, C.byref(c)), "tsdf_create")
+        return vol
+
+    def tsdf_fuse(self, vol: TsdfVolume, camera, depth: np.ndarray) -> None:
+        depth = np.ascontiguousarray(depth, dtype=np.float32)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        c = vol.to_c()
+        _ok(self.lib.gso_tsdf_fuse(C.byref(c), C.byref(cam), depth.ctypes.data_as(_fp),
+                                   depth.shape[1], depth.shape[0]), "tsdf_fuse")
+
+    def gaussians_to_tsdf(self, field: GaussianField, voxel_size: float) -> TsdfVolume:
+        v = field.view()
+        c = abi.gsim_tsdf_volume()
+        _ok(self.lib.gso_gaussians_to_tsdf(C.byref(v), voxel_size, C.byref(c)), "gaussians_to_tsdf")
+        vol = TsdfVolume.from_c(c).allocate()
+        c = vol.to_c()
+        _ok(self.lib.gso_gaussians_to_tsdf(C.byref(v), voxel_size, C.byref(c)), "gaussians_to_tsdf")
+        return vol
 
     # -- the path ----------------------------------------------------------------------------
     def project(self, field: GaussianField, nodes, camera) -> np.ndarray:
@@ -313,6 +387,55 @@ class Ref:
         L.ref_slerp.argtypes = [_dp, _dp, C.c_double, _dp]
         L.ref_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
                                       C.c_uint64, C.POINTER(abi.gsim_rigid)]
+        vol = C.POINTER(abi.gsim_tsdf_volume)
+        L.ref_render_depth_ring.argtypes = [_vp, C.c_int, C.c_double, C.c_int,
+                                            C.POINTER(abi.gsim_camera), _fp]
+        L.ref_tsdf_create.argtypes = [_dp, C.c_double, C.POINTER(C.c_int32), C.c_double, vol]
+        L.ref_tsdf_fuse.argtypes = [vol, C.POINTER(abi.gsim_camera), _fp, C.c_int, C.c_int]
+        L.ref_gaussians_to_tsdf.argtypes = [_vp, C.c_double, vol]
+
+    # -- GS -> TSDF (transfer.cpp) -------------------------------------------------------------
+    def _with_field(self, field: GaussianField, fn):
+        v = field.view()
+        h = self.lib.ref_field_create(C.byref(v))
+        try:
+            return fn(h)
+        finally:
+            self.lib.ref_field_destroy(h)
+
+    def render_depth_ring(self, field: GaussianField, n_views: int, radius: float, resolution: int):
+        n = 3 * max(n_views, 1)
+        cams = (abi.gsim_camera * n)()
+        depth = np.zeros((n, resolution, resolution), dtype=np.float32)
+        _ok(self._with_field(field, lambda h: self.lib.ref_render_depth_ring(
+            h, n_views, radius, resolution, cams, depth.ctypes.data_as(_fp))), "ref render_depth_ring")
+        return cams, depth
+
+    def tsdf_create(self, origin, voxel_size, dims, truncation) -> TsdfVolume:
+        vol = TsdfVolume(origin, voxel_size, dims, truncation)
+        if min(vol.dims) >= 2:
+            vol.allocate()
+        c = vol.to_c()
+        _ok(self.lib.ref_tsdf_create(_vec3(origin), voxel_size, (C.c_int32 * 3)(*vol.dims),
+                                     truncation, C.byref(c)), "ref tsdf_create")
+        return vol
+
+    def tsdf_fuse(self, vol: TsdfVolume, camera, depth: np.ndarray) -> None:
+        depth = np.ascontiguousarray(depth, dtype=np.float32)
+        cam = camera.to_c() if isinstance(camera, CameraModel) else camera
+        c = vol.to_c()
+        _ok(self.lib.ref_tsdf_fuse(C.byref(c), C.byref(cam), depth.ctypes.data_as(_fp),
+                                   depth.shape[1], depth.shape[0]), "ref tsdf_fuse")
+
+    def gaussians_to_tsdf(self, field: GaussianField, voxel_size: float) -> TsdfVolume:
+        def run(h):
+            c = abi.gsim_tsdf_volume()
+            _ok(self.lib.ref_gaussians_to_tsdf(h, voxel_size, C.byref(c)), "ref gaussians_to_tsdf")
+            vol = TsdfVolume.from_c(c).allocate()
+            c = vol.to_c()
+            _ok(self.lib.ref_gaussians_to_tsdf(h, voxel_size, C.byref(c)), "ref gaussians_to_tsdf")
+            return vol
+        return self._with_field(field, run)
 
     def set_threads(self, n: int) -> None:
         self.lib.ref_set_threads(n)

@@ -16,9 +16,12 @@
 //     to libpng instead of compressing them)
 //   gsim::PoseStream::append / sample, gsim::slerp          pose_stream.hpp:28-45, math.hpp:196
 //   gsim::load_splat_ply / save_splat_ply                   splat_ply.hpp:20-24
+//   gsim::render_depth_ring / TsdfVolume::create / tsdf_fuse / gaussians_to_mesh
+//                                                           transfer.hpp:33-90
 // Used by tests/test_oracle_pin.py (pin the C restatement), tests/golden/make_golden.py and
 // bench.py --impl reference (the reference's CPU renderer timed on the host cores).
 #include <cstring>
+#include <limits>
 #include <exception>
 #include <string>
 #include <vector>
@@ -28,6 +31,7 @@
 #include "gsim/image_io.hpp"
 #include "gsim/pose_stream.hpp"
 #include "gsim/splat_ply.hpp"
+#include "gsim/transfer.hpp"
 #include "png.h"
 #include "gsim/parallel.hpp"
 #include "gsim/raster.hpp"
@@ -117,6 +121,30 @@ void from_splat(const ProjectedSplat& s, gsim_projected_splat* o) {
     o->rgb[2] = s.rgb.z;
     o->radius = s.radius;
     o->prim_index = s.prim_index;
+}
+
+void from_camera(const CameraModel& c, gsim_camera* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->fx = c.fx;
+    out->fy = c.fy;
+    out->cx = c.cx;
+    out->cy = c.cy;
+    out->width = c.width;
+    out->height = c.height;
+    from_rigid(c.pose, &out->pose);
+    out->near_plane = c.near;
+    out->far_plane = c.far;
+}
+
+void copy_volume_out(const TsdfVolume& v, gsim_tsdf_volume* out) {
+    for (int k = 0; k < 3; ++k) out->dims[k] = v.dims[k];
+    out->origin[0] = v.origin.x;
+    out->origin[1] = v.origin.y;
+    out->origin[2] = v.origin.z;
+    out->voxel_size = v.voxel_size;
+    out->truncation = v.truncation;
+    if (out->tsdf) std::memcpy(out->tsdf, v.tsdf.data(), v.tsdf.size() * sizeof(double));
+    if (out->weights) std::memcpy(out->weights, v.weights.data(), v.weights.size() * sizeof(double));
 }
 
 ProjectedSplat to_splat(const gsim_projected_splat& o) {
@@ -393,6 +421,56 @@ int ref_load_splat_ply(const char* path, std::uint64_t capacity, std::uint64_t* 
 
 int ref_save_splat_ply(const char* path, const gsim_field_view* view) {
     return guarded([&] { save_splat_ply(to_field(view), path); });
+}
+
+// ---- GS -> TSDF (transfer.cpp) ---------------------------------------------------------------
+int ref_render_depth_ring(void* field, int n_views, double radius, int resolution,
+                          gsim_camera* cameras, float* depth) {
+    return guarded([&] {
+        const auto views = render_depth_ring(*static_cast<GaussianField*>(field), n_views, radius,
+                                             resolution);
+        const std::size_t npx = static_cast<std::size_t>(resolution) * resolution;
+        for (std::size_t v = 0; v < views.size(); ++v) {
+            from_camera(views[v].camera, &cameras[v]);
+            std::memcpy(depth + v * npx, views[v].depth.data.data(), npx * sizeof(float));
+        }
+    });
+}
+
+// TsdfVolume::create with the given geometry, the host tsdf / weights copied in, then one
+// tsdf_fuse; the updated grids are copied back.
+int ref_tsdf_fuse(gsim_tsdf_volume* vol, const gsim_camera* camera, const float* depth, int width,
+                  int height) {
+    return guarded([&] {
+        TsdfVolume v = TsdfVolume::create(to_vec(vol->origin), vol->voxel_size,
+                                          {vol->dims[0], vol->dims[1], vol->dims[2]},
+                                          vol->truncation);
+        std::memcpy(v.tsdf.data(), vol->tsdf, v.tsdf.size() * sizeof(double));
+        std::memcpy(v.weights.data(), vol->weights, v.weights.size() * sizeof(double));
+        Image1 img(width, height);
+        std::memcpy(img.data.data(), depth, img.data.size() * sizeof(float));
+        tsdf_fuse(v, to_camera(*camera), img);
+        copy_volume_out(v, vol);
+    });
+}
+
+int ref_tsdf_create(const double* origin, double voxel_size, const int32_t* dims,
+                    double truncation, gsim_tsdf_volume* vol) {
+    return guarded([&] {
+        copy_volume_out(TsdfVolume::create(to_vec(origin), voxel_size, {dims[0], dims[1], dims[2]},
+                                           truncation),
+                        vol);
+    });
+}
+
+// gaussians_to_mesh(field, voxel_size, no decimation, &volume): the fused volume it builds.
+int ref_gaussians_to_tsdf(void* field, double voxel_size, gsim_tsdf_volume* vol) {
+    return guarded([&] {
+        TsdfVolume v;
+        gaussians_to_mesh(*static_cast<GaussianField*>(field), voxel_size,
+                          std::numeric_limits<std::size_t>::max(), &v);
+        copy_volume_out(v, vol);
+    });
 }
 
 }  // extern "C"

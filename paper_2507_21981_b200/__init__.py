@@ -17,21 +17,25 @@ from .api import (  # noqa: F401
     RigidTransform,
     Scene,
     SceneNode,
+    TsdfVolume,
     ValidationError,
     default_context,
+    depth_ring_cameras,
     io_error,
     project,
     quat_from_axis_angle,
     rasterize,
     render,
     transform_primitives,
+    tsdf_create,
     validation_error,
 )
 from .abi import SPLAT_DTYPE, load_library  # noqa: F401
 
 __all__ = [
     "CameraModel", "Context", "EncodeOptions", "GaussianField", "IoError", "NodeKind", "PoseTracks", "RasterOptions",
-    "RenderTarget", "RigidTransform", "Scene", "SceneNode", "ValidationError", "SPLAT_DTYPE",
+    "RenderTarget", "RigidTransform", "Scene", "SceneNode", "TsdfVolume", "ValidationError",
+    "SPLAT_DTYPE", "depth_ring_cameras", "tsdf_create",
     "default_context", "io_error", "load_library", "project", "quat_from_axis_angle",
     "rasterize", "render", "transform_primitives", "validation_error",
 ]

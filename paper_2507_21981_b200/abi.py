@@ -84,6 +84,12 @@ class gsim_render_stats(C.Structure):
                 ("groups", C.c_uint32), ("reserved", C.c_float)]
 
 
+class gsim_tsdf_volume(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("voxel_size", C.c_double), ("dims", C.c_int32 * 3),
+                ("reserved", C.c_int32), ("truncation", C.c_double),
+                ("tsdf", C.POINTER(C.c_double)), ("weights", C.POINTER(C.c_double))]
+
+
 # numpy view of gsim_projected_splat (ProjectedSplat, raster.hpp:20-29), 120 bytes
 SPLAT_DTYPE = np.dtype([
     ("pixel_center", "<f8", (2,)), ("cov_xx", "<f8"), ("cov_xy", "<f8"), ("cov_yy", "<f8"),
@@ -146,6 +152,18 @@ SIGNATURES = [
                                           C.POINTER(gsim_camera), C.c_uint64,
                                           C.POINTER(gsim_raster_options),
                                           C.POINTER(gsim_encode_options), _P, C.c_int32]),
+    ("gsim_gpu_scene_bounds", C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("gsim_gpu_depth_ring_cameras", C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                              C.c_int32, C.c_double, C.c_int32,
+                                              C.POINTER(gsim_camera)]),
+    ("gsim_gpu_render_depth_ring", C.c_int, [_P, _P, C.c_int32, C.c_double, C.c_int32,
+                                             C.POINTER(gsim_camera), _P, C.c_int32]),
+    ("gsim_gpu_tsdf_create", C.c_int, [C.POINTER(C.c_double), C.c_double, C.POINTER(C.c_int32),
+                                       C.c_double, C.POINTER(gsim_tsdf_volume)]),
+    ("gsim_gpu_tsdf_reset", C.c_int, [_P, C.POINTER(gsim_tsdf_volume)]),
+    ("gsim_gpu_tsdf_fuse", C.c_int, [_P, C.POINTER(gsim_tsdf_volume), C.POINTER(gsim_camera),
+                                     C.c_uint64, _P, C.c_int32]),
+    ("gsim_gpu_gaussians_to_tsdf", C.c_int, [_P, _P, C.c_double, C.POINTER(gsim_tsdf_volume)]),
 ]
 
 _lib = None

@@ -319,6 +319,77 @@ class GaussianField:
         return v
 
 
+class TsdfVolume:
+    """TsdfVolume (transfer.hpp:40-62): a voxel grid of truncated signed distances fused from
+    depth maps. tsdf / weights are (dims[2], dims[1], dims[0]) float64 arrays, x fastest
+    (index(), transfer.hpp:50-52); None until allocated."""
+
+    def __init__(self, origin, voxel_size: float, dims, truncation: float, tsdf=None, weights=None):
+        self.origin = tuple(float(v) for v in origin)
+        self.voxel_size = float(voxel_size)
+        self.dims = tuple(int(d) for d in dims)
+        self.truncation = float(truncation)
+        self.tsdf = tsdf
+        self.weights = weights
+
+    @property
+    def voxel_count(self) -> int:
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    @property
+    def shape(self) -> tuple:
+        return (self.dims[2], self.dims[1], self.dims[0])
+
+    def allocate(self) -> "TsdfVolume":
+        """Host grids in the TsdfVolume::create state (tsdf 1, weights 0)."""
+        self.tsdf = np.ones(self.shape)
+        self.weights = np.zeros(self.shape)
+        return self
+
+    def device_grids(self) -> "TsdfVolume":
+        """Device grids (torch cuda float64 tensors) in the TsdfVolume::create state; the
+        library's tsdf entry points take these."""
+        import torch
+        self.tsdf = torch.ones(self.shape, dtype=torch.float64, device="cuda")
+        self.weights = torch.zeros(self.shape, dtype=torch.float64, device="cuda")
+        return self
+
+    def to_numpy(self) -> "TsdfVolume":
+        """Copy of the volume with host grids."""
+        conv = lambda a: a.detach().cpu().numpy() if hasattr(a, "detach") else a
+        return TsdfVolume(self.origin, self.voxel_size, self.dims, self.truncation,
+                          conv(self.tsdf), conv(self.weights))
+
+    def to_c(self, tsdf_ptr: int | None = None, weights_ptr: int | None = None) -> abi.gsim_tsdf_volume:
+        """C view; the grid pointers default to the volume's arrays (host numpy or device torch
+        tensors), or NULL when unallocated."""
+        v = abi.gsim_tsdf_volume()
+        for k in range(3):
+            v.origin[k] = self.origin[k]
+            v.dims[k] = self.dims[k]
+        v.voxel_size = self.voxel_size
+        v.truncation = self.truncation
+        dp = C.POINTER(C.c_double)
+
+        def ptr(a):
+            if a is None:
+                return None
+            if hasattr(a, "data_ptr"):  # torch tensor (device grids)
+                assert a.is_contiguous() and a.element_size() == 8 and a.numel() == self.voxel_count
+                return a.data_ptr()
+            assert a.dtype == np.float64 and a.flags.c_contiguous and a.size == self.voxel_count
+            return a.ctypes.data
+        tsdf_ptr = ptr(self.tsdf) if tsdf_ptr is None else tsdf_ptr
+        weights_ptr = ptr(self.weights) if weights_ptr is None else weights_ptr
+        v.tsdf = C.cast(C.c_void_p(tsdf_ptr), dp) if tsdf_ptr else dp()
+        v.weights = C.cast(C.c_void_p(weights_ptr), dp) if weights_ptr else dp()
+        return v
+
+    @staticmethod
+    def from_c(v: abi.gsim_tsdf_volume) -> "TsdfVolume":
+        return TsdfVolume(tuple(v.origin), v.voxel_size, tuple(v.dims), v.truncation)
+
+
 def _nodes_array(nodes: Sequence[SceneNode]):
     arr = (abi.gsim_node * max(len(nodes), 1))()
     for k, n in enumerate(nodes):
@@ -613,6 +684,59 @@ class Context:
                                                 out.ctypes.data_as(C.c_void_p), 0), self.ptr)
         return out[:n]
 
+    # -- GS -> TSDF (transfer.cpp) -----------------------------------------
+    def scene_bounds(self, scene: Scene):
+        """field_bounds (transfer.cpp:27-34) of a device scene -> (lo, hi)."""
+        lo = (C.c_double * 3)(); hi = (C.c_double * 3)()
+        _check(self.lib.gsim_gpu_scene_bounds(self.ptr, scene.handle, lo, hi), self.ptr)
+        return tuple(lo), tuple(hi)
+
+    def render_depth_ring(self, scene: Scene, n_views: int, radius: float, resolution: int,
+                          device_out: int | None = None):
+        """render_depth_ring (transfer.cpp:81-124) -> (3 * n_views cameras, depth): a host float32
+        (3 * n_views, resolution, resolution) array, or device_out filled asynchronously-safe
+        (the call returns after the copy)."""
+        n = 3 * max(int(n_views), 1)
+        cams = (abi.gsim_camera * n)()
+        if device_out:
+            _check(self.lib.gsim_gpu_render_depth_ring(self.ptr, scene.handle, n_views, radius,
+                                                       resolution, cams, C.c_void_p(device_out), 1),
+                   self.ptr)
+            return cams, device_out
+        depth = np.zeros((n, resolution, resolution), dtype=np.float32)
+        _check(self.lib.gsim_gpu_render_depth_ring(self.ptr, scene.handle, n_views, radius,
+                                                   resolution, cams,
+                                                   depth.ctypes.data_as(C.c_void_p), 0), self.ptr)
+        return cams, depth
+
+    def tsdf_reset(self, volume: "TsdfVolume") -> None:
+        c = volume.to_c()
+        _check(self.lib.gsim_gpu_tsdf_reset(self.ptr, C.byref(c)), self.ptr)
+
+    def tsdf_fuse(self, volume: "TsdfVolume", cameras, depth) -> None:
+        """tsdf_fuse (transfer.cpp:143-172) of the views in order; volume grids on the device
+        (TsdfVolume.device_grids). depth: host float32 images (n, H, W) or a device pointer."""
+        ca = _cams_array(cameras)
+        c = volume.to_c()
+        if isinstance(depth, int):
+            _check(self.lib.gsim_gpu_tsdf_fuse(self.ptr, C.byref(c), ca, len(cameras),
+                                               C.c_void_p(depth), 1), self.ptr)
+            return
+        d = np.ascontiguousarray(depth, dtype=np.float32)
+        _check(self.lib.gsim_gpu_tsdf_fuse(self.ptr, C.byref(c), ca, len(cameras),
+                                           d.ctypes.data_as(C.c_void_p), 0), self.ptr)
+
+    def gaussians_to_tsdf(self, scene: Scene, voxel_size: float) -> "TsdfVolume":
+        """gaussians_to_mesh up to the fused volume (transfer.cpp:174-198); device grids."""
+        c = abi.gsim_tsdf_volume()
+        _check(self.lib.gsim_gpu_gaussians_to_tsdf(self.ptr, scene.handle, voxel_size, C.byref(c)),
+               self.ptr)
+        vol = TsdfVolume.from_c(c).device_grids()
+        c = vol.to_c()
+        _check(self.lib.gsim_gpu_gaussians_to_tsdf(self.ptr, scene.handle, voxel_size, C.byref(c)),
+               self.ptr)
+        return vol
+
     def tile_lists(self, camera: int):
         """Sorted per-tile lists of `camera` from the last render (tile offsets, indices)."""
         count = C.c_uint64(0)
@@ -679,3 +803,25 @@ def transform_primitives(field: GaussianField, rng: tuple, transform: RigidTrans
     field.touch()
     with _default_lock:  # the device copy already holds the transformed field
         _default["key"] = (id(field), field.size(), field.generation, field.means.ctypes.data)
+
+
+def depth_ring_cameras(lo, hi, n_views: int, radius: float, resolution: int):
+    """The 3 * n_views cameras of render_depth_ring (transfer.cpp:84-112); host only."""
+    lib = abi.load_library()
+    cams = (abi.gsim_camera * (3 * max(int(n_views), 1)))()
+    st = lib.gsim_gpu_depth_ring_cameras((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), n_views,
+                                         radius, resolution, cams)
+    if st != 0:
+        raise ValidationError("depth_ring_cameras: invalid ring (n_views < 8, radius, or box)")
+    return cams
+
+
+def tsdf_create(origin, voxel_size: float, dims, truncation: float) -> "TsdfVolume":
+    """TsdfVolume::create (transfer.cpp:126-141) validation; geometry only (no grids)."""
+    lib = abi.load_library()
+    c = abi.gsim_tsdf_volume()
+    st = lib.gsim_gpu_tsdf_create((C.c_double * 3)(*origin), voxel_size,
+                                  (C.c_int32 * 3)(*[int(d) for d in dims]), truncation, C.byref(c))
+    if st != 0:
+        raise ValidationError("tsdf: invalid volume (voxel_size, dims >= 2, truncation >= 2 voxels)")
+    return TsdfVolume.from_c(c)

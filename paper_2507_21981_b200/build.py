@@ -30,6 +30,7 @@ SOURCES = {
     "encode.cu": [],
     "tracks.cu": ["-fmad=false"],
     "ply.cu": ["-fmad=false"],
+    "transfer.cu": ["-fmad=false"],
     "host.cu": [],
 }
 DEPS = ["common.cuh", "kernels.hpp", "encode.cuh"]

@@ -189,6 +189,11 @@ struct gsim_gpu_context {
     DevBuf<gsim_projected_splat> full;
     DevBuf<uint8_t> full_vis;
     DevBuf<gsim_projected_splat> splats_in;
+    // GS -> TSDF scratch (transfer.cu)
+    DevBuf<double> bounds_buf;       // per-block boxes + the reduced box
+    DevBuf<DevFuseView> fuse_views;
+    DevBuf<float> depth_in;          // host depth maps staged for tsdf_fuse
+    float frame_valid_alpha = 0.0f;  // render_depth_ring's depth mask (raster epilogue)
 
     uint32_t epoch = 0;
     uint64_t launches_total = 0;
@@ -570,6 +575,7 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.rect_w = ctx->raster_rect_w;
     rr.batch = ctx->raster_batch;
     rr.exact_cull = ctx->raster_exact_cull;
+    rr.valid_alpha = ctx->frame_valid_alpha;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
@@ -1149,6 +1155,85 @@ struct Guard {
     }
 };
 
+// ---- GS -> TSDF helpers (transfer.cpp) ------------------------------------------------------
+
+void scene_bounds(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, double lo[3], double hi[3]) {
+    const int max_blocks = ctx->num_sms * 4;
+    ctx->bounds_buf.reserve(size_t(6) * (max_blocks + 1));
+    double* out = ctx->bounds_buf.ptr + 6 * size_t(max_blocks);
+    launch_bounds(scene->f, ctx->bounds_buf.ptr, max_blocks, out, ctx->stream);
+    check_launch();
+    double box[6];
+    GSIM_CK(cudaMemcpyAsync(box, out, sizeof(box), cudaMemcpyDeviceToHost, ctx->stream));
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = box[k];
+        hi[k] = box[3 + k];
+    }
+}
+
+struct ValidAlphaScope {  // the depth mask applies to the renders of one call only
+    gsim_gpu_context* c;
+    ValidAlphaScope(gsim_gpu_context* ctx, float a) : c(ctx) { c->frame_valid_alpha = a; }
+    ~ValidAlphaScope() { c->frame_valid_alpha = 0.0f; }
+};
+
+// render_depth_ring (transfer.cpp:81-124) into ctx->out; returns the per-camera offsets.
+std::vector<uint64_t> depth_ring_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                                        int n_views, double radius, int resolution,
+                                        std::vector<gsim_camera>& cams) {
+    if (scene->f.n == 0) throw ValidationError{"render_depth_ring: empty field"};
+    if (n_views < 8) throw ValidationError{"render_depth_ring: n_views must be >= 8"};
+    if (!(radius > 0.0)) throw ValidationError{"render_depth_ring: radius must be positive"};
+    double lo[3], hi[3];
+    scene_bounds(ctx, scene, lo, hi);
+    cams.assign(size_t(3) * n_views, gsim_camera{});
+    if (const char* msg = depth_ring_cameras(lo, hi, n_views, radius, resolution, cams.data()))
+        throw ValidationError{msg};
+    gsim_raster_options opt{1, 0, 1e-4};  // RasterOptions{normalize_depth = true}
+    ValidAlphaScope mask(ctx, 0.5f);      // kDepthValidAlpha, transfer.cpp:23
+    return render_cameras(ctx, scene, nullptr, 0, cams.data(), cams.size(), &opt, nullptr, true);
+}
+
+void check_volume(const gsim_tsdf_volume* v, bool buffers) {
+    if (!v) throw ValidationError{"tsdf: null volume"};
+    if (!(v->voxel_size > 0.0)) throw ValidationError{"tsdf: voxel_size must be positive"};
+    if (v->dims[0] < 2 || v->dims[1] < 2 || v->dims[2] < 2)
+        throw ValidationError{"tsdf: dims must be at least 2 per axis"};
+    if (v->truncation < 2.0 * v->voxel_size)
+        throw ValidationError{"tsdf: truncation must be >= 2 * voxel_size"};
+    if (buffers && (!v->tsdf || !v->weights)) throw ValidationError{"tsdf: null device grids"};
+}
+
+TsdfArgs tsdf_args(const gsim_tsdf_volume* v) {
+    TsdfArgs a{};
+    for (int k = 0; k < 3; ++k) {
+        a.origin[k] = v->origin[k];
+        a.dims[k] = v->dims[k];
+    }
+    a.voxel_size = v->voxel_size;
+    a.truncation = v->truncation;
+    a.tsdf = v->tsdf;
+    a.weights = v->weights;
+    return a;
+}
+
+void fuse_views(gsim_gpu_context* ctx, const gsim_tsdf_volume* vol,
+                const std::vector<DevFuseView>& views, const float* depth_dev) {
+    if (views.empty()) return;
+    ctx->fuse_views.reserve(views.size());
+    GSIM_CK(cudaMemcpyAsync(ctx->fuse_views.ptr, views.data(), views.size() * sizeof(DevFuseView),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    TsdfArgs a = tsdf_args(vol);
+    a.n_views = uint32_t(views.size());
+    a.views = ctx->fuse_views.ptr;
+    a.depth = depth_dev;
+    launch_tsdf_fuse(a, ctx->num_sms, ctx->stream);
+    check_launch();
+    // the view table is staged from host memory that dies with this call
+    GSIM_CK(cudaStreamSynchronize(ctx->stream));
+}
+
 }  // namespace
 
 extern "C" {
@@ -1228,6 +1313,9 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->full.release();
     ctx->full_vis.release();
     ctx->splats_in.release();
+    ctx->bounds_buf.release();
+    ctx->fuse_views.release();
+    ctx->depth_in.release();
     ctx->readback.release();
     ctx->srgb_thr.release();
     ctx->enc_buf.release();
@@ -1828,6 +1916,141 @@ int gsim_gpu_tile_lists(gsim_gpu_context* ctx, uint32_t camera, uint32_t* tile_b
             const uint64_t sb = p.slot_base[camera];
             for (uint64_t k = 0; k < total && k < capacity; ++k) values[k] = uint32_t(v[k] - sb);
         }
+    });
+}
+
+// ---- GS -> TSDF (transfer.cpp) ------------------------------------------
+
+int gsim_gpu_scene_bounds(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, double lo[3],
+                          double hi[3]) {
+    return Guard(ctx).run([&] {
+        if (!scene || !lo || !hi) throw ValidationError{"scene_bounds: null argument"};
+        scene_bounds(ctx, scene, lo, hi);
+    });
+}
+
+int gsim_gpu_depth_ring_cameras(const double lo[3], const double hi[3], int32_t n_views,
+                                double radius, int32_t resolution, gsim_camera* cameras) {
+    if (!lo || !hi || !cameras) return GSIM_ERR_VALIDATION;
+    return gsim_gpu::depth_ring_cameras(lo, hi, n_views, radius, resolution, cameras)
+               ? GSIM_ERR_VALIDATION
+               : GSIM_OK;
+}
+
+int gsim_gpu_render_depth_ring(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                               int32_t n_views, double radius, int32_t resolution,
+                               gsim_camera* cameras, float* depth, int32_t depth_is_device) {
+    return Guard(ctx).run([&] {
+        if (!scene || !depth) throw ValidationError{"render_depth_ring: null argument"};
+        std::vector<gsim_camera> cams;
+        const std::vector<uint64_t> off =
+            depth_ring_render(ctx, scene, n_views, radius, resolution, cams);
+        if (cameras) std::copy(cams.begin(), cams.end(), cameras);
+        // depth plane of every camera block [rgb 3 npx | depth npx | alpha npx]
+        const size_t npx = size_t(resolution) * resolution;
+        GSIM_CK(cudaMemcpy2DAsync(depth, npx * sizeof(float), ctx->out.ptr + 3 * npx,
+                                  5 * npx * sizeof(float), npx * sizeof(float), cams.size(),
+                                  depth_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        (void)off;
+    });
+}
+
+int gsim_gpu_tsdf_create(const double origin[3], double voxel_size, const int32_t dims[3],
+                         double truncation, gsim_tsdf_volume* volume) {
+    // TsdfVolume::create, transfer.cpp:126-141 (geometry only; the grids are the caller's)
+    if (!origin || !dims || !volume) return GSIM_ERR_VALIDATION;
+    if (!(voxel_size > 0.0)) return GSIM_ERR_VALIDATION;
+    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2) return GSIM_ERR_VALIDATION;
+    if (truncation < 2.0 * voxel_size) return GSIM_ERR_VALIDATION;
+    for (int k = 0; k < 3; ++k) {
+        volume->origin[k] = origin[k];
+        volume->dims[k] = dims[k];
+    }
+    volume->voxel_size = voxel_size;
+    volume->truncation = truncation;
+    return GSIM_OK;
+}
+
+int gsim_gpu_tsdf_reset(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume) {
+    return Guard(ctx).run([&] {
+        check_volume(volume, true);
+        const uint64_t n = uint64_t(volume->dims[0]) * volume->dims[1] * volume->dims[2];
+        launch_tsdf_reset(volume->tsdf, volume->weights, n, ctx->num_sms, ctx->stream);
+        check_launch();
+    });
+}
+
+int gsim_gpu_tsdf_fuse(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume,
+                       const gsim_camera* cameras, uint64_t n_views, const float* depth,
+                       int32_t depth_is_device) {
+    return Guard(ctx).run([&] {
+        check_volume(volume, true);
+        if (n_views && (!cameras || !depth)) throw ValidationError{"tsdf_fuse: null argument"};
+        std::vector<DevFuseView> views(n_views);
+        uint64_t total = 0;
+        for (uint64_t k = 0; k < n_views; ++k) {
+            validate_camera(cameras[k], k);  // tsdf_fuse validates its camera (transfer.cpp:144)
+            views[k] = fuse_view(cameras[k], total);
+            total += uint64_t(cameras[k].width) * cameras[k].height;
+        }
+        const float* src = depth;
+        if (!depth_is_device && total) {
+            ctx->depth_in.reserve(total);
+            GSIM_CK(cudaMemcpyAsync(ctx->depth_in.ptr, depth, total * sizeof(float),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+            src = ctx->depth_in.ptr;
+        }
+        fuse_views(ctx, volume, views, src);
+    });
+}
+
+int gsim_gpu_gaussians_to_tsdf(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
+                               double voxel_size, gsim_tsdf_volume* volume) {
+    // gaussians_to_mesh up to the fused volume, transfer.cpp:174-198
+    return Guard(ctx).run([&] {
+        if (!scene || !volume) throw ValidationError{"gaussians_to_tsdf: null argument"};
+        if (scene->f.n == 0) throw ValidationError{"gaussians_to_mesh: empty field"};
+        if (!(voxel_size > 0.0)) throw ValidationError{"gaussians_to_mesh: voxel_size must be positive"};
+        double blo[3], bhi[3];
+        scene_bounds(ctx, scene, blo, bhi);
+        const dv3 bl = mk3(blo[0], blo[1], blo[2]), bh = mk3(bhi[0], bhi[1], bhi[2]);
+        const dv3 ext_box = sub3(bh, bl);
+        const double diag =
+            std::sqrt(ext_box.x * ext_box.x + ext_box.y * ext_box.y + ext_box.z * ext_box.z);
+        if (!(diag > 0.0)) throw ValidationError{"gaussians_to_mesh: degenerate field bounding box"};
+        const double truncation = 3.0 * voxel_size;
+        const double margin = truncation + 2.0 * voxel_size;
+        const dv3 lo = sub3(bl, mk3(margin, margin, margin));
+        const dv3 hi = add3(bh, mk3(margin, margin, margin));
+        const dv3 extent = sub3(hi, lo);
+        const double e[3] = {extent.x, extent.y, extent.z};
+        int32_t dims[3];
+        for (int k = 0; k < 3; ++k)
+            dims[k] = std::max(2, static_cast<int>(std::ceil(e[k] / voxel_size)) + 1);
+        double* tsdf = volume->tsdf;
+        double* weights = volume->weights;
+        const double origin[3] = {lo.x, lo.y, lo.z};
+        if (gsim_gpu_tsdf_create(origin, voxel_size, dims, truncation, volume) != GSIM_OK)
+            throw ValidationError{"tsdf: invalid volume"};
+        volume->tsdf = tsdf;
+        volume->weights = weights;
+        if (!tsdf) return;  // geometry-only call
+        check_volume(volume, true);
+        const uint64_t n = uint64_t(dims[0]) * dims[1] * dims[2];
+        launch_tsdf_reset(volume->tsdf, volume->weights, n, ctx->num_sms, ctx->stream);
+        check_launch();
+        constexpr int kFusionAzimuths = 20, kFusionResolution = 256;  // transfer.cpp:25-26
+        constexpr double kRingRadiusFactor = 2.5;                      // transfer.cpp:24
+        std::vector<gsim_camera> cams;
+        const std::vector<uint64_t> off = depth_ring_render(
+            ctx, scene, kFusionAzimuths, kRingRadiusFactor * diag, kFusionResolution, cams);
+        // fuse straight from the render output: depth plane of camera c at off[c] + 3 npx
+        const uint64_t npx = uint64_t(kFusionResolution) * kFusionResolution;
+        std::vector<DevFuseView> views(cams.size());
+        for (size_t k = 0; k < cams.size(); ++k) views[k] = fuse_view(cams[k], off[k] + 3 * npx);
+        fuse_views(ctx, volume, views, ctx->out.ptr);
     });
 }
 

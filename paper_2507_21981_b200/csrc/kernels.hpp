@@ -104,7 +104,8 @@ struct RasterArgs {
     int rect_w;                      // warp-rectangle width: 16 (16x4 bands) or 8 (8x8)
     int batch;                       // records per shared-memory batch: 128 or 256
     int exact_cull;                  // exact ellipse-vs-warp-rectangle test in the compaction
-    int reserved2;
+    float valid_alpha;               // depth written as 0 where accum_alpha < valid_alpha
+                                     // (render_depth_ring, transfer.cpp:116-118); 0 = off
     float* out;                      // per camera [rgb W*H*3 | depth W*H | alpha W*H]
     unsigned long long* consumed;    // += list entries fetched before the tile saturated
     uint64_t capacity;               // pair-buffer capacity (reads are clamped to it)
@@ -170,5 +171,33 @@ void launch_track_query(const DevTracks& tr, const uint32_t* track, const double
 void launch_ply_convert(const PlyArgs& a, int grid_cap, cudaStream_t stream);
 void launch_pose_segments(const DevTracks& tr, DevSegment* segs, const int32_t* seg_track,
                           uint32_t n_segs, double t, cudaStream_t stream);
+
+// GS -> TSDF (transfer.cu): one view of a batched tsdf_fuse.
+struct DevFuseView {
+    double q[4], t[3];               // world -> camera pose
+    double fx, fy, cx, cy;
+    int width, height;
+    uint64_t depth_offset;           // first float of this view's depth image in TsdfArgs::depth
+};
+
+struct TsdfArgs {
+    double origin[3];
+    double voxel_size;
+    double truncation;
+    int dims[3];
+    uint32_t n_views;
+    const DevFuseView* views;        // [n_views], fused in order
+    const float* depth;
+    double* tsdf;                    // [dims[2]][dims[1]][dims[0]]
+    double* weights;
+};
+
+void launch_bounds(const DevField& f, double* partial, int max_blocks, double* out,
+                   cudaStream_t s);
+void launch_tsdf_reset(double* tsdf, double* weights, uint64_t n, int n_sms, cudaStream_t s);
+void launch_tsdf_fuse(const TsdfArgs& a, int n_sms, cudaStream_t s);
+const char* depth_ring_cameras(const double lo[3], const double hi[3], int n_views, double radius,
+                               int resolution, gsim_camera* cameras);
+DevFuseView fuse_view(const gsim_camera& c, uint64_t depth_offset);
 
 }  // namespace gsim_gpu

@@ -88,7 +88,8 @@ __device__ __forceinline__ void write_pixel(const RasterArgs& a, const DevCamera
     if (x >= cam.width || y >= cam.height) return;
     const float r = fminf(fmaxf(cr, 0.f), 1.f), gg = fminf(fmaxf(cg, 0.f), 1.f),
                 bb = fminf(fmaxf(cb, 0.f), 1.f);
-    const float depth = a.normalize_depth ? (acc > 1e-12f ? d / acc : 0.f) : d;
+    float depth = a.normalize_depth ? (acc > 1e-12f ? d / acc : 0.f) : d;
+    if (acc < a.valid_alpha) depth = 0.f;  // render_depth_ring's invalid pixels
     if (a.out) {
         float* base = a.out + cam.out_offset;
         const size_t npx = size_t(cam.width) * cam.height;

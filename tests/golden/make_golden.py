@@ -35,6 +35,12 @@ def test_camera(w=128, h=128, f=100.0) -> CameraModel:  # test_raster.cpp:18-28
     return CameraModel(fx=f, fy=f, cx=w * 0.5, cy=h * 0.5, width=w, height=h)
 
 
+def camera_table(cams) -> np.ndarray:
+    """fx, fy, cx, cy, width, height, pose (q, t), near, far of C cameras, one row each."""
+    return np.array([[c.fx, c.fy, c.cx, c.cy, c.width, c.height, *c.pose.rotation,
+                      *c.pose.translation, c.near_plane, c.far_plane] for c in cams])
+
+
 def cases():
     """Scene cases: acceptance.cpp:47-82 style, test_raster.cpp:142-157 style, nodes."""
     out = []
@@ -109,6 +115,17 @@ def main() -> None:
     # look_at (raster.cpp:25-42) for the BASELINE config-0 camera
     cam = ref.look_at((5.0, 0.0, 0.0), (0.0, 0.0, 0.0), 554.2562584220407, 554.2562584220407, 640, 480)
     data["look_at"] = dict(rotation=list(cam.pose.rotation), translation=list(cam.pose.translation))
+    # GS -> TSDF (transfer.cpp:81-198): render_depth_ring and gaussians_to_mesh's fused volume
+    t = dict(seed=4040, count=600, box=1.5, slo=0.02, shi=0.1, deg=2, n_views=8, radius=6.0,
+             resolution=48, voxel_size=0.1)
+    f3 = ref.random_field(t["seed"], t["count"], t["box"], t["slo"], t["shi"], t["deg"])
+    cams, depth = ref.render_depth_ring(f3, t["n_views"], t["radius"], t["resolution"])
+    vol = ref.gaussians_to_tsdf(f3, t["voxel_size"])
+    t.update(ring_cams_sha=sha(camera_table(cams)), ring_depth_sha=sha(depth),
+             valid_fraction=float((depth > 0).mean()), dims=list(vol.dims),
+             origin=list(vol.origin), truncation=vol.truncation, tsdf_sha=sha(vol.tsdf),
+             weights_sha=sha(vol.weights), observed_fraction=float((vol.weights > 0).mean()))
+    data["transfer"] = t
     OUT.write_text(json.dumps(data, indent=1) + "\n")
     print("wrote", OUT)
 
