@@ -360,6 +360,15 @@ int gsim_gpu_tsdf_fuse(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume,
                        const gsim_camera* cameras, uint64_t n_views, const float* depth,
                        int32_t depth_is_device);
 
+/* Device grids for a volume's dims (cudaMalloc'd by the library; free with tsdf_free), and
+ * host <-> device copies of both grids (synchronous; NULL skips a grid). */
+int gsim_gpu_tsdf_alloc(gsim_gpu_context* ctx, gsim_tsdf_volume* volume);
+int gsim_gpu_tsdf_free(gsim_tsdf_volume* volume);
+int gsim_gpu_tsdf_download(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume, double* tsdf,
+                           double* weights);
+int gsim_gpu_tsdf_upload(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume, const double* tsdf,
+                         const double* weights);
+
 /* gaussians_to_mesh up to the fused volume. Two calls: with volume->tsdf == NULL only the
  * geometry (origin, voxel_size, dims, truncation) is written; then, with device buffers of
  * dims[0] * dims[1] * dims[2] doubles in tsdf and weights, the volume is reset, the depth ring

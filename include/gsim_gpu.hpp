@@ -15,12 +15,17 @@
 //   PoseTracks + Renderer::render_at(tracks, t, ...)    PoseStream::sample + Scene::step_to
 //                                                       (pose_stream.hpp:41-45, scene.cpp:176)
 //   Renderer::render_encoded(...)                       render + encode fused on the GPU
+//   gsim::gpu::render_depth_ring(field, n, radius, res) render_depth_ring (transfer.hpp:33-37)
+//   gsim::gpu::tsdf_fuse(volume, camera, depth)         tsdf_fuse (transfer.hpp:68-71)
+//   gsim::gpu::gaussians_to_tsdf(field, voxel_size)     gaussians_to_mesh's fused volume
+//                                                       (transfer.hpp:82-86, transfer.cpp:174-198)
 //
 // Errors are rethrown as the reference's gsim::validation_error (status 2) and gsim::io_error
 // (status 1). The free functions upload the field on every call (a pure function of their
 // inputs, like the reference); gsim::gpu::Renderer keeps it resident in HBM for the fast path.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -32,6 +37,7 @@
 #include "gsim/gaussian.hpp"
 #include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
+#include "gsim/transfer.hpp"
 #include "gsim_gpu.h"
 
 namespace gsim::gpu {
@@ -88,6 +94,55 @@ inline gsim_camera camera(const CameraModel& c) {
 inline gsim_raster_options options(const RasterOptions& o) {
     return gsim_raster_options{o.normalize_depth ? 1 : 0, 0, o.transmittance_cutoff};
 }
+
+inline CameraModel from_camera(const gsim_camera& c) {
+    CameraModel cam;
+    cam.fx = c.fx;
+    cam.fy = c.fy;
+    cam.cx = c.cx;
+    cam.cy = c.cy;
+    cam.width = c.width;
+    cam.height = c.height;
+    cam.pose = RigidTransform{Quat(c.pose.rotation[0], c.pose.rotation[1], c.pose.rotation[2],
+                                   c.pose.rotation[3]),
+                              Vec3(c.pose.translation[0], c.pose.translation[1], c.pose.translation[2])};
+    cam.near = c.near_plane;
+    cam.far = c.far_plane;
+    return cam;
+}
+
+inline gsim_tsdf_volume volume(const TsdfVolume& v) {
+    gsim_tsdf_volume c{};
+    c.origin[0] = v.origin.x;
+    c.origin[1] = v.origin.y;
+    c.origin[2] = v.origin.z;
+    c.voxel_size = v.voxel_size;
+    for (int k = 0; k < 3; ++k) c.dims[k] = v.dims[k];
+    c.truncation = v.truncation;
+    return c;
+}
+
+// Device grids of one volume for the duration of a call.
+struct DeviceVolume {
+    gsim_gpu_context* ctx;
+    gsim_tsdf_volume v;
+    DeviceVolume(gsim_gpu_context* c, const gsim_tsdf_volume& geometry) : ctx(c), v(geometry) {
+        v.tsdf = v.weights = nullptr;
+        check(gsim_gpu_tsdf_alloc(ctx, &v), ctx);
+    }
+    ~DeviceVolume() { gsim_gpu_tsdf_free(&v); }
+    DeviceVolume(const DeviceVolume&) = delete;
+    DeviceVolume& operator=(const DeviceVolume&) = delete;
+    void upload(const TsdfVolume& host) {
+        check(gsim_gpu_tsdf_upload(ctx, &v, host.tsdf.data(), host.weights.data()), ctx);
+    }
+    TsdfVolume download() const {
+        TsdfVolume out = TsdfVolume::create(Vec3(v.origin[0], v.origin[1], v.origin[2]), v.voxel_size,
+                                            {v.dims[0], v.dims[1], v.dims[2]}, v.truncation);
+        check(gsim_gpu_tsdf_download(ctx, &v, out.tsdf.data(), out.weights.data()), ctx);
+        return out;
+    }
+};
 
 }  // namespace detail
 
@@ -248,6 +303,47 @@ public:
         return out;
     }
 
+    // render_depth_ring (transfer.cpp:81-124) of the resident field.
+    std::vector<DepthView> render_depth_ring(int n_views, double radius, int resolution) {
+        const std::size_t n = std::size_t(3) * std::size_t(n_views > 0 ? n_views : 0);
+        std::vector<gsim_camera> cs(n ? n : 1);
+        std::vector<float> depth(std::max<std::size_t>(n, 1) * std::size_t(resolution > 0 ? resolution : 0) *
+                                 std::size_t(resolution > 0 ? resolution : 0));
+        detail::check(gsim_gpu_render_depth_ring(ctx_.get(), scene_.get(), n_views, radius, resolution,
+                                                 cs.data(), depth.data(), 0),
+                      ctx_.get());
+        std::vector<DepthView> views(n);
+        const std::size_t npx = std::size_t(resolution) * resolution;
+        for (std::size_t v = 0; v < n; ++v) {
+            views[v].camera = detail::from_camera(cs[v]);
+            views[v].depth = Image1(resolution, resolution);
+            std::memcpy(views[v].depth.data.data(), depth.data() + v * npx, npx * sizeof(float));
+        }
+        return views;
+    }
+
+    // gaussians_to_mesh (transfer.cpp:174-198) up to the fused volume, on the resident field.
+    TsdfVolume gaussians_to_tsdf(double voxel_size) {
+        gsim_tsdf_volume v{};
+        detail::check(gsim_gpu_gaussians_to_tsdf(ctx_.get(), scene_.get(), voxel_size, &v), ctx_.get());
+        detail::DeviceVolume dev(ctx_.get(), v);
+        detail::check(gsim_gpu_gaussians_to_tsdf(ctx_.get(), scene_.get(), voxel_size, &dev.v), ctx_.get());
+        return dev.download();
+    }
+
+    // tsdf_fuse (transfer.cpp:143-172): the volume's grids make a round trip through HBM.
+    void tsdf_fuse(TsdfVolume& volume, const CameraModel& camera, const Image1& depth) {
+        if (depth.width != camera.width || depth.height != camera.height)
+            throw validation_error("tsdf_fuse: depth image does not match camera resolution");
+        detail::DeviceVolume dev(ctx_.get(), detail::volume(volume));
+        dev.upload(volume);
+        const gsim_camera c = detail::camera(camera);
+        detail::check(gsim_gpu_tsdf_fuse(ctx_.get(), &dev.v, &c, 1, depth.data.data(), 0), ctx_.get());
+        const TsdfVolume out = dev.download();
+        volume.tsdf = out.tsdf;
+        volume.weights = out.weights;
+    }
+
     gsim_gpu_context* context() { return ctx_.get(); }
     gsim_gpu_scene* scene() { return scene_.get(); }
 
@@ -328,6 +424,27 @@ inline void transform_primitives(GaussianField& field, const IndexRange& range,
         p.mean = Vec3(means[3 * i], means[3 * i + 1], means[3 * i + 2]);
         p.rotation = Quat(rots[4 * i], rots[4 * i + 1], rots[4 * i + 2], rots[4 * i + 3]);
     }
+}
+
+// render_depth_ring (transfer.cpp:81-124): same signature, views rendered on the GPU.
+inline std::vector<DepthView> render_depth_ring(const GaussianField& field, int n_views, double radius,
+                                                int resolution) {
+    Renderer& r = default_renderer();
+    r.upload(field);
+    return r.render_depth_ring(n_views, radius, resolution);
+}
+
+// tsdf_fuse (transfer.cpp:143-172): same signature.
+inline void tsdf_fuse(TsdfVolume& volume, const CameraModel& camera, const Image1& depth) {
+    default_renderer().tsdf_fuse(volume, camera, depth);
+}
+
+// The volume gaussians_to_mesh fuses (its fused_volume output, transfer.cpp:194-195); marching
+// cubes and decimation stay with the caller (extract_mesh, decimate).
+inline TsdfVolume gaussians_to_tsdf(const GaussianField& field, double voxel_size) {
+    Renderer& r = default_renderer();
+    r.upload(field);
+    return r.gaussians_to_tsdf(voxel_size);
 }
 
 // The bytes gsim::write_png_rgb8 (srgb), write_png_gray8, write_png_gray16 (scale) and write_pfm

@@ -164,6 +164,12 @@ SIGNATURES = [
     ("gsim_gpu_tsdf_fuse", C.c_int, [_P, C.POINTER(gsim_tsdf_volume), C.POINTER(gsim_camera),
                                      C.c_uint64, _P, C.c_int32]),
     ("gsim_gpu_gaussians_to_tsdf", C.c_int, [_P, _P, C.c_double, C.POINTER(gsim_tsdf_volume)]),
+    ("gsim_gpu_tsdf_alloc", C.c_int, [_P, C.POINTER(gsim_tsdf_volume)]),
+    ("gsim_gpu_tsdf_free", C.c_int, [C.POINTER(gsim_tsdf_volume)]),
+    ("gsim_gpu_tsdf_download", C.c_int, [_P, C.POINTER(gsim_tsdf_volume), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
+    ("gsim_gpu_tsdf_upload", C.c_int, [_P, C.POINTER(gsim_tsdf_volume), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
 ]
 
 _lib = None

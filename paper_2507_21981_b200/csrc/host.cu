@@ -2006,6 +2006,61 @@ int gsim_gpu_tsdf_fuse(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume,
     });
 }
 
+int gsim_gpu_tsdf_alloc(gsim_gpu_context* ctx, gsim_tsdf_volume* volume) {
+    return Guard(ctx).run([&] {
+        check_volume(volume, false);
+        const uint64_t n = uint64_t(volume->dims[0]) * volume->dims[1] * volume->dims[2];
+        double* t = nullptr;
+        double* w = nullptr;
+        GSIM_CK(cudaMalloc(&t, n * sizeof(double)));
+        if (cudaMalloc(&w, n * sizeof(double)) != cudaSuccess) {
+            cudaFree(t);
+            throw CudaError{"tsdf_alloc: out of device memory"};
+        }
+        volume->tsdf = t;
+        volume->weights = w;
+    });
+}
+
+int gsim_gpu_tsdf_free(gsim_tsdf_volume* volume) {
+    if (!volume) return GSIM_ERR_VALIDATION;
+    if (volume->tsdf) cudaFree(volume->tsdf);
+    if (volume->weights) cudaFree(volume->weights);
+    volume->tsdf = nullptr;
+    volume->weights = nullptr;
+    return GSIM_OK;
+}
+
+int gsim_gpu_tsdf_download(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume, double* tsdf,
+                           double* weights) {
+    return Guard(ctx).run([&] {
+        check_volume(volume, true);
+        const uint64_t n = uint64_t(volume->dims[0]) * volume->dims[1] * volume->dims[2];
+        if (tsdf)
+            GSIM_CK(cudaMemcpyAsync(tsdf, volume->tsdf, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        if (weights)
+            GSIM_CK(cudaMemcpyAsync(weights, volume->weights, n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int gsim_gpu_tsdf_upload(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume, const double* tsdf,
+                         const double* weights) {
+    return Guard(ctx).run([&] {
+        check_volume(volume, true);
+        const uint64_t n = uint64_t(volume->dims[0]) * volume->dims[1] * volume->dims[2];
+        if (tsdf)
+            GSIM_CK(cudaMemcpyAsync(volume->tsdf, tsdf, n * sizeof(double), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+        if (weights)
+            GSIM_CK(cudaMemcpyAsync(volume->weights, weights, n * sizeof(double),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int gsim_gpu_gaussians_to_tsdf(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
                                double voxel_size, gsim_tsdf_volume* volume) {
     // gaussians_to_mesh up to the fused volume, transfer.cpp:174-198

@@ -14,6 +14,7 @@
 #include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
 #include "gsim/splat_ply.hpp"
+#include "gsim/transfer.hpp"
 #include "gsim_gpu.hpp"
 #include "png.h"  // oracle/png_capture: the row bytes the reference writers hand to libpng
 #include "test_oracles.hpp"
@@ -197,6 +198,61 @@ int main() {
             }
         }
         std::printf("render_at: 4 times x 2 cameras checked against PoseStream::sample + render\n");
+    }
+
+    // GS -> TSDF (transfer.cpp): depth ring, fuse, fused volume
+    {
+        GaussianField small = oracle::random_field(77, 800, 1.5, 0.02, 0.1, 1);
+        const auto ra = render_depth_ring(small, 8, 6.0, 48);
+        const auto ga = gpu::render_depth_ring(small, 8, 6.0, 48);
+        std::size_t cam_diff = ra.size() != ga.size(), mask_diff = 0, depth_bad = 0, both = 0, px = 0;
+        for (std::size_t v = 0; v < std::min(ra.size(), ga.size()); ++v) {
+            const auto &a = ra[v].camera, &b = ga[v].camera;
+            cam_diff += a.fx != b.fx || a.cx != b.cx || a.near != b.near || a.far != b.far ||
+                        a.pose.rotation.w != b.pose.rotation.w || a.pose.rotation.x != b.pose.rotation.x ||
+                        a.pose.translation.x != b.pose.translation.x ||
+                        a.pose.translation.z != b.pose.translation.z;
+            for (std::size_t i = 0; i < ra[v].depth.data.size(); ++i, ++px) {
+                const double da = ra[v].depth.data[i], db = ga[v].depth.data[i];
+                mask_diff += (da > 0) != (db > 0);
+                if (da > 0 && db > 0) {
+                    ++both;
+                    depth_bad += std::fabs(db - da) > 1e-3 * std::fabs(da);
+                }
+            }
+        }
+        std::printf("render_depth_ring: %zu camera mismatches, mask differs on %zu of %zu px, "
+                    "%zu of %zu depths beyond 1e-3\n", cam_diff, mask_diff, px, depth_bad, both);
+        if (cam_diff || mask_diff > px / 1000 || depth_bad > both / 1000) ++failures;
+        // tsdf_fuse on the reference's own depth maps: bit-exact
+        TsdfVolume va = TsdfVolume::create({-1.7, -1.8, -1.6}, 0.06, {57, 60, 55}, 0.18);
+        TsdfVolume vb = va;
+        for (const auto& view : ra) {
+            tsdf_fuse(va, view.camera, view.depth);
+            gpu::tsdf_fuse(vb, view.camera, view.depth);
+        }
+        std::size_t fuse_diff = 0;
+        for (std::size_t i = 0; i < va.tsdf.size(); ++i)
+            fuse_diff += va.tsdf[i] != vb.tsdf[i] || va.weights[i] != vb.weights[i];
+        std::printf("tsdf_fuse: %zu of %zu voxels differ\n", fuse_diff, va.tsdf.size());
+        if (fuse_diff) ++failures;
+        // gaussians_to_mesh's fused volume vs gsim::gpu::gaussians_to_tsdf
+        TsdfVolume fused;
+        gaussians_to_mesh(small, 0.1, std::size_t(-1), &fused);
+        const TsdfVolume g = gpu::gaussians_to_tsdf(small, 0.1);
+        std::size_t close = 0;
+        const bool geo = g.dims == fused.dims && g.origin.x == fused.origin.x &&
+                         g.origin.z == fused.origin.z && g.truncation == fused.truncation;
+        for (std::size_t i = 0; geo && i < g.tsdf.size(); ++i)
+            close += g.weights[i] == fused.weights[i] && std::fabs(g.tsdf[i] - fused.tsdf[i]) <= 1e-3;
+        std::printf("gaussians_to_tsdf: geometry %s, %zu of %zu voxels match\n", geo ? "equal" : "DIFFERENT",
+                    close, fused.tsdf.size());
+        if (!geo || close < fused.tsdf.size() * 99 / 100) ++failures;
+        bool ref_threw = false, gpu_threw = false;
+        try { render_depth_ring(small, 7, 6.0, 48); } catch (const validation_error&) { ref_threw = true; }
+        try { gpu::render_depth_ring(small, 7, 6.0, 48); } catch (const validation_error&) { gpu_threw = true; }
+        std::printf("render_depth_ring validation_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
+        if (!ref_threw || !gpu_threw) ++failures;
     }
 
     std::printf(failures ? "DROP-IN FAILED\n" : "DROP-IN OK\n");
