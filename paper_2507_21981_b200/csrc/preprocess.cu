@@ -101,9 +101,11 @@ __device__ __forceinline__ void shade_sh(const float4* sh, uint64_t n, uint64_t 
                 c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
             }
         }
+        // explicit FMAs: this file is compiled with -fmad=false for the double geometry, but
+        // the fp32 shading has no bit-exactness contract (the reference shades in double)
         float acc = 0.5f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) acc += basis[k] * c[ch * K + k - 4 * p0];
+        for (int k = 0; k < K; ++k) acc = __fmaf_rn(basis[k], c[ch * K + k - 4 * p0], acc);
         rgb[ch] = (acc < 0.0f) ? 0.0f : acc;
     }
 }
