@@ -6,11 +6,15 @@ raises. Build it with ``python -m paper_2507_21981_b200.build`` (or __graft_entr
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libgsim_gpu.so"
+# A/B measurement hook: another in-tree build of the same library (e.g. libgsim_gpu_b.so)
+if os.environ.get("GSIM_GPU_LIB"):
+    LIB_PATH = Path(__file__).resolve().parent / Path(os.environ["GSIM_GPU_LIB"]).name
 
 GSIM_OK = 0
 GSIM_ERR_IO = 1

@@ -470,13 +470,18 @@ void record_ev(gsim_gpu_context* ctx, int e) {
 void check_launch() { GSIM_CK(cudaGetLastError()); }
 
 int bin_warps_for(uint32_t max_tc) {
-    // u32 counter + u8 probe per grid cell per warp (bin.cu bin_warp_bytes)
-    const size_t per_warp = (size_t(max_tc) * 5 + 15) & ~size_t(15);
+    // u32 counter + u32 lane bitmap per grid cell per warp (bin.cu bin_warp_bytes)
+    static const int cap = [] {
+        const char* e = std::getenv("GSIM_GPU_BIN_WARPS");
+        const int v = e ? std::atoi(e) : 4;  // 4 measured faster than 8 (occupancy)
+        return v >= 1 && v <= 8 ? v : 4;
+    }();
+    const size_t per_warp = size_t(max_tc) * 8;
     const size_t budget = 200 * 1024;
-    const int w = int(std::min<size_t>(8, budget / std::max<size_t>(per_warp, 1)));
+    const int w = int(std::min<size_t>(size_t(cap), budget / std::max<size_t>(per_warp, 1)));
     if (w < 1)
         throw ValidationError{"camera with " + std::to_string(max_tc) +
-                              " tiles exceeds the binning shared-memory budget (40960 tiles)"};
+                              " tiles exceeds the binning shared-memory budget (25600 tiles)"};
     return w;
 }
 
