@@ -15,10 +15,10 @@
 //   3. each warp walks its list with a branch-free blend: a splat that fails the box test or
 //      the 1/255 skip gets weight 0, which leaves C, D, A and T bit-for-bit unchanged, so the
 //      result equals the reference's skip-with-continue loop;
-//   4. a pixel that saturates (T < cutoff after accumulating) parks at T = 0, so later
-//      weights are exactly zero; T is therefore always 0 or >= cutoff, which makes the park
-//      test independent of the skip test. A warp stops when all its pixels are parked and the
-//      CTA leaves when __syncthreads_count says every pixel is.
+//   4. a splat is composited only while T >= cutoff (a fourth condition of the gate), which is
+//      the reference's break after the accumulation that takes T below the cutoff; a warp stops
+//      when all its pixels are done and the CTA leaves when __syncthreads_count says every
+//      pixel is. Lists whose splats all have peak opacity <= 0.989 skip the 0.99 clamp.
 //
 // Per-pixel contract (raster.cpp:215-249): box test |dx|>r || |dy|>r, q with 2*inv_xy,
 // alpha = min(o*exp(-q/2), 0.99), skip alpha < 1/255, accumulate, T *= 1-alpha, stop after
@@ -42,10 +42,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 __device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
 
-// (e0, e1) with each lane zeroed unless |dx_i| <= r, |dy| <= r and e_i >= 1/255: the chained
-// setp.and form gives one compare per condition and one select per pixel.
+// (e0, e1) with each lane zeroed unless |dx_i| <= r, |dy| <= r, e_i >= 1/255 and the pixel is
+// still alive (T_i >= cutoff: the reference breaks once T drops below the cutoff, so a splat is
+// composited iff T before it is >= cutoff). The chained setp.and form gives one compare per
+// condition and one select per pixel.
 __device__ __forceinline__ float2 gate(float e0, float e1, float adx0, float adx1, float ady,
-                                       float r) {
+                                       float r, float2 T, float cutoff) {
     static_assert(float(kAlphaSkip) == 0x1.010102p-8f, "skip constant below");
     float2 o;
     asm("{\n\t.reg .pred py, p0, p1;\n\t"
@@ -54,12 +56,30 @@ __device__ __forceinline__ float2 gate(float e0, float e1, float adx0, float adx
         "setp.le.and.f32 p1, %3, %5, py;\n\t"
         "setp.ge.and.f32 p0, %6, 0f3B808081, p0;\n\t"
         "setp.ge.and.f32 p1, %7, 0f3B808081, p1;\n\t"
+        "setp.ge.and.f32 p0, %8, %10, p0;\n\t"
+        "setp.ge.and.f32 p1, %9, %10, p1;\n\t"
         "selp.f32 %0, %6, 0f00000000, p0;\n\t"
         "selp.f32 %1, %7, 0f00000000, p1;\n\t}"
         : "=f"(o.x), "=f"(o.y)
-        : "f"(adx0), "f"(adx1), "f"(ady), "f"(r), "f"(e0), "f"(e1));
+        : "f"(adx0), "f"(adx1), "f"(ady), "f"(r), "f"(e0), "f"(e1), "f"(T.x), "f"(T.y),
+          "f"(cutoff));
     return o;
 }
+
+// Record at a 16-bit shared-memory address (the compacted list holds addresses, so the blend
+// loop needs no address arithmetic).
+__device__ __forceinline__ void load_record(uint32_t addr, float4& a, float4& b, float4& c) {
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%12];\n\t"
+        "ld.shared.v4.f32 {%4, %5, %6, %7}, [%12+16];\n\t"
+        "ld.shared.v4.f32 {%8, %9, %10, %11}, [%12+32];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w),
+          "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
+        : "r"(addr));
+}
+
+// log2 of the largest peak opacity whose alpha can never reach the 0.99 clamp (0.989, a margin
+// for the rounding of the exponent): batches without brighter splats skip the clamp.
+constexpr float kNoClampLog2 = -0.015957f;  // log2(0.989) rounded down
 
 // Can the splat reach alpha >= 1/255 at any point of the rectangle [x_lo, x_hi] x [y_lo, y_hi]
 // of pixel centres? The ex2 exponent E(dx, dy) = lop + dx (A dx + B dy) + C dy^2 (dx = u - px,
@@ -107,6 +127,44 @@ __device__ __forceinline__ void write_pixel(const RasterArgs& a, const DevCamera
     }
 }
 }  // namespace
+
+// Front-to-back blend of a warp's compacted list for the thread's pixel pair (raster.cpp:
+// 221-238). kClamp: some splat of the list can reach the 0.99 alpha clamp.
+template <bool kClamp>
+__device__ __forceinline__ void blend_list(const uint16_t* list, uint32_t count, float2 npx,
+                                           float py, float cutoff, float2& cr, float2& cg,
+                                           float2& cb, float2& d, float2& acc, float2& T) {
+    for (uint32_t k0 = 0; k0 < count; k0 += 32) {
+        const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
+#pragma unroll 4
+        for (uint32_t k = k0; k < k1; ++k) {
+            float4 p0, p1, p2;
+            load_record(list[k], p0, p1, p2);
+            // row terms, shared by the pair
+            const float dy = p0.y - py;
+            const float kq = fmaf(p1.z * dy, dy, p0.w);
+            // pair terms on the packed pipe
+            const float2 dx = __fadd2_rn(bc(p0.x), npx);
+            const float2 t = __ffma2_rn(bc(p1.x), dx, bc(p1.y * dy));
+            const float2 E = __ffma2_rn(t, dx, bc(kq));
+            float e0 = ex2_approx(E.x), e1 = ex2_approx(E.y);
+            if (kClamp) {
+                e0 = fminf(e0, 0.99f);
+                e1 = fminf(e1, 0.99f);
+            }
+            const float2 w = __fmul2_rn(gate(e0, e1, fabsf(dx.x), fabsf(dx.y), fabsf(dy), p0.z, T, cutoff), T);
+            cr = __ffma2_rn(bc(p2.x), w, cr);
+            cg = __ffma2_rn(bc(p2.y), w, cg);
+            cb = __ffma2_rn(bc(p2.z), w, cb);
+            d = __ffma2_rn(bc(p1.w), w, d);
+            acc = __fadd2_rn(acc, w);
+            // T * (1 - alpha) == T - w up to rounding; once T < cutoff the gate zeroes every
+            // later weight, so T (and the pixel) stays put: the reference's break.
+            T = __fadd2_rn(T, make_float2(-w.x, -w.y));
+        }
+        if (__all_sync(0xffffffffu, T.x < cutoff && T.y < cutoff)) break;
+    }
+}
 
 // RW = warp-rectangle width in pixels (16: 16x4 bands, 8: 8x8 quadrants); kBatch = records
 // per batch (two buffers of kBatch * 48 bytes of shared memory).
@@ -190,14 +248,17 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
             load_slots(b0 + 2 * kBatch);
         }
 
-        if (!__all_sync(0xffffffffu, T.x == 0.0f && T.y == 0.0f)) {
+        if (!__all_sync(0xffffffffu, T.x < cutoff && T.y < cutoff)) {
             // Compact the splats that can reach this warp's rectangle (depth order preserved)
-            // as byte offsets into s_spl.
+            // as shared-memory addresses of their records.
             const Record* spl_buf = s_spl[buf];
+            const uint32_t spl_addr = uint32_t(__cvta_generic_to_shared(spl_buf));
             uint32_t count = 0;
+            bool bright = false;
             for (uint32_t j = 0; j < n_b; j += 32) {
                 const uint32_t idx = j + lane;
                 bool mine = false;
+                float lop = -INFINITY;
                 if (idx < n_b) {
                     const float4 p0 = spl_buf[idx].a;
                     const float rw = spl_buf[idx].c.w;
@@ -206,46 +267,22 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
                     mine = p0.x + ex >= wx_lo && p0.x - ex <= wx_hi && p0.y + ey >= wy_lo &&
                            p0.y - ey <= wy_hi;
                     if (a.exact_cull) mine = mine && reaches_rect(p0, spl_buf[idx].b, wx_lo, wx_hi, wy_lo, wy_hi);
+                    lop = p0.w;
                 }
                 const uint32_t bits = __ballot_sync(0xffffffffu, mine);
+                bright |= __any_sync(0xffffffffu, mine && !(lop <= kNoClampLog2));
                 if (mine)
                     s_list[warp][count + __popc(bits & lanemask_lt())] =
-                        uint16_t(idx * sizeof(Record));
+                        uint16_t(spl_addr + idx * sizeof(Record));
                 count += __popc(bits);
             }
             __syncwarp();
-            const char* spl = reinterpret_cast<const char*>(spl_buf);
-            for (uint32_t k0 = 0; k0 < count; k0 += 32) {
-                const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
-#pragma unroll 4
-                for (uint32_t k = k0; k < k1; ++k) {
-                    const Record& sp = *reinterpret_cast<const Record*>(spl + s_list[warp][k]);
-                    const float4 p0 = sp.a, p1 = sp.b, p2 = sp.c;
-                    // row terms, shared by the pair
-                    const float dy = p0.y - py;
-                    const float kq = fmaf(p1.z * dy, dy, p0.w);
-                    // pair terms on the packed pipe
-                    const float2 dx = __fadd2_rn(bc(p0.x), npx);
-                    const float2 t = __ffma2_rn(bc(p1.x), dx, bc(p1.y * dy));
-                    const float2 E = __ffma2_rn(t, dx, bc(kq));
-                    const float e0 = fminf(ex2_approx(E.x), 0.99f);
-                    const float e1 = fminf(ex2_approx(E.y), 0.99f);
-                    const float2 w = __fmul2_rn(gate(e0, e1, fabsf(dx.x), fabsf(dx.y), fabsf(dy), p0.z), T);
-                    cr = __ffma2_rn(bc(p2.x), w, cr);
-                    cg = __ffma2_rn(bc(p2.y), w, cg);
-                    cb = __ffma2_rn(bc(p2.z), w, cb);
-                    d = __ffma2_rn(bc(p1.w), w, d);
-                    acc = __fadd2_rn(acc, w);
-                    // T * (1 - alpha) == T - w up to rounding; a saturated pixel parks at T = 0,
-                    // where every later weight is exactly zero (the reference's break).
-                    const float2 Tn = __fadd2_rn(T, make_float2(-w.x, -w.y));
-                    T.x = Tn.x < cutoff ? 0.0f : Tn.x;
-                    T.y = Tn.y < cutoff ? 0.0f : Tn.y;
-                }
-                if (__all_sync(0xffffffffu, T.x == 0.0f && T.y == 0.0f)) break;
-            }
+            if (bright)
+                blend_list<true>(s_list[warp], count, npx, py, cutoff, cr, cg, cb, d, acc, T);
+            else
+                blend_list<false>(s_list[warp], count, npx, py, cutoff, cr, cg, cb, d, acc, T);
         }
-        if (__syncthreads_count(T.x == 0.0f && T.y == 0.0f ? 0 : 1) == 0) break;
+        if (__syncthreads_count(T.x < cutoff && T.y < cutoff ? 0 : 1) == 0) break;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // no copy may land after the CTA exits
 
