@@ -10,7 +10,8 @@
 //   count     per unit, pairs per tile: every record adds +1 / -1 at both ends of each of its
 //             rect rows in a shared row-difference array (red.shared), rows are then
 //             prefix-summed by warp scans; the row goes to a per-camera [unit][tile] matrix;
-//   colscan   per (camera, tile): exclusive scan over the camera's units (lanes = tiles);
+//   colscan   per (camera, tile): exclusive scan over the camera's units (lanes = tiles,
+//             warps = unit segments);
 //   tilescan  per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:198-202);
 //   campre    per batch: pair base of every camera;
 //   scatter   per unit: each warp recounts its slice the same way, the CTA turns the counts
@@ -275,28 +276,54 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinArgs a) {
     (void)lane;
 }
 
-// ---- column scan: one thread per (camera, tile), serial over the camera's units ----------------
+// ---- column scan: lanes = 32 consecutive (camera, tile) columns, warps = 8 unit segments ------
+// Each warp sums its segment of units for its lane's column (coalesced 128-byte rows of the
+// [unit][tile] matrix), the block combines the 8 segment sums, and a second sweep writes the
+// exclusive prefixes. A lane's column may belong to another camera than its neighbours'.
 __global__ void __launch_bounds__(kThreads) bin_colscan_kernel(BinArgs a) {
+    __shared__ uint32_t s_seg[kWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t n_cols = a.cam_tile_base[a.n_cams];
-    for (uint32_t g = blockIdx.x * kThreads + threadIdx.x; g < n_cols; g += gridDim.x * kThreads) {
+    const uint32_t g = blockIdx.x * 32 + lane;
+    const bool in = g < n_cols;
+    uint32_t* col = nullptr;
+    uint32_t tc = 0, k_lo = 0, k_hi = 0;
+    if (in) {
         const int c = upper_index(a.cam_tile_base, a.n_cams, g);
-        const uint32_t tc = a.cam_tile_base[c + 1] - a.cam_tile_base[c];
-        const uint32_t t = g - a.cam_tile_base[c];
+        tc = a.cam_tile_base[c + 1] - a.cam_tile_base[c];
         const uint32_t nk = a.cam_chunk_base[c + 1] - a.cam_chunk_base[c];
-        uint32_t* col = a.counts + a.cam_mbase[c] + t;
-        uint32_t run = 0;
-        constexpr uint32_t kU = 8;  // loads in flight
-        for (uint32_t k0 = 0; k0 < nk; k0 += kU) {
-            uint32_t v[kU];
+        col = a.counts + a.cam_mbase[c] + (g - a.cam_tile_base[c]);
+        k_lo = uint32_t(uint64_t(nk) * warp / kWarps);
+        k_hi = uint32_t(uint64_t(nk) * (warp + 1) / kWarps);
+    }
+    constexpr uint32_t kU = 4;  // loads in flight per lane
+    uint32_t sum = 0;
+    for (uint32_t k0 = k_lo; k0 < k_hi; k0 += kU) {
+        uint32_t v[kU];
 #pragma unroll
-            for (uint32_t q = 0; q < kU; ++q) v[q] = k0 + q < nk ? col[uint64_t(k0 + q) * tc] : 0u;
+        for (uint32_t q = 0; q < kU; ++q) v[q] = k0 + q < k_hi ? col[uint64_t(k0 + q) * tc] : 0u;
 #pragma unroll
-            for (uint32_t q = 0; q < kU; ++q) {
-                if (k0 + q < nk) col[uint64_t(k0 + q) * tc] = run;
-                run += v[q];
-            }
+        for (uint32_t q = 0; q < kU; ++q) sum += v[q];
+    }
+    s_seg[warp][lane] = sum;
+    __syncthreads();
+    uint32_t run = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t x = s_seg[w][lane];
+        if (w < warp) run += x;
+        total += x;
+    }
+    if (in && warp == 0) a.tile_count[g] = total;
+    for (uint32_t k0 = k_lo; k0 < k_hi; k0 += kU) {
+        uint32_t v[kU];
+#pragma unroll
+        for (uint32_t q = 0; q < kU; ++q) v[q] = k0 + q < k_hi ? col[uint64_t(k0 + q) * tc] : 0u;
+#pragma unroll
+        for (uint32_t q = 0; q < kU; ++q) {
+            if (k0 + q < k_hi) col[uint64_t(k0 + q) * tc] = run;
+            run += v[q];
         }
-        a.tile_count[g] = run;
     }
 }
 

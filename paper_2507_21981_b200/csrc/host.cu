@@ -638,7 +638,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     const int chunk_grid = int(std::max<uint64_t>(1, kmax));
     launch_bin_count(b, chunk_grid, s);
     check_launch();
-    launch_bin_colscan(b, int(std::max<uint64_t>(1, (uint64_t(p.tiles) + 255) / 256)), s);
+    launch_bin_colscan(b, int(std::max<uint64_t>(1, (uint64_t(p.tiles) + 31) / 32)), s);
     check_launch();
     launch_bin_tilescan(b, int(std::min<uint64_t>(p.cams.size(), uint64_t(n_sms) * 2)), s);
     check_launch();

@@ -99,7 +99,8 @@ def main() -> None:
         (PROF / f"{a.tag}_launches.md").write_text("\n".join(lines) + "\n")
         # stage traffic (per frame): sum over the stage's kernels of mean bytes per launch x
         # launches per frame
-        frames = len(agg.get("raster_kernel", {}).get("gpu__time_duration.sum", [1]))
+        frames = sum(len(m["gpu__time_duration.sum"]) for n, m in agg.items()
+                     if n.startswith("raster_kernel")) or 1
         traffic = {}
         for stage, kernels in STAGES.items():
             b = 0.0
