@@ -112,12 +112,13 @@ def stage_bytes(stats: dict, n_prims: int, sh_degree: int, pixels: int, n_cams: 
         # 4 B rect per visible slot, 4 B key per culled slot
         "preprocess": (88 + sh_bytes) * n_prims + 52 * V + 4 * S,
         # histogram reads S keys; pass 1 reads S keys, writes V (key, slot); passes 2-3 read
-        # and write 8 B; pass 4 reads 8 B, writes the 4 B slot
-        "depth_sort": 4 * S + 4 * S + 8 * V + 2 * 16 * V + 12 * V,
-        # count: V slots + V rects; column scan reads and writes the count matrix
-        "binning": 8 * V + 12 * M,
-        # scatter: V slots + V rects again, column prefixes, P record slots written
-        "scatter": 8 * V + 4 * M + 4 * P,
+        # and write 8 B; pass 4 reads 8 B, writes the 4 B slot and gathers + writes the 4 B rect
+        "depth_sort": 4 * S + 4 * S + 8 * V + 2 * 16 * V + 16 * V,
+        # count: V sorted rects; column scan reads the count matrix twice and writes it once
+        "binning": 4 * V + 12 * M,
+        # scatter: V rects (recount) + V rects and slots (placement), column prefixes, P record
+        # slots written
+        "scatter": 12 * V + 4 * M + 4 * P,
         # K list entries + 48 B records (2 sectors: 64 B) + 20 B/px outputs
         "raster": 4 * K + 64 * K + 20 * pixels,
     }
@@ -324,6 +325,18 @@ def run_ours(args, rank, world, local):
         "pipeline_frac": round(sum(bytes_.values()) / (total_ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)
         if total_ms else None,
     }
+    # The rasterizer is FP32-issue-bound, not HBM-bound: its warp instructions
+    # per frame (profiles/instructions.json, ncu) over the live stage time, against the issue
+    # peak of 4 warp instructions per SM per cycle at the sampled SM clock.
+    inst = load_profile_json("instructions.json", dominant)
+    if inst and per_step_ms[dominant] > 0:
+        sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        n_sms = torch.cuda.get_device_properties(local).multi_processor_count
+        peak_ipc = n_sms * 4 * sm_mhz * 1e6
+        ach = inst / (per_step_ms[dominant] / 1e3)
+        roofline["issue"] = {"kernel": dominant, "warp_instructions": int(inst),
+                             "achieved": round(ach / 1e9, 1), "peak": round(peak_ipc / 1e9, 1),
+                             "unit": "G warp-instr/s", "frac": round(ach / peak_ipc, 4)}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -353,15 +366,20 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
 
 
-def load_traffic(stage: str):
-    """dram read+write bytes per launch of the stage's kernel from the committed ncu capture."""
-    p = ROOT / "profiles" / "traffic.json"
+def load_profile_json(name: str, stage: str):
+    """Per-stage figure from a committed ncu summary under profiles/ (None if absent)."""
+    p = ROOT / "profiles" / name
     if p.exists():
         try:
             return json.loads(p.read_text()).get(stage)
         except Exception:
             return None
     return None
+
+
+def load_traffic(stage: str):
+    """dram read+write bytes per frame of the stage's kernels from the committed ncu capture."""
+    return load_profile_json("traffic.json", stage)
 
 
 def cpu_baseline(w, budget_s: float) -> dict:

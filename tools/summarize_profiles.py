@@ -139,6 +139,14 @@ def main() -> None:
                 for k, u, s in keys)
             lines.append(f"| {name} | {vals} | {st} |")
         (PROF / f"{a.tag}_frame.md").write_text("\n".join(lines) + "\n")
+        # warp instructions per frame of every stage (bench.py's issue-rate roofline)
+        inst = {}
+        for stage, kernels in STAGES.items():
+            inst[stage] = int(sum(f(d, "smsp__inst_executed.sum", 0.0) for d in rows
+                                  if any(short(d.get("Kernel Name", "")).startswith(k) for k in kernels)))
+        (PROF / "instructions.json").write_text(json.dumps(
+            {"source": f"profiles/{a.tag}_frame.md (ncu smsp__inst_executed.sum per frame, config 1, "
+                       "one context)", **inst}, indent=1) + "\n")
 
 
 if __name__ == "__main__":
