@@ -376,6 +376,42 @@ int gsim_gpu_tsdf_upload(gsim_gpu_context* ctx, const gsim_tsdf_volume* volume, 
 int gsim_gpu_gaussians_to_tsdf(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
                                double voxel_size, gsim_tsdf_volume* volume);
 
+
+/* ---- LiDAR: Gaussian ray tracing for a spinning-scan sensor -------------
+ * trace.cpp:14-36   pose_primitive (inverse covariance with the 1e-7 scale floor, 3-sigma AABB)
+ * trace.cpp:38-49   ray_gaussian_peak      trace.cpp:65-85  composite (front to back in (t, index)
+ *                                          order, alpha clamp 0.99, skip < 1/255, cutoff 1e-4)
+ * trace.cpp:88-111  GaussianBvh::build (node poses painted like PoseTable; range check)
+ * trace.cpp:113-134 trace / trace_linear (the BVH only accelerates: the candidate set is every
+ *                   primitive whose box the ray hits, bvh.hpp:20-36)
+ * trace.cpp:136-197 validate_lidar, lidar_azimuth_count, scan (channel-major, azimuth ascending,
+ *                   misses omitted; points in the sensor frame). */
+typedef struct gsim_lidar {
+    const double* channels; /* elevation angles, radians */
+    uint64_t n_channels;
+    double azimuth_step;    /* radians; must divide 2*pi into an integer ray count */
+    double max_range;       /* metres */
+    gsim_rigid pose;        /* sensor -> world */
+    double alpha_threshold; /* accumulated alpha declaring a surface, (0, 1] */
+    int32_t env;            /* environment whose nodes the sensor sees (as gsim_camera.env) */
+    int32_t reserved;
+} gsim_lidar;
+
+/* GaussianBvh::build(field, nodes).scan(lidar). points: 3 * capacity doubles (x, y, z in the
+ * sensor frame), ring: capacity, azimuth: capacity (radians); *count = returns. The arrays are
+ * written when *count <= capacity (call with capacity 0 to size them). */
+int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                        uint64_t n_nodes, const gsim_lidar* lidar, double* points, uint32_t* ring,
+                        double* azimuth, uint64_t capacity, uint64_t* count);
+
+/* GaussianBvh::trace for n arbitrary rays (origin, unit direction, t_max per ray; host arrays):
+ * hit, depth (renormalised by accumulated alpha) and accumulated alpha per ray. Every primitive
+ * is a candidate of every ray here (trace_linear's scan); the LiDAR scan bins them instead. */
+int gsim_gpu_trace_rays(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                        uint64_t n_nodes, const double* origins, const double* directions,
+                        const double* t_max, uint64_t n_rays, double alpha_threshold,
+                        uint8_t* hit, double* depth, double* accum_alpha);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1103,3 +1103,211 @@ int gso_gaussians_to_tsdf(const gsim_field_view* field, double voxel_size, gsim_
     free(depth);
     return st;
 }
+
+
+/* ---- LiDAR (trace.cpp) ------------------------------------------------------------------- */
+
+typedef struct {
+    v3 mean;
+    mat3 inv_cov;
+    double opacity;
+    v3 lo, hi;
+    int seen;
+} posed_t;
+
+static const double kTraceScaleFloor = 1e-7; /* trace.hpp:24 */
+
+static posed_t pose_primitive(const gsim_field_view* f, uint64_t i, const gsim_rigid* pose) {
+    /* trace.cpp:14-36 */
+    posed_t o;
+    const double* pm = f->means + i * f->means_stride;
+    const double* ps = f->scales + i * f->scales_stride;
+    const double* pq = f->rotations + i * f->rotations_stride;
+    o.mean = rigid_apply(pose, v3_make(pm[0], pm[1], pm[2]));
+    o.opacity = f->opacities[i * f->opacities_stride];
+    const quat rot = q_mul(rigid_q(pose), q_make(pq[0], pq[1], pq[2], pq[3]));
+    const mat3 r = q_to_matrix(rot);
+    const mat3 rt = m3_transposed(&r);
+    /* std::max(scale, kTraceScaleFloor) */
+    const double sx = (ps[0] < kTraceScaleFloor) ? kTraceScaleFloor : ps[0];
+    const double sy = (ps[1] < kTraceScaleFloor) ? kTraceScaleFloor : ps[1];
+    const double sz = (ps[2] < kTraceScaleFloor) ? kTraceScaleFloor : ps[2];
+    const mat3 di = m3_diag(1.0 / (sx * sx), 1.0 / (sy * sy), 1.0 / (sz * sz));
+    const mat3 rdi = m3_mul(&r, &di);
+    o.inv_cov = m3_mul(&rdi, &rt);
+    const mat3 d = m3_diag(ps[0] * ps[0], ps[1] * ps[1], ps[2] * ps[2]);
+    const mat3 rd = m3_mul(&r, &d);
+    const mat3 cov = m3_mul(&rd, &rt);
+    const double hx = kBoundsSigma * sqrt(cov.m[0]), hy = kBoundsSigma * sqrt(cov.m[4]),
+                 hz = kBoundsSigma * sqrt(cov.m[8]);
+    const v3 a = v3_make(o.mean.x - hx, o.mean.y - hy, o.mean.z - hz);
+    const v3 b = v3_make(o.mean.x + hx, o.mean.y + hy, o.mean.z + hz);
+    o.lo = v3_make(fmin(fmin(INFINITY, a.x), b.x), fmin(fmin(INFINITY, a.y), b.y),
+                   fmin(fmin(INFINITY, a.z), b.z));
+    o.hi = v3_make(fmax(fmax(-INFINITY, a.x), b.x), fmax(fmax(-INFINITY, a.y), b.y),
+                   fmax(fmax(-INFINITY, a.z), b.z));
+    o.seen = 1;
+    return o;
+}
+
+static int ray_aabb_hit(v3 lo, v3 hi, v3 origin, v3 inv, double t_max) { /* bvh.hpp:20-36 */
+    double t0 = 0.0, t1 = t_max;
+    const double tx0 = (lo.x - origin.x) * inv.x, tx1 = (hi.x - origin.x) * inv.x;
+    t0 = fmax(t0, fmin(tx0, tx1));
+    t1 = fmin(t1, fmax(tx0, tx1));
+    const double ty0 = (lo.y - origin.y) * inv.y, ty1 = (hi.y - origin.y) * inv.y;
+    t0 = fmax(t0, fmin(ty0, ty1));
+    t1 = fmin(t1, fmax(ty0, ty1));
+    const double tz0 = (lo.z - origin.z) * inv.z, tz1 = (hi.z - origin.z) * inv.z;
+    t0 = fmax(t0, fmin(tz0, tz1));
+    t1 = fmin(t1, fmax(tz0, tz1));
+    return t0 <= t1;
+}
+
+static v3 m3_apply(const mat3* m, v3 v) { /* Mat3 * Vec3, math.hpp:87-90 */
+    return v3_make(m->m[0] * v.x + m->m[1] * v.y + m->m[2] * v.z,
+                   m->m[3] * v.x + m->m[4] * v.y + m->m[5] * v.z,
+                   m->m[6] * v.x + m->m[7] * v.y + m->m[8] * v.z);
+}
+
+typedef struct { double t, response; uint32_t index; } cand_t;
+
+static int cand_cmp(const void* pa, const void* pb) { /* trace.cpp:66-68 */
+    const cand_t* a = (const cand_t*)pa;
+    const cand_t* b = (const cand_t*)pb;
+    if (a->t != b->t) return a->t < b->t ? -1 : 1;
+    return a->index < b->index ? -1 : (a->index > b->index ? 1 : 0);
+}
+
+static void trace_one(const posed_t* posed, uint64_t n, v3 origin, v3 dir, double t_max,
+                      double alpha_threshold, cand_t* buf, uint8_t* hit, double* depth,
+                      double* accum) {
+    /* trace_linear (trace.cpp:125-134) + ray_gaussian_peak (:38-49) + composite (:65-85) */
+    const v3 inv = v3_make(1.0 / dir.x, 1.0 / dir.y, 1.0 / dir.z);
+    uint64_t nc = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const posed_t* p = &posed[i];
+        if (!p->seen) continue;
+        if (!ray_aabb_hit(p->lo, p->hi, origin, inv, t_max)) continue;
+        const v3 to_mean = v3_sub(p->mean, origin);
+        const v3 si_d = m3_apply(&p->inv_cov, dir);
+        const double denom = v3_dot(dir, si_d);
+        cand_t c = {0.0, 0.0, (uint32_t)i};
+        if (denom > 0.0) {
+            c.t = clampd(v3_dot(to_mean, si_d) / denom, 0.0, t_max);
+            const v3 delta = v3_sub(v3_add(origin, v3_scale(dir, c.t)), p->mean);
+            const double q = v3_dot(delta, m3_apply(&p->inv_cov, delta));
+            c.response = p->opacity * exp(-0.5 * q);
+        }
+        buf[nc++] = c;
+    }
+    qsort(buf, nc, sizeof(cand_t), cand_cmp);
+    double depth_sum = 0.0, acc = 0.0, transmittance = 1.0;
+    for (uint64_t k = 0; k < nc; ++k) {
+        const double alpha = buf[k].response < 0.99 ? buf[k].response : 0.99;
+        if (alpha < 1.0 / 255.0) continue;
+        const double w = alpha * transmittance;
+        depth_sum += buf[k].t * w;
+        acc += w;
+        transmittance *= 1.0 - alpha;
+        if (transmittance < 1e-4) break;
+    }
+    *accum = acc;
+    *hit = acc >= alpha_threshold;
+    *depth = *hit ? depth_sum / acc : 0.0;
+}
+
+static posed_t* pose_all(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+                         int env, int* status) {
+    /* GaussianBvh::build, trace.cpp:88-111 */
+    const uint64_t n = field->count;
+    int64_t* pose_of = (int64_t*)malloc((n ? n : 1) * sizeof(int64_t));
+    for (uint64_t i = 0; i < n; ++i) pose_of[i] = -1;
+    for (uint64_t k = 0; k < n_nodes; ++k) {
+        if (nodes[k].end > n) { free(pose_of); *status = GSIM_ERR_VALIDATION; return NULL; }
+        for (uint64_t i = nodes[k].begin; i < nodes[k].end; ++i) pose_of[i] = (int64_t)k;
+    }
+    gsim_rigid identity;
+    memset(&identity, 0, sizeof(identity));
+    identity.rotation[0] = 1.0;
+    posed_t* posed = (posed_t*)malloc((n ? n : 1) * sizeof(posed_t));
+    for (uint64_t i = 0; i < n; ++i) {
+        const int64_t k = pose_of[i];
+        posed[i] = pose_primitive(field, i, k >= 0 ? &nodes[k].pose : &identity);
+        if (k >= 0 && nodes[k].env >= 0 && nodes[k].env != env) posed[i].seen = 0;
+    }
+    free(pose_of);
+    *status = GSIM_OK;
+    return posed;
+}
+
+int gso_trace_rays(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+                   const double* origins, const double* directions, const double* t_max,
+                   uint64_t n_rays, double alpha_threshold, uint8_t* hit, double* depth,
+                   double* accum_alpha) {
+    int st;
+    posed_t* posed = pose_all(field, nodes, n_nodes, -1, &st);
+    if (!posed) return st;
+    cand_t* buf = (cand_t*)malloc((field->count ? field->count : 1) * sizeof(cand_t));
+    for (uint64_t r = 0; r < n_rays; ++r)
+        trace_one(posed, field->count,
+                  v3_make(origins[3 * r], origins[3 * r + 1], origins[3 * r + 2]),
+                  v3_make(directions[3 * r], directions[3 * r + 1], directions[3 * r + 2]),
+                  t_max[r], alpha_threshold, buf, &hit[r], &depth[r], &accum_alpha[r]);
+    free(buf);
+    free(posed);
+    return GSIM_OK;
+}
+
+static int validate_lidar(const gsim_lidar* l) { /* trace.cpp:136-155 */
+    if (l->n_channels == 0) return GSIM_ERR_VALIDATION;
+    for (uint64_t c = 0; c < l->n_channels; ++c)
+        if (!isfinite(l->channels[c])) return GSIM_ERR_VALIDATION;
+    if (!(l->azimuth_step > 0.0)) return GSIM_ERR_VALIDATION;
+    const double n = 2.0 * kPiD / l->azimuth_step;
+    if (fabs(n - round(n)) * l->azimuth_step > 1e-9) return GSIM_ERR_VALIDATION;
+    if (!(l->max_range > 0.0)) return GSIM_ERR_VALIDATION;
+    if (!(l->alpha_threshold > 0.0) || l->alpha_threshold > 1.0) return GSIM_ERR_VALIDATION;
+    return GSIM_OK;
+}
+
+int gso_lidar_scan(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+                   const gsim_lidar* lidar, double* points, uint32_t* ring, double* azimuth,
+                   uint64_t capacity, uint64_t* count) {
+    /* GaussianBvh::build (trace.cpp:88-111) then scan (:169-197) */
+    int st;
+    posed_t* posed = pose_all(field, nodes, n_nodes, lidar->env, &st);
+    if (!posed) return st;
+    st = validate_lidar(lidar);
+    if (st != GSIM_OK) { free(posed); return st; }
+    const uint64_t azimuths = (uint64_t)llround(2.0 * kPiD / lidar->azimuth_step);
+    const uint64_t rays = lidar->n_channels * azimuths;
+    cand_t* buf = (cand_t*)malloc((field->count ? field->count : 1) * sizeof(cand_t));
+    const quat sq = rigid_q(&lidar->pose);
+    const v3 origin = rigid_t(&lidar->pose);
+    uint64_t hits = 0;
+    for (uint64_t k = 0; k < rays; ++k) {
+        const uint64_t channel = k / azimuths, step = k % azimuths;
+        const double elevation = lidar->channels[channel];
+        const double az = (double)step * lidar->azimuth_step;
+        const double ce = cos(elevation);
+        const v3 dir_sensor = v3_make(ce * cos(az), ce * sin(az), sin(elevation));
+        const v3 dir = q_rotate(sq, dir_sensor);
+        uint8_t h;
+        double d, a;
+        trace_one(posed, field->count, origin, dir, lidar->max_range, lidar->alpha_threshold, buf,
+                  &h, &d, &a);
+        if (!h) continue;
+        if (hits < capacity) {
+            const v3 p = v3_scale(dir_sensor, d);
+            points[3 * hits] = p.x; points[3 * hits + 1] = p.y; points[3 * hits + 2] = p.z;
+            ring[hits] = (uint32_t)channel;
+            azimuth[hits] = az;
+        }
+        ++hits;
+    }
+    free(buf);
+    free(posed);
+    *count = hits;
+    return GSIM_OK;
+}

@@ -20,6 +20,8 @@
  *   load_splat_ply   splat_ply.cpp:40-162 (status only: 1 io, 2 format/validation)
  *   GS -> TSDF: field_bounds, render_depth_ring, TsdfVolume::create, tsdf_fuse,
  *       gaussians_to_mesh up to the fused volume   transfer.cpp:27-34, 81-198
+ *   LiDAR: pose_primitive, ray_aabb_hit, ray_gaussian_peak, composite, trace_linear,
+ *       validate_lidar, GaussianBvh::scan   trace.cpp:14-197, bvh.hpp:20-36
  *
  * Parity pin: tests/test_oracle_pin.py checks every function against the reference itself
  * (oracle/_ref/libgsim_ref.so, compiled from /root/reference sources by oracle/Makefile) and
@@ -122,6 +124,19 @@ int gso_tsdf_fuse(gsim_tsdf_volume* volume, const gsim_camera* camera, const flo
                   int width, int height);
 int gso_gaussians_to_tsdf(const gsim_field_view* field, double voxel_size,
                           gsim_tsdf_volume* volume);
+
+/* ---- LiDAR (trace.cpp) ---------------------------------------------------
+ * trace_linear over every primitive (pose_primitive trace.cpp:14-36, ray_aabb_hit bvh.hpp:20-36,
+ * ray_gaussian_peak trace.cpp:38-49, composite trace.cpp:65-85) and GaussianBvh::scan
+ * (trace.cpp:169-197, validate_lidar :136-160). Nodes with env >= 0 other than the sensor's
+ * are not seen (the batched-env extension). Two-call scan like the library. */
+int gso_trace_rays(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+                   const double* origins, const double* directions, const double* t_max,
+                   uint64_t n_rays, double alpha_threshold, uint8_t* hit, double* depth,
+                   double* accum_alpha);
+int gso_lidar_scan(const gsim_field_view* field, const gsim_node* nodes, uint64_t n_nodes,
+                   const gsim_lidar* lidar, double* points, uint32_t* ring, double* azimuth,
+                   uint64_t capacity, uint64_t* count);
 
 uint64_t gso_hash_bytes(const void* data, uint64_t size, uint64_t seed);
 uint64_t gso_hash_target(const float* rgb, const float* depth, const float* alpha, int width,

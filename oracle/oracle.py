@@ -120,6 +120,12 @@ class Oracle:
         L.gso_tsdf_create.argtypes = [_dp, C.c_double, C.POINTER(C.c_int32), C.c_double, vol]
         L.gso_tsdf_fuse.argtypes = [vol, C.POINTER(abi.gsim_camera), _fp, C.c_int, C.c_int]
         L.gso_gaussians_to_tsdf.argtypes = [C.POINTER(abi.gsim_field_view), C.c_double, vol]
+        L.gso_trace_rays.argtypes = [C.POINTER(abi.gsim_field_view), C.POINTER(abi.gsim_node),
+                                     C.c_uint64, _dp, _dp, _dp, C.c_uint64, C.c_double,
+                                     C.POINTER(C.c_uint8), _dp, _dp]
+        L.gso_lidar_scan.argtypes = [C.POINTER(abi.gsim_field_view), C.POINTER(abi.gsim_node),
+                                     C.c_uint64, C.POINTER(abi.gsim_lidar), _dp, _u32p, _dp,
+                                     C.c_uint64, _u64p]
         L.gso_pose_sample.argtypes = [_dp, _dp, _dp, C.c_uint64, C.POINTER(abi.gsim_rigid), _dp,
                                       C.c_uint64, C.POINTER(abi.gsim_rigid)]
 
@@ -196,6 +202,27 @@ class Oracle:
         c = vol.to_c()
         _ok(self.lib.gso_gaussians_to_tsdf(C.byref(v), voxel_size, C.byref(c)), "gaussians_to_tsdf")
         return vol
+
+    # -- LiDAR (trace.cpp) ---------------------------------------------------------------------
+    def trace_rays(self, field: GaussianField, nodes, origins, directions, t_max, alpha_threshold=0.5):
+        """trace_linear per ray -> (hit u8, depth, accum_alpha)."""
+        o, d, t = _rays(origins, directions, t_max)
+        n = len(t)
+        hit = np.zeros(n, np.uint8); depth = np.zeros(n); acc = np.zeros(n)
+        v = field.view()
+        na = _nodes(nodes)
+        _ok(self.lib.gso_trace_rays(C.byref(v), na, len(nodes), o.ctypes.data_as(_dp),
+                                    d.ctypes.data_as(_dp), t.ctypes.data_as(_dp), n, alpha_threshold,
+                                    hit.ctypes.data_as(C.POINTER(C.c_uint8)), depth.ctypes.data_as(_dp),
+                                    acc.ctypes.data_as(_dp)), "trace_rays")
+        return hit, depth, acc
+
+    def lidar_scan(self, field: GaussianField, nodes, lidar) -> dict:
+        """GaussianBvh::scan -> {"points" (n, 3), "ring" (n,), "azimuth" (n,)}."""
+        v = field.view()
+        na = _nodes(nodes)
+        return _two_call_scan(lambda l, p, r, a, cap, cnt: self.lib.gso_lidar_scan(
+            C.byref(v), na, len(nodes), l, p, r, a, cap, cnt), lidar, "lidar_scan")
 
     # -- the path ----------------------------------------------------------------------------
     def project(self, field: GaussianField, nodes, camera) -> np.ndarray:
@@ -393,6 +420,10 @@ class Ref:
         L.ref_tsdf_create.argtypes = [_dp, C.c_double, C.POINTER(C.c_int32), C.c_double, vol]
         L.ref_tsdf_fuse.argtypes = [vol, C.POINTER(abi.gsim_camera), _fp, C.c_int, C.c_int]
         L.ref_gaussians_to_tsdf.argtypes = [_vp, C.c_double, vol]
+        L.ref_trace_rays.argtypes = [_vp, C.POINTER(abi.gsim_node), C.c_uint64, _dp, _dp, _dp,
+                                     C.c_uint64, C.c_double, C.c_int, C.POINTER(C.c_uint8), _dp, _dp]
+        L.ref_lidar_scan.argtypes = [_vp, C.POINTER(abi.gsim_node), C.c_uint64,
+                                     C.POINTER(abi.gsim_lidar), _dp, _u32p, _dp, C.c_uint64, _u64p]
 
     # -- GS -> TSDF (transfer.cpp) -------------------------------------------------------------
     def _with_field(self, field: GaussianField, fn):
@@ -436,6 +467,25 @@ class Ref:
             _ok(self.lib.ref_gaussians_to_tsdf(h, voxel_size, C.byref(c)), "ref gaussians_to_tsdf")
             return vol
         return self._with_field(field, run)
+
+    # -- LiDAR (trace.cpp) ---------------------------------------------------------------------
+    def trace_rays(self, field: GaussianField, nodes, origins, directions, t_max, alpha_threshold=0.5,
+                   linear=False):
+        o, d, t = _rays(origins, directions, t_max)
+        n = len(t)
+        hit = np.zeros(n, np.uint8); depth = np.zeros(n); acc = np.zeros(n)
+        na = _nodes(nodes)
+        _ok(self._with_field(field, lambda h: self.lib.ref_trace_rays(
+            h, na, len(nodes), o.ctypes.data_as(_dp), d.ctypes.data_as(_dp), t.ctypes.data_as(_dp), n,
+            alpha_threshold, int(linear), hit.ctypes.data_as(C.POINTER(C.c_uint8)),
+            depth.ctypes.data_as(_dp), acc.ctypes.data_as(_dp))), "ref trace_rays")
+        return hit, depth, acc
+
+    def lidar_scan(self, field: GaussianField, nodes, lidar) -> dict:
+        na = _nodes(nodes)
+        return self._with_field(field, lambda h: _two_call_scan(
+            lambda l, p, r, a, cap, cnt: self.lib.ref_lidar_scan(h, na, len(nodes), l, p, r, a, cap, cnt),
+            lidar, "ref lidar_scan"))
 
     def set_threads(self, n: int) -> None:
         self.lib.ref_set_threads(n)
@@ -617,3 +667,25 @@ def cpu_count() -> int:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+def _rays(origins, directions, t_max):
+    o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+    d = np.ascontiguousarray(directions, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, np.float64), (len(o),)))
+    return o, d, t
+
+
+def _two_call_scan(fn, lidar, what: str) -> dict:
+    """Size, then fill, a scan's point cloud through a (lidar, points, ring, azimuth, capacity,
+    count) entry point."""
+    lc = lidar.to_c() if hasattr(lidar, "to_c") else lidar
+    cnt = C.c_uint64(0)
+    z = np.zeros(1)
+    _ok(fn(C.byref(lc), z.ctypes.data_as(_dp), np.zeros(1, np.uint32).ctypes.data_as(_u32p),
+           z.ctypes.data_as(_dp), 0, C.byref(cnt)), what)
+    n = cnt.value
+    pts = np.zeros((max(n, 1), 3)); ring = np.zeros(max(n, 1), np.uint32); az = np.zeros(max(n, 1))
+    _ok(fn(C.byref(lc), pts.ctypes.data_as(_dp), ring.ctypes.data_as(_u32p), az.ctypes.data_as(_dp),
+           n, C.byref(cnt)), what)
+    return {"points": pts[:n], "ring": ring[:n], "azimuth": az[:n]}

@@ -18,6 +18,7 @@
 //   gsim::load_splat_ply / save_splat_ply                   splat_ply.hpp:20-24
 //   gsim::render_depth_ring / TsdfVolume::create / tsdf_fuse / gaussians_to_mesh
 //                                                           transfer.hpp:33-90
+//   gsim::GaussianBvh::build / trace / trace_linear / scan  trace.hpp:66-82
 // Used by tests/test_oracle_pin.py (pin the C restatement), tests/golden/make_golden.py and
 // bench.py --impl reference (the reference's CPU renderer timed on the host cores).
 #include <cstring>
@@ -31,6 +32,7 @@
 #include "gsim/image_io.hpp"
 #include "gsim/pose_stream.hpp"
 #include "gsim/splat_ply.hpp"
+#include "gsim/trace.hpp"
 #include "gsim/transfer.hpp"
 #include "png.h"
 #include "gsim/parallel.hpp"
@@ -470,6 +472,54 @@ int ref_gaussians_to_tsdf(void* field, double voxel_size, gsim_tsdf_volume* vol)
         gaussians_to_mesh(*static_cast<GaussianField*>(field), voxel_size,
                           std::numeric_limits<std::size_t>::max(), &v);
         copy_volume_out(v, vol);
+    });
+}
+
+// ---- LiDAR (trace.cpp) --------------------------------------------------------------------------
+// GaussianBvh::build + trace (BVH) for every ray; `linear` selects trace_linear instead.
+int ref_trace_rays(void* field, const gsim_node* nodes, std::uint64_t n_nodes, const double* origins,
+                   const double* dirs, const double* t_max, std::uint64_t n, double alpha_threshold,
+                   int linear, std::uint8_t* hit, double* depth, double* acc) {
+    return guarded([&] {
+        const GaussianBvh bvh = GaussianBvh::build(*static_cast<GaussianField*>(field),
+                                                   to_nodes(nodes, n_nodes));
+        for (std::uint64_t r = 0; r < n; ++r) {
+            Ray ray;
+            ray.origin = to_vec(origins + 3 * r);
+            ray.direction = to_vec(dirs + 3 * r);
+            ray.t_max = t_max[r];
+            const TraceResult t = linear ? bvh.trace_linear(ray, alpha_threshold)
+                                         : bvh.trace(ray, alpha_threshold);
+            hit[r] = t.hit ? 1 : 0;
+            depth[r] = t.depth;
+            acc[r] = t.accum_alpha;
+        }
+    });
+}
+
+int ref_lidar_scan(void* field, const gsim_node* nodes, std::uint64_t n_nodes, const gsim_lidar* l,
+                   double* points, std::uint32_t* ring, double* azimuth, std::uint64_t capacity,
+                   std::uint64_t* count) {
+    return guarded([&] {
+        const GaussianBvh bvh = GaussianBvh::build(*static_cast<GaussianField*>(field),
+                                                   to_nodes(nodes, n_nodes));
+        LidarModel m;
+        m.id = "lidar";
+        m.channels.assign(l->channels, l->channels + l->n_channels);
+        m.azimuth_step = l->azimuth_step;
+        m.max_range = l->max_range;
+        m.pose = to_rigid(l->pose);
+        m.alpha_threshold = l->alpha_threshold;
+        const PointCloud c = bvh.scan(m);
+        *count = c.size();
+        if (c.size() > capacity) return;
+        for (std::size_t k = 0; k < c.size(); ++k) {
+            points[3 * k] = c.points[k].x;
+            points[3 * k + 1] = c.points[k].y;
+            points[3 * k + 2] = c.points[k].z;
+            ring[k] = c.ring[k];
+            azimuth[k] = c.azimuth[k];
+        }
     });
 }
 

@@ -10,6 +10,7 @@ from .api import (  # noqa: F401
     EncodeOptions,
     GaussianField,
     IoError,
+    LidarModel,
     NodeKind,
     PoseTracks,
     RasterOptions,
@@ -33,7 +34,7 @@ from .api import (  # noqa: F401
 from .abi import SPLAT_DTYPE, load_library  # noqa: F401
 
 __all__ = [
-    "CameraModel", "Context", "EncodeOptions", "GaussianField", "IoError", "NodeKind", "PoseTracks", "RasterOptions",
+    "CameraModel", "Context", "EncodeOptions", "GaussianField", "IoError", "LidarModel", "NodeKind", "PoseTracks", "RasterOptions",
     "RenderTarget", "RigidTransform", "Scene", "SceneNode", "TsdfVolume", "ValidationError",
     "SPLAT_DTYPE", "depth_ring_cameras", "tsdf_create",
     "default_context", "io_error", "load_library", "project", "quat_from_axis_angle",

@@ -94,6 +94,12 @@ class gsim_tsdf_volume(C.Structure):
                 ("tsdf", C.POINTER(C.c_double)), ("weights", C.POINTER(C.c_double))]
 
 
+class gsim_lidar(C.Structure):
+    _fields_ = [("channels", C.POINTER(C.c_double)), ("n_channels", C.c_uint64),
+                ("azimuth_step", C.c_double), ("max_range", C.c_double), ("pose", gsim_rigid),
+                ("alpha_threshold", C.c_double), ("env", C.c_int32), ("reserved", C.c_int32)]
+
+
 # numpy view of gsim_projected_splat (ProjectedSplat, raster.hpp:20-29), 120 bytes
 SPLAT_DTYPE = np.dtype([
     ("pixel_center", "<f8", (2,)), ("cov_xx", "<f8"), ("cov_xy", "<f8"), ("cov_yy", "<f8"),
@@ -172,6 +178,13 @@ SIGNATURES = [
     ("gsim_gpu_tsdf_free", C.c_int, [C.POINTER(gsim_tsdf_volume)]),
     ("gsim_gpu_tsdf_download", C.c_int, [_P, C.POINTER(gsim_tsdf_volume), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]),
+    ("gsim_gpu_lidar_scan", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64, C.POINTER(gsim_lidar),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_double), C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("gsim_gpu_trace_rays", C.c_int, [_P, _P, C.POINTER(gsim_node), C.c_uint64, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_uint64,
+                                      C.c_double, C.POINTER(C.c_uint8), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]),
     ("gsim_gpu_tsdf_upload", C.c_int, [_P, C.POINTER(gsim_tsdf_volume), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]),
 ]

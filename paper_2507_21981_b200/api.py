@@ -390,6 +390,35 @@ class TsdfVolume:
         return TsdfVolume(tuple(v.origin), v.voxel_size, tuple(v.dims), v.truncation)
 
 
+class LidarModel:
+    """LidarModel (trace.hpp:47-54): spinning scan, one ray per (channel elevation, azimuth step);
+    pose maps sensor -> world."""
+
+    def __init__(self, channels, azimuth_step: float, max_range: float,
+                 pose: "RigidTransform | None" = None, alpha_threshold: float = 0.5, env: int = -1):
+        self.channels = np.ascontiguousarray(channels, dtype=np.float64).reshape(-1)
+        self.azimuth_step = float(azimuth_step)
+        self.max_range = float(max_range)
+        self.pose = pose or RigidTransform()
+        self.alpha_threshold = float(alpha_threshold)
+        self.env = int(env)
+
+    def azimuth_count(self) -> int:  # lidar_azimuth_count, trace.cpp:162-164
+        return int(round(2.0 * math.pi / self.azimuth_step))
+
+    def to_c(self) -> abi.gsim_lidar:
+        c = abi.gsim_lidar()
+        c.channels = self.channels.ctypes.data_as(C.POINTER(C.c_double))
+        c.n_channels = len(self.channels)
+        c.azimuth_step = self.azimuth_step
+        c.max_range = self.max_range
+        c.pose = self.pose.to_c()
+        c.alpha_threshold = self.alpha_threshold
+        c.env = self.env
+        c._keep = self.channels  # the C struct points into this array
+        return c
+
+
 def _nodes_array(nodes: Sequence[SceneNode]):
     arr = (abi.gsim_node * max(len(nodes), 1))()
     for k, n in enumerate(nodes):
@@ -736,6 +765,41 @@ class Context:
         _check(self.lib.gsim_gpu_gaussians_to_tsdf(self.ptr, scene.handle, voxel_size, C.byref(c)),
                self.ptr)
         return vol
+
+    # -- LiDAR (trace.cpp) --------------------------------------------------
+    def lidar_scan(self, scene: Scene, nodes, lidar: "LidarModel") -> dict:
+        """GaussianBvh::build(field, nodes).scan(lidar) -> {"points" (n, 3) sensor frame,
+        "ring" (n,), "azimuth" (n,)} in channel-major, azimuth-ascending order, misses omitted."""
+        na = _nodes_array(nodes)
+        lc = lidar.to_c()
+        cnt = C.c_uint64(0)
+        dp, u32p = C.POINTER(C.c_double), C.POINTER(C.c_uint32)
+        z = np.zeros(1)
+        zr = np.zeros(1, np.uint32)
+        _check(self.lib.gsim_gpu_lidar_scan(self.ptr, scene.handle, na, len(nodes), C.byref(lc),
+                                            z.ctypes.data_as(dp), zr.ctypes.data_as(u32p),
+                                            z.ctypes.data_as(dp), 0, C.byref(cnt)), self.ptr)
+        n = cnt.value
+        pts = np.zeros((max(n, 1), 3)); ring = np.zeros(max(n, 1), np.uint32); az = np.zeros(max(n, 1))
+        _check(self.lib.gsim_gpu_lidar_scan(self.ptr, scene.handle, na, len(nodes), C.byref(lc),
+                                            pts.ctypes.data_as(dp), ring.ctypes.data_as(u32p),
+                                            az.ctypes.data_as(dp), n, C.byref(cnt)), self.ptr)
+        return {"points": pts[:n], "ring": ring[:n], "azimuth": az[:n]}
+
+    def trace_rays(self, scene: Scene, nodes, origins, directions, t_max, alpha_threshold: float = 0.5):
+        """GaussianBvh::trace per ray -> (hit u8, depth, accum_alpha)."""
+        o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+        d = np.ascontiguousarray(directions, dtype=np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, np.float64), (len(o),)))
+        n = len(t)
+        hit = np.zeros(max(n, 1), np.uint8); depth = np.zeros(max(n, 1)); acc = np.zeros(max(n, 1))
+        dp = C.POINTER(C.c_double)
+        na = _nodes_array(nodes)
+        _check(self.lib.gsim_gpu_trace_rays(self.ptr, scene.handle, na, len(nodes), o.ctypes.data_as(dp),
+                                            d.ctypes.data_as(dp), t.ctypes.data_as(dp), n,
+                                            alpha_threshold, hit.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                            depth.ctypes.data_as(dp), acc.ctypes.data_as(dp)), self.ptr)
+        return hit[:n], depth[:n], acc[:n]
 
     def tile_lists(self, camera: int):
         """Sorted per-tile lists of `camera` from the last render (tile offsets, indices)."""

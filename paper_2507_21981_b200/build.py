@@ -31,6 +31,7 @@ SOURCES = {
     "tracks.cu": ["-fmad=false"],
     "ply.cu": ["-fmad=false"],
     "transfer.cu": ["-fmad=false"],
+    "lidar.cu": ["-fmad=false"],
     "host.cu": [],
 }
 DEPS = ["common.cuh", "kernels.hpp", "encode.cuh"]

@@ -194,6 +194,23 @@ struct gsim_gpu_context {
     DevBuf<DevFuseView> fuse_views;
     DevBuf<float> depth_in;          // host depth maps staged for tsdf_fuse
     float frame_valid_alpha = 0.0f;  // render_depth_ring's depth mask (raster epilogue)
+    // LiDAR scratch (lidar.cu)
+    struct {
+        DevBuf<double> posed, rays, depth, acc, points, azimuth, rank_elev;
+        DevBuf<uint8_t> seen, ray_all;
+        DevBuf<LidarRect> rects;
+        DevBuf<uint32_t> all_list, counts, list, hit, ring, rank_channel;
+        DevBuf<int> diff;
+        DevBuf<unsigned long long> offsets, cursor, scratch, hit_offsets;
+        DevBuf<DevSegment> segs;
+        void release() {
+            posed.release(); rays.release(); depth.release(); acc.release(); points.release();
+            azimuth.release(); rank_elev.release(); seen.release(); ray_all.release();
+            rects.release(); all_list.release(); counts.release(); list.release(); hit.release();
+            ring.release(); rank_channel.release(); diff.release(); offsets.release();
+            cursor.release(); scratch.release(); hit_offsets.release(); segs.release();
+        }
+    } lidar;
 
     uint32_t epoch = 0;
     uint64_t launches_total = 0;
@@ -1239,6 +1256,89 @@ void fuse_views(gsim_gpu_context* ctx, const gsim_tsdf_volume* vol,
     GSIM_CK(cudaStreamSynchronize(ctx->stream));
 }
 
+// ---- LiDAR helpers (trace.cpp) ---------------------------------------------------------------
+
+// GaussianBvh::build's node painting (trace.cpp:93-102: later nodes overwrite, range check) as
+// maximal segments; entry_count marks whether the sensor sees the segment (env filter).
+std::vector<DevSegment> paint_segments(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
+                                       int32_t env) {
+    for (uint64_t k = 0; k < n_nodes; ++k)
+        if (nodes[k].end > n_prims)
+            throw ValidationError{"node " + std::to_string(k) + " range exceeds field size"};
+    std::vector<uint64_t> pts{0, n_prims};
+    for (uint64_t k = 0; k < n_nodes; ++k)
+        if (nodes[k].begin < nodes[k].end) {
+            pts.push_back(nodes[k].begin);
+            pts.push_back(nodes[k].end);
+        }
+    std::sort(pts.begin(), pts.end());
+    pts.erase(std::unique(pts.begin(), pts.end()), pts.end());
+    std::vector<DevSegment> segs;
+    for (size_t k = 0; k + 1 < pts.size(); ++k) {
+        if (!(pts[k] < pts[k + 1])) continue;
+        int64_t owner = -1;
+        for (uint64_t j = 0; j < n_nodes; ++j)
+            if (nodes[j].begin <= pts[k] && pts[k] < nodes[j].end) owner = int64_t(j);
+        DevSegment sg{};
+        sg.begin = pts[k];
+        sg.end = pts[k + 1];
+        const gsim_rigid id{{1.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        const gsim_rigid& pose = owner >= 0 ? nodes[owner].pose : id;
+        for (int c = 0; c < 4; ++c) sg.q[c] = pose.rotation[c];
+        for (int c = 0; c < 3; ++c) sg.t[c] = pose.translation[c];
+        sg.entry_count = (owner >= 0 && nodes[owner].env >= 0 && nodes[owner].env != env) ? 0u : 1u;
+        segs.push_back(sg);
+    }
+    if (segs.empty()) {
+        DevSegment sg{};
+        sg.q[0] = 1.0;
+        segs.push_back(sg);
+    }
+    return segs;
+}
+
+void validate_lidar(const gsim_lidar& l) {  // trace.cpp:136-155
+    constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
+    if (l.n_channels == 0 || !l.channels) throw ValidationError{"lidar: no channels"};
+    for (uint64_t c = 0; c < l.n_channels; ++c)
+        if (!std::isfinite(l.channels[c])) throw ValidationError{"lidar: non-finite elevation"};
+    if (!(l.azimuth_step > 0.0)) throw ValidationError{"lidar: azimuth_step must be positive"};
+    const double n = kTwoPi / l.azimuth_step;
+    if (std::abs(n - std::round(n)) * l.azimuth_step > 1e-9)
+        throw ValidationError{"lidar: azimuth_step must divide 2*pi into an integer ray count"};
+    if (!(l.max_range > 0.0)) throw ValidationError{"lidar: max_range must be positive"};
+    if (!(l.alpha_threshold > 0.0) || l.alpha_threshold > 1.0)
+        throw ValidationError{"lidar: alpha_threshold outside (0,1]"};
+}
+
+LidarArgs lidar_pose_stage(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                           uint64_t n_nodes, int32_t env, bool scan) {
+    auto& L = ctx->lidar;
+    const uint64_t n = scene->f.n;
+    const std::vector<DevSegment> segs = paint_segments(n, nodes, n_nodes, env);
+    L.segs.reserve(segs.size());
+    GSIM_CK(cudaMemcpyAsync(L.segs.ptr, segs.data(), segs.size() * sizeof(DevSegment),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    L.posed.reserve(std::max<uint64_t>(19 * n, 1));
+    L.seen.reserve(std::max<uint64_t>(n, 1));
+    L.rects.reserve(std::max<uint64_t>(n, 1));
+    L.all_list.reserve(std::max<uint64_t>(n, 1) + 1);
+    LidarArgs a{};
+    a.field = scene->f;
+    a.segs = L.segs.ptr;
+    a.n_segs = int(segs.size());
+    a.scan = scan ? 1 : 0;
+    a.n = n;
+    a.posed = L.posed.ptr;
+    a.seen = L.seen.ptr;
+    a.rects = L.rects.ptr;
+    a.all_count = L.all_list.ptr;      // [0] = count
+    a.all_list = L.all_list.ptr + 1;
+    a.two_pi = 2.0 * 3.14159265358979323846;
+    GSIM_CK(cudaMemsetAsync(a.all_count, 0, sizeof(uint32_t), ctx->stream));
+    return a;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1319,6 +1419,7 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->full_vis.release();
     ctx->splats_in.release();
     ctx->bounds_buf.release();
+    ctx->lidar.release();
     ctx->fuse_views.release();
     ctx->depth_in.release();
     ctx->readback.release();
@@ -2111,6 +2212,200 @@ int gsim_gpu_gaussians_to_tsdf(gsim_gpu_context* ctx, const gsim_gpu_scene* scen
         std::vector<DevFuseView> views(cams.size());
         for (size_t k = 0; k < cams.size(); ++k) views[k] = fuse_view(cams[k], off[k] + 3 * npx);
         fuse_views(ctx, volume, views, ctx->out.ptr);
+    });
+}
+
+// ---- LiDAR (trace.cpp) -----------------------------------------------------
+
+int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                        uint64_t n_nodes, const gsim_lidar* lidar, double* points, uint32_t* ring,
+                        double* azimuth, uint64_t capacity, uint64_t* count) {
+    return Guard(ctx).run([&] {
+        if (!scene || !lidar || !count || (n_nodes && !nodes))
+            throw ValidationError{"lidar_scan: null argument"};
+        auto& L = ctx->lidar;
+        cudaStream_t s = ctx->stream;
+        // GaussianBvh::build validates the nodes before scan validates the sensor
+        LidarArgs a = lidar_pose_stage(ctx, scene, nodes, n_nodes, lidar->env, true);
+        validate_lidar(*lidar);
+        constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
+        const uint64_t n_az = uint64_t(std::llround(kTwoPi / lidar->azimuth_step));
+        const uint64_t n_ch = lidar->n_channels;
+        const uint64_t n_rays = n_ch * n_az;
+        if (n_az == 0 || n_az > (1u << 30) || n_ch > 65535)
+            throw ValidationError{"lidar: ray grid too large"};
+        // rays exactly as GaussianBvh::scan builds them (trace.cpp:180-189), on the host
+        const dq sq{lidar->pose.rotation[0], lidar->pose.rotation[1], lidar->pose.rotation[2],
+                    lidar->pose.rotation[3]};
+        std::vector<double> rays(6 * n_rays);
+        for (uint64_t k = 0; k < n_rays; ++k) {
+            const double elevation = lidar->channels[k / n_az];
+            const double az = static_cast<double>(k % n_az) * lidar->azimuth_step;
+            const double ce = std::cos(elevation);
+            const dv3 ds = mk3(ce * std::cos(az), ce * std::sin(az), std::sin(elevation));
+            const dv3 dw = qrotate(sq, ds);
+            double* r = rays.data() + 6 * k;
+            r[0] = dw.x; r[1] = dw.y; r[2] = dw.z;
+            r[3] = ds.x; r[4] = ds.y; r[5] = ds.z;
+        }
+        // regular channels (cos(elevation) clearly positive) bin by elevation rank; rays of the
+        // others take every primitive as a candidate
+        std::vector<std::pair<double, uint32_t>> reg;
+        std::vector<uint8_t> ray_all(n_ch, 0);
+        for (uint64_t c = 0; c < n_ch; ++c) {
+            const double e = lidar->channels[c];
+            if (std::cos(e) > 1e-3) reg.push_back({e, uint32_t(c)});
+            else ray_all[c] = 1;
+        }
+        std::sort(reg.begin(), reg.end());
+        std::vector<double> rank_elev;
+        std::vector<uint32_t> rank_channel;
+        for (const auto& r : reg) {
+            rank_elev.push_back(r.first);
+            rank_channel.push_back(r.second);
+        }
+        L.rays.reserve(std::max<uint64_t>(6 * n_rays, 1));
+        // split the interleaved host rays into the two device planes
+        std::vector<double> dw(3 * n_rays), ds(3 * n_rays);
+        for (uint64_t k = 0; k < n_rays; ++k)
+            for (int c = 0; c < 3; ++c) {
+                dw[3 * k + c] = rays[6 * k + c];
+                ds[3 * k + c] = rays[6 * k + 3 + c];
+            }
+        GSIM_CK(cudaMemcpyAsync(L.rays.ptr, dw.data(), dw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        GSIM_CK(cudaMemcpyAsync(L.rays.ptr + 3 * n_rays, ds.data(), ds.size() * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+        L.ray_all.reserve(n_ch);
+        GSIM_CK(cudaMemcpyAsync(L.ray_all.ptr, ray_all.data(), n_ch, cudaMemcpyHostToDevice, s));
+        L.rank_elev.reserve(std::max<size_t>(rank_elev.size(), 1));
+        L.rank_channel.reserve(std::max<size_t>(rank_channel.size(), 1));
+        if (!rank_elev.empty()) {
+            GSIM_CK(cudaMemcpyAsync(L.rank_elev.ptr, rank_elev.data(), rank_elev.size() * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+            GSIM_CK(cudaMemcpyAsync(L.rank_channel.ptr, rank_channel.data(),
+                                    rank_channel.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        }
+        // world -> sensor pose (RigidTransform::inverse, math.hpp:235-238)
+        const dq wq{sq.w, -sq.x, -sq.y, -sq.z};
+        const dv3 wt = qrotate(wq, mk3(lidar->pose.translation[0], lidar->pose.translation[1],
+                                       lidar->pose.translation[2]));
+        a.w2s_q[0] = wq.w; a.w2s_q[1] = wq.x; a.w2s_q[2] = wq.y; a.w2s_q[3] = wq.z;
+        a.w2s_t[0] = -wt.x; a.w2s_t[1] = -wt.y; a.w2s_t[2] = -wt.z;
+        for (int c = 0; c < 3; ++c) a.origin[c] = lidar->pose.translation[c];
+        a.max_range = lidar->max_range;
+        a.step = lidar->azimuth_step;
+        a.rank_elev = L.rank_elev.ptr;
+        a.rank_channel = L.rank_channel.ptr;
+        a.n_ranks = int(rank_elev.size());
+        a.n_az = uint32_t(n_az);
+        a.n_rays = n_rays;
+        a.ray_dir = L.rays.ptr;
+        a.ray_dir_sensor = L.rays.ptr + 3 * n_rays;
+        a.ray_all = L.ray_all.ptr;
+        a.alpha_threshold = lidar->alpha_threshold;
+        launch_lidar_pose(a, ctx->num_sms, s);
+        check_launch();
+        // bin: row differences -> candidates per ray -> offsets -> candidate lists
+        L.diff.reserve(n_ch * (n_az + 1));
+        GSIM_CK(cudaMemsetAsync(L.diff.ptr, 0, n_ch * (n_az + 1) * sizeof(int), s));
+        a.diff = L.diff.ptr;
+        launch_lidar_count(a, ctx->num_sms, s);
+        check_launch();
+        L.counts.reserve(n_rays);
+        a.ray_count = L.counts.ptr;
+        launch_lidar_rowscan(a, uint32_t(n_ch), s);
+        check_launch();
+        L.offsets.reserve(n_rays + 1);
+        L.scratch.reserve((n_rays + 1023) / 1024 + 2);
+        exclusive_scan_u32(L.counts.ptr, n_rays, L.offsets.ptr, L.scratch.ptr, s);
+        check_launch();
+        unsigned long long pairs = 0;
+        GSIM_CK(cudaMemcpyAsync(&pairs, L.offsets.ptr + n_rays, sizeof(pairs), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+        if (pairs >= (1ull << 32)) throw CudaError{"lidar: more than 2^32 ray candidates"};
+        L.list.reserve(std::max<unsigned long long>(pairs, 1));
+        L.cursor.reserve(n_rays);
+        GSIM_CK(cudaMemcpyAsync(L.cursor.ptr, L.offsets.ptr, n_rays * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToDevice, s));
+        a.ray_offset = L.offsets.ptr;
+        a.cursor = L.cursor.ptr;
+        a.list = L.list.ptr;
+        launch_lidar_scatter(a, ctx->num_sms, s);
+        check_launch();
+        // trace every ray, then compact the returns in ray order
+        L.hit.reserve(n_rays);
+        L.depth.reserve(n_rays);
+        L.acc.reserve(n_rays);
+        a.out_hit = L.hit.ptr;
+        a.out_depth = L.depth.ptr;
+        a.out_acc = L.acc.ptr;
+        launch_lidar_trace(a, ctx->num_sms, s);
+        check_launch();
+        L.hit_offsets.reserve(n_rays + 1);
+        exclusive_scan_u32(L.hit.ptr, n_rays, L.hit_offsets.ptr, L.scratch.ptr, s);
+        check_launch();
+        unsigned long long hits = 0;
+        GSIM_CK(cudaMemcpyAsync(&hits, L.hit_offsets.ptr + n_rays, sizeof(hits), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+        *count = hits;
+        if (hits > capacity || hits == 0) return;
+        if (!points || !ring || !azimuth) throw ValidationError{"lidar_scan: null output"};
+        L.points.reserve(3 * hits);
+        L.ring.reserve(hits);
+        L.azimuth.reserve(hits);
+        a.hit_offset = L.hit_offsets.ptr;
+        a.capacity = hits;
+        a.points = L.points.ptr;
+        a.ring = L.ring.ptr;
+        a.azimuth = L.azimuth.ptr;
+        launch_lidar_emit(a, ctx->num_sms, s);
+        check_launch();
+        GSIM_CK(cudaMemcpyAsync(points, L.points.ptr, 3 * hits * sizeof(double), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaMemcpyAsync(ring, L.ring.ptr, hits * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaMemcpyAsync(azimuth, L.azimuth.ptr, hits * sizeof(double), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+    });
+}
+
+int gsim_gpu_trace_rays(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
+                        uint64_t n_nodes, const double* origins, const double* directions,
+                        const double* t_max, uint64_t n_rays, double alpha_threshold,
+                        uint8_t* hit, double* depth, double* accum_alpha) {
+    return Guard(ctx).run([&] {
+        if (!scene || (n_nodes && !nodes) ||
+            (n_rays && (!origins || !directions || !t_max || !hit || !depth || !accum_alpha)))
+            throw ValidationError{"trace_rays: null argument"};
+        auto& L = ctx->lidar;
+        cudaStream_t s = ctx->stream;
+        LidarArgs a = lidar_pose_stage(ctx, scene, nodes, n_nodes, GSIM_ENV_ALL, false);
+        if (!n_rays) return;
+        L.rays.reserve(7 * n_rays);
+        GSIM_CK(cudaMemcpyAsync(L.rays.ptr, origins, 3 * n_rays * sizeof(double), cudaMemcpyHostToDevice, s));
+        GSIM_CK(cudaMemcpyAsync(L.rays.ptr + 3 * n_rays, directions, 3 * n_rays * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+        GSIM_CK(cudaMemcpyAsync(L.rays.ptr + 6 * n_rays, t_max, n_rays * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+        a.n_rays = n_rays;
+        a.ray_origin = L.rays.ptr;
+        a.ray_dir = L.rays.ptr + 3 * n_rays;
+        a.ray_tmax = L.rays.ptr + 6 * n_rays;
+        a.alpha_threshold = alpha_threshold;
+        launch_lidar_pose(a, ctx->num_sms, s);
+        check_launch();
+        L.hit.reserve(n_rays);
+        L.depth.reserve(n_rays);
+        L.acc.reserve(n_rays);
+        a.out_hit = L.hit.ptr;
+        a.out_depth = L.depth.ptr;
+        a.out_acc = L.acc.ptr;
+        launch_lidar_trace(a, ctx->num_sms, s);
+        check_launch();
+        std::vector<uint32_t> h(n_rays);
+        GSIM_CK(cudaMemcpyAsync(h.data(), L.hit.ptr, n_rays * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaMemcpyAsync(depth, L.depth.ptr, n_rays * sizeof(double), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaMemcpyAsync(accum_alpha, L.acc.ptr, n_rays * sizeof(double), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaStreamSynchronize(s));
+        for (uint64_t k = 0; k < n_rays; ++k) hit[k] = uint8_t(h[k]);
     });
 }
 

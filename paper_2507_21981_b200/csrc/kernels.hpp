@@ -200,4 +200,62 @@ const char* depth_ring_cameras(const double lo[3], const double hi[3], int n_vie
                                int resolution, gsim_camera* cameras);
 DevFuseView fuse_view(const gsim_camera& c, uint64_t depth_offset);
 
+// LiDAR (lidar.cu): the conservative (channel rank, azimuth step) rectangle of rays that can hit
+// a primitive's box. k1 < k0 wraps around azimuth 0.
+enum : uint32_t { kRectNone = 0, kRectRange = 1, kRectAll = 2 };
+struct LidarRect {
+    uint16_t r0, r1;
+    uint32_t k0, k1;
+    uint32_t kind;
+};
+
+struct LidarArgs {
+    DevField field;
+    const DevSegment* segs;          // painted node ranges; entry_count 0 = not seen
+    int n_segs;
+    int scan;                        // 1: LiDAR grid scan, 0: arbitrary rays, every primitive
+    uint64_t n;                      // primitives
+    double* posed;                   // [19][n]: mean xyz, inv_cov 9, opacity, lo xyz, hi xyz
+    uint8_t* seen;                   // [n]
+    LidarRect* rects;                // [n]
+    uint32_t* all_list;              // primitives whose box holds the sensor
+    uint32_t* all_count;
+    double w2s_q[4], w2s_t[3];       // world -> sensor
+    double origin[3];
+    double max_range, two_pi, step;
+    const double* rank_elev;         // regular channels' elevations, ascending
+    const uint32_t* rank_channel;    // rank -> channel index
+    int n_ranks;
+    uint32_t n_az;
+    int* diff;                       // [channels][n_az + 1] row differences
+    uint32_t* ray_count;             // [rays]
+    const unsigned long long* ray_offset;  // [rays + 1]
+    unsigned long long* cursor;      // [rays]
+    uint32_t* list;                  // candidates per ray
+    uint64_t n_rays;
+    const double* ray_origin;        // [rays][3] (arbitrary rays)
+    const double* ray_dir;           // [rays][3] world directions
+    const double* ray_dir_sensor;    // [rays][3] (scan)
+    const double* ray_tmax;          // [rays] (arbitrary rays)
+    const uint8_t* ray_all;          // [channels] every primitive is a candidate (scan)
+    double alpha_threshold;
+    uint32_t* out_hit;               // [rays] 0 / 1
+    double* out_depth;
+    double* out_acc;
+    const unsigned long long* hit_offset;  // [rays + 1]
+    uint64_t capacity;
+    double* points;
+    uint32_t* ring;
+    double* azimuth;
+};
+
+void launch_lidar_pose(const LidarArgs& a, int n_sms, cudaStream_t s);
+void launch_lidar_count(const LidarArgs& a, int n_sms, cudaStream_t s);
+void launch_lidar_rowscan(const LidarArgs& a, uint32_t n_channels, cudaStream_t s);
+void launch_lidar_scatter(const LidarArgs& a, int n_sms, cudaStream_t s);
+void launch_lidar_trace(const LidarArgs& a, int n_sms, cudaStream_t s);
+void launch_lidar_emit(const LidarArgs& a, int n_sms, cudaStream_t s);
+void exclusive_scan_u32(const uint32_t* in, uint64_t n, unsigned long long* out,
+                        unsigned long long* scratch, cudaStream_t s);
+
 }  // namespace gsim_gpu

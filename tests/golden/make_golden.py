@@ -126,6 +126,18 @@ def main() -> None:
              origin=list(vol.origin), truncation=vol.truncation, tsdf_sha=sha(vol.tsdf),
              weights_sha=sha(vol.weights), observed_fraction=float((vol.weights > 0).mean()))
     data["transfer"] = t
+    # LiDAR (trace.cpp): GaussianBvh::build(field, nodes).scan(lidar)
+    from paper_2507_21981_b200.api import LidarModel
+    f4 = ref.random_field(5150, 1500, 2.0, 0.02, 0.15, 0)
+    lid = LidarModel(np.radians(np.linspace(-15.0, 15.0, 8)), np.radians(3.0), 6.0,
+                     RigidTransform(quat_normalized((0.99, 0.1, 0.0, 0.05)), (0.1, -0.2, 0.05)))
+    scan = ref.lidar_scan(f4, make_nodes("two", 1500), lid)
+    data["lidar"] = dict(seed=5150, count=1500, box=2.0, slo=0.02, shi=0.15, deg=0,
+                         channels_deg=[float(x) for x in np.linspace(-15.0, 15.0, 8)],
+                         azimuth_step_deg=3.0, max_range=6.0,
+                         pose_q=[0.99, 0.1, 0.0, 0.05], pose_t=[0.1, -0.2, 0.05],
+                         returns=int(len(scan["ring"])), points_sha=sha(scan["points"]),
+                         ring_sha=sha(scan["ring"]), azimuth_sha=sha(scan["azimuth"]))
     OUT.write_text(json.dumps(data, indent=1) + "\n")
     print("wrote", OUT)
 
