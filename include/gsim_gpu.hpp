@@ -19,6 +19,9 @@
 //   gsim::gpu::tsdf_fuse(volume, camera, depth)         tsdf_fuse (transfer.hpp:68-71)
 //   gsim::gpu::gaussians_to_tsdf(field, voxel_size)     gaussians_to_mesh's fused volume
 //                                                       (transfer.hpp:82-86, transfer.cpp:174-198)
+//   gsim::gpu::lidar_scan(field, nodes, lidar)          GaussianBvh::build(field, nodes).scan(lidar)
+//                                                       (trace.hpp:66-82)
+//   gsim::gpu::trace(field, nodes, rays, threshold)     GaussianBvh::trace per ray (trace.hpp:70-74)
 //
 // Errors are rethrown as the reference's gsim::validation_error (status 2) and gsim::io_error
 // (status 1). The free functions upload the field on every call (a pure function of their
@@ -37,6 +40,7 @@
 #include "gsim/gaussian.hpp"
 #include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
+#include "gsim/trace.hpp"
 #include "gsim/transfer.hpp"
 #include "gsim_gpu.h"
 
@@ -344,6 +348,60 @@ public:
         volume.weights = out.weights;
     }
 
+    // GaussianBvh::build(field, nodes).scan(lidar) (trace.cpp:88-111, 169-197) on the resident field.
+    PointCloud lidar_scan(const std::vector<SceneNode>& nodes, const LidarModel& lidar) {
+        const auto ns = detail::nodes(nodes);
+        gsim_lidar l{};
+        l.channels = lidar.channels.data();
+        l.n_channels = lidar.channels.size();
+        l.azimuth_step = lidar.azimuth_step;
+        l.max_range = lidar.max_range;
+        l.pose = detail::rigid(lidar.pose);
+        l.alpha_threshold = lidar.alpha_threshold;
+        l.env = GSIM_ENV_ALL;
+        uint64_t count = 0;
+        detail::check(gsim_gpu_lidar_scan(ctx_.get(), scene_.get(), ns.data(), ns.size(), &l, nullptr,
+                                          nullptr, nullptr, 0, &count),
+                      ctx_.get());
+        std::vector<double> pts(3 * count), az(count);
+        std::vector<uint32_t> ring(count);
+        detail::check(gsim_gpu_lidar_scan(ctx_.get(), scene_.get(), ns.data(), ns.size(), &l, pts.data(),
+                                          ring.data(), az.data(), count, &count),
+                      ctx_.get());
+        PointCloud cloud;
+        for (uint64_t k = 0; k < count; ++k) {
+            cloud.points.push_back(Vec3(pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]));
+            cloud.ring.push_back(ring[k]);
+            cloud.azimuth.push_back(az[k]);
+        }
+        return cloud;
+    }
+
+    // GaussianBvh::trace (trace.cpp:113-123) for a batch of rays on the resident field.
+    std::vector<TraceResult> trace(const std::vector<SceneNode>& nodes, const std::vector<Ray>& rays,
+                                   double alpha_threshold = 0.5) {
+        const auto ns = detail::nodes(nodes);
+        std::vector<double> o, d, t;
+        for (const Ray& r : rays) {
+            o.insert(o.end(), {r.origin.x, r.origin.y, r.origin.z});
+            d.insert(d.end(), {r.direction.x, r.direction.y, r.direction.z});
+            t.push_back(r.t_max);
+        }
+        std::vector<uint8_t> hit(rays.size());
+        std::vector<double> depth(rays.size()), acc(rays.size());
+        detail::check(gsim_gpu_trace_rays(ctx_.get(), scene_.get(), ns.data(), ns.size(), o.data(), d.data(),
+                                          t.data(), rays.size(), alpha_threshold, hit.data(),
+                                          depth.data(), acc.data()),
+                      ctx_.get());
+        std::vector<TraceResult> out(rays.size());
+        for (std::size_t k = 0; k < rays.size(); ++k) {
+            out[k].hit = hit[k] != 0;
+            out[k].depth = depth[k];
+            out[k].accum_alpha = acc[k];
+        }
+        return out;
+    }
+
     gsim_gpu_context* context() { return ctx_.get(); }
     gsim_gpu_scene* scene() { return scene_.get(); }
 
@@ -445,6 +503,22 @@ inline TsdfVolume gaussians_to_tsdf(const GaussianField& field, double voxel_siz
     Renderer& r = default_renderer();
     r.upload(field);
     return r.gaussians_to_tsdf(voxel_size);
+}
+
+// GaussianBvh::build(field, nodes).scan(lidar) (trace.cpp:88-111, 169-197) on the GPU.
+inline PointCloud lidar_scan(const GaussianField& field, const std::vector<SceneNode>& nodes,
+                             const LidarModel& lidar) {
+    Renderer& r = default_renderer();
+    r.upload(field);
+    return r.lidar_scan(nodes, lidar);
+}
+
+// GaussianBvh::build(field, nodes).trace(ray, threshold) for every ray.
+inline std::vector<TraceResult> trace(const GaussianField& field, const std::vector<SceneNode>& nodes,
+                                      const std::vector<Ray>& rays, double alpha_threshold = 0.5) {
+    Renderer& r = default_renderer();
+    r.upload(field);
+    return r.trace(nodes, rays, alpha_threshold);
 }
 
 // The bytes gsim::write_png_rgb8 (srgb), write_png_gray8, write_png_gray16 (scale) and write_pfm

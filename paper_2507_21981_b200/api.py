@@ -774,16 +774,13 @@ class Context:
         lc = lidar.to_c()
         cnt = C.c_uint64(0)
         dp, u32p = C.POINTER(C.c_double), C.POINTER(C.c_uint32)
-        z = np.zeros(1)
-        zr = np.zeros(1, np.uint32)
-        _check(self.lib.gsim_gpu_lidar_scan(self.ptr, scene.handle, na, len(nodes), C.byref(lc),
-                                            z.ctypes.data_as(dp), zr.ctypes.data_as(u32p),
-                                            z.ctypes.data_as(dp), 0, C.byref(cnt)), self.ptr)
-        n = cnt.value
-        pts = np.zeros((max(n, 1), 3)); ring = np.zeros(max(n, 1), np.uint32); az = np.zeros(max(n, 1))
+        # a scan returns at most one point per ray: one call with that capacity
+        cap = max(1, len(lidar.channels) * lidar.azimuth_count()) if lidar.azimuth_step > 0 else 1
+        pts = np.zeros((cap, 3)); ring = np.zeros(cap, np.uint32); az = np.zeros(cap)
         _check(self.lib.gsim_gpu_lidar_scan(self.ptr, scene.handle, na, len(nodes), C.byref(lc),
                                             pts.ctypes.data_as(dp), ring.ctypes.data_as(u32p),
-                                            az.ctypes.data_as(dp), n, C.byref(cnt)), self.ptr)
+                                            az.ctypes.data_as(dp), cap, C.byref(cnt)), self.ptr)
+        n = cnt.value
         return {"points": pts[:n], "ring": ring[:n], "azimuth": az[:n]}
 
     def trace_rays(self, scene: Scene, nodes, origins, directions, t_max, alpha_threshold: float = 0.5):

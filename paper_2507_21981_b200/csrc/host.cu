@@ -196,19 +196,23 @@ struct gsim_gpu_context {
     float frame_valid_alpha = 0.0f;  // render_depth_ring's depth mask (raster epilogue)
     // LiDAR scratch (lidar.cu)
     struct {
-        DevBuf<double> posed, rays, depth, acc, points, azimuth, rank_elev;
+        DevBuf<double> posed, rays, depth, acc, points, azimuth, rank_elev, cand_t, cand_r;
         DevBuf<uint8_t> seen, ray_all;
         DevBuf<LidarRect> rects;
-        DevBuf<uint32_t> all_list, counts, list, hit, ring, rank_channel;
+        DevBuf<uint32_t> all_list, counts, list, hit, ring, rank_channel, cursor, big_list;
         DevBuf<int> diff;
-        DevBuf<unsigned long long> offsets, cursor, scratch, hit_offsets;
+        DevBuf<unsigned long long> offsets, scratch, hit_offsets;
         DevBuf<DevSegment> segs;
+        std::vector<double> ray_key;  // (channels, step) of the sensor directions in rays
         void release() {
             posed.release(); rays.release(); depth.release(); acc.release(); points.release();
             azimuth.release(); rank_elev.release(); seen.release(); ray_all.release();
+            cand_t.release(); cand_r.release();
             rects.release(); all_list.release(); counts.release(); list.release(); hit.release();
             ring.release(); rank_channel.release(); diff.release(); offsets.release();
-            cursor.release(); scratch.release(); hit_offsets.release(); segs.release();
+            cursor.release(); big_list.release(); scratch.release(); hit_offsets.release();
+            segs.release();
+            ray_key.clear();
         }
     } lidar;
 
@@ -2234,20 +2238,30 @@ int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, cons
         const uint64_t n_rays = n_ch * n_az;
         if (n_az == 0 || n_az > (1u << 30) || n_ch > 65535)
             throw ValidationError{"lidar: ray grid too large"};
-        // rays exactly as GaussianBvh::scan builds them (trace.cpp:180-189), on the host
-        const dq sq{lidar->pose.rotation[0], lidar->pose.rotation[1], lidar->pose.rotation[2],
-                    lidar->pose.rotation[3]};
-        std::vector<double> rays(6 * n_rays);
-        for (uint64_t k = 0; k < n_rays; ++k) {
-            const double elevation = lidar->channels[k / n_az];
-            const double az = static_cast<double>(k % n_az) * lidar->azimuth_step;
-            const double ce = std::cos(elevation);
-            const dv3 ds = mk3(ce * std::cos(az), ce * std::sin(az), std::sin(elevation));
-            const dv3 dw = qrotate(sq, ds);
-            double* r = rays.data() + 6 * k;
-            r[0] = dw.x; r[1] = dw.y; r[2] = dw.z;
-            r[3] = ds.x; r[4] = ds.y; r[5] = ds.z;
+        // Sensor-frame ray directions exactly as GaussianBvh::scan builds them (trace.cpp:
+        // 180-186, glibc cos / sin) are computed on the host once per (channels, step) and kept
+        // on the device; the world directions (the pose rotation) are a kernel.
+        std::vector<double> key(lidar->channels, lidar->channels + n_ch);
+        key.push_back(lidar->azimuth_step);
+        L.rays.reserve(std::max<uint64_t>(6 * n_rays, 1));
+        if (key != L.ray_key) {
+            std::vector<double> ds(3 * n_rays);
+            for (uint64_t k = 0; k < n_rays; ++k) {
+                const double elevation = lidar->channels[k / n_az];
+                const double az = static_cast<double>(k % n_az) * lidar->azimuth_step;
+                const double ce = std::cos(elevation);
+                ds[3 * k] = ce * std::cos(az);
+                ds[3 * k + 1] = ce * std::sin(az);
+                ds[3 * k + 2] = std::sin(elevation);
+            }
+            GSIM_CK(cudaMemcpyAsync(L.rays.ptr + 3 * n_rays, ds.data(), ds.size() * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+            GSIM_CK(cudaStreamSynchronize(s));  // ds dies with this scope
+            L.ray_key = key;
         }
+        launch_lidar_rays(L.rays.ptr + 3 * n_rays, L.rays.ptr, n_rays, lidar->pose.rotation,
+                          ctx->num_sms, s);
+        check_launch();
         // regular channels (cos(elevation) clearly positive) bin by elevation rank; rays of the
         // others take every primitive as a candidate
         std::vector<std::pair<double, uint32_t>> reg;
@@ -2264,17 +2278,6 @@ int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, cons
             rank_elev.push_back(r.first);
             rank_channel.push_back(r.second);
         }
-        L.rays.reserve(std::max<uint64_t>(6 * n_rays, 1));
-        // split the interleaved host rays into the two device planes
-        std::vector<double> dw(3 * n_rays), ds(3 * n_rays);
-        for (uint64_t k = 0; k < n_rays; ++k)
-            for (int c = 0; c < 3; ++c) {
-                dw[3 * k + c] = rays[6 * k + c];
-                ds[3 * k + c] = rays[6 * k + 3 + c];
-            }
-        GSIM_CK(cudaMemcpyAsync(L.rays.ptr, dw.data(), dw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-        GSIM_CK(cudaMemcpyAsync(L.rays.ptr + 3 * n_rays, ds.data(), ds.size() * sizeof(double),
-                                cudaMemcpyHostToDevice, s));
         L.ray_all.reserve(n_ch);
         GSIM_CK(cudaMemcpyAsync(L.ray_all.ptr, ray_all.data(), n_ch, cudaMemcpyHostToDevice, s));
         L.rank_elev.reserve(std::max<size_t>(rank_elev.size(), 1));
@@ -2286,6 +2289,8 @@ int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, cons
                                     rank_channel.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
         }
         // world -> sensor pose (RigidTransform::inverse, math.hpp:235-238)
+        const dq sq{lidar->pose.rotation[0], lidar->pose.rotation[1], lidar->pose.rotation[2],
+                    lidar->pose.rotation[3]};
         const dq wq{sq.w, -sq.x, -sq.y, -sq.z};
         const dv3 wt = qrotate(wq, mk3(lidar->pose.translation[0], lidar->pose.translation[1],
                                        lidar->pose.translation[2]));
@@ -2320,17 +2325,29 @@ int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, cons
         exclusive_scan_u32(L.counts.ptr, n_rays, L.offsets.ptr, L.scratch.ptr, s);
         check_launch();
         unsigned long long pairs = 0;
+        uint32_t n_all = 0;
         GSIM_CK(cudaMemcpyAsync(&pairs, L.offsets.ptr + n_rays, sizeof(pairs), cudaMemcpyDeviceToHost, s));
+        GSIM_CK(cudaMemcpyAsync(&n_all, a.all_count, sizeof(n_all), cudaMemcpyDeviceToHost, s));
         GSIM_CK(cudaStreamSynchronize(s));
+        const uint64_t cache = std::max<uint64_t>(pairs + n_rays * uint64_t(n_all), 1);
+        L.cand_t.reserve(cache);
+        L.cand_r.reserve(cache);
+        a.cand_t = L.cand_t.ptr;
+        a.cand_r = L.cand_r.ptr;
         if (pairs >= (1ull << 32)) throw CudaError{"lidar: more than 2^32 ray candidates"};
         L.list.reserve(std::max<unsigned long long>(pairs, 1));
         L.cursor.reserve(n_rays);
-        GSIM_CK(cudaMemcpyAsync(L.cursor.ptr, L.offsets.ptr, n_rays * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToDevice, s));
+        GSIM_CK(cudaMemsetAsync(L.cursor.ptr, 0, n_rays * sizeof(uint32_t), s));
+        L.big_list.reserve(std::max<uint64_t>(scene->f.n, 1) + 1);
+        GSIM_CK(cudaMemsetAsync(L.big_list.ptr, 0, sizeof(uint32_t), s));
         a.ray_offset = L.offsets.ptr;
         a.cursor = L.cursor.ptr;
+        a.big_count = L.big_list.ptr;
+        a.big_list = L.big_list.ptr + 1;
         a.list = L.list.ptr;
         launch_lidar_scatter(a, ctx->num_sms, s);
+        check_launch();
+        launch_lidar_scatter_big(a, ctx->num_sms, s);
         check_launch();
         // trace every ray, then compact the returns in ray order
         L.hit.reserve(n_rays);
@@ -2339,8 +2356,21 @@ int gsim_gpu_lidar_scan(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, cons
         a.out_hit = L.hit.ptr;
         a.out_depth = L.depth.ptr;
         a.out_acc = L.acc.ptr;
+        static const bool debug = std::getenv("GSIM_GPU_LIDAR_DEBUG") != nullptr;
+        if (debug) {
+            L.scratch.reserve((n_rays + 1023) / 1024 + 8);
+            a.debug = L.scratch.ptr + (n_rays + 1023) / 1024 + 4;
+            GSIM_CK(cudaMemsetAsync(a.debug, 0, 3 * sizeof(unsigned long long), s));
+        }
         launch_lidar_trace(a, ctx->num_sms, s);
         check_launch();
+        if (debug) {
+            unsigned long long d[3];
+            GSIM_CK(cudaMemcpyAsync(d, a.debug, sizeof(d), cudaMemcpyDeviceToHost, s));
+            GSIM_CK(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "lidar: rays %llu candidates %llu (%.1f per ray), pairs %llu, around the sensor %u\n",
+                         d[0], d[1], double(d[1]) / double(std::max(d[0], 1ull)), pairs, n_all);
+        }
         L.hit_offsets.reserve(n_rays + 1);
         exclusive_scan_u32(L.hit.ptr, n_rays, L.hit_offsets.ptr, L.scratch.ptr, s);
         check_launch();

@@ -230,7 +230,9 @@ struct LidarArgs {
     int* diff;                       // [channels][n_az + 1] row differences
     uint32_t* ray_count;             // [rays]
     const unsigned long long* ray_offset;  // [rays + 1]
-    unsigned long long* cursor;      // [rays]
+    uint32_t* cursor;                // [rays] slots taken in each ray's list (zeroed)
+    uint32_t* big_list;              // primitives with rectangles too big for one thread
+    uint32_t* big_count;
     uint32_t* list;                  // candidates per ray
     uint64_t n_rays;
     const double* ray_origin;        // [rays][3] (arbitrary rays)
@@ -247,12 +249,18 @@ struct LidarArgs {
     double* points;
     uint32_t* ring;
     double* azimuth;
+    double* cand_t;                  // scan: per-candidate (t, response) cache, [pairs + rays *
+    double* cand_r;                  //   all_count] (ray region at offset + ray * all_count)
+    unsigned long long* debug;       // optional counters: rays, candidates
 };
 
 void launch_lidar_pose(const LidarArgs& a, int n_sms, cudaStream_t s);
+void launch_lidar_rays(const double* ds, double* dw, uint64_t n, const double* q, int n_sms,
+                       cudaStream_t s);
 void launch_lidar_count(const LidarArgs& a, int n_sms, cudaStream_t s);
 void launch_lidar_rowscan(const LidarArgs& a, uint32_t n_channels, cudaStream_t s);
 void launch_lidar_scatter(const LidarArgs& a, int n_sms, cudaStream_t s);
+void launch_lidar_scatter_big(const LidarArgs& a, int n_sms, cudaStream_t s);
 void launch_lidar_trace(const LidarArgs& a, int n_sms, cudaStream_t s);
 void launch_lidar_emit(const LidarArgs& a, int n_sms, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t* in, uint64_t n, unsigned long long* out,

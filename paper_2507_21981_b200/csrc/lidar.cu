@@ -15,13 +15,14 @@
 //   lidar_scatter_kernel  every (ray, primitive) candidate at its ray's cursor (order free: the
 //                         tracer orders by (t, index) itself)
 //   lidar_trace_kernel    one warp per ray: exact ray_aabb_hit + ray_gaussian_peak per candidate,
-//                         the survivors (response >= 1/255) kept in registers, composited in
-//                         (t, index) order by repeated warp arg-min (trace.cpp:65-85) until the
-//                         transmittance cutoff; lanes with more survivors than registers fall
-//                         back to re-scanning the list per step (same order, same result)
+//                         the survivors (response >= 1/255) compacted into a shared-memory pool,
+//                         composited in (t, index) order by repeated warp arg-min over the pool
+//                         (trace.cpp:65-85) until the transmittance cutoff; a ray with more
+//                         survivors than the pool re-scans its list per step (same result)
 //   lidar_emit_kernel     returns compacted in ray order: channel-major, azimuth ascending
-// Ray directions are computed on the host with the reference's cos / sin (glibc), so the rays
-// are bit-identical; only exp differs (CUDA's vs glibc's, <= 1 ulp).
+// Sensor-frame ray directions are computed on the host with the reference's cos / sin (glibc,
+// cached per channel set) and rotated on the device in the reference's double order, so the
+// rays are bit-identical; only exp differs (CUDA's vs glibc's, <= 1 ulp).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -38,7 +39,6 @@ constexpr double kBoundsSigmaL = 3.0;      // trace.hpp:25
 constexpr double kTraceAlphaClamp = 0.99;  // trace.cpp:59-61
 constexpr double kTraceAlphaSkip = 1.0 / 255.0;
 constexpr double kTraceCutoff = 1e-4;
-constexpr int kSurvivors = 8;              // per lane, in registers
 constexpr double kAngleMargin = 1e-7;      // radians added to every angular bound
 
 __device__ __forceinline__ dv3 ld3(const double* p, uint64_t n, uint64_t i) {  // SoA planes
@@ -286,17 +286,55 @@ __global__ void __launch_bounds__(256) lidar_rowscan_kernel(LidarArgs a) {
     }
 }
 
+// Rays of a rectangle (both wrapped parts), enumerated by one thread.
+__device__ __forceinline__ uint32_t rect_rays(const LidarRect& rc, uint32_t n_az) {
+    const uint32_t w = rc.k0 <= rc.k1 ? rc.k1 - rc.k0 + 1 : (n_az - rc.k0) + rc.k1 + 1;
+    return (uint32_t(rc.r1) - rc.r0 + 1) * w;
+}
+
+// Ray id of position p (row-major over the rectangle) of a rectangle.
+__device__ __forceinline__ uint64_t rect_ray(const LidarArgs& a, const LidarRect& rc, uint32_t p) {
+    const uint32_t w = rc.k0 <= rc.k1 ? rc.k1 - rc.k0 + 1 : (a.n_az - rc.k0) + rc.k1 + 1;
+    const uint32_t r = rc.r0 + p / w;
+    uint32_t k = rc.k0 + p % w;
+    if (k >= a.n_az) k -= a.n_az;
+    return uint64_t(a.rank_channel[r]) * a.n_az + k;
+}
+
+// Order within a ray's list is free (the tracer orders by (t, index)): every candidate takes
+// its slot with one atomic on the ray's cursor. Small rectangles are walked by their thread;
+// big ones (primitives close to the sensor cover thousands of rays) are queued and spread over
+// whole warps by lidar_scatter_big_kernel, so no thread serialises thousands of atomics.
+constexpr uint32_t kSmallRect = 64;
+
 __global__ void __launch_bounds__(256) lidar_scatter_kernel(LidarArgs a) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < a.n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const LidarRect rc = a.rects[i];
         if (rc.kind != kRectRange) continue;
-        for (uint32_t r = rc.r0; r <= rc.r1; ++r) {
-            const uint64_t ray0 = uint64_t(a.rank_channel[r]) * a.n_az;
-            for_row_ranges(rc, a.n_az, [&](uint32_t k0, uint32_t k1) {
-                for (uint32_t k = k0; k <= k1; ++k)
-                    a.list[atomicAdd(a.cursor + ray0 + k, 1ull)] = uint32_t(i);
-            });
+        const uint32_t m = rect_rays(rc, a.n_az);
+        if (m > kSmallRect) {
+            a.big_list[atomicAdd(a.big_count, 1u)] = uint32_t(i);
+            continue;
+        }
+        for (uint32_t p = 0; p < m; ++p) {
+            const uint64_t ray = rect_ray(a, rc, p);
+            a.list[a.ray_offset[ray] + atomicAdd(a.cursor + ray, 1u)] = uint32_t(i);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) lidar_scatter_big_kernel(LidarArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_big = *a.big_count;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_big;
+         w += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t i = a.big_list[w];
+        const LidarRect rc = a.rects[i];
+        const uint32_t m = rect_rays(rc, a.n_az);
+        for (uint32_t p = lane; p < m; p += 32) {
+            const uint64_t ray = rect_ray(a, rc, p);
+            a.list[a.ray_offset[ray] + atomicAdd(a.cursor + ray, 1u)] = i;
         }
     }
 }
@@ -330,11 +368,90 @@ __device__ __forceinline__ bool survivor(const LidarArgs& a, uint32_t i, dv3 o, 
 }
 }  // namespace
 
-// One warp per ray.
-__global__ void __launch_bounds__(256) lidar_trace_kernel(LidarArgs a) {
+// One warp per ray, composite in (t, index) order (trace.cpp:65-85) from a per-warp pool of
+// at most kPool survivors (box hit, response >= 1/255) in shared memory, picked by warp arg-min.
+//
+// Scan rays (binned candidate lists): pass A computes every candidate's (t, response) once and
+// stores it coalesced in the ray's scratch region (t = +inf marks a non-survivor). The rest
+// works on that cache: the survivors after the last composited one are counted (with their t
+// range); if more than the pool holds, a 64-bin histogram of t picks a window [lo, tau] that fits;
+// the window is pooled and composited; the ray stops at the cutoff or moves to the next window.
+// Rays that take every primitive (arbitrary rays, near-pole channels) recompute instead of
+// caching, and re-scan per composite step when their survivors overflow the pool.
+constexpr int kPool = 256;
+constexpr int kTraceWarps = 8;
+constexpr int kBins = 64;
+
+namespace {
+struct Composite {
+    double depth_sum = 0.0, acc = 0.0, T = 1.0;
+    double last_t = -INFINITY;
+    uint32_t last_i = 0;
+    bool first = true, done = false;
+    __device__ __forceinline__ bool after(double t, uint32_t i) const {
+        return first || before(last_t, last_i, t, i);
+    }
+    __device__ __forceinline__ void add(double t, double resp, uint32_t i) {
+        const double alpha = resp < kTraceAlphaClamp ? resp : kTraceAlphaClamp;  // std::min
+        const double w = alpha * T;
+        depth_sum += t * w;
+        acc += w;
+        T *= 1.0 - alpha;
+        last_t = t;
+        last_i = i;
+        first = false;
+        if (T < kTraceCutoff) done = true;
+    }
+};
+
+// Warp arg-min of (t, index) among the lanes' candidates.
+__device__ __forceinline__ bool warp_argmin(double& bt, double& br, uint32_t& bi, bool have) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+        const double orr = __shfl_xor_sync(0xffffffffu, br, off);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        const bool oh = __shfl_xor_sync(0xffffffffu, have, off);
+        if (oh && (!have || before(ot, oi, bt, bi))) {
+            bt = ot; br = orr; bi = oi; have = true;
+        }
+    }
+    return have;
+}
+
+// Composite the pool (ns entries) in order until exhausted or saturated.
+__device__ __forceinline__ void composite_pool(Composite& c, const double* pt, const double* pr,
+                                               const uint32_t* pi, uint32_t ns) {
     const int lane = threadIdx.x & 31;
+    while (!c.done) {
+        double bt = INFINITY, br = 0.0;
+        uint32_t bi = 0xFFFFFFFFu;
+        bool have = false;
+        for (uint32_t q = lane; q < ns; q += 32) {
+            const double t = pt[q];
+            const uint32_t i = pi[q];
+            if (c.after(t, i) && (!have || before(t, i, bt, bi))) {
+                bt = t; br = pr[q]; bi = i; have = true;
+            }
+        }
+        if (!warp_argmin(bt, br, bi, have)) break;
+        c.add(bt, br, bi);
+    }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(32 * kTraceWarps) lidar_trace_kernel(LidarArgs a) {
+    __shared__ double s_t[kTraceWarps][kPool];
+    __shared__ double s_r[kTraceWarps][kPool];
+    __shared__ uint32_t s_i[kTraceWarps][kPool];
+    __shared__ uint32_t s_hist[kTraceWarps][kBins];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    double* pt = s_t[wib];
+    double* pr = s_r[wib];
+    uint32_t* pi = s_i[wib];
+    uint32_t* hist = s_hist[wib];
     for (uint64_t ray = warp; ray < a.n_rays; ray += n_warps) {
         const dv3 o = a.scan ? mk3(a.origin[0], a.origin[1], a.origin[2]) : ldx3(a.ray_origin, ray);
         const dv3 d = ldx3(a.ray_dir, ray);
@@ -350,88 +467,195 @@ __global__ void __launch_bounds__(256) lidar_trace_kernel(LidarArgs a) {
             cs.n_extra = *a.all_count;
         }
         const uint32_t nc = cs.count(a.n);
-        // 1. survivors into registers (lane-private, up to kSurvivors)
-        double st[kSurvivors], sr[kSurvivors];
-        uint32_t si[kSurvivors];
-        int ns = 0;
-        bool overflow = false;
-        for (uint32_t j0 = 0; j0 < nc; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            double t, resp;
-            if (j < nc) {
-                const uint32_t i = cs.at(j);
-                if (survivor(a, i, o, d, inv, t_max, t, resp)) {
-                    if (ns < kSurvivors) {
-#pragma unroll
-                        for (int q = 0; q < kSurvivors; ++q)
-                            if (q == ns) { st[q] = t; sr[q] = resp; si[q] = i; }
-                        ++ns;
-                    } else {
-                        overflow = true;
-                    }
-                }
+        Composite c;
+        if (!brute) {
+            // pass A: (t, response) of every candidate, cached (t = inf: not a survivor)
+            const uint64_t base = a.ray_offset[ray] + ray * uint64_t(cs.n_extra);
+            double* ct = a.cand_t + base;
+            double* cr = a.cand_r + base;
+            for (uint32_t j = lane; j < nc; j += 32) {
+                double t = 0.0, resp = 0.0;
+                const bool keep = survivor(a, cs.at(j), o, d, inv, t_max, t, resp);
+                ct[j] = keep ? t : INFINITY;
+                cr[j] = resp;
             }
-        }
-        overflow = __any_sync(0xffffffffu, overflow);
-        // 2. composite in (t, index) order (trace.cpp:65-85)
-        double depth_sum = 0.0, acc = 0.0, T = 1.0;
-        double last_t = -INFINITY;
-        uint32_t last_i = 0;
-        bool first = true;
-        while (true) {
-            // lane's smallest (t, index) after the last composited one
-            double bt = INFINITY, br = 0.0;
-            uint32_t bi = 0xFFFFFFFFu;
-            bool have = false;
-            if (!overflow) {
-#pragma unroll
-                for (int q = 0; q < kSurvivors; ++q) {
-                    if (q < ns && (first || before(last_t, last_i, st[q], si[q])) &&
-                        (!have || before(st[q], si[q], bt, bi))) {
-                        bt = st[q]; br = sr[q]; bi = si[q]; have = true;
+            __syncwarp();
+            // windows of at most kPool survivors, in t order
+            double lo = -INFINITY;  // survivors with t > lo remain (all of t <= lo were pooled)
+            while (!c.done) {
+                uint32_t cnt = 0;
+                double tmin = INFINITY, tmax = -INFINITY;
+                for (uint32_t j = lane; j < nc; j += 32) {
+                    const double t = ct[j];
+                    if (t != INFINITY && t > lo) {
+                        ++cnt;
+                        tmin = fmin(tmin, t);
+                        tmax = fmax(tmax, t);
                     }
                 }
-            } else {
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+                    tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, off));
+                    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+                }
+                if (cnt == 0) break;
+                if (cnt > uint32_t(kPool)) {
+                    // 64-bin histogram of t over [tmin, tmax]; tau = upper edge of the last bin
+                    // whose prefix fits the pool (bin 0 alone too big: selection on the cache)
+                    for (int b = lane; b < kBins; b += 32) hist[b] = 0;
+                    __syncwarp();
+                    const double scale = double(kBins) / (tmax - tmin);
+                    for (uint32_t j = lane; j < nc; j += 32) {
+                        const double t = ct[j];
+                        if (t != INFINITY && t > lo) {
+                            int b = int((t - tmin) * scale);
+                            b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
+                            atomicAdd(&hist[b], 1u);
+                        }
+                    }
+                    __syncwarp();
+                    uint32_t run = 0;
+                    int last_fit = -1;
+                    for (int b = 0; b < kBins; ++b) {
+                        run += hist[b];
+                        if (run <= uint32_t(kPool)) last_fit = b;
+                    }
+                    __syncwarp();
+                    if (last_fit < 0) {
+                        // a tie cluster: pick survivors one by one straight from the cache
+                        while (!c.done) {
+                            double bt = INFINITY, br = 0.0;
+                            uint32_t bi = 0xFFFFFFFFu;
+                            bool have = false;
+                            for (uint32_t j = lane; j < nc; j += 32) {
+                                const double t = ct[j];
+                                if (t == INFINITY || !(t > lo)) continue;
+                                const uint32_t i = cs.at(j);
+                                if (c.after(t, i) && (!have || before(t, i, bt, bi))) {
+                                    bt = t; br = cr[j]; bi = i; have = true;
+                                }
+                            }
+                            if (!warp_argmin(bt, br, bi, have)) break;
+                            c.add(bt, br, bi);
+                        }
+                        break;
+                    }
+                    // a survivor is in the window iff its bin index (the same rounding as the
+                    // histogram) is <= last_fit
+                    uint32_t ns = 0;
+                    double wmax = -INFINITY;
+                    for (uint32_t j0 = 0; j0 < nc; j0 += 32) {
+                        const uint32_t j = j0 + lane;
+                        bool in = false;
+                        double t = INFINITY;
+                        if (j < nc) {
+                            t = ct[j];
+                            if (t != INFINITY && t > lo) {
+                                int b = int((t - tmin) * scale);
+                                b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
+                                in = b <= last_fit;
+                            }
+                        }
+                        const uint32_t bits = __ballot_sync(0xffffffffu, in);
+                        if (in) {
+                            const uint32_t slot = ns + __popc(bits & lanemask_lt());
+                            pt[slot] = t;
+                            pr[slot] = cr[j];
+                            pi[slot] = cs.at(j);
+                            wmax = fmax(wmax, t);
+                        }
+                        ns += __popc(bits);
+                    }
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1)
+                        wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+                    __syncwarp();
+                    composite_pool(c, pt, pr, pi, ns);
+                    __syncwarp();
+                    // every survivor with t <= wmax was in the window (bins are monotone in t)
+                    lo = wmax;
+                    continue;
+                }
+                // everything left fits the pool
+                uint32_t ns = 0;
                 for (uint32_t j0 = 0; j0 < nc; j0 += 32) {
                     const uint32_t j = j0 + lane;
-                    double t, resp;
-                    if (j < nc) {
+                    const double t = j < nc ? ct[j] : INFINITY;
+                    const bool in = t != INFINITY && t > lo;
+                    const uint32_t bits = __ballot_sync(0xffffffffu, in);
+                    if (in) {
+                        const uint32_t slot = ns + __popc(bits & lanemask_lt());
+                        pt[slot] = t;
+                        pr[slot] = cr[j];
+                        pi[slot] = cs.at(j);
+                    }
+                    ns += __popc(bits);
+                }
+                __syncwarp();
+                composite_pool(c, pt, pr, pi, ns);
+                __syncwarp();
+                break;
+            }
+        } else {
+            // every primitive is a candidate: pool the survivors, or re-scan per step on overflow
+            uint32_t ns = 0;
+            bool overflow = false;
+            for (uint32_t j0 = 0; j0 < nc; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                double t = 0.0, resp = 0.0;
+                uint32_t i = 0;
+                bool keep = false;
+                if (j < nc) {
+                    i = cs.at(j);
+                    keep = survivor(a, i, o, d, inv, t_max, t, resp);
+                }
+                const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+                if (ns + __popc(bits) > uint32_t(kPool)) {
+                    overflow = true;
+                    break;
+                }
+                if (keep) {
+                    const uint32_t slot = ns + __popc(bits & lanemask_lt());
+                    pt[slot] = t;
+                    pr[slot] = resp;
+                    pi[slot] = i;
+                }
+                ns += __popc(bits);
+            }
+            __syncwarp();
+            if (!overflow) {
+                composite_pool(c, pt, pr, pi, ns);
+            } else {
+                while (!c.done) {
+                    double bt = INFINITY, br = 0.0;
+                    uint32_t bi = 0xFFFFFFFFu;
+                    bool have = false;
+                    for (uint32_t j = lane; j < nc; j += 32) {
+                        double t, resp;
                         const uint32_t i = cs.at(j);
-                        if (survivor(a, i, o, d, inv, t_max, t, resp) &&
-                            (first || before(last_t, last_i, t, i)) && (!have || before(t, i, bt, bi))) {
+                        if (survivor(a, i, o, d, inv, t_max, t, resp) && c.after(t, i) &&
+                            (!have || before(t, i, bt, bi))) {
                             bt = t; br = resp; bi = i; have = true;
                         }
                     }
+                    if (!warp_argmin(bt, br, bi, have)) break;
+                    c.add(bt, br, bi);
                 }
             }
-            // warp arg-min over (t, index)
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
-                const double orr = __shfl_xor_sync(0xffffffffu, br, off);
-                const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                const bool oh = __shfl_xor_sync(0xffffffffu, have, off);
-                if (oh && (!have || before(ot, oi, bt, bi))) {
-                    bt = ot; br = orr; bi = oi; have = true;
-                }
-            }
-            if (!have) break;
-            const double alpha = br < kTraceAlphaClamp ? br : kTraceAlphaClamp;  // std::min
-            const double w = alpha * T;
-            depth_sum += bt * w;
-            acc += w;
-            T *= 1.0 - alpha;
-            last_t = bt;
-            last_i = bi;
-            first = false;
-            if (T < kTraceCutoff) break;
+            __syncwarp();
+        }
+        if (a.debug && lane == 0) {
+            atomicAdd(a.debug, 1ull);
+            atomicAdd(a.debug + 1, (unsigned long long)nc);
         }
         if (lane == 0) {
-            const bool hit = acc >= a.alpha_threshold;
+            const bool hit = c.acc >= a.alpha_threshold;
             a.out_hit[ray] = hit ? 1u : 0u;
-            a.out_depth[ray] = hit ? depth_sum / acc : 0.0;
-            a.out_acc[ray] = acc;
+            a.out_depth[ray] = hit ? c.depth_sum / c.acc : 0.0;
+            a.out_acc[ray] = c.acc;
         }
+        __syncwarp();  // the pool is reused by the warp's next ray
     }
 }
 
@@ -513,7 +737,28 @@ void exclusive_scan_u32(const uint32_t* in, uint64_t n, unsigned long long* out,
     scan_add_kernel<<<unsigned(blocks), 1024, 0, s>>>(out, n, scratch, scratch + blocks);
 }
 
+// World ray directions: the sensor rotation applied to the sensor-frame directions (Quat::rotate,
+// math.hpp:139-143, the reference's double operation order).
+__global__ void lidar_rays_kernel(const double* ds, double* dw, uint64_t n, double q0, double q1,
+                                  double q2, double q3) {
+    const dq q{q0, q1, q2, q3};
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const dv3 w = qrotate(q, ldx3(ds, k));
+        dw[3 * k] = w.x;
+        dw[3 * k + 1] = w.y;
+        dw[3 * k + 2] = w.z;
+    }
+}
+
 // ---- launchers -------------------------------------------------------------------------------------
+void launch_lidar_rays(const double* ds, double* dw, uint64_t n, const double* q, int n_sms,
+                       cudaStream_t s) {
+    if (!n) return;
+    const uint64_t want = (n + 255) / 256;
+    lidar_rays_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(n_sms) * 8))),
+                        256, 0, s>>>(ds, dw, n, q[0], q[1], q[2], q[3]);
+}
 void launch_lidar_pose(const LidarArgs& a, int n_sms, cudaStream_t s) {
     const uint64_t want = (a.n + 255) / 256;
     lidar_pose_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(n_sms) * 8))),
@@ -532,11 +777,14 @@ void launch_lidar_scatter(const LidarArgs& a, int n_sms, cudaStream_t s) {
     lidar_scatter_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(n_sms) * 8))),
                            256, 0, s>>>(a);
 }
+void launch_lidar_scatter_big(const LidarArgs& a, int n_sms, cudaStream_t s) {
+    lidar_scatter_big_kernel<<<unsigned(n_sms) * 8, 256, 0, s>>>(a);
+}
 void launch_lidar_trace(const LidarArgs& a, int n_sms, cudaStream_t s) {
     if (!a.n_rays) return;
     const uint64_t want = (a.n_rays * 32 + 255) / 256;
     lidar_trace_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(n_sms) * 16))),
-                         256, 0, s>>>(a);
+                         32 * kTraceWarps, 0, s>>>(a);
 }
 void launch_lidar_emit(const LidarArgs& a, int n_sms, cudaStream_t s) {
     if (!a.n_rays) return;

@@ -14,6 +14,7 @@
 #include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
 #include "gsim/splat_ply.hpp"
+#include "gsim/trace.hpp"
 #include "gsim/transfer.hpp"
 #include "gsim_gpu.hpp"
 #include "png.h"  // oracle/png_capture: the row bytes the reference writers hand to libpng
@@ -252,6 +253,57 @@ int main() {
         try { render_depth_ring(small, 7, 6.0, 48); } catch (const validation_error&) { ref_threw = true; }
         try { gpu::render_depth_ring(small, 7, 6.0, 48); } catch (const validation_error&) { gpu_threw = true; }
         std::printf("render_depth_ring validation_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
+        if (!ref_threw || !gpu_threw) ++failures;
+    }
+
+    // LiDAR (trace.cpp): GaussianBvh::scan and trace vs gsim::gpu
+    {
+        GaussianField f = oracle::random_field(91, 2500, 2.0, 0.02, 0.15, 0);
+        std::vector<SceneNode> ln(2);
+        ln[0] = {"bg", NodeKind::background, RigidTransform::identity(), {0, 1600}};
+        ln[1] = {"obj", NodeKind::interactive,
+                 RigidTransform{Quat::from_axis_angle({0, 0, 1}, 0.3), {0.2, 0.1, 0.0}}, {1600, 2500}};
+        LidarModel lid;
+        lid.id = "l0";
+        for (int c = 0; c < 16; ++c) lid.channels.push_back((-15.0 + 2.0 * c) * kPi / 180.0);
+        lid.azimuth_step = 2.0 * kPi / 180.0;
+        lid.max_range = 10.0;
+        lid.pose = RigidTransform{Quat::from_axis_angle({1, 0, 0}, 0.1), {0.1, -0.2, 0.05}};
+        const GaussianBvh bvh = GaussianBvh::build(f, ln);
+        const PointCloud a = bvh.scan(lid);
+        const PointCloud b = gpu::lidar_scan(f, ln, lid);
+        double worst = 0.0;
+        bool same = a.size() == b.size();
+        for (std::size_t k = 0; same && k < a.size(); ++k) {
+            same = a.ring[k] == b.ring[k] && a.azimuth[k] == b.azimuth[k];
+            worst = std::fmax(worst, (a.points[k] - b.points[k]).norm());
+        }
+        std::printf("lidar_scan: %zu returns (reference %zu), order %s, max point distance %.3g m\n",
+                    b.size(), a.size(), same ? "equal" : "DIFFERENT", worst);
+        if (!same || worst > 1e-12) ++failures;
+        std::vector<Ray> rays;
+        for (int k = 0; k < 64; ++k) {
+            Ray r;
+            r.origin = {0.1 * (k % 5) - 0.2, 0.05 * (k % 7), -0.1};
+            r.direction = Vec3{std::cos(0.1 * k), std::sin(0.1 * k), 0.05 * (k % 3)}.normalized();
+            r.t_max = 6.0;
+            rays.push_back(r);
+        }
+        const auto tg = gpu::trace(f, ln, rays, 0.5);
+        std::size_t trace_bad = 0;
+        for (std::size_t k = 0; k < rays.size(); ++k) {
+            const TraceResult t = bvh.trace(rays[k], 0.5);
+            trace_bad += t.hit != tg[k].hit || std::fabs(t.depth - tg[k].depth) > 1e-12 ||
+                         std::fabs(t.accum_alpha - tg[k].accum_alpha) > 1e-12;
+        }
+        std::printf("trace: %zu of %zu rays differ\n", trace_bad, rays.size());
+        if (trace_bad) ++failures;
+        LidarModel bad = lid;
+        bad.azimuth_step = 7.0 * kPi / 180.0;
+        bool ref_threw = false, gpu_threw = false;
+        try { bvh.scan(bad); } catch (const validation_error&) { ref_threw = true; }
+        try { gpu::lidar_scan(f, ln, bad); } catch (const validation_error&) { gpu_threw = true; }
+        std::printf("lidar validation_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
         if (!ref_threw || !gpu_threw) ++failures;
     }
 

@@ -99,3 +99,14 @@ def test_lidar_validation(ctx, oracle):
     empty = GaussianField(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros(0),
                           np.zeros((0, 48)), 0)
     assert len(ctx.lidar_scan(ctx.upload(empty), [], LidarModel(**good))["ring"]) == 0
+
+
+def test_scan_dense_windows(ctx, oracle):
+    """Hundreds of survivors per ray: the histogram windows over the candidate cache."""
+    f = oracle.random_field(44, 20000, 0.6, 0.01, 0.05, 0)
+    f.opacities[:] = 0.05  # slow saturation: many windows per ray
+    f.touch()
+    lid = LidarModel(np.radians(np.linspace(-20, 20, 6)), np.radians(4.0), 5.0)
+    got = ctx.lidar_scan(ctx.upload(f), [], lid)
+    assert_scan_close(got, oracle.lidar_scan(f, [], lid))
+    assert len(got["ring"]) > 0
