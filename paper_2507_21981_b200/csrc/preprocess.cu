@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) pose_kernel(DevField f, uint64_t begin, u
 }
 
 // ---- K2: project + shade_sh (raster.cpp:66-163, sh.cpp:10-51) ---------------------------
-template <int DEG, bool kFull, int NT, int MINB>
+template <int DEG, bool kFull, int NT, int MINB, bool kSmemCams>
 __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs args) {
     __shared__ uint64_t s_seg_begin[kMaxSmemSegments];
     __shared__ DevCamera s_cams[kMaxSmemCams];
@@ -138,8 +138,9 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
     for (int k = threadIdx.x; k < n_seg_smem; k += blockDim.x) s_seg_begin[k] = args.segs[k].begin;
     // Cameras are read in every iteration of the camera loop: shared memory keeps those reads
     // off the L1 miss path.
-    const bool cams_smem = args.n_cams <= uint32_t(kMaxSmemCams);
-    if (cams_smem) {
+    // kSmemCams: the batch has at most kMaxSmemCams cameras (the loop then reads shared memory
+    // only, no generic loads)
+    if (kSmemCams) {
         static_assert(sizeof(DevCamera) % 8 == 0, "DevCamera copy");
         const uint64_t* src = reinterpret_cast<const uint64_t*>(args.cams);
         uint64_t* dst = reinterpret_cast<uint64_t*>(s_cams);
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
 
         for (uint32_t e = 0; e < seg.entry_count; ++e) {
             const SegEntry ent = args.entries[seg.entry_begin + e];
-            const DevCamera& cam = cams_smem ? s_cams[ent.cam] : args.cams[ent.cam];
+            const DevCamera& cam = kSmemCams ? s_cams[ent.cam] : args.cams[ent.cam];
             const uint64_t slot = ent.slot_base + (i - seg.begin);
 
             const dq cq{cam.q[0], cam.q[1], cam.q[2], cam.q[3]};
@@ -355,10 +356,14 @@ static void launch_pre_deg(const PreprocessArgs& a, bool full, uint64_t n, int n
     constexpr int kNT = 128, kMinB = 5;
     const unsigned grid =
         unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + kNT - 1) / kNT, uint64_t(n_sms) * kMinB)));
-    if (full)
-        preprocess_kernel<DEG, true, kNT, kMinB><<<grid, kNT, 0, s>>>(a);
-    else
-        preprocess_kernel<DEG, false, kNT, kMinB><<<grid, kNT, 0, s>>>(a);
+    const bool smem_cams = a.n_cams <= uint32_t(kMaxSmemCams);
+    if (full) {
+        if (smem_cams) preprocess_kernel<DEG, true, kNT, kMinB, true><<<grid, kNT, 0, s>>>(a);
+        else preprocess_kernel<DEG, true, kNT, kMinB, false><<<grid, kNT, 0, s>>>(a);
+    } else {
+        if (smem_cams) preprocess_kernel<DEG, false, kNT, kMinB, true><<<grid, kNT, 0, s>>>(a);
+        else preprocess_kernel<DEG, false, kNT, kMinB, false><<<grid, kNT, 0, s>>>(a);
+    }
 }
 
 void launch_preprocess(const PreprocessArgs& a, bool full, int n_sms, cudaStream_t stream) {
