@@ -22,8 +22,9 @@
 // pair position comes from one redux.sync.or of the records' start bits and a popc. The lanes
 // of a step hitting the same tile come from one shared atomicOr of the lane bit into the
 // tile's bitmap (match.any issues at ~1 per 40 SM cycles on sm_100 and is avoided); they are
-// ranked by lane. The result equals the reference's stable (tile, depth, primitive) order bit
-// for bit.
+// ranked by lane. Cameras with many tiles use a u8 last-writer probe instead (a quarter of the
+// shared memory) and rank with ballots only when two lanes collide. The result equals the
+// reference's stable (tile, depth, primitive) order bit for bit.
 #include <cstdint>
 
 #include "common.cuh"
@@ -44,8 +45,10 @@ __device__ __forceinline__ uint32_t rect_area(uint32_t r) {
     return (((r >> 16) & 255u) - (r & 255u) + 1u) * ((r >> 24) - ((r >> 8) & 255u) + 1u);
 }
 
-__host__ __device__ inline size_t bin_warp_bytes(int max_cells) {
-    return size_t(max_cells) * 8;  // u32 counters / positions + u32 peer bitmap per cell
+// Per-warp scatter tables: u32 counters / positions per cell plus either a u32 lane bitmap
+// (bitmap peers) or a u8 last-writer probe (large cameras: a quarter of the bytes).
+__host__ __device__ inline size_t bin_warp_bytes(int max_cells, bool bitmap) {
+    return bitmap ? size_t(max_cells) * 8 : (size_t(max_cells) * 5 + 15) & ~size_t(15);
 }
 
 struct Unit {
@@ -395,12 +398,14 @@ __global__ void __launch_bounds__(1024) bin_campre_kernel(BinArgs a) {
 // ---- scatter: one CTA per unit ----------------------------------------------------------------
 // Shared memory per warp: [tiles_y][tiles_x + 1] u32 counters, turned into first positions, and
 // a u32 lane bitmap per cell (bin_warp_bytes).
+template <bool kBitmap>
 __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     extern __shared__ __align__(16) char s_bin[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const size_t wbytes = bin_warp_bytes(a.max_tc);
+    const size_t wbytes = bin_warp_bytes(a.max_tc, kBitmap);
     uint32_t* pos = reinterpret_cast<uint32_t*>(s_bin + warp * wbytes);
     uint32_t* peer_bits = pos + a.max_tc;
+    uint8_t* probe = reinterpret_cast<uint8_t*>(pos + a.max_tc);
     // row-major position -> (row, column) with a magic reciprocal per rect width: for
     // kk < 2^16 and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
     __shared__ uint32_t s_magic[257];
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         // 1. this warp's pairs per tile (row differences, then row scans in place)
         int* D = reinterpret_cast<int*>(pos);
         for (int t = lane; t < wd * u.tiles_y; t += 32) D[t] = 0;
-        if (k == blockIdx.x)  // the bitmaps are left cleared by every step
+        if (kBitmap && k == blockIdx.x)  // the bitmaps are left cleared by every step
             for (int t = lane; t < wd * u.tiles_y; t += 32) peer_bits[t] = 0u;
         __syncwarp();
         walk_groups<false>(a, wb, we, [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
@@ -472,24 +477,50 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                 const uint32_t w = tx1 - tx0 + 1u;
                 const uint32_t q = mg ? __umulhi(kk, mg) : kk;
                 const uint32_t cell = (ty0 + q) * uint32_t(wd) + tx0 + (kk - q * w);
-                // lanes of this step on the same cell, from one atomicOr into the cell's
-                // bitmap; ranked by lane (= emission) order, the lowest lane bumps the
-                // position and clears the bitmap
-                if (in) atomicOr(&peer_bits[cell], 1u << lane);
-                __syncwarp();
-                const uint32_t peers = in ? peer_bits[cell] : 0u;
-                const uint32_t below = peers & lanemask_lt();
-                __syncwarp();
-                uint32_t pre = 0;
-                if (in && below == 0) {
-                    pre = pos[cell];
-                    pos[cell] = pre + __popc(peers);
-                    peer_bits[cell] = 0u;
-                }
-                pre = __shfl_sync(kFull, pre, in ? __ffs(peers) - 1 : lane);
-                if (in) {
-                    const uint32_t p = pre + __popc(below);
-                    if (p < a.capacity) a.vals_out[p] = sl;
+                if (kBitmap) {
+                    // lanes of this step on the same cell, from one atomicOr into the cell's
+                    // bitmap; ranked by lane (= emission) order, the lowest lane bumps the
+                    // position and clears the bitmap
+                    if (in) atomicOr(&peer_bits[cell], 1u << lane);
+                    __syncwarp();
+                    const uint32_t peers = in ? peer_bits[cell] : 0u;
+                    const uint32_t below = peers & lanemask_lt();
+                    __syncwarp();
+                    uint32_t pre = 0;
+                    if (in && below == 0) {
+                        pre = pos[cell];
+                        pos[cell] = pre + __popc(peers);
+                        peer_bits[cell] = 0u;
+                    }
+                    pre = __shfl_sync(kFull, pre, in ? __ffs(peers) - 1 : lane);
+                    if (in) {
+                        const uint32_t p = pre + __popc(below);
+                        if (p < a.capacity) a.vals_out[p] = sl;
+                    }
+                } else {
+                    // last-writer probe: did another lane of this step write the same cell?
+                    if (in) probe[cell] = uint8_t(lane);
+                    __syncwarp();
+                    const bool lost = in && probe[cell] != uint8_t(lane);
+                    if (!__any_sync(kFull, lost)) {
+                        if (in) {
+                            const uint32_t p = pos[cell];
+                            pos[cell] = p + 1u;
+                            if (p < a.capacity) a.vals_out[p] = sl;
+                        }
+                    } else {  // rank the lanes of each cell by lane order from ballots
+                        const uint32_t m = __ballot_sync(kFull, in);
+                        const uint32_t tile = (ty0 + q) * uint32_t(u.tiles_x) + tx0 + (kk - q * w);
+                        const uint32_t peers = peers_of_bits(kFull, tile, u.tbits) & m;
+                        const uint32_t below = peers & lanemask_lt();
+                        const uint32_t pre = in ? pos[cell] : 0u;
+                        __syncwarp();
+                        if (in) {
+                            if (below == 0) pos[cell] = pre + __popc(peers);
+                            const uint32_t p = pre + __popc(below);
+                            if (p < a.capacity) a.vals_out[p] = sl;
+                        }
+                    }
                 }
                 __syncwarp();
             }
@@ -503,7 +534,9 @@ void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
     key_hist_kernel<<<grid, kThreads, 0, s>>>(a);
 }
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 1024, 0, s>>>(a); }
-size_t bin_smem_bytes(const BinArgs& a) { return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc); }
+size_t bin_smem_bytes(const BinArgs& a) {
+    return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc, a.bitmap_peers != 0);
+}
 void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = size_t(a.max_tc) * sizeof(int);
     cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -518,8 +551,13 @@ void launch_bin_tilescan(const BinArgs& a, int grid, cudaStream_t s) {
 void launch_bin_campre(const BinArgs& a, cudaStream_t s) { bin_campre_kernel<<<1, 1024, 0, s>>>(a); }
 void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = bin_smem_bytes(a);
-    cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    bin_scatter_kernel<<<grid, 32 * a.bin_warps, smem, s>>>(a);
+    if (a.bitmap_peers) {
+        cudaFuncSetAttribute(bin_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        bin_scatter_kernel<true><<<grid, 32 * a.bin_warps, smem, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(bin_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        bin_scatter_kernel<false><<<grid, 32 * a.bin_warps, smem, s>>>(a);
+    }
 }
 
 }  // namespace gsim_gpu

@@ -490,19 +490,25 @@ void record_ev(gsim_gpu_context* ctx, int e) {
 
 void check_launch() { GSIM_CK(cudaGetLastError()); }
 
+// The scatter's peer method by camera size: lane bitmaps (8 B per tile-grid cell and warp) up to
+// kBitmapCells cells, the u8 probe (5 B) beyond, so large cameras keep several warps per SM.
+constexpr uint32_t kBitmapCells = 2048;
+
+bool bitmap_peers_for(uint32_t max_tc) { return max_tc <= kBitmapCells; }
+
 int bin_warps_for(uint32_t max_tc) {
-    // u32 counter + u32 lane bitmap per grid cell per warp (bin.cu bin_warp_bytes)
     static const int cap = [] {
         const char* e = std::getenv("GSIM_GPU_BIN_WARPS");
         const int v = e ? std::atoi(e) : 4;  // 4 measured faster than 8 (occupancy)
         return v >= 1 && v <= 8 ? v : 4;
     }();
-    const size_t per_warp = size_t(max_tc) * 8;
+    const size_t per_warp = bitmap_peers_for(max_tc) ? size_t(max_tc) * 8
+                                                     : (size_t(max_tc) * 5 + 15) & ~size_t(15);
     const size_t budget = 200 * 1024;
     const int w = int(std::min<size_t>(size_t(cap), budget / std::max<size_t>(per_warp, 1)));
     if (w < 1)
         throw ValidationError{"camera with " + std::to_string(max_tc) +
-                              " tiles exceeds the binning shared-memory budget (25600 tiles)"};
+                              " tiles exceeds the binning shared-memory budget (40960 tiles)"};
     return w;
 }
 
@@ -576,6 +582,7 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
     b.capacity = ctx->pair_capacity;
     b.max_tc = int(p.max_tc);
     b.bin_warps = bin_warps_for(p.max_tc);
+    b.bitmap_peers = bitmap_peers_for(p.max_tc) ? 1 : 0;
     b.chunk_records = kWarpRecords * b.bin_warps;
     return b;
 }

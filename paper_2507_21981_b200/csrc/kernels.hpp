@@ -87,7 +87,7 @@ struct BinArgs {
     int max_tc;                      // largest (tiles_x + 1) * (tiles_y + 1) of the batch
     int chunk_records;               // records per unit = 1024 * bin_warps
     int bin_warps;                   // warps per unit CTA
-    int reserved;
+    int bitmap_peers;                // scatter: lane bitmaps (small cameras) or probe
 };
 
 struct RasterArgs {

@@ -89,6 +89,25 @@ def test_tile_lists_bit_exact(ctx, oracle):
         assert np.array_equal(values, splats["prim_index"][vals]), scene
 
 
+def test_tile_lists_bit_exact_large_camera(ctx, oracle):
+    """A 1280x720 camera (81 x 46 tile-grid cells): the scatter ranks same-tile lanes with the
+    last-writer probe and ballots instead of lane bitmaps (bin.cu kBitmap = false)."""
+    cam = ref_camera(1280, 720, 700.0)
+    f = oracle.random_field(8080, 30000, 3.0, 0.01, 0.3, 1)
+    f.means[:, 2] += 3.0
+    f.touch()
+    nodes = two_nodes(30000)
+    s = ctx.upload(f)
+    g = ctx.render(s, nodes, [cam])[0]
+    offsets, values = ctx.tile_lists(0)
+    splats = oracle.project(f, nodes, cam)
+    tb, vals = oracle.rasterize_lists(splats, cam)
+    assert len(vals) > 100000
+    assert np.array_equal(offsets[: len(tb)], tb)
+    assert np.array_equal(values, splats["prim_index"][vals])
+    assert_parity(g, oracle.rasterize(splats, cam), "1280x720")
+
+
 # ---- K4 / end to end ----------------------------------------------------------------------------
 
 def test_render_parity_acceptance_scenes(ctx, oracle):
