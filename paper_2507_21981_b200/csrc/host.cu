@@ -790,7 +790,7 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
     finish_stats(ctx, plan, launches);
 }
 
-void check_pending(gsim_gpu_context* ctx);
+bool check_pending(gsim_gpu_context* ctx);
 
 // A camera batch is rendered in groups whose (camera | depth) record keys fit 32 bits and whose
 // (camera, primitive) slots stay below 2^31: e.g. BASELINE config 2 (320 cameras, near/far
@@ -849,14 +849,15 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
 // Completes the deferred pair-count check of an asynchronous render: by now its readback has
 // long landed; on overflow the buffers of that frame are still intact (nothing new has been
 // enqueued), so scatter + raster are re-run into the same output before anything else.
-void check_pending(gsim_gpu_context* ctx) {
-    if (!ctx->pending) return;
+// Returns whether they were re-run.
+bool check_pending(gsim_gpu_context* ctx) {
+    if (!ctx->pending) return false;
     ctx->pending = false;
     GSIM_CK(cudaEventSynchronize(ctx->bin_ev));
     const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
     ctx->stats.visible = rb[0];
     ctx->stats.pairs = rb[1];
-    if (rb[1] <= ctx->pair_capacity) return;
+    if (rb[1] <= ctx->pair_capacity) return false;
     GSIM_CK(cudaStreamSynchronize(ctx->stream));
     ctx->pair_capacity = rb[1] + rb[1] / 4 + (1u << 20);
     ctx->vals.reserve(ctx->pair_capacity);
@@ -872,6 +873,7 @@ void check_pending(gsim_gpu_context* ctx) {
     ctx->frame_enc = enc;
     ctx->frame_enc_only = enc_only;
     GSIM_CK(cudaStreamSynchronize(ctx->stream));
+    return true;
 }
 
 // ---- output encoding (image_io.cpp) ---------------------------------------------------------
@@ -1151,6 +1153,7 @@ gsim_gpu_scene* load_ply(gsim_gpu_context* ctx, const std::string& path) {
 // D2H of the internal output buffer into host RenderTargets (the drop-in's by-value return).
 void copy_targets(gsim_gpu_context* ctx, const gsim_camera* cameras, uint64_t n,
                   const std::vector<uint64_t>& off, gsim_target* outs) {
+    ctx->stats.d2h_bytes = 0;
     for (uint64_t c = 0; c < n; ++c) {
         const size_t npx = size_t(cameras[c].width) * cameras[c].height;
         const float* base = ctx->out.ptr + off[c];
@@ -1746,9 +1749,13 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
     return Guard(ctx).run([&] {
         if (!scene || (n_cameras && (!cameras || !outs)) || (n_nodes && !nodes))
             throw ValidationError{"render: null argument"};
+        // Asynchronous render with the copies queued behind it: the pair-buffer check is done
+        // once at the end (no mid-frame host round trip); on an overflow the tail is re-run
+        // and the targets copied again.
         const std::vector<uint64_t> off =
-            render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, true);
+            render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, false);
         copy_targets(ctx, cameras, n_cameras, off, outs);
+        if (check_pending(ctx)) copy_targets(ctx, cameras, n_cameras, off, outs);
     });
 }
 
@@ -1860,11 +1867,18 @@ int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
         ctx->frame_enc = e;
         ctx->frame_enc_only = true;
         render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, raster_options, nullptr,
-                       !out_is_device);
-        if (!out_is_device && bytes) {
-            GSIM_CK(cudaMemcpyAsync(out, ctx->enc_buf.ptr, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-            GSIM_CK(cudaStreamSynchronize(ctx->stream));
-            ctx->stats.d2h_bytes = bytes;
+                       false);
+        if (!out_is_device) {
+            // one check at the end, as gsim_gpu_render; the encoding of a re-run tail is part
+            // of its raster epilogue (check_pending restores the frame's encode parameters)
+            for (int pass = 0; pass < 2; ++pass) {
+                if (bytes)
+                    GSIM_CK(cudaMemcpyAsync(out, ctx->enc_buf.ptr, bytes, cudaMemcpyDeviceToHost,
+                                            ctx->stream));
+                GSIM_CK(cudaStreamSynchronize(ctx->stream));
+                ctx->stats.d2h_bytes = bytes;
+                if (!check_pending(ctx)) break;
+            }
         }
     });
 }
@@ -1999,8 +2013,11 @@ int gsim_gpu_render_at(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
         ctx->frame_node_track = node_track;
         const bool host = outs != nullptr;
         const std::vector<uint64_t> off = render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras,
-                                                         options, host ? nullptr : device_out, host);
-        if (host) copy_targets(ctx, cameras, n_cameras, off, outs);
+                                                         options, host ? nullptr : device_out, false);
+        if (host) {
+            copy_targets(ctx, cameras, n_cameras, off, outs);
+            if (check_pending(ctx)) copy_targets(ctx, cameras, n_cameras, off, outs);
+        }
     });
 }
 
