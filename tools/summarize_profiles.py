@@ -115,10 +115,16 @@ def main() -> None:
     if a.report:
         rows, units = raw_report(Path(a.report))
         scale_to = {"us": {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3},
-                    "MB": {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1, "Gbyte": 1e3}}
+                    "MB": {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1, "Gbyte": 1e3},
+                    "GB/s": {"byte/s": 1e-9, "Kbyte/s": 1e-6, "Mbyte/s": 1e-3, "Gbyte/s": 1,
+                             "Tbyte/s": 1e3}}
         keys = [("gpu__time_duration.sum", "us", None), ("dram__bytes_read.sum", "MB", None),
                 ("dram__bytes_write.sum", "MB", None),
+                ("dram__bytes.sum.per_second", "GB/s", None),
                 ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "% DRAM", 1),
+                ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "% L2", 1),
+                ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                 "% smem", 1),
                 ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "% SM", 1),
                 ("smsp__issue_active.avg.pct_of_peak_sustained_active", "% issue", 1),
                 ("sm__warps_active.avg.per_cycle_active", "warps/SM", 1),
