@@ -59,6 +59,7 @@ __device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoc
     while (true) {
         const uint64_t s = ld_volatile_u64(p);
         if ((s >> 62) != 0 && uint32_t((s >> 40) & kEpochMask) == (epoch & kEpochMask)) return s;
+        __nanosleep(64);  // back off: spinning warps would steal issue slots from working ones
     }
 }
 
