@@ -446,9 +446,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         __syncthreads();
         // 3. place this warp's pairs in emission order
         walk_groups<true>(a, wb, we, [&](uint32_t slot, uint32_t r, bool valid) {
-            const uint32_t cnt = valid ? (((r >> 16) & 255u) - (r & 255u) + 1u) *
-                                             ((r >> 24) - ((r >> 8) & 255u) + 1u)
-                                       : 0u;
+            const uint32_t cnt = valid ? rect_area(r) : 0u;
             uint32_t incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
