@@ -202,44 +202,62 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
     }
 }
 
+// Inclusive scan of one u64 per thread over the block (blockDim.x <= 1024) with warp shuffles:
+// two barriers instead of a log-step shared-memory scan. *total = the block's sum.
+__device__ unsigned long long block_scan_u64(unsigned long long v, unsigned long long* s_w,
+                                             unsigned long long* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) s_w[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long x = lane < nw ? s_w[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += t;
+        }
+        if (lane < nw) s_w[lane] = x;
+    }
+    __syncthreads();
+    if (warp > 0) v += s_w[warp - 1];
+    *total = s_w[nw - 1];
+    __syncthreads();
+    return v;
+}
+
 // ---- per-camera unit tables (one block) -----------------------------------------------------
-__global__ void __launch_bounds__(1024) chunk_table_kernel(BinArgs a) {
-    __shared__ unsigned long long s_scan[1024];
+__global__ void __launch_bounds__(256) chunk_table_kernel(BinArgs a) {
+    __shared__ unsigned long long s_w[32];
     __shared__ unsigned long long s_carry[3];
     const int tid = threadIdx.x;
     if (tid < 3) s_carry[tid] = 0;
     __syncthreads();
     const uint32_t R = uint32_t(a.chunk_records);
-    auto scan = [&](unsigned long long v) {  // inclusive block scan
-        s_scan[tid] = v;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const unsigned long long t = tid >= o ? s_scan[tid - o] : 0ull;
-            __syncthreads();
-            s_scan[tid] += t;
-            __syncthreads();
-        }
-        const unsigned long long r = s_scan[tid];
-        __syncthreads();
-        return r;
-    };
-    for (int c0 = 0; c0 < a.n_cams; c0 += 1024) {
+    for (int c0 = 0; c0 < a.n_cams; c0 += blockDim.x) {
         const int c = c0 + tid;
         const uint32_t v = c < a.n_cams ? a.cam_visible[c] : 0u;
         const uint32_t k = (v + R - 1) / R;
         const uint32_t tc = c < a.n_cams ? a.cam_tile_base[c + 1] - a.cam_tile_base[c] : 0u;
         const unsigned long long m = (unsigned long long)k * tc;
-        const unsigned long long iv = scan(v), ik = scan(k), im = scan(m);
+        unsigned long long tv, tk, tm;
+        const unsigned long long iv = block_scan_u64(v, s_w, &tv);
+        const unsigned long long ik = block_scan_u64(k, s_w, &tk);
+        const unsigned long long im = block_scan_u64(m, s_w, &tm);
         if (c < a.n_cams) {
             a.cam_vbase[c] = uint32_t(s_carry[0] + iv - v);
             a.cam_chunk_base[c] = uint32_t(s_carry[1] + ik - k);
             a.cam_mbase[c] = s_carry[2] + im - m;
         }
         __syncthreads();
-        if (tid == 1023) {
-            s_carry[0] += iv;
-            s_carry[1] += ik;
-            s_carry[2] += im;
+        if (tid == 0) {
+            s_carry[0] += tv;
+            s_carry[1] += tk;
+            s_carry[2] += tm;
         }
         __syncthreads();
     }
@@ -252,7 +270,7 @@ __global__ void __launch_bounds__(1024) chunk_table_kernel(BinArgs a) {
     }
     __syncthreads();
     const uint32_t K = uint32_t(s_carry[1]);
-    for (uint32_t k = tid; k < K; k += 1024)
+    for (uint32_t k = tid; k < K; k += blockDim.x)
         a.chunk_cam[k] = uint32_t(upper_index(a.cam_chunk_base, a.n_cams, k));
 }
 
@@ -367,26 +385,20 @@ __global__ void __launch_bounds__(1024) bin_tilescan_kernel(BinArgs a) {
 }
 
 // ---- camera pair bases (one block) -------------------------------------------------------------
-__global__ void __launch_bounds__(1024) bin_campre_kernel(BinArgs a) {
-    __shared__ unsigned long long s_m[1024];
+__global__ void __launch_bounds__(256) bin_campre_kernel(BinArgs a) {
+    __shared__ unsigned long long s_w[32];
     __shared__ unsigned long long s_carry;
     const int tid = threadIdx.x;
     if (tid == 0) s_carry = 0;
     __syncthreads();
-    for (int c0 = 0; c0 < a.n_cams; c0 += 1024) {
+    for (int c0 = 0; c0 < a.n_cams; c0 += blockDim.x) {
         const int c = c0 + tid;
         const unsigned long long v = c < a.n_cams ? a.cam_pairs[c] : 0ull;
-        s_m[tid] = v;
+        unsigned long long tot;
+        const unsigned long long inc = block_scan_u64(v, s_w, &tot);
+        if (c < a.n_cams) a.cam_pair_base[c] = s_carry + inc - v;
         __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const unsigned long long t = tid >= o ? s_m[tid - o] : 0ull;
-            __syncthreads();
-            s_m[tid] += t;
-            __syncthreads();
-        }
-        if (c < a.n_cams) a.cam_pair_base[c] = s_carry + s_m[tid] - v;
-        __syncthreads();
-        if (tid == 1023) s_carry += s_m[1023];
+        if (tid == 0) s_carry += tot;
         __syncthreads();
     }
     if (tid == 0) {
@@ -531,7 +543,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
 void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
     key_hist_kernel<<<grid, kThreads, 0, s>>>(a);
 }
-void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 1024, 0, s>>>(a); }
+void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 256, 0, s>>>(a); }
 size_t bin_smem_bytes(const BinArgs& a) {
     return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc, a.bitmap_peers != 0);
 }
@@ -546,7 +558,7 @@ void launch_bin_colscan(const BinArgs& a, int grid, cudaStream_t s) {
 void launch_bin_tilescan(const BinArgs& a, int grid, cudaStream_t s) {
     bin_tilescan_kernel<<<grid, 1024, 0, s>>>(a);
 }
-void launch_bin_campre(const BinArgs& a, cudaStream_t s) { bin_campre_kernel<<<1, 1024, 0, s>>>(a); }
+void launch_bin_campre(const BinArgs& a, cudaStream_t s) { bin_campre_kernel<<<1, 256, 0, s>>>(a); }
 void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = bin_smem_bytes(a);
     if (a.bitmap_peers) {
