@@ -18,10 +18,11 @@ ap.add_argument("report")
 ap.add_argument("kernel")
 ap.add_argument("--top", type=int, default=25)
 ap.add_argument("--by", default="samples", choices=["samples", "inst"])
+ap.add_argument("--skip", type=int, default=0, help="launches of the kernel to skip")
 a = ap.parse_args()
 
 out = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--kernel-name", a.kernel,
-                      "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+                      "--print-source", "cuda,sass", "--launch-skip", str(a.skip), "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = None
 cur = None
