@@ -81,13 +81,15 @@ struct alignas(16) Record {
 constexpr float kLog2eF = 1.4426950408889634f;
 
 // Builds the raster record from the fp32 projection (u, v, depth, radius, inverse covariance,
-// peak alpha, rgb). The exponent of ex2 is then log2(o) + dx*(A*dx + B*dy) + C*dy*dy, i.e.
+// peak alpha, rgb). Record.b = (B, C, A, depth); the exponent of ex2 is then
+// log2(o) + dx*(A*dx + B*dy) + C*dy*dy, i.e.
 // log2(o * exp(-q/2)) with q = inv_xx dx^2 + 2 inv_xy dx dy + inv_yy dy^2 (raster.cpp:226-229).
 __device__ inline Record make_record(float u, float v, float z, float rad, float ia, float ib,
                                      float ic, float op, float r, float g, float b) {
     Record rec;
     rec.a = make_float4(u, v, rad, __log2f(op));
-    rec.b = make_float4(ia * (-0.5f * kLog2eF), ib * -kLog2eF, ic * (-0.5f * kLog2eF), z);
+    // (B, C) first: the blend scales them by dy as one aligned register pair (FMUL2)
+    rec.b = make_float4(ib * -kLog2eF, ic * (-0.5f * kLog2eF), ia * (-0.5f * kLog2eF), z);
     // Reachable half-extents: the box test bounds |dx|,|dy| <= r; alpha >= 1/255 needs
     // q <= qc = 2 ln(255 o), whose ellipse has half-extents sqrt(qc * cov_xx/yy) (conservatively
     // widened), so no contributing splat is ever culled by them.

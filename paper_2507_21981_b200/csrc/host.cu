@@ -635,7 +635,12 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     oa.n_dev = ctx->counts.ptr + 0;
     oa.status = ctx->status.ptr;
     uint64_t dgrid = (S + kOnesweepTile - 1) / kOnesweepTile;
-    dgrid = std::max<uint64_t>(1, std::min<uint64_t>(dgrid, uint64_t(n_sms) * 3));
+    static const int sort_ctas = [] {
+        const char* e = std::getenv("GSIM_GPU_SORT_CTAS");  // resident onesweep CTAs per SM
+        const int v = e ? std::atoi(e) : 3;
+        return v < 1 ? 1 : v > 3 ? 3 : v;
+    }();
+    dgrid = std::max<uint64_t>(1, std::min<uint64_t>(dgrid, uint64_t(n_sms) * sort_ctas));
     const uint32_t* kin = ctx->keys.ptr;
     const uint32_t* vin = nullptr;
     for (int pass = 0; pass < 4; ++pass) {

@@ -66,7 +66,7 @@ __device__ __forceinline__ float2 gate(float e0, float e1, float adx0, float adx
     return o;
 }
 
-// Record at a 16-bit shared-memory address (the compacted list holds addresses, so the blend
+// Record at a shared-memory address (the compacted list holds addresses, so the blend
 // loop needs no address arithmetic).
 __device__ __forceinline__ void load_record(uint32_t addr, float4& a, float4& b, float4& c) {
     asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%12];\n\t"
@@ -91,7 +91,7 @@ constexpr float kNoClampLog2 = -0.015957f;  // log2(0.989) rounded down
 // 0.02 margin below log2(1/255) so rounding can never drop a contributing splat.
 __device__ __forceinline__ bool reaches_rect(float4 p0, float4 p1, float x_lo, float x_hi,
                                              float y_lo, float y_hi) {
-    const float A = p1.x, B = p1.y, C = p1.z;
+    const float A = p1.z, B = p1.x, C = p1.y;
     const float dx_lo = p0.x - x_hi, dx_hi = p0.x - x_lo;  // range of dx over the rectangle
     const float dy_lo = p0.y - y_hi, dy_hi = p0.y - y_lo;
     const float dx1 = fminf(fmaxf(0.0f, dx_lo), dx_hi);
@@ -131,36 +131,51 @@ __device__ __forceinline__ void write_pixel(const RasterArgs& a, const DevCamera
 // Front-to-back blend of a warp's compacted list for the thread's pixel pair (raster.cpp:
 // 221-238). kClamp: some splat of the list can reach the 0.99 alpha clamp.
 template <bool kClamp>
-__device__ __forceinline__ void blend_list(const uint16_t* list, uint32_t count, float2 npx,
+__device__ __forceinline__ void blend_one(uint32_t addr, float2 npx, float py, float cutoff,
+                                          float2& cr, float2& cg, float2& cb, float2& d,
+                                          float2& acc, float2& T) {
+    float4 p0, p1, p2;
+    load_record(addr, p0, p1, p2);
+    // row terms, shared by the pair: (B dy, C dy) on the packed pipe
+    const float dy = p0.y - py;
+    const float2 bcdy = __fmul2_rn(make_float2(p1.x, p1.y), bc(dy));
+    const float kq = fmaf(bcdy.y, dy, p0.w);
+    // pair terms on the packed pipe
+    const float2 dx = __fadd2_rn(bc(p0.x), npx);
+    const float2 t = __ffma2_rn(bc(p1.z), dx, bc(bcdy.x));
+    const float2 E = __ffma2_rn(t, dx, bc(kq));
+    float e0 = ex2_approx(E.x), e1 = ex2_approx(E.y);
+    if (kClamp) {
+        e0 = fminf(e0, 0.99f);
+        e1 = fminf(e1, 0.99f);
+    }
+    const float2 w = __fmul2_rn(gate(e0, e1, fabsf(dx.x), fabsf(dx.y), fabsf(dy), p0.z, T, cutoff), T);
+    cr = __ffma2_rn(bc(p2.x), w, cr);
+    cg = __ffma2_rn(bc(p2.y), w, cg);
+    cb = __ffma2_rn(bc(p2.z), w, cb);
+    d = __ffma2_rn(bc(p1.w), w, d);
+    acc = __fadd2_rn(acc, w);
+    // T * (1 - alpha) == T - w up to rounding; once T < cutoff the gate zeroes every later
+    // weight, so T (and the pixel) stays put: the reference's break.
+    T = __fadd2_rn(T, make_float2(-w.x, -w.y));
+}
+
+// Front-to-back blend of a warp's compacted list for the thread's pixel pair (raster.cpp:
+// 221-238). The list is padded to a multiple of 4 with the null record (r = -1: the box test
+// fails, weight 0, nothing changes), so it is walked 4 entries per 128-bit list load without
+// remainder branches. kClamp: some splat of the list can reach the 0.99 alpha clamp.
+template <bool kClamp>
+__device__ __forceinline__ void blend_list(const uint32_t* list, uint32_t count, float2 npx,
                                            float py, float cutoff, float2& cr, float2& cg,
                                            float2& cb, float2& d, float2& acc, float2& T) {
     for (uint32_t k0 = 0; k0 < count; k0 += 32) {
         const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
-#pragma unroll 4
-        for (uint32_t k = k0; k < k1; ++k) {
-            float4 p0, p1, p2;
-            load_record(list[k], p0, p1, p2);
-            // row terms, shared by the pair
-            const float dy = p0.y - py;
-            const float kq = fmaf(p1.z * dy, dy, p0.w);
-            // pair terms on the packed pipe
-            const float2 dx = __fadd2_rn(bc(p0.x), npx);
-            const float2 t = __ffma2_rn(bc(p1.x), dx, bc(p1.y * dy));
-            const float2 E = __ffma2_rn(t, dx, bc(kq));
-            float e0 = ex2_approx(E.x), e1 = ex2_approx(E.y);
-            if (kClamp) {
-                e0 = fminf(e0, 0.99f);
-                e1 = fminf(e1, 0.99f);
-            }
-            const float2 w = __fmul2_rn(gate(e0, e1, fabsf(dx.x), fabsf(dx.y), fabsf(dy), p0.z, T, cutoff), T);
-            cr = __ffma2_rn(bc(p2.x), w, cr);
-            cg = __ffma2_rn(bc(p2.y), w, cg);
-            cb = __ffma2_rn(bc(p2.z), w, cb);
-            d = __ffma2_rn(bc(p1.w), w, d);
-            acc = __fadd2_rn(acc, w);
-            // T * (1 - alpha) == T - w up to rounding; once T < cutoff the gate zeroes every
-            // later weight, so T (and the pixel) stays put: the reference's break.
-            T = __fadd2_rn(T, make_float2(-w.x, -w.y));
+        for (uint32_t k = k0; k < k1; k += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(list + k);
+            blend_one<kClamp>(q.x, npx, py, cutoff, cr, cg, cb, d, acc, T);
+            blend_one<kClamp>(q.y, npx, py, cutoff, cr, cg, cb, d, acc, T);
+            blend_one<kClamp>(q.z, npx, py, cutoff, cr, cg, cb, d, acc, T);
+            blend_one<kClamp>(q.w, npx, py, cutoff, cr, cg, cb, d, acc, T);
         }
         if (__all_sync(0xffffffffu, T.x < cutoff && T.y < cutoff)) break;
     }
@@ -175,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     constexpr int PC = RW / 2;   // pixel-pair columns of a warp rectangle
     constexpr int WX = 16 / RW;  // warp rectangles per tile row
     __shared__ Record s_spl[2][kBatch];
-    __shared__ uint16_t s_list[kWarps][kBatch];
+    __shared__ __align__(16) uint32_t s_list[kWarps][kBatch];
+    __shared__ Record s_null;  // pads the compacted lists: fails the box test (r = -1)
 
     const uint32_t g = blockIdx.x;
     const int cam_idx = upper_index(a.cam_tile_base, a.n_cams, g);
@@ -230,6 +246,12 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
+    if (tid == 0) {
+        s_null.a = make_float4(0.f, 0.f, -1.f, 0.f);
+        s_null.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        s_null.c = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const uint32_t null_addr = uint32_t(__cvta_generic_to_shared(&s_null));
     uint32_t fetched = 0;
     if (begin < end) {
         load_slots(begin);
@@ -273,9 +295,12 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
                 bright |= __any_sync(0xffffffffu, mine && !(lop <= kNoClampLog2));
                 if (mine)
                     s_list[warp][count + __popc(bits & lanemask_lt())] =
-                        uint16_t(spl_addr + idx * sizeof(Record));
+                        spl_addr + idx * uint32_t(sizeof(Record));
                 count += __popc(bits);
             }
+            const uint32_t padded = (count + 3u) & ~3u;
+            if (count + uint32_t(lane) < padded) s_list[warp][count + lane] = null_addr;
+            count = padded;
             __syncwarp();
             if (bright)
                 blend_list<true>(s_list[warp], count, npx, py, cutoff, cr, cg, cb, d, acc, T);
