@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     __shared__ uint32_t s_vals[kOnesweepTile];
     __shared__ uint32_t s_warp_hist[kWarps][kRadix];
     __shared__ uint32_t s_bstart[kRadix];
-    __shared__ unsigned long long s_dest[kRadix];
+    __shared__ uint32_t s_dest[kRadix];
     __shared__ uint32_t s_tmp[kWarps];
     __shared__ uint32_t s_ticket;
     __shared__ uint32_t s_total;
@@ -102,19 +102,26 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
         __syncthreads();
         const uint32_t t = s_ticket;
         if (t >= chunks) break;
-        const uint64_t base = uint64_t(t) * kOnesweepTile + uint64_t(warp) * (kItems * 32);
-
+        // 32-bit indices: slot counts stay below 2^31 (host.cu splits larger batches)
+        const uint32_t base = t * uint32_t(kOnesweepTile) + uint32_t(warp) * (kItems * 32) + uint32_t(lane);
+        const uint32_t* kin = a.keys_in + base;
+        const uint32_t* vin = a.vals_in + base;
         uint32_t keys[kItems], vals[kItems], rank[kItems];
+        if ((uint64_t(t) + 1) * kOnesweepTile <= n) {  // full chunk: no bounds checks
 #pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const uint64_t idx = base + uint64_t(i) * 32 + lane;
-            const bool in = idx < n;
-            keys[i] = in ? __ldcs(a.keys_in + idx) : kInvalidKey;
-            if (kFirst) vals[i] = uint32_t(idx);
-            else vals[i] = in ? __ldcs(a.vals_in + idx) : 0u;
-            if (!kFirst && !in) keys[i] = kInvalidKey;
-            rank[i] = in ? 1u : 0u;  // reuse as "valid" until ranked
-            if (kFirst && keys[i] == kInvalidKey) rank[i] = 0u;
+            for (int i = 0; i < kItems; ++i) {
+                keys[i] = __ldcs(kin + i * 32);
+                vals[i] = kFirst ? base + uint32_t(i) * 32 : __ldcs(vin + i * 32);
+                rank[i] = (!kFirst || keys[i] != kInvalidKey) ? 1u : 0u;  // "valid" until ranked
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const bool in = uint64_t(base) + uint64_t(i) * 32 < n;
+                keys[i] = in ? __ldcs(kin + i * 32) : kInvalidKey;
+                vals[i] = kFirst ? base + uint32_t(i) * 32 : (in ? __ldcs(vin + i * 32) : 0u);
+                rank[i] = (in && (!kFirst || keys[i] != kInvalidKey)) ? 1u : 0u;
+            }
         }
         // Warp-level stable ranking: item order is (i, lane) = memory order.
 #pragma unroll
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
             }
             st_volatile_u64(my_status, make_status(kFlagInclusive, a.epoch, prefix + count));
         }
-        s_dest[tid] = (unsigned long long)(uint64_t(gbase) + prefix - bstart);
+        s_dest[tid] = uint32_t(uint64_t(gbase) + prefix - bstart);
         if (tid == 0) s_total = block_total;
         __syncthreads();
         // Stage the chunk in smem in sorted order, then write it out in digit runs.
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
         const uint32_t total = s_total;
         for (uint32_t p = tid; p < total; p += kThreads) {
             const uint32_t key = s_keys[p];
-            const uint64_t dst = s_dest[(key >> a.shift) & 255u] + p;
+            const uint32_t dst = s_dest[(key >> a.shift) & 255u] + p;
             if (kWriteKeys) a.keys_out[dst] = key;
             a.vals_out[dst] = s_vals[p];
             if (a.rects_out) a.rects_out[dst] = __ldg(a.rects_in + s_vals[p]);
