@@ -142,62 +142,85 @@ __device__ __forceinline__ uint32_t reduce_or(uint32_t v) {
 }  // namespace
 
 // ---- depth-key histograms + per-camera record counts ---------------------------------------
+// The three low digits are spread over many values: plain shared atomics into per-warp
+// sub-histograms. The top digit (camera and exponent bits) repeats within a warp: one round
+// per distinct value (usually 1-3) aggregates it with ballots, and when the camera index sits
+// inside the top digit (depth_bits >= 24) the same rounds give the per-camera counts.
 __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
-    __shared__ uint32_t s_hist[kWarps][4][256];
+    __shared__ uint32_t s_hist[kWarps][3][256];
+    __shared__ uint32_t s_top[256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < kWarps * 4 * 256; k += kThreads) (&s_hist[0][0][0])[k] = 0;
+    for (int k = threadIdx.x; k < kWarps * 3 * 256; k += kThreads) (&s_hist[0][0][0])[k] = 0;
+    for (int k = threadIdx.x; k < 256; k += kThreads) s_top[k] = 0;
     __syncthreads();
-    const uint64_t n = a.n_slots;
+    const uint32_t n = uint32_t(a.n_slots);  // slot counts stay below 2^31
+    const int cshift = a.depth_bits - 24;     // >= 0: camera = top digit >> cshift
     constexpr int kKeys = 16;  // keys per lane in flight: memory-level parallelism
-    const uint64_t stride = uint64_t(gridDim.x) * kThreads * kKeys;
-    for (uint64_t base = (uint64_t(blockIdx.x) * kWarps + warp) * 32 * kKeys; base < n; base += stride) {
-        uint32_t keys[kKeys];
-#pragma unroll
-        for (int i = 0; i < kKeys; ++i) {
-            const uint64_t idx = base + uint64_t(i) * 32 + lane;
-            keys[i] = idx < n ? __ldcs(a.keys + idx) : kInvalidKey;
+    const uint32_t stride = gridDim.x * uint32_t(kThreads * kKeys);
+    uint32_t cam_run = 0xFFFFFFFFu, cam_cnt = 0;  // runs of one camera (uniform in the warp)
+    auto count_cam = [&](uint32_t c, uint32_t cnt) {
+        if (c == cam_run) {
+            cam_cnt += cnt;
+        } else {
+            if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
+            cam_run = c;
+            cam_cnt = cnt;
         }
-        uint32_t cam_run = 0xFFFFFFFFu, cam_cnt = 0;  // lane 0 accumulates runs of one camera
+    };
+    // the loop bound is warp-uniform (no lane term): the rounds below use full-warp ballots
+    for (uint32_t wbase = (blockIdx.x * kWarps + warp) * 32u * kKeys; wbase < n; wbase += stride) {
+        const uint32_t base = wbase + uint32_t(lane);
+        uint32_t keys[kKeys];
+        const uint32_t* kp = a.keys + base;
+        if (wbase + 32u * kKeys <= n) {
+#pragma unroll
+            for (int i = 0; i < kKeys; ++i) keys[i] = __ldcs(kp + i * 32);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kKeys; ++i) keys[i] = base + i * 32u < n ? __ldcs(kp + i * 32) : kInvalidKey;
+        }
 #pragma unroll
         for (int i = 0; i < kKeys; ++i) {
             const uint32_t key = keys[i];
             const bool valid = key != kInvalidKey;
-            const uint32_t vmask = __ballot_sync(kFull, valid);
-            // digit histograms: the three low digits are spread over many values, so plain
-            // shared atomics (per-warp sub-histograms) are cheap; the top digit (camera and
-            // exponent bits) repeats within a warp and is aggregated over ballot peers.
 #pragma unroll
             for (int p = 0; p < 3; ++p)
                 if (valid) atomicAdd(&s_hist[warp][p][(key >> (8 * p)) & 255u], 1u);
-            {
-                const uint32_t d = key >> 24;
-                const uint32_t peers = peers_of<8>(kFull, d) & vmask;
-                if (valid && (peers & lanemask_lt()) == 0) s_hist[warp][3][d] += __popc(peers);
-            }
-            // per-camera counts: one round per distinct camera in the group (usually one)
-            const uint32_t cam = key_camera(key, a.depth_bits);
-            uint32_t rem = vmask;
-            while (rem) {
-                const int leader = __ffs(rem) - 1;
-                const uint32_t c = __shfl_sync(kFull, cam, leader);
-                const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
-                if (c == cam_run) {
-                    cam_cnt += __popc(same);
-                } else {
-                    if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
-                    cam_run = c;
-                    cam_cnt = __popc(same);
+            const uint32_t d3 = key >> 24;
+            uint32_t rem = __ballot_sync(kFull, valid);
+            if (cshift >= 0) {
+                while (rem) {
+                    const int leader = __ffs(rem) - 1;
+                    const uint32_t v = __shfl_sync(kFull, d3, leader);
+                    const uint32_t same = __ballot_sync(kFull, d3 == v) & rem;
+                    if (lane == leader) atomicAdd(&s_top[v], uint32_t(__popc(same)));
+                    count_cam(cshift >= 8 ? 0u : v >> cshift, __popc(same));
+                    rem &= ~same;
                 }
-                rem &= ~same;
+            } else {
+                const uint32_t peers = peers_of<8>(kFull, d3) & rem;
+                if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&s_top[d3], uint32_t(__popc(peers)));
+                const uint32_t cam = key_camera(key, a.depth_bits);
+                while (rem) {  // one round per distinct camera in the group (usually one)
+                    const int leader = __ffs(rem) - 1;
+                    const uint32_t c = __shfl_sync(kFull, cam, leader);
+                    const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
+                    count_cam(c, __popc(same));
+                    rem &= ~same;
+                }
             }
         }
-        if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
     }
+    if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
     __syncthreads();
     for (int k = threadIdx.x; k < 4 * 256; k += kThreads) {
         uint32_t s = 0;
+        if (k < 3 * 256) {
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
+            for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
+        } else {
+            s = s_top[k - 3 * 256];
+        }
         if (s) atomicAdd(a.hist + k, s);
     }
 }
