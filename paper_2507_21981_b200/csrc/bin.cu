@@ -447,6 +447,8 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     for (int w = threadIdx.x; w <= 256; w += blockDim.x) s_magic[w] = w > 1 ? 0xFFFFFFFFu / uint32_t(w) + 1u : 0u;
     __syncthreads();
     const uint32_t K = *a.n_chunks;
+    // pair positions are 32-bit; a capacity beyond that bounds nothing
+    const uint32_t cap32 = a.capacity < 0xFFFFFFFFull ? uint32_t(a.capacity) : 0xFFFFFFFFu;
     for (uint32_t k = blockIdx.x; k < K; k += gridDim.x) {
         const Unit u = unit_info(a, k);
         const int wd = u.tiles_x + 1;
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                     pre = __shfl_sync(kFull, pre, in ? __ffs(peers) - 1 : lane);
                     if (in) {
                         const uint32_t p = pre + __popc(below);
-                        if (p < a.capacity) a.vals_out[p] = sl;
+                        if (p < cap32) a.vals_out[p] = sl;
                     }
                 } else {
                     // last-writer probe: did another lane of this step write the same cell?
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                         if (in) {
                             const uint32_t p = pos[cell];
                             pos[cell] = p + 1u;
-                            if (p < a.capacity) a.vals_out[p] = sl;
+                            if (p < cap32) a.vals_out[p] = sl;
                         }
                     } else {  // rank the lanes of each cell by lane order from ballots
                         const uint32_t m = __ballot_sync(kFull, in);
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                         if (in) {
                             if (below == 0) pos[cell] = pre + __popc(peers);
                             const uint32_t p = pre + __popc(below);
-                            if (p < a.capacity) a.vals_out[p] = sl;
+                            if (p < cap32) a.vals_out[p] = sl;
                         }
                     }
                 }

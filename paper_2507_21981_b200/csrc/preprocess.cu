@@ -258,8 +258,13 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
             float vx = float(mean_world.x - cam.center[0]);
             float vy = float(mean_world.y - cam.center[1]);
             float vz = float(mean_world.z - cam.center[2]);
-            const float dn = sqrtf(vx * vx + vy * vy + vz * vz);
-            if (dn > 0.0f) { vx /= dn; vy /= dn; vz /= dn; }
+            // normalize with one reciprocal square root (fp32 shading direction: no exactness
+            // contract, the approximation moves the colour by ~1e-7)
+            const float d2 = vx * vx + vy * vy + vz * vz;
+            if (d2 > 0.0f) {
+                const float inv = rsqrtf(d2);
+                vx *= inv; vy *= inv; vz *= inv;
+            }
             // inverse_rotate(view) = conj(q).rotate(view), math.hpp:139-144, in fp32.
             const float t0 = 2.0f * (nqy * vz - nqz * vy);
             const float t1v = 2.0f * (nqz * vx - nqx * vz);
