@@ -81,31 +81,28 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float* basis
 }
 
 // rgb_c = max(0, 0.5 + sum_k basis_k * sh[c][k])  (sh.cpp:45-49). Coefficient c*K + k of a
-// primitive is component (c*K + k) % 4 of float4 plane (c*K + k) / 4; the planes are loaded
-// channel by channel, so at most two channels' coefficients are live at once.
+// primitive is component (c*K + k) % 4 of float4 plane (c*K + k) / 4. All planes are loaded
+// before the first FMA (one memory round trip; the double geometry is dead by now).
 template <int DEG>
 __device__ __forceinline__ void shade_sh(const float4* sh, uint64_t n, uint64_t i, float x,
                                          float y, float z, float rgb[3]) {
     constexpr int K = (DEG + 1) * (DEG + 1);
+    constexpr int kPlanes = (3 * K + 3) / 4;
+    float c[4 * kPlanes];
+#pragma unroll
+    for (int p = 0; p < kPlanes; ++p) {
+        const float4 v = __ldg(sh + uint64_t(p) * n + i);
+        c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
+    }
     float basis[16];
     sh_basis<DEG>(x, y, z, basis);
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-        constexpr int kMaxPl = (K + 3) / 4 + 1;
-        const int p0 = (ch * K) / 4, p1 = (ch * K + K - 1) / 4;
-        float c[kMaxPl * 4];
-#pragma unroll
-        for (int p = 0; p < kMaxPl; ++p) {
-            if (p0 + p <= p1) {
-                const float4 v = __ldg(sh + uint64_t(p0 + p) * n + i);
-                c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
-            }
-        }
         // explicit FMAs: this file is compiled with -fmad=false for the double geometry, but
         // the fp32 shading has no bit-exactness contract (the reference shades in double)
         float acc = 0.5f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) acc = __fmaf_rn(basis[k], c[ch * K + k - 4 * p0], acc);
+        for (int k = 0; k < K; ++k) acc = __fmaf_rn(basis[k], c[ch * K + k], acc);
         rgb[ch] = (acc < 0.0f) ? 0.0f : acc;
     }
 }
@@ -250,7 +247,7 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
                         frad = __double2float_rn(radius);
             float fia = 0.f, fib = 0.f, fic = 0.f;
             if (!off_grid) {
-                const double inv_det = 1.0 / det;
+                const double inv_det = __drcp_rn(det);  // == 1.0 / det (both correctly rounded)
                 fia = __double2float_rn(cov_yy * inv_det);
                 fib = __double2float_rn(-cov_xy * inv_det);
                 fic = __double2float_rn(cov_xx * inv_det);
