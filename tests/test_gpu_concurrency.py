@@ -1,0 +1,94 @@
+"""Concurrent renderer contexts (how bench.py and a multi-threaded caller drive the library).
+
+Every context owns its stream, workspaces, onesweep status words and tickets; frames of different
+contexts overlap on the GPU. The bar is bit-identity: a frame rendered while other contexts run
+must equal the same frame rendered alone (raster.hpp:62-63 makes the reference's render a pure,
+thread-count independent function, and so is ours).
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2507_21981_b200 import Context
+from paper_2507_21981_b200.api import NodeKind, RigidTransform, SceneNode, quat_from_axis_angle
+from tests.helpers import ref_camera
+
+pytestmark = pytest.mark.gpu
+
+
+def scene_and_frames(oracle, n_frames):
+    field = oracle.random_field(4242, 20000, 3.0, 0.005, 0.08, 2)
+    field.means[:, 2] += 3.0
+    n = field.size()
+    cams = []
+    for k in range(3):
+        c = ref_camera(160, 120, 140.0)
+        c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.07 * (k - 1)), (0.15 * (k - 1), 0.0, 0.0))
+        cams.append(c)
+    frames = []
+    for i in range(n_frames):
+        q = quat_from_axis_angle((0, 0, 1), 0.37 * i)
+        frames.append([SceneNode("bg", NodeKind.background, RigidTransform(), (0, n - 3001)),
+                       SceneNode("obj", NodeKind.interactive, RigidTransform(q, (0.05 * i, 0.0, 0.1)),
+                                 (n - 3001, n))])
+    return field, cams, frames
+
+
+def same(a, b):
+    return (np.array_equal(a.rgb, b.rgb) and np.array_equal(a.depth, b.depth)
+            and np.array_equal(a.accum_alpha, b.accum_alpha))
+
+
+def test_threaded_contexts_equal_sequential(oracle):
+    field, cams, frames = scene_and_frames(oracle, 8)
+    solo = Context(0)
+    s0 = solo.upload(field)
+    want = [solo.render(s0, nodes, cams) for nodes in frames]
+    assert any(t.accum_alpha.max() > 0.5 for t in want[0])
+
+    ctxs = [Context(0) for _ in range(4)]
+    scenes = [c.upload(field) for c in ctxs]
+    got = {}
+    errors = []
+
+    def worker(k):
+        try:
+            for rep in range(2):
+                for i in range(k, len(frames), len(ctxs)):
+                    got[(i, rep)] = ctxs[k].render(scenes[k], frames[i], cams)
+        except Exception as e:  # noqa: BLE001 (reported below)
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(ctxs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (i, rep), out in got.items():
+        for c in range(len(cams)):
+            assert same(out[c], want[i][c]), (i, rep, c)
+
+
+def test_interleaved_device_frames_equal_sequential(oracle):
+    import torch
+    field, cams, frames = scene_and_frames(oracle, 6)
+    ctxs = [Context(0) for _ in range(3)]
+    scenes = [c.upload(field) for c in ctxs]
+    floats = sum(5 * c.width * c.height for c in cams)
+    outs = [torch.empty(floats, dtype=torch.float32, device="cuda:0") for _ in frames]
+    # every context enqueues its frames without waiting; frames of different contexts overlap
+    for i, nodes in enumerate(frames):
+        ctxs[i % 3].render_device(scenes[i % 3], nodes, cams, None, outs[i].data_ptr())
+    for c in ctxs:
+        c.synchronize()
+    solo = Context(0)
+    s0 = solo.upload(field)
+    for i, nodes in enumerate(frames):
+        want = solo.render(s0, nodes, cams)
+        flat = np.concatenate([np.concatenate([t.rgb.reshape(-1), t.depth.reshape(-1),
+                                               t.accum_alpha.reshape(-1)]) for t in want])
+        assert np.array_equal(outs[i].cpu().numpy(), flat), i
