@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/gsim_gpu.h"
@@ -184,6 +185,15 @@ struct gsim_gpu_context {
     DevBuf<char> query_buf;
     DevBuf<float> enc_src;
     DevBuf<EncodeCam> enc_cams;
+    // host-target renders: camera c's copies start when its tiles are done (copy_stream waits
+    // on cam_done[c] reaching cam_done_expect[c]; the counters only grow, compared cyclically)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_ev = nullptr;
+    DevBuf<uint32_t> cam_done;
+    std::vector<uint32_t> cam_done_expect;
+    gsim_target* frame_outs = nullptr;   // targets of the camera group in flight (nullptr: none)
+    bool copies_stale = false;           // a group was re-run after its copies were issued
+    bool overlap_copies = true;          // GSIM_GPU_OVERLAP_COPIES=0: copies follow the frame
     // outputs / API scratch
     DevBuf<float> out;
     DevBuf<gsim_projected_splat> full;
@@ -587,6 +597,10 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
     return b;
 }
 
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn();
+bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out);
+
 void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
                          float* out) {
     RasterArgs rr{};
@@ -610,8 +624,22 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.exact_cull = ctx->raster_exact_cull;
     rr.valid_alpha = ctx->frame_valid_alpha;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
+    const bool overlap = ctx->frame_outs && rr.out && wait_value_fn();
+    if (overlap) {
+        if (ctx->cam_done_expect.size() < p.cams.size()) {
+            // new counters start at zero on both sides (nothing can be waiting on them yet)
+            const size_t n = std::max<size_t>(p.cams.size(), 64);
+            GSIM_CK(cudaStreamSynchronize(ctx->copy_stream));
+            GSIM_CK(cudaStreamSynchronize(ctx->stream));
+            ctx->cam_done.reserve(n);
+            GSIM_CK(cudaMemset(ctx->cam_done.ptr, 0, n * sizeof(uint32_t)));
+            ctx->cam_done_expect.assign(n, 0u);
+        }
+        rr.cam_done = ctx->cam_done.ptr;
+    }
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
+    if (overlap) queue_camera_copies(ctx, p, out);
 }
 
 // K3 + K4 over records/keys/rects already produced for `p` (by K2 or the splat converter).
@@ -831,14 +859,19 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
         group = std::max<uint64_t>(1, std::min<uint64_t>(group, (uint64_t(1) << 31) / n));
     }
     uint64_t launches = 0, h2d = 0;
+    gsim_target* const targets = ctx->frame_outs;  // host targets of the whole batch, if any
+    ctx->frame_outs = nullptr;
     for (uint64_t c0 = 0; c0 < n_cams || (n_cams == 0 && c0 == 0); c0 += group) {
         const uint64_t g = n_cams ? std::min(group, n_cams - c0) : 0;
-        if (c0 > 0 && !wait_for_count) check_pending(ctx);
+        // a re-run group had its copies queued already: the caller copies everything again
+        if (c0 > 0 && !wait_for_count && check_pending(ctx)) ctx->copies_stale = true;
         Plan plan;
         const EncodeParams enc_batch = ctx->frame_enc;
         if (enc_batch.flags) ctx->frame_enc.dst += offsets[c0] / 5 * encoded_bpp(enc_batch.flags);
+        ctx->frame_outs = targets ? targets + c0 : nullptr;
         render_frame(ctx, scene, nodes, n_nodes, cameras + c0, g, options, out + offsets[c0], plan,
                      wait_for_count);
+        ctx->frame_outs = nullptr;
         ctx->frame_enc = enc_batch;
         launches += ctx->stats.launches;
         h2d += ctx->stats.h2d_bytes;
@@ -1155,6 +1188,45 @@ gsim_gpu_scene* load_ply(gsim_gpu_context* ctx, const std::string& path) {
     return sc;
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda link); nullptr when
+// the driver does not offer stream memory operations (copies then follow the whole frame).
+WaitValueFn wait_value_fn() {
+    static const WaitValueFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return WaitValueFn(nullptr);
+        return reinterpret_cast<WaitValueFn>(f);
+    }();
+    return fn;
+}
+
+// Per-camera copies of a host-target render, queued right after the raster launch: the copy
+// stream waits for each camera's tile counter, so camera c crosses PCIe while later cameras
+// (and other contexts' frames) are still being composited.
+bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out) {
+    const WaitValueFn wait = wait_value_fn();
+    if (!wait || !ctx->frame_outs) return false;
+    uint64_t off = 0;
+    for (size_t c = 0; c < p.cams.size(); ++c) {
+        const DevCamera& cam = p.cams[c];
+        const size_t npx = size_t(cam.width) * cam.height;
+        ctx->cam_done_expect[c] += uint32_t(cam.tiles_x) * uint32_t(cam.tiles_y);
+        const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(ctx->cam_done.ptr + c);
+        if (wait(reinterpret_cast<CUstream>(ctx->copy_stream), flag, ctx->cam_done_expect[c],
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            throw CudaError{"cuStreamWaitValue32 failed"};
+        const gsim_target& t = ctx->frame_outs[c];
+        const float* base = out + off;
+        GSIM_CK(cudaMemcpyAsync(t.rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
+        GSIM_CK(cudaMemcpyAsync(t.depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
+        GSIM_CK(cudaMemcpyAsync(t.accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
+        off += 5 * npx;
+    }
+    return true;
+}
+
 // D2H of the internal output buffer into host RenderTargets (the drop-in's by-value return).
 void copy_targets(gsim_gpu_context* ctx, const gsim_camera* cameras, uint64_t n,
                   const std::vector<uint64_t>& off, gsim_target* outs) {
@@ -1389,6 +1461,7 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         if (const char* e = std::getenv("GSIM_GPU_RASTER_RECT")) ctx->raster_rect_w = std::atoi(e) == 16 ? 16 : 8;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_EXACT")) ctx->raster_exact_cull = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
+        if (const char* e = std::getenv("GSIM_GPU_OVERLAP_COPIES")) ctx->overlap_copies = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_INITIAL_PAIR_CAPACITY")) {
             ctx->fixed_initial_capacity = std::strtoull(e, nullptr, 10);
             ctx->pair_capacity = ctx->fixed_initial_capacity;
@@ -1447,6 +1520,7 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->enc_src.release();
     ctx->enc_cams.release();
     ctx->query_buf.release();
+    ctx->cam_done.release();
     {
         std::lock_guard<std::mutex> lk(ctx->mu);
         for (auto* sc : ctx->scenes) sc->ctx = nullptr;
@@ -1457,6 +1531,11 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     for (auto& e : ctx->staging_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->bin_ev) cudaEventDestroy(ctx->bin_ev);
+    if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GSIM_OK;
@@ -1757,10 +1836,35 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
         // Asynchronous render with the copies queued behind it: the pair-buffer check is done
         // once at the end (no mid-frame host round trip); on an overflow the tail is re-run
         // and the targets copied again.
-        const std::vector<uint64_t> off =
-            render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, false);
-        copy_targets(ctx, cameras, n_cameras, off, outs);
-        if (check_pending(ctx)) copy_targets(ctx, cameras, n_cameras, off, outs);
+        // Per-camera copies overlap the compositing when the driver has stream memory
+        // operations (queue_camera_copies); otherwise they follow the frame.
+        const bool overlap = ctx->overlap_copies && wait_value_fn() != nullptr;
+        if (overlap && !ctx->copy_stream) {
+            GSIM_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            GSIM_CK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
+        }
+        ctx->copies_stale = false;
+        ctx->frame_outs = overlap ? outs : nullptr;
+        std::vector<uint64_t> off;
+        try {
+            off = render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, options, nullptr, false);
+        } catch (...) {
+            ctx->frame_outs = nullptr;
+            if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+            throw;
+        }
+        ctx->frame_outs = nullptr;
+        if (overlap) {
+            GSIM_CK(cudaStreamSynchronize(ctx->copy_stream));
+            ctx->stats.d2h_bytes = 0;
+            for (uint64_t c = 0; c < n_cameras; ++c)
+                ctx->stats.d2h_bytes += 5 * uint64_t(cameras[c].width) * cameras[c].height * sizeof(float);
+            GSIM_CK(cudaStreamSynchronize(ctx->stream));
+            if (check_pending(ctx) || ctx->copies_stale) copy_targets(ctx, cameras, n_cameras, off, outs);
+        } else {
+            copy_targets(ctx, cameras, n_cameras, off, outs);
+            if (check_pending(ctx)) copy_targets(ctx, cameras, n_cameras, off, outs);
+        }
     });
 }
 

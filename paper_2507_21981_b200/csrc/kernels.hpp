@@ -112,6 +112,8 @@ struct RasterArgs {
     uint64_t n_slots;                // record slots (stale values are clamped to a valid slot)
     EncodeParams enc;                // fused encoding when enc.flags != 0; camera c's block
                                      // starts at enc.dst + out_offset / 5 * encoded_bpp
+    uint32_t* cam_done;              // optional: += 1 per finished tile of camera c (after a
+                                     // system fence), for copies that wait on cuStreamWaitValue32
 };
 
 // Device pose tracks (tracks.cu): records of track k are begin[k] .. begin[k+1]-1.

@@ -314,6 +314,11 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
     write_pixel(a, cam, x, y, cr.x, cg.x, cb.x, d.x, acc.x);
     write_pixel(a, cam, x + 1, y, cr.y, cg.y, cb.y, d.y, acc.y);
+    if (a.cam_done) {  // the tile's pixels are visible to the copy engine before it is counted
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) atomicAdd(a.cam_done + cam_idx, 1u);
+    }
 }
 
 void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream) {

@@ -92,3 +92,26 @@ def test_interleaved_device_frames_equal_sequential(oracle):
         flat = np.concatenate([np.concatenate([t.rgb.reshape(-1), t.depth.reshape(-1),
                                                t.accum_alpha.reshape(-1)]) for t in want])
         assert np.array_equal(outs[i].cpu().numpy(), flat), i
+
+
+def test_overlapped_copies_equal_frame_copies(oracle, monkeypatch):
+    """render() copies camera c while later cameras are composited (per-camera tile counters +
+    cuStreamWaitValue32); GSIM_GPU_OVERLAP_COPIES=0 copies after the frame. Same bytes, including
+    multi-group batches (40 cameras -> several camera groups) and back-to-back frames."""
+    field, cams, frames = scene_and_frames(oracle, 3)
+    many = []
+    for k in range(40):
+        c = ref_camera(64, 48, 60.0)
+        c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.01 * k), (0.02 * k, 0.0, 0.0))
+        many.append(c)
+    monkeypatch.setenv("GSIM_GPU_OVERLAP_COPIES", "0")
+    plain = Context(0)
+    monkeypatch.delenv("GSIM_GPU_OVERLAP_COPIES")
+    fast = Context(0)
+    sp, sf = plain.upload(field), fast.upload(field)
+    for nodes in frames:
+        for batch in (cams, many):
+            want = plain.render(sp, nodes, batch)
+            got = fast.render(sf, nodes, batch)
+            assert all(same(a, b) for a, b in zip(got, want))
+    assert fast.stats()["groups"] > 1 or len(many) <= 32
