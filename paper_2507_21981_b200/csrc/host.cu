@@ -715,7 +715,11 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     for (int attempt = 0; attempt < 3; ++attempt) {
         b.vals_out = ctx->vals.ptr;
         b.capacity = ctx->pair_capacity;
-        launch_bin_scatter(b, chunk_grid, s);
+        static const int scatter_ctas = [] {  // GSIM_GPU_SCATTER_CTAS: per SM, 0 = one per unit
+            const char* e = std::getenv("GSIM_GPU_SCATTER_CTAS");
+            return e ? std::max(0, std::atoi(e)) : 0;
+        }();
+        launch_bin_scatter(b, scatter_ctas ? std::min(chunk_grid, n_sms * scatter_ctas) : chunk_grid, s);
         check_launch();
         record_ev(ctx, kEvScatter);
         launch_raster_stage(ctx, p, opt, out);

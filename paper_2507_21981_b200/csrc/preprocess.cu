@@ -12,6 +12,7 @@
 // histograms of the keys for the onesweep depth sort.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/gsim_gpu.h"
 #include "common.cuh"
@@ -356,8 +357,15 @@ template <int DEG>
 static void launch_pre_deg(const PreprocessArgs& a, bool full, uint64_t n, int n_sms,
                            cudaStream_t s) {
     constexpr int kNT = 128, kMinB = 5;
+    // GSIM_GPU_PRE_CTAS: resident blocks per SM of the grid (fewer leave room for other
+    // contexts' kernels on the same SM)
+    static const int per_sm = [] {
+        const char* e = std::getenv("GSIM_GPU_PRE_CTAS");
+        const int v = e ? std::atoi(e) : kMinB;
+        return v < 1 ? 1 : v > kMinB ? kMinB : v;
+    }();
     const unsigned grid =
-        unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + kNT - 1) / kNT, uint64_t(n_sms) * kMinB)));
+        unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n + kNT - 1) / kNT, uint64_t(n_sms) * per_sm)));
     const bool smem_cams = a.n_cams <= uint32_t(kMaxSmemCams);
     if (full) {
         if (smem_cams) preprocess_kernel<DEG, true, kNT, kMinB, true><<<grid, kNT, 0, s>>>(a);
