@@ -142,31 +142,22 @@ __device__ __forceinline__ uint32_t reduce_or(uint32_t v) {
 }  // namespace
 
 // ---- depth-key histograms + per-camera record counts ---------------------------------------
-// The three low digits are spread over many values: plain shared atomics into per-warp
-// sub-histograms. The top digit (camera and exponent bits) repeats within a warp: one round
-// per distinct value (usually 1-3) aggregates it with ballots, and when the camera index sits
-// inside the top digit (depth_bits >= 24) the same rounds give the per-camera counts.
+// The three low digits are spread over many values: warp-aggregated shared atomics. The top
+// digit (camera and exponent bits) repeats within a warp: one round per distinct value (usually
+// 1-3) adds its lane count to a per-warp sub-histogram. When the camera index sits inside the
+// top digit (depth_bits >= 24) the per-camera counts follow from that histogram (chunk_table);
+// otherwise they are counted here, one round per distinct camera.
 __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
-    __shared__ uint32_t s_hist[kWarps][3][256];
-    __shared__ uint32_t s_top[256];
+    __shared__ uint32_t s_hist[kWarps][4][256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < kWarps * 3 * 256; k += kThreads) (&s_hist[0][0][0])[k] = 0;
-    for (int k = threadIdx.x; k < 256; k += kThreads) s_top[k] = 0;
+    for (int k = threadIdx.x; k < kWarps * 4 * 256; k += kThreads) (&s_hist[0][0][0])[k] = 0;
     __syncthreads();
     const uint32_t n = uint32_t(a.n_slots);  // slot counts stay below 2^31
-    const int cshift = a.depth_bits - 24;     // >= 0: camera = top digit >> cshift
+    const bool cams_in_top = a.depth_bits >= 24;
     constexpr int kKeys = 16;  // keys per lane in flight: memory-level parallelism
     const uint32_t stride = gridDim.x * uint32_t(kThreads * kKeys);
     uint32_t cam_run = 0xFFFFFFFFu, cam_cnt = 0;  // runs of one camera (uniform in the warp)
-    auto count_cam = [&](uint32_t c, uint32_t cnt) {
-        if (c == cam_run) {
-            cam_cnt += cnt;
-        } else {
-            if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
-            cam_run = c;
-            cam_cnt = cnt;
-        }
-    };
+    uint32_t* top = s_hist[warp][3];
     // the loop bound is warp-uniform (no lane term): the rounds below use full-warp ballots
     for (uint32_t wbase = (blockIdx.x * kWarps + warp) * 32u * kKeys; wbase < n; wbase += stride) {
         const uint32_t base = wbase + uint32_t(lane);
@@ -187,25 +178,29 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
             for (int p = 0; p < 3; ++p)
                 if (valid) atomicAdd(&s_hist[warp][p][(key >> (8 * p)) & 255u], 1u);
             const uint32_t d3 = key >> 24;
-            uint32_t rem = __ballot_sync(kFull, valid);
-            if (cshift >= 0) {
-                while (rem) {
-                    const int leader = __ffs(rem) - 1;
-                    const uint32_t v = __shfl_sync(kFull, d3, leader);
-                    const uint32_t same = __ballot_sync(kFull, d3 == v) & rem;
-                    if (lane == leader) atomicAdd(&s_top[v], uint32_t(__popc(same)));
-                    count_cam(cshift >= 8 ? 0u : v >> cshift, __popc(same));
-                    rem &= ~same;
-                }
-            } else {
-                const uint32_t peers = peers_of<8>(kFull, d3) & rem;
-                if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&s_top[d3], uint32_t(__popc(peers)));
+            const uint32_t vmask = __ballot_sync(kFull, valid);
+            uint32_t rem = vmask;
+            while (rem) {  // the warp's own sub-histogram: the leader adds without atomics
+                const int leader = __ffs(rem) - 1;
+                const uint32_t v = __shfl_sync(kFull, d3, leader);
+                const uint32_t same = __ballot_sync(kFull, d3 == v) & rem;
+                if (lane == leader) top[v] += uint32_t(__popc(same));
+                rem &= ~same;
+            }
+            if (!cams_in_top) {
                 const uint32_t cam = key_camera(key, a.depth_bits);
+                rem = vmask;
                 while (rem) {  // one round per distinct camera in the group (usually one)
                     const int leader = __ffs(rem) - 1;
                     const uint32_t c = __shfl_sync(kFull, cam, leader);
                     const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
-                    count_cam(c, __popc(same));
+                    if (c == cam_run) {
+                        cam_cnt += __popc(same);
+                    } else {
+                        if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
+                        cam_run = c;
+                        cam_cnt = __popc(same);
+                    }
                     rem &= ~same;
                 }
             }
@@ -215,12 +210,8 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
     __syncthreads();
     for (int k = threadIdx.x; k < 4 * 256; k += kThreads) {
         uint32_t s = 0;
-        if (k < 3 * 256) {
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
-        } else {
-            s = s_top[k - 3 * 256];
-        }
+        for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
         if (s) atomicAdd(a.hist + k, s);
     }
 }
@@ -263,7 +254,19 @@ __global__ void __launch_bounds__(256) chunk_table_kernel(BinArgs a) {
     const uint32_t R = uint32_t(a.chunk_records);
     for (int c0 = 0; c0 < a.n_cams; c0 += blockDim.x) {
         const int c = c0 + tid;
-        const uint32_t v = c < a.n_cams ? a.cam_visible[c] : 0u;
+        uint32_t v = 0;
+        if (c < a.n_cams) {
+            if (a.depth_bits >= 24) {
+                // camera c owns the top digits [c << cshift, (c + 1) << cshift) (key_hist)
+                const int cshift = a.depth_bits - 24;
+                const uint32_t d0 = cshift >= 8 ? 0u : uint32_t(c) << cshift;
+                const uint32_t d1 = cshift >= 8 ? 256u : min(256u, uint32_t(c + 1) << cshift);
+                for (uint32_t d = d0; d < d1; ++d) v += a.hist[3 * 256 + d];
+                a.cam_visible[c] = v;
+            } else {
+                v = a.cam_visible[c];
+            }
+        }
         const uint32_t k = (v + R - 1) / R;
         const uint32_t tc = c < a.n_cams ? a.cam_tile_base[c + 1] - a.cam_tile_base[c] : 0u;
         const unsigned long long m = (unsigned long long)k * tc;
