@@ -201,13 +201,14 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 // ---- launchers -----------------------------------------------------------------------------
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream) {
-    // passes 1-3 rank the spread low digits; pass 4 (no key output) ranks the top digit
+    // every pass finds digit peers with the shared-memory bitmaps: even the top digit (camera
+    // and exponent bits, ~3 lanes per value after the low passes) measured cheaper than ballots
     if (first) {
         if (write_keys) onesweep_kernel<true, true, true><<<grid, kThreads, 0, stream>>>(a);
         else onesweep_kernel<true, false, false><<<grid, kThreads, 0, stream>>>(a);
     } else {
         if (write_keys) onesweep_kernel<false, true, true><<<grid, kThreads, 0, stream>>>(a);
-        else onesweep_kernel<false, false, false><<<grid, kThreads, 0, stream>>>(a);
+        else onesweep_kernel<false, false, true><<<grid, kThreads, 0, stream>>>(a);
     }
 }
 
