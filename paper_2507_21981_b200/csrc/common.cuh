@@ -195,17 +195,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Lanes of `mask` holding the same low `bits` bits of v as this lane, from one ballot per bit.
 // match.any.sync does the same in one instruction, but it issues at roughly one per ~40 SM
 // cycles on sm_100 and stalls everything behind it (measured, profiles/); ballots are cheap.
-template <int BITS>
-__device__ __forceinline__ uint32_t peers_of(uint32_t mask, uint32_t v) {
-    uint32_t peers = mask;
-#pragma unroll
-    for (int b = 0; b < BITS; ++b) {
-        const uint32_t bit = (v >> b) & 1u;
-        const uint32_t bal = __ballot_sync(mask, bit);
-        peers &= bit ? bal : ~bal;
-    }
-    return peers;
-}
 __device__ __forceinline__ uint32_t peers_of_bits(uint32_t mask, uint32_t v, int bits) {
     uint32_t peers = mask;
     for (int b = 0; b < bits; ++b) {

@@ -65,14 +65,14 @@ __device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoc
 
 }  // namespace
 
-// kBitmapPeers: find the lanes sharing a digit with one shared-memory atomicOr per item into a
+// Digit peers (the lanes sharing a digit) come from one shared-memory atomicOr per item into a
 // per-warp digit bitmap (two buffers alternate, so clearing item i's bits never races item
-// i+1's); right for the low digits, whose values are spread (shared atomics cost ~3 cycles
-// per warp instruction without same-address contention, tools/microbench.cu). The top digit
-// (camera and exponent bits) repeats within a warp and keeps the 8-ballot peer detection.
-// The bitmaps live in s_keys (ranking is done before the chunk is staged there) and are
-// cleared at the start of every chunk.
-template <bool kFirst, bool kWriteKeys, bool kBitmapPeers>
+// i+1's); shared atomics cost ~3 cycles per warp instruction without heavy same-address
+// contention (tools/microbench.cu), and even the top digit (camera and exponent bits, ~3 lanes
+// per value after the low passes) measured cheaper this way than with 8 ballots. The bitmaps
+// live in s_keys (ranking is done before the chunk is staged there) and are cleared at the start
+// of every chunk.
+template <bool kFirst, bool kWriteKeys>
 __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     __shared__ uint32_t s_keys[kOnesweepTile];
     static_assert(2 * kWarps * kRadix <= kOnesweepTile, "peer bitmaps alias s_keys");
@@ -97,8 +97,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     while (true) {
         if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
         for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_warp_hist[0][0])[k] = 0;
-        if (kBitmapPeers)
-            for (int k = tid; k < 2 * kWarps * kRadix; k += kThreads) s_keys[k] = 0;
+        for (int k = tid; k < 2 * kWarps * kRadix; k += kThreads) s_keys[k] = 0;
         __syncthreads();
         const uint32_t t = s_ticket;
         if (t >= chunks) break;
@@ -128,18 +127,12 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
         for (int i = 0; i < kItems; ++i) {
             const bool valid = rank[i] != 0u;
             const uint32_t d = (keys[i] >> a.shift) & 255u;
-            uint32_t peers;
-            if (kBitmapPeers) {
-                uint32_t* bits = &s_peer[i & 1][warp][d];
-                if (valid) atomicOr(bits, 1u << lane);
-                __syncwarp();
-                peers = valid ? *bits : 0u;
-                __syncwarp();
-                if (valid && (peers & lanemask_lt()) == 0) *bits = 0u;  // leader clears
-            } else {
-                const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-                peers = peers_of<8>(0xffffffffu, d) & vmask;
-            }
+            uint32_t* bits = &s_peer[i & 1][warp][d];
+            if (valid) atomicOr(bits, 1u << lane);
+            __syncwarp();
+            const uint32_t peers = valid ? *bits : 0u;
+            __syncwarp();
+            if (valid && (peers & lanemask_lt()) == 0) *bits = 0u;  // leader clears
             const uint32_t below = peers & lanemask_lt();
             const int leader = peers ? __ffs(peers) - 1 : lane;
             uint32_t pre = 0;
@@ -201,14 +194,12 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 // ---- launchers -----------------------------------------------------------------------------
 void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
                      cudaStream_t stream) {
-    // every pass finds digit peers with the shared-memory bitmaps: even the top digit (camera
-    // and exponent bits, ~3 lanes per value after the low passes) measured cheaper than ballots
     if (first) {
-        if (write_keys) onesweep_kernel<true, true, true><<<grid, kThreads, 0, stream>>>(a);
-        else onesweep_kernel<true, false, false><<<grid, kThreads, 0, stream>>>(a);
+        if (write_keys) onesweep_kernel<true, true><<<grid, kThreads, 0, stream>>>(a);
+        else onesweep_kernel<true, false><<<grid, kThreads, 0, stream>>>(a);
     } else {
-        if (write_keys) onesweep_kernel<false, true, true><<<grid, kThreads, 0, stream>>>(a);
-        else onesweep_kernel<false, false, true><<<grid, kThreads, 0, stream>>>(a);
+        if (write_keys) onesweep_kernel<false, true><<<grid, kThreads, 0, stream>>>(a);
+        else onesweep_kernel<false, false><<<grid, kThreads, 0, stream>>>(a);
     }
 }
 
