@@ -373,3 +373,29 @@ def test_config1_one_camera_parity(ctx, oracle):
     tb, vals = oracle.rasterize_lists(splats, cam)
     assert np.array_equal(offsets[: len(tb)], tb)
     assert np.array_equal(values, splats["prim_index"][vals])
+
+
+def test_narrow_depth_window_batch(ctx, oracle):
+    """near/far 2.0/3.9: 23 depth-key bits, so the camera index sits below the top key digit and
+    key_hist counts cameras itself (bin.cu); tile lists and images of a 3-camera batch must still
+    equal the reference's per camera."""
+    f = oracle.random_field(6161, 6000, 2.0, 0.01, 0.2, 2)
+    f.means[:, 2] += 3.0
+    f.touch()
+    nodes = two_nodes(6000)
+    cams = []
+    for k in range(3):
+        c = ref_camera(128, 96, 90.0)
+        c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.1 * (k - 1)), (0.2 * (k - 1), 0.0, 0.0))
+        c.near_plane, c.far_plane = 2.0, 3.9
+        cams.append(c)
+    s = ctx.upload(f)
+    got = ctx.render(s, nodes, cams)
+    for k, cam in enumerate(cams):
+        offsets, values = ctx.tile_lists(k)
+        splats = oracle.project(f, nodes, cam)
+        assert 0 < len(splats) < 6000  # the window culls some splats, keeps others
+        tb, vals = oracle.rasterize_lists(splats, cam)
+        assert np.array_equal(offsets[: len(tb)], tb), k
+        assert np.array_equal(values, splats["prim_index"][vals]), k
+        assert_parity(got[k], oracle.rasterize(splats, cam), k)
