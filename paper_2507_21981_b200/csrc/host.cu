@@ -192,6 +192,7 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> cam_done;
     std::vector<uint32_t> cam_done_expect;
     gsim_target* frame_outs = nullptr;   // targets of the camera group in flight (nullptr: none)
+    uint8_t* frame_enc_host = nullptr;   // render_encoded: host bytes of the group in flight
     bool copies_stale = false;           // a group was re-run after its copies were issued
     bool overlap_copies = true;          // GSIM_GPU_OVERLAP_COPIES=0: copies follow the frame
     // outputs / API scratch
@@ -600,6 +601,7 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
 using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WaitValueFn wait_value_fn();
 bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out);
+bool queue_camera_copies_enc(gsim_gpu_context* ctx, const Plan& p, const uint8_t* dev, uint32_t bpp);
 
 void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
                          float* out) {
@@ -624,7 +626,8 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.exact_cull = ctx->raster_exact_cull;
     rr.valid_alpha = ctx->frame_valid_alpha;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
-    const bool overlap = ctx->frame_outs && rr.out && wait_value_fn();
+    const bool overlap_enc = ctx->frame_enc_host && rr.enc.flags && wait_value_fn();
+    const bool overlap = (ctx->frame_outs && rr.out && wait_value_fn()) || overlap_enc;
     if (overlap) {
         if (ctx->cam_done_expect.size() < p.cams.size()) {
             // new counters start at zero on both sides (nothing can be waiting on them yet)
@@ -639,7 +642,10 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     }
     launch_raster(rr, p.tiles, ctx->stream);
     check_launch();
-    if (overlap) queue_camera_copies(ctx, p, out);
+    if (overlap_enc)
+        queue_camera_copies_enc(ctx, p, rr.enc.dst, encoded_bpp(rr.enc.flags));
+    else if (overlap)
+        queue_camera_copies(ctx, p, out);
 }
 
 // K3 + K4 over records/keys/rects already produced for `p` (by K2 or the splat converter).
@@ -864,7 +870,9 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
     }
     uint64_t launches = 0, h2d = 0;
     gsim_target* const targets = ctx->frame_outs;  // host targets of the whole batch, if any
+    uint8_t* const enc_host = ctx->frame_enc_host;  // render_encoded host bytes, if any
     ctx->frame_outs = nullptr;
+    ctx->frame_enc_host = nullptr;
     for (uint64_t c0 = 0; c0 < n_cams || (n_cams == 0 && c0 == 0); c0 += group) {
         const uint64_t g = n_cams ? std::min(group, n_cams - c0) : 0;
         // a re-run group had its copies queued already: the caller copies everything again
@@ -873,9 +881,11 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
         const EncodeParams enc_batch = ctx->frame_enc;
         if (enc_batch.flags) ctx->frame_enc.dst += offsets[c0] / 5 * encoded_bpp(enc_batch.flags);
         ctx->frame_outs = targets ? targets + c0 : nullptr;
+        ctx->frame_enc_host = enc_host ? enc_host + offsets[c0] / 5 * encoded_bpp(enc_batch.flags) : nullptr;
         render_frame(ctx, scene, nodes, n_nodes, cameras + c0, g, options, out + offsets[c0], plan,
                      wait_for_count);
         ctx->frame_outs = nullptr;
+        ctx->frame_enc_host = nullptr;
         ctx->frame_enc = enc_batch;
         launches += ctx->stats.launches;
         h2d += ctx->stats.h2d_bytes;
@@ -1227,6 +1237,27 @@ bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out)
         GSIM_CK(cudaMemcpyAsync(t.depth, base + 3 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
         GSIM_CK(cudaMemcpyAsync(t.accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
         off += 5 * npx;
+    }
+    return true;
+}
+
+// The same for render_encoded: camera c's encoded block crosses PCIe once its tiles are done.
+bool queue_camera_copies_enc(gsim_gpu_context* ctx, const Plan& p, const uint8_t* dev, uint32_t bpp) {
+    const WaitValueFn wait = wait_value_fn();
+    if (!wait || !ctx->frame_enc_host) return false;
+    uint64_t off = 0;
+    for (size_t c = 0; c < p.cams.size(); ++c) {
+        const DevCamera& cam = p.cams[c];
+        const uint64_t bytes = uint64_t(bpp) * uint64_t(cam.width) * uint64_t(cam.height);
+        ctx->cam_done_expect[c] += uint32_t(cam.tiles_x) * uint32_t(cam.tiles_y);
+        const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(ctx->cam_done.ptr + c);
+        if (wait(reinterpret_cast<CUstream>(ctx->copy_stream), flag, ctx->cam_done_expect[c],
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            throw CudaError{"cuStreamWaitValue32 failed"};
+        if (bytes)
+            GSIM_CK(cudaMemcpyAsync(ctx->frame_enc_host + off, dev + off, bytes, cudaMemcpyDeviceToHost,
+                                    ctx->copy_stream));
+        off += bytes;
     }
     return true;
 }
@@ -1979,9 +2010,32 @@ int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
         } reset{ctx};
         ctx->frame_enc = e;
         ctx->frame_enc_only = true;
-        render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, raster_options, nullptr,
-                       false);
-        if (!out_is_device) {
+        const bool overlap = !out_is_device && ctx->overlap_copies && wait_value_fn() != nullptr;
+        if (overlap && !ctx->copy_stream) {
+            GSIM_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            GSIM_CK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
+        }
+        ctx->copies_stale = false;
+        ctx->frame_enc_host = overlap ? out : nullptr;
+        try {
+            render_cameras(ctx, scene, nodes, n_nodes, cameras, n_cameras, raster_options, nullptr,
+                           false);
+        } catch (...) {
+            ctx->frame_enc_host = nullptr;
+            if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+            throw;
+        }
+        ctx->frame_enc_host = nullptr;
+        if (overlap) {
+            GSIM_CK(cudaStreamSynchronize(ctx->copy_stream));
+            GSIM_CK(cudaStreamSynchronize(ctx->stream));
+            ctx->stats.d2h_bytes = bytes;
+            if (check_pending(ctx) || ctx->copies_stale) {
+                if (bytes)
+                    GSIM_CK(cudaMemcpyAsync(out, ctx->enc_buf.ptr, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+                GSIM_CK(cudaStreamSynchronize(ctx->stream));
+            }
+        } else if (!out_is_device) {
             // one check at the end, as gsim_gpu_render; the encoding of a re-run tail is part
             // of its raster epilogue (check_pending restores the frame's encode parameters)
             for (int pass = 0; pass < 2; ++pass) {

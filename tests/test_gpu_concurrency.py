@@ -109,9 +109,14 @@ def test_overlapped_copies_equal_frame_copies(oracle, monkeypatch):
     monkeypatch.delenv("GSIM_GPU_OVERLAP_COPIES")
     fast = Context(0)
     sp, sf = plain.upload(field), fast.upload(field)
+    from paper_2507_21981_b200 import EncodeOptions
+    eo = EncodeOptions()
     for nodes in frames:
         for batch in (cams, many):
             want = plain.render(sp, nodes, batch)
             got = fast.render(sf, nodes, batch)
             assert all(same(a, b) for a, b in zip(got, want))
+            # render_encoded's per-camera copies (the same counters) give the same bytes
+            assert np.array_equal(fast.render_encoded(sf, nodes, batch, None, eo),
+                                  plain.render_encoded(sp, nodes, batch, None, eo))
     assert fast.stats()["groups"] > 1 or len(many) <= 32
