@@ -139,7 +139,7 @@ struct gsim_gpu_context {
     // per-pair plane (final per-tile order)
     DevBuf<uint32_t> vals;
     uint64_t pair_capacity = 0;
-    // GSIM_GPU_INITIAL_PAIR_CAPACITY (tests): start from this capacity instead of 4 x slots,
+    // GSIM_GPU_INITIAL_PAIR_CAPACITY (tests): start from this capacity instead of 8 x slots,
     // to exercise the overflow -> regrow -> re-run path.
     uint64_t fixed_initial_capacity = 0;
     // zeroed per frame: histograms, tickets, per-camera visible counts
