@@ -136,8 +136,12 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = CONFIGS[args.config](seed=1000 + rank)  # each rank renders its own environment(s)
     # --contexts K: K renderer contexts (each its own stream and workspaces) take frames in
-    # turn, so consecutive frames overlap on the GPU.
-    ctxs = [Context(local) for _ in range(args.contexts)]
+    # turn, so consecutive frames overlap on the GPU. The e2e leg drives each from its own host
+    # thread, and a waiting thread spins: keep ranks x contexts within the host's cores.
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    n_ctx = max(1, min(args.contexts, max(2, cores // max(local_world, 1) - 1)))
+    ctxs = [Context(local) for _ in range(n_ctx)]
     scenes = [c.upload(w.field) for c in ctxs]
     streams = [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local)) for c in ctxs]
     outs = [torch.empty(sum(5 * c.width * c.height for c in w.cameras), dtype=torch.float32,
