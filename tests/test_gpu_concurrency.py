@@ -120,3 +120,20 @@ def test_overlapped_copies_equal_frame_copies(oracle, monkeypatch):
             assert np.array_equal(fast.render_encoded(sf, nodes, batch, None, eo),
                                   plain.render_encoded(sp, nodes, batch, None, eo))
     assert fast.stats()["groups"] > 1 or len(many) <= 32
+
+
+def test_pinned_and_pageable_targets_agree(oracle):
+    """render() into page-locked targets (copies run asynchronously behind the compositing)
+    and into ordinary numpy arrays (each copy blocks the caller) gives the same bytes."""
+    import torch
+    from paper_2507_21981_b200 import RenderTarget
+    field, cams, frames = scene_and_frames(oracle, 2)
+    ctx = Context(0)
+    s = ctx.upload(field)
+    pinned = [RenderTarget(torch.empty((c.height, c.width, 3), pin_memory=True).numpy(),
+                           torch.empty((c.height, c.width), pin_memory=True).numpy(),
+                           torch.empty((c.height, c.width), pin_memory=True).numpy()) for c in cams]
+    for nodes in frames:
+        want = ctx.render(s, nodes, cams)
+        got = ctx.render(s, nodes, cams, None, pinned)
+        assert all(same(a, b) for a, b in zip(got, want))
