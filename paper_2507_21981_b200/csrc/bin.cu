@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinArgs a) {
         const int wd = u.tiles_x + 1;
         for (int t = threadIdx.x; t < wd * u.tiles_y; t += blockDim.x) D[t] = 0;
         __syncthreads();
-        const uint32_t wb = u.rec_begin + uint32_t(warp) * kWarpRecords;
-        walk_groups<false>(a, wb, min(wb + kWarpRecords, u.rec_end),
+        const uint32_t wb = u.rec_begin + uint32_t(warp) * uint32_t(a.warp_records);
+        walk_groups<false>(a, wb, min(wb + uint32_t(a.warp_records), u.rec_end),
                            [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
         __syncthreads();
         uint32_t* mrow = a.counts + u.mbase + uint64_t(u.unit_in_cam) * u.tc;
@@ -455,8 +455,8 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     for (uint32_t k = blockIdx.x; k < K; k += gridDim.x) {
         const Unit u = unit_info(a, k);
         const int wd = u.tiles_x + 1;
-        const uint32_t wb = u.rec_begin + uint32_t(warp) * kWarpRecords;
-        const uint32_t we = min(wb + kWarpRecords, u.rec_end);
+        const uint32_t wb = u.rec_begin + uint32_t(warp) * uint32_t(a.warp_records);
+        const uint32_t we = min(wb + uint32_t(a.warp_records), u.rec_end);
         // 1. this warp's pairs per tile (row differences, then row scans in place)
         int* D = reinterpret_cast<int*>(pos);
         for (int t = lane; t < wd * u.tiles_y; t += 32) D[t] = 0;

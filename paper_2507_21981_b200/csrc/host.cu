@@ -523,6 +523,15 @@ int bin_warps_for(uint32_t max_tc) {
     return w;
 }
 
+// Records per binning warp: 1024, fewer for small batches so the count and scatter kernels
+// still run ~8 warps per SM (a warp walks its records serially: config 0 has 93k visible).
+int warp_records_for(uint64_t slots, int n_sms) {
+    const uint64_t per = slots / (uint64_t(std::max(n_sms, 1)) * 8);
+    int w = kWarpRecords;
+    while (w > 128 && uint64_t(w) > per) w >>= 1;
+    return w;
+}
+
 // Workspaces sized for a plan (grow-only).
 void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     const uint64_t S = std::max<uint64_t>(p.slots, 1);
@@ -546,7 +555,7 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     }
     ctx->zero_block.reserve(kZeroCams + C);
     ctx->counts.reserve(4);
-    const uint64_t R = uint64_t(kWarpRecords) * bin_warps_for(p.max_tc);
+    const uint64_t R = uint64_t(warp_records_for(p.slots, ctx->num_sms)) * bin_warps_for(p.max_tc);
     const uint64_t kmax = (S + R - 1) / R + C;
     ctx->cam_vbase.reserve(C + 1);
     ctx->cam_chunk_base.reserve(C + 1);
@@ -594,7 +603,8 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
     b.max_tc = int(p.max_tc);
     b.bin_warps = bin_warps_for(p.max_tc);
     b.bitmap_peers = bitmap_peers_for(p.max_tc) ? 1 : 0;
-    b.chunk_records = kWarpRecords * b.bin_warps;
+    b.warp_records = warp_records_for(p.slots, ctx->num_sms);
+    b.chunk_records = b.warp_records * b.bin_warps;
     return b;
 }
 

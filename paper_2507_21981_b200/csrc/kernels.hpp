@@ -14,7 +14,7 @@ namespace gsim_gpu {
 constexpr int kMaxSmemSegments = 1024;
 constexpr int kMaxSmemCams = 32;        // K2 stages up to this many cameras in shared memory
 constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
-constexpr int kWarpRecords = 1024;      // depth-sorted records per warp of a binning unit
+constexpr int kWarpRecords = 1024;      // depth-sorted records per warp of a binning unit (max)
 
 struct PreprocessArgs {
     DevField field;
@@ -85,7 +85,8 @@ struct BinArgs {
     uint32_t* vals_out;              // [capacity] record slot of every pair, final order
     uint64_t capacity;
     int max_tc;                      // largest (tiles_x + 1) * (tiles_y + 1) of the batch
-    int chunk_records;               // records per unit = 1024 * bin_warps
+    int chunk_records;               // records per unit = warp_records * bin_warps
+    int warp_records;                // depth-sorted records walked by one warp (<= kWarpRecords)
     int bin_warps;                   // warps per unit CTA
     int bitmap_peers;                // scatter: lane bitmaps (small cameras) or probe
 };
