@@ -526,6 +526,12 @@ int bin_warps_for(uint32_t max_tc) {
 // Records per binning warp: 1024, fewer for small batches so the count and scatter kernels
 // still run ~8 warps per SM (a warp walks its records serially: config 0 has 93k visible).
 int warp_records_for(uint64_t slots, int n_sms) {
+    static const int forced = [] {  // GSIM_GPU_WARP_RECORDS: 128..1024 (power of two)
+        const char* e = std::getenv("GSIM_GPU_WARP_RECORDS");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 128 && v <= kWarpRecords && (v & (v - 1)) == 0 ? v : 0;
+    }();
+    if (forced) return forced;
     const uint64_t per = slots / (uint64_t(std::max(n_sms, 1)) * 8);
     int w = kWarpRecords;
     while (w > 128 && uint64_t(w) > per) w >>= 1;
