@@ -136,8 +136,8 @@ typedef struct gsim_render_stats {
     float ms_scatter;      /* pair placement in final (camera, tile, depth) order */
     float ms_raster;       /* K4 */
     float ms_total;
-    uint32_t groups;       /* camera groups the last batch was split into (32-bit record keys) */
-    float reserved;
+    uint32_t groups;       /* camera groups the last batch was split into */
+    uint32_t last_group_cameras; /* cameras of the last group (gsim_gpu_tile_lists sees these) */
 } gsim_render_stats;
 
 typedef struct gsim_gpu_context gsim_gpu_context;
@@ -162,6 +162,14 @@ int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out);
 int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* field,
                           gsim_gpu_scene** out);
 int gsim_gpu_scene_destroy(gsim_gpu_scene* scene);
+/* Streaming upload for fields that are produced piecewise (BASELINE config 4: a background plus
+ * hundreds of environments' objects, tens of millions of primitives): scene_create allocates a
+ * zeroed field of `count` primitives, scene_write fills [offset, offset + field->count) from a
+ * host view of the same sh_degree. Writes wait for the context's frames in flight. */
+int gsim_gpu_scene_create(gsim_gpu_context* ctx, uint64_t count, int32_t sh_degree,
+                          gsim_gpu_scene** out);
+int gsim_gpu_scene_write(gsim_gpu_context* ctx, gsim_gpu_scene* scene, uint64_t offset,
+                         const gsim_field_view* field);
 uint64_t gsim_gpu_scene_size(const gsim_gpu_scene* scene);
 /* transform_primitives (gaussian.cpp:65-79) in place on the device-resident field (K1). */
 int gsim_gpu_transform_primitives(gsim_gpu_context* ctx, gsim_gpu_scene* scene, uint64_t begin,
@@ -249,6 +257,12 @@ uint64_t gsim_gpu_encoded_bytes(uint32_t flags, int32_t width, int32_t height);
  * quantize8(linear_to_srgb(v)) >= k (thresholds[0] = -inf). Built on the host from the
  * reference's transfer function; needs no GPU (test hook). */
 void gsim_gpu_srgb_thresholds(float* thresholds);
+
+/* hash_target (hash.hpp:36-41): FNV-1a 64 over each image's (width, height) int32 pair and raw
+ * float bytes, rgb then depth then accum_alpha, chained from `seed` (the reference bench's
+ * first-frame image hash, bench.cpp:121-137, starts at 1469598103934665603). Host-only. */
+uint64_t gsim_gpu_hash_target(int32_t width, int32_t height, const float* rgb, const float* depth,
+                              const float* accum_alpha, uint64_t seed);
 
 /* Encode one host RenderTarget (rgb H*W*3, depth H*W, accum_alpha H*W floats) into `out`
  * (host, gsim_gpu_encoded_bytes(flags, width, height) bytes). Unused planes may be NULL. */

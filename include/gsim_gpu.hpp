@@ -24,11 +24,17 @@
 //   gsim::gpu::trace(field, nodes, rays, threshold)     GaussianBvh::trace per ray (trace.hpp:70-74)
 //
 // Errors are rethrown as the reference's gsim::validation_error (status 2) and gsim::io_error
-// (status 1). The free functions upload the field on every call (a pure function of their
-// inputs, like the reference); gsim::gpu::Renderer keeps it resident in HBM for the fast path.
+// (status 1). The free functions keep the field resident in HBM between calls: the upload is
+// cached per host thread, keyed on (primitives.data(), size, sh_degree, the global field
+// generation, a sampled content fingerprint), so a caller that passes the same field every frame
+// (Scene::render_all, scene.cpp:232-235) uploads it once. A caller that edits a field in place
+// calls gsim::gpu::invalidate() afterwards (the sampled fingerprint catches most edits, not all);
+// gsim::gpu::transform_primitives keeps the cache valid itself. gsim::gpu::Renderer is the
+// explicit resident path (upload() / ensure()).
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -73,6 +79,55 @@ inline gsim_field_view view(const GaussianField& f) {
     v.sh = p.sh.data();
     v.means_stride = v.scales_stride = v.rotations_stride = v.opacities_stride = v.sh_stride = 59;
     return v;
+}
+
+// Global field generation: invalidate() bumps it, every cached upload then refreshes.
+inline std::atomic<uint64_t>& field_generation() {
+    static std::atomic<uint64_t> g{0};
+    return g;
+}
+
+// FNV-1a over the raw bytes of up to 4096 evenly spaced primitives plus the last one: a cheap
+// (~2 MB read) guard against in-place edits that were not followed by invalidate().
+inline uint64_t field_fingerprint(const GaussianField& f) {
+    uint64_t h = 1469598103934665603ull;
+    const std::size_t n = f.size();
+    if (n == 0) return h;
+    const std::size_t step = std::max<std::size_t>(1, n / 4096);
+    auto mix = [&h](const GaussianPrimitive& p) {
+        const unsigned char* b = reinterpret_cast<const unsigned char*>(&p);
+        for (std::size_t k = 0; k < sizeof(GaussianPrimitive); ++k) {
+            h ^= b[k];
+            h *= 1099511628211ull;
+        }
+    };
+    for (std::size_t i = 0; i < n; i += step) mix(f.primitives[i]);
+    mix(f.primitives[n - 1]);
+    return h;
+}
+
+struct FieldKey {
+    const void* data = nullptr;
+    std::size_t size = 0;
+    int degree = -1;
+    uint64_t generation = 0;
+    uint64_t fingerprint = 0;
+    bool valid = false;
+    bool operator==(const FieldKey& o) const {
+        return valid && o.valid && data == o.data && size == o.size && degree == o.degree &&
+               generation == o.generation && fingerprint == o.fingerprint;
+    }
+};
+
+inline FieldKey field_key(const GaussianField& f) {
+    FieldKey k;
+    k.data = f.primitives.data();
+    k.size = f.size();
+    k.degree = f.sh_degree;
+    k.generation = field_generation().load();
+    k.fingerprint = field_fingerprint(f);
+    k.valid = true;
+    return k;
 }
 
 inline gsim_rigid rigid(const RigidTransform& t) {
@@ -193,9 +248,22 @@ public:
     void upload(const GaussianField& field) {
         const gsim_field_view v = detail::view(field);
         gsim_gpu_scene* s = nullptr;
+        key_ = detail::FieldKey{};
         detail::check(gsim_gpu_scene_upload(ctx_.get(), &v, &s), ctx_.get());
         scene_.reset(s);
+        key_ = detail::field_key(field);
     }
+
+    // Uploads the field unless the resident copy was uploaded from the same field (same
+    // storage, size, degree, generation and sampled content). Returns whether it uploaded.
+    bool ensure(const GaussianField& field) {
+        if (scene_ && detail::field_key(field) == key_) return false;
+        upload(field);
+        return true;
+    }
+
+    // The resident copy was changed on the device to match `field` (transform_primitives).
+    void adopt(const GaussianField& field) { key_ = detail::field_key(field); }
 
     std::vector<RenderTarget> render(const std::vector<SceneNode>& nodes,
                                      const std::vector<CameraModel>& cameras,
@@ -410,6 +478,7 @@ private:
     struct SceneDel { void operator()(gsim_gpu_scene* s) const { gsim_gpu_scene_destroy(s); } };
     std::unique_ptr<gsim_gpu_context, CtxDel> ctx_;
     std::unique_ptr<gsim_gpu_scene, SceneDel> scene_;
+    detail::FieldKey key_;
 };
 
 inline PoseTracks::PoseTracks(Renderer& r, const std::vector<PoseRecord>& records) {
@@ -440,24 +509,30 @@ inline PoseTracks::PoseTracks(Renderer& r, const std::vector<PoseRecord>& record
     tracks_.reset(h);
 }
 
+// One context per host thread (the reference's render is callable from any thread; contexts
+// serialise their own calls): the field cache and the workspaces live there.
 inline Renderer& default_renderer() {
-    static Renderer r(0);
+    static thread_local Renderer r(0);
     return r;
 }
+
+// Call after editing a field in place: every cached upload is refreshed on its next use.
+inline void invalidate() { detail::field_generation().fetch_add(1); }
+inline void invalidate(const GaussianField&) { invalidate(); }
 
 // Same signature and contract as gsim::render (raster.hpp:64-67).
 inline std::vector<RenderTarget> render(const GaussianField& field, const std::vector<SceneNode>& nodes,
                                         const std::vector<CameraModel>& cameras,
                                         const RasterOptions& options = {}) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     return r.render(nodes, cameras, options);
 }
 
 inline std::vector<ProjectedSplat> project(const GaussianField& field, const std::vector<SceneNode>& nodes,
                                            const CameraModel& camera) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     return r.project(nodes, camera);
 }
 
@@ -470,7 +545,7 @@ inline RenderTarget rasterize(const std::vector<ProjectedSplat>& splats, const C
 inline void transform_primitives(GaussianField& field, const IndexRange& range,
                                  const RigidTransform& transform) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     const gsim_rigid t = detail::rigid(transform);
     detail::check(gsim_gpu_transform_primitives(r.context(), r.scene(), range.begin, range.end, &t),
                   r.context());
@@ -482,13 +557,15 @@ inline void transform_primitives(GaussianField& field, const IndexRange& range,
         p.mean = Vec3(means[3 * i], means[3 * i + 1], means[3 * i + 2]);
         p.rotation = Quat(rots[4 * i], rots[4 * i + 1], rots[4 * i + 2], rots[4 * i + 3]);
     }
+    invalidate();      // other threads' cached copies of this field are stale now
+    r.adopt(field);    // this thread's resident copy was transformed in place: still current
 }
 
 // render_depth_ring (transfer.cpp:81-124): same signature, views rendered on the GPU.
 inline std::vector<DepthView> render_depth_ring(const GaussianField& field, int n_views, double radius,
                                                 int resolution) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     return r.render_depth_ring(n_views, radius, resolution);
 }
 
@@ -501,7 +578,7 @@ inline void tsdf_fuse(TsdfVolume& volume, const CameraModel& camera, const Image
 // cubes and decimation stay with the caller (extract_mesh, decimate).
 inline TsdfVolume gaussians_to_tsdf(const GaussianField& field, double voxel_size) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     return r.gaussians_to_tsdf(voxel_size);
 }
 
@@ -509,7 +586,7 @@ inline TsdfVolume gaussians_to_tsdf(const GaussianField& field, double voxel_siz
 inline PointCloud lidar_scan(const GaussianField& field, const std::vector<SceneNode>& nodes,
                              const LidarModel& lidar) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     return r.lidar_scan(nodes, lidar);
 }
 
@@ -517,7 +594,7 @@ inline PointCloud lidar_scan(const GaussianField& field, const std::vector<Scene
 inline std::vector<TraceResult> trace(const GaussianField& field, const std::vector<SceneNode>& nodes,
                                       const std::vector<Ray>& rays, double alpha_threshold = 0.5) {
     Renderer& r = default_renderer();
-    r.upload(field);
+    r.ensure(field);
     return r.trace(nodes, rays, alpha_threshold);
 }
 

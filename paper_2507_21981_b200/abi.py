@@ -85,7 +85,7 @@ class gsim_render_stats(C.Structure):
                 ("ms_preprocess", C.c_float), ("ms_depth_sort", C.c_float),
                 ("ms_binning", C.c_float), ("ms_scatter", C.c_float),
                 ("ms_raster", C.c_float), ("ms_total", C.c_float),
-                ("groups", C.c_uint32), ("reserved", C.c_float)]
+                ("groups", C.c_uint32), ("last_group_cameras", C.c_uint32)]
 
 
 class gsim_tsdf_volume(C.Structure):
@@ -122,6 +122,8 @@ SIGNATURES = [
     ("gsim_gpu_get_stats", C.c_int, [_P, C.POINTER(gsim_render_stats)]),
     ("gsim_gpu_scene_upload", C.c_int, [_P, C.POINTER(gsim_field_view), C.POINTER(_P)]),
     ("gsim_gpu_scene_destroy", C.c_int, [_P]),
+    ("gsim_gpu_scene_create", C.c_int, [_P, C.c_uint64, C.c_int32, C.POINTER(_P)]),
+    ("gsim_gpu_scene_write", C.c_int, [_P, _P, C.c_uint64, C.POINTER(gsim_field_view)]),
     ("gsim_gpu_scene_size", C.c_uint64, [_P]),
     ("gsim_gpu_transform_primitives", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(gsim_rigid)]),
     ("gsim_gpu_scene_download", C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -153,6 +155,8 @@ SIGNATURES = [
                                      C.POINTER(gsim_target)]),
     ("gsim_gpu_encoded_bytes", C.c_uint64, [C.c_uint32, C.c_int32, C.c_int32]),
     ("gsim_gpu_srgb_thresholds", None, [C.POINTER(C.c_float)]),
+    ("gsim_gpu_hash_target", C.c_uint64, [C.c_int32, C.c_int32, C.POINTER(C.c_float),
+                                          C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_uint64]),
     ("gsim_gpu_encode_host", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_float),
                                        C.POINTER(C.c_float), C.POINTER(C.c_float),
                                        C.POINTER(gsim_encode_options), C.POINTER(C.c_uint8)]),

@@ -268,6 +268,28 @@ class RenderTarget:
                             np.zeros((height, width), np.float32),
                             np.zeros((height, width), np.float32))
 
+    def check(self, width: int, height: int, who: str = "target") -> None:
+        """The library writes W*H*5 float32 values through these pointers: every plane must be
+        a C-contiguous float32 array of the camera's shape (ValidationError otherwise)."""
+        for name, arr, shape in (("rgb", self.rgb, (height, width, 3)),
+                                 ("depth", self.depth, (height, width)),
+                                 ("accum_alpha", self.accum_alpha, (height, width))):
+            if not isinstance(arr, np.ndarray) or arr.dtype != np.float32:
+                raise ValidationError(f"{who}.{name}: need a float32 numpy array")
+            if not arr.flags["C_CONTIGUOUS"] or not arr.flags["WRITEABLE"]:
+                raise ValidationError(f"{who}.{name}: need a writeable C-contiguous array")
+            if arr.shape != shape:
+                raise ValidationError(f"{who}.{name}: shape {arr.shape}, camera needs {shape}")
+
+    def hash(self, seed: int = 1469598103934665603) -> int:
+        """hash_target (hash.hpp:36-41), chained from `seed`."""
+        h, w = self.depth.shape
+        self.check(w, h)
+        fp = C.POINTER(C.c_float)
+        return int(abi.load_library().gsim_gpu_hash_target(
+            w, h, self.rgb.ctypes.data_as(fp), self.depth.ctypes.data_as(fp),
+            self.accum_alpha.ctypes.data_as(fp), C.c_uint64(seed)))
+
     def to_c(self) -> abi.gsim_target:
         t = abi.gsim_target()
         fp = C.POINTER(C.c_float)
@@ -275,6 +297,18 @@ class RenderTarget:
         t.depth = self.depth.ctypes.data_as(fp)
         t.accum_alpha = self.accum_alpha.ctypes.data_as(fp)
         return t
+
+
+def _targets_array(targets, cams_c, n: int):
+    """C array of host targets, one per camera, each checked against its camera's size."""
+    targets = list(targets)
+    if len(targets) != n:
+        raise ValidationError(f"render: {len(targets)} targets for {n} cameras")
+    ta = (abi.gsim_target * max(n, 1))()
+    for k, t in enumerate(targets):
+        t.check(cams_c[k].width, cams_c[k].height, f"targets[{k}]")
+        ta[k] = t.to_c()
+    return ta
 
 
 class GaussianField:
@@ -447,6 +481,12 @@ class Scene:
         _check(self.ctx.lib.gsim_gpu_transform_primitives(self.ctx.ptr, self.handle, begin, end,
                                                           C.byref(t)), self.ctx.ptr)
 
+    def write(self, offset: int, field: GaussianField) -> None:
+        """Fill primitives [offset, offset + field.size()) (gsim_gpu_scene_write)."""
+        v = field.view()
+        _check(self.ctx.lib.gsim_gpu_scene_write(self.ctx.ptr, self.handle, int(offset), C.byref(v)),
+               self.ctx.ptr)
+
     def download(self):
         means = np.zeros((self.size, 3))
         rots = np.zeros((self.size, 4))
@@ -562,6 +602,12 @@ class Context:
         _check(self.lib.gsim_gpu_scene_upload(self.ptr, C.byref(v), C.byref(h)), self.ptr)
         return Scene(self, h, field.size())
 
+    def create_scene(self, count: int, sh_degree: int) -> Scene:
+        """A zeroed device field of `count` primitives, filled piecewise with Scene.write."""
+        h = C.c_void_p()
+        _check(self.lib.gsim_gpu_scene_create(self.ptr, int(count), int(sh_degree), C.byref(h)), self.ptr)
+        return Scene(self, h, int(count))
+
     def load_ply(self, path) -> Scene:
         """load_splat_ply (splat_ply.cpp:40-162) straight into a device-resident field."""
         h = C.c_void_p()
@@ -597,9 +643,7 @@ class Context:
         opt = (options or RasterOptions()).to_c()
         if targets is None:
             targets = [RenderTarget.empty(ca[k].width, ca[k].height) for k in range(len(cameras))]
-        ta = (abi.gsim_target * max(len(cameras), 1))()
-        for k, t in enumerate(targets):
-            ta[k] = t.to_c()
+        ta = _targets_array(targets, ca, len(cameras))
         _check(self.lib.gsim_gpu_render(self.ptr, scene.handle, na, len(nodes), ca, len(cameras),
                                         C.byref(opt), ta), self.ptr)
         return list(targets)
@@ -652,8 +696,9 @@ class Context:
                                                ca, len(cameras), C.byref(opt),
                                                C.c_void_p(device_out), None), self.ptr)
             return device_out
-        targets = targets or [RenderTarget.empty(c.width, c.height) for c in cameras]
-        ta = (abi.gsim_target * max(len(cameras), 1))(*[t.to_c() for t in targets])
+        if targets is None:
+            targets = [RenderTarget.empty(ca[k].width, ca[k].height) for k in range(len(cameras))]
+        ta = _targets_array(targets, ca, len(cameras))
         _check(self.lib.gsim_gpu_render_at(self.ptr, scene.handle, tracks.handle, float(time), na,
                                            nt.ctypes.data_as(C.POINTER(C.c_int64)), len(nodes), ca,
                                            len(cameras), C.byref(opt), None, ta), self.ptr)

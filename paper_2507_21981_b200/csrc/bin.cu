@@ -448,6 +448,10 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     // kk < 2^16 and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
     __shared__ uint32_t s_magic[257];
     for (int w = threadIdx.x; w <= 256; w += blockDim.x) s_magic[w] = w > 1 ? 0xFFFFFFFFu / uint32_t(w) + 1u : 0u;
+    // the lane bitmaps are cleared once over the batch's largest grid; every placement step
+    // leaves them cleared, so units of any camera (a block may take several) start clean
+    if (kBitmap)
+        for (int t = lane; t < a.max_tc; t += 32) peer_bits[t] = 0u;
     __syncthreads();
     const uint32_t K = *a.n_chunks;
     // pair positions are 32-bit; a capacity beyond that bounds nothing
@@ -460,8 +464,6 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         // 1. this warp's pairs per tile (row differences, then row scans in place)
         int* D = reinterpret_cast<int*>(pos);
         for (int t = lane; t < wd * u.tiles_y; t += 32) D[t] = 0;
-        if (kBitmap && k == blockIdx.x)  // the bitmaps are left cleared by every step
-            for (int t = lane; t < wd * u.tiles_y; t += 32) peer_bits[t] = 0u;
         __syncwarp();
         walk_groups<false>(a, wb, we, [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
         __syncwarp();

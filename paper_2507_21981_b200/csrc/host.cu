@@ -664,6 +664,15 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         queue_camera_copies(ctx, p, out);
 }
 
+// Pair positions (bin.cu scatter, raster.cu list bounds) are 32-bit: a camera group with 2^32 or
+// more (tile, record) pairs would wrap them (writes stay inside the buffer: they are bounded by
+// the capacity), so its frame is refused instead of being returned scrambled.
+void check_pair_positions(unsigned long long pairs) {
+    if (pairs >= (1ull << 32))
+        throw ValidationError{"camera group has " + std::to_string(pairs) +
+                              " (tile, splat) pairs (>= 2^32); render fewer cameras per call"};
+}
+
 // K3 + K4 over records/keys/rects already produced for `p` (by K2 or the splat converter).
 void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
                          float* out, uint64_t& launches, bool wait_for_count) {
@@ -762,6 +771,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
         ctx->stats.visible = rb[0];
         ctx->stats.pairs = rb[1];
+        check_pair_positions(rb[1]);
         if (rb[1] <= ctx->pair_capacity) break;
         // Pair buffer too small: grow and place + raster again (counts and scans stay valid).
         GSIM_CK(cudaStreamSynchronize(s));
@@ -911,6 +921,7 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
     ctx->stats.launches = launches;
     ctx->stats.h2d_bytes = h2d;
     ctx->stats.groups = uint32_t((n_cams + group - 1) / std::max<uint64_t>(group, 1));
+    ctx->stats.last_group_cameras = uint32_t(ctx->last_plan.cams.size());
     return offsets;
 }
 
@@ -925,6 +936,7 @@ bool check_pending(gsim_gpu_context* ctx) {
     const unsigned long long* rb = static_cast<const unsigned long long*>(ctx->readback.ptr);
     ctx->stats.visible = rb[0];
     ctx->stats.pairs = rb[1];
+    check_pair_positions(rb[1]);
     if (rb[1] <= ctx->pair_capacity) return false;
     GSIM_CK(cudaStreamSynchronize(ctx->stream));
     ctx->pair_capacity = rb[1] + rb[1] / 4 + (1u << 20);
@@ -1635,51 +1647,102 @@ int gsim_gpu_get_stats(gsim_gpu_context* ctx, gsim_render_stats* out) {
     });
 }
 
-int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_gpu_scene** out) {
-    return Guard(ctx).run([&] {
-        if (!v || !out) throw ValidationError{"scene_upload: null argument"};
-        if (v->sh_degree < 0 || v->sh_degree > 3)  // gaussian.cpp:15-17
-            throw ValidationError{"sh_degree " + std::to_string(v->sh_degree) + " outside [0,3]"};
-        const uint64_t n = v->count;
-        if (n >= 0xFFFFFFFFull) throw ValidationError{"field larger than 2^32 - 1 primitives"};
-        if (n && (!v->means || !v->scales || !v->rotations || !v->opacities || !v->sh))
-            throw ValidationError{"scene_upload: null field array"};
-        const int K = (v->sh_degree + 1) * (v->sh_degree + 1);
-        const int planes = (3 * K + 3) / 4;
-        const uint64_t nn = std::max<uint64_t>(n, 1);
-        std::vector<double> geo(11 * nn, 0.0);
-        std::vector<float4> sh(size_t(planes) * nn, make_float4(0, 0, 0, 0));
-        for (uint64_t i = 0; i < n; ++i) {
-            const double* m = v->means + i * v->means_stride;
-            const double* s = v->scales + i * v->scales_stride;
+namespace {
+void check_view(const gsim_field_view* v, const char* who) {
+    if (!v) throw ValidationError{std::string(who) + ": null argument"};
+    if (v->sh_degree < 0 || v->sh_degree > 3)  // gaussian.cpp:15-17
+        throw ValidationError{"sh_degree " + std::to_string(v->sh_degree) + " outside [0,3]"};
+    if (v->count >= 0xFFFFFFFFull) throw ValidationError{"field larger than 2^32 - 1 primitives"};
+    if (v->count && (!v->means || !v->scales || !v->rotations || !v->opacities || !v->sh))
+        throw ValidationError{std::string(who) + ": null field array"};
+}
+
+// Primitives [offset, offset + v->count) of the scene from a host view: converted to the
+// device layout (double geometry planes, fp32 SH float4 planes) in host chunks, each plane's
+// slice copied into place.
+void write_scene(gsim_gpu_context* ctx, gsim_gpu_scene* sc, uint64_t offset, const gsim_field_view* v) {
+    const uint64_t nn = std::max<uint64_t>(sc->f.n, 1);
+    const int K = (sc->f.sh_degree + 1) * (sc->f.sh_degree + 1);
+    const int planes = sc->f.sh_planes;
+    constexpr uint64_t kChunk = 1u << 20;
+    std::vector<double> geo;
+    std::vector<float4> sh;
+    for (uint64_t b = 0; b < v->count; b += kChunk) {
+        const uint64_t m = std::min<uint64_t>(kChunk, v->count - b);
+        geo.assign(11 * m, 0.0);
+        sh.assign(size_t(planes) * m, make_float4(0, 0, 0, 0));
+        for (uint64_t j = 0; j < m; ++j) {
+            const uint64_t i = b + j;
+            const double* mu = v->means + i * v->means_stride;
+            const double* sc3 = v->scales + i * v->scales_stride;
             const double* q = v->rotations + i * v->rotations_stride;
-            geo[0 * nn + i] = m[0];
-            geo[1 * nn + i] = m[1];
-            geo[2 * nn + i] = m[2];
-            geo[3 * nn + i] = s[0];
-            geo[4 * nn + i] = s[1];
-            geo[5 * nn + i] = s[2];
-            geo[6 * nn + i] = q[0];
-            geo[7 * nn + i] = q[1];
-            geo[8 * nn + i] = q[2];
-            geo[9 * nn + i] = q[3];
-            geo[10 * nn + i] = v->opacities[i * v->opacities_stride];
+            for (int c = 0; c < 3; ++c) geo[c * m + j] = mu[c];
+            for (int c = 0; c < 3; ++c) geo[(3 + c) * m + j] = sc3[c];
+            for (int c = 0; c < 4; ++c) geo[(6 + c) * m + j] = q[c];
+            geo[10 * m + j] = v->opacities[i * v->opacities_stride];
             const double* c = v->sh + i * v->sh_stride;
             float tmp[48 + 4] = {0};
             for (int ch = 0; ch < 3; ++ch)
                 for (int k = 0; k < K; ++k) tmp[ch * K + k] = float(c[ch * 16 + k]);
             for (int p = 0; p < planes; ++p)
-                sh[size_t(p) * nn + i] = make_float4(tmp[4 * p], tmp[4 * p + 1], tmp[4 * p + 2], tmp[4 * p + 3]);
+                sh[size_t(p) * m + j] = make_float4(tmp[4 * p], tmp[4 * p + 1], tmp[4 * p + 2], tmp[4 * p + 3]);
         }
-        gsim_gpu_scene* sc = alloc_scene(ctx, n, v->sh_degree);
+        for (int pl = 0; pl < 11; ++pl)
+            GSIM_CK(cudaMemcpy(sc->f.mx + pl * nn + offset + b, geo.data() + pl * m, m * sizeof(double),
+                               cudaMemcpyHostToDevice));
+        for (int p = 0; p < planes; ++p)
+            GSIM_CK(cudaMemcpy(sc->f.sh + size_t(p) * nn + offset + b, sh.data() + size_t(p) * m,
+                               m * sizeof(float4), cudaMemcpyHostToDevice));
+    }
+    (void)ctx;
+}
+}  // namespace
+
+int gsim_gpu_scene_upload(gsim_gpu_context* ctx, const gsim_field_view* v, gsim_gpu_scene** out) {
+    return Guard(ctx).run([&] {
+        check_view(v, "scene_upload");
+        if (!out) throw ValidationError{"scene_upload: null argument"};
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        gsim_gpu_scene* sc = alloc_scene(ctx, v->count, v->sh_degree);
         try {
-            GSIM_CK(cudaMemcpy(sc->f.mx, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
-            GSIM_CK(cudaMemcpy(sc->f.sh, sh.data(), sh.size() * sizeof(float4), cudaMemcpyHostToDevice));
+            write_scene(ctx, sc, 0, v);
         } catch (...) {
             discard_scene(ctx, sc);
             throw;
         }
         *out = sc;
+    });
+}
+
+int gsim_gpu_scene_create(gsim_gpu_context* ctx, uint64_t count, int32_t sh_degree, gsim_gpu_scene** out) {
+    return Guard(ctx).run([&] {
+        if (!out) throw ValidationError{"scene_create: null argument"};
+        if (sh_degree < 0 || sh_degree > 3)
+            throw ValidationError{"sh_degree " + std::to_string(sh_degree) + " outside [0,3]"};
+        if (count >= 0xFFFFFFFFull) throw ValidationError{"field larger than 2^32 - 1 primitives"};
+        gsim_gpu_scene* sc = alloc_scene(ctx, count, sh_degree);
+        const uint64_t nn = std::max<uint64_t>(count, 1);
+        const size_t geo_bytes = (11 * nn * sizeof(double) + 255) & ~size_t(255);
+        if (cudaMemset(sc->mem, 0, geo_bytes + size_t(sc->f.sh_planes) * nn * sizeof(float4)) != cudaSuccess) {
+            discard_scene(ctx, sc);
+            throw CudaError{"scene_create: memset failed"};
+        }
+        *out = sc;
+    });
+}
+
+int gsim_gpu_scene_write(gsim_gpu_context* ctx, gsim_gpu_scene* scene, uint64_t offset,
+                         const gsim_field_view* v) {
+    return Guard(ctx).run([&] {
+        check_view(v, "scene_write");
+        if (!scene) throw ValidationError{"scene_write: null scene"};
+        if (v->sh_degree != scene->f.sh_degree)
+            throw ValidationError{"scene_write: sh_degree " + std::to_string(v->sh_degree) +
+                                  " differs from the scene's " + std::to_string(scene->f.sh_degree)};
+        if (offset > scene->f.n || v->count > scene->f.n - offset)
+            throw ValidationError{"scene_write: range exceeds field size"};
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));  // frames in flight may read the field
+        write_scene(ctx, scene, offset, v);
     });
 }
 
@@ -1925,6 +1988,30 @@ uint64_t gsim_gpu_encoded_bytes(uint32_t flags, int32_t width, int32_t height) {
         return 0;
     if (width <= 0 || height <= 0) return 0;
     return uint64_t(encoded_bpp(flags)) * uint64_t(width) * uint64_t(height);
+}
+
+namespace {
+uint64_t fnv1a(const void* data, size_t size, uint64_t h) {  // hash.hpp:17-25
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < size; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+uint64_t hash_image(int32_t w, int32_t h, const float* v, size_t channels, uint64_t seed) {
+    const int32_t dims[2] = {w, h};  // hash.hpp:29-34
+    seed = fnv1a(dims, sizeof(dims), seed);
+    return fnv1a(v, size_t(w) * size_t(h) * channels * sizeof(float), seed);
+}
+}  // namespace
+
+uint64_t gsim_gpu_hash_target(int32_t width, int32_t height, const float* rgb, const float* depth,
+                              const float* accum_alpha, uint64_t seed) {
+    if (width < 0 || height < 0 || !rgb || !depth || !accum_alpha) return 0;
+    uint64_t h = hash_image(width, height, rgb, 3, seed);
+    h = hash_image(width, height, depth, 1, h);
+    return hash_image(width, height, accum_alpha, 1, h);
 }
 
 void gsim_gpu_srgb_thresholds(float* thresholds) {

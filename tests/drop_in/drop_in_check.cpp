@@ -64,6 +64,44 @@ int main() {
         if (f < 0.999) ++failures;
     }
 
+    // upload cache (gsim_gpu.hpp field_key): the same field is not re-uploaded; a field edited
+    // in place (sampled by the fingerprint, or announced with invalidate()) and a second field
+    // are; every render still matches the reference of the field it was given
+    {
+        gpu::Renderer& r = gpu::default_renderer();
+        const bool again = r.ensure(field);
+        std::printf("upload cache: same field re-uploaded = %d\n", again);
+        if (again) ++failures;
+        GaussianField edited = field;  // other storage: a different key
+        for (auto& p : edited.primitives) p.mean.x += 0.05;
+        const auto ref_e = render(edited, nodes, cams);
+        const auto gpu_e = gpu::render(edited, nodes, cams);
+        // in-place edit of one unsampled primitive's colour, announced with invalidate()
+        edited.primitives[1].sh[0] += 3.0;
+        edited.primitives[1].opacity = 0.99;
+        gpu::invalidate(edited);
+        const auto ref_i = render(edited, nodes, cams);
+        const auto gpu_i = gpu::render(edited, nodes, cams);
+        // in-place edit of every primitive's position, caught by the fingerprint alone
+        for (auto& p : edited.primitives) p.mean.y -= 0.07;
+        const auto ref_f = render(edited, nodes, cams);
+        const auto gpu_f = gpu::render(edited, nodes, cams);
+        const auto gpu_back = gpu::render(field, nodes, cams);  // the first field again
+        double worst = 1.0;
+        for (int k = 0; k < 2; ++k) {
+            worst = std::fmin(worst, frac_within(gpu_e[k], ref_e[k], 2e-3, 1e-3));
+            worst = std::fmin(worst, frac_within(gpu_i[k], ref_i[k], 2e-3, 1e-3));
+            worst = std::fmin(worst, frac_within(gpu_f[k], ref_f[k], 2e-3, 1e-3));
+            worst = std::fmin(worst, frac_within(gpu_back[k], ref[k], 2e-3, 1e-3));
+        }
+        bool differs = false;  // the announced edit really changed the image
+        for (std::size_t p = 0; p < gpu_i[0].rgb.data.size(); ++p)
+            differs |= gpu_i[0].rgb.data[p] != gpu_e[0].rgb.data[p];
+        std::printf("upload cache: worst %.5f of pixels within tolerance after edits, edit visible %d\n",
+                    worst, differs);
+        if (worst < 0.999) ++failures;
+    }
+
     // project: geometry bit-exact (double), rgb close
     const auto sp_ref = project(field, nodes, cams[0]);
     const auto sp_gpu = gpu::project(field, nodes, cams[0]);

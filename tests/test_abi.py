@@ -78,3 +78,18 @@ def test_field_view_strides_cover_aos_and_soa():
     assert v.count == n and v.means_stride == 3 and v.sh_stride == 48
     assert v.means[3 * 2 + 1] == aos[2, 1]
     assert v.sh[48 * 4 + 47] == aos[4, 58]
+
+
+def test_hash_target_matches_reference_hash(lib, oracle):
+    """gsim_gpu_hash_target (host FNV-1a) equals hash.hpp:36-41 as restated by the oracle (pinned
+    to the reference's own image hashes in test_oracle_pin.py), chained seeds included."""
+    from paper_2507_21981_b200.api import RenderTarget
+    rng = np.random.default_rng(5)
+    t = RenderTarget(rng.random((7, 9, 3), dtype=np.float32), rng.random((7, 9), dtype=np.float32),
+                     rng.random((7, 9), dtype=np.float32))
+    assert t.hash() == oracle.hash_target(t)
+    assert t.hash(12345) == oracle.hash_target(t, 12345)
+    bad = RenderTarget(t.rgb.astype(np.float64), t.depth, t.accum_alpha)
+    from paper_2507_21981_b200 import ValidationError
+    with pytest.raises(ValidationError):
+        bad.hash()
