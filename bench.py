@@ -3,18 +3,25 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg1]
 
-A step is one frame of BASELINE config 1 (the metric's configuration): a 1M-Gaussian SH3
-background + 4 x 20k object nodes with fresh random rigid poses, rendered by 5 cameras at
-640x480 into RGB + depth + accumulated alpha. Under torchrun (N > 1) every rank renders its own
-environment's frame (weak scaling, no data-path collective); the timed region is bracketed by a
-barrier + synchronize on both sides and the elapsed device time is the max over ranks.
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run
+(N ranks, 127.0.0.1); under torchrun, WORLD_SIZE must equal N.
 
-value  : camera-frames/s over all ranks, scene resident in HBM, outputs left in HBM
-         (CUDA events on the renderer's stream).
+cfg0-cfg3: a step is one frame of the BASELINE config (default cfg1, the metric's
+configuration: a 1M-Gaussian SH3 background + 4 x 20k object nodes with fresh random rigid
+poses, rendered by 5 cameras at 640x480 into RGB + depth + accumulated alpha). Under N > 1
+every rank renders its own environment's frame (weak scaling, no data-path collective).
+cfg4 (BASELINE config 4): a step is the whole 512-environment x 5-camera batch, split over the
+ranks by environment; every rank renders its environments in chunks of <= 64 (config-2-sized
+launches) and the frames of chunk j go to rank 0 with grouped NCCL point-to-point while chunk
+j+1 renders (shard.ChunkGather); value is box-wide camera-frames/s (strong scaling).
+The timed region is bracketed by a barrier + synchronize on both sides and the elapsed device
+time (CUDA events on the renderer's stream) is the max over ranks.
+
+value  : camera-frames/s over all ranks, scene resident in HBM, outputs left in HBM.
 e2e    : the same metric through the public API with host buffers: per step the node/camera
          tables go host->device and the 20 B/px RGB-D targets come back device->host into
          pinned memory (gsim_gpu_render), one host thread per renderer context.
-roofline / cpu_baseline: see DESIGN.md §Measurement.
+roofline / cpu_baseline: see DESIGN.md §5.
 """
 from __future__ import annotations
 
@@ -37,13 +44,15 @@ sys.path.insert(0, str(ROOT))
 METRIC = "RGB-D camera-frames/sec (5 cams 640x480, 1M Gaussians)"
 UNIT = "camera-frames/s"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+PAPER_CAMERA_FRAMES_PER_S = 650.0 * 5  # BASELINE.md, stricter unit reading (one GPU)
+FNV_SEED = 1469598103934665603
 
 
 def peaks() -> tuple[dict, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         return json.loads(p.read_text()), "measured"
-    return PEAKS_FALLBACK, "fallback"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
@@ -53,79 +62,132 @@ def dist_env():
     return rank, world, local
 
 
+def machine_descriptor() -> str:
+    """bench.cpp:79-96: first /proc/cpuinfo model name + hardware threads."""
+    model = "unknown-cpu"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model} ({os.cpu_count() or 1} hw threads)"
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled every 2 ms through NVML during the timed region
+    (nvidia-smi at 100 ms when NVML is unavailable)."""
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.nvml = None
 
     def start(self):
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.device])
+                except ValueError:
+                    pass
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.nvml = None
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        pynvml, h = self.nvml
+        while not self.stop_ev.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self) -> dict | None:
-        if self.proc is None:
+        if self.nvml is None:
             return None
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        rows = []
-        for line in Path(self.path).read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
-        os.unlink(self.path)
-        if not rows:
+        self.stop_ev.set()
+        self.thread.join(timeout=2)
+        pynvml, _ = self.nvml
+        if not self.rows:
             return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted(name for name, attr in self.NAMES.items()
+                         if any(r[1] & getattr(pynvml, attr, 0) for r in self.rows))
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)),
+                "sm_max_mhz": float(self.max_mhz), "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml, 2 ms"}
 
 
-# ---- algorithmic byte model (DESIGN.md §Measurement) ----------------------------------------
+# ---- byte models (DESIGN.md §5) ----------------------------------------------------------------
+
+def survey_bytes(stats: dict, n_unique: int, n_obj: int, sh_degree: int, n_cams: int,
+                 slots_per_cam: float, pixels: int) -> dict:
+    """SURVEY.md §8(d) algorithmic bytes of one step (a reference-style pipeline that sorts the
+    P pairs on 46-bit keys; fp32 records of 40 B): the model roofline.achieved uses."""
+    V, P, K = stats["visible"], stats["pairs"], stats["consumed"]
+    passes = math.ceil(46 / 8)
+    return {
+        "pose": 56 * n_obj,
+        "preprocess": (44 + 12 * (sh_degree + 1) ** 2) * n_unique + 48 * V,
+        "scan": 12 * n_cams * slots_per_cam,
+        "duplicate": 16 * V + 12 * P,
+        "sort": passes * 24 * P + 8 * P,
+        "ranges": 8 * P,
+        "raster": 44 * K + 20 * pixels,
+    }
+
 
 def stage_bytes(stats: dict, n_prims: int, sh_degree: int, pixels: int, n_cams: int) -> dict:
-    """Minimum HBM bytes each stage of OUR pipeline must move for one step."""
+    """Minimum HBM bytes each stage of OUR pipeline moves for one step (its own layout)."""
     S, V, P, K = stats["slots"], stats["visible"], stats["pairs"], stats["consumed"]
+    passes = stats["depth_passes"]
     sh_bytes = 12 * (sh_degree + 1) ** 2
-    M = stats["tiles"] // max(1, n_cams) * stats["chunks"]  # count-matrix entries
     return {
         # scene read once per batch (f64 geometry 88 B + fp32 SH) + 48 B record, 4 B key and
         # 4 B rect per visible slot, 4 B key per culled slot
         "preprocess": (88 + sh_bytes) * n_prims + 52 * V + 4 * S,
-        # histogram reads S keys; pass 1 reads S keys, writes V (key, slot); passes 2-3 read
-        # and write 8 B; pass 4 reads 8 B, writes the 4 B slot and gathers + writes the 4 B rect
-        "depth_sort": 4 * S + 4 * S + 8 * V + 2 * 16 * V + 16 * V,
-        # count: V sorted rects; column scan reads the count matrix twice and writes it once
-        "binning": 4 * V + 12 * M,
-        # scatter: V rects (recount) + V rects and slots (placement), column prefixes, P record
-        # slots written
-        "scatter": 12 * V + 4 * M + 4 * P,
-        # K list entries + 48 B records (2 sectors: 64 B) + 20 B/px outputs
-        "raster": 4 * K + 64 * K + 20 * pixels,
+        # histogram reads S keys; pass 1 reads S keys, writes V (key, slot); middle passes read
+        # and write 8 B; the last pass reads 8 B, writes the 4 B slot and gathers + writes the rect
+        "depth_sort": 4 * S + 4 * S + 8 * V + (passes - 2) * 16 * V + 16 * V,
+        "binning": 4 * V,
+        # recount V rects + V rects and slots for the placement, P record slots written
+        "scatter": 12 * V + 4 * P,
+        # SURVEY §8(d): 4 B list entry + 40 B record per consumed pair, 20 B per output pixel
+        "raster": 44 * K + 20 * pixels,
     }
 
 
-PAPER_CAMERA_FRAMES_PER_S = 650.0 * 5  # BASELINE.md, stricter unit reading
+def load_profile_json(name: str, config: str, stage: str):
+    """Per-stage figure from a committed ncu summary under profiles/, for THIS config only."""
+    p = ROOT / "profiles" / name
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(config, {}).get(stage)
+    except Exception:
+        return None
 
+
+# ---- our arm ------------------------------------------------------------------------------------
 
 def run_ours(args, rank, world, local):
     import torch
@@ -137,6 +199,8 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "cfg4":
+        return run_cfg4(args, rank, world, local, dist)
     w = CONFIGS[args.config](seed=1000 + rank)  # each rank renders its own environment(s)
     # --contexts K: K renderer contexts (each its own stream and workspaces) take frames in
     # turn, so consecutive frames overlap on the GPU. The e2e leg drives each from its own host
@@ -155,26 +219,18 @@ def run_ours(args, rank, world, local):
 
     def step(i):
         k = i % len(ctxs)
-        ptr = ctxs[k].render_device(scenes[k], w.frame_nodes(i, seed=rank), w.cameras, None,
-                                    outs[k].data_ptr())
-        if args.gather and dist:
-            # BASELINE config 4: the frame (every rank's environment) goes to rank 0 over NCCL
-            from paper_2507_21981_b200.shard import gather_frames
-            torch.cuda.current_stream().wait_stream(streams[k])
-            gather_frames(outs[k], world, outs[k].numel(), dst=0)
-            streams[k].wait_stream(torch.cuda.current_stream())
-        return ptr
+        return ctxs[k].render_device(scenes[k], w.frame_nodes(i, seed=rank), w.cameras, None,
+                                     outs[k].data_ptr())
 
     for i in range(args.warmup):
         step(i)
-    ctx.synchronize()
+    for c in ctxs:
+        c.synchronize()
 
     # ---- timed region: device-resident inputs and outputs -------------------------------
     # Frames are enqueued back to back: render_device is asynchronous (the pair-count check of
     # frame k is completed by the call for frame k+1), so the host builds the next frame's
     # plan while the GPU renders.
-    for c in ctxs:
-        c.synchronize()
     launches_before = sum(c.stats()["launches_total"] for c in ctxs)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -205,7 +261,8 @@ def run_ours(args, rank, world, local):
     ctx.set_profiling(True)
     stage_ms = {k: 0.0 for k in ("preprocess", "depth_sort", "binning", "scatter", "raster")}
     stats = None
-    for i in range(args.steps):
+    n_prof = min(args.steps, 50)
+    for i in range(n_prof):
         ctx.render_device(scene, w.frame_nodes(args.warmup + i, seed=rank), w.cameras, None,
                           outs[0].data_ptr())
         stats = ctx.stats()
@@ -219,6 +276,13 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_ms = float(t.item())
     value = world * args.steps * n_cams / (elapsed_ms / 1e3)
+
+    # first timed frame again (renders are deterministic): its image hash, bench.cpp:121-137
+    first = ctx.render(scene, w.frame_nodes(args.warmup, seed=rank), w.cameras)
+    h = FNV_SEED
+    for tg in first:
+        h = tg.hash(h)
+    first_hash = f"{h:016x}"
 
     # ---- e2e: public API, host buffers (pinned), H2D + D2H inside the timed region ------
     e2e = None
@@ -248,27 +312,32 @@ def run_ours(args, rank, world, local):
                 st = ctxs[k].stats()
                 io[k] = [st["h2d_bytes"], st["d2h_bytes"]]
 
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        torch.cuda.synchronize()
-        threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(ctxs))]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        e1.record(stream)
-        e1.synchronize()
+        def timed_threads(fn):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            torch.cuda.synchronize()
+            threads = [threading.Thread(target=fn, args=(k,)) for k in range(len(ctxs))]
+            for th in threads:
+                th.start()
+            for th in threads:
+                th.join()
+            e1.record(stream)
+            e1.synchronize()
+            te = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
+            if dist:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            return float(te.item())
+
+        te = timed_threads(worker)
         h2d, d2h = io[0]
-        te = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
-        if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * args.steps * n_cams / (float(te.item()) / 1e3), "unit": UNIT,
+        e2e = {"value": round(world * args.steps * n_cams / (te / 1e3), 2), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": float(te.item()) / args.steps, "contexts": len(ctxs)}
+               "ms_per_step": round(te / args.steps, 4), "contexts": len(ctxs),
+               "api": "gsim_gpu_render (host float targets, pinned)"}
 
         # Same loop through render_encoded: the compositing kernel writes
         # the reference CLI's outputs (sRGB RGB8, alpha8, 16-bit mm depth, PFM depth) and only
@@ -288,22 +357,8 @@ def run_ours(args, rank, world, local):
                 st = ctxs[k].stats()
                 io_enc[k] = [st["h2d_bytes"], st["d2h_bytes"]]
 
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        torch.cuda.synchronize()
-        threads = [threading.Thread(target=worker_enc, args=(k,)) for k in range(len(ctxs))]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        e1.record(stream)
-        e1.synchronize()
-        te2 = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
-        if dist:
-            dist.all_reduce(te2, op=dist.ReduceOp.MAX)
-        e2e["encoded"] = {"value": world * args.steps * n_cams / (float(te2.item()) / 1e3),
+        te2 = timed_threads(worker_enc)
+        e2e["encoded"] = {"value": round(world * args.steps * n_cams / (te2 / 1e3), 2),
                           "unit": UNIT, "h2d_bytes_per_step": int(io_enc[0][0]),
                           "d2h_bytes_per_step": int(io_enc[0][1]),
                           "outputs": "rgb8 sRGB + alpha8 + depth16 mm + depth PFM (10 B/px)"}
@@ -314,59 +369,79 @@ def run_ours(args, rank, world, local):
         return
 
     pk, pk_kind = peaks()
-    per_step_ms = {k: v / args.steps for k, v in stage_ms.items()}
+    per_step_ms = {k: v / n_prof for k, v in stage_ms.items()}
     bytes_ = stage_bytes(stats, w.field.size(), w.field.sh_degree, pixels, n_cams)
     dominant = max(per_step_ms, key=per_step_ms.get)
-    achieved = bytes_[dominant] / (per_step_ms[dominant] / 1e3) / 1e9 if per_step_ms[dominant] > 0 else 0.0
     total_ms = sum(per_step_ms.values())
-    traffic = load_traffic(dominant)
+    dom_ms = per_step_ms[dominant]
+    achieved = bytes_[dominant] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    n_obj = sum(n.range[1] - n.range[0] for k, n in enumerate(w.nodes) if k in set(w.object_nodes))
+    sv = survey_bytes(stats, w.field.size(), n_obj, w.field.sh_degree, n_cams,
+                      stats["slots"] / max(n_cams, 1), pixels)
+    sv_total = sum(sv.values())
+    ms_step = elapsed_ms / args.steps
     roofline = {
-        "bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1),
-        "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s",
-        "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
+        "bound": "hbm", "kernel": "raster_kernel" if dominant == "raster" else dominant,
+        "stage": dominant,
+        "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s",
+        "frac": round(achieved / pk["hbm_gbs"], 4),
+        "traffic": load_profile_json("traffic.json", args.config, dominant),
         "algorithmic_bytes": int(bytes_[dominant]),
-        "share_of_step": round(per_step_ms[dominant] / total_ms, 3) if total_ms else None,
+        "bytes_model": ("SURVEY 8(d): 44 B per consumed pair (4 B index + 40 B record) x K + "
+                        "20 B per pixel x X" if dominant == "raster" else "DESIGN.md §5 stage model"),
+        "counts": {"K_consumed_pairs": stats["consumed"], "X_pixels": pixels},
+        "stage_ms": round(dom_ms, 4),
+        "share_of_step": round(dom_ms / total_ms, 3) if total_ms else None,
         "stages_ms": {k: round(v, 4) for k, v in per_step_ms.items()},
         "stages_gbs": {k: round(bytes_[k] / (per_step_ms[k] / 1e3) / 1e9, 1) if per_step_ms[k] > 0 else None
                        for k in per_step_ms},
-        "pipeline_frac": round(sum(bytes_.values()) / (total_ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)
-        if total_ms else None,
+        "sector_model": {  # 48 B records fetched as two 32 B sectors: what K4 really reads
+            "bytes": int(68 * stats["consumed"] + 20 * pixels),
+            "frac": round((68 * stats["consumed"] + 20 * pixels) / (dom_ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)
+            if dominant == "raster" and dom_ms > 0 else None},
+        # the whole step against the SURVEY 8(d) pipeline model (a reference-style pipeline
+        # that sorts the P pairs): its HBM floor over our measured step time
+        "survey_pipeline": {"bytes": int(sv_total), "floor_ms": round(sv_total / pk["hbm_gbs"] / 1e6, 4),
+                            "frac": round(sv_total / pk["hbm_gbs"] / 1e6 / ms_step, 4) if world == 1 else None,
+                            "stages": {k: int(v) for k, v in sv.items()}},
     }
     # The rasterizer is FP32-issue-bound, not HBM-bound: its warp instructions
-    # per frame (profiles/instructions.json, ncu) over the live stage time, against the issue
-    # peak of 4 warp instructions per SM per cycle at the sampled SM clock.
-    inst = load_profile_json("instructions.json", dominant)
-    if inst and per_step_ms[dominant] > 0:
+    # per frame (ncu, same config) over the live stage time, against the issue peak of 4 warp
+    # instructions per SM per cycle at the sampled SM clock.
+    inst = load_profile_json("instructions.json", args.config, dominant)
+    if inst and dom_ms > 0:
         sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
         n_sms = torch.cuda.get_device_properties(local).multi_processor_count
         peak_ipc = n_sms * 4 * sm_mhz * 1e6
-        ach = inst / (per_step_ms[dominant] / 1e3)
+        ach = inst / (dom_ms / 1e3)
         roofline["issue"] = {"kernel": dominant, "warp_instructions": int(inst),
                              "achieved": round(ach / 1e9, 1), "peak": round(peak_ipc / 1e9, 1),
                              "unit": "G warp-instr/s", "frac": round(ach / peak_ipc, 4)}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "weak",
-        # the paper's "650 FPS" for 5 cameras at 640x480 (RTX 6000 Ada), gated on the
-        # stricter reading 650 five-camera frames/s = 3250 camera-frames/s
-        "vs_baseline": round(value / PAPER_CAMERA_FRAMES_PER_S, 3) if args.config == "cfg1" else None,
-        "vs_baseline_basis": "paper 650 five-camera frames/s = 3250 camera-frames/s (BASELINE.md)",
-        "dtype": "f32 (f64 geometry)", "data": "synthetic",
+        # the paper's "650 FPS" for 5 cameras at 640x480 on ONE GPU (RTX 6000 Ada),
+        # gated on the stricter reading 650 five-camera frames/s = 3250 camera-frames/s; per GPU
+        "vs_baseline": round(value / world / PAPER_CAMERA_FRAMES_PER_S, 3) if args.config == "cfg1" else None,
+        "vs_baseline_basis": ("device-resident value per GPU / paper 650 five-camera frames/s "
+                              "= 3250 camera-frames/s (BASELINE.md)"),
+        "dtype": "f32 (f64 geometry)", "data": "synthetic (seeded, BASELINE.json distributions)",
         "config": {"workload": f"{args.config}: {w.description}", "gaussians": w.field.size(),
                    "sh_degree": w.field.sh_degree, "cameras_per_rank": n_cams,
                    "resolution": f"{w.cameras[0].width}x{w.cameras[0].height}",
                    "parallelism": (f"env-sharded x{world} (replicated background, "
-                                   + ("frames gathered to rank 0 over NCCL each step)" if args.gather and world > 1
-                                      else "no data-path collective)")),
+                                   "no data-path collective)"),
                    "l2": "inputs larger than L2 (scene 300 MB, per-frame working set > 500 MB); no flush",
                    "seed": "1000+rank", "contexts_per_gpu": len(ctxs)},
         "five_camera_frames_per_s": round(value / n_cams, 2),
         "e2e": e2e,
         "gpu_launches": int(launches),
+        "first_frame_hash": first_hash,
+        "machine": machine_descriptor(),
         "stats_last_step": {k: stats[k] for k in ("slots", "visible", "pairs", "consumed", "tiles",
-                                                  "depth_passes", "chunks")},
+                                                  "depth_passes", "groups")},
         "roofline": roofline,
         "clocks": clocks,
         "wall_s_timed": round(wall, 4),
@@ -378,20 +453,113 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
 
 
-def load_profile_json(name: str, stage: str):
-    """Per-stage figure from a committed ncu summary under profiles/ (None if absent)."""
-    p = ROOT / "profiles" / name
-    if p.exists():
-        try:
-            return json.loads(p.read_text()).get(stage)
-        except Exception:
-            return None
-    return None
+def run_cfg4(args, rank, world, local, dist):
+    """BASELINE config 4: 512 envs x 5 cameras split by environment over the ranks, rendered in
+    <= 64-env chunks, frames gathered to rank 0 (shard.ChunkGather) behind the next chunk."""
+    import torch
+    from paper_2507_21981_b200 import Context
+    from paper_2507_21981_b200.scenes import config4_rank
+    from paper_2507_21981_b200.shard import ChunkGather, env_range
 
+    dev = torch.device("cuda", local)
+    n_envs = args.envs
+    b, e = env_range(n_envs, rank, world)
+    ctx = Context(local)
+    t0 = time.perf_counter()
+    r = config4_rank(ctx, b, e, seed=1000, n_envs=n_envs)
+    setup_s = time.perf_counter() - t0
+    cams_per_env = r.cams_per_env
+    px_per_env = sum(c.width * c.height for c in r.cameras[:cams_per_env])
+    fpe = 5 * px_per_env
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    gather = ChunkGather(n_envs, fpe, args.chunk_envs, dev, rank=rank, world=world, dst=0)
+    chunk_cams = [r.camera_table(cb, ce) for cb, ce in gather.my_chunks]
 
-def load_traffic(stage: str):
-    """dram read+write bytes per frame of the stage's kernels from the committed ncu capture."""
-    return load_profile_json("traffic.json", stage)
+    def step(i, sums=None):
+        nodes = r.frame_nodes(i)
+        with torch.cuda.stream(stream):
+            for j in range(len(gather.my_chunks)):
+                buf = gather.target(j)
+                ctx.render_device(r.scene, nodes, chunk_cams[j], None, buf.data_ptr())
+                if sums is not None:  # exact per-env checksums of what this rank sends
+                    cb, ce = gather.my_chunks[j]
+                    sums[cb:ce] = buf.view(ce - cb, fpe).view(torch.int32).sum(1, dtype=torch.int64)
+                gather.send(j)
+            gather.finish()
+
+    for i in range(args.warmup):
+        step(i)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    launches_before = ctx.stats()["launches_total"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    ev0.record(stream)
+    t_wall = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    launches = ctx.stats()["launches_total"] - launches_before
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
+    if dist:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    cam_frames = n_envs * cams_per_env
+    value = args.steps * cam_frames / (elapsed_ms / 1e3)
+    # One more step with checksums: rank 0's gathered blocks must equal, bit for bit, what every
+    # rank rendered (exact integer sums of the float bits per environment).
+    sums = torch.zeros(n_envs, dtype=torch.int64, device=dev)
+    step(args.warmup + args.steps, sums)
+    torch.cuda.synchronize()
+    if dist:
+        dist.all_reduce(sums)  # env ranges are disjoint: the sum assembles every rank's part
+    check = None
+    if rank == 0:
+        got = gather.out.view(n_envs, fpe).view(torch.int32).sum(1, dtype=torch.int64)
+        check = {"envs": n_envs, "mismatched_envs": int((got != sums).sum().item())}
+        if world == 1:
+            # batch == separate renders: env 3's cameras alone reproduce its block of the batch
+            e3 = min(3, n_envs - 1)
+            one = torch.empty(fpe, dtype=torch.float32, device=dev)
+            ctx.render_device(r.scene, r.frame_nodes(args.warmup + args.steps),
+                              r.camera_table(e3, e3 + 1), None, one.data_ptr())
+            ctx.synchronize()
+            check["env_batch_equals_single"] = bool(torch.equal(one, gather.out[e3 * fpe:(e3 + 1) * fpe]))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(elapsed_ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (f64 geometry)", "data": "synthetic (seeded, BASELINE.json distributions)",
+            "config": {"workload": f"cfg4: {n_envs} envs x {cams_per_env} cams 640x480, shared 1M SH3 "
+                                   "background replica per GPU + each env's 4x20k objects",
+                       "envs_per_rank": e - b, "chunk_envs": args.chunk_envs,
+                       "gaussians_per_rank": r.scene.size,
+                       "parallelism": f"env-sharded x{world}, frames gathered to rank 0 "
+                                      "(grouped NCCL P2P, overlapped with the next chunk)",
+                       "gather_bytes_per_step": int(gather.bytes_to_dst * 4),
+                       "l2": "inputs larger than L2; no flush", "seed": 1000},
+            "gpu_launches": int(launches),
+            "gather_check": check,
+            "setup_s": round(setup_s, 1),
+            "machine": machine_descriptor(),
+            "clocks": clocks,
+            "wall_s_timed": round(wall, 3),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
 
 
 def cpu_baseline(w, budget_s: float) -> dict:
@@ -434,7 +602,7 @@ def cpu_baseline(w, budget_s: float) -> dict:
                "sample": f"1 camera of {w.name} ({d1:.1f} s)"}
         rf.close()
     out = {"value": round(frames * len(w.cameras) / dt, 4), "unit": UNIT, "cores": busy,
-           "kind": kind, "host_threads_configured": cores,
+           "kind": kind, "host_threads_configured": cores, "machine": machine_descriptor(),
            "sample": f"{frames} frame(s) x {len(w.cameras)} cameras of {w.name} ({dt:.1f} s)"}
     if one:
         out["one_thread"] = one
@@ -447,7 +615,8 @@ def run_reference(args, rank, world):
         return
     from paper_2507_21981_b200.scenes import CONFIGS
     from oracle.oracle import REF_LIB, Oracle, Ref, cpu_count
-    w = CONFIGS[args.config](seed=1000)
+    cfg = args.config if args.config != "cfg4" else "cfg2"  # cfg4 = cfg2-shaped envs
+    w = CONFIGS[cfg](seed=1000)
     cores = cpu_count()
     if REF_LIB.exists():
         ref = Ref()
@@ -461,18 +630,25 @@ def run_reference(args, rank, world):
         render = lambda nodes, cams: orc.render(w.field, nodes, cams)  # noqa: E731
     # bound the run to a few minutes: whole frames if affordable, else one camera per step
     t0 = time.perf_counter()
-    render(w.frame_nodes(0), w.cameras)
+    render(w.frame_nodes(0), w.cameras[:5])
     per_frame = time.perf_counter() - t0
-    cams = w.cameras
+    cams = w.cameras[:5]
     if per_frame * (args.steps + args.warmup) > 150:
         cams = w.cameras[:1]
     if kind == "reference":
         busy = min(len(cams), cores) if len(cams) > 1 else cores
     for i in range(args.warmup):
         render(w.frame_nodes(i + 1), cams)
+    first_hash = None
+    hasher = Oracle()  # hash_target restated (oracle pinned to hash.hpp)
     t0 = time.perf_counter()
     for i in range(args.steps):
-        render(w.frame_nodes(args.warmup + i + 1), cams)
+        targets = render(w.frame_nodes(args.warmup + i + 1), cams)
+        if i == 0:  # bench.cpp:121-137 (hashing stays inside the timed loop, as there)
+            h = FNV_SEED
+            for tg in targets:
+                h = hasher.hash_target(tg, h)
+            first_hash = f"{h:016x}"
     dt = time.perf_counter() - t0
     value = args.steps * len(cams) / dt
     line = {
@@ -482,8 +658,10 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {w.description}", "gaussians": w.field.size(),
                    "cameras_per_step": len(cams)},
+        "first_frame_hash": first_hash,
+        "machine": machine_descriptor(),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": busy, "kind": kind,
-                         "host_threads_configured": cores,
+                         "host_threads_configured": cores, "machine": machine_descriptor(),
                          "sample": f"{args.steps} steps x {len(cams)} camera(s) of {w.name}"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -492,23 +670,42 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg0", "cfg1", "cfg2", "cfg3"], default="cfg1")
+    ap.add_argument("--config", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"], default="cfg1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--contexts", type=int, default=4,
                     help="renderer contexts taking frames in turn (frame-level overlap)")
-    ap.add_argument("--gather", action="store_true",
-                    help="N > 1: gather every step's frames to rank 0 (config 4) inside the timed step")
+    ap.add_argument("--envs", type=int, default=512, help="cfg4: environments per step (box-wide)")
+    ap.add_argument("--chunk-envs", type=int, default=64, help="cfg4: environments per launch")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
+    if args.config == "cfg4" and args.steps == 400:
+        args.steps = 3  # a cfg4 step is 2560 camera-frames
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

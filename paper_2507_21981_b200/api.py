@@ -454,6 +454,8 @@ class LidarModel:
 
 
 def _nodes_array(nodes: Sequence[SceneNode]):
+    if isinstance(nodes, C.Array) and nodes._type_ is abi.gsim_node:
+        return nodes  # prebuilt table (scenes.nodes_table)
     arr = (abi.gsim_node * max(len(nodes), 1))()
     for k, n in enumerate(nodes):
         arr[k] = n.to_c() if isinstance(n, SceneNode) else n
@@ -461,6 +463,8 @@ def _nodes_array(nodes: Sequence[SceneNode]):
 
 
 def _cams_array(cameras: Sequence[CameraModel]):
+    if isinstance(cameras, C.Array) and cameras._type_ is abi.gsim_camera:
+        return cameras
     arr = (abi.gsim_camera * max(len(cameras), 1))()
     for k, c in enumerate(cameras):
         arr[k] = c.to_c() if isinstance(c, CameraModel) else c

@@ -37,10 +37,6 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kFull = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t key_camera(uint32_t key, int depth_bits) {
-    return depth_bits >= 32 ? 0u : (key >> depth_bits);
-}
-
 __device__ __forceinline__ uint32_t rect_area(uint32_t r) {
     return (((r >> 16) & 255u) - (r & 255u) + 1u) * ((r >> 24) - ((r >> 8) & 255u) + 1u);
 }
@@ -141,79 +137,66 @@ __device__ __forceinline__ uint32_t reduce_or(uint32_t v) {
 
 }  // namespace
 
-// ---- depth-key histograms + per-camera record counts ---------------------------------------
-// The three low digits are spread over many values: warp-aggregated shared atomics. The top
-// digit (camera and exponent bits) repeats within a warp: one round per distinct value (usually
-// 1-3) adds its lane count to a per-warp sub-histogram. When the camera index sits inside the
-// top digit (depth_bits >= 24) the per-camera counts follow from that histogram (chunk_table);
-// otherwise they are counted here, one round per distinct camera.
+// ---- depth-key digit histograms per (camera, pass) ------------------------------------------
+// Block b takes the contiguous slot range [b * per, (b + 1) * per) and walks it camera piece by
+// camera piece (slots are camera-major): per-warp shared histograms of every pass's digit
+// (shared atomics; their same-digit conflicts are mild because the keys are spread), summed over
+// the warps and added to the camera's global histogram when the piece ends. The per-camera
+// visible counts are the sums of the first pass's histogram (chunk_table).
 __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
-    __shared__ uint32_t s_hist[kWarps][4][256];
+    extern __shared__ __align__(16) uint32_t s_hist[];  // [kWarps][passes][radix]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < kWarps * 4 * 256; k += kThreads) (&s_hist[0][0][0])[k] = 0;
-    __syncthreads();
+    const int radix = 1 << a.sort_bits, np = a.sort_passes, per_warp = np * radix;
+    const uint32_t mask = uint32_t(radix - 1);
+    uint32_t* wh = s_hist + warp * per_warp;
     const uint32_t n = uint32_t(a.n_slots);  // slot counts stay below 2^31
-    const bool cams_in_top = a.depth_bits >= 24;
-    constexpr int kKeys = 16;  // keys per lane in flight: memory-level parallelism
-    const uint32_t stride = gridDim.x * uint32_t(kThreads * kKeys);
-    uint32_t cam_run = 0xFFFFFFFFu, cam_cnt = 0;  // runs of one camera (uniform in the warp)
-    uint32_t* top = s_hist[warp][3];
-    // the loop bound is warp-uniform (no lane term): the rounds below use full-warp ballots
-    for (uint32_t wbase = (blockIdx.x * kWarps + warp) * 32u * kKeys; wbase < n; wbase += stride) {
-        const uint32_t base = wbase + uint32_t(lane);
-        uint32_t keys[kKeys];
-        const uint32_t* kp = a.keys + base;
-        if (wbase + 32u * kKeys <= n) {
+    constexpr int kKeys = 8;                 // keys per lane in flight: memory-level parallelism
+    constexpr uint32_t kWarpSpan = 32u * kKeys;
+    const uint32_t per = ((n + gridDim.x - 1) / gridDim.x + kWarpSpan - 1) / kWarpSpan * kWarpSpan;
+    const uint32_t lo = min(n, blockIdx.x * per), hi = min(n, lo + per);
+    if (lo >= hi) return;
+    int c = upper_index(a.cam_slot_base, a.n_cams, uint64_t(lo));
+    while (true) {
+        while (c < a.n_cams && a.cam_slot_base[c + 1] <= lo) ++c;  // skip empty cameras
+        if (c >= a.n_cams || a.cam_slot_base[c] >= hi) break;
+        const uint32_t plo = max(lo, uint32_t(a.cam_slot_base[c]));
+        const uint32_t phi = min(hi, uint32_t(a.cam_slot_base[c + 1]));
+        for (int k = threadIdx.x; k < kWarps * per_warp; k += kThreads) s_hist[k] = 0;
+        __syncthreads();
+        for (uint32_t w0 = plo + uint32_t(warp) * kWarpSpan; w0 < phi; w0 += kWarps * kWarpSpan) {
+            uint32_t keys[kKeys];
+            const uint32_t* kp = a.keys + w0 + lane;
 #pragma unroll
-            for (int i = 0; i < kKeys; ++i) keys[i] = __ldcs(kp + i * 32);
-        } else {
+            for (int i = 0; i < kKeys; ++i)
+                keys[i] = w0 + lane + i * 32u < phi ? __ldcs(kp + i * 32) : kInvalidKey;
 #pragma unroll
-            for (int i = 0; i < kKeys; ++i) keys[i] = base + i * 32u < n ? __ldcs(kp + i * 32) : kInvalidKey;
-        }
-#pragma unroll
-        for (int i = 0; i < kKeys; ++i) {
-            const uint32_t key = keys[i];
-            const bool valid = key != kInvalidKey;
-#pragma unroll
-            for (int p = 0; p < 3; ++p)
-                if (valid) atomicAdd(&s_hist[warp][p][(key >> (8 * p)) & 255u], 1u);
-            const uint32_t d3 = key >> 24;
-            const uint32_t vmask = __ballot_sync(kFull, valid);
-            uint32_t rem = vmask;
-            while (rem) {  // the warp's own sub-histogram: the leader adds without atomics
-                const int leader = __ffs(rem) - 1;
-                const uint32_t v = __shfl_sync(kFull, d3, leader);
-                const uint32_t same = __ballot_sync(kFull, d3 == v) & rem;
-                if (lane == leader) top[v] += uint32_t(__popc(same));
-                rem &= ~same;
-            }
-            if (!cams_in_top) {
-                const uint32_t cam = key_camera(key, a.depth_bits);
-                rem = vmask;
-                while (rem) {  // one round per distinct camera in the group (usually one)
-                    const int leader = __ffs(rem) - 1;
-                    const uint32_t c = __shfl_sync(kFull, cam, leader);
-                    const uint32_t same = __ballot_sync(kFull, cam == c) & rem;
-                    if (c == cam_run) {
-                        cam_cnt += __popc(same);
-                    } else {
-                        if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
-                        cam_run = c;
-                        cam_cnt = __popc(same);
-                    }
-                    rem &= ~same;
-                }
+            for (int i = 0; i < kKeys; ++i) {
+                if (keys[i] == kInvalidKey) continue;
+                for (int p = 0; p < np; ++p)
+                    atomicAdd(&wh[p * radix + ((keys[i] >> (p * a.sort_bits)) & mask)], 1u);
             }
         }
-    }
-    if (lane == 0 && cam_cnt) atomicAdd(a.cam_visible + cam_run, cam_cnt);
-    __syncthreads();
-    for (int k = threadIdx.x; k < 4 * 256; k += kThreads) {
-        uint32_t s = 0;
+        __syncthreads();
+        uint32_t* g = a.hist + uint64_t(c) * per_warp;
+        uint32_t visible = 0;  // the piece's valid keys: sum of its first-pass digit counts
+        for (int k = threadIdx.x; k < per_warp; k += kThreads) {
+            uint32_t sum = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) s += (&s_hist[w][0][0])[k];
-        if (s) atomicAdd(a.hist + k, s);
+            for (int w = 0; w < kWarps; ++w) sum += s_hist[w * per_warp + k];
+            if (sum) atomicAdd(g + k, sum);
+            if (k < radix) visible += sum;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) visible += __shfl_xor_sync(kFull, visible, o);
+        if (lane == 0 && visible) atomicAdd(a.cam_visible + c, visible);
+        __syncthreads();
+        ++c;
     }
+    (void)lane;
+}
+
+size_t key_hist_smem(const BinArgs& a) {
+    return size_t(kWarps) * size_t(a.sort_passes) * (size_t(1) << a.sort_bits) * sizeof(uint32_t);
 }
 
 // Inclusive scan of one u64 per thread over the block (blockDim.x <= 1024) with warp shuffles:
@@ -247,43 +230,36 @@ __device__ unsigned long long block_scan_u64(unsigned long long v, unsigned long
 // ---- per-camera unit tables (one block) -----------------------------------------------------
 __global__ void __launch_bounds__(256) chunk_table_kernel(BinArgs a) {
     __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_carry[3];
+    __shared__ unsigned long long s_carry[4];
     const int tid = threadIdx.x;
-    if (tid < 3) s_carry[tid] = 0;
+    if (tid < 4) s_carry[tid] = 0;
     __syncthreads();
     const uint32_t R = uint32_t(a.chunk_records);
     for (int c0 = 0; c0 < a.n_cams; c0 += blockDim.x) {
         const int c = c0 + tid;
         uint32_t v = 0;
-        if (c < a.n_cams) {
-            if (a.depth_bits >= 24) {
-                // camera c owns the top digits [c << cshift, (c + 1) << cshift) (key_hist)
-                const int cshift = a.depth_bits - 24;
-                const uint32_t d0 = cshift >= 8 ? 0u : uint32_t(c) << cshift;
-                const uint32_t d1 = cshift >= 8 ? 256u : min(256u, uint32_t(c + 1) << cshift);
-                for (uint32_t d = d0; d < d1; ++d) v += a.hist[3 * 256 + d];
-                a.cam_visible[c] = v;
-            } else {
-                v = a.cam_visible[c];
-            }
-        }
+        if (c < a.n_cams) v = a.cam_visible[c];  // V_c, counted by key_hist
         const uint32_t k = (v + R - 1) / R;
+        const uint32_t ks = (v + uint32_t(kOnesweepTile) - 1) / uint32_t(kOnesweepTile);
         const uint32_t tc = c < a.n_cams ? a.cam_tile_base[c + 1] - a.cam_tile_base[c] : 0u;
         const unsigned long long m = (unsigned long long)k * tc;
-        unsigned long long tv, tk, tm;
+        unsigned long long tv, tk, tm, ts;
         const unsigned long long iv = block_scan_u64(v, s_w, &tv);
         const unsigned long long ik = block_scan_u64(k, s_w, &tk);
         const unsigned long long im = block_scan_u64(m, s_w, &tm);
+        const unsigned long long is = block_scan_u64(ks, s_w, &ts);
         if (c < a.n_cams) {
             a.cam_vbase[c] = uint32_t(s_carry[0] + iv - v);
             a.cam_chunk_base[c] = uint32_t(s_carry[1] + ik - k);
             a.cam_mbase[c] = s_carry[2] + im - m;
+            a.sort_chunk_base[c] = uint32_t(s_carry[3] + is - ks);
         }
         __syncthreads();
         if (tid == 0) {
             s_carry[0] += tv;
             s_carry[1] += tk;
             s_carry[2] += tm;
+            s_carry[3] += ts;
         }
         __syncthreads();
     }
@@ -291,6 +267,7 @@ __global__ void __launch_bounds__(256) chunk_table_kernel(BinArgs a) {
         a.cam_vbase[a.n_cams] = uint32_t(s_carry[0]);
         a.cam_chunk_base[a.n_cams] = uint32_t(s_carry[1]);
         a.cam_mbase[a.n_cams] = s_carry[2];
+        a.sort_chunk_base[a.n_cams] = uint32_t(s_carry[3]);
         *a.n_chunks = uint32_t(s_carry[1]);
         a.totals[0] = s_carry[0];  // V
     }
@@ -571,7 +548,9 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
 
 // ---- launchers ---------------------------------------------------------------------------------
 void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
-    key_hist_kernel<<<grid, kThreads, 0, s>>>(a);
+    const size_t smem = key_hist_smem(a);
+    cudaFuncSetAttribute(key_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    key_hist_kernel<<<grid, kThreads, smem, s>>>(a);
 }
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 256, 0, s>>>(a); }
 size_t bin_smem_bytes(const BinArgs& a) {

@@ -107,12 +107,14 @@ struct Plan {
     uint64_t out_floats = 0;
     uint32_t key_base = 0;
     int depth_bits = 32;
+    int sort_bits = 8;                 // depth digit bits of the segmented onesweep (8 or 9)
+    int sort_passes = 4;
+    std::vector<uint32_t> chunk_base0; // C + 1: first onesweep chunk of every camera, pass 1
 };
 
 // profiling events
 enum Ev { kEvStart = 0, kEvPre, kEvDepth, kEvBin, kEvScatter, kEvRaster, kNumEv };
 
-constexpr int kZeroHist = 0;       // [4][256] depth digit histograms
 constexpr int kZeroTickets = 1024; // 16 onesweep tickets
 constexpr int kZeroCams = 1040;    // per-camera visible counts
 
@@ -133,6 +135,8 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> rects;
     DevBuf<uint32_t> dk[2], dv[2];   // depth-sort ping-pong
     DevBuf<uint64_t> status;         // onesweep lookback words
+    DevBuf<uint32_t> sort_hist;      // [C][passes][radix] depth digit histograms (zeroed per frame)
+    DevBuf<uint32_t> sort_chunk_base;  // [C+1] onesweep chunks of passes >= 2
     int raster_rect_w = 8;           // GSIM_GPU_RASTER_RECT=16: 16x4 warp bands in K4 (default 8x8)
     int raster_exact_cull = 1;       // GSIM_GPU_RASTER_EXACT=0: bounding-box warp culling only
     int raster_batch = 128;          // GSIM_GPU_RASTER_BATCH=256: larger K4 batches, fewer CTAs/SM
@@ -142,6 +146,9 @@ struct gsim_gpu_context {
     // GSIM_GPU_INITIAL_PAIR_CAPACITY (tests): start from this capacity instead of 8 x slots,
     // to exercise the overflow -> regrow -> re-run path.
     uint64_t fixed_initial_capacity = 0;
+    // GSIM_GPU_GROUP_SLOTS (tests): (camera, primitive) slots per camera group; the kernels index
+    // slots in 32 bits, so the default is 2^31 - 1
+    uint64_t group_slots = (uint64_t(1) << 31) - 1;
     // zeroed per frame: histograms, tickets, per-camera visible counts
     DevBuf<uint32_t> zero_block;
     DevBuf<unsigned long long> counts;  // [0] V, [1] P, [2] consumed
@@ -155,6 +162,7 @@ struct gsim_gpu_context {
     uint64_t* cam_slot_base = nullptr;
     uint32_t* cam_tile_base = nullptr;
     int* cam_tiles_x = nullptr;
+    uint32_t* cam_chunk_base0 = nullptr;
     DevSegment* segs = nullptr;
     SegEntry* entries = nullptr;
     int32_t* seg_track = nullptr;
@@ -339,6 +347,74 @@ void finish_cameras(Plan& p, const gsim_camera* cameras, uint64_t n_cams) {
     p.out_floats = out_off;
 }
 
+// Digit width and pass count of the segmented depth sort (sort.cu): 8-bit digits (27-bit keys of
+// near/far 0.05/100: 4 passes). 9-bit digits save a pass there but measured slower per pass
+// (config 1, ncu: 67/61/100 us for 3 x 9-bit vs 48/46/44/68 us for 4 x 8-bit: twice the
+// digit runs per chunk, twice the look-back words); GSIM_GPU_SORT_BITS=9 selects them.
+// Plus the pass-1 chunk table (chunks never straddle cameras).
+void finish_sort(Plan& p) {
+    static const int forced = [] {  // GSIM_GPU_SORT_BITS=8|9: digit width (measurements)
+        const char* e = std::getenv("GSIM_GPU_SORT_BITS");
+        const int v = e ? std::atoi(e) : 0;
+        return v == 8 || v == 9 ? v : 0;
+    }();
+    const int b = std::max(1, p.depth_bits);
+    const int p8 = (b + 7) / 8, p9 = (b + 8) / 9;
+    p.sort_bits = forced ? forced : 8;
+    p.sort_passes = p.sort_bits == 9 ? p9 : p8;
+    const size_t C = p.cams.size();
+    p.chunk_base0.assign(C + 1, 0);
+    for (size_t c = 0; c < C; ++c) {
+        const uint64_t sc = p.slot_base[c + 1] - p.slot_base[c];
+        p.chunk_base0[c + 1] = p.chunk_base0[c] + uint32_t((sc + kOnesweepTile - 1) / kOnesweepTile);
+    }
+}
+
+struct PaintedRange { uint64_t b, e; int64_t owner; };
+
+// Node painting like PoseTable (raster.cpp:47-62): maximal primitive ranges with the index of the
+// node that owns them (later nodes win), -1 where no node does.
+std::vector<PaintedRange> paint_nodes(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes) {
+    std::vector<uint64_t> pts{0, n_prims};
+    for (uint64_t k = 0; k < n_nodes; ++k)
+        if (nodes[k].begin < nodes[k].end) {
+            pts.push_back(nodes[k].begin);
+            pts.push_back(nodes[k].end);
+        }
+    std::sort(pts.begin(), pts.end());
+    pts.erase(std::unique(pts.begin(), pts.end()), pts.end());
+    std::vector<PaintedRange> ivs;
+    for (size_t k = 0; k + 1 < pts.size(); ++k)
+        if (pts[k] < pts[k + 1]) ivs.push_back({pts[k], pts[k + 1], -1});
+    for (uint64_t k = 0; k < n_nodes; ++k) {
+        if (!(nodes[k].begin < nodes[k].end)) continue;
+        auto it = std::lower_bound(ivs.begin(), ivs.end(), nodes[k].begin,
+                                   [](const PaintedRange& iv, uint64_t v) { return iv.b < v; });
+        for (; it != ivs.end() && it->b < nodes[k].end; ++it) it->owner = int64_t(k);
+    }
+    std::vector<PaintedRange> merged;
+    for (const auto& iv : ivs) {
+        if (!merged.empty() && merged.back().owner == iv.owner && merged.back().e == iv.b)
+            merged.back().e = iv.e;
+        else
+            merged.push_back(iv);
+    }
+    if (merged.empty()) merged.push_back({0, 0, -1});
+    return merged;
+}
+
+// (camera, primitive) slots of every camera: the primitives of nodes of its env (or of no env).
+std::vector<uint64_t> camera_slots(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
+                                   const gsim_camera* cameras, uint64_t n_cams) {
+    const std::vector<PaintedRange> merged = paint_nodes(n_prims, nodes, n_nodes);
+    std::vector<uint64_t> out(n_cams, 0);
+    for (const auto& iv : merged)
+        for (uint64_t c = 0; c < n_cams; ++c)
+            if (iv.owner < 0 || nodes[iv.owner].env < 0 || nodes[iv.owner].env == cameras[c].env)
+                out[c] += iv.e - iv.b;
+    return out;
+}
+
 // Paint node ranges like PoseTable (raster.cpp:47-62) into maximal segments and assign each
 // (camera, primitive) a record slot; cameras' slot lists keep primitive order.
 Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
@@ -349,34 +425,8 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         if (nodes[k].end > n_prims)
             throw ValidationError{"node " + std::to_string(k) + " range exceeds field size"};
 
-    std::vector<uint64_t> pts{0, n_prims};
-    for (uint64_t k = 0; k < n_nodes; ++k)
-        if (nodes[k].begin < nodes[k].end) {
-            pts.push_back(nodes[k].begin);
-            pts.push_back(nodes[k].end);
-        }
-    std::sort(pts.begin(), pts.end());
-    pts.erase(std::unique(pts.begin(), pts.end()), pts.end());
-    struct Iv { uint64_t b, e; int64_t owner; };
-    std::vector<Iv> ivs;
-    for (size_t k = 0; k + 1 < pts.size(); ++k)
-        if (pts[k] < pts[k + 1]) ivs.push_back({pts[k], pts[k + 1], -1});
-    for (uint64_t k = 0; k < n_nodes; ++k) {
-        if (!(nodes[k].begin < nodes[k].end)) continue;
-        auto it = std::lower_bound(ivs.begin(), ivs.end(), nodes[k].begin,
-                                   [](const Iv& iv, uint64_t v) { return iv.b < v; });
-        for (; it != ivs.end() && it->b < nodes[k].end; ++it) it->owner = int64_t(k);
-    }
-    std::vector<Iv> merged;
-    for (const auto& iv : ivs) {
-        if (!merged.empty() && merged.back().owner == iv.owner && merged.back().e == iv.b)
-            merged.back().e = iv.e;
-        else
-            merged.push_back(iv);
-    }
-    if (merged.empty()) merged.push_back({0, 0, -1});
-
-    auto visible = [&](const Iv& iv, uint64_t c) {
+    const std::vector<PaintedRange> merged = paint_nodes(n_prims, nodes, n_nodes);
+    auto visible = [&](const PaintedRange& iv, uint64_t c) {
         if (iv.owner < 0) return true;
         const int env = nodes[iv.owner].env;
         return env < 0 || env == cameras[c].env;
@@ -417,9 +467,9 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         p.seg_owner.push_back(int32_t(iv.owner));
     }
     finish_cameras(p, cameras, n_cams);
-    // Record key = camera index above the float32 depth bits rebased to [near_min, far_max]:
-    // near < z < far implies RN(near) <= RN(z) <= RN(far), and positive floats order like
-    // their bit patterns, so the rebased key keeps the reference's depth_sort_key order.
+    // Record key = float32 depth bits rebased to [near_min, far_max]: near < z < far implies
+    // RN(near) <= RN(z) <= RN(far), and positive floats order like their bit patterns, so the
+    // rebased key keeps the reference's depth_sort_key order. The camera is the sort's segment.
     if (n_cams) {
         double near_min = cameras[0].near_plane, far_max = cameras[0].far_plane;
         for (uint64_t c = 1; c < n_cams; ++c) {
@@ -429,12 +479,8 @@ Plan build_plan(uint64_t n_prims, const gsim_node* nodes, uint64_t n_nodes,
         p.key_base = float_bits(near_min);
         const uint64_t span = uint64_t(float_bits(far_max)) - p.key_base;
         p.depth_bits = int(ceil_log2_bits(span + 2));  // keeps kInvalidKey unreachable
-        const int cam_bits = int(ceil_log2_bits(n_cams));
-        if (p.depth_bits + cam_bits > 32)
-            throw ValidationError{"batch of " + std::to_string(n_cams) + " cameras with near/far span " +
-                                  "needs " + std::to_string(p.depth_bits + cam_bits) +
-                                  " key bits (> 32); split the batch"};
     }
+    finish_sort(p);
     return p;
 }
 
@@ -450,6 +496,7 @@ Plan build_splat_plan(uint64_t n, const gsim_camera& cam) {
     finish_cameras(p, &cam, 1);
     p.key_base = 0;
     p.depth_bits = 32;
+    finish_sort(p);
     return p;
 }
 
@@ -471,6 +518,7 @@ void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
     const size_t o_sb = append_bytes(blob, p.slot_base);
     const size_t o_tb = append_bytes(blob, p.tile_base);
     const size_t o_tx = append_bytes(blob, p.tiles_x);
+    const size_t o_cb0 = append_bytes(blob, p.chunk_base0);
     const size_t o_seg = append_bytes(blob, p.segs);
     const size_t o_ent = append_bytes(blob, p.entries);
     const size_t o_st = append_bytes(blob, p.seg_track);
@@ -490,6 +538,7 @@ void upload_plan(gsim_gpu_context* ctx, const Plan& p) {
     ctx->cam_slot_base = reinterpret_cast<uint64_t*>(d + o_sb);
     ctx->cam_tile_base = reinterpret_cast<uint32_t*>(d + o_tb);
     ctx->cam_tiles_x = reinterpret_cast<int*>(d + o_tx);
+    ctx->cam_chunk_base0 = reinterpret_cast<uint32_t*>(d + o_cb0);
     ctx->segs = reinterpret_cast<DevSegment*>(d + o_seg);
     ctx->entries = reinterpret_cast<SegEntry*>(d + o_ent);
     ctx->seg_track = p.seg_track.empty() ? nullptr : reinterpret_cast<int32_t*>(d + o_st);
@@ -554,7 +603,9 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     if (ctx->fixed_initial_capacity == 0 && ctx->pair_capacity < 8 * S + (1u << 20))
         ctx->pair_capacity = 8 * S + (1u << 20);
     ctx->vals.reserve(std::max<uint64_t>(ctx->pair_capacity, 1));
-    const uint64_t words = (S + kOnesweepTile - 1) / kOnesweepTile * 256;
+    const uint64_t words = ((S + kOnesweepTile - 1) / kOnesweepTile + C) * (uint64_t(1) << p.sort_bits);
+    ctx->sort_hist.reserve(C * p.sort_passes * (uint64_t(1) << p.sort_bits));
+    ctx->sort_chunk_base.reserve(C + 1);
     if (words > ctx->status.cap) {
         ctx->status.reserve(words);
         GSIM_CK(cudaMemsetAsync(ctx->status.ptr, 0, ctx->status.cap * sizeof(uint64_t), ctx->stream));
@@ -581,14 +632,18 @@ float smallest_float_geq(double x) {
     return f;
 }
 
-BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sorted_slots) {
+BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p) {
     BinArgs b{};
     b.keys = ctx->keys.ptr;
     b.n_slots = p.slots;
-    b.depth_bits = p.depth_bits;
+    b.cam_slot_base = ctx->cam_slot_base;
+    b.sort_bits = p.sort_bits;
+    b.sort_passes = p.sort_passes;
     b.n_cams = int(p.cams.size());
-    b.sorted_slots = sorted_slots;
-    b.sorted_rects = ctx->dk[1].ptr;  // written by the last depth pass
+    // the last depth pass writes the slots into dv[o] and gathers the rects into dk[o]
+    const int last_o = (p.sort_passes - 1) & 1;
+    b.sorted_slots = ctx->dv[last_o].ptr;
+    b.sorted_rects = ctx->dk[last_o].ptr;
     b.cam_tile_base = ctx->cam_tile_base;
     b.cam_tiles_x = ctx->cam_tiles_x;
     b.cam_visible = ctx->zero_block.ptr + kZeroCams;
@@ -602,7 +657,8 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p, const uint32_t* sort
     b.counts = ctx->count_matrix.ptr;
     b.tile_count = ctx->tile_count.ptr;
     b.tile_rel = ctx->tile_rel.ptr;
-    b.hist = ctx->zero_block.ptr + kZeroHist;
+    b.hist = ctx->sort_hist.ptr;
+    b.sort_chunk_base = ctx->sort_chunk_base.ptr;
     b.totals = ctx->counts.ptr;
     b.vals_out = ctx->vals.ptr;
     b.capacity = ctx->pair_capacity;
@@ -680,20 +736,22 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     const uint64_t S = p.slots;
     const int n_sms = ctx->num_sms;
 
-    // key histograms + per-camera counts, then the chunk table (needs only the counts)
-    BinArgs b = make_bin_args(ctx, p, ctx->dv[1].ptr);
-    launch_key_hist(b, n_sms * 4, s);
-    b.hist = ctx->zero_block.ptr + kZeroHist;
+    // digit histograms per (camera, pass), then the chunk tables (need only the counts)
+    BinArgs b = make_bin_args(ctx, p);
+    launch_key_hist(b, n_sms * 2, s);
     check_launch();
     launch_chunk_table(b, s);
     check_launch();
     launches += 2;
 
-    // 4 onesweep passes over (camera | depth) keys; pass 1 compacts the culled slots away.
+    // segmented onesweep passes over the depth keys; pass 1 compacts the culled slots away
+    const int passes = p.sort_passes, radix = 1 << p.sort_bits;
     OnesweepArgs oa{};
-    oa.n_dev = ctx->counts.ptr + 0;
     oa.status = ctx->status.ptr;
-    uint64_t dgrid = (S + kOnesweepTile - 1) / kOnesweepTile;
+    oa.n_cams = int(p.cams.size());
+    oa.vbase = ctx->cam_vbase.ptr;
+    oa.hist_stride = uint64_t(passes) * radix;
+    uint64_t dgrid = (S + kOnesweepTile - 1) / kOnesweepTile + p.cams.size();
     static const int sort_ctas = [] {
         const char* e = std::getenv("GSIM_GPU_SORT_CTAS");  // resident onesweep CTAs per SM
         const int v = e ? std::atoi(e) : 3;
@@ -702,21 +760,25 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     dgrid = std::max<uint64_t>(1, std::min<uint64_t>(dgrid, uint64_t(n_sms) * sort_ctas));
     const uint32_t* kin = ctx->keys.ptr;
     const uint32_t* vin = nullptr;
-    for (int pass = 0; pass < 4; ++pass) {
+    for (int pass = 0; pass < passes; ++pass) {
         const int o = pass & 1;
+        const bool last = pass == passes - 1;
         oa.keys_in = kin;
         oa.vals_in = vin;
         oa.keys_out = ctx->dk[o].ptr;
         oa.vals_out = ctx->dv[o].ptr;
-        oa.n_host = S;
-        oa.hist = b.hist + 256 * pass;
+        oa.seg_base64 = ctx->cam_slot_base;
+        oa.seg_base32 = ctx->cam_vbase.ptr;
+        oa.chunk_base = pass == 0 ? ctx->cam_chunk_base0 : ctx->sort_chunk_base.ptr;
+        oa.hist = ctx->sort_hist.ptr + uint64_t(pass) * radix;
         oa.ticket = ctx->zero_block.ptr + kZeroTickets + pass;
         oa.epoch = ctx->next_epoch();
-        oa.shift = 8 * pass;
-        // the last pass also gathers the tile rects into depth order (into dk[1], free by then)
-        oa.rects_in = pass == 3 ? ctx->rects.ptr : nullptr;
-        oa.rects_out = pass == 3 ? ctx->dk[1].ptr : nullptr;
-        launch_onesweep(oa, pass == 0, pass < 3, int(dgrid), s);
+        oa.shift = p.sort_bits * pass;
+        // the last pass writes no keys: it gathers the tile rects into depth order instead,
+        // into its own (unused) key output buffer
+        oa.rects_in = last ? ctx->rects.ptr : nullptr;
+        oa.rects_out = last ? ctx->dk[o].ptr : nullptr;
+        launch_onesweep(oa, p.sort_bits, pass == 0, !last, int(dgrid), s);
         check_launch();
         ++launches;
         kin = ctx->dk[o].ptr;
@@ -780,12 +842,15 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         GSIM_CK(cudaMemsetAsync(ctx->counts.ptr + 2, 0, sizeof(unsigned long long), s));
     }
     if (ctx->stats.pairs > ctx->pair_capacity) throw CudaError{"pair buffer overflow after regrowth"};
-    ctx->stats.depth_passes = 4;
+    ctx->stats.depth_passes = uint32_t(p.sort_passes);
 }
 
 void begin_frame(gsim_gpu_context* ctx, const Plan& p) {
-    GSIM_CK(cudaMemsetAsync(ctx->zero_block.ptr, 0, (kZeroCams + std::max<size_t>(p.cams.size(), 1)) * sizeof(uint32_t),
+    GSIM_CK(cudaMemsetAsync(ctx->zero_block.ptr + kZeroTickets, 0,
+                            (kZeroCams - kZeroTickets + std::max<size_t>(p.cams.size(), 1)) * sizeof(uint32_t),
                             ctx->stream));
+    const size_t hist_words = std::max<size_t>(p.cams.size(), 1) * size_t(p.sort_passes) << p.sort_bits;
+    GSIM_CK(cudaMemsetAsync(ctx->sort_hist.ptr, 0, hist_words * sizeof(uint32_t), ctx->stream));
     GSIM_CK(cudaMemsetAsync(ctx->counts.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
 }
 
@@ -861,11 +926,10 @@ void render_frame(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim
 
 bool check_pending(gsim_gpu_context* ctx);
 
-// A camera batch is rendered in groups whose (camera | depth) record keys fit 32 bits and whose
-// (camera, primitive) slots stay below 2^31: e.g. BASELINE config 2 (320 cameras, near/far
-// 0.05/100 -> 27 depth bits) runs as 10 groups of 32 cameras. Every group re-reads the shared
-// background once (a few microseconds per camera); outputs keep the batch's camera order.
-// Returns the float offset of every camera's block in the output.
+// A camera batch is rendered in one launch sequence whenever its (camera, primitive) slots stay
+// below 2^31 (the kernels index slots in 32 bits): BASELINE config 2 (320 cameras x 1.08M slots)
+// is one group. Larger batches are split into consecutive camera groups by slot count; outputs
+// keep the batch's camera order. Returns the float offset of every camera's block in the output.
 std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
                                      const gsim_node* nodes, uint64_t n_nodes,
                                      const gsim_camera* cameras, uint64_t n_cams,
@@ -881,26 +945,32 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
         ctx->out.reserve(std::max<uint64_t>(offsets[n_cams], 1));
         out = ctx->out.ptr;
     }
-    uint64_t group = n_cams ? n_cams : 1;
+    for (uint64_t k = 0; k < n_nodes; ++k)
+        if (nodes[k].end > scene->f.n)
+            throw ValidationError{"node " + std::to_string(k) + " range exceeds field size"};
+    // group boundaries: consecutive cameras while their slots fit the group budget
+    std::vector<uint64_t> group_begin{0};
     if (n_cams) {
-        double near_min = cameras[0].near_plane, far_max = cameras[0].far_plane;
-        for (uint64_t c = 1; c < n_cams; ++c) {
-            near_min = std::min(near_min, cameras[c].near_plane);
-            far_max = std::max(far_max, cameras[c].far_plane);
+        const std::vector<uint64_t> cs = camera_slots(scene->f.n, nodes, n_nodes, cameras, n_cams);
+        uint64_t acc = 0;
+        for (uint64_t c = 0; c < n_cams; ++c) {
+            if (c > group_begin.back() && acc + cs[c] > ctx->group_slots) {
+                group_begin.push_back(c);
+                acc = 0;
+            }
+            acc += cs[c];
         }
-        const uint64_t span = uint64_t(float_bits(far_max)) - float_bits(near_min);
-        const int depth_bits = int(ceil_log2_bits(span + 2));
-        group = std::min<uint64_t>(group, uint64_t(1) << (32 - std::min(depth_bits, 32)));
-        const uint64_t n = std::max<uint64_t>(scene->f.n, 1);
-        group = std::max<uint64_t>(1, std::min<uint64_t>(group, (uint64_t(1) << 31) / n));
     }
+    group_begin.push_back(n_cams);
     uint64_t launches = 0, h2d = 0;
     gsim_target* const targets = ctx->frame_outs;  // host targets of the whole batch, if any
     uint8_t* const enc_host = ctx->frame_enc_host;  // render_encoded host bytes, if any
     ctx->frame_outs = nullptr;
     ctx->frame_enc_host = nullptr;
-    for (uint64_t c0 = 0; c0 < n_cams || (n_cams == 0 && c0 == 0); c0 += group) {
-        const uint64_t g = n_cams ? std::min(group, n_cams - c0) : 0;
+    const size_t n_groups = group_begin.size() - 1;
+    for (size_t gi = 0; gi < n_groups; ++gi) {
+        const uint64_t c0 = group_begin[gi];
+        const uint64_t g = group_begin[gi + 1] - c0;
         // a re-run group had its copies queued already: the caller copies everything again
         if (c0 > 0 && !wait_for_count && check_pending(ctx)) ctx->copies_stale = true;
         Plan plan;
@@ -916,11 +986,10 @@ std::vector<uint64_t> render_cameras(gsim_gpu_context* ctx, const gsim_gpu_scene
         launches += ctx->stats.launches;
         h2d += ctx->stats.h2d_bytes;
         ctx->last_plan = std::move(plan);
-        if (n_cams == 0) break;
     }
     ctx->stats.launches = launches;
     ctx->stats.h2d_bytes = h2d;
-    ctx->stats.groups = uint32_t((n_cams + group - 1) / std::max<uint64_t>(group, 1));
+    ctx->stats.groups = uint32_t(n_groups);
     ctx->stats.last_group_cameras = uint32_t(ctx->last_plan.cams.size());
     return offsets;
 }
@@ -942,7 +1011,7 @@ bool check_pending(gsim_gpu_context* ctx) {
     ctx->pair_capacity = rb[1] + rb[1] / 4 + (1u << 20);
     ctx->vals.reserve(ctx->pair_capacity);
     GSIM_CK(cudaMemsetAsync(ctx->counts.ptr + 2, 0, sizeof(unsigned long long), ctx->stream));
-    BinArgs b = make_bin_args(ctx, ctx->last_plan, ctx->dv[1].ptr);
+    BinArgs b = make_bin_args(ctx, ctx->last_plan);
     launch_bin_scatter(b, ctx->pending_grid, ctx->stream);
     check_launch();
     const EncodeParams enc = ctx->frame_enc;
@@ -1525,6 +1594,10 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         if (const char* e = std::getenv("GSIM_GPU_RASTER_EXACT")) ctx->raster_exact_cull = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
         if (const char* e = std::getenv("GSIM_GPU_OVERLAP_COPIES")) ctx->overlap_copies = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GSIM_GPU_GROUP_SLOTS")) {
+            const uint64_t v = std::strtoull(e, nullptr, 10);
+            if (v > 0 && v < ctx->group_slots) ctx->group_slots = v;
+        }
         if (const char* e = std::getenv("GSIM_GPU_INITIAL_PAIR_CAPACITY")) {
             ctx->fixed_initial_capacity = std::strtoull(e, nullptr, 10);
             ctx->pair_capacity = ctx->fixed_initial_capacity;

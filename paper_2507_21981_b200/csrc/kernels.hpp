@@ -20,7 +20,7 @@ struct PreprocessArgs {
     DevField field;
     const DevSegment* segs;
     int n_segs;
-    int depth_bits;                  // camera index sits above this many key bits
+    int depth_bits;                  // bits of the rebased depth key
     const SegEntry* entries;
     const DevCamera* cams;
     Record* records;                 // [slots]
@@ -41,17 +41,25 @@ struct SplatArgs {
     uint32_t* keys;
 };
 
-// One onesweep LSD pass over (u32 key, u32 value) pairs, 8-bit digit at `shift`.
+// One segmented onesweep LSD pass over (u32 key, u32 value) pairs, 8- or 9-bit digit at
+// `shift` (sort.cu). Segment c = camera c's items: pass 1 reads slots [seg_base64[c],
+// seg_base64[c+1]) (culled slots carry kInvalidKey and are dropped), later passes read
+// [seg_base32[c], seg_base32[c+1]) of the compacted records; every pass writes camera c's
+// records to [vbase[c], vbase[c+1]). Chunks of kOnesweepTile items never straddle cameras:
+// camera c owns chunks [chunk_base[c], chunk_base[c+1]).
 struct OnesweepArgs {
     const uint32_t* keys_in;
-    const uint32_t* vals_in;         // nullptr on the first depth pass: value = input index
+    const uint32_t* vals_in;         // nullptr on the first pass: value = input index (slot)
     uint32_t* keys_out;
     uint32_t* vals_out;
-    const unsigned long long* n_dev; // element count on device (ignored when n_host used)
-    uint64_t n_host;
-    uint64_t capacity;               // n_dev is clamped to this (0 = no clamp)
-    const uint32_t* hist;            // [256] digit histogram of this pass
-    uint64_t* status;                // decoupled-lookback words, [chunks][256]
+    const uint64_t* seg_base64;      // pass 1: camera slot bases [C+1]
+    const uint32_t* seg_base32;      // later passes: camera record bases [C+1] (= vbase)
+    const uint32_t* chunk_base;      // [C+1] first chunk of every camera; [C] = chunk count
+    const uint32_t* vbase;           // [C+1] output base of every camera
+    const uint32_t* hist;            // digit histogram of this pass for camera 0 ...
+    uint64_t hist_stride;            // ... and the stride between cameras (passes * radix)
+    int n_cams;
+    uint64_t* status;                // decoupled-lookback words, [chunks][radix]
     uint32_t* ticket;                // zeroed per pass
     uint32_t epoch;
     int shift;
@@ -61,9 +69,11 @@ struct OnesweepArgs {
 
 // Tile binning of the camera-major depth-sorted records (bin.cu).
 struct BinArgs {
-    const uint32_t* keys;            // [S] packed keys (key_hist)
+    const uint32_t* keys;            // [S] rebased depth keys (key_hist)
     uint64_t n_slots;
-    int depth_bits;
+    const uint64_t* cam_slot_base;   // [C+1] slot segment of every camera
+    int sort_bits;                   // depth digit bits (8 or 9)
+    int sort_passes;                 // onesweep passes
     int n_cams;
     const uint32_t* sorted_slots;    // [V] record slots, camera-major depth order
     const uint32_t* sorted_rects;    // [V] tile rects of sorted_slots (gathered by the sort)
@@ -80,7 +90,8 @@ struct BinArgs {
     uint32_t* counts;                // count matrix / column prefixes
     uint32_t* tile_count;            // [tiles]
     uint32_t* tile_rel;              // [tiles] first pair of the tile within its camera
-    uint32_t* hist;                  // [4][256] depth digit histograms (zeroed per frame)
+    uint32_t* hist;                  // [C][passes][radix] digit histograms (zeroed per frame)
+    uint32_t* sort_chunk_base;       // [C+1] onesweep chunks of passes >= 2 per camera (out)
     unsigned long long* totals;      // [0] V, [1] P
     uint32_t* vals_out;              // [capacity] record slot of every pair, final order
     uint64_t capacity;
@@ -155,7 +166,7 @@ void launch_pose(const DevField& f, uint64_t begin, uint64_t end, const gsim_rig
                  int grid_cap, cudaStream_t stream);
 void launch_preprocess(const PreprocessArgs& a, bool full, int n_sms, cudaStream_t stream);
 void launch_splats_to_records(const SplatArgs& a, int grid_cap, cudaStream_t stream);
-void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
+void launch_onesweep(const OnesweepArgs& a, int bits, bool first, bool write_keys, int grid,
                      cudaStream_t stream);
 void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s);
 void launch_chunk_table(const BinArgs& a, cudaStream_t s);

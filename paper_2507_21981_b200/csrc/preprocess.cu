@@ -299,10 +299,10 @@ __global__ void __launch_bounds__(NT, MINB) preprocess_kernel(PreprocessArgs arg
                                              __double2float_rn(opacity), rgb[0], rgb[1], rgb[2]);
             const uint32_t rec_rect = pack_rect(tx0, ty0, tx1, ty1);
             args.rects[slot] = rec_rect;
-            // Camera-major sort key: camera index above the float32 depth bits
-            // (depth_sort_key, raster.hpp:45-47) rebased to the batch's [near, far) range;
-            // positive floats order like their bit patterns, so the order is unchanged.
-            args.keys[slot] = (ent.cam << args.depth_bits) | (__float_as_uint(fz) - args.key_base);
+            // Sort key: the float32 depth bits (depth_sort_key, raster.hpp:45-47) rebased to the
+            // batch's [near, far] range; positive floats order like their bit patterns, so the
+            // order is unchanged. The camera is the sort's segment (sort.cu), not a key digit.
+            args.keys[slot] = __float_as_uint(fz) - args.key_base;
         }
     }
 }

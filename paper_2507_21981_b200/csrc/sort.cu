@@ -1,19 +1,23 @@
-// sort.cu — K3a: onesweep LSD radix sort of the (camera | depth) record keys.
+// sort.cu — K3a: segmented onesweep LSD radix sort of the record depth keys, per camera.
 //
 // The reference bins splats into (tile << 32 | float32 depth bits) keys and std::sorts
-// (key, splat index) pairs (raster.cpp:174-202). We produce the same order with an LSD radix
-// sort whose depth digits are sorted BEFORE duplication, on the V visible records instead of
-// the P ~ 3.5 V pairs:
-//   pass 1..4  onesweep over the 32-bit depth key of every (camera, primitive) slot; pass 1
-//              also compacts (drops culled slots). Input order = (camera, primitive) order,
-//              so the stable sort leaves ties in primitive order, as the reference does.
-//   The key carries the camera index above the rebased depth bits, so the result is in
-//   (camera, depth, primitive) order; bin.cu then places every (tile, record) pair directly
-//   at its final position, which gives the reference's per-camera pair order without
-//   sorting the P ~ 3.5 V pairs.
-// Every pass is single-sweep: chunks are claimed through an atomic ticket (so predecessors
-// are always resident) and per-digit prefixes come from decoupled lookback over epoch-tagged
-// status words (no clearing between passes).
+// (key, splat index) pairs per camera (raster.cpp:174-202). We produce the same order with an LSD
+// radix sort whose depth digits are sorted BEFORE duplication, on the V visible records instead
+// of the P ~ 3.5 V pairs, and place the pairs afterwards (bin.cu):
+//   * Every camera's records are a contiguous SEGMENT (pass 1: its slots, camera-major in
+//     primitive order; later passes: its compacted records). Chunks of 4096 items never straddle
+//     a camera, digit histograms are per (camera, pass), and the decoupled look-back of a chunk
+//     stops at its camera's first chunk. The camera index therefore never enters the key: a
+//     batch of any number of cameras (BASELINE config 2: 320) sorts in one launch per pass, and
+//     the key is only the float32 depth bits rebased to the batch's [near, far] range
+//     (depth_sort_key, raster.hpp:45-47): 27 bits for near/far 0.05/100 -> 3 passes of 9-bit
+//     digits (4 of 8 bits when the span needs 28-32 bits).
+//   * Pass 1 also compacts (drops culled slots). Input order = primitive order within a camera,
+//     so the stable sort leaves ties in primitive order, as the reference's pair sort does.
+//   * Every pass is single-sweep: chunks are claimed through an atomic ticket (so predecessors
+//     are always resident) and per-digit prefixes come from decoupled look-back over
+//     epoch-tagged status words (no clearing between passes).
+//   * The last pass also gathers every record's tile rect into depth order for the binning.
 #include <cstdint>
 
 #include "common.cuh"
@@ -26,7 +30,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = kOnesweepTile / kThreads;  // 16
-constexpr int kRadix = 256;
 constexpr uint64_t kCountMask = (1ull << 40) - 1;
 
 // Exclusive scan of one u32 per thread over a 256-thread block. Returns the exclusive
@@ -54,7 +57,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     return warp_prefix + incl - v;
 }
 
-// Spin until chunk j's word for `lane_index` is published in this epoch; return it.
+// Spin until chunk j's word for a digit is published in this epoch; return it.
 __device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoch) {
     while (true) {
         const uint64_t s = ld_volatile_u64(p);
@@ -66,19 +69,23 @@ __device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoc
 }  // namespace
 
 // Digit peers (the lanes sharing a digit) come from one shared-memory atomicOr per item into a
-// per-warp digit bitmap (two buffers alternate, so clearing item i's bits never races item
-// i+1's); shared atomics cost ~3 cycles per warp instruction without heavy same-address
-// contention (tools/microbench.cu), and even the top digit (camera and exponent bits, ~3 lanes
-// per value after the low passes) measured cheaper this way than with 8 ballots. The bitmaps
-// live in s_keys (ranking is done before the chunk is staged there) and are cleared at the start
-// of every chunk.
-template <bool kFirst, bool kWriteKeys>
+// per-warp digit bitmap; shared atomics cost ~3 cycles per warp instruction without heavy
+// same-address contention (tools/microbench.cu). The bitmaps have their own shared memory: they
+// are cleared once per CTA and every item's leader clears its word again (a warp barrier orders
+// that clear before the next item's atomicOr), so chunks never re-clear them.
+// Thread t owns digits t*kDpt .. t*kDpt + kDpt - 1 for the per-digit scans and the look-back.
+template <int kBits, bool kFirst, bool kWriteKeys>
 __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
-    __shared__ uint32_t s_keys[kOnesweepTile];
-    static_assert(2 * kWarps * kRadix <= kOnesweepTile, "peer bitmaps alias s_keys");
-    auto s_peer = reinterpret_cast<uint32_t(*)[kWarps][kRadix]>(s_keys);
-    __shared__ uint32_t s_vals[kOnesweepTile];
-    __shared__ uint32_t s_warp_hist[kWarps][kRadix];
+    constexpr int kRadix = 1 << kBits;
+    constexpr int kDpt = kRadix / kThreads;  // 1 (8-bit digits) or 2 (9-bit)
+    constexpr uint32_t kMask = kRadix - 1;
+    // dynamic: [keys | values of the staged chunk][per-warp digit counts][per-warp digit
+    // bitmaps] (launch_one)
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    uint32_t* s_keys = s_dyn;
+    uint32_t* s_vals = s_dyn + kOnesweepTile;
+    auto s_warp_hist = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 2 * kOnesweepTile);
+    auto s_peer = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 2 * kOnesweepTile + kWarps * kRadix);
     __shared__ uint32_t s_bstart[kRadix];
     __shared__ uint32_t s_dest[kRadix];
     __shared__ uint32_t s_tmp[kWarps];
@@ -86,27 +93,50 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
     __shared__ uint32_t s_total;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint64_t n = kFirst ? a.n_host : uint64_t(*a.n_dev);
-    if (a.capacity && n > a.capacity) n = a.capacity;
-    const uint64_t chunks = (n + kOnesweepTile - 1) / kOnesweepTile;
-
-    // Global start of each digit: exclusive scan of the pass histogram.
-    uint32_t hist_total;
-    const uint32_t gbase = block_exclusive_scan(a.hist[tid], s_tmp, &hist_total);
+    const uint32_t n_chunks = a.chunk_base[a.n_cams];
+    const uint32_t* seg32 = a.seg_base32;
+    int cam_cached = -1;
+    uint32_t gbase[kDpt];  // output position of each of this thread's digits, this camera
+    for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_peer[0][0])[k] = 0;
 
     while (true) {
         if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
         for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_warp_hist[0][0])[k] = 0;
-        for (int k = tid; k < 2 * kWarps * kRadix; k += kThreads) s_keys[k] = 0;
         __syncthreads();
         const uint32_t t = s_ticket;
-        if (t >= chunks) break;
-        // 32-bit indices: slot counts stay below 2^31 (host.cu splits larger batches)
-        const uint32_t base = t * uint32_t(kOnesweepTile) + uint32_t(warp) * (kItems * 32) + uint32_t(lane);
+        if (t >= n_chunks) break;
+        const int cam = upper_index(a.chunk_base, a.n_cams, t);
+        const uint32_t first_chunk = a.chunk_base[cam];
+        const uint64_t sb = kFirst ? a.seg_base64[cam] : uint64_t(seg32[cam]);
+        const uint64_t se = kFirst ? a.seg_base64[cam + 1] : uint64_t(seg32[cam + 1]);
+        const uint32_t cbegin = uint32_t(sb) + (t - first_chunk) * uint32_t(kOnesweepTile);
+        const uint64_t cend64 = uint64_t(cbegin) + kOnesweepTile;
+        const uint32_t cend = uint32_t(cend64 < se ? cend64 : se);
+        if (cam != cam_cached) {
+            // global start of each digit in this camera: camera's output base + exclusive scan
+            // of the camera's histogram of this pass
+            const uint32_t* h = a.hist + uint64_t(cam) * a.hist_stride;
+            uint32_t v[kDpt], loc = 0;
+#pragma unroll
+            for (int j = 0; j < kDpt; ++j) {
+                v[j] = h[tid * kDpt + j];
+                loc += v[j];
+            }
+            uint32_t tot;
+            uint32_t run = block_exclusive_scan(loc, s_tmp, &tot) + a.vbase[cam];
+#pragma unroll
+            for (int j = 0; j < kDpt; ++j) {
+                gbase[j] = run;
+                run += v[j];
+            }
+            cam_cached = cam;
+        }
+        // 32-bit indices: slot counts stay below 2^31 (host.cu groups larger batches)
+        const uint32_t base = cbegin + uint32_t(warp) * (kItems * 32) + uint32_t(lane);
         const uint32_t* kin = a.keys_in + base;
         const uint32_t* vin = a.vals_in + base;
         uint32_t keys[kItems], vals[kItems], rank[kItems];
-        if ((uint64_t(t) + 1) * kOnesweepTile <= n) {  // full chunk: no bounds checks
+        if (cbegin + uint32_t(kOnesweepTile) == cend) {  // full chunk: no bounds checks
 #pragma unroll
             for (int i = 0; i < kItems; ++i) {
                 keys[i] = __ldcs(kin + i * 32);
@@ -116,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
         } else {
 #pragma unroll
             for (int i = 0; i < kItems; ++i) {
-                const bool in = uint64_t(base) + uint64_t(i) * 32 < n;
+                const bool in = base + uint32_t(i) * 32 < cend;
                 keys[i] = in ? __ldcs(kin + i * 32) : kInvalidKey;
                 vals[i] = kFirst ? base + uint32_t(i) * 32 : (in ? __ldcs(vin + i * 32) : 0u);
                 rank[i] = (in && (!kFirst || keys[i] != kInvalidKey)) ? 1u : 0u;
@@ -126,8 +156,8 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const bool valid = rank[i] != 0u;
-            const uint32_t d = (keys[i] >> a.shift) & 255u;
-            uint32_t* bits = &s_peer[i & 1][warp][d];
+            const uint32_t d = (keys[i] >> a.shift) & kMask;
+            uint32_t* bits = &s_peer[warp][d];
             if (valid) atomicOr(bits, 1u << lane);
             __syncwarp();
             const uint32_t peers = valid ? *bits : 0u;
@@ -139,68 +169,134 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
             if (valid && below == 0) pre = atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
             pre = __shfl_sync(0xffffffffu, pre, leader);
             rank[i] = valid ? (pre + __popc(below)) : 0xFFFFFFFFu;
+            __syncwarp();  // the leader's clear is visible before the next item's atomicOr
         }
         __syncthreads();
-        // Per digit (thread = digit): exclusive prefix across warps, block count.
-        uint32_t count = 0;
+        // Per digit (thread = kDpt digits): exclusive prefix across warps, block count.
+        uint32_t count[kDpt], loc = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = s_warp_hist[w][tid];
-            s_warp_hist[w][tid] = count;
-            count += c;
-        }
-        uint64_t* my_status = a.status + uint64_t(t) * kRadix + tid;
-        st_volatile_u64(my_status, make_status(t == 0 ? kFlagInclusive : kFlagAggregate, a.epoch, count));
-        uint32_t block_total;
-        const uint32_t bstart = block_exclusive_scan(count, s_tmp, &block_total);
-        s_bstart[tid] = bstart;
-        // Decoupled lookback for this digit.
-        uint64_t prefix = 0;
-        if (t > 0) {
-            int64_t j = int64_t(t) - 1;
-            while (true) {
-                const uint64_t s = wait_status(a.status + uint64_t(j) * kRadix + tid, a.epoch);
-                prefix += s & kCountMask;
-                if ((s >> 62) == kFlagInclusive) break;
-                --j;
+        for (int j = 0; j < kDpt; ++j) {
+            const int dg = tid * kDpt + j;
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t x = s_warp_hist[w][dg];
+                s_warp_hist[w][dg] = c;
+                c += x;
             }
-            st_volatile_u64(my_status, make_status(kFlagInclusive, a.epoch, prefix + count));
+            count[j] = c;
+            loc += c;
+            uint64_t* my_status = a.status + uint64_t(t) * kRadix + dg;
+            st_volatile_u64(my_status, make_status(t == first_chunk ? kFlagInclusive : kFlagAggregate,
+                                                   a.epoch, c));
         }
-        s_dest[tid] = uint32_t(uint64_t(gbase) + prefix - bstart);
+        uint32_t block_total;
+        uint32_t bst = block_exclusive_scan(loc, s_tmp, &block_total);
+#pragma unroll
+        for (int j = 0; j < kDpt; ++j) {
+            s_bstart[tid * kDpt + j] = bst;
+            bst += count[j];
+        }
+        // Decoupled look-back, back to the camera's first chunk; a thread's digits walk back
+        // together (their status words are adjacent, their waits overlap).
+        uint64_t prefix[kDpt];
+#pragma unroll
+        for (int j = 0; j < kDpt; ++j) prefix[j] = 0;
+        if (t > first_chunk) {
+            bool done[kDpt];
+#pragma unroll
+            for (int j = 0; j < kDpt; ++j) done[j] = false;
+            int64_t q = int64_t(t) - 1;
+            while (true) {
+                bool all = true;
+#pragma unroll
+                for (int j = 0; j < kDpt; ++j) {
+                    if (done[j]) continue;
+                    const uint64_t s = wait_status(a.status + uint64_t(q) * kRadix + tid * kDpt + j, a.epoch);
+                    prefix[j] += s & kCountMask;
+                    done[j] = (s >> 62) == kFlagInclusive;
+                    all = all && done[j];
+                }
+                if (all) break;
+                --q;
+            }
+#pragma unroll
+            for (int j = 0; j < kDpt; ++j)
+                st_volatile_u64(a.status + uint64_t(t) * kRadix + tid * kDpt + j,
+                                make_status(kFlagInclusive, a.epoch, prefix[j] + count[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < kDpt; ++j)
+            s_dest[tid * kDpt + j] = uint32_t(uint64_t(gbase[j]) + prefix[j] - s_bstart[tid * kDpt + j]);
         if (tid == 0) s_total = block_total;
         __syncthreads();
         // Stage the chunk in smem in sorted order, then write it out in digit runs.
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             if (rank[i] == 0xFFFFFFFFu) continue;
-            const uint32_t d = (keys[i] >> a.shift) & 255u;
+            const uint32_t d = (keys[i] >> a.shift) & kMask;
             const uint32_t pos = s_bstart[d] + s_warp_hist[warp][d] + rank[i];
             s_keys[pos] = keys[i];
             s_vals[pos] = vals[i];
         }
         __syncthreads();
         const uint32_t total = s_total;
-        for (uint32_t p = tid; p < total; p += kThreads) {
-            const uint32_t key = s_keys[p];
-            const uint32_t dst = s_dest[(key >> a.shift) & 255u] + p;
-            if (kWriteKeys) a.keys_out[dst] = key;
-            a.vals_out[dst] = s_vals[p];
-            if (a.rects_out) a.rects_out[dst] = __ldg(a.rects_in + s_vals[p]);
+        if (kWriteKeys) {
+            for (uint32_t p = tid; p < total; p += kThreads) {
+                const uint32_t key = s_keys[p];
+                const uint32_t dst = s_dest[(key >> a.shift) & kMask] + p;
+                a.keys_out[dst] = key;
+                a.vals_out[dst] = s_vals[p];
+            }
+        } else {
+            // last pass: gather the tile rects of the sorted slots, all kItems loads of a
+            // thread in flight before its stores (random 4-byte reads; latency-bound otherwise)
+            uint32_t dst[kItems], val[kItems], rect[kItems];
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                const uint32_t p = uint32_t(tid) + uint32_t(i) * kThreads;
+                const bool in = p < total;
+                val[i] = in ? s_vals[p] : 0u;
+                dst[i] = in ? s_dest[(s_keys[p] >> a.shift) & kMask] + p : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int i = 0; i < kItems; ++i)
+                rect[i] = dst[i] != 0xFFFFFFFFu ? __ldg(a.rects_in + val[i]) : 0u;
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {
+                if (dst[i] == 0xFFFFFFFFu) continue;
+                a.vals_out[dst[i]] = val[i];
+                a.rects_out[dst[i]] = rect[i];
+            }
         }
         __syncthreads();
     }
 }
 
 // ---- launchers -----------------------------------------------------------------------------
-void launch_onesweep(const OnesweepArgs& a, bool first, bool write_keys, int grid,
-                     cudaStream_t stream) {
+template <int kBits, bool kFirst, bool kWriteKeys>
+static void launch_one(const OnesweepArgs& a, int grid, cudaStream_t s) {
+    const int smem = int((2 * kOnesweepTile + 2 * kWarps * (1 << kBits)) * sizeof(uint32_t));
+    cudaFuncSetAttribute(onesweep_kernel<kBits, kFirst, kWriteKeys>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    onesweep_kernel<kBits, kFirst, kWriteKeys><<<grid, kThreads, smem, s>>>(a);
+}
+
+template <int kBits>
+static void launch_bits(const OnesweepArgs& a, bool first, bool write_keys, int grid, cudaStream_t s) {
     if (first) {
-        if (write_keys) onesweep_kernel<true, true><<<grid, kThreads, 0, stream>>>(a);
-        else onesweep_kernel<true, false><<<grid, kThreads, 0, stream>>>(a);
+        if (write_keys) launch_one<kBits, true, true>(a, grid, s);
+        else launch_one<kBits, true, false>(a, grid, s);
     } else {
-        if (write_keys) onesweep_kernel<false, true><<<grid, kThreads, 0, stream>>>(a);
-        else onesweep_kernel<false, false><<<grid, kThreads, 0, stream>>>(a);
+        if (write_keys) launch_one<kBits, false, true>(a, grid, s);
+        else launch_one<kBits, false, false>(a, grid, s);
     }
+}
+
+void launch_onesweep(const OnesweepArgs& a, int bits, bool first, bool write_keys, int grid,
+                     cudaStream_t stream) {
+    if (bits == 9) launch_bits<9>(a, first, write_keys, grid, stream);
+    else launch_bits<8>(a, first, write_keys, grid, stream);
 }
 
 }  // namespace gsim_gpu

@@ -200,4 +200,79 @@ def config3(seed: int = 0, n: int = 3_000_000) -> Workload:
     return Workload("cfg3", field, nodes, cams, [], "3M SH3 room, 2x1280x720")
 
 
+NODE_DTYPE = np.dtype([("begin", "<u8"), ("end", "<u8"), ("q", "<f8", (4,)), ("t", "<f8", (3,)),
+                       ("kind", "<i4"), ("env", "<i4")])  # == abi.gsim_node (80 bytes)
+
+
+@dataclass
+class RankEnvs:
+    """BASELINE config 4 on one rank: a device-resident scene holding a replica of the shared
+    1M SH3 background followed by the rank's environments' 4 x 20k objects each (written
+    piecewise, never materialised on the host as a whole), env-tagged nodes and cameras."""
+    scene: object
+    cameras: list
+    cams_per_env: int
+    env_begin: int
+    env_end: int
+    node_table: np.ndarray  # NODE_DTYPE rows: background, then 4 objects per env
+    seed: int
+
+    def frame_nodes(self, frame: int):
+        """ctypes gsim_node table with fresh random rigid poses (yaw ~ U[0, 2pi) about +z,
+        t ~ U[-0.5, 0.5]^3) for every object node (config 1/2/4 motion)."""
+        import ctypes as C
+        from . import abi
+        rng = np.random.default_rng((self.seed, 7919, frame, self.env_begin))
+        tab = self.node_table.copy()
+        n = len(tab) - 1
+        yaw = rng.uniform(0.0, 2.0 * math.pi, size=n)
+        tab["q"][1:, 0] = np.cos(0.5 * yaw)
+        tab["q"][1:, 3] = np.sin(0.5 * yaw)
+        tab["t"][1:] = rng.uniform(-0.5, 0.5, size=(n, 3))
+        arr = (abi.gsim_node * len(tab))()
+        C.memmove(arr, tab.ctypes.data, tab.nbytes)
+        return arr
+
+    def camera_table(self, env_a: int, env_b: int):
+        """ctypes gsim_camera table of envs [env_a, env_b) (global env indices)."""
+        from . import abi
+        cams = self.cameras[(env_a - self.env_begin) * self.cams_per_env:
+                            (env_b - self.env_begin) * self.cams_per_env]
+        arr = (abi.gsim_camera * len(cams))()
+        for k, c in enumerate(cams):
+            arr[k] = c.to_c()
+        return arr
+
+
+def config4_rank(ctx, env_begin: int, env_end: int, seed: int = 0, n_bg: int = 1_000_000,
+                 n_objects: int = 4, per_object: int = 20_000, cams_per_env: int = 5,
+                 size=VGA) -> RankEnvs:
+    """Environments [env_begin, env_end) of config 4 on `ctx`'s device. The background and every
+    env's objects/cameras come from the same seeded streams as config2 (env e of config 4 equals
+    env e of config2(seed, n_envs > e)), so env renders can be checked against config 2."""
+    rng = np.random.default_rng((seed, 2))
+    n_env = env_end - env_begin
+    total = n_bg + n_env * n_objects * per_object
+    scene = ctx.create_scene(total, 3)
+    scene.write(0, concat_fields([gaussians(rng, n_bg, 3)], 3))
+    rows = [(0, n_bg, (1.0, 0.0, 0.0, 0.0), (0.0, 0.0, 0.0), NodeKind.background, -1)]
+    cams = []
+    base = ring_cameras(cams_per_env, 4.0, 1.5, size[0], size[1])
+    b = n_bg
+    for e in range(env_begin, env_end):
+        erng = np.random.default_rng((seed, 2, e))
+        objs = _env_objects(erng, n_objects, per_object, 3)
+        scene.write(b, concat_fields(objs, 3))
+        for k in range(n_objects):
+            rows.append((b, b + per_object, (1.0, 0.0, 0.0, 0.0), (0.0, 0.0, 0.0), NodeKind.interactive, e))
+            b += per_object
+        for c in base:
+            jc = jitter_camera(erng, c)
+            jc.env = e
+            jc.id = f"env{e}/{c.id}"
+            cams.append(jc)
+    table = np.array(rows, dtype=NODE_DTYPE)
+    return RankEnvs(scene, cams, cams_per_env, env_begin, env_end, table, seed)
+
+
 CONFIGS = {"cfg0": config0, "cfg1": config1, "cfg2": config2, "cfg3": config3}

@@ -46,6 +46,91 @@ def gather_frames(frames: torch.Tensor, n_envs: int, floats_per_env: int, dst: i
     return out
 
 
+class ChunkGather:
+    """BASELINE config 4's frame gather, overlapped with rendering.
+
+    Every rank renders its env_range in chunks of <= chunk_envs environments (config-2-sized
+    launches); round j moves every rank's chunk j to rank `dst` with one grouped point-to-point
+    exchange (dist.batch_isend_irecv: NCCL over NVLink on the GPU box, gloo on CPU) while chunk
+    j+1 renders. Issue send(j) on the stream that rendered chunk j (NCCL orders its transfer
+    after that stream's work) and call target(j) on it before rendering: a send buffer is reused
+    only after its previous transfer completed (double buffering). Rank `dst` renders straight
+    into its slices of `out` ([n_envs * floats_per_env], environment order) and receives the
+    others' chunks into theirs.
+    """
+
+    def __init__(self, n_envs: int, floats_per_env: int, chunk_envs: int, device, rank: int | None = None,
+                 world: int | None = None, dst: int = 0, n_buffers: int = 2, dtype=torch.float32):
+        initialized = dist.is_available() and dist.is_initialized()
+        self.rank = rank if rank is not None else (dist.get_rank() if initialized else 0)
+        self.world = world if world is not None else (dist.get_world_size() if initialized else 1)
+        self.n_envs, self.fpe, self.dst = n_envs, floats_per_env, dst
+        self.ranges = [env_range(n_envs, r, self.world) for r in range(self.world)]
+        self.chunks = [list(env_chunks(b, e, chunk_envs)) for b, e in self.ranges]
+        self.my_chunks = self.chunks[self.rank]
+        self.rounds = max(len(c) for c in self.chunks)
+        self.out = None
+        self.bufs = []
+        if self.rank == dst:
+            self.out = torch.empty(n_envs * floats_per_env, dtype=dtype, device=device)
+        else:
+            self.bufs = [torch.empty(chunk_envs * floats_per_env, dtype=dtype, device=device)
+                         for _ in range(n_buffers)]
+        self.pending = [[] for _ in range(max(n_buffers, 1))]
+        self.recv_pending = []
+        # bytes rank dst receives per step (floats)
+        self.bytes_to_dst = sum((e - b) * floats_per_env for r, (b, e) in enumerate(self.ranges) if r != dst)
+        if self.world > 1:
+            dist.barrier()  # the communicator exists before the first point-to-point batch
+
+    def _view(self, b: int, e: int):
+        return self.out[b * self.fpe: e * self.fpe]
+
+    def target(self, j: int) -> torch.Tensor:
+        """Where this rank renders its chunk j (waits for the buffer's previous transfer)."""
+        b, e = self.my_chunks[j]
+        if self.rank == self.dst:
+            return self._view(b, e)
+        slot = j % len(self.bufs)
+        for w in self.pending[slot]:
+            w.wait()
+        self.pending[slot] = []
+        return self.bufs[slot][: (e - b) * self.fpe]
+
+    def send(self, j: int) -> None:
+        """Round j: this rank's chunk j to dst, and at dst every other rank's chunk j."""
+        if self.world == 1:
+            return
+        ops = []
+        if self.rank == self.dst:
+            for r in range(self.world):
+                if r != self.dst and j < len(self.chunks[r]):
+                    b, e = self.chunks[r][j]
+                    ops.append(dist.P2POp(dist.irecv, self._view(b, e), r))
+        elif j < len(self.my_chunks):
+            b, e = self.my_chunks[j]
+            slot = j % len(self.bufs)
+            ops.append(dist.P2POp(dist.isend, self.bufs[slot][: (e - b) * self.fpe], self.dst))
+        if not ops:
+            return
+        works = dist.batch_isend_irecv(ops)
+        if self.rank == self.dst:
+            self.recv_pending.extend(works)
+        else:
+            self.pending[j % len(self.bufs)].extend(works)
+
+    def finish(self) -> None:
+        """Every transfer of the step is ordered before the current stream's next work (NCCL)
+        or complete (gloo); on dst, `out` then holds every environment's frames."""
+        for works in self.pending:
+            for w in works:
+                w.wait()
+        self.pending = [[] for _ in self.pending]
+        for w in self.recv_pending:
+            w.wait()
+        self.recv_pending = []
+
+
 def max_over_ranks(value: float, device) -> float:
     """Max of a per-rank scalar (device time) over all ranks."""
     t = torch.tensor([value], dtype=torch.float64, device=device)

@@ -112,16 +112,19 @@ def test_encode_of_device_output_and_device_destination(ctx, oracle):
     assert np.array_equal(views[0]["depth_pfm"][::-1], targets[0].depth)
 
 
-def test_render_encoded_camera_groups(ctx, oracle):
-    """40 cameras with near/far 0.05/100 (27 depth bits, 32 cameras per key group): the batch
-    runs as two groups; the encoded blocks still follow the batch's camera order."""
+def test_render_encoded_camera_groups(oracle, monkeypatch):
+    """40 cameras of mixed sizes, run as 3 camera groups (GSIM_GPU_GROUP_SLOTS budget): the
+    encoded blocks still follow the batch's camera order."""
+    from paper_2507_21981_b200 import Context
     field = oracle.random_field(41, 3000, 3.0, 0.01, 0.3, 1)
     field.means[:, 2] += 3.0
     cams = [ref_camera(32 + (k % 3) * 16, 32, 30.0 + k) for k in range(40)]
+    monkeypatch.setenv("GSIM_GPU_GROUP_SLOTS", str(16 * 3000))
+    ctx = Context(0)
     scene = ctx.upload(field)
     o = EncodeOptions(ALL, True, 1000.0)
     got = ctx.render_encoded(scene, [], cams, None, o)
-    assert ctx.stats()["groups"] > 1
+    assert ctx.stats()["groups"] == 3
     want = oracle_blob(oracle, ctx.render(scene, [], cams), o)
     assert np.array_equal(got, want)
 

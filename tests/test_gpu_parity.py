@@ -325,23 +325,31 @@ def test_env_batch_equals_separate_renders(ctx, oracle):
             assert_parity(batch[2 * e + k], o[k], (e, k))
 
 
-def test_large_batch_is_split_and_order_preserved(ctx, oracle):
-    """40 cameras with near/far 0.05/100 need 27 depth bits + 6 camera bits > 32: the batch
-    runs as camera groups; every camera must equal its own single-camera render."""
+def test_large_batch_one_launch_and_groups(ctx, oracle, monkeypatch):
+    """40 cameras render in one launch sequence (the camera is the depth sort's segment, not a
+    key digit); with a small slot budget per group (GSIM_GPU_GROUP_SLOTS) the same batch runs as
+    camera groups. Every camera must equal its own single-camera render either way."""
+    from paper_2507_21981_b200 import Context
     field = oracle.random_field(321, 2500, 3.0, 0.01, 0.2, 1)
     field.means[:, 2] += 3.0
-    s = ctx.upload(field)
     cams = []
     for k in range(40):
         c = ref_camera(64, 48, 50.0)
         c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.01 * (k - 20)), (0.02 * (k % 7), 0.0, 0.0))
         cams.append(c)
+    s = ctx.upload(field)
     batch = ctx.render(s, [], cams)
-    assert ctx.stats()["groups"] == 2
-    for k in (0, 17, 31, 32, 39):
+    assert ctx.stats()["groups"] == 1
+    monkeypatch.setenv("GSIM_GPU_GROUP_SLOTS", str(16 * 2500))
+    small = Context(0)
+    s2 = small.upload(field)
+    grouped = small.render(s2, [], cams)
+    assert small.stats()["groups"] == 3 and small.stats()["last_group_cameras"] == 8
+    for k in (0, 15, 16, 17, 31, 32, 39):
         single = ctx.render(s, [], [cams[k]])[0]
-        assert np.array_equal(batch[k].rgb, single.rgb), k
-        assert np.array_equal(batch[k].depth, single.depth), k
+        for got in (batch[k], grouped[k]):
+            assert np.array_equal(got.rgb, single.rgb), k
+            assert np.array_equal(got.depth, single.depth), k
 
 
 # ---- BASELINE-shaped parity ----------------------------------------------------------------
