@@ -466,7 +466,7 @@ def run_cfg4(args, rank, world, local, dist):
     b, e = env_range(n_envs, rank, world)
     ctx = Context(local)
     t0 = time.perf_counter()
-    r = config4_rank(ctx, b, e, seed=1000, n_envs=n_envs)
+    r = config4_rank(ctx, b, e, seed=1000)
     setup_s = time.perf_counter() - t0
     cams_per_env = r.cams_per_env
     px_per_env = sum(c.width * c.height for c in r.cameras[:cams_per_env])

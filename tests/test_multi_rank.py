@@ -73,3 +73,48 @@ def test_gather_frames_gloo_world2(n_envs):
         assert p.exitcode == 0
     assert all(ok for ok, _ in results)
     assert all(t == 3.0 for _, t in results)  # max over ranks of (rank + 1) * 1.5
+
+
+def _chunk_worker(rank, world, port, n_envs, per_env, chunk, steps, q):
+    import torch.distributed as dist
+
+    from paper_2507_21981_b200.shard import ChunkGather, env_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = ChunkGather(n_envs, per_env, chunk, torch.device("cpu"), dst=0)
+    b, e = env_range(n_envs, rank, world)
+    ok = True
+    for step in range(steps):  # the bench's schedule: render chunk j, send j, next chunk
+        for j, (cb, ce) in enumerate(g.my_chunks):
+            buf = g.target(j)
+            buf.copy_(torch.cat([torch.arange(per_env, dtype=torch.float32) + env * 1000 + step * 1e6
+                                 for env in range(cb, ce)]))
+            g.send(j)
+        g.finish()
+        if rank == 0:
+            want = torch.cat([torch.arange(per_env, dtype=torch.float32) + env * 1000 + step * 1e6
+                              for env in range(n_envs)])
+            ok = ok and bool(torch.equal(g.out, want))
+    q.put((rank, ok, g.rounds, (b, e)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_envs,chunk", [(12, 2), (7, 2), (9, 4)])
+def test_chunk_gather_schedule_gloo_world2(n_envs, chunk):
+    """Config 4's schedule (shard.ChunkGather: chunks of <= chunk envs per rank, round j's grouped
+    point-to-point batch, double-buffered sends reused across rounds and steps): rank 0 ends every
+    step with every environment's frames in environment order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, 2, port, n_envs, 5, chunk, 3, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert results[0][1], results
+    assert results[0][2] == -(-((n_envs + 1) // 2) // chunk)

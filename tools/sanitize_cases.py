@@ -1,0 +1,107 @@
+"""compute-sanitizer workloads: small renders that exercise every race-prone
+mechanism of the path, run under memcheck / racecheck / synccheck by tools/sanitize.sh.
+
+    python tools/sanitize_cases.py smoke|copies|contexts|batch
+
+smoke     __graft_entry__.smoke(): K2, key_hist, onesweep look-back, binning, scatter, raster
+copies    3-camera render into host targets: per-camera tile counters + system fence +
+          cuStreamWaitValue32 copy handoff (raster.cu epilogue, host.cu queue_camera_copies),
+          then render_encoded (the same handoff for encoded blocks)
+contexts  two contexts rendering concurrently from two host threads (shared device, separate
+          streams and workspaces)
+batch     a 12-camera env batch with a multi-unit scatter per camera (bitmap peers) and a
+          1280x720 camera (u8 probe peers), plus a forced pair-buffer overflow re-run
+"""
+from __future__ import annotations
+
+import os
+import sys
+import threading
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+
+def scene(orc, seed=7, n=6000, deg=2):
+    f = orc.random_field(seed, n, 3.0, 0.01, 0.2, deg)
+    f.means[:, 2] += 3.0
+    f.touch()
+    return f
+
+
+def cams(k, w=128, h=96):
+    from paper_2507_21981_b200.api import CameraModel, RigidTransform, quat_from_axis_angle
+    out = []
+    for i in range(k):
+        c = CameraModel(fx=90.0, fy=90.0, cx=w / 2, cy=h / 2, width=w, height=h)
+        c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 0.05 * (i - k / 2)), (0.1 * i, 0.0, 0.0))
+        out.append(c)
+    return out
+
+
+def main(case: str) -> None:
+    from oracle.oracle import Oracle
+    from paper_2507_21981_b200 import Context, EncodeOptions
+    orc = Oracle()
+    if case == "smoke":
+        import __graft_entry__ as g
+        g.smoke()
+        return
+    if case == "copies":
+        ctx = Context(0)
+        f = scene(orc)
+        s = ctx.upload(f)
+        c3 = cams(3)
+        a = ctx.render(s, [], c3)
+        b = ctx.render(s, [], c3)
+        assert all(np.array_equal(x.rgb, y.rgb) for x, y in zip(a, b))
+        ctx.render_encoded(s, [], c3, None, EncodeOptions())
+        print("copies ok")
+        return
+    if case == "contexts":
+        f = scene(orc)
+        ctxs = [Context(0), Context(0)]
+        scenes = [c.upload(f) for c in ctxs]
+        res = [None, None]
+
+        def run(k):
+            for _ in range(3):
+                res[k] = ctxs[k].render(scenes[k], [], cams(2))
+        th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert all(np.array_equal(x.rgb, y.rgb) for x, y in zip(res[0], res[1]))
+        print("contexts ok")
+        return
+    if case == "batch":
+        from paper_2507_21981_b200.api import NodeKind, RigidTransform, SceneNode, quat_from_axis_angle
+        f = scene(orc, seed=9, n=30000, deg=1)
+        nodes = [SceneNode("bg", NodeKind.background, RigidTransform(), (0, 20000))]
+        for e in range(4):
+            nodes.append(SceneNode(f"o{e}", NodeKind.interactive,
+                                   RigidTransform(quat_from_axis_angle((0, 0, 1), 0.3 * e), (0.1 * e, 0, 0)),
+                                   (20000 + 2500 * e, 22500 + 2500 * e), env=e))
+        cs = cams(12)
+        for i, c in enumerate(cs):
+            c.env = i % 4
+        big = cams(1, 1280, 720)[0]
+        big.env = 0
+        ctx = Context(0)
+        s = ctx.upload(f)
+        ctx.render(s, nodes, cs + [big])
+        os.environ["GSIM_GPU_INITIAL_PAIR_CAPACITY"] = "5000"
+        small = Context(0)
+        ss = small.upload(f)
+        small.render(ss, nodes, cs[:3])
+        print("batch ok, pairs", small.stats()["pairs"])
+        return
+    raise SystemExit(f"unknown case {case}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
