@@ -51,17 +51,23 @@ def _stale(target: Path, inputs: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in inputs)
 
 
-def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False,
+          debug: bool = False) -> Path:
+    """libgsim_gpu.so, or with debug=True libgsim_gpu_debug.so: the same sources with the
+    GSIM_DCHECK bounds checks compiled in (common.cuh; select it with GSIM_GPU_LIB)."""
+    build_dir = BUILD.with_name(BUILD.name + "_debug") if debug else BUILD
+    lib = LIB.with_name("libgsim_gpu_debug.so") if debug else LIB
+    flags = ["-DGSIM_DEBUG_CHECKS"] if debug else []
+    build_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     header_deps = [CSRC / d for d in DEPS] + [ROOT / "include" / "gsim_gpu.h", Path(__file__)]
     objs = []
     for src, extra in SOURCES.items():
-        obj = BUILD / (src + ".o")
+        obj = build_dir / (src + ".o")
         objs.append(obj)
         if not force and not ptxas_info and not _stale(obj, [CSRC / src] + header_deps):
             continue
-        cmd = [cc, *ARCH, *COMMON, *extra, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [cc, *ARCH, *COMMON, *flags, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
         if verbose:
@@ -71,8 +77,8 @@ def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) 
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")
         if ptxas_info or verbose:
             sys.stdout.write(res.stderr)
-    if force or _stale(LIB, objs):
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or _stale(lib, objs):
+        tmp = lib.with_suffix(".so.tmp")
         # static CUDA runtime: the library needs only the driver, whoever loads it
         cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
         if verbose:
@@ -80,9 +86,10 @@ def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) 
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose=True, ptxas_info="--ptxas" in sys.argv, force="--force" in sys.argv)
+    build(verbose=True, ptxas_info="--ptxas" in sys.argv, force="--force" in sys.argv,
+          debug="--debug" in sys.argv)

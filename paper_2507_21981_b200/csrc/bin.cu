@@ -104,6 +104,7 @@ __device__ __forceinline__ void add_rect_rows(int* D, int wd, uint32_t r, bool v
     if (!valid) return;
     const uint32_t tx0 = r & 255u, ty0 = (r >> 8) & 255u, tx1 = (r >> 16) & 255u, ty1 = r >> 24;
     for (uint32_t ty = ty0; ty <= ty1; ++ty) {
+        GSIM_DCHECK(tx0 <= tx1 && tx1 + 1u < uint32_t(wd));
         atomicAdd(D + ty * uint32_t(wd) + tx0, 1);
         atomicAdd(D + ty * uint32_t(wd) + tx1 + 1u, -1);
     }
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(BinArgs a) {
     int c = upper_index(a.cam_slot_base, a.n_cams, uint64_t(lo));
     while (true) {
         while (c < a.n_cams && a.cam_slot_base[c + 1] <= lo) ++c;  // skip empty cameras
+        GSIM_DCHECK(c >= 0);
         if (c >= a.n_cams || a.cam_slot_base[c] >= hi) break;
         const uint32_t plo = max(lo, uint32_t(a.cam_slot_base[c]));
         const uint32_t phi = min(hi, uint32_t(a.cam_slot_base[c + 1]));
@@ -494,6 +496,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                 const uint32_t w = tx1 - tx0 + 1u;
                 const uint32_t q = mg ? __umulhi(kk, mg) : kk;
                 const uint32_t cell = (ty0 + q) * uint32_t(wd) + tx0 + (kk - q * w);
+                GSIM_DCHECK(!in || (cell < uint32_t(wd) * uint32_t(u.tiles_y) && ty0 + q <= (ro >> 24)));
                 if (kBitmap) {
                     // lanes of this step on the same cell, from one atomicOr into the cell's
                     // bitmap; ranked by lane (= emission) order, the lowest lane bumps the

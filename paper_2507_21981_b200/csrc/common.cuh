@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -183,6 +184,25 @@ __host__ __device__ inline dm3 mtransposed(const dm3& a) {
 __host__ __device__ inline double clampd(double v, double lo, double hi) {  // std::clamp
     return (v < lo) ? lo : (hi < v) ? hi : v;
 }
+
+// ---- debug checks (libgsim_gpu_debug.so, build.py --debug) ---------------------------------
+// compute-sanitizer is closed on the GPU pool this was developed on; the debug build instead
+// bounds-checks every computed index of the race- and overflow-prone mechanisms (onesweep
+// destinations and look-back, key histograms, binning cells and pair positions, raster list
+// reads) and traps with the failing check's file and line.
+#ifdef GSIM_DEBUG_CHECKS
+#define GSIM_DCHECK(cond)                                                              \
+    do {                                                                               \
+        if (!(cond)) {                                                                 \
+            printf("GSIM_DCHECK failed: %s at %s:%d\n", #cond, __FILE__, __LINE__);   \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define GSIM_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
 
 // ---- small device helpers ----------------------------------------------------------------
 

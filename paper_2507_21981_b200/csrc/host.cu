@@ -140,6 +140,7 @@ struct gsim_gpu_context {
     int raster_rect_w = 8;           // GSIM_GPU_RASTER_RECT=16: 16x4 warp bands in K4 (default 8x8)
     int raster_exact_cull = 1;       // GSIM_GPU_RASTER_EXACT=0: bounding-box warp culling only
     int raster_batch = 128;          // GSIM_GPU_RASTER_BATCH=256: larger K4 batches, fewer CTAs/SM
+    int raster_bulk = 0;             // GSIM_GPU_RASTER_BULK=1: records staged by cp.async.bulk
     // per-pair plane (final per-tile order)
     DevBuf<uint32_t> vals;
     uint64_t pair_capacity = 0;
@@ -696,6 +697,7 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.rect_w = ctx->raster_rect_w;
     rr.batch = ctx->raster_batch;
     rr.exact_cull = ctx->raster_exact_cull;
+    rr.bulk_copy = ctx->raster_bulk;
     rr.valid_alpha = ctx->frame_valid_alpha;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
     const bool overlap_enc = ctx->frame_enc_host && rr.enc.flags && wait_value_fn();
@@ -1593,6 +1595,7 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         if (const char* e = std::getenv("GSIM_GPU_RASTER_RECT")) ctx->raster_rect_w = std::atoi(e) == 16 ? 16 : 8;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_EXACT")) ctx->raster_exact_cull = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
+        if (const char* e = std::getenv("GSIM_GPU_RASTER_BULK")) ctx->raster_bulk = std::atoi(e) == 1 ? 1 : 0;
         if (const char* e = std::getenv("GSIM_GPU_OVERLAP_COPIES")) ctx->overlap_copies = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_GROUP_SLOTS")) {
             const uint64_t v = std::strtoull(e, nullptr, 10);

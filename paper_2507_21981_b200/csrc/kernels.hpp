@@ -116,6 +116,7 @@ struct RasterArgs {
     int rect_w;                      // warp-rectangle width: 16 (16x4 bands) or 8 (8x8)
     int batch;                       // records per shared-memory batch: 128 or 256
     int exact_cull;                  // exact ellipse-vs-warp-rectangle test in the compaction
+    int bulk_copy;                   // stage records with cp.async.bulk + mbarrier (8x8 rects)
     float valid_alpha;               // depth written as 0 where accum_alpha < valid_alpha
                                      // (render_depth_ring, transfer.cpp:116-118); 0 = off
     float* out;                      // per camera [rgb W*H*3 | depth W*H | alpha W*H]

@@ -181,9 +181,30 @@ __device__ __forceinline__ void blend_list(const uint32_t* list, uint32_t count,
     }
 }
 
+// mbarrier helpers for the bulk-copy (TMA engine) staging variant.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
 // RW = warp-rectangle width in pixels (16: 16x4 bands, 8: 8x8 quadrants); kBatch = records
-// per batch (two buffers of kBatch * 48 bytes of shared memory).
-template <int RW, int kBatch>
+// per batch (two buffers of kBatch * 48 bytes of shared memory). kBulk: the records are staged
+// with one cp.async.bulk (TMA engine, UBLKCP) per 48-byte record completing on a per-buffer
+// mbarrier, instead of three 16-byte cp.async (LDGSTS) per record and a wait_all.
+template <int RW, int kBatch, bool kBulk>
 __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kernel(RasterArgs a) {
     constexpr int kPerThread = kBatch / kThreads;
     constexpr int RH = 64 / RW;  // warp-rectangle height
@@ -192,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     __shared__ Record s_spl[2][kBatch];
     __shared__ __align__(16) uint32_t s_list[kWarps][kBatch];
     __shared__ Record s_null;  // pads the compacted lists: fails the box test (r = -1)
+    __shared__ __align__(8) uint64_t s_bar[2];  // kBulk: one mbarrier per record buffer
 
     const uint32_t g = blockIdx.x;
     const int cam_idx = upper_index(a.cam_tile_base, a.n_cams, g);
@@ -227,11 +249,30 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
             const uint32_t i = b + uint32_t(tid + h * kThreads);
             uint32_t sl = i < end ? __ldg(a.values + i) : 0xFFFFFFFFu;
             // a stale slot is only possible in a clamped (overflowed) frame
+            GSIM_DCHECK(!(i < end && e64 <= a.capacity) || sl < a.n_slots);
             if (i < end && sl >= a.n_slots) sl = 0;
             slot_next[h] = sl;
         }
     };
+    const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&s_bar[0]));
+    uint32_t phase_bits = 0;   // kBulk: parity of the next phase of each buffer's barrier
+    uint32_t pending_bulk = 0; // kBulk: buffers with copies issued and not yet waited for
     auto issue_copy = [&](int buf) {
+        if constexpr (kBulk) {
+            // every thread arrives once per phase, announcing the bytes of its own copies first
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int h = 0; h < kPerThread; ++h) bytes += slot_next[h] != 0xFFFFFFFFu ? 48u : 0u;
+            const uint32_t bar = bar0 + 8u * uint32_t(buf);
+            mbar_arrive_expect(bar, bytes);
+            pending_bulk |= 1u << buf;
+#pragma unroll
+            for (int h = 0; h < kPerThread; ++h)
+                if (slot_next[h] != 0xFFFFFFFFu)
+                    bulk_copy(uint32_t(__cvta_generic_to_shared(&s_spl[buf][tid + h * kThreads])),
+                              a.records + slot_next[h], 48u, bar);
+            return;
+        }
 #pragma unroll
         for (int h = 0; h < kPerThread; ++h) {
             if (slot_next[h] != 0xFFFFFFFFu) {
@@ -250,7 +291,13 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         s_null.a = make_float4(0.f, 0.f, -1.f, 0.f);
         s_null.b = make_float4(0.f, 0.f, 0.f, 0.f);
         s_null.c = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kBulk) {
+            mbar_init(bar0, kThreads);
+            mbar_init(bar0 + 8u, kThreads);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
     }
+    if (kBulk) __syncthreads();  // barriers initialised before any thread arrives
     const uint32_t null_addr = uint32_t(__cvta_generic_to_shared(&s_null));
     uint32_t fetched = 0;
     if (begin < end) {
@@ -262,7 +309,13 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     for (uint32_t b0 = begin; b0 < end; b0 += kBatch, buf ^= 1) {
         const uint32_t n_b = (end - b0) < uint32_t(kBatch) ? (end - b0) : uint32_t(kBatch);
         fetched += n_b;
-        asm volatile("cp.async.wait_all;" ::: "memory");
+        if constexpr (kBulk) {
+            mbar_wait(bar0 + 8u * uint32_t(buf), (phase_bits >> buf) & 1u);
+            phase_bits ^= 1u << buf;
+            pending_bulk &= ~(1u << buf);
+        } else {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
         __syncthreads();
         // every warp has left batch i-1, so its buffer takes batch i+1
         if (b0 + kBatch < end) {
@@ -309,7 +362,14 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         }
         if (__syncthreads_count(T.x < cutoff && T.y < cutoff ? 0 : 1) == 0) break;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");  // no copy may land after the CTA exits
+    // no copy may land after the CTA exits
+    if constexpr (kBulk) {
+        // a batch whose copies were issued but never waited for (early saturation exit)
+        for (int bb = 0; bb < 2; ++bb)
+            if (pending_bulk & (1u << bb)) mbar_wait(bar0 + 8u * uint32_t(bb), (phase_bits >> bb) & 1u);
+    } else {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
 
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
     write_pixel(a, cam, x, y, cr.x, cg.x, cb.x, d.x, acc.x);
@@ -324,12 +384,17 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
 void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream) {
     if (n_tiles == 0) return;
     const bool small = a.batch == 128;
+    if (a.bulk_copy) {  // GSIM_GPU_RASTER_BULK=1 (A/B measurement)
+        if (small) raster_kernel<8, 128, true><<<n_tiles, kThreads, 0, stream>>>(a);
+        else raster_kernel<8, 256, true><<<n_tiles, kThreads, 0, stream>>>(a);
+        return;
+    }
     if (a.rect_w == 8) {
-        if (small) raster_kernel<8, 128><<<n_tiles, kThreads, 0, stream>>>(a);
-        else raster_kernel<8, 256><<<n_tiles, kThreads, 0, stream>>>(a);
+        if (small) raster_kernel<8, 128, false><<<n_tiles, kThreads, 0, stream>>>(a);
+        else raster_kernel<8, 256, false><<<n_tiles, kThreads, 0, stream>>>(a);
     } else {
-        if (small) raster_kernel<16, 128><<<n_tiles, kThreads, 0, stream>>>(a);
-        else raster_kernel<16, 256><<<n_tiles, kThreads, 0, stream>>>(a);
+        if (small) raster_kernel<16, 128, false><<<n_tiles, kThreads, 0, stream>>>(a);
+        else raster_kernel<16, 256, false><<<n_tiles, kThreads, 0, stream>>>(a);
     }
 }
 

@@ -107,11 +107,13 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
         if (t >= n_chunks) break;
         const int cam = upper_index(a.chunk_base, a.n_cams, t);
         const uint32_t first_chunk = a.chunk_base[cam];
+        GSIM_DCHECK(cam >= 0 && cam < a.n_cams && t >= first_chunk && t < a.chunk_base[cam + 1]);
         const uint64_t sb = kFirst ? a.seg_base64[cam] : uint64_t(seg32[cam]);
         const uint64_t se = kFirst ? a.seg_base64[cam + 1] : uint64_t(seg32[cam + 1]);
         const uint32_t cbegin = uint32_t(sb) + (t - first_chunk) * uint32_t(kOnesweepTile);
         const uint64_t cend64 = uint64_t(cbegin) + kOnesweepTile;
         const uint32_t cend = uint32_t(cend64 < se ? cend64 : se);
+        GSIM_DCHECK(uint64_t(cbegin) >= sb && cbegin < cend);
         if (cam != cam_cached) {
             // global start of each digit in this camera: camera's output base + exclusive scan
             // of the camera's histogram of this pass
@@ -212,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 #pragma unroll
                 for (int j = 0; j < kDpt; ++j) {
                     if (done[j]) continue;
+                    GSIM_DCHECK(q >= int64_t(first_chunk));
                     const uint64_t s = wait_status(a.status + uint64_t(q) * kRadix + tid * kDpt + j, a.epoch);
                     prefix[j] += s & kCountMask;
                     done[j] = (s >> 62) == kFlagInclusive;
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
             if (rank[i] == 0xFFFFFFFFu) continue;
             const uint32_t d = (keys[i] >> a.shift) & kMask;
             const uint32_t pos = s_bstart[d] + s_warp_hist[warp][d] + rank[i];
+            GSIM_DCHECK(pos < uint32_t(kOnesweepTile));
             s_keys[pos] = keys[i];
             s_vals[pos] = vals[i];
         }
@@ -245,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
             for (uint32_t p = tid; p < total; p += kThreads) {
                 const uint32_t key = s_keys[p];
                 const uint32_t dst = s_dest[(key >> a.shift) & kMask] + p;
+                GSIM_DCHECK(dst >= a.vbase[cam] && dst < a.vbase[cam + 1]);
                 a.keys_out[dst] = key;
                 a.vals_out[dst] = s_vals[p];
             }
@@ -265,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
 #pragma unroll
             for (int i = 0; i < kItems; ++i) {
                 if (dst[i] == 0xFFFFFFFFu) continue;
+                GSIM_DCHECK(dst[i] >= a.vbase[cam] && dst[i] < a.vbase[cam + 1]);
                 a.vals_out[dst[i]] = val[i];
                 a.rects_out[dst[i]] = rect[i];
             }

@@ -1,7 +1,7 @@
 """compute-sanitizer workloads: small renders that exercise every race-prone
 mechanism of the path, run under memcheck / racecheck / synccheck by tools/sanitize.sh.
 
-    python tools/sanitize_cases.py smoke|copies|contexts|batch
+    python tools/sanitize_cases.py smoke|copies|contexts|batch|determinism
 
 smoke     __graft_entry__.smoke(): K2, key_hist, onesweep look-back, binning, scatter, raster
 copies    3-camera render into host targets: per-camera tile counters + system fence +
@@ -46,6 +46,8 @@ def main(case: str) -> None:
     from oracle.oracle import Oracle
     from paper_2507_21981_b200 import Context, EncodeOptions
     orc = Oracle()
+    from paper_2507_21981_b200 import abi
+    print("library:", abi.LIB_PATH.name)
     if case == "smoke":
         import __graft_entry__ as g
         g.smoke()
@@ -99,6 +101,31 @@ def main(case: str) -> None:
         ss = small.upload(f)
         small.render(ss, nodes, cs[:3])
         print("batch ok, pairs", small.stats()["pairs"])
+        return
+    if case == "determinism":
+        # races would show as run-to-run differences: 3 contexts x 20 frames of a 1.08M-Gaussian
+        # config-1 scene from 3 host threads, every output bit-identical to the first
+        from paper_2507_21981_b200.scenes import config1
+        w = config1(seed=5)
+        nodes = w.frame_nodes(1)
+        ctxs = [Context(0) for _ in range(3)]
+        scenes = [c.upload(w.field) for c in ctxs]
+        want = ctxs[0].render(scenes[0], nodes, w.cameras)
+        bad = [0]
+
+        def run(k):
+            for _ in range(20):
+                got = ctxs[k].render(scenes[k], nodes, w.cameras)
+                bad[0] += sum(not (np.array_equal(g.rgb, t.rgb) and np.array_equal(g.depth, t.depth)
+                                   and np.array_equal(g.accum_alpha, t.accum_alpha))
+                              for g, t in zip(got, want))
+        th = [threading.Thread(target=run, args=(k,)) for k in range(3)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        print("determinism: 60 frames x 5 cameras,", bad[0], "differ")
+        assert bad[0] == 0
         return
     raise SystemExit(f"unknown case {case}")
 

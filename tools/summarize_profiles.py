@@ -1,12 +1,13 @@
 """Summarise ncu outputs brought back in gpurun_out/ into profiles/ (tracked).
 
-    python tools/summarize_profiles.py --tag r1 --launches gpurun_out/launches_bench.csv \
-        --report gpurun_out/prof_frame.ncu-rep
+    python tools/summarize_profiles.py --tag r2_cfg1 --config cfg1 \
+        --launches gpurun_out/launches_bench.csv --report gpurun_out/prof_frame.ncu-rep
 
 Writes profiles/<tag>_launches.md (per-kernel launch statistics of the bench command),
-profiles/<tag>_frame.md (one full-set capture of every kernel of a config-1 frame) and
-profiles/traffic.json (DRAM read+write bytes per launch of every pipeline stage, read by
-bench.py for the roofline "traffic" field).
+profiles/<tag>_frame.md (one full-set capture of every kernel of one frame) and, under the
+config's key, profiles/traffic.json (DRAM read+write bytes per frame of every pipeline stage)
+and profiles/instructions.json (warp instructions per frame), which bench.py reads for the
+SAME config only.
 """
 from __future__ import annotations
 
@@ -75,11 +76,25 @@ def f(d, k, default=float("nan")):
         return default
 
 
+def merge_json(path: Path, config: str, entry: dict) -> None:
+    """profiles/*.json hold one entry per config (bench.py never reads another config's)."""
+    data = {}
+    if path.exists():
+        try:
+            data = json.loads(path.read_text())
+        except ValueError:
+            data = {}
+    data = {k: v for k, v in data.items() if isinstance(v, dict)}  # drop the r1 flat layout
+    data[config] = entry
+    path.write_text(json.dumps(data, indent=1) + "\n")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--launches")
     ap.add_argument("--report")
+    ap.add_argument("--config", default="cfg1")
     a = ap.parse_args()
     PROF.mkdir(exist_ok=True)
     if a.launches:
@@ -109,9 +124,9 @@ def main() -> None:
                     continue
                 b += (sum(m.get("dram__bytes_read.sum", [0])) + sum(m.get("dram__bytes_write.sum", [0]))) / frames
             traffic[stage] = int(b)
-        (PROF / "traffic.json").write_text(json.dumps(
-            {"source": f"profiles/{a.tag}_launches.md (ncu dram__bytes_read.sum + dram__bytes_write.sum "
-                       "per frame, config 1)", **traffic}, indent=1) + "\n")
+        merge_json(PROF / "traffic.json", a.config, {
+            "source": f"profiles/{a.tag}_launches.md (ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                      f"per frame, {a.config})", **traffic})
     if a.report:
         rows, units = raw_report(Path(a.report))
         scale_to = {"us": {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3},
@@ -130,8 +145,8 @@ def main() -> None:
                 ("sm__warps_active.avg.per_cycle_active", "warps/SM", 1),
                 ("launch__registers_per_thread", "regs", 1),
                 ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "% fp64 pipe", 1)]
-        lines = [f"# {a.tag}: `ncu --set full --clock-control none` of every kernel of one config-1 "
-                 "frame (tools/profile_step.py, 5 cameras 640x480, 1.08M Gaussians)", "",
+        lines = [f"# {a.tag}: `ncu --set full --clock-control none` of every kernel of one {a.config} "
+                 "frame (tools/profile_step.py)", "",
                  "| kernel | " + " | ".join(f"{k.split('__')[-1][:28]} ({u})" for k, u, _ in keys) + " | top stalls |",
                  "|---|" + "---|" * (len(keys) + 1)]
         for d in rows:
@@ -150,9 +165,9 @@ def main() -> None:
         for stage, kernels in STAGES.items():
             inst[stage] = int(sum(f(d, "smsp__inst_executed.sum", 0.0) for d in rows
                                   if any(short(d.get("Kernel Name", "")).startswith(k) for k in kernels)))
-        (PROF / "instructions.json").write_text(json.dumps(
-            {"source": f"profiles/{a.tag}_frame.md (ncu smsp__inst_executed.sum per frame, config 1, "
-                       "one context)", **inst}, indent=1) + "\n")
+        merge_json(PROF / "instructions.json", a.config, {
+            "source": f"profiles/{a.tag}_frame.md (ncu smsp__inst_executed.sum per frame, {a.config}, "
+                      "one context)", **inst})
 
 
 if __name__ == "__main__":
