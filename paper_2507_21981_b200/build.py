@@ -32,6 +32,7 @@ SOURCES = {
     "ply.cu": ["-fmad=false"],
     "transfer.cu": ["-fmad=false"],
     "lidar.cu": ["-fmad=false"],
+    "bvh.cu": ["-fmad=false"],
     "host.cu": [],
 }
 DEPS = ["common.cuh", "kernels.hpp", "encode.cuh"]

@@ -1,0 +1,281 @@
+// bvh.cu — SURVEY.md 8f row 4: the acceleration structure for arbitrary LiDAR rays.
+//
+// The reference traces arbitrary rays through a SAH BVH over the posed 3-sigma boxes
+// (bvh.cpp:26-124, trace.cpp:113-123). The BVH only accelerates: a ray's candidate set is
+// exactly {i : ray_aabb_hit(box_i, ray)} (bvh.hpp:58-80, trace_linear is the contract), and the
+// tracer composites those candidates in (t, index) order. We build a linear BVH on the device
+// (Karras 2012) instead of a SAH tree:
+//   bvh_morton_kernel     30-bit Morton code of every seen box centre within the centres' bounds
+//                         (kInvalidKey for primitives no node shows the sensor: dropped)
+//   (segmented onesweep)  sort.cu sorts (code, primitive) pairs, 4 passes of 8-bit digits
+//   bvh_build_kernel      internal node i of the n-1: its key range by the delta function (code,
+//                         then primitive index, so duplicate codes still split) and split point
+//   bvh_refit_kernel      leaves upward: the second child to arrive at a node writes the union
+//                         of the children's boxes (exact fmin / fmax of doubles)
+//   bvh_collect_kernel    one thread per ray, stack traversal with the reference's slab test on
+//                         every node box; a leaf is a candidate iff ray_aabb_hit(its own box) —
+//                         count pass, then fill pass into the ray's list
+// A union box contains its children's boxes, and the slab test is monotone under containment
+// in floating point too ((lo - o) * inv rounds monotonically), so no hit box is ever pruned: the
+// lists equal the reference's candidate sets and lidar_trace_kernel composites them as for scans.
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace gsim_gpu {
+
+namespace {
+
+__device__ __forceinline__ uint64_t ordered_bits(double x) {  // monotone double -> u64
+    const uint64_t u = uint64_t(__double_as_longlong(x));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_ordered(uint64_t u) {
+    return __longlong_as_double((u >> 63) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u);
+}
+
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {  // 10 bits -> every third bit
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__device__ __forceinline__ bool slab_hit(double lx, double ly, double lz, double hx, double hy,
+                                         double hz, dv3 o, dv3 inv, double t_max) {
+    // bvh.hpp:20-36, the reference's slab test over [0, t_max]
+    double t0 = 0.0, t1 = t_max;
+    const double tx0 = (lx - o.x) * inv.x, tx1 = (hx - o.x) * inv.x;
+    t0 = fmax(t0, fmin(tx0, tx1));
+    t1 = fmin(t1, fmax(tx0, tx1));
+    const double ty0 = (ly - o.y) * inv.y, ty1 = (hy - o.y) * inv.y;
+    t0 = fmax(t0, fmin(ty0, ty1));
+    t1 = fmin(t1, fmax(ty0, ty1));
+    const double tz0 = (lz - o.z) * inv.z, tz1 = (hz - o.z) * inv.z;
+    t0 = fmax(t0, fmin(tz0, tz1));
+    t1 = fmin(t1, fmax(tz0, tz1));
+    return t0 <= t1;
+}
+
+}  // namespace
+
+// Centre bounds of the seen boxes: block min/max, then one atomic per block on ordered bits.
+__global__ void __launch_bounds__(256) bvh_bounds_kernel(BvhArgs a) {
+    __shared__ double s_v[6][8];
+    double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    const uint64_t n = a.n;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        if (!a.seen[i]) continue;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double c = 0.5 * (a.posed[(13 + k) * n + i] + a.posed[(16 + k) * n + i]);
+            v[k] = fmin(v[k], c);
+            v[3 + k] = fmax(v[3 + k], c);
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const double x = __shfl_xor_sync(0xffffffffu, v[k], o);
+            v[k] = k < 3 ? fmin(v[k], x) : fmax(v[k], x);
+        }
+        if (lane == 0) s_v[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        double r = s_v[k][0];
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) r = k < 3 ? fmin(r, s_v[k][w]) : fmax(r, s_v[k][w]);
+        if (k < 3) atomicMin(reinterpret_cast<unsigned long long*>(a.bounds_bits + k), ordered_bits(r));
+        else atomicMax(reinterpret_cast<unsigned long long*>(a.bounds_bits + k), ordered_bits(r));
+    }
+}
+
+__global__ void __launch_bounds__(256) bvh_morton_kernel(BvhArgs a) {
+    const uint64_t n = a.n;
+    double lo[3], ext[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = from_ordered(a.bounds_bits[k]);
+        const double e = from_ordered(a.bounds_bits[3 + k]) - lo[k];
+        ext[k] = e > 0.0 ? 1023.0 / e : 0.0;
+    }
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t key = kInvalidKey;
+        if (a.seen[i]) {
+            uint32_t q[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double c = 0.5 * (a.posed[(13 + k) * n + i] + a.posed[(16 + k) * n + i]);
+                const double f = (c - lo[k]) * ext[k];
+                q[k] = f <= 0.0 ? 0u : (f >= 1023.0 ? 1023u : uint32_t(f));
+            }
+            key = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
+        }
+        a.codes_in[i] = key;
+    }
+}
+
+// Sort bookkeeping for one segment: V = the valid keys (histogram of pass 1), the chunk tables
+// of the later passes.
+__global__ void bvh_sort_setup_kernel(BvhArgs a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t v = 0;
+    for (int d = 0; d < 256; ++d) v += a.hist[d];
+    a.vbase[0] = 0;
+    a.vbase[1] = v;
+    a.chunk_base1[0] = 0;
+    a.chunk_base1[1] = (v + uint32_t(kOnesweepTile) - 1) / uint32_t(kOnesweepTile);
+    *a.n_leaves = v;
+}
+
+namespace {
+// delta(i, j) of Karras 2012 over the sorted codes, ties broken by position.
+__device__ __forceinline__ int delta(const uint32_t* codes, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    const uint32_t ci = codes[i], cj = codes[j];
+    if (ci != cj) return __clz(ci ^ cj);
+    return 32 + __clz(uint32_t(i) ^ uint32_t(j));
+}
+}  // namespace
+
+// Internal nodes 0 .. n-2 (node 0 is the root); children >= kLeafBit are leaves (sorted index).
+__global__ void __launch_bounds__(256) bvh_build_kernel(BvhArgs a) {
+    const int n = int(*a.n_leaves);
+    const uint32_t* codes = a.codes_sorted;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+        const int d = (delta(codes, n, i, i + 1) - delta(codes, n, i, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = delta(codes, n, i, i - d);
+        int lmax = 2;
+        while (delta(codes, n, i, i + lmax * d) > dmin) lmax <<= 1;
+        int l = 0;
+        for (int t = lmax >> 1; t >= 1; t >>= 1)
+            if (delta(codes, n, i, i + (l + t) * d) > dmin) l += t;
+        const int j = i + l * d;
+        const int dnode = delta(codes, n, i, j);
+        int s = 0;
+        for (int t = (l + 1) >> 1;; t = (t + 1) >> 1) {
+            if (delta(codes, n, i, i + (s + t) * d) > dnode) s += t;
+            if (t == 1) break;
+        }
+        const int gamma = i + s * d + (d < 0 ? -1 : 0);
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        const uint32_t left = lo == gamma ? (kLeafBit | uint32_t(gamma)) : uint32_t(gamma);
+        const uint32_t right = hi == gamma + 1 ? (kLeafBit | uint32_t(gamma + 1)) : uint32_t(gamma + 1);
+        a.child[2 * i] = left;
+        a.child[2 * i + 1] = right;
+        if (left & kLeafBit) a.leaf_parent[gamma] = uint32_t(i);
+        else a.node_parent[gamma] = uint32_t(i);
+        if (right & kLeafBit) a.leaf_parent[gamma + 1] = uint32_t(i);
+        else a.node_parent[gamma + 1] = uint32_t(i);
+        a.visits[i] = 0u;
+    }
+}
+
+// Boxes upward from the leaves: node boxes [node][6] = lo xyz, hi xyz (doubles).
+__global__ void __launch_bounds__(256) bvh_refit_kernel(BvhArgs a) {
+    const int n = int(*a.n_leaves);
+    const uint64_t np = a.n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        if (n == 1) break;
+        uint32_t node = a.leaf_parent[k];
+        while (true) {
+            __threadfence();
+            if (atomicAdd(a.visits + node, 1u) == 0u) break;  // the sibling finishes this node
+            __threadfence();
+            double b[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) b[q] = q < 3 ? INFINITY : -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const uint32_t ch = a.child[2 * node + c];
+                double cb[6];
+                if (ch & kLeafBit) {
+                    const uint32_t prim = a.leaf_prim[ch & ~kLeafBit];
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) cb[q] = a.posed[(13 + q) * np + prim];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) cb[q] = __ldcg(a.node_box + 6 * uint64_t(ch) + q);
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    b[q] = fmin(b[q], cb[q]);
+                    b[3 + q] = fmax(b[3 + q], cb[3 + q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) __stcg(a.node_box + 6 * uint64_t(node) + q, b[q]);
+            if (node == 0) break;
+            node = a.node_parent[node];
+        }
+    }
+}
+
+// Candidates of every ray: count (list == nullptr) or fill (list at ray_offset[ray]).
+__global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const LidarArgs la, int fill) {
+    const int n = int(*a.n_leaves);
+    const uint64_t np = a.n;
+    for (uint64_t ray = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; ray < la.n_rays;
+         ray += uint64_t(gridDim.x) * blockDim.x) {
+        const dv3 o = mk3(la.ray_origin[3 * ray], la.ray_origin[3 * ray + 1], la.ray_origin[3 * ray + 2]);
+        const dv3 d = mk3(la.ray_dir[3 * ray], la.ray_dir[3 * ray + 1], la.ray_dir[3 * ray + 2]);
+        const dv3 inv = mk3(1.0 / d.x, 1.0 / d.y, 1.0 / d.z);
+        const double t_max = la.ray_tmax[ray];
+        uint32_t count = 0;
+        uint32_t* out = fill ? la.list + la.ray_offset[ray] : nullptr;
+        auto leaf = [&](uint32_t sorted_idx) {
+            const uint32_t prim = a.leaf_prim[sorted_idx];
+            if (slab_hit(a.posed[13 * np + prim], a.posed[14 * np + prim], a.posed[15 * np + prim],
+                         a.posed[16 * np + prim], a.posed[17 * np + prim], a.posed[18 * np + prim],
+                         o, inv, t_max)) {
+                if (out) out[count] = prim;
+                ++count;
+            }
+        };
+        if (n == 1) {
+            leaf(0);
+        } else if (n > 1) {
+            uint32_t stack[64];
+            int sp = 0;
+            stack[sp++] = 0u;
+            while (sp > 0) {
+                const uint32_t node = stack[--sp];
+                const double* b = a.node_box + 6 * uint64_t(node);
+                if (!slab_hit(b[0], b[1], b[2], b[3], b[4], b[5], o, inv, t_max)) continue;
+                const uint32_t l = a.child[2 * node], r = a.child[2 * node + 1];
+                if (r & kLeafBit) leaf(r & ~kLeafBit); else stack[sp++] = r;
+                if (l & kLeafBit) leaf(l & ~kLeafBit); else stack[sp++] = l;
+                GSIM_DCHECK(sp <= 64);
+            }
+        }
+        if (!fill) la.ray_count[ray] = count;
+    }
+}
+
+void launch_bvh_bounds(const BvhArgs& a, int n_sms, cudaStream_t s) {
+    bvh_bounds_kernel<<<unsigned(n_sms * 4), 256, 0, s>>>(a);
+}
+void launch_bvh_morton(const BvhArgs& a, int n_sms, cudaStream_t s) {
+    bvh_morton_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
+}
+void launch_bvh_sort_setup(const BvhArgs& a, cudaStream_t s) { bvh_sort_setup_kernel<<<1, 32, 0, s>>>(a); }
+void launch_bvh_build(const BvhArgs& a, int n_sms, cudaStream_t s) {
+    bvh_build_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
+}
+void launch_bvh_refit(const BvhArgs& a, int n_sms, cudaStream_t s) {
+    bvh_refit_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
+}
+void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, bool fill, int n_sms, cudaStream_t s) {
+    const uint64_t want = (la.n_rays + 127) / 128;
+    bvh_collect_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(n_sms) * 16))),
+                         128, 0, s>>>(a, la, fill ? 1 : 0);
+}
+
+}  // namespace gsim_gpu

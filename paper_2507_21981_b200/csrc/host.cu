@@ -223,8 +223,16 @@ struct gsim_gpu_context {
         DevBuf<int> diff;
         DevBuf<unsigned long long> offsets, scratch, hit_offsets;
         DevBuf<DevSegment> segs;
+        // arbitrary rays: linear BVH (bvh.cu)
+        DevBuf<uint32_t> bvh_keys[2], bvh_vals[2], bvh_small, bvh_nodes;
+        DevBuf<uint64_t> bvh_seg;
+        DevBuf<unsigned long long> bvh_bounds;
+        DevBuf<double> bvh_box;
         std::vector<double> ray_key;  // (channels, step) of the sensor directions in rays
         void release() {
+            for (int k = 0; k < 2; ++k) { bvh_keys[k].release(); bvh_vals[k].release(); }
+            bvh_small.release(); bvh_nodes.release(); bvh_seg.release(); bvh_bounds.release();
+            bvh_box.release();
             posed.release(); rays.release(); depth.release(); acc.release(); points.release();
             azimuth.release(); rank_elev.release(); seen.release(); ray_all.release();
             cand_t.release(); cand_r.release();
@@ -1564,6 +1572,132 @@ LidarArgs lidar_pose_stage(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, c
     return a;
 }
 
+// Linear BVH over the posed boxes of `a` (bvh.cu) and the candidate list of every arbitrary
+// ray (la.ray_origin / ray_dir / ray_tmax set): la.list / ray_offset / cand_t / cand_r filled,
+// la.ray_lists = 1. Returns the total number of candidates.
+uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
+    auto& L = ctx->lidar;
+    cudaStream_t s = ctx->stream;
+    const uint64_t n = la.n;
+    const int n_sms = ctx->num_sms;
+    if (n >= (uint64_t(1) << 31)) throw ValidationError{"trace_rays: field too large for the BVH"};
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    for (int k = 0; k < 2; ++k) {
+        L.bvh_keys[k].reserve(nn);
+        L.bvh_vals[k].reserve(nn);
+    }
+    // small tables: [0..1023] hist (4 x 256), tickets [1024..1031], vbase [1040..1041],
+    // chunk_base0 [1044..1045], chunk_base1 [1048..1049], n_leaves [1052], cam_visible [1056]
+    L.bvh_small.reserve(1088);
+    uint32_t* sm = L.bvh_small.ptr;
+    L.bvh_nodes.reserve(5 * nn);  // child 2(n-1), node_parent n-1, leaf_parent n, visits n-1
+    L.bvh_box.reserve(6 * nn);
+    L.bvh_seg.reserve(2);
+    L.bvh_bounds.reserve(6);
+    const uint32_t chunks0 = uint32_t((n + kOnesweepTile - 1) / kOnesweepTile);
+    const uint64_t seg_host[2] = {0, n};
+    const uint32_t cb0_host[2] = {0, chunks0};
+    GSIM_CK(cudaMemsetAsync(sm, 0, 1088 * sizeof(uint32_t), s));
+    GSIM_CK(cudaMemcpyAsync(L.bvh_seg.ptr, seg_host, sizeof(seg_host), cudaMemcpyHostToDevice, s));
+    GSIM_CK(cudaMemcpyAsync(sm + 1044, cb0_host, sizeof(cb0_host), cudaMemcpyHostToDevice, s));
+    const unsigned long long init_bits[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+    GSIM_CK(cudaMemcpyAsync(L.bvh_bounds.ptr, init_bits, sizeof(init_bits), cudaMemcpyHostToDevice, s));
+    const uint64_t words = (uint64_t(chunks0) + 1) * 256;
+    if (words > ctx->status.cap) {
+        ctx->status.reserve(words);
+        GSIM_CK(cudaMemsetAsync(ctx->status.ptr, 0, ctx->status.cap * sizeof(uint64_t), s));
+    }
+    BvhArgs b{};
+    b.n = n;
+    b.posed = la.posed;
+    b.seen = la.seen;
+    b.bounds_bits = L.bvh_bounds.ptr;
+    b.codes_in = L.bvh_keys[0].ptr;  // sorted into bvh_keys[1] / bvh_vals[1] after 4 passes
+    b.hist = sm;
+    b.vbase = sm + 1040;
+    b.chunk_base1 = sm + 1048;
+    b.n_leaves = sm + 1052;
+    b.child = L.bvh_nodes.ptr;
+    b.node_parent = L.bvh_nodes.ptr + 2 * nn;
+    b.leaf_parent = L.bvh_nodes.ptr + 3 * nn;
+    b.visits = L.bvh_nodes.ptr + 4 * nn;
+    b.node_box = L.bvh_box.ptr;
+    launch_bvh_bounds(b, n_sms, s);
+    launch_bvh_morton(b, n_sms, s);
+    check_launch();
+    // (code, primitive) sort: the render path's segmented onesweep with one segment
+    BinArgs hb{};
+    hb.keys = b.codes_in;
+    hb.n_slots = n;
+    hb.cam_slot_base = L.bvh_seg.ptr;
+    hb.sort_bits = 8;
+    hb.sort_passes = 4;
+    hb.n_cams = 1;
+    hb.hist = sm;
+    hb.cam_visible = sm + 1056;
+    launch_key_hist(hb, n_sms * 2, s);
+    launch_bvh_sort_setup(b, s);
+    check_launch();
+    OnesweepArgs oa{};
+    oa.status = ctx->status.ptr;
+    oa.n_cams = 1;
+    oa.vbase = b.vbase;
+    oa.hist_stride = 4 * 256;
+    oa.seg_base64 = L.bvh_seg.ptr;
+    oa.seg_base32 = b.vbase;
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(chunks0 + 1, uint64_t(n_sms) * 3)));
+    const uint32_t* kin = b.codes_in;
+    const uint32_t* vin = nullptr;
+    const int out_of[4] = {1, 0, 1, 0};  // codes_in is bvh_keys[0]: pass 1 writes buffer 1
+    for (int pass = 0; pass < 4; ++pass) {
+        const int o = out_of[pass];
+        oa.keys_in = kin;
+        oa.vals_in = vin;
+        oa.keys_out = L.bvh_keys[o].ptr;
+        oa.vals_out = L.bvh_vals[o].ptr;
+        oa.chunk_base = pass == 0 ? sm + 1044 : b.chunk_base1;
+        oa.hist = sm + 256 * pass;
+        oa.ticket = sm + 1024 + pass;
+        oa.epoch = ctx->next_epoch();
+        oa.shift = 8 * pass;
+        launch_onesweep(oa, 8, pass == 0, true, grid, s);
+        check_launch();
+        kin = L.bvh_keys[o].ptr;
+        vin = L.bvh_vals[o].ptr;
+    }
+    b.codes_sorted = kin;
+    b.leaf_prim = vin;
+    launch_bvh_build(b, n_sms, s);
+    launch_bvh_refit(b, n_sms, s);
+    check_launch();
+    // candidate lists: count, scan, fill
+    const uint64_t R = la.n_rays;
+    L.counts.reserve(std::max<uint64_t>(R, 1));
+    L.offsets.reserve(R + 1);
+    L.scratch.reserve((R + 1023) / 1024 + 2);
+    la.ray_count = L.counts.ptr;
+    launch_bvh_collect(b, la, false, n_sms, s);
+    check_launch();
+    exclusive_scan_u32(L.counts.ptr, R, L.offsets.ptr, L.scratch.ptr, s);
+    check_launch();
+    unsigned long long total = 0;
+    GSIM_CK(cudaMemcpyAsync(&total, L.offsets.ptr + R, sizeof(total), cudaMemcpyDeviceToHost, s));
+    GSIM_CK(cudaStreamSynchronize(s));
+    if (total >= (1ull << 32)) throw CudaError{"trace_rays: more than 2^32 ray candidates"};
+    L.list.reserve(std::max<unsigned long long>(total, 1));
+    L.cand_t.reserve(std::max<unsigned long long>(total, 1));
+    L.cand_r.reserve(std::max<unsigned long long>(total, 1));
+    la.ray_offset = L.offsets.ptr;
+    la.list = L.list.ptr;
+    la.cand_t = L.cand_t.ptr;
+    la.cand_r = L.cand_r.ptr;
+    launch_bvh_collect(b, la, true, n_sms, s);
+    check_launch();
+    la.ray_lists = 1;
+    ctx->launches_total += 14;
+    return total;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2792,6 +2926,12 @@ int gsim_gpu_trace_rays(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, cons
         a.alpha_threshold = alpha_threshold;
         launch_lidar_pose(a, ctx->num_sms, s);
         check_launch();
+        // GSIM_GPU_TRACE_BRUTE=1: every primitive is every ray's candidate (A/B and tests)
+        static const bool brute = [] {
+            const char* e = std::getenv("GSIM_GPU_TRACE_BRUTE");
+            return e && std::atoi(e) == 1;
+        }();
+        if (!brute && scene->f.n) ctx->stats.pairs = bvh_ray_lists(ctx, a);
         L.hit.reserve(n_rays);
         L.depth.reserve(n_rays);
         L.acc.reserve(n_rays);

@@ -228,7 +228,9 @@ struct LidarArgs {
     DevField field;
     const DevSegment* segs;          // painted node ranges; entry_count 0 = not seen
     int n_segs;
-    int scan;                        // 1: LiDAR grid scan, 0: arbitrary rays, every primitive
+    int scan;                        // 1: LiDAR grid scan, 0: arbitrary rays
+    int ray_lists;                   // arbitrary rays: candidates in list/ray_offset (BVH), else
+                                     // every primitive is a candidate
     uint64_t n;                      // primitives
     double* posed;                   // [19][n]: mean xyz, inv_cov 9, opacity, lo xyz, hi xyz
     uint8_t* seen;                   // [n]
@@ -268,6 +270,34 @@ struct LidarArgs {
     double* cand_r;                  //   all_count] (ray region at offset + ray * all_count)
     unsigned long long* debug;       // optional counters: rays, candidates
 };
+
+// Linear BVH over the posed boxes for arbitrary rays (bvh.cu).
+constexpr uint32_t kLeafBit = 0x80000000u;
+struct BvhArgs {
+    uint64_t n;                      // primitives (LidarArgs::n)
+    const double* posed;             // LidarArgs::posed ([19][n]: boxes in planes 13..18)
+    const uint8_t* seen;
+    unsigned long long* bounds_bits; // [6] ordered bits of the centre bounds (min xyz, max xyz)
+    uint32_t* codes_in;              // [n] Morton codes (kInvalidKey: not seen)
+    const uint32_t* codes_sorted;    // [n_leaves] sorted codes
+    const uint32_t* leaf_prim;       // [n_leaves] primitive of sorted leaf k
+    const uint32_t* hist;            // [4][256] digit histograms of the codes
+    uint32_t* vbase;                 // [2] sort output segment
+    uint32_t* chunk_base1;           // [2] chunks of passes >= 2
+    uint32_t* n_leaves;              // [1]
+    uint32_t* child;                 // [n - 1][2]: internal node or kLeafBit | sorted leaf
+    uint32_t* node_parent;           // [n - 1]
+    uint32_t* leaf_parent;           // [n]
+    uint32_t* visits;                // [n - 1] refit arrivals
+    double* node_box;                // [n - 1][6]
+};
+
+void launch_bvh_bounds(const BvhArgs& a, int n_sms, cudaStream_t s);
+void launch_bvh_morton(const BvhArgs& a, int n_sms, cudaStream_t s);
+void launch_bvh_sort_setup(const BvhArgs& a, cudaStream_t s);
+void launch_bvh_build(const BvhArgs& a, int n_sms, cudaStream_t s);
+void launch_bvh_refit(const BvhArgs& a, int n_sms, cudaStream_t s);
+void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, bool fill, int n_sms, cudaStream_t s);
 
 void launch_lidar_pose(const LidarArgs& a, int n_sms, cudaStream_t s);
 void launch_lidar_rays(const double* ds, double* dw, uint64_t n, const double* q, int n_sms,

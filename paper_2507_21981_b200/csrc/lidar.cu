@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps) lidar_trace_kernel(LidarArgs
         const double t_max = a.scan ? a.max_range : a.ray_tmax[ray];
         const dv3 inv = mk3(1.0 / d.x, 1.0 / d.y, 1.0 / d.z);
         RayCands cs{};
-        const bool brute = !a.scan || a.ray_all[ray / a.n_az];
+        const bool brute = a.scan ? a.ray_all[ray / a.n_az] != 0 : a.ray_lists == 0;
         if (!brute) {
             const uint64_t b = a.ray_offset[ray];
             cs.list = a.list + b;

@@ -110,3 +110,63 @@ def test_scan_dense_windows(ctx, oracle):
     got = ctx.lidar_scan(ctx.upload(f), [], lid)
     assert_scan_close(got, oracle.lidar_scan(f, [], lid))
     assert len(got["ring"]) > 0
+
+
+def test_trace_rays_bvh_larger_scene(ctx, oracle):
+    """Arbitrary rays through the linear BVH (bvh.cu) on 60k primitives with posed nodes: rays
+    from inside and outside the cloud, axis-aligned directions (zero components: infinite slab
+    reciprocals), a ray along a box face, short and long t_max. Same results as the reference's
+    tracer (trace_linear semantics: the candidate set is every box the ray hits)."""
+    f = oracle.random_field(77, 60000, 2.5, 0.005, 0.12, 1)
+    nodes = two_nodes(60000)
+    rng = np.random.default_rng(11)
+    n = 2500
+    org = rng.uniform(-3.5, 3.5, (n, 3))
+    d = rng.normal(size=(n, 3))
+    d[:40] = 0.0
+    d[np.arange(40), np.arange(40) % 3] = np.where(np.arange(40) % 2 == 0, 1.0, -1.0)
+    d[40:60, 2] = 0.0
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    tmax = rng.uniform(0.2, 12.0, n)
+    tmax[:100] = 100.0
+    g = ctx.trace_rays(ctx.upload(f), nodes, org, d, tmax, 0.3)
+    cand = ctx.stats()["pairs"]
+    r = oracle.trace_rays(f, nodes, org, d, tmax, 0.3)
+    assert np.array_equal(g[0], r[0])
+    assert np.abs(g[1] - r[1]).max() <= TOL and np.abs(g[2] - r[2]).max() <= TOL
+    assert cand > 10 * n  # the BVH produced candidate lists (not the every-primitive path)
+
+
+BRUTE_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from oracle.oracle import Oracle
+from paper_2507_21981_b200 import Context
+orc = Oracle()
+f = orc.random_field(78, 20000, 2.0, 0.01, 0.15, 0)
+rng = np.random.default_rng(5)
+org = rng.uniform(-3, 3, (1500, 3)); d = rng.normal(size=(1500, 3))
+d /= np.linalg.norm(d, axis=1, keepdims=True); t = rng.uniform(0.5, 9.0, 1500)
+ctx = Context(0)
+hit, dep, acc = ctx.trace_rays(ctx.upload(f), [], org, d, t, 0.4)
+np.save(sys.argv[1], np.concatenate([hit.astype(np.float64), dep, acc]))
+"""
+
+
+def test_trace_rays_bvh_equals_every_primitive(tmp_path):
+    """The BVH candidate lists and the every-primitive path (GSIM_GPU_TRACE_BRUTE=1) composite
+    the same survivors in the same (t, index) order: bit-identical results."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    outs = []
+    for brute in ("0", "1"):
+        p = tmp_path / f"r{brute}.npy"
+        env = dict(os.environ, GSIM_GPU_TRACE_BRUTE=brute)
+        r = subprocess.run([sys.executable, "-c", BRUTE_SCRIPT.format(root=root), str(p)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(p))
+    assert np.array_equal(outs[0], outs[1])

@@ -29,6 +29,8 @@ ap.add_argument("--channels", type=int, default=32)
 ap.add_argument("--step-deg", type=float, default=0.2)
 ap.add_argument("--cpu-channels", type=int, default=1)
 ap.add_argument("--no-cpu", action="store_true")
+ap.add_argument("--trace", type=int, default=0,
+                help="also time N arbitrary rays through gsim_gpu_trace_rays (linear BVH)")
 a = ap.parse_args()
 
 w = CONFIGS["cfg1"](seed=1000)
@@ -60,4 +62,35 @@ if not a.no_cpu:
     line["cpu_reference"] = {"threads": os.cpu_count(), "sample_rays": a.cpu_channels * lid.azimuth_count(),
                              "sample_s": round(cpu_s, 2), "scans_per_s_extrapolated": round(1.0 / (per_ray * rays), 4),
                              "note": "includes one BVH build per sample (the reference rebuilds per scan)"}
+if a.trace:
+    # arbitrary rays (trace.cpp:113-123 per ray): origins in and around the cloud, random
+    # directions, t_max 100 m; each call builds the BVH over the 1.08M posed boxes
+    rng = np.random.default_rng(9)
+    org = rng.uniform(-3.0, 3.0, (a.trace, 3))
+    dirs = rng.normal(size=(a.trace, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    tmax = np.full(a.trace, 100.0)
+    ctx.trace_rays(scene, nodes, org, dirs, tmax, 0.5)  # warm-up
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        hit, _, _ = ctx.trace_rays(scene, nodes, org, dirs, tmax, 0.5)
+    gpu_t = (time.perf_counter() - t0) / reps
+    line["trace_rays"] = {"rays": a.trace, "gpu_ms_per_call": round(gpu_t * 1e3, 2),
+                          "gpu_rays_per_s": round(a.trace / gpu_t, 1),
+                          "candidates_per_ray": round(ctx.stats()["pairs"] / a.trace, 1),
+                          "hits": int(hit.sum()), "note": "BVH build + traversal + trace per call"}
+    if not a.no_cpu:
+        from oracle.oracle import Ref
+        ref = Ref()
+        import os
+        ref.set_threads(os.cpu_count() or 1)
+        k = min(a.trace, 2000)
+        t0 = time.perf_counter()
+        ref.trace_rays(w.field, nodes, org[:k], dirs[:k], tmax[:k], 0.5)  # BVH build + trace
+        cpu_t = time.perf_counter() - t0
+        line["trace_rays"]["cpu_reference"] = {"threads": os.cpu_count(), "sample_rays": k,
+                                               "sample_s": round(cpu_t, 2),
+                                               "rays_per_s": round(k / cpu_t, 1),
+                                               "note": "GaussianBvh::build + trace (SAH BVH)"}
 print(json.dumps(line))
