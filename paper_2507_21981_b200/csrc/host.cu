@@ -9,7 +9,7 @@
 //   validate_field sh_degree gaussian.cpp:15-17
 //
 // Frame pipeline (all on the context stream, no host round trip before the raster):
-//   K2 preprocess -> key_hist -> chunk_table -> 4 x onesweep (camera | depth)
+//   K2 preprocess -> key_hist -> chunk_table -> 4 x segmented onesweep (depth within camera)
 //   -> bin_count -> bin_colscan -> bin_tilescan -> bin_campre -> bin_scatter -> K4 raster
 // The host waits only for the small (V, P) readback behind bin_campre, while the GPU runs the
 // scatter and the raster, to catch a pair-buffer overflow (then it grows and re-runs the tail).
