@@ -247,17 +247,20 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
 #pragma unroll
         for (int h = 0; h < kPerThread; ++h) {
             const uint32_t i = b + uint32_t(tid + h * kThreads);
-            uint32_t sl = i < end ? __ldg(a.values + i) : 0xFFFFFFFFu;
-            // a stale slot is only possible in a clamped (overflowed) frame
-            GSIM_DCHECK(!(i < end && e64 <= a.capacity) || sl < a.n_slots);
-            if (i < end && sl >= a.n_slots) sl = 0;
-            slot_next[h] = sl;
+            // in flight while the current batch blends: checked only when the copy is issued
+            slot_next[h] = i < end ? __ldg(a.values + i) : 0xFFFFFFFFu;
         }
     };
     const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&s_bar[0]));
     uint32_t phase_bits = 0;   // kBulk: parity of the next phase of each buffer's barrier
     uint32_t pending_bulk = 0; // kBulk: buffers with copies issued and not yet waited for
     auto issue_copy = [&](int buf) {
+#pragma unroll
+        for (int h = 0; h < kPerThread; ++h) {
+            // a stale slot is only possible in a clamped (overflowed) frame
+            GSIM_DCHECK(slot_next[h] == 0xFFFFFFFFu || e64 > a.capacity || slot_next[h] < a.n_slots);
+            if (slot_next[h] != 0xFFFFFFFFu && slot_next[h] >= a.n_slots) slot_next[h] = 0;
+        }
         if constexpr (kBulk) {
             // every thread arrives once per phase, announcing the bytes of its own copies first
             uint32_t bytes = 0;
