@@ -12,8 +12,10 @@ poses, rendered by 5 cameras at 640x480 into RGB + depth + accumulated alpha). U
 every rank renders its own environment's frame (weak scaling, no data-path collective).
 cfg4 (BASELINE config 4): a step is the whole 512-environment x 5-camera batch, split over the
 ranks by environment; every rank renders its environments in chunks of <= 64 (config-2-sized
-launches) and the frames of chunk j go to rank 0 with grouped NCCL point-to-point while chunk
-j+1 renders (shard.ChunkGather); value is box-wide camera-frames/s (strong scaling).
+launches) straight into rank 0's gathered output over NVLink peer memory (--gather p2p, the
+default: the compositing kernel's epilogue is the gather), or sends chunk j to rank 0 with grouped
+NCCL point-to-point while chunk j+1 renders (--gather nccl); shard.ChunkGather. value is box-wide
+camera-frames/s (strong scaling).
 The timed region is bracketed by a barrier + synchronize on both sides and the elapsed device
 time (CUDA events on the renderer's stream) is the max over ranks.
 
@@ -472,7 +474,8 @@ def run_cfg4(args, rank, world, local, dist):
     px_per_env = sum(c.width * c.height for c in r.cameras[:cams_per_env])
     fpe = 5 * px_per_env
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    gather = ChunkGather(n_envs, fpe, args.chunk_envs, dev, rank=rank, world=world, dst=0)
+    gather = ChunkGather(n_envs, fpe, args.chunk_envs, dev, rank=rank, world=world, dst=0,
+                         mode=args.gather)
     chunk_cams = [r.camera_table(cb, ce) for cb, ce in gather.my_chunks]
 
     def step(i, sums=None):
@@ -546,8 +549,10 @@ def run_cfg4(args, rank, world, local, dist):
                                    "background replica per GPU + each env's 4x20k objects",
                        "envs_per_rank": e - b, "chunk_envs": args.chunk_envs,
                        "gaussians_per_rank": r.scene.size,
-                       "parallelism": f"env-sharded x{world}, frames gathered to rank 0 "
-                                      "(grouped NCCL P2P, overlapped with the next chunk)",
+                       "parallelism": f"env-sharded x{world}, frames gathered to rank 0 " + (
+                           "(fused: the compositing kernels store into rank 0's HBM over NVLink "
+                           "peer memory)" if args.gather == "p2p" else
+                           "(grouped NCCL P2P, overlapped with the next chunk)"),
                        "gather_bytes_per_step": int(gather.bytes_to_dst * 4),
                        "l2": "inputs larger than L2; no flush", "seed": 1000},
             "gpu_launches": int(launches),
@@ -696,6 +701,9 @@ def main():
                     help="renderer contexts taking frames in turn (frame-level overlap)")
     ap.add_argument("--envs", type=int, default=512, help="cfg4: environments per step (box-wide)")
     ap.add_argument("--chunk-envs", type=int, default=64, help="cfg4: environments per launch")
+    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
+                    help="cfg4, N > 1: frames stored into rank 0's HBM by the compositing kernels "
+                         "over peer memory (p2p) or sent after each chunk with NCCL (nccl)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

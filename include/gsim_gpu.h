@@ -221,6 +221,16 @@ int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
 /* Device pointer of the internal output buffer of the last render_device(NULL) call. */
 float* gsim_gpu_device_output(gsim_gpu_context* ctx);
 
+/* Peer memory for BASELINE config 4's fused frame gather: rank 0 allocates the gathered output
+ * and exports it (CUDA IPC handle, 64 bytes); every other rank of the node opens the handle and
+ * passes pointers into it as gsim_gpu_render_device's device_out, so the compositing kernel's
+ * epilogue stores its pixels straight into rank 0's HBM over NVLink (no separate collective).
+ * Host-side plumbing only (cudaMalloc / cudaIpcGetMemHandle / cudaIpcOpenMemHandle). */
+int gsim_gpu_ipc_alloc(int32_t device, uint64_t bytes, void** ptr, uint8_t handle[64]);
+int gsim_gpu_ipc_free(int32_t device, void* ptr);
+int gsim_gpu_ipc_open(int32_t device, const uint8_t handle[64], void** ptr);
+int gsim_gpu_ipc_close(int32_t device, void* ptr);
+
 /* Sorted tile lists of one camera of the last render/rasterize on ctx (test hook for the
  * reference's pair sort, raster.cpp:174-202): tile_begin gets tiles_x*tiles_y+1 offsets,
  * values gets the primitive index (render) or splat index (rasterize) of each pair in

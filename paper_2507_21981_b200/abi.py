@@ -123,6 +123,10 @@ SIGNATURES = [
     ("gsim_gpu_scene_upload", C.c_int, [_P, C.POINTER(gsim_field_view), C.POINTER(_P)]),
     ("gsim_gpu_scene_destroy", C.c_int, [_P]),
     ("gsim_gpu_scene_create", C.c_int, [_P, C.c_uint64, C.c_int32, C.POINTER(_P)]),
+    ("gsim_gpu_ipc_alloc", C.c_int, [C.c_int32, C.c_uint64, C.POINTER(_P), C.POINTER(C.c_uint8)]),
+    ("gsim_gpu_ipc_free", C.c_int, [C.c_int32, _P]),
+    ("gsim_gpu_ipc_open", C.c_int, [C.c_int32, C.POINTER(C.c_uint8), C.POINTER(_P)]),
+    ("gsim_gpu_ipc_close", C.c_int, [C.c_int32, _P]),
     ("gsim_gpu_scene_write", C.c_int, [_P, _P, C.c_uint64, C.POINTER(gsim_field_view)]),
     ("gsim_gpu_scene_size", C.c_uint64, [_P]),
     ("gsim_gpu_transform_primitives", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(gsim_rigid)]),

@@ -2151,6 +2151,46 @@ int gsim_gpu_render_device(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
 
 float* gsim_gpu_device_output(gsim_gpu_context* ctx) { return ctx ? ctx->out.ptr : nullptr; }
 
+// ---- peer memory (config 4 fused gather) ------------------------------------------------------
+int gsim_gpu_ipc_alloc(int32_t device, uint64_t bytes, void** ptr, uint8_t handle[64]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+    if (!ptr || !handle || bytes == 0) return GSIM_ERR_VALIDATION;
+    *ptr = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return GSIM_ERR_IO;
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return GSIM_ERR_IO;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return GSIM_ERR_IO;
+    }
+    std::memcpy(handle, &h, 64);
+    *ptr = p;
+    return GSIM_OK;
+}
+
+int gsim_gpu_ipc_free(int32_t device, void* ptr) {
+    if (!ptr) return GSIM_OK;
+    if (cudaSetDevice(device) != cudaSuccess) return GSIM_ERR_IO;
+    return cudaFree(ptr) == cudaSuccess ? GSIM_OK : GSIM_ERR_IO;
+}
+
+int gsim_gpu_ipc_open(int32_t device, const uint8_t handle[64], void** ptr) {
+    if (!ptr || !handle) return GSIM_ERR_VALIDATION;
+    *ptr = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return GSIM_ERR_IO;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    return cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? GSIM_OK
+                                                                                       : GSIM_ERR_IO;
+}
+
+int gsim_gpu_ipc_close(int32_t device, void* ptr) {
+    if (!ptr) return GSIM_OK;
+    if (cudaSetDevice(device) != cudaSuccess) return GSIM_ERR_IO;
+    return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? GSIM_OK : GSIM_ERR_IO;
+}
+
 int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gsim_node* nodes,
                     uint64_t n_nodes, const gsim_camera* cameras, uint64_t n_cameras,
                     const gsim_raster_options* options, gsim_target* outs) {

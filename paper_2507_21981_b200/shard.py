@@ -46,6 +46,57 @@ def gather_frames(frames: torch.Tensor, n_envs: int, floats_per_env: int, dst: i
     return out
 
 
+class _CudaArray:
+    """A raw device range seen through __cuda_array_interface__ (torch.as_tensor views it)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, n_floats: int, device) -> torch.Tensor:
+    return torch.as_tensor(_CudaArray(ptr, n_floats), device=device)
+
+
+class PeerBuffer:
+    """Rank `dst`'s gathered output in peer memory (gsim_gpu_ipc_*): dst allocates and exports it,
+    every other rank of the node opens it, so their renders can store straight into it."""
+
+    def __init__(self, n_floats: int, device, rank: int, world: int, dst: int = 0):
+        import ctypes as C
+        from . import abi
+        self.lib = abi.load_library()
+        self.dev_index = device.index if isinstance(device, torch.device) else int(device)
+        self.owner = rank == dst
+        ptr = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        if self.owner:
+            st = self.lib.gsim_gpu_ipc_alloc(self.dev_index, 4 * n_floats, C.byref(ptr), handle)
+            if st != abi.GSIM_OK:
+                raise RuntimeError("gsim_gpu_ipc_alloc failed")
+        msg = [bytes(handle) if self.owner else None]
+        if world > 1:
+            dist.broadcast_object_list(msg, src=dst)
+        if not self.owner:
+            h = (C.c_uint8 * 64).from_buffer_copy(msg[0])
+            st = self.lib.gsim_gpu_ipc_open(self.dev_index, h, C.byref(ptr))
+            if st != abi.GSIM_OK:
+                raise RuntimeError("gsim_gpu_ipc_open failed (peer access between the ranks' GPUs?)")
+        self.ptr = int(ptr.value)
+        self.n = n_floats
+
+    def view(self, first: int, count: int, device) -> torch.Tensor:
+        return device_view(self.ptr + 4 * first, count, device)
+
+    def close(self) -> None:
+        if self.ptr:
+            if self.owner:
+                self.lib.gsim_gpu_ipc_free(self.dev_index, self.ptr)
+            else:
+                self.lib.gsim_gpu_ipc_close(self.dev_index, self.ptr)
+            self.ptr = 0
+
+
 class ChunkGather:
     """BASELINE config 4's frame gather, overlapped with rendering.
 
@@ -60,7 +111,8 @@ class ChunkGather:
     """
 
     def __init__(self, n_envs: int, floats_per_env: int, chunk_envs: int, device, rank: int | None = None,
-                 world: int | None = None, dst: int = 0, n_buffers: int = 2, dtype=torch.float32):
+                 world: int | None = None, dst: int = 0, n_buffers: int = 2, dtype=torch.float32,
+                 mode: str = "nccl"):
         initialized = dist.is_available() and dist.is_initialized()
         self.rank = rank if rank is not None else (dist.get_rank() if initialized else 0)
         self.world = world if world is not None else (dist.get_world_size() if initialized else 1)
@@ -71,14 +123,22 @@ class ChunkGather:
         self.rounds = max(len(c) for c in self.chunks)
         self.out = None
         self.bufs = []
-        if self.rank == dst:
+        self.mode = mode if self.world > 1 else "local"
+        self.device = device
+        self.peer = None
+        if self.mode == "p2p":
+            # fused gather: every rank's compositing kernel stores into dst's HBM over NVLink
+            self.peer = PeerBuffer(n_envs * floats_per_env, device, self.rank, self.world, dst)
+            if self.rank == dst:
+                self.out = self.peer.view(0, n_envs * floats_per_env, device)
+        elif self.rank == dst:
             self.out = torch.empty(n_envs * floats_per_env, dtype=dtype, device=device)
         else:
             self.bufs = [torch.empty(chunk_envs * floats_per_env, dtype=dtype, device=device)
                          for _ in range(n_buffers)]
         self.pending = [[] for _ in range(max(n_buffers, 1))]
         self.recv_pending = []
-        # bytes rank dst receives per step (floats)
+        # floats rank dst receives per step
         self.bytes_to_dst = sum((e - b) * floats_per_env for r, (b, e) in enumerate(self.ranges) if r != dst)
         if self.world > 1:
             dist.barrier()  # the communicator exists before the first point-to-point batch
@@ -91,6 +151,8 @@ class ChunkGather:
         b, e = self.my_chunks[j]
         if self.rank == self.dst:
             return self._view(b, e)
+        if self.mode == "p2p":
+            return self.peer.view(b * self.fpe, (e - b) * self.fpe, self.device)
         slot = j % len(self.bufs)
         for w in self.pending[slot]:
             w.wait()
@@ -99,8 +161,8 @@ class ChunkGather:
 
     def send(self, j: int) -> None:
         """Round j: this rank's chunk j to dst, and at dst every other rank's chunk j."""
-        if self.world == 1:
-            return
+        if self.world == 1 or self.mode == "p2p":
+            return  # p2p: the render already stored the chunk in dst's memory
         ops = []
         if self.rank == self.dst:
             for r in range(self.world):
@@ -121,7 +183,12 @@ class ChunkGather:
 
     def finish(self) -> None:
         """Every transfer of the step is ordered before the current stream's next work (NCCL)
-        or complete (gloo); on dst, `out` then holds every environment's frames."""
+        or complete (gloo); on dst, `out` then holds every environment's frames. p2p: every
+        rank's renders are complete (stream synchronised) before the barrier releases dst."""
+        if self.mode == "p2p":
+            torch.cuda.current_stream().synchronize()
+            dist.barrier()
+            return
         for works in self.pending:
             for w in works:
                 w.wait()
