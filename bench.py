@@ -78,7 +78,7 @@ def machine_descriptor() -> str:
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled every 2 ms through NVML during the timed region
+    """SM clock + throttle reasons sampled every ~1 ms through NVML during the timed region
     (nvidia-smi at 100 ms when NVML is unavailable)."""
     NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
              "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -121,7 +121,7 @@ class ClockSampler:
                 self.rows.append((sm, rs))
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
     def stop(self) -> dict | None:
         if self.nvml is None:
@@ -136,7 +136,7 @@ class ClockSampler:
                          if any(r[1] & getattr(pynvml, attr, 0) for r in self.rows))
         return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)),
                 "sm_max_mhz": float(self.max_mhz), "reasons": reasons, "samples": len(self.rows),
-                "source": "nvml, 2 ms"}
+                "source": "nvml, ~1 ms"}
 
 
 # ---- byte models ----------------------------------------------------------------

@@ -93,3 +93,18 @@ def test_hash_target_matches_reference_hash(lib, oracle):
     from paper_2507_21981_b200 import ValidationError
     with pytest.raises(ValidationError):
         bad.hash()
+
+
+def test_bench_refuses_mismatched_world_size():
+    """bench.py --gpus N under a launcher whose WORLD_SIZE differs exits non-zero (it never
+    silently reports fewer GPUs than asked)."""
+    import json
+    import os
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2
+    assert "WORLD_SIZE" in json.loads(r.stdout.strip().splitlines()[-1])["error"]
