@@ -76,24 +76,37 @@ __device__ __forceinline__ Unit unit_info(const BinArgs& a, uint32_t k) {
     return u;
 }
 
-// Walk records [wb, we) in order, 32 per group (lane = record), with the coalesced loads of kG
-// groups in flight; fn(slot, rect, valid) per group.
+// Walk records [wb, we) in order, 32 per group (lane = record), kG groups per step; fn(slot,
+// rect, valid) per group. The coalesced loads of the NEXT step are issued before the current
+// step is processed, so their latency hides behind it (ncu: the loads of a step issued at its
+// start were the scatter's top stall, long_scoreboard on a third of the samples).
 template <bool kSlots, class F>
 __device__ __forceinline__ void walk_groups(const BinArgs& a, uint32_t wb, uint32_t we, F&& fn) {
     constexpr int kG = 4;
     const int lane = threadIdx.x & 31;
-    for (uint32_t g0 = wb; g0 < we; g0 += 32 * kG) {
-        uint32_t slot[kG], rect[kG];
+    uint32_t slot[kG], rect[kG];
+    auto load = [&](uint32_t g0, uint32_t* sl, uint32_t* rc) {
 #pragma unroll
         for (int q = 0; q < kG; ++q) {
             const uint32_t e = g0 + q * 32 + lane;
-            rect[q] = e < we ? __ldcs(a.sorted_rects + e) : 0u;
-            slot[q] = (kSlots && e < we) ? __ldcs(a.sorted_slots + e) : 0u;
+            rc[q] = e < we ? __ldcs(a.sorted_rects + e) : 0u;
+            sl[q] = (kSlots && e < we) ? __ldcs(a.sorted_slots + e) : 0u;
         }
+    };
+    if (wb < we) load(wb, slot, rect);
+    for (uint32_t g0 = wb; g0 < we; g0 += 32 * kG) {
+        uint32_t nslot[kG], nrect[kG];
+        const uint32_t g1 = g0 + 32 * kG;
+        if (g1 < we) load(g1, nslot, nrect);
 #pragma unroll
         for (int q = 0; q < kG; ++q) {
             if (g0 + q * 32 >= we) break;
             fn(slot[q], rect[q], g0 + q * 32 + lane < we);
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            slot[q] = nslot[q];
+            rect[q] = nrect[q];
         }
     }
 }
