@@ -120,7 +120,8 @@ typedef struct gsim_target {
 typedef struct gsim_render_stats {
     uint64_t slots;        /* (camera, primitive) candidates */
     uint64_t visible;      /* records that touch at least one tile (V) */
-    uint64_t pairs;        /* (tile, record) pairs (P) */
+    uint64_t pairs;        /* (tile, record) pairs (P); after gsim_gpu_trace_rays: the rays'
+                              BVH candidates */
     uint64_t tiles;        /* total tiles over all cameras */
     uint64_t launches;     /* kernels launched by the last render */
     uint64_t launches_total; /* kernels launched on this context since creation */
