@@ -757,6 +757,12 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     // segmented onesweep passes over the depth keys; pass 1 compacts the culled slots away
     const int passes = p.sort_passes, radix = 1 << p.sort_bits;
     OnesweepArgs oa{};
+    static const uint32_t backoff = [] {  // GSIM_GPU_SORT_BACKOFF: look-back retry sleep (ns)
+        const char* e = std::getenv("GSIM_GPU_SORT_BACKOFF");
+        const int v = e ? std::atoi(e) : 64;
+        return uint32_t(v < 0 ? 0 : v > 1000 ? 1000 : v);
+    }();
+    oa.backoff_ns = backoff;
     oa.status = ctx->status.ptr;
     oa.n_cams = int(p.cams.size());
     oa.vbase = ctx->cam_vbase.ptr;
@@ -764,8 +770,8 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     uint64_t dgrid = (S + kOnesweepTile - 1) / kOnesweepTile + p.cams.size();
     static const int sort_ctas = [] {
         const char* e = std::getenv("GSIM_GPU_SORT_CTAS");  // resident onesweep CTAs per SM
-        const int v = e ? std::atoi(e) : 3;
-        return v < 1 ? 1 : v > 3 ? 3 : v;
+        const int v = e ? std::atoi(e) : kOnesweepMinBlocks;
+        return v < 1 ? 1 : v > kOnesweepMinBlocks ? kOnesweepMinBlocks : v;
     }();
     dgrid = std::max<uint64_t>(1, std::min<uint64_t>(dgrid, uint64_t(n_sms) * sort_ctas));
     const uint32_t* kin = ctx->keys.ptr;
@@ -1639,13 +1645,14 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
     launch_bvh_sort_setup(b, s);
     check_launch();
     OnesweepArgs oa{};
+    oa.backoff_ns = 64;
     oa.status = ctx->status.ptr;
     oa.n_cams = 1;
     oa.vbase = b.vbase;
     oa.hist_stride = 4 * 256;
     oa.seg_base64 = L.bvh_seg.ptr;
     oa.seg_base32 = b.vbase;
-    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(chunks0 + 1, uint64_t(n_sms) * 3)));
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(chunks0 + 1, uint64_t(n_sms) * kOnesweepMinBlocks)));
     const uint32_t* kin = b.codes_in;
     const uint32_t* vin = nullptr;
     const int out_of[4] = {1, 0, 1, 0};  // codes_in is bvh_keys[0]: pass 1 writes buffer 1

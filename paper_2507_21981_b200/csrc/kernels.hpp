@@ -13,7 +13,9 @@ namespace gsim_gpu {
 
 constexpr int kMaxSmemSegments = 1024;
 constexpr int kMaxSmemCams = 32;        // K2 stages up to this many cameras in shared memory
-constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16)
+constexpr int kOnesweepTile = 4096;     // keys per onesweep chunk (256 threads x 16); 8192-item
+                                        // chunks (32 per thread, 2 CTAs/SM) measured the same
+constexpr int kOnesweepMinBlocks = 3;   // resident onesweep CTAs per SM (register-bound)
 constexpr int kWarpRecords = 1024;      // depth-sorted records per warp of a binning unit (max)
 
 struct PreprocessArgs {
@@ -65,6 +67,7 @@ struct OnesweepArgs {
     int shift;
     const uint32_t* rects_in;        // last pass: gather rects_in[slot] ...
     uint32_t* rects_out;             // ... into depth order (nullptr on the other passes)
+    uint32_t backoff_ns;             // look-back retry sleep
 };
 
 // Tile binning of the camera-major depth-sorted records (bin.cu).

@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = kOnesweepTile / kThreads;  // 16
+constexpr int kItems = kOnesweepTile / kThreads;  // 16 (32 with 8192-item chunks)
 constexpr uint64_t kCountMask = (1ull << 40) - 1;
 
 // Exclusive scan of one u32 per thread over a 256-thread block. Returns the exclusive
@@ -58,11 +58,11 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 }
 
 // Spin until chunk j's word for a digit is published in this epoch; return it.
-__device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoch) {
+__device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoch, uint32_t backoff) {
     while (true) {
         const uint64_t s = ld_volatile_u64(p);
         if ((s >> 62) != 0 && uint32_t((s >> 40) & kEpochMask) == (epoch & kEpochMask)) return s;
-        __nanosleep(64);  // back off: spinning warps would steal issue slots from working ones
+        __nanosleep(backoff);  // back off: spinning warps would steal issue slots from working ones
     }
 }
 
@@ -75,7 +75,7 @@ __device__ __forceinline__ uint64_t wait_status(const uint64_t* p, uint32_t epoc
 // that clear before the next item's atomicOr), so chunks never re-clear them.
 // Thread t owns digits t*kDpt .. t*kDpt + kDpt - 1 for the per-digit scans and the look-back.
 template <int kBits, bool kFirst, bool kWriteKeys>
-__global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
+__global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(OnesweepArgs a) {
     constexpr int kRadix = 1 << kBits;
     constexpr int kDpt = kRadix / kThreads;  // 1 (8-bit digits) or 2 (9-bit)
     constexpr uint32_t kMask = kRadix - 1;
@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(OnesweepArgs a) {
                 for (int j = 0; j < kDpt; ++j) {
                     if (done[j]) continue;
                     GSIM_DCHECK(q >= int64_t(first_chunk));
-                    const uint64_t s = wait_status(a.status + uint64_t(q) * kRadix + tid * kDpt + j, a.epoch);
+                    const uint64_t s = wait_status(a.status + uint64_t(q) * kRadix + tid * kDpt + j, a.epoch,
+                                                   a.backoff_ns);
                     prefix[j] += s & kCountMask;
                     done[j] = (s >> 62) == kFlagInclusive;
                     all = all && done[j];
