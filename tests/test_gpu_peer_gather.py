@@ -75,7 +75,19 @@ def _same_poses(r, frame):
     return r.frame_nodes(frame)
 
 
+def _compute_mode() -> str:
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=compute_mode", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=30).stdout.strip()
+    except Exception:
+        out = ""
+    return out
+
+
 def test_fused_peer_gather_two_ranks_one_gpu():
+    if "Exclusive" in _compute_mode():
+        pytest.skip("GPU in an exclusive compute mode: two processes cannot share it")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
