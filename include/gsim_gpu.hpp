@@ -22,6 +22,10 @@
 //   gsim::gpu::lidar_scan(field, nodes, lidar)          GaussianBvh::build(field, nodes).scan(lidar)
 //                                                       (trace.hpp:66-82)
 //   gsim::gpu::trace(field, nodes, rays, threshold)     GaussianBvh::trace per ray (trace.hpp:70-74)
+//   gsim::gpu::render_all(scene, cameras, options)      Scene::render_all (scene.cpp:232-235)
+//   gsim::gpu::run_bench(scene, options)                run_bench (bench.hpp:45, bench.cpp:98-160):
+//                                                       the reference's timed camera-ring loop,
+//                                                       rendered by the GPU
 //
 // Errors are rethrown as the reference's gsim::validation_error (status 2) and gsim::io_error
 // (status 1). The free functions keep the field resident in HBM between calls: the upload is
@@ -35,15 +39,21 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <memory>
 #include <string>
 #include <vector>
 
+#include "gsim/bench.hpp"
 #include "gsim/errors.hpp"
 #include "gsim/gaussian.hpp"
+#include "gsim/hash.hpp"
+#include "gsim/reference_raster.hpp"
 #include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
 #include "gsim/trace.hpp"
@@ -602,6 +612,125 @@ inline std::vector<TraceResult> trace(const GaussianField& field, const std::vec
 // would write for `t` (GSIM_ENCODE_* order), encoded on the GPU.
 inline std::vector<uint8_t> encode(const RenderTarget& t, const EncodeOptions& options = {}) {
     return default_renderer().encode(t, options);
+}
+
+// Scene::render_all (scene.cpp:232-235): the scene's field (upload cached) and node poses.
+inline std::vector<RenderTarget> render_all(const Scene& scene, const std::vector<CameraModel>& cameras,
+                                            const RasterOptions& options = {}) {
+    return gsim::gpu::render(scene.field(), scene.nodes(), cameras, options);
+}
+
+namespace detail {
+// The reference bench's helpers (bench.cpp:36-75, file-local there), restated.
+inline Aabb posed_field_bounds(const Scene& scene) {
+    Aabb box;
+    for (const auto& node : scene.nodes())
+        for (std::size_t i = node.range.begin; i < node.range.end; ++i)
+            box.expand(pose_primitive(scene.field().primitives[i], node.pose).bounds);
+    return box;
+}
+
+inline std::vector<CameraModel> camera_ring(const Scene& scene, int count, int width, int height) {
+    Aabb box = posed_field_bounds(scene);
+    if (box.empty()) {
+        box.expand({-1, -1, -1});
+        box.expand({1, 1, 1});
+    }
+    const Vec3 center = box.center();
+    const double diag = std::max(box.extent().norm(), 1e-3);
+    const double radius = 1.2 * diag;
+    const double focal = 0.8 * width;
+    std::vector<CameraModel> cameras;
+    for (int k = 0; k < count; ++k) {
+        const double azimuth = kTwoPi * k / count;
+        const Vec3 eye = center + Vec3{radius * std::cos(azimuth), radius * std::sin(azimuth), 0.35 * radius};
+        CameraModel cam = CameraModel::look_at(eye, center, focal, focal, width, height);
+        cam.id = "bench_cam" + std::to_string(k);
+        cam.near = 0.01 * radius;
+        cam.far = 10.0 * radius;
+        cameras.push_back(cam);
+    }
+    return cameras;
+}
+
+inline void pose_frame(Scene& scene, int frame) {  // 30 Hz nominal clock, first interactive node
+    for (auto& node : scene.nodes()) {
+        if (node.kind != NodeKind::interactive) continue;
+        node.pose.rotation = Quat::from_axis_angle({0, 0, 1}, deg_to_rad(30.0) * frame / 30.0);
+        return;
+    }
+}
+
+inline std::string gpu_machine_descriptor() {  // bench.cpp:79-96, plus the device
+    std::string model = "unknown-cpu";
+    std::ifstream cpuinfo("/proc/cpuinfo");
+    std::string line;
+    while (std::getline(cpuinfo, line)) {
+        if (line.rfind("model name", 0) == 0) {
+            const auto colon = line.find(':');
+            if (colon != std::string::npos) {
+                model = line.substr(colon + 1);
+                const auto first = model.find_first_not_of(' ');
+                if (first != std::string::npos) model = model.substr(first);
+            }
+            break;
+        }
+    }
+    return model + " + " + gsim_gpu_version();
+}
+}  // namespace detail
+
+// run_bench (bench.cpp:98-160) with the frames rendered by the GPU drop-in: the same camera
+// ring, node motion, warm-up and timed loop (wall clock over whole frames, host RGB-D targets
+// returned by value), first-frame image hash and fps; the optional brute-force crop stays the
+// reference's CPU reference_rasterize, as in the reference bench.
+inline BenchReport run_bench(Scene& scene, const BenchOptions& options) {
+    using Clock = std::chrono::steady_clock;
+    auto since = [](Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+    if (options.cameras < 1) throw validation_error("bench: need at least one camera");
+    BenchReport report;
+    report.primitives = scene.field().size();
+    report.width = options.width;
+    report.height = options.height;
+    report.cameras = options.cameras;
+    report.threads = 1;  // one host thread drives the device
+    report.machine = options.machine.empty() ? detail::gpu_machine_descriptor() : options.machine;
+    const auto cameras = detail::camera_ring(scene, options.cameras, options.width, options.height);
+    for (int frame = 0; frame < options.warmup_frames; ++frame) {
+        detail::pose_frame(scene, frame);
+        render_all(scene, cameras);
+    }
+    int frame = options.warmup_frames, timed = 0;
+    std::uint64_t first_hash = 0;
+    const auto start = Clock::now();
+    while (timed < options.min_frames || since(start) < options.seconds) {
+        detail::pose_frame(scene, frame);
+        const auto targets = render_all(scene, cameras);
+        if (timed == 0) {
+            std::uint64_t h = 1469598103934665603ull;
+            for (const auto& t : targets) h = hash_target(t, h);
+            first_hash = h;
+        }
+        ++frame;
+        ++timed;
+    }
+    report.wall_time = since(start);
+    report.frames = timed;
+    report.fps = timed * options.cameras / report.wall_time;
+    report.image_hash = first_hash;
+    if (options.run_brute_force) {
+        detail::pose_frame(scene, options.warmup_frames);
+        CameraModel crop = cameras[0];
+        crop.width = crop.height = options.brute_crop;
+        crop.cx = crop.cy = options.brute_crop * 0.5;
+        const auto brute_start = Clock::now();
+        reference_rasterize(gsim::project(scene.field(), scene.nodes(), crop), crop);
+        report.brute_wall = since(brute_start);
+        report.brute_crop = options.brute_crop;
+        const double tiled = double(timed) * options.cameras * options.width * options.height / report.wall_time;
+        report.brute_speedup = tiled / (double(options.brute_crop) * options.brute_crop / report.brute_wall);
+    }
+    return report;
 }
 
 }  // namespace gsim::gpu

@@ -4,12 +4,15 @@
 // run by tests/test_gpu_dropin.py on a GPU box).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <iterator>
 #include <string>
 #include <vector>
 
+#include "gsim/bench.hpp"
 #include "gsim/gaussian.hpp"
+#include "gsim/hash.hpp"
 #include "gsim/image_io.hpp"
 #include "gsim/pose_stream.hpp"
 #include "gsim/raster.hpp"
@@ -343,6 +346,58 @@ int main() {
         try { gpu::lidar_scan(f, ln, bad); } catch (const validation_error&) { gpu_threw = true; }
         std::printf("lidar validation_error: reference %d, gpu %d\n", ref_threw, gpu_threw);
         if (!ref_threw || !gpu_threw) ++failures;
+    }
+
+    // run_bench / Scene::render_all (bench.cpp:98-160, scene.cpp:232-235): a scene loaded by the
+    // reference's own Scene::load from a manifest + splat PLYs, benched by the reference and by
+    // gsim::gpu::run_bench. The restated camera ring and node motion reproduce the reference's
+    // first-frame hash bit for bit; the GPU frames match the reference's within tolerance.
+    {
+        const std::string dir = "/tmp/gsim_dropin_scene";
+        if (std::system(("mkdir -p " + dir).c_str()) != 0) ++failures;
+        GaussianField bg = oracle::random_field(31, 2500, 2.0, 0.01, 0.15, 2);
+        GaussianField obj = oracle::random_field(32, 800, 0.5, 0.01, 0.08, 2);
+        save_splat_ply(bg, dir + "/bg.ply");
+        save_splat_ply(obj, dir + "/obj.ply");
+        {
+            std::ofstream m(dir + "/scene.json");
+            m << R"({"nodes": [{"id": "bg", "kind": "background", "splat": "bg.ply"},
+                              {"id": "obj", "kind": "interactive", "splat": "obj.ply",
+                               "pose": {"p": [0.2, 0.0, 0.1], "q": [1, 0, 0, 0]}}]})";
+        }
+        BenchOptions opt;
+        opt.cameras = 3;
+        opt.width = 160;
+        opt.height = 120;
+        opt.seconds = 0.0;
+        opt.warmup_frames = 1;
+        opt.min_frames = 2;
+        opt.run_brute_force = false;
+        Scene ref_scene = Scene::load(dir + "/scene.json");
+        Scene gpu_scene = Scene::load(dir + "/scene.json");
+        const BenchReport r_ref = run_bench(ref_scene, opt);
+        const BenchReport r_gpu = gpu::run_bench(gpu_scene, opt);
+        // the first timed frame: frame index warmup_frames on the restated camera ring
+        Scene probe = Scene::load(dir + "/scene.json");
+        gpu::detail::pose_frame(probe, opt.warmup_frames);
+        const auto ring = gpu::detail::camera_ring(probe, opt.cameras, opt.width, opt.height);
+        const auto ref_frame = render(probe.field(), probe.nodes(), ring);
+        const auto gpu_frame = gpu::render_all(probe, ring);
+        std::uint64_t h_ref = 1469598103934665603ull, h_gpu = 1469598103934665603ull;
+        double worst = 1.0;
+        for (int k = 0; k < opt.cameras; ++k) {
+            h_ref = hash_target(ref_frame[k], h_ref);
+            h_gpu = hash_target(gpu_frame[k], h_gpu);
+            worst = std::fmin(worst, frac_within(gpu_frame[k], ref_frame[k], 2e-3, 1e-3));
+        }
+        const bool ring_exact = h_ref == r_ref.image_hash;
+        const bool gpu_consistent = h_gpu == r_gpu.image_hash;
+        std::printf("run_bench: reference %.1f camera-frames/s, gpu %.1f camera-frames/s (%d frames); "
+                    "ring hash matches the reference %d, gpu hash consistent %d, frame within tolerance %.5f\n",
+                    r_ref.fps, r_gpu.fps, r_gpu.frames, ring_exact, gpu_consistent, worst);
+        if (!ring_exact || !gpu_consistent || worst < 0.999 || r_gpu.frames < opt.min_frames ||
+            r_gpu.primitives != r_ref.primitives)
+            ++failures;
     }
 
     std::printf(failures ? "DROP-IN FAILED\n" : "DROP-IN OK\n");
