@@ -407,3 +407,80 @@ def test_narrow_depth_window_batch(ctx, oracle):
         assert np.array_equal(offsets[: len(tb)], tb), k
         assert np.array_equal(values, splats["prim_index"][vals]), k
         assert_parity(got[k], oracle.rasterize(splats, cam), k)
+
+
+def test_segmented_sort_edge_cameras(ctx, oracle):
+    """Sort segments that are empty or tiny: a batch interleaving cameras that see nothing
+    (facing away), a camera that sees a single splat and ordinary cameras; every camera's image
+    and tile lists equal the oracle's, and equal its own single-camera render."""
+    f = oracle.random_field(515, 9000, 2.0, 0.01, 0.2, 1)
+    f.means[:, 2] += 3.0
+    f.touch()
+    from paper_2507_21981_b200.api import CameraModel, GaussianField
+    cams = []
+    for k in range(7):
+        c = ref_camera(96, 80, 70.0)
+        if k in (0, 3, 6):  # facing away from the cloud: no visible record at all
+            c.pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 3.14159), (0.0, 0.0, 0.0))
+        else:
+            c.pose = RigidTransform(quat_from_axis_angle((1, 0, 0), 0.03 * k), (0.05 * k, 0.0, 0.0))
+        cams.append(c)
+    s = ctx.upload(f)
+    got = ctx.render(s, [], cams)
+    for k, cam in enumerate(cams):
+        splats = oracle.project(f, [], cam)
+        tb, vals = oracle.rasterize_lists(splats, cam)
+        offsets, values = ctx.tile_lists(k)
+        assert np.array_equal(offsets[: len(tb)], tb), k
+        assert np.array_equal(values, splats["prim_index"][vals]), k
+        if k in (0, 3, 6):
+            assert len(vals) == 0 and not got[k].accum_alpha.any()
+        else:
+            assert_parity(got[k], oracle.rasterize(splats, cam), k)
+    # one splat seen by one camera of a batch
+    one = single_prim_field((0.0, 0.0, 2.0), (0.05, 0.05, 0.05), 0.8)
+    s1 = ctx.upload(one)
+    pair = [ref_camera(64, 64, 60.0), ref_camera(64, 64, 60.0)]
+    pair[1].pose = RigidTransform(quat_from_axis_angle((0, 1, 0), 3.14159), (0.0, 0.0, 0.0))
+    t = ctx.render(s1, [], pair)
+    assert t[0].accum_alpha.max() > 0.5 and not t[1].accum_alpha.any()
+
+
+NINE_BIT_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from oracle.oracle import Oracle
+from paper_2507_21981_b200 import Context
+from paper_2507_21981_b200.scenes import config1
+orc = Oracle()
+w = config1(seed=44, n_bg=200_000, per_object=5_000)
+nodes = w.frame_nodes(1)
+ctx = Context(0)
+s = ctx.upload(w.field)
+ctx.render(s, nodes, w.cameras)
+assert ctx.stats()["depth_passes"] == 3, ctx.stats()
+bad = 0
+for k in (0, 4):
+    offsets, values = ctx.tile_lists(k)
+    splats = orc.project(w.field, nodes, w.cameras[k])
+    tb, vals = orc.rasterize_lists(splats, w.cameras[k])
+    bad += int(not np.array_equal(offsets[: len(tb)], tb))
+    bad += int(not np.array_equal(values, splats["prim_index"][vals]))
+print("9-bit digits: 3 passes, mismatches", bad)
+sys.exit(1 if bad else 0)
+"""
+
+
+def test_nine_bit_digit_sort_lists_bit_exact():
+    """GSIM_GPU_SORT_BITS=9 (3 passes of 9-bit digits over the 27-bit keys) keeps
+    the tile lists bit-exact."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, GSIM_GPU_SORT_BITS="9")
+    r = subprocess.run([sys.executable, "-c", NINE_BIT_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    print(r.stdout, r.stderr[-2000:])
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
