@@ -108,3 +108,28 @@ def test_bench_refuses_mismatched_world_size():
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 2
     assert "WORLD_SIZE" in json.loads(r.stdout.strip().splitlines()[-1])["error"]
+
+
+def test_bench_reference_arm_self_launches_two_ranks():
+    """--gpus 2 outside torchrun re-launches under torch.distributed.run; in the reference arm
+    rank 0 alone times the reference's CPU renderer (oracle/_ref) and prints one JSON line with
+    impl = reference, the other rank exits 0 without work."""
+    import json
+    import os
+    import sys
+    from pathlib import Path
+    from oracle.oracle import REF_LIB
+    if not REF_LIB.exists():
+        pytest.skip("oracle/_ref not built")
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "cfg0", "--steps", "1", "--warmup", "3"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and len(d["first_frame_hash"]) == 16
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
