@@ -1167,80 +1167,98 @@ struct FileCloser {
     void operator()(std::FILE* f) const { if (f) std::fclose(f); }
 };
 
+// The header contract of load_splat_ply (splat_ply.cpp:40-113): the "ply" magic, keyword lines
+// up to end_header, binary_little_endian, one vertex element, float properties in the 3DGS order
+// of SH degree 0-3 (the degree follows from the f_rest count). The header is first read into a
+// PlyHeader (every line classified by its keyword), then judged as a whole; any violation is a
+// validation error (status 2), as every format_error of the reference is.
+struct PlyHeader {
+    bool magic = false, closed = false;
+    std::vector<std::string> formats;                      // format names, in order
+    std::vector<std::pair<std::string, uint64_t>> elements;  // (name, count)
+    std::vector<std::pair<std::string, std::string>> props;  // (type, name)
+    std::vector<std::string> unknown;                      // unexpected keywords
+};
+
+PlyHeader read_ply_header(std::FILE* fp) {
+    PlyHeader h;
+    std::string line;
+    auto next_line = [&](bool strip_cr) {
+        line.clear();
+        int ch;
+        while ((ch = std::fgetc(fp)) != EOF && ch != '\n') line.push_back(char(ch));
+        const bool got = ch != EOF || !line.empty();
+        if (strip_cr && !line.empty() && line.back() == '\r') line.pop_back();
+        return got;
+    };
+    if (!next_line(false)) return h;
+    h.magic = line == "ply";  // the reference compares the raw first line (no CR stripping)
+    if (!h.magic) return h;
+    while (next_line(true)) {
+        if (line == "end_header") {
+            h.closed = true;
+            break;
+        }
+        std::vector<std::string> f;  // whitespace-separated fields
+        size_t i = 0;
+        while (i < line.size()) {
+            while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+            const size_t j0 = i;
+            while (i < line.size() && !std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+            if (i > j0) f.emplace_back(line, j0, i - j0);
+        }
+        f.resize(std::max<size_t>(f.size(), 3));
+        const std::string& kw = f[0];
+        if (kw.empty() || kw == "comment") continue;
+        if (kw == "format") h.formats.push_back(f[1]);
+        else if (kw == "element") h.elements.emplace_back(f[1], std::strtoull(f[2].c_str(), nullptr, 10));
+        else if (kw == "property") h.props.emplace_back(f[1], f[2]);
+        else h.unknown.push_back(kw);
+    }
+    return h;
+}
+
+// Validates the header; returns (SH degree, primitive count).
+std::pair<int, uint64_t> check_ply_header(const PlyHeader& h, const std::string& who) {
+    auto fail = [&](const std::string& why) { throw ValidationError{who + ": " + why}; };
+    if (!h.magic) fail("missing 'ply' magic");
+    for (const auto& fmt : h.formats)
+        if (fmt != "binary_little_endian") fail("format must be binary_little_endian, got '" + fmt + "'");
+    uint64_t count = 0;
+    for (const auto& e : h.elements) {
+        if (e.first != "vertex") fail("unexpected element '" + e.first + "'");
+        count = e.second;
+    }
+    for (const auto& pr : h.props)
+        if (pr.first != "float") fail("property '" + pr.second + "' must be float, got '" + pr.first + "'");
+    if (!h.unknown.empty()) fail("unexpected header token '" + h.unknown.front() + "'");
+    if (!h.closed) fail("header missing end_header");
+    if (h.formats.empty()) fail("header missing format line");
+    if (h.elements.empty()) fail("header missing element vertex line");
+    const size_t rest = size_t(std::count_if(h.props.begin(), h.props.end(), [](const auto& pr) {
+        return pr.second.compare(0, 7, "f_rest_") == 0;
+    }));
+    int degree = -1;
+    for (int d = 0; d <= 3; ++d)
+        if (rest == size_t(3 * (sh_coeff_count(d) - 1))) degree = d;
+    if (degree < 0) fail("f_rest property count " + std::to_string(rest) + " matches no SH degree in [0,3]");
+    const std::vector<std::string> want = ply_expected_properties(degree);
+    for (size_t k = 0; k < std::max(want.size(), h.props.size()); ++k) {
+        if (k >= h.props.size()) fail("missing property '" + want[k] + "'");
+        if (k >= want.size()) fail("unexpected extra property '" + h.props[k].second + "'");
+        if (h.props[k].second != want[k])
+            fail("property " + std::to_string(k) + " is '" + h.props[k].second + "', expected '" + want[k] + "'");
+    }
+    if (count >= 0xFFFFFFFFull) fail("more than 2^32 - 1 primitives");
+    return {degree, count};
+}
+
 gsim_gpu_scene* load_ply(gsim_gpu_context* ctx, const std::string& path) {
     std::unique_ptr<std::FILE, FileCloser> fp(std::fopen(path.c_str(), "rb"));
     if (!fp) throw CudaError{"cannot open splat PLY '" + path + "'"};  // io_error -> status 1
     const std::string who = "'" + path + "'";
-    auto getline = [&](std::string& line) {
-        line.clear();
-        int ch;
-        while ((ch = std::fgetc(fp.get())) != EOF && ch != '\n') line.push_back(char(ch));
-        return !(ch == EOF && line.empty());
-    };
-    std::string line;
-    if (!getline(line) || line != "ply") throw ValidationError{who + ": missing 'ply' magic"};
-    bool format_seen = false, element_seen = false, header_closed = false;
-    uint64_t count = 0;
-    std::vector<std::string> props;
-    while (getline(line)) {
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (line == "end_header") {
-            header_closed = true;
-            break;
-        }
-        // whitespace tokens, as operator>> on an istringstream would split the line
-        std::vector<std::string> words;
-        for (size_t i = 0; i < line.size();) {
-            while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
-            size_t j = i;
-            while (j < line.size() && !std::isspace(static_cast<unsigned char>(line[j]))) ++j;
-            if (j > i) words.emplace_back(line, i, j - i);
-            i = j;
-        }
-        auto word = [&](size_t k) { return k < words.size() ? words[k] : std::string(); };
-        const std::string tok = word(0);
-        if (tok == "comment") continue;
-        if (tok == "format") {
-            const std::string fmt = word(1);
-            if (fmt != "binary_little_endian")
-                throw ValidationError{who + ": format must be binary_little_endian, got '" + fmt + "'"};
-            format_seen = true;
-        } else if (tok == "element") {
-            const std::string name = word(1);
-            count = std::strtoull(word(2).c_str(), nullptr, 10);
-            if (name != "vertex") throw ValidationError{who + ": unexpected element '" + name + "'"};
-            element_seen = true;
-        } else if (tok == "property") {
-            const std::string type = word(1), name = word(2);
-            if (type != "float")
-                throw ValidationError{who + ": property '" + name + "' must be float, got '" + type + "'"};
-            props.push_back(name);
-        } else if (!tok.empty()) {
-            throw ValidationError{who + ": unexpected header token '" + tok + "'"};
-        }
-    }
-    if (!header_closed) throw ValidationError{who + ": header missing end_header"};
-    if (!format_seen) throw ValidationError{who + ": header missing format line"};
-    if (!element_seen) throw ValidationError{who + ": header missing element vertex line"};
-    size_t rest_count = 0;
-    for (const auto& p : props)
-        if (p.rfind("f_rest_", 0) == 0) ++rest_count;
-    int degree = -1;
-    for (int d = 0; d <= 3; ++d)
-        if (rest_count == size_t(3 * (sh_coeff_count(d) - 1))) degree = d;
-    if (degree < 0)
-        throw ValidationError{who + ": f_rest property count " + std::to_string(rest_count) +
-                              " does not match any SH degree in [0,3]"};
+    const auto [degree, count] = check_ply_header(read_ply_header(fp.get()), who);
     const std::vector<std::string> expected = ply_expected_properties(degree);
-    for (size_t i = 0; i < expected.size(); ++i) {
-        if (i >= props.size()) throw ValidationError{who + ": missing property '" + expected[i] + "'"};
-        if (props[i] != expected[i])
-            throw ValidationError{who + ": expected property '" + expected[i] + "' at position " +
-                                  std::to_string(i) + ", found '" + props[i] + "'"};
-    }
-    if (props.size() > expected.size())
-        throw ValidationError{who + ": unexpected extra property '" + props[expected.size()] + "'"};
-    if (count >= 0xFFFFFFFFull) throw ValidationError{who + ": more than 2^32 - 1 primitives"};
 
     // Payload: pinned double-buffered chunks, disk read of chunk k+1 overlapping the H2D of k.
     const int stride = int(expected.size());
