@@ -489,11 +489,15 @@ def run_cfg4(args, rank, world, local, dist):
         nodes = r.frame_nodes(i)
         with torch.cuda.stream(stream):
             for j in range(len(gather.my_chunks)):
-                buf = gather.target(j)
-                ctx.render_device(r.scene, nodes, chunk_cams[j], None, buf.data_ptr())
+                tgt = gather.target(j)
+                ctx.render_device(r.scene, nodes, chunk_cams[j], None, tgt.ptr)
                 if sums is not None:  # exact per-env checksums of what this rank sends
                     cb, ce = gather.my_chunks[j]
-                    sums[cb:ce] = buf.view(ce - cb, fpe).view(torch.int32).sum(1, dtype=torch.int64)
+                    local = tgt.local
+                    if local is None:  # stored in rank 0's memory: re-render (deterministic)
+                        local = torch.empty((ce - cb) * fpe, dtype=torch.float32, device=dev)
+                        ctx.render_device(r.scene, nodes, chunk_cams[j], None, local.data_ptr())
+                    sums[cb:ce] = local.view(ce - cb, fpe).view(torch.int32).sum(1, dtype=torch.int64)
                 gather.send(j)
             gather.finish()
 
@@ -556,7 +560,8 @@ def run_cfg4(args, rank, world, local, dist):
                                    "background replica per GPU + each env's 4x20k objects",
                        "envs_per_rank": e - b, "chunk_envs": args.chunk_envs,
                        "gaussians_per_rank": r.scene.size,
-                       "parallelism": f"env-sharded x{world}, frames gathered to rank 0 " + (
+                       "parallelism": "one rank: every environment rendered into the gathered output"
+                       if world == 1 else f"env-sharded x{world}, frames gathered to rank 0 " + (
                            "(fused: the compositing kernels store into rank 0's HBM over NVLink "
                            "peer memory)" if args.gather == "p2p" else
                            "(grouped NCCL P2P, overlapped with the next chunk)"),

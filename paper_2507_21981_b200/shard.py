@@ -97,6 +97,16 @@ class PeerBuffer:
             self.ptr = 0
 
 
+class ChunkTarget:
+    """A chunk's render destination: device pointer + local tensor view (None for peer memory)."""
+
+    def __init__(self, ptr: int, local: torch.Tensor | None):
+        self.ptr, self.local = int(ptr), local
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
 class ChunkGather:
     """BASELINE config 4's frame gather, overlapped with rendering.
 
@@ -146,18 +156,23 @@ class ChunkGather:
     def _view(self, b: int, e: int):
         return self.out[b * self.fpe: e * self.fpe]
 
-    def target(self, j: int) -> torch.Tensor:
-        """Where this rank renders its chunk j (waits for the buffer's previous transfer)."""
+    def target(self, j: int) -> "ChunkTarget":
+        """Where this rank renders its chunk j (waits for the buffer's previous transfer): the
+        device pointer to pass as the render's output, and a local tensor view of it, or None
+        when the memory is another GPU's (p2p on ranks other than dst: no tensor is made over
+        peer memory, which torch would attribute to the owner's device)."""
         b, e = self.my_chunks[j]
         if self.rank == self.dst:
-            return self._view(b, e)
+            v = self._view(b, e)
+            return ChunkTarget(v.data_ptr(), v)
         if self.mode == "p2p":
-            return self.peer.view(b * self.fpe, (e - b) * self.fpe, self.device)
+            return ChunkTarget(self.peer.ptr + 4 * b * self.fpe, None)
         slot = j % len(self.bufs)
         for w in self.pending[slot]:
             w.wait()
         self.pending[slot] = []
-        return self.bufs[slot][: (e - b) * self.fpe]
+        v = self.bufs[slot][: (e - b) * self.fpe]
+        return ChunkTarget(v.data_ptr(), v)
 
     def send(self, j: int) -> None:
         """Round j: this rank's chunk j to dst, and at dst every other rank's chunk j."""

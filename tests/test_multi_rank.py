@@ -87,7 +87,7 @@ def _chunk_worker(rank, world, port, n_envs, per_env, chunk, steps, q):
     ok = True
     for step in range(steps):  # the bench's schedule: render chunk j, send j, next chunk
         for j, (cb, ce) in enumerate(g.my_chunks):
-            buf = g.target(j)
+            buf = g.target(j).local
             buf.copy_(torch.cat([torch.arange(per_env, dtype=torch.float32) + env * 1000 + step * 1e6
                                  for env in range(cb, ce)]))
             g.send(j)
