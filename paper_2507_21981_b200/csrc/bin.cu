@@ -514,18 +514,19 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                     // lanes of this step on the same cell, from one atomicOr into the cell's
                     // bitmap; ranked by lane (= emission) order, the lowest lane bumps the
                     // position and clears the bitmap
+                    // Every lane reads the cell's position together with the bitmap (same-address
+                    // reads broadcast), so no shuffle from the leader sits on the chain; the
+                    // leader's update follows a warp barrier that orders it after all reads.
                     if (in) atomicOr(&peer_bits[cell], 1u << lane);
                     __syncwarp();
                     const uint32_t peers = in ? peer_bits[cell] : 0u;
+                    const uint32_t pre = in ? pos[cell] : 0u;
                     const uint32_t below = peers & lanemask_lt();
                     __syncwarp();
-                    uint32_t pre = 0;
                     if (in && below == 0) {
-                        pre = pos[cell];
                         pos[cell] = pre + __popc(peers);
                         peer_bits[cell] = 0u;
                     }
-                    pre = __shfl_sync(kFull, pre, in ? __ffs(peers) - 1 : lane);
                     if (in) {
                         const uint32_t p = pre + __popc(below);
                         if (p < cap32) a.vals_out[p] = sl;

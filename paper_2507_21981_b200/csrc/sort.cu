@@ -159,19 +159,23 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
         for (int i = 0; i < kItems; ++i) {
             const bool valid = rank[i] != 0u;
             const uint32_t d = (keys[i] >> a.shift) & kMask;
+            // The digit's warp count is read by every peer together with the bitmap (the
+            // histogram is warp-private: no atomic, no shuffle from the leader); the leader
+            // bumps it and clears the bitmap after a warp barrier orders that after all reads.
             uint32_t* bits = &s_peer[warp][d];
+            uint32_t* cnt = &s_warp_hist[warp][d];
             if (valid) atomicOr(bits, 1u << lane);
             __syncwarp();
             const uint32_t peers = valid ? *bits : 0u;
-            __syncwarp();
-            if (valid && (peers & lanemask_lt()) == 0) *bits = 0u;  // leader clears
+            const uint32_t pre = valid ? *cnt : 0u;
             const uint32_t below = peers & lanemask_lt();
-            const int leader = peers ? __ffs(peers) - 1 : lane;
-            uint32_t pre = 0;
-            if (valid && below == 0) pre = atomicAdd(&s_warp_hist[warp][d], uint32_t(__popc(peers)));
-            pre = __shfl_sync(0xffffffffu, pre, leader);
+            __syncwarp();
+            if (valid && below == 0) {
+                *cnt = pre + uint32_t(__popc(peers));
+                *bits = 0u;
+            }
             rank[i] = valid ? (pre + __popc(below)) : 0xFFFFFFFFu;
-            __syncwarp();  // the leader's clear is visible before the next item's atomicOr
+            __syncwarp();  // the leader's updates are visible before the next item's reads
         }
         __syncthreads();
         // Per digit (thread = kDpt digits): exclusive prefix across warps, block count.
