@@ -12,9 +12,11 @@
 //                         then primitive index, so duplicate codes still split) and split point
 //   bvh_refit_kernel      leaves upward: the second child to arrive at a node writes the union
 //                         of the children's boxes (exact fmin / fmax of doubles)
-//   bvh_collect_kernel    one thread per ray, stack traversal with the reference's slab test on
-//                         every node box; a leaf is a candidate iff ray_aabb_hit(its own box) —
-//                         count pass, then fill pass into the ray's list
+//   bvh_widen_kernel      traversal nodes: both children's boxes in fp32 (rounded outward, widened)
+//   bvh_collect_kernel    one thread per ray, stack traversal testing both children of a visited
+//                         node in fp32 (a conservative filter); a leaf is a candidate iff the
+//                         reference's double ray_aabb_hit of its own box passes — count pass,
+//                         then fill pass into the ray's list
 // A union box contains its children's boxes, and the slab test is monotone under containment
 // in floating point too ((lo - o) * inv rounds monotonically), so no hit box is ever pruned: the
 // lists equal the reference's candidate sets and lidar_trace_kernel composites them as for scans.
@@ -218,6 +220,63 @@ __global__ void __launch_bounds__(256) bvh_refit_kernel(BvhArgs a) {
     }
 }
 
+// Traversal nodes: node i carries BOTH children's boxes in fp32, rounded outward and widened by
+// a margin, plus the child links (4 float4 = 64 B, one load per visited node):
+//   w[0] = (L.lo.x, L.lo.y, L.lo.z, L.hi.x)  w[1] = (L.hi.y, L.hi.z, R.lo.x, R.lo.y)
+//   w[2] = (R.lo.z, R.hi.x, R.hi.y, R.hi.z)  w[3] = (child L, child R, -, -) as bits
+// The fp32 tests only filter (false positives are harmless: a leaf is a candidate only after the
+// reference's exact double slab test of its own box); the outward rounding plus the margin keep
+// every box a ray can hit in double inside what the fp32 test accepts.
+__device__ __forceinline__ void child_box(const BvhArgs& a, uint32_t ch, double b[6]) {
+    if (ch & kLeafBit) {
+        const uint32_t prim = a.leaf_prim[ch & ~kLeafBit];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) b[q] = a.posed[(13 + q) * a.n + prim];
+    } else {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) b[q] = a.node_box[6 * uint64_t(ch) + q];
+    }
+}
+
+__global__ void __launch_bounds__(256) bvh_widen_kernel(BvhArgs a) {
+    const int n = int(*a.n_leaves);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+        float f[12];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            double b[6];
+            child_box(a, a.child[2 * i + c], b);
+            const double m = 1e-5 * (fabs(b[0]) + fabs(b[1]) + fabs(b[2]) + fabs(b[3]) + fabs(b[4]) +
+                                     fabs(b[5])) + 1e-6;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                f[6 * c + q] = __double2float_rd(b[q] - m);
+                f[6 * c + 3 + q] = __double2float_ru(b[3 + q] + m);
+            }
+        }
+        float4* w = a.wide + 4 * uint64_t(i);
+        w[0] = make_float4(f[0], f[1], f[2], f[3]);
+        w[1] = make_float4(f[4], f[5], f[6], f[7]);
+        w[2] = make_float4(f[8], f[9], f[10], f[11]);
+        w[3] = make_float4(__uint_as_float(a.child[2 * i]), __uint_as_float(a.child[2 * i + 1]), 0.f, 0.f);
+    }
+}
+
+__device__ __forceinline__ bool slab_hit_f(float lx, float ly, float lz, float hx, float hy, float hz,
+                                           float3 o, float3 inv, float t_max) {
+    float t0 = 0.0f, t1 = t_max;
+    const float tx0 = (lx - o.x) * inv.x, tx1 = (hx - o.x) * inv.x;
+    t0 = fmaxf(t0, fminf(tx0, tx1));
+    t1 = fminf(t1, fmaxf(tx0, tx1));
+    const float ty0 = (ly - o.y) * inv.y, ty1 = (hy - o.y) * inv.y;
+    t0 = fmaxf(t0, fminf(ty0, ty1));
+    t1 = fminf(t1, fmaxf(ty0, ty1));
+    const float tz0 = (lz - o.z) * inv.z, tz1 = (hz - o.z) * inv.z;
+    t0 = fmaxf(t0, fminf(tz0, tz1));
+    t1 = fminf(t1, fmaxf(tz0, tz1));
+    return t0 <= t1 + 1e-4f * fabsf(t1) + 1e-6f;  // a margin for the fp32 rounding of the ts
+}
+
 // Candidates of every ray: count (list == nullptr) or fill (list at ray_offset[ray]).
 __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const LidarArgs la, int fill) {
     const int n = int(*a.n_leaves);
@@ -228,6 +287,10 @@ __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const Lidar
         const dv3 d = mk3(la.ray_dir[3 * ray], la.ray_dir[3 * ray + 1], la.ray_dir[3 * ray + 2]);
         const dv3 inv = mk3(1.0 / d.x, 1.0 / d.y, 1.0 / d.z);
         const double t_max = la.ray_tmax[ray];
+        const float3 of = make_float3(float(o.x), float(o.y), float(o.z));
+        const float3 invf = make_float3(float(inv.x), float(inv.y), float(inv.z));
+        // t_max rounded up (and +inf stays +inf): the fp32 range never ends before the double one
+        const float tmf = __double2float_ru(t_max);
         uint32_t count = 0;
         uint32_t* out = fill ? la.list + la.ray_offset[ray] : nullptr;
         auto leaf = [&](uint32_t sorted_idx) {
@@ -244,14 +307,20 @@ __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const Lidar
         } else if (n > 1) {
             uint32_t stack[64];
             int sp = 0;
-            stack[sp++] = 0u;
+            stack[sp++] = 0u;  // the root: its children's boxes are tested when it is visited
             while (sp > 0) {
                 const uint32_t node = stack[--sp];
-                const double* b = a.node_box + 6 * uint64_t(node);
-                if (!slab_hit(b[0], b[1], b[2], b[3], b[4], b[5], o, inv, t_max)) continue;
-                const uint32_t l = a.child[2 * node], r = a.child[2 * node + 1];
-                if (r & kLeafBit) leaf(r & ~kLeafBit); else stack[sp++] = r;
-                if (l & kLeafBit) leaf(l & ~kLeafBit); else stack[sp++] = l;
+                const float4* w = a.wide + 4 * uint64_t(node);
+                const float4 w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
+                const uint32_t l = __float_as_uint(w3.x), r = __float_as_uint(w3.y);
+                const bool hl = slab_hit_f(w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, of, invf, tmf);
+                const bool hr = slab_hit_f(w1.z, w1.w, w2.x, w2.y, w2.z, w2.w, of, invf, tmf);
+                if (hr) {
+                    if (r & kLeafBit) leaf(r & ~kLeafBit); else stack[sp++] = r;
+                }
+                if (hl) {
+                    if (l & kLeafBit) leaf(l & ~kLeafBit); else stack[sp++] = l;
+                }
                 GSIM_DCHECK(sp <= 64);
             }
         }
@@ -271,6 +340,7 @@ void launch_bvh_build(const BvhArgs& a, int n_sms, cudaStream_t s) {
 }
 void launch_bvh_refit(const BvhArgs& a, int n_sms, cudaStream_t s) {
     bvh_refit_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
+    bvh_widen_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
 }
 void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, bool fill, int n_sms, cudaStream_t s) {
     const uint64_t want = (la.n_rays + 127) / 128;

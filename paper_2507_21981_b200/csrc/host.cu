@@ -228,11 +228,13 @@ struct gsim_gpu_context {
         DevBuf<uint64_t> bvh_seg;
         DevBuf<unsigned long long> bvh_bounds;
         DevBuf<double> bvh_box;
+        DevBuf<float4> bvh_wide;
         std::vector<double> ray_key;  // (channels, step) of the sensor directions in rays
         void release() {
             for (int k = 0; k < 2; ++k) { bvh_keys[k].release(); bvh_vals[k].release(); }
             bvh_small.release(); bvh_nodes.release(); bvh_seg.release(); bvh_bounds.release();
             bvh_box.release();
+            bvh_wide.release();
             posed.release(); rays.release(); depth.release(); acc.release(); points.release();
             azimuth.release(); rank_elev.release(); seen.release(); ray_all.release();
             cand_t.release(); cand_r.release();
@@ -1616,6 +1618,7 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
     uint32_t* sm = L.bvh_small.ptr;
     L.bvh_nodes.reserve(5 * nn);  // child 2(n-1), node_parent n-1, leaf_parent n, visits n-1
     L.bvh_box.reserve(6 * nn);
+    L.bvh_wide.reserve(4 * nn);
     L.bvh_seg.reserve(2);
     L.bvh_bounds.reserve(6);
     const uint32_t chunks0 = uint32_t((n + kOnesweepTile - 1) / kOnesweepTile);
@@ -1646,6 +1649,7 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
     b.leaf_parent = L.bvh_nodes.ptr + 3 * nn;
     b.visits = L.bvh_nodes.ptr + 4 * nn;
     b.node_box = L.bvh_box.ptr;
+    b.wide = L.bvh_wide.ptr;
     launch_bvh_bounds(b, n_sms, s);
     launch_bvh_morton(b, n_sms, s);
     check_launch();

@@ -293,6 +293,7 @@ struct BvhArgs {
     uint32_t* leaf_parent;           // [n]
     uint32_t* visits;                // [n - 1] refit arrivals
     double* node_box;                // [n - 1][6]
+    float4* wide;                    // [n - 1][4] traversal nodes (bvh_widen_kernel)
 };
 
 void launch_bvh_bounds(const BvhArgs& a, int n_sms, cudaStream_t s);
