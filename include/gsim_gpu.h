@@ -128,7 +128,7 @@ typedef struct gsim_render_stats {
     uint64_t consumed;     /* pair-list entries the rasterizer fetched before saturating (K) */
     uint64_t h2d_bytes;    /* host->device bytes copied by the last call */
     uint64_t d2h_bytes;    /* device->host bytes copied by the last call */
-    uint32_t depth_passes; /* onesweep passes over the (camera | depth) record keys */
+    uint32_t depth_passes; /* segmented onesweep passes over the depth keys (per camera) */
     uint32_t chunks;       /* binning chunks (runs of depth-sorted records of one camera) */
     /* per-stage device milliseconds, filled when profiling is on (gsim_gpu_set_profiling) */
     float ms_preprocess;   /* K2 projection + SH */
