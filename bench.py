@@ -92,6 +92,42 @@ class ClockSampler:
         self.thread = None
         self.nvml = None
 
+    SMI_QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+
+    def _start_smi(self):
+        try:
+            fd, self.smi_path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.smi = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.SMI_QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.smi_path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.smi = None
+
+    def _stop_smi(self) -> dict | None:
+        if getattr(self, "smi", None) is None:
+            return None
+        time.sleep(0.25)
+        self.smi.terminate()
+        try:
+            self.smi.wait(timeout=5)
+        except Exception:
+            self.smi.kill()
+        rows = [[x.strip() for x in ln.split(",")] for ln in Path(self.smi_path).read_text().splitlines()]
+        os.unlink(self.smi_path)
+        rows = [r for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        sm = [float(r[1]) for r in rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)),
+                "sm_max_mhz": max(float(r[2]) for r in rows), "reasons": reasons,
+                "samples": len(rows), "source": "nvidia-smi, 100 ms"}
+
     def start(self):
         try:
             import pynvml
@@ -108,6 +144,7 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nvml = None
+            self._start_smi()
             return
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
@@ -125,7 +162,7 @@ class ClockSampler:
 
     def stop(self) -> dict | None:
         if self.nvml is None:
-            return None
+            return self._stop_smi()
         self.stop_ev.set()
         self.thread.join(timeout=2)
         pynvml, _ = self.nvml
