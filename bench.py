@@ -606,6 +606,8 @@ def run_cfg4(args, rank, world, local, dist):
                        "l2": "inputs larger than L2; no flush", "seed": 1000},
             "gpu_launches": int(launches),
             "gather_check": check,
+            "gather_mode": gather.mode if world > 1 else None,
+            "gather_fallback": gather.fallback,
             "setup_s": round(setup_s, 1),
             "machine": machine_descriptor(),
             "clocks": clocks,

@@ -136,11 +136,29 @@ class ChunkGather:
         self.mode = mode if self.world > 1 else "local"
         self.device = device
         self.peer = None
+        self.fallback = None
         if self.mode == "p2p":
-            # fused gather: every rank's compositing kernel stores into dst's HBM over NVLink
-            self.peer = PeerBuffer(n_envs * floats_per_env, device, self.rank, self.world, dst)
-            if self.rank == dst:
-                self.out = self.peer.view(0, n_envs * floats_per_env, device)
+            # fused gather: every rank's compositing kernel stores into dst's HBM over NVLink.
+            # Every rank must be able to map dst's buffer, else all fall back to NCCL together.
+            err = None
+            try:
+                self.peer = PeerBuffer(n_envs * floats_per_env, device, self.rank, self.world, dst)
+            except RuntimeError as e:
+                err = e
+            ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                              device=device if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 1:
+                if self.rank == dst:
+                    self.out = self.peer.view(0, n_envs * floats_per_env, device)
+            else:
+                if self.peer is not None:
+                    self.peer.close()
+                    self.peer = None
+                self.mode = "nccl"
+                self.fallback = f"p2p unavailable ({err or 'on another rank'}), NCCL used"
+        if self.mode == "p2p":
+            pass
         elif self.rank == dst:
             self.out = torch.empty(n_envs * floats_per_env, dtype=dtype, device=device)
         else:
