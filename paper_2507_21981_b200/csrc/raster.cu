@@ -17,7 +17,7 @@
 //      result equals the reference's skip-with-continue loop;
 //   4. a splat is composited only while T >= cutoff (a fourth condition of the gate), which is
 //      the reference's break after the accumulation that takes T below the cutoff; a warp stops
-//      when all its pixels are done and the CTA leaves when __syncthreads_count says every
+//      when all its pixels are done and the CTA leaves when the batch barrier's count says every
 //      pixel is. Lists whose splats all have peak opacity <= 0.989 skip the 0.99 clamp.
 //
 // Per-pixel contract (raster.cpp:215-249): box test |dx|>r || |dy|>r, q with 2*inv_xy,
@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     int buf = 0;
     for (uint32_t b0 = begin; b0 < end; b0 += kBatch, buf ^= 1) {
         const uint32_t n_b = (end - b0) < uint32_t(kBatch) ? (end - b0) : uint32_t(kBatch);
-        fetched += n_b;
         if constexpr (kBulk) {
             mbar_wait(bar0 + 8u * uint32_t(buf), (phase_bits >> buf) & 1u);
             phase_bits ^= 1u << buf;
@@ -319,7 +318,10 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         } else {
             asm volatile("cp.async.wait_all;" ::: "memory");
         }
-        __syncthreads();
+        // One barrier per batch: it publishes the batch's records, frees batch i-1's buffer and
+        // counts the pixels still compositing (the tile leaves once every pixel is done).
+        if (__syncthreads_count(T.x < cutoff && T.y < cutoff ? 0 : 1) == 0) break;
+        fetched += n_b;
         // every warp has left batch i-1, so its buffer takes batch i+1
         if (b0 + kBatch < end) {
             issue_copy(buf ^ 1);
@@ -363,7 +365,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
             else
                 blend_list<false>(s_list[warp], count, npx, py, cutoff, cr, cg, cb, d, acc, T);
         }
-        if (__syncthreads_count(T.x < cutoff && T.y < cutoff ? 0 : 1) == 0) break;
     }
     // no copy may land after the CTA exits
     if constexpr (kBulk) {
