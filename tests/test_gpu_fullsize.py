@@ -189,3 +189,17 @@ def test_config3_full_camera(ctx, oracle):
     _check(got[k], img, "cfg3 camera 1 (1280x720, 3M)")
     n = _lists_equal(ctx, k, splats, lists)
     assert n > 5_000_000
+
+
+def test_config1_options_full_size(ctx, oracle):
+    """RasterOptions at full size (raster.hpp:31-36): normalize_depth and a 1e-3 transmittance
+    cutoff on a config-1 camera, against the oracle; the tile lists do not depend on them."""
+    from paper_2507_21981_b200.api import RasterOptions
+    from paper_2507_21981_b200.scenes import config1
+    w = config1(seed=13)
+    nodes = w.frame_nodes(7)
+    cam = w.cameras[3]
+    opt = RasterOptions(normalize_depth=True, transmittance_cutoff=1e-3)
+    g = ctx.render(ctx.upload(w.field), nodes, [cam], opt)[0]
+    splats = oracle.project(w.field, nodes, cam)
+    _check(g, oracle.rasterize(splats, cam, opt), "cfg1 camera 3, normalize_depth + cutoff 1e-3")
