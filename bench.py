@@ -247,6 +247,8 @@ def run_ours(args, rank, world, local):
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     n_ctx = max(1, min(args.contexts, max(2, cores // max(local_world, 1) - 1)))
+    if len(w.cameras) > 32:
+        n_ctx = 1  # config 2: one context's workspaces are ~36 GB; its launches fill the GPU alone
     ctxs = [Context(local) for _ in range(n_ctx)]
     scenes = [c.upload(w.field) for c in ctxs]
     streams = [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local)) for c in ctxs]
