@@ -173,6 +173,10 @@ struct gsim_gpu_context {
     int staging_index = 0;
     PinnedBuf readback;
     cudaEvent_t bin_ev = nullptr;
+    // GSIM_GPU_BLOCKING_SYNC=1: the synchronous calls wait on blocking-sync events (the host
+    // thread sleeps instead of spinning; more renderer threads per core)
+    bool blocking_sync = false;
+    cudaEvent_t wait_ev[2] = {};
     // deferred pair-count check of the last asynchronous render (see check_pending)
     bool pending = false;
     float* pending_out = nullptr;
@@ -1349,6 +1353,20 @@ WaitValueFn wait_value_fn() {
     return fn;
 }
 
+// Waits for everything queued on the copy stream and the context stream (a synchronous call's
+// end): cudaStreamSynchronize, or blocking-sync events when the context asks for them.
+void wait_frame(gsim_gpu_context* ctx) {
+    if (!ctx->blocking_sync) {
+        if (ctx->copy_stream) GSIM_CK(cudaStreamSynchronize(ctx->copy_stream));
+        GSIM_CK(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
+    if (ctx->copy_stream) GSIM_CK(cudaEventRecord(ctx->wait_ev[0], ctx->copy_stream));
+    GSIM_CK(cudaEventRecord(ctx->wait_ev[1], ctx->stream));
+    if (ctx->copy_stream) GSIM_CK(cudaEventSynchronize(ctx->wait_ev[0]));
+    GSIM_CK(cudaEventSynchronize(ctx->wait_ev[1]));
+}
+
 // Per-camera copies of a host-target render, queued right after the raster launch: the copy
 // stream waits for each camera's tile counter, so camera c crosses PCIe while later cameras
 // (and other contexts' frames) are still being composited.
@@ -1760,6 +1778,10 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BULK")) ctx->raster_bulk = std::atoi(e) == 1 ? 1 : 0;
         if (const char* e = std::getenv("GSIM_GPU_OVERLAP_COPIES")) ctx->overlap_copies = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GSIM_GPU_BLOCKING_SYNC")) ctx->blocking_sync = std::atoi(e) == 1;
+        for (int k = 0; k < 2; ++k)
+            GSIM_CK(cudaEventCreateWithFlags(&ctx->wait_ev[k], cudaEventDisableTiming |
+                                             (ctx->blocking_sync ? cudaEventBlockingSync : 0)));
         if (const char* e = std::getenv("GSIM_GPU_GROUP_SLOTS")) {
             const uint64_t v = std::strtoull(e, nullptr, 10);
             if (v > 0 && v < ctx->group_slots) ctx->group_slots = v;
@@ -1833,6 +1855,8 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     for (auto& e : ctx->staging_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->bin_ev) cudaEventDestroy(ctx->bin_ev);
+    for (int k = 0; k < 2; ++k)
+        if (ctx->wait_ev[k]) cudaEventDestroy(ctx->wait_ev[k]);
     if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
@@ -2248,11 +2272,10 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
         }
         ctx->frame_outs = nullptr;
         if (overlap) {
-            GSIM_CK(cudaStreamSynchronize(ctx->copy_stream));
+            wait_frame(ctx);
             ctx->stats.d2h_bytes = 0;
             for (uint64_t c = 0; c < n_cameras; ++c)
                 ctx->stats.d2h_bytes += 5 * uint64_t(cameras[c].width) * cameras[c].height * sizeof(float);
-            GSIM_CK(cudaStreamSynchronize(ctx->stream));
             if (check_pending(ctx) || ctx->copies_stale) copy_targets(ctx, cameras, n_cameras, off, outs);
         } else {
             copy_targets(ctx, cameras, n_cameras, off, outs);
