@@ -70,13 +70,16 @@ class PeerBuffer:
         self.owner = rank == dst
         ptr = C.c_void_p()
         handle = (C.c_uint8 * 64)()
+        ok = True
         if self.owner:
-            st = self.lib.gsim_gpu_ipc_alloc(self.dev_index, 4 * n_floats, C.byref(ptr), handle)
-            if st != abi.GSIM_OK:
-                raise RuntimeError("gsim_gpu_ipc_alloc failed")
-        msg = [bytes(handle) if self.owner else None]
+            ok = self.lib.gsim_gpu_ipc_alloc(self.dev_index, 4 * n_floats, C.byref(ptr), handle) == abi.GSIM_OK
+        # the owner always takes part in the broadcast (None on failure), so no rank waits forever
+        msg = [bytes(handle) if (self.owner and ok) else None]
         if world > 1:
             dist.broadcast_object_list(msg, src=dst)
+        self.ptr, self.n = 0, n_floats
+        if msg[0] is None:
+            raise RuntimeError("gsim_gpu_ipc_alloc failed on the gathering rank")
         if not self.owner:
             h = (C.c_uint8 * 64).from_buffer_copy(msg[0])
             st = self.lib.gsim_gpu_ipc_open(self.dev_index, h, C.byref(ptr))
