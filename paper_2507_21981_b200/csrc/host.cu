@@ -116,6 +116,7 @@ struct Plan {
 enum Ev { kEvStart = 0, kEvPre, kEvDepth, kEvBin, kEvScatter, kEvRaster, kNumEv };
 
 constexpr int kZeroTickets = 1024; // 16 onesweep tickets
+constexpr int kRasterTicket = 12;  // the raster's tile counter (within the ticket words)
 constexpr int kZeroCams = 1040;    // per-camera visible counts
 
 }  // namespace
@@ -141,6 +142,7 @@ struct gsim_gpu_context {
     int raster_exact_cull = 1;       // GSIM_GPU_RASTER_EXACT=0: bounding-box warp culling only
     int raster_batch = 128;          // GSIM_GPU_RASTER_BATCH=256: larger K4 batches, fewer CTAs/SM
     int raster_bulk = 0;             // GSIM_GPU_RASTER_BULK=1: records staged by cp.async.bulk
+    int raster_ctas = 0;             // GSIM_GPU_RASTER_CTAS=k: k CTAs per SM looping over tiles
     // per-pair plane (final per-tile order)
     DevBuf<uint32_t> vals;
     uint64_t pair_capacity = 0;
@@ -712,6 +714,11 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.batch = ctx->raster_batch;
     rr.exact_cull = ctx->raster_exact_cull;
     rr.bulk_copy = ctx->raster_bulk;
+    rr.grid_cap = ctx->raster_ctas > 0 ? ctx->raster_ctas * ctx->num_sms : 0;
+    if (rr.grid_cap > 0 && uint32_t(rr.grid_cap) < p.tiles) {
+        rr.tile_ticket = ctx->zero_block.ptr + kZeroTickets + kRasterTicket;
+        GSIM_CK(cudaMemsetAsync(rr.tile_ticket, 0, sizeof(uint32_t), ctx->stream));
+    }
     rr.valid_alpha = ctx->frame_valid_alpha;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
     const bool overlap_enc = ctx->frame_enc_host && rr.enc.flags && wait_value_fn();
@@ -1777,6 +1784,7 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         if (const char* e = std::getenv("GSIM_GPU_RASTER_EXACT")) ctx->raster_exact_cull = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BATCH")) ctx->raster_batch = std::atoi(e) == 256 ? 256 : 128;
         if (const char* e = std::getenv("GSIM_GPU_RASTER_BULK")) ctx->raster_bulk = std::atoi(e) == 1 ? 1 : 0;
+        if (const char* e = std::getenv("GSIM_GPU_RASTER_CTAS")) ctx->raster_ctas = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("GSIM_GPU_OVERLAP_COPIES")) ctx->overlap_copies = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_BLOCKING_SYNC")) ctx->blocking_sync = std::atoi(e) == 1;
         for (int k = 0; k < 2; ++k)

@@ -120,6 +120,9 @@ struct RasterArgs {
     int batch;                       // records per shared-memory batch: 128 or 256
     int exact_cull;                  // exact ellipse-vs-warp-rectangle test in the compaction
     int bulk_copy;                   // stage records with cp.async.bulk + mbarrier (8x8 rects)
+    uint32_t n_tiles;                // tiles of the launch (set by launch_raster)
+    int grid_cap;                    // CTAs of the launch (0: one per tile)
+    uint32_t* tile_ticket;           // grid_cap > 0: tile counter, zero before the launch
     float valid_alpha;               // depth written as 0 where accum_alpha < valid_alpha
                                      // (render_depth_ring, transfer.cpp:116-118); 0 = off
     float* out;                      // per camera [rgb W*H*3 | depth W*H | alpha W*H]

@@ -215,13 +215,39 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     __shared__ Record s_null;  // pads the compacted lists: fails the box test (r = -1)
     __shared__ __align__(8) uint64_t s_bar[2];  // kBulk: one mbarrier per record buffer
 
-    const uint32_t g = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&s_bar[0]));
+    uint32_t phase_bits = 0;   // kBulk: parity of the next phase of each buffer's barrier
+    uint32_t pending_bulk = 0; // kBulk: buffers with copies issued and not yet waited for
+    if (tid == 0) {
+        s_null.a = make_float4(0.f, 0.f, -1.f, 0.f);
+        s_null.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        s_null.c = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kBulk) {
+            mbar_init(bar0, kThreads);
+            mbar_init(bar0 + 8u, kThreads);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+    }
+    if (kBulk) __syncthreads();  // barriers initialised before any thread arrives
+    const uint32_t null_addr = uint32_t(__cvta_generic_to_shared(&s_null));
+
+    // One CTA per tile, or (GSIM_GPU_RASTER_CTAS) a capped grid whose CTAs claim tiles in
+    // order from a counter (cameras still finish in order, for the per-camera copies, and the
+    // tail balances).
+    __shared__ uint32_t s_tile;
+    for (uint32_t g = blockIdx.x;;) {
+        if (a.tile_ticket) {
+            if (tid == 0) s_tile = atomicAdd(a.tile_ticket, 1u);
+            __syncthreads();
+            g = s_tile;
+        }
+        if (g >= a.n_tiles) break;
     const int cam_idx = upper_index(a.cam_tile_base, a.n_cams, g);
     const DevCamera& cam = a.cams[cam_idx];
     const uint32_t tile = g - a.cam_tile_base[cam_idx];
     const int tiles_x = cam.tiles_x;
     const int tx = int(tile % uint32_t(tiles_x)), ty = int(tile / uint32_t(tiles_x));
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rx0 = tx * kTileSize + (warp % WX) * RW, ry0 = ty * kTileSize + (warp / WX) * RH;
     const int x = rx0 + 2 * (lane % PC);  // first pixel of the pair
     const int y = ry0 + lane / PC;
@@ -251,9 +277,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
             slot_next[h] = i < end ? __ldg(a.values + i) : 0xFFFFFFFFu;
         }
     };
-    const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&s_bar[0]));
-    uint32_t phase_bits = 0;   // kBulk: parity of the next phase of each buffer's barrier
-    uint32_t pending_bulk = 0; // kBulk: buffers with copies issued and not yet waited for
     auto issue_copy = [&](int buf) {
 #pragma unroll
         for (int h = 0; h < kPerThread; ++h) {
@@ -290,18 +313,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    if (tid == 0) {
-        s_null.a = make_float4(0.f, 0.f, -1.f, 0.f);
-        s_null.b = make_float4(0.f, 0.f, 0.f, 0.f);
-        s_null.c = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (kBulk) {
-            mbar_init(bar0, kThreads);
-            mbar_init(bar0 + 8u, kThreads);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-    }
-    if (kBulk) __syncthreads();  // barriers initialised before any thread arrives
-    const uint32_t null_addr = uint32_t(__cvta_generic_to_shared(&s_null));
     uint32_t fetched = 0;
     if (begin < end) {
         load_slots(begin);
@@ -383,11 +394,19 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         __syncthreads();
         if (tid == 0) atomicAdd(a.cam_done + cam_idx, 1u);
     }
+    __syncthreads();  // the next tile reuses the record buffers and lists
+    if (!a.tile_ticket) break;  // one tile per CTA
+    }
 }
 
-void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream) {
+void launch_raster(const RasterArgs& a_in, uint32_t n_tiles, cudaStream_t stream) {
     if (n_tiles == 0) return;
+    RasterArgs a = a_in;
+    a.n_tiles = n_tiles;
     const bool small = a.batch == 128;
+    // capped grid: the CTAs loop over the tiles (leaves room on every SM for other contexts'
+    // kernels); 0 = one CTA per tile
+    if (a.grid_cap > 0 && uint32_t(a.grid_cap) < n_tiles) n_tiles = uint32_t(a.grid_cap);
     if (a.bulk_copy) {  // GSIM_GPU_RASTER_BULK=1 (A/B measurement)
         if (small) raster_kernel<8, 128, true><<<n_tiles, kThreads, 0, stream>>>(a);
         else raster_kernel<8, 256, true><<<n_tiles, kThreads, 0, stream>>>(a);
