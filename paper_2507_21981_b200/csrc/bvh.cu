@@ -277,7 +277,9 @@ __device__ __forceinline__ bool slab_hit_f(float lx, float ly, float lz, float h
     return t0 <= t1 + 1e-4f * fabsf(t1) + 1e-6f;  // a margin for the fp32 rounding of the ts
 }
 
-// Candidates of every ray: count (list == nullptr) or fill (list at ray_offset[ray]).
+// Candidates of every ray. mode 0: count into ray_count; 1: fill the list at ray_offset[ray];
+// 2: single pass, fill at ray * list_stride up to list_stride entries and count them all into
+// ray_count (the host falls back to count + fill when a ray overflows).
 __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const LidarArgs la, int fill) {
     const int n = int(*a.n_leaves);
     const uint64_t np = a.n;
@@ -292,13 +294,15 @@ __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const Lidar
         // t_max rounded up (and +inf stays +inf): the fp32 range never ends before the double one
         const float tmf = __double2float_ru(t_max);
         uint32_t count = 0;
-        uint32_t* out = fill ? la.list + la.ray_offset[ray] : nullptr;
+        uint32_t* out = fill == 1 ? la.list + la.ray_offset[ray]
+                      : fill == 2 ? la.list + ray * uint64_t(la.list_stride) : nullptr;
+        const uint32_t cap = fill == 2 ? la.list_stride : 0xFFFFFFFFu;
         auto leaf = [&](uint32_t sorted_idx) {
             const uint32_t prim = a.leaf_prim[sorted_idx];
             if (slab_hit(a.posed[13 * np + prim], a.posed[14 * np + prim], a.posed[15 * np + prim],
                          a.posed[16 * np + prim], a.posed[17 * np + prim], a.posed[18 * np + prim],
                          o, inv, t_max)) {
-                if (out) out[count] = prim;
+                if (out && count < cap) out[count] = prim;
                 ++count;
             }
         };
@@ -324,7 +328,8 @@ __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const Lidar
                 GSIM_DCHECK(sp <= 64);
             }
         }
-        if (!fill) la.ray_count[ray] = count;
+        if (fill != 1) la.ray_count[ray] = count;
+        if (fill == 2 && count > cap) atomicMax(a.overflow, count);
     }
 }
 
@@ -342,10 +347,10 @@ void launch_bvh_refit(const BvhArgs& a, int n_sms, cudaStream_t s) {
     bvh_refit_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
     bvh_widen_kernel<<<unsigned(n_sms * 8), 256, 0, s>>>(a);
 }
-void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, bool fill, int n_sms, cudaStream_t s) {
+void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, int mode, int n_sms, cudaStream_t s) {
     const uint64_t want = (la.n_rays + 127) / 128;
     bvh_collect_kernel<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(n_sms) * 16))),
-                         128, 0, s>>>(a, la, fill ? 1 : 0);
+                         128, 0, s>>>(a, la, mode);
 }
 
 }  // namespace gsim_gpu

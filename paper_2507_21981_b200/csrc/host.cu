@@ -235,6 +235,7 @@ struct gsim_gpu_context {
         DevBuf<unsigned long long> bvh_bounds;
         DevBuf<double> bvh_box;
         DevBuf<float4> bvh_wide;
+        uint32_t bvh_capacity = 256;  // candidate slots per ray of the single-pass collect
         std::vector<double> ray_key;  // (channels, step) of the sensor directions in rays
         void release() {
             for (int k = 0; k < 2; ++k) { bvh_keys[k].release(); bvh_vals[k].release(); }
@@ -1638,7 +1639,8 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
         L.bvh_vals[k].reserve(nn);
     }
     // small tables: [0..1023] hist (4 x 256), tickets [1024..1031], vbase [1040..1041],
-    // chunk_base0 [1044..1045], chunk_base1 [1048..1049], n_leaves [1052], cam_visible [1056]
+    // chunk_base0 [1044..1045], chunk_base1 [1048..1049], n_leaves [1052], cam_visible [1056],
+    // collect overflow [1060]
     L.bvh_small.reserve(1088);
     uint32_t* sm = L.bvh_small.ptr;
     L.bvh_nodes.reserve(5 * nn);  // child 2(n-1), node_parent n-1, leaf_parent n, visits n-1
@@ -1724,29 +1726,53 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
     launch_bvh_build(b, n_sms, s);
     launch_bvh_refit(b, n_sms, s);
     check_launch();
-    // candidate lists: count, scan, fill
+    // candidate lists: one pass into per-ray slots of the capacity learned from earlier calls
+    // (counting every candidate); a ray that overflows makes the lists exact: scan of the
+    // counts, then a fill pass at the offsets (and a larger capacity for the next call)
     const uint64_t R = la.n_rays;
     L.counts.reserve(std::max<uint64_t>(R, 1));
     L.offsets.reserve(R + 1);
     L.scratch.reserve((R + 1023) / 1024 + 2);
     la.ray_count = L.counts.ptr;
-    launch_bvh_collect(b, la, false, n_sms, s);
+    uint32_t cap = L.bvh_capacity;
+    constexpr uint64_t kSlotBudget = uint64_t(1) << 28;  // 5 GB of list + (t, response) slots
+    if (uint64_t(cap) * R > kSlotBudget) cap = uint32_t(std::max<uint64_t>(kSlotBudget / std::max<uint64_t>(R, 1), 16));
+    L.list.reserve(std::max<uint64_t>(uint64_t(cap) * R, 1));
+    L.cand_t.reserve(std::max<uint64_t>(uint64_t(cap) * R, 1));
+    L.cand_r.reserve(std::max<uint64_t>(uint64_t(cap) * R, 1));
+    b.overflow = sm + 1060;
+    GSIM_CK(cudaMemsetAsync(b.overflow, 0, sizeof(uint32_t), s));
+    la.list = L.list.ptr;
+    la.cand_t = L.cand_t.ptr;
+    la.cand_r = L.cand_r.ptr;
+    la.list_stride = cap;
+    la.list_count = L.counts.ptr;
+    launch_bvh_collect(b, la, 2, n_sms, s);
     check_launch();
     exclusive_scan_u32(L.counts.ptr, R, L.offsets.ptr, L.scratch.ptr, s);
     check_launch();
     unsigned long long total = 0;
+    uint32_t overflow = 0;
     GSIM_CK(cudaMemcpyAsync(&total, L.offsets.ptr + R, sizeof(total), cudaMemcpyDeviceToHost, s));
+    GSIM_CK(cudaMemcpyAsync(&overflow, b.overflow, sizeof(overflow), cudaMemcpyDeviceToHost, s));
     GSIM_CK(cudaStreamSynchronize(s));
     if (total >= (1ull << 32)) throw CudaError{"trace_rays: more than 2^32 ray candidates"};
-    L.list.reserve(std::max<unsigned long long>(total, 1));
-    L.cand_t.reserve(std::max<unsigned long long>(total, 1));
-    L.cand_r.reserve(std::max<unsigned long long>(total, 1));
-    la.ray_offset = L.offsets.ptr;
-    la.list = L.list.ptr;
-    la.cand_t = L.cand_t.ptr;
-    la.cand_r = L.cand_r.ptr;
-    launch_bvh_collect(b, la, true, n_sms, s);
-    check_launch();
+    if (overflow) {
+        uint32_t grow = 16;
+        while (grow < overflow && grow < (1u << 30)) grow <<= 1;
+        L.bvh_capacity = std::max(L.bvh_capacity, grow);
+        L.list.reserve(std::max<unsigned long long>(total, 1));
+        L.cand_t.reserve(std::max<unsigned long long>(total, 1));
+        L.cand_r.reserve(std::max<unsigned long long>(total, 1));
+        la.list = L.list.ptr;
+        la.cand_t = L.cand_t.ptr;
+        la.cand_r = L.cand_r.ptr;
+        la.list_stride = 0;
+        la.list_count = nullptr;
+        la.ray_offset = L.offsets.ptr;
+        launch_bvh_collect(b, la, 1, n_sms, s);
+        check_launch();
+    }
     la.ray_lists = 1;
     ctx->launches_total += 14;
     return total;

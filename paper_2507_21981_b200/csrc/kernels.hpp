@@ -237,6 +237,8 @@ struct LidarArgs {
     int scan;                        // 1: LiDAR grid scan, 0: arbitrary rays
     int ray_lists;                   // arbitrary rays: candidates in list/ray_offset (BVH), else
                                      // every primitive is a candidate
+    uint32_t list_stride;            // > 0: ray r's list at r * list_stride, list_count[r] long
+    const uint32_t* list_count;
     uint64_t n;                      // primitives
     double* posed;                   // [19][n]: mean xyz, inv_cov 9, opacity, lo xyz, hi xyz
     uint8_t* seen;                   // [n]
@@ -297,6 +299,7 @@ struct BvhArgs {
     uint32_t* visits;                // [n - 1] refit arrivals
     double* node_box;                // [n - 1][6]
     float4* wide;                    // [n - 1][4] traversal nodes (bvh_widen_kernel)
+    uint32_t* overflow;              // single-pass collect: largest count over the capacity
 };
 
 void launch_bvh_bounds(const BvhArgs& a, int n_sms, cudaStream_t s);
@@ -304,7 +307,7 @@ void launch_bvh_morton(const BvhArgs& a, int n_sms, cudaStream_t s);
 void launch_bvh_sort_setup(const BvhArgs& a, cudaStream_t s);
 void launch_bvh_build(const BvhArgs& a, int n_sms, cudaStream_t s);
 void launch_bvh_refit(const BvhArgs& a, int n_sms, cudaStream_t s);
-void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, bool fill, int n_sms, cudaStream_t s);
+void launch_bvh_collect(const BvhArgs& a, const LidarArgs& la, int mode, int n_sms, cudaStream_t s);
 
 void launch_lidar_pose(const LidarArgs& a, int n_sms, cudaStream_t s);
 void launch_lidar_rays(const double* ds, double* dw, uint64_t n, const double* q, int n_sms,

@@ -460,9 +460,10 @@ __global__ void __launch_bounds__(32 * kTraceWarps) lidar_trace_kernel(LidarArgs
         RayCands cs{};
         const bool brute = a.scan ? a.ray_all[ray / a.n_az] != 0 : a.ray_lists == 0;
         if (!brute) {
-            const uint64_t b = a.ray_offset[ray];
+            // lists at ray_offset (exact sizes) or, single-pass BVH lists, at ray * list_stride
+            const uint64_t b = a.list_stride ? ray * uint64_t(a.list_stride) : a.ray_offset[ray];
             cs.list = a.list + b;
-            cs.n_list = uint32_t(a.ray_offset[ray + 1] - b);
+            cs.n_list = a.list_stride ? a.list_count[ray] : uint32_t(a.ray_offset[ray + 1] - b);
             cs.extra = a.all_list;
             cs.n_extra = *a.all_count;
         }
@@ -470,7 +471,8 @@ __global__ void __launch_bounds__(32 * kTraceWarps) lidar_trace_kernel(LidarArgs
         Composite c;
         if (!brute) {
             // pass A: (t, response) of every candidate, cached (t = inf: not a survivor)
-            const uint64_t base = a.ray_offset[ray] + ray * uint64_t(cs.n_extra);
+            const uint64_t base = (a.list_stride ? ray * uint64_t(a.list_stride) : a.ray_offset[ray]) +
+                                  ray * uint64_t(cs.n_extra);
             double* ct = a.cand_t + base;
             double* cr = a.cand_r + base;
             for (uint32_t j = lane; j < nc; j += 32) {
