@@ -1813,6 +1813,8 @@ int gsim_gpu_context_create(int device, gsim_gpu_context** out) {
         if (const char* e = std::getenv("GSIM_GPU_RASTER_CTAS")) ctx->raster_ctas = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("GSIM_GPU_OVERLAP_COPIES")) ctx->overlap_copies = std::atoi(e) != 0;
         if (const char* e = std::getenv("GSIM_GPU_BLOCKING_SYNC")) ctx->blocking_sync = std::atoi(e) == 1;
+        if (const char* e = std::getenv("GSIM_GPU_BVH_CAPACITY"))  // tests: start small (overflow path)
+            ctx->lidar.bvh_capacity = uint32_t(std::max(1, std::atoi(e)));
         for (int k = 0; k < 2; ++k)
             GSIM_CK(cudaEventCreateWithFlags(&ctx->wait_ev[k], cudaEventDisableTiming |
                                              (ctx->blocking_sync ? cudaEventBlockingSync : 0)));

@@ -153,6 +153,32 @@ np.save(sys.argv[1], np.concatenate([hit.astype(np.float64), dep, acc]))
 """
 
 
+def test_trace_rays_bvh_list_overflow_path(tmp_path):
+    """Single-pass BVH lists start at 4 slots per ray (GSIM_GPU_BVH_CAPACITY): the first call
+    overflows and takes the exact count + scan + fill path, the second runs with the grown
+    capacity; both give the default's bits."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    script = BRUTE_SCRIPT.replace("hit, dep, acc = ctx.trace_rays(ctx.upload(f), [], org, d, t, 0.4)",
+                                  "s = ctx.upload(f)\n"
+                                  "ctx.trace_rays(s, [], org, d, t, 0.4)\n"
+                                  "hit, dep, acc = ctx.trace_rays(s, [], org, d, t, 0.4)")
+    outs = []
+    for cap in ("4", ""):
+        p = tmp_path / f"c{cap or 'def'}.npy"
+        env = dict(os.environ)
+        if cap:
+            env["GSIM_GPU_BVH_CAPACITY"] = cap
+        r = subprocess.run([sys.executable, "-c", script.format(root=root), str(p)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(p))
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_trace_rays_bvh_equals_every_primitive(tmp_path):
     """The BVH candidate lists and the every-primitive path (GSIM_GPU_TRACE_BRUTE=1) composite
     the same survivors in the same (t, index) order: bit-identical results."""
