@@ -484,3 +484,24 @@ def test_nine_bit_digit_sort_lists_bit_exact():
                        capture_output=True, text=True, timeout=900)
     print(r.stdout, r.stderr[-2000:])
     assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+
+
+def test_maximum_camera_size(ctx, oracle):
+    """The largest camera the binning's shared memory holds ((tiles_x + 1) *
+    (tiles_y + 1) <= 40960 cells, e.g. 3200x3200) renders with bit-exact tile lists; one tile
+    row more is refused with a validation error naming the limit."""
+    f = oracle.random_field(4242, 20000, 3.0, 0.005, 0.08, 1)
+    f.means[:, 2] += 2.5
+    f.touch()
+    cam = ref_camera(3200, 3200, 1600.0)
+    s = ctx.upload(f)
+    g = ctx.render(s, [], [cam])[0]
+    offsets, values = ctx.tile_lists(0)
+    splats = oracle.project(f, [], cam)
+    tb, vals = oracle.rasterize_lists(splats, cam)
+    assert np.array_equal(offsets[: len(tb)], tb)
+    assert np.array_equal(values, splats["prim_index"][vals])
+    assert_parity(g, oracle.rasterize(splats, cam), "3200x3200")
+    too_big = ref_camera(3200, 3280, 1600.0)  # (200 + 1) x (205 + 1) = 41406 cells
+    with pytest.raises(ValidationError, match="40960"):
+        ctx.render(s, [], [too_big])
