@@ -757,6 +757,10 @@ class Context:
         n = sum(o.bytes_per_camera(c.width, c.height) for c in cameras)
         if out is None:
             out = np.zeros(max(n, 1), dtype=np.uint8)
+        elif (not isinstance(out, np.ndarray) or out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]
+              or not out.flags["WRITEABLE"] or out.size < n):
+            raise ValidationError(f"render_encoded: out must be a writeable contiguous uint8 array of "
+                                  f">= {n} bytes")
         _check(self.lib.gsim_gpu_render_encoded(self.ptr, scene.handle, na, len(nodes), ca,
                                                 len(cameras), C.byref(opt), C.byref(oc),
                                                 out.ctypes.data_as(C.c_void_p), 0), self.ptr)
