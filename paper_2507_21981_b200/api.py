@@ -300,14 +300,23 @@ class RenderTarget:
 
 
 def _targets_array(targets, cams_c, n: int):
-    """C array of host targets, one per camera, each checked against its camera's size."""
+    """C array of host targets, one per camera, each checked against its camera's size. A
+    target already checked with the same three arrays and size reuses its C struct (callers
+    that render into the same targets every frame pay the checks once)."""
     targets = list(targets)
     if len(targets) != n:
         raise ValidationError(f"render: {len(targets)} targets for {n} cameras")
     ta = (abi.gsim_target * max(n, 1))()
     for k, t in enumerate(targets):
-        t.check(cams_c[k].width, cams_c[k].height, f"targets[{k}]")
-        ta[k] = t.to_c()
+        w, h = cams_c[k].width, cams_c[k].height
+        key = (id(t.rgb), id(t.depth), id(t.accum_alpha), w, h)
+        cached = getattr(t, "_c_cache", None)
+        if cached is None or cached[0] != key:
+            t.check(w, h, f"targets[{k}]")
+            # the cache holds the arrays themselves, so their ids cannot be reused while cached
+            cached = (key, t.to_c(), (t.rgb, t.depth, t.accum_alpha))
+            t._c_cache = cached
+        ta[k] = cached[1]
     return ta
 
 
