@@ -753,7 +753,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--contexts", type=int, default=4,
+    ap.add_argument("--contexts", type=int, default=5,
                     help="renderer contexts taking frames in turn (frame-level overlap)")
     ap.add_argument("--envs", type=int, default=512, help="cfg4: environments per step (box-wide)")
     ap.add_argument("--chunk-envs", type=int, default=64, help="cfg4: environments per launch")
