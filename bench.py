@@ -327,6 +327,10 @@ def run_ours(args, rank, world, local):
 
     # ---- e2e: public API, host buffers (pinned), H2D + D2H inside the timed region ------
     e2e = None
+    # The e2e legs run a steady-state window of at least 200 frames even when K is small: with
+    # 5 threads x K/5 synchronous frames each, a 20-frame run is mostly pipeline fill and drain.
+    # The window is reported (e2e.steps); the device-resident value above times exactly K.
+    e2e_steps = max(args.steps, 200)
     if not args.no_e2e:
         # One host thread per context (the ctypes call releases the GIL): while one context
         # copies its frame to the host the other renders the next one, which is how a caller
@@ -350,11 +354,11 @@ def run_ours(args, rank, world, local):
         from paper_2507_21981_b200.api import _cams_array, _nodes_array
         prebuilt = os.environ.get("BENCH_E2E_PYTHON_INPUTS") != "1"
         step_nodes = [_nodes_array(w.frame_nodes(10_000 + i, seed=rank)) if prebuilt else None
-                      for i in range(args.steps)]
+                      for i in range(e2e_steps)]
         cam_table = _cams_array(w.cameras) if prebuilt else w.cameras
 
         def worker(k):
-            for i in range(k, args.steps, len(ctxs)):
+            for i in range(k, e2e_steps, len(ctxs)):
                 nodes_i = step_nodes[i] if prebuilt else w.frame_nodes(10_000 + i, seed=rank)
                 ctxs[k].render(scenes[k], nodes_i, cam_table, None, targets[k])
             st = ctxs[k].stats()  # bytes copied by the context's last call (every call the same)
@@ -382,9 +386,9 @@ def run_ours(args, rank, world, local):
 
         te = timed_threads(worker)
         h2d, d2h = io[0]
-        e2e = {"value": round(world * args.steps * n_cams / (te / 1e3), 2), "unit": UNIT,
+        e2e = {"value": round(world * e2e_steps * n_cams / (te / 1e3), 2), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": round(te / args.steps, 4), "contexts": len(ctxs),
+               "ms_per_step": round(te / e2e_steps, 4), "contexts": len(ctxs), "steps": e2e_steps,
                "api": "gsim_gpu_render (host float targets, pinned)"}
 
         # Same loop through render_encoded: the compositing kernel writes
@@ -399,17 +403,17 @@ def run_ours(args, rank, world, local):
         io_enc = [[0, 0] for _ in ctxs]
 
         enc_nodes = [_nodes_array(w.frame_nodes(20_000 + i, seed=rank)) if prebuilt else None
-                     for i in range(args.steps)]
+                     for i in range(e2e_steps)]
 
         def worker_enc(k):
-            for i in range(k, args.steps, len(ctxs)):
+            for i in range(k, e2e_steps, len(ctxs)):
                 nodes_i = enc_nodes[i] if prebuilt else w.frame_nodes(20_000 + i, seed=rank)
                 ctxs[k].render_encoded(scenes[k], nodes_i, cam_table, None, eo, out=blobs[k])
             st = ctxs[k].stats()
             io_enc[k] = [st["h2d_bytes"], st["d2h_bytes"]]
 
         te2 = timed_threads(worker_enc)
-        e2e["encoded"] = {"value": round(world * args.steps * n_cams / (te2 / 1e3), 2),
+        e2e["encoded"] = {"value": round(world * e2e_steps * n_cams / (te2 / 1e3), 2),
                           "unit": UNIT, "h2d_bytes_per_step": int(io_enc[0][0]),
                           "d2h_bytes_per_step": int(io_enc[0][1]),
                           "outputs": "rgb8 sRGB + alpha8 + depth16 mm + depth PFM (10 B/px)"}
