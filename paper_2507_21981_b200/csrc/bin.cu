@@ -111,6 +111,57 @@ __device__ __forceinline__ void walk_groups(const BinArgs& a, uint32_t wb, uint3
     }
 }
 
+// walk_groups for the scatter: fn(slot, rect, valid, excl, total) also gets each lane's exclusive
+// prefix of the rect areas over its 32-record group and the group's pair total. The prefix
+// scans of the kG groups loaded together run interleaved (four independent shuffle chains
+// instead of four chains back to back).
+template <class F>
+__device__ __forceinline__ void walk_groups_scanned(const BinArgs& a, uint32_t wb, uint32_t we, F&& fn) {
+    constexpr int kG = 4;
+    const int lane = threadIdx.x & 31;
+    uint32_t slot[kG], rect[kG];
+    auto load = [&](uint32_t g0, uint32_t* sl, uint32_t* rc) {
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const uint32_t e = g0 + q * 32 + lane;
+            rc[q] = e < we ? __ldcs(a.sorted_rects + e) : 0u;
+            sl[q] = e < we ? __ldcs(a.sorted_slots + e) : 0u;
+        }
+    };
+    if (wb < we) load(wb, slot, rect);
+    for (uint32_t g0 = wb; g0 < we; g0 += 32 * kG) {
+        uint32_t nslot[kG], nrect[kG];
+        const uint32_t g1 = g0 + 32 * kG;
+        if (g1 < we) load(g1, nslot, nrect);
+        uint32_t cnt[kG], incl[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            cnt[q] = g0 + q * 32 + lane < we ? rect_area(rect[q]) : 0u;
+            incl[q] = cnt[q];
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t[kG];
+#pragma unroll
+            for (int q = 0; q < kG; ++q) t[q] = __shfl_up_sync(kFull, incl[q], o);
+#pragma unroll
+            for (int q = 0; q < kG; ++q)
+                if (lane >= o) incl[q] += t[q];
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            if (g0 + q * 32 >= we) break;
+            fn(slot[q], rect[q], g0 + q * 32 + lane < we, incl[q] - cnt[q],
+               __shfl_sync(kFull, incl[q], 31));
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            slot[q] = nslot[q];
+            rect[q] = nrect[q];
+        }
+    }
+}
+
 // Row-difference counting: +1 at (ty, tx0) and -1 at (ty, tx1 + 1) for every rect row of every
 // valid lane's record. D is [tiles_y][tiles_x + 1]; shared atomics (order is irrelevant here).
 __device__ __forceinline__ void add_rect_rows(int* D, int wd, uint32_t r, bool valid) {
@@ -459,8 +510,26 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         __syncwarp();
         walk_groups<false>(a, wb, we, [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
         __syncwarp();
-        for (int ty = 0; ty < u.tiles_y; ++ty)
-            scan_row(D, wd, ty, u.tiles_x, [&](int x, int v) { D[ty * wd + x] = v; });
+        // row prefixes with one lane per tile row: independent per-lane chains, no shuffles
+        // (row stride wd: conflict-free shared accesses when wd is odd)
+        for (int ty = lane; ty < u.tiles_y; ty += 32) {
+            int* row = D + ty * wd;
+            int acc = 0, x = 0;
+            for (; x + 8 <= u.tiles_x; x += 8) {
+                int v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = row[x + k];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    acc += v[k];
+                    row[x + k] = acc;
+                }
+            }
+            for (; x < u.tiles_x; ++x) {
+                acc += row[x];
+                row[x] = acc;
+            }
+        }
         __syncthreads();
         // 2. first position of every tile for every warp: camera base + tile base + units
         //    before this one + warps before this one
@@ -479,16 +548,9 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         }
         __syncthreads();
         // 3. place this warp's pairs in emission order
-        walk_groups<true>(a, wb, we, [&](uint32_t slot, uint32_t r, bool valid) {
+        walk_groups_scanned(a, wb, we, [&](uint32_t slot, uint32_t r, bool valid, uint32_t excl,
+                                           uint32_t total) {
             const uint32_t cnt = valid ? rect_area(r) : 0u;
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const uint32_t excl = incl - cnt;
-            const uint32_t total = __shfl_sync(kFull, incl, 31);
             const uint32_t magic = s_magic[((r >> 16) & 255u) - (r & 255u) + 1u];
             const uint32_t lanemask_le = lanemask_lt() | (1u << lane);
             int started = 0;  // records whose pair range starts before this step
