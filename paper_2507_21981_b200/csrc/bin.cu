@@ -9,7 +9,8 @@
 //             records; one W-warp CTA owns one unit, warp w its w-th 1024-record slice;
 //   count     per unit, pairs per tile: every record adds +1 / -1 at both ends of each of its
 //             rect rows in a shared row-difference array (red.shared), rows are then
-//             prefix-summed by warp scans; the row goes to a per-camera [unit][tile] matrix;
+//             prefix-summed (one thread per row); the row goes to a per-camera [unit][tile]
+//             matrix;
 //   colscan   per (camera, tile): exclusive scan over the camera's units (lanes = tiles,
 //             warps = unit segments);
 //   tilescan  per camera: exclusive scan of the tile totals -> tile ranges (raster.cpp:198-202);
@@ -174,23 +175,24 @@ __device__ __forceinline__ void add_rect_rows(int* D, int wd, uint32_t r, bool v
     }
 }
 
-// Inclusive prefix of row `row` of D (length n, row stride wd) by one warp; calls
-// out(x, value) for every x < n. Reads before writes within each 32-chunk.
-template <class F>
-__device__ __forceinline__ void scan_row(int* D, int wd, int row, int n, F&& out) {
-    const int lane = threadIdx.x & 31;
-    int carry = 0;
-    for (int x0 = 0; x0 < n; x0 += 32) {
-        const int x = x0 + lane;
-        int v = x < n ? D[row * wd + x] : 0;
+// In-place inclusive prefix of one tile row of n counters by one thread (rows of a table with
+// an odd stride sit in distinct banks, so the lanes of a warp scanning neighbouring rows do not
+// conflict); loads are batched 8 at a time so their latencies overlap.
+__device__ __forceinline__ void scan_row_serial(int* row, int n) {
+    int acc = 0, x = 0;
+    for (; x + 8 <= n; x += 8) {
+        int v[8];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(kFull, v, o);
-            if (lane >= o) v += t;
+        for (int k = 0; k < 8; ++k) v[k] = row[x + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc += v[k];
+            row[x + k] = acc;
         }
-        v += carry;
-        if (x < n) out(x, v);
-        carry = __shfl_sync(kFull, v, 31);
+    }
+    for (; x < n; ++x) {
+        acc += row[x];
+        row[x] = acc;
     }
 }
 
@@ -359,11 +361,18 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinArgs a) {
                            [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
         __syncthreads();
         uint32_t* mrow = a.counts + u.mbase + uint64_t(u.unit_in_cam) * u.tc;
-        for (int ty = warp; ty < u.tiles_y; ty += nw)
-            scan_row(D, wd, ty, u.tiles_x, [&](int x, int v) { mrow[ty * u.tiles_x + x] = uint32_t(v); });
+        // row prefixes in place, one thread per tile row, then one coalesced copy of the rows
+        for (int ty = threadIdx.x; ty < u.tiles_y; ty += blockDim.x) scan_row_serial(D + ty * wd, u.tiles_x);
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < u.tc; t += blockDim.x) {
+            const uint32_t ty = t / uint32_t(u.tiles_x), tx = t - ty * uint32_t(u.tiles_x);
+            mrow[t] = uint32_t(D[ty * uint32_t(wd) + tx]);
+        }
         __syncthreads();
     }
     (void)lane;
+    (void)warp;
+    (void)nw;
 }
 
 // ---- column scan: lanes = 32 consecutive (camera, tile) columns, warps = 8 unit segments ------
@@ -511,39 +520,33 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
         walk_groups<false>(a, wb, we, [&](uint32_t, uint32_t r, bool valid) { add_rect_rows(D, wd, r, valid); });
         __syncwarp();
         // row prefixes with one lane per tile row: independent per-lane chains, no shuffles
-        // (row stride wd: conflict-free shared accesses when wd is odd)
-        for (int ty = lane; ty < u.tiles_y; ty += 32) {
-            int* row = D + ty * wd;
-            int acc = 0, x = 0;
-            for (; x + 8 <= u.tiles_x; x += 8) {
-                int v[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = row[x + k];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    acc += v[k];
-                    row[x + k] = acc;
-                }
-            }
-            for (; x < u.tiles_x; ++x) {
-                acc += row[x];
-                row[x] = acc;
-            }
-        }
+        for (int ty = lane; ty < u.tiles_y; ty += 32) scan_row_serial(D + ty * wd, u.tiles_x);
         __syncthreads();
         // 2. first position of every tile for every warp: camera base + tile base + units
         //    before this one + warps before this one
         const uint32_t pbase = uint32_t(a.cam_pair_base[u.cam]);
         const uint32_t* mrow = a.counts + u.mbase + uint64_t(u.unit_in_cam) * u.tc;
-        for (uint32_t t = threadIdx.x; t < u.tc; t += blockDim.x) {
-            const uint32_t ty = t / uint32_t(u.tiles_x), tx = t - ty * uint32_t(u.tiles_x);
-            const uint32_t cell = ty * uint32_t(wd) + tx;
-            uint32_t base = pbase + a.tile_rel[u.tile_base + t] + mrow[t];
-            for (int w = 0; w < nw; ++w) {
-                uint32_t* pw = reinterpret_cast<uint32_t*>(s_bin + w * wbytes);
-                const uint32_t c = pw[cell];
-                pw[cell] = base;
-                base += c;
+        // four tiles per thread per round, their global loads issued together
+        for (uint32_t t0 = threadIdx.x; t0 < u.tc; t0 += 4 * blockDim.x) {
+            uint32_t base[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const uint32_t t = t0 + h * blockDim.x;
+                base[h] = t < u.tc ? pbase + a.tile_rel[u.tile_base + t] + mrow[t] : 0u;
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const uint32_t t = t0 + h * blockDim.x;
+                if (t >= u.tc) break;
+                const uint32_t ty = t / uint32_t(u.tiles_x), tx = t - ty * uint32_t(u.tiles_x);
+                const uint32_t cell = ty * uint32_t(wd) + tx;
+                uint32_t b = base[h];
+                for (int w = 0; w < nw; ++w) {
+                    uint32_t* pw = reinterpret_cast<uint32_t*>(s_bin + w * wbytes);
+                    const uint32_t c = pw[cell];
+                    pw[cell] = b;
+                    b += c;
+                }
             }
         }
         __syncthreads();
