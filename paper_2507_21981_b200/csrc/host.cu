@@ -135,6 +135,7 @@ struct gsim_gpu_context {
     DevBuf<uint32_t> keys;
     DevBuf<uint32_t> rects;
     DevBuf<uint32_t> dk[2], dv[2];   // depth-sort ping-pong
+    DevBuf<uint32_t> sort_rects;     // tile rects between depth passes (with the slot-order plane)
     DevBuf<uint64_t> status;         // onesweep lookback words
     DevBuf<uint32_t> sort_hist;      // [C][passes][radix] depth digit histograms (zeroed per frame)
     DevBuf<uint32_t> sort_chunk_base;  // [C+1] onesweep chunks of passes >= 2
@@ -612,6 +613,7 @@ void reserve_workspace(gsim_gpu_context* ctx, const Plan& p) {
     ctx->records.reserve(S);
     ctx->keys.reserve(S);
     ctx->rects.reserve(S);
+    ctx->sort_rects.reserve(S);
     for (int k = 0; k < 2; ++k) {
         ctx->dk[k].reserve(S);
         ctx->dv[k].reserve(S);
@@ -790,6 +792,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     dgrid = std::max<uint64_t>(1, std::min<uint64_t>(dgrid, uint64_t(n_sms) * sort_ctas));
     const uint32_t* kin = ctx->keys.ptr;
     const uint32_t* vin = nullptr;
+    const uint32_t* rin = ctx->rects.ptr;
     for (int pass = 0; pass < passes; ++pass) {
         const int o = pass & 1;
         const bool last = pass == passes - 1;
@@ -804,15 +807,17 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
         oa.ticket = ctx->zero_block.ptr + kZeroTickets + pass;
         oa.epoch = ctx->next_epoch();
         oa.shift = p.sort_bits * pass;
-        // the last pass writes no keys: it gathers the tile rects into depth order instead,
-        // into its own (unused) key output buffer
-        oa.rects_in = last ? ctx->rects.ptr : nullptr;
-        oa.rects_out = last ? ctx->dk[o].ptr : nullptr;
+        // the rects move with the keys: pass 1 reads them in slot order, the passes alternate
+        // between sort_rects and the slot-order rect plane (free once pass 1 has read it), and
+        // the last pass, which writes no keys, puts them into its own key output buffer
+        oa.rects_in = rin;
+        oa.rects_out = last ? ctx->dk[o].ptr : (pass & 1) ? ctx->rects.ptr : ctx->sort_rects.ptr;
         launch_onesweep(oa, p.sort_bits, pass == 0, !last, int(dgrid), s);
         check_launch();
         ++launches;
         kin = ctx->dk[o].ptr;
         vin = ctx->dv[o].ptr;
+        rin = oa.rects_out;
     }
     record_ev(ctx, kEvDepth);
 
@@ -1846,6 +1851,7 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->records.release();
     ctx->keys.release();
     ctx->rects.release();
+    ctx->sort_rects.release();
     for (int k = 0; k < 2; ++k) {
         ctx->dk[k].release();
         ctx->dv[k].release();

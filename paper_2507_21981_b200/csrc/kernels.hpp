@@ -65,8 +65,8 @@ struct OnesweepArgs {
     uint32_t* ticket;                // zeroed per pass
     uint32_t epoch;
     int shift;
-    const uint32_t* rects_in;        // last pass: gather rects_in[slot] ...
-    uint32_t* rects_out;             // ... into depth order (nullptr on the other passes)
+    const uint32_t* rects_in;        // tile rects moved with the keys (same positions as
+    uint32_t* rects_out;             // keys_in / keys_out); nullptr: keys and values only
     uint32_t backoff_ns;             // look-back retry sleep
 };
 

@@ -17,7 +17,9 @@
 //   * Every pass is single-sweep: chunks are claimed through an atomic ticket (so predecessors
 //     are always resident) and per-digit prefixes come from decoupled look-back over
 //     epoch-tagged status words (no clearing between passes).
-//   * The last pass also gathers every record's tile rect into depth order for the binning.
+//   * Every record's tile rect rides along as a third stream (read in slot order by pass 1,
+//     moved with its key by every pass), so the binning gets the rects in depth order without
+//     a random gather (optional: rects_in == nullptr sorts keys and values only).
 #include <cstdint>
 
 #include "common.cuh"
@@ -79,13 +81,15 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
     constexpr int kRadix = 1 << kBits;
     constexpr int kDpt = kRadix / kThreads;  // 1 (8-bit digits) or 2 (9-bit)
     constexpr uint32_t kMask = kRadix - 1;
-    // dynamic: [keys | values of the staged chunk][per-warp digit counts][per-warp digit
-    // bitmaps] (launch_one)
+    // dynamic: [keys | values | rects of the staged chunk][per-warp digit counts][per-warp
+    // digit bitmaps] (launch_one)
     extern __shared__ __align__(16) uint32_t s_dyn[];
     uint32_t* s_keys = s_dyn;
     uint32_t* s_vals = s_dyn + kOnesweepTile;
-    auto s_warp_hist = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 2 * kOnesweepTile);
-    auto s_peer = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 2 * kOnesweepTile + kWarps * kRadix);
+    uint32_t* s_rects = s_dyn + 2 * kOnesweepTile;
+    auto s_warp_hist = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 3 * kOnesweepTile);
+    auto s_peer = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 3 * kOnesweepTile + kWarps * kRadix);
+    const bool carry = a.rects_in != nullptr;
     __shared__ uint32_t s_bstart[kRadix];
     __shared__ uint32_t s_dest[kRadix];
     __shared__ uint32_t s_tmp[kWarps];
@@ -177,6 +181,18 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
             rank[i] = valid ? (pre + __popc(below)) : 0xFFFFFFFFu;
             __syncwarp();  // the leader's updates are visible before the next item's reads
         }
+        // the rects (coalesced, same positions as the keys) are copied into s_rects in load order
+        // with cp.async, in flight during the look-back without holding registers
+        if (carry) {
+            const uint32_t* rin = a.rects_in + base;
+            const uint32_t raw = uint32_t(__cvta_generic_to_shared(s_rects + warp * (kItems * 32) + lane));
+#pragma unroll
+            for (int i = 0; i < kItems; ++i)
+                if (rank[i] != 0xFFFFFFFFu)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(raw + 128u * i),
+                                 "l"(rin + i * 32) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         __syncthreads();
         // Per digit (thread = kDpt digits): exclusive prefix across warps, block count.
         uint32_t count[kDpt], loc = 0;
@@ -247,6 +263,17 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
             GSIM_DCHECK(pos < uint32_t(kOnesweepTile));
             s_keys[pos] = keys[i];
             s_vals[pos] = vals[i];
+            rank[i] = pos;
+        }
+        if (carry) {  // the rects: load order -> registers -> sorted order
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            uint32_t rc[kItems];
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) rc[i] = s_rects[warp * (kItems * 32) + i * 32 + lane];
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < kItems; ++i)
+                if (rank[i] != 0xFFFFFFFFu) s_rects[rank[i]] = rc[i];
         }
         __syncthreads();
         const uint32_t total = s_total;
@@ -257,27 +284,15 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
                 GSIM_DCHECK(dst >= a.vbase[cam] && dst < a.vbase[cam + 1]);
                 a.keys_out[dst] = key;
                 a.vals_out[dst] = s_vals[p];
+                if (carry) a.rects_out[dst] = s_rects[p];
             }
         } else {
-            // last pass: gather the tile rects of the sorted slots, all kItems loads of a
-            // thread in flight before its stores (random 4-byte reads; latency-bound otherwise)
-            uint32_t dst[kItems], val[kItems], rect[kItems];
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                const uint32_t p = uint32_t(tid) + uint32_t(i) * kThreads;
-                const bool in = p < total;
-                val[i] = in ? s_vals[p] : 0u;
-                dst[i] = in ? s_dest[(s_keys[p] >> a.shift) & kMask] + p : 0xFFFFFFFFu;
-            }
-#pragma unroll
-            for (int i = 0; i < kItems; ++i)
-                rect[i] = dst[i] != 0xFFFFFFFFu ? __ldg(a.rects_in + val[i]) : 0u;
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {
-                if (dst[i] == 0xFFFFFFFFu) continue;
-                GSIM_DCHECK(dst[i] >= a.vbase[cam] && dst[i] < a.vbase[cam + 1]);
-                a.vals_out[dst[i]] = val[i];
-                a.rects_out[dst[i]] = rect[i];
+            // last pass: slots and rects in depth order, no keys
+            for (uint32_t p = tid; p < total; p += kThreads) {
+                const uint32_t dst = s_dest[(s_keys[p] >> a.shift) & kMask] + p;
+                GSIM_DCHECK(dst >= a.vbase[cam] && dst < a.vbase[cam + 1]);
+                a.vals_out[dst] = s_vals[p];
+                if (carry) a.rects_out[dst] = s_rects[p];
             }
         }
         __syncthreads();
@@ -287,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
 // ---- launchers -----------------------------------------------------------------------------
 template <int kBits, bool kFirst, bool kWriteKeys>
 static void launch_one(const OnesweepArgs& a, int grid, cudaStream_t s) {
-    const int smem = int((2 * kOnesweepTile + 2 * kWarps * (1 << kBits)) * sizeof(uint32_t));
+    const int smem = int((3 * kOnesweepTile + 2 * kWarps * (1 << kBits)) * sizeof(uint32_t));
     cudaFuncSetAttribute(onesweep_kernel<kBits, kFirst, kWriteKeys>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     onesweep_kernel<kBits, kFirst, kWriteKeys><<<grid, kThreads, smem, s>>>(a);
