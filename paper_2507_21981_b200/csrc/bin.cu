@@ -44,6 +44,7 @@ __device__ __forceinline__ uint32_t rect_area(uint32_t r) {
 
 // Per-warp scatter tables: u32 counters / positions per cell plus either a u32 lane bitmap
 // (bitmap peers) or a u8 last-writer probe (large cameras: a quarter of the bytes).
+constexpr int kSpare = 32;
 __host__ __device__ inline size_t bin_warp_bytes(int max_cells, bool bitmap) {
     return bitmap ? size_t(max_cells) * 8 : (size_t(max_cells) * 5 + 15) & ~size_t(15);
 }
@@ -492,9 +493,12 @@ template <bool kBitmap>
 __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     extern __shared__ __align__(16) char s_bin[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const size_t wbytes = bin_warp_bytes(a.max_tc, kBitmap);
+    // bitmap peers: kSpare extra cells per table, one per lane, take the lanes of a step that
+    // have no pair, so every lane runs the same shared-memory sequence without branches
+    const int cells = a.max_tc + (kBitmap ? kSpare : 0);
+    const size_t wbytes = bin_warp_bytes(cells, kBitmap);
     uint32_t* pos = reinterpret_cast<uint32_t*>(s_bin + warp * wbytes);
-    uint32_t* peer_bits = pos + a.max_tc;
+    uint32_t* peer_bits = pos + cells;
     uint8_t* probe = reinterpret_cast<uint8_t*>(pos + a.max_tc);
     // row-major position -> (row, column) with a magic reciprocal per rect width: for
     // kk < 2^16 and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     // the lane bitmaps are cleared once over the batch's largest grid; every placement step
     // leaves them cleared, so units of any camera (a block may take several) start clean
     if (kBitmap)
-        for (int t = lane; t < a.max_tc; t += 32) peer_bits[t] = 0u;
+        for (int t = lane; t < cells; t += 32) peer_bits[t] = 0u;
     __syncthreads();
     const uint32_t K = *a.n_chunks;
     // pair positions are 32-bit; a capacity beyond that bounds nothing
@@ -582,20 +586,19 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                     // Every lane reads the cell's position together with the bitmap (same-address
                     // reads broadcast), so no shuffle from the leader sits on the chain; the
                     // leader's update follows a warp barrier that orders it after all reads.
-                    if (in) atomicOr(&peer_bits[cell], 1u << lane);
+                    const uint32_t c = in ? cell : uint32_t(a.max_tc + lane);  // spare: alone
+                    atomicOr(&peer_bits[c], 1u << lane);
                     __syncwarp();
-                    const uint32_t peers = in ? peer_bits[cell] : 0u;
-                    const uint32_t pre = in ? pos[cell] : 0u;
+                    const uint32_t peers = peer_bits[c];
+                    const uint32_t pre = pos[c];
                     const uint32_t below = peers & lanemask_lt();
                     __syncwarp();
-                    if (in && below == 0) {
-                        pos[cell] = pre + __popc(peers);
-                        peer_bits[cell] = 0u;
+                    if (below == 0) {
+                        pos[c] = pre + __popc(peers);
+                        peer_bits[c] = 0u;
                     }
-                    if (in) {
-                        const uint32_t p = pre + __popc(below);
-                        if (p < cap32) a.vals_out[p] = sl;
-                    }
+                    const uint32_t p = pre + __popc(below);
+                    if (in && p < cap32) a.vals_out[p] = sl;
                 } else {
                     // last-writer probe: did another lane of this step write the same cell?
                     if (in) probe[cell] = uint8_t(lane);
@@ -636,7 +639,7 @@ void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
 }
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 256, 0, s>>>(a); }
 size_t bin_smem_bytes(const BinArgs& a) {
-    return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc, a.bitmap_peers != 0);
+    return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc + (a.bitmap_peers ? kSpare : 0), a.bitmap_peers != 0);
 }
 void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = size_t(a.max_tc) * sizeof(int);
