@@ -87,8 +87,11 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
     uint32_t* s_keys = s_dyn;
     uint32_t* s_vals = s_dyn + kOnesweepTile;
     uint32_t* s_rects = s_dyn + 2 * kOnesweepTile;
-    auto s_warp_hist = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 3 * kOnesweepTile);
-    auto s_peer = reinterpret_cast<uint32_t(*)[kRadix]>(s_dyn + 3 * kOnesweepTile + kWarps * kRadix);
+    // rows of kRow words: the kRadix digits, then one spare word per lane that an invalid item
+    // ranks in alone (so every lane runs the same shared-memory sequence, without branches)
+    constexpr int kRow = kRadix + 32;
+    auto s_warp_hist = reinterpret_cast<uint32_t(*)[kRow]>(s_dyn + 3 * kOnesweepTile);
+    auto s_peer = reinterpret_cast<uint32_t(*)[kRow]>(s_dyn + 3 * kOnesweepTile + kWarps * kRow);
     const bool carry = a.rects_in != nullptr;
     __shared__ uint32_t s_bstart[kRadix];
     __shared__ uint32_t s_dest[kRadix];
@@ -101,11 +104,11 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
     const uint32_t* seg32 = a.seg_base32;
     int cam_cached = -1;
     uint32_t gbase[kDpt];  // output position of each of this thread's digits, this camera
-    for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_peer[0][0])[k] = 0;
+    for (int k = tid; k < kWarps * kRow; k += kThreads) (&s_peer[0][0])[k] = 0;
 
     while (true) {
         if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
-        for (int k = tid; k < kWarps * kRadix; k += kThreads) (&s_warp_hist[0][0])[k] = 0;
+        for (int k = tid; k < kWarps * kRow; k += kThreads) (&s_warp_hist[0][0])[k] = 0;
         __syncthreads();
         const uint32_t t = s_ticket;
         if (t >= n_chunks) break;
@@ -166,15 +169,16 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
             // The digit's warp count is read by every peer together with the bitmap (the
             // histogram is warp-private: no atomic, no shuffle from the leader); the leader
             // bumps it and clears the bitmap after a warp barrier orders that after all reads.
-            uint32_t* bits = &s_peer[warp][d];
-            uint32_t* cnt = &s_warp_hist[warp][d];
-            if (valid) atomicOr(bits, 1u << lane);
+            const uint32_t dd = valid ? d : uint32_t(kRadix + lane);
+            uint32_t* bits = &s_peer[warp][dd];
+            uint32_t* cnt = &s_warp_hist[warp][dd];
+            atomicOr(bits, 1u << lane);
             __syncwarp();
-            const uint32_t peers = valid ? *bits : 0u;
-            const uint32_t pre = valid ? *cnt : 0u;
+            const uint32_t peers = *bits;
+            const uint32_t pre = *cnt;
             const uint32_t below = peers & lanemask_lt();
             __syncwarp();
-            if (valid && below == 0) {
+            if (below == 0) {
                 *cnt = pre + uint32_t(__popc(peers));
                 *bits = 0u;
             }
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, kOnesweepMinBlocks) onesweep_kernel(
 // ---- launchers -----------------------------------------------------------------------------
 template <int kBits, bool kFirst, bool kWriteKeys>
 static void launch_one(const OnesweepArgs& a, int grid, cudaStream_t s) {
-    const int smem = int((3 * kOnesweepTile + 2 * kWarps * (1 << kBits)) * sizeof(uint32_t));
+    const int smem = int((3 * kOnesweepTile + 2 * kWarps * ((1 << kBits) + 32)) * sizeof(uint32_t));
     cudaFuncSetAttribute(onesweep_kernel<kBits, kFirst, kWriteKeys>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     onesweep_kernel<kBits, kFirst, kWriteKeys><<<grid, kThreads, smem, s>>>(a);
