@@ -493,13 +493,13 @@ template <bool kBitmap>
 __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
     extern __shared__ __align__(16) char s_bin[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // bitmap peers: kSpare extra cells per table, one per lane, take the lanes of a step that
-    // have no pair, so every lane runs the same shared-memory sequence without branches
-    const int cells = a.max_tc + (kBitmap ? kSpare : 0);
+    // kSpare extra cells per table, one per lane, take the lanes of a step that have no pair,
+    // so every lane runs the same shared-memory sequence without branches
+    const int cells = a.max_tc + kSpare;
     const size_t wbytes = bin_warp_bytes(cells, kBitmap);
     uint32_t* pos = reinterpret_cast<uint32_t*>(s_bin + warp * wbytes);
     uint32_t* peer_bits = pos + cells;
-    uint8_t* probe = reinterpret_cast<uint8_t*>(pos + a.max_tc);
+    uint8_t* probe = reinterpret_cast<uint8_t*>(pos + cells);
     // row-major position -> (row, column) with a magic reciprocal per rect width: for
     // kk < 2^16 and width w <= 256, umulhi(kk, 0xFFFFFFFF / w + 1) == kk / w exactly.
     __shared__ uint32_t s_magic[257];
@@ -601,15 +601,14 @@ __global__ void __launch_bounds__(kThreads) bin_scatter_kernel(BinArgs a) {
                     if (in && p < cap32) a.vals_out[p] = sl;
                 } else {
                     // last-writer probe: did another lane of this step write the same cell?
-                    if (in) probe[cell] = uint8_t(lane);
+                    const uint32_t c = in ? cell : uint32_t(a.max_tc + lane);  // spare: alone
+                    probe[c] = uint8_t(lane);
                     __syncwarp();
-                    const bool lost = in && probe[cell] != uint8_t(lane);
+                    const bool lost = probe[c] != uint8_t(lane);
                     if (!__any_sync(kFull, lost)) {
-                        if (in) {
-                            const uint32_t p = pos[cell];
-                            pos[cell] = p + 1u;
-                            if (p < cap32) a.vals_out[p] = sl;
-                        }
+                        const uint32_t p = pos[c];
+                        pos[c] = p + 1u;
+                        if (in && p < cap32) a.vals_out[p] = sl;
                     } else {  // rank the lanes of each cell by lane order from ballots
                         const uint32_t m = __ballot_sync(kFull, in);
                         const uint32_t tile = (ty0 + q) * uint32_t(u.tiles_x) + tx0 + (kk - q * w);
@@ -639,7 +638,7 @@ void launch_key_hist(const BinArgs& a, int grid, cudaStream_t s) {
 }
 void launch_chunk_table(const BinArgs& a, cudaStream_t s) { chunk_table_kernel<<<1, 256, 0, s>>>(a); }
 size_t bin_smem_bytes(const BinArgs& a) {
-    return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc + (a.bitmap_peers ? kSpare : 0), a.bitmap_peers != 0);
+    return size_t(a.bin_warps) * bin_warp_bytes(a.max_tc + kSpare, a.bitmap_peers != 0);
 }
 void launch_bin_count(const BinArgs& a, int grid, cudaStream_t s) {
     const size_t smem = size_t(a.max_tc) * sizeof(int);

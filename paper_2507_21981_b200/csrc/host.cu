@@ -581,8 +581,8 @@ int bin_warps_for(uint32_t max_tc) {
         const int v = e ? std::atoi(e) : 4;  // 4 measured faster than 8 (occupancy)
         return v >= 1 && v <= 8 ? v : 4;
     }();
-    const size_t per_warp = bitmap_peers_for(max_tc) ? size_t(max_tc) * 8
-                                                     : (size_t(max_tc) * 5 + 15) & ~size_t(15);
+    const size_t cells = size_t(max_tc) + 32;  // + one spare cell per lane (bin.cu kSpare)
+    const size_t per_warp = bitmap_peers_for(max_tc) ? cells * 8 : (cells * 5 + 15) & ~size_t(15);
     const size_t budget = 200 * 1024;
     const int w = int(std::min<size_t>(size_t(cap), budget / std::max<size_t>(per_warp, 1)));
     if (w < 1)
