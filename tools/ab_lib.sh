@@ -14,6 +14,6 @@ for i in $(seq "$R"); do
     timeout 300 python bench.py "$@" 2>/dev/null | python -c "
 import json, sys
 d = json.loads([l for l in sys.stdin if l.startswith('{')][-1])
-print('$(basename "$v")', d['value'], d['e2e']['value'], d['roofline']['stages_ms'])"
+print('$(basename "$v")', d['value'], d['e2e']['value'], d['roofline']['stages_ms'], d.get('first_frame_hash'))"
   done
 done
