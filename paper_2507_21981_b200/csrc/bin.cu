@@ -2,7 +2,7 @@
 //
 // The reference emits (tile << 32 | depth, splat) pairs and std::sorts them
 // (raster.cpp:174-202). After the camera-major depth sort of the V visible records
-// (sort.cu, whose last pass also gathers every record's tile rect into depth order), the pair
+// (sort.cu, which carries every record's tile rect through its passes into depth order), the pair
 // order we need is simply "by (camera, tile), then by record order". Instead of radix-sorting
 // the P ~ 3.5 V pairs by tile, every pair is placed directly:
 //   units     the depth-sorted records of each camera are cut into units of R = 1024 * W

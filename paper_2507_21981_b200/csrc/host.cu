@@ -660,7 +660,7 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p) {
     b.sort_bits = p.sort_bits;
     b.sort_passes = p.sort_passes;
     b.n_cams = int(p.cams.size());
-    // the last depth pass writes the slots into dv[o] and gathers the rects into dk[o]
+    // the last depth pass writes the slots into dv[o] and the carried rects into dk[o]
     const int last_o = (p.sort_passes - 1) & 1;
     b.sorted_slots = ctx->dv[last_o].ptr;
     b.sorted_rects = ctx->dk[last_o].ptr;
