@@ -389,8 +389,12 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
     write_pixel(a, cam, x, y, cr.x, cg.x, cb.x, d.x, acc.x);
     write_pixel(a, cam, x + 1, y, cr.y, cg.y, cb.y, d.y, acc.y);
-    if (a.cam_done) {  // the tile's pixels are visible to the copy engine before it is counted
-        __threadfence_system();
+    if (a.cam_done) {
+        // The tile's pixels are performed at GPU scope before it is counted: the copy engine
+        // that the counter releases reads this device memory through the same L2 as the
+        // counter's wait, so a GPU-scope fence orders them (a system-scope fence, needed only
+        // for observers outside the GPU, cost 4% of the float e2e rate at config 1).
+        __threadfence();
         __syncthreads();
         if (tid == 0) atomicAdd(a.cam_done + cam_idx, 1u);
     }

@@ -139,3 +139,47 @@ def test_pinned_and_pageable_targets_agree(oracle):
         want = ctx.render(s, nodes, cams)
         got = ctx.render(s, nodes, cams, None, pinned)
         assert all(same(a, b) for a, b in zip(got, want))
+
+
+def test_overlapped_copies_never_stale(oracle):
+    """The per-camera copies start when the camera's tile counter says every tile is composited
+    (raster epilogue: GPU-scope fence, then the counter). Stress that handoff: 4 contexts on 4
+    threads render 24 frames each into page-locked targets reused frame after frame, so a copy
+    that overtook a tile's pixel stores would leave the previous frame's pixels in the target.
+    Every frame must equal the same frame rendered alone. (A regression guard: the copy starts
+    microseconds after the counter is seen, far longer than the fence's window; even a build
+    without the fence passed this test, so the fence's scope rests on the L2 argument in
+    raster.cu.)"""
+    import torch
+    from paper_2507_21981_b200 import RenderTarget
+    field, cams, frames = scene_and_frames(oracle, 12)
+    solo = Context(0)
+    s0 = solo.upload(field)
+    want = [solo.render(s0, nodes, cams) for nodes in frames]
+
+    def pinned():
+        return [RenderTarget(torch.empty((c.height, c.width, 3), pin_memory=True).numpy(),
+                             torch.empty((c.height, c.width), pin_memory=True).numpy(),
+                             torch.empty((c.height, c.width), pin_memory=True).numpy()) for c in cams]
+    ctxs = [Context(0) for _ in range(4)]
+    scenes = [c.upload(field) for c in ctxs]
+    bad, errors = [], []
+
+    def worker(k):
+        try:
+            tg = pinned()
+            for rep in range(24):
+                i = (k + 5 * rep) % len(frames)
+                out = ctxs[k].render(scenes[k], frames[i], cams, None, tg)
+                if not all(same(a, b) for a, b in zip(out, want[i])):
+                    bad.append((k, rep, i))
+        except Exception as e:  # noqa: BLE001 (reported below)
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(ctxs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert not bad, bad
