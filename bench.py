@@ -248,7 +248,11 @@ def run_ours(args, rank, world, local):
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     n_ctx = max(1, min(args.contexts, max(2, cores // max(local_world, 1) - 1)))
     if len(w.cameras) > 32:
-        n_ctx = 1  # config 2: one context's workspaces are ~36 GB; its launches fill the GPU alone
+        # config 2: one context's workspaces are ~36 GB and its launches fill the GPU; a second
+        # context overlaps one batch's host copies with the next batch (measured: e2e 4,223 ->
+        # 5,866, value 6,123 -> 6,225; a third adds nothing), when HBM holds both
+        free = torch.cuda.mem_get_info(local)[0]
+        n_ctx = min(n_ctx, 2 if free > 2 * (48 << 30) else 1)
     ctxs = [Context(local) for _ in range(n_ctx)]
     scenes = [c.upload(w.field) for c in ctxs]
     streams = [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local)) for c in ctxs]
