@@ -24,6 +24,7 @@
 // alpha = min(o*exp(-q/2), 0.99), skip alpha < 1/255, accumulate, T *= 1-alpha, stop after
 // accumulating once T < cutoff; rgb clamped to [0,1] at write, depth unnormalised unless
 // asked, accum_alpha = sum of weights. Empty tiles write zeros (image.hpp:44).
+#include <climits>
 #include <cstdint>
 
 #include "common.cuh"
@@ -254,8 +255,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     const float2 npx = make_float2(-(float(x) + 0.5f), -(float(x) + 1.5f));
     const float py = float(y) + 0.5f;
     // pixel-centre bounds of this warp's rectangle
-    const float wx_lo = float(rx0) + 0.5f, wx_hi = wx_lo + float(RW - 1);
-    const float wy_lo = float(ry0) + 0.5f, wy_hi = wy_lo + float(RH - 1);
 
     // On a pair-buffer overflow the host re-runs scatter + raster; until then keep every read
     // in bounds (the clamped frame is discarded).
@@ -340,8 +339,18 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         }
 
         if (!__all_sync(0xffffffffu, T.x < cutoff && T.y < cutoff)) {
-            // Compact the splats that can reach this warp's rectangle (depth order preserved)
-            // as shared-memory addresses of their records.
+            // Compact the splats that can reach this warp's still-compositing pixels (depth
+            // order preserved) as shared-memory addresses of their records. The cull rectangle
+            // is the bounding box of the warp's pixels with T >= cutoff: a finished pixel takes
+            // no more weight, so splats that only reach finished pixels are dropped (results
+            // unchanged, fewer blend steps near the end of a tile).
+            const bool al0 = !(T.x < cutoff), al1 = !(T.y < cutoff);
+            const int bx_lo = __reduce_min_sync(0xffffffffu, al0 ? x : (al1 ? x + 1 : INT_MAX));
+            const int bx_hi = __reduce_max_sync(0xffffffffu, al1 ? x + 1 : (al0 ? x : INT_MIN));
+            const int by_lo = __reduce_min_sync(0xffffffffu, (al0 || al1) ? y : INT_MAX);
+            const int by_hi = __reduce_max_sync(0xffffffffu, (al0 || al1) ? y : INT_MIN);
+            const float cx_lo = float(bx_lo) + 0.5f, cx_hi = float(bx_hi) + 0.5f;
+            const float cy_lo = float(by_lo) + 0.5f, cy_hi = float(by_hi) + 0.5f;
             const Record* spl_buf = s_spl[buf];
             const uint32_t spl_addr = uint32_t(__cvta_generic_to_shared(spl_buf));
             uint32_t count = 0;
@@ -355,9 +364,9 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
                     const float rw = spl_buf[idx].c.w;
                     const __half2 reach = *reinterpret_cast<const __half2*>(&rw);
                     const float ex = __low2float(reach), ey = __high2float(reach);
-                    mine = p0.x + ex >= wx_lo && p0.x - ex <= wx_hi && p0.y + ey >= wy_lo &&
-                           p0.y - ey <= wy_hi;
-                    if (a.exact_cull) mine = mine && reaches_rect(p0, spl_buf[idx].b, wx_lo, wx_hi, wy_lo, wy_hi);
+                    mine = p0.x + ex >= cx_lo && p0.x - ex <= cx_hi && p0.y + ey >= cy_lo &&
+                           p0.y - ey <= cy_hi;
+                    if (a.exact_cull) mine = mine && reaches_rect(p0, spl_buf[idx].b, cx_lo, cx_hi, cy_lo, cy_hi);
                     lop = p0.w;
                 }
                 const uint32_t bits = __ballot_sync(0xffffffffu, mine);
