@@ -162,15 +162,16 @@ __device__ __forceinline__ void blend_one(uint32_t addr, float2 npx, float py, f
 }
 
 // Front-to-back blend of a warp's compacted list for the thread's pixel pair (raster.cpp:
-// 221-238). The list is padded to a multiple of 4 with the null record (r = -1: the box test
-// fails, weight 0, nothing changes), so it is walked 4 entries per 128-bit list load without
-// remainder branches. kClamp: some splat of the list can reach the 0.99 alpha clamp.
+// 221-238), 4 entries per 128-bit list load and the last 0-3 one by one (padding them with a
+// null record instead cost a blend step per padding entry). kClamp: some splat of the list can
+// reach the 0.99 alpha clamp.
 template <bool kClamp>
 __device__ __forceinline__ void blend_list(const uint32_t* list, uint32_t count, float2 npx,
                                            float py, float cutoff, float2& cr, float2& cg,
                                            float2& cb, float2& d, float2& acc, float2& T) {
-    for (uint32_t k0 = 0; k0 < count; k0 += 32) {
-        const uint32_t k1 = (k0 + 32 < count) ? k0 + 32 : count;
+    const uint32_t count4 = count & ~3u;
+    for (uint32_t k0 = 0; k0 < count4; k0 += 32) {
+        const uint32_t k1 = (k0 + 32 < count4) ? k0 + 32 : count4;
         for (uint32_t k = k0; k < k1; k += 4) {
             const uint4 q = *reinterpret_cast<const uint4*>(list + k);
             blend_one<kClamp>(q.x, npx, py, cutoff, cr, cg, cb, d, acc, T);
@@ -178,8 +179,10 @@ __device__ __forceinline__ void blend_list(const uint32_t* list, uint32_t count,
             blend_one<kClamp>(q.z, npx, py, cutoff, cr, cg, cb, d, acc, T);
             blend_one<kClamp>(q.w, npx, py, cutoff, cr, cg, cb, d, acc, T);
         }
-        if (__all_sync(0xffffffffu, T.x < cutoff && T.y < cutoff)) break;
+        if (__all_sync(0xffffffffu, T.x < cutoff && T.y < cutoff)) return;
     }
+    for (uint32_t k = count4; k < count; ++k)  // the last 0-3 entries, one at a time
+        blend_one<kClamp>(list[k], npx, py, cutoff, cr, cg, cb, d, acc, T);
 }
 
 // mbarrier helpers for the bulk-copy (TMA engine) staging variant.
@@ -213,7 +216,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     constexpr int WX = 16 / RW;  // warp rectangles per tile row
     __shared__ Record s_spl[2][kBatch];
     __shared__ __align__(16) uint32_t s_list[kWarps][kBatch];
-    __shared__ Record s_null;  // pads the compacted lists: fails the box test (r = -1)
     __shared__ __align__(8) uint64_t s_bar[2];  // kBulk: one mbarrier per record buffer
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -221,9 +223,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     uint32_t phase_bits = 0;   // kBulk: parity of the next phase of each buffer's barrier
     uint32_t pending_bulk = 0; // kBulk: buffers with copies issued and not yet waited for
     if (tid == 0) {
-        s_null.a = make_float4(0.f, 0.f, -1.f, 0.f);
-        s_null.b = make_float4(0.f, 0.f, 0.f, 0.f);
-        s_null.c = make_float4(0.f, 0.f, 0.f, 0.f);
         if (kBulk) {
             mbar_init(bar0, kThreads);
             mbar_init(bar0 + 8u, kThreads);
@@ -231,7 +230,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
         }
     }
     if (kBulk) __syncthreads();  // barriers initialised before any thread arrives
-    const uint32_t null_addr = uint32_t(__cvta_generic_to_shared(&s_null));
 
     // One CTA per tile, or (GSIM_GPU_RASTER_CTAS) a capped grid whose CTAs claim tiles in
     // order from a counter (cameras still finish in order, for the per-camera copies, and the
@@ -376,9 +374,6 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
                         spl_addr + idx * uint32_t(sizeof(Record));
                 count += __popc(bits);
             }
-            const uint32_t padded = (count + 3u) & ~3u;
-            if (count + uint32_t(lane) < padded) s_list[warp][count + lane] = null_addr;
-            count = padded;
             __syncwarp();
             if (bright)
                 blend_list<true>(s_list[warp], count, npx, py, cutoff, cr, cg, cb, d, acc, T);
