@@ -185,6 +185,11 @@ __global__ void __launch_bounds__(256) bvh_refit_kernel(BvhArgs a) {
     const int n = int(*a.n_leaves);
     const uint64_t np = a.n;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        {   // the leaf's box in sorted order, contiguous for the traversal's leaf tests
+            const uint32_t prim = a.leaf_prim[k];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) a.leaf_box[6 * uint64_t(k) + q] = a.posed[(13 + q) * np + prim];
+        }
         if (n == 1) break;
         uint32_t node = a.leaf_parent[k];
         while (true) {
@@ -282,7 +287,6 @@ __device__ __forceinline__ bool slab_hit_f(float lx, float ly, float lz, float h
 // ray_count (the host falls back to count + fill when a ray overflows).
 __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const LidarArgs la, int fill) {
     const int n = int(*a.n_leaves);
-    const uint64_t np = a.n;
     for (uint64_t ray = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; ray < la.n_rays;
          ray += uint64_t(gridDim.x) * blockDim.x) {
         const dv3 o = mk3(la.ray_origin[3 * ray], la.ray_origin[3 * ray + 1], la.ray_origin[3 * ray + 2]);
@@ -298,11 +302,11 @@ __global__ void __launch_bounds__(128) bvh_collect_kernel(BvhArgs a, const Lidar
                       : fill == 2 ? la.list + ray * uint64_t(la.list_stride) : nullptr;
         const uint32_t cap = fill == 2 ? la.list_stride : 0xFFFFFFFFu;
         auto leaf = [&](uint32_t sorted_idx) {
-            const uint32_t prim = a.leaf_prim[sorted_idx];
-            if (slab_hit(a.posed[13 * np + prim], a.posed[14 * np + prim], a.posed[15 * np + prim],
-                         a.posed[16 * np + prim], a.posed[17 * np + prim], a.posed[18 * np + prim],
-                         o, inv, t_max)) {
-                if (out && count < cap) out[count] = prim;
+            // one 48-byte row (refit's copy of the primitive's double box, in leaf order)
+            const double2* lb = reinterpret_cast<const double2*>(a.leaf_box + 6 * uint64_t(sorted_idx));
+            const double2 b0 = __ldg(lb), b1 = __ldg(lb + 1), b2 = __ldg(lb + 2);
+            if (slab_hit(b0.x, b0.y, b1.x, b1.y, b2.x, b2.y, o, inv, t_max)) {
+                if (out && count < cap) out[count] = a.leaf_prim[sorted_idx];
                 ++count;
             }
         };

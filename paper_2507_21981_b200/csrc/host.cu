@@ -234,7 +234,7 @@ struct gsim_gpu_context {
         DevBuf<uint32_t> bvh_keys[2], bvh_vals[2], bvh_small, bvh_nodes;
         DevBuf<uint64_t> bvh_seg;
         DevBuf<unsigned long long> bvh_bounds;
-        DevBuf<double> bvh_box;
+        DevBuf<double> bvh_box, bvh_leaf_box;
         DevBuf<float4> bvh_wide;
         uint32_t bvh_capacity = 256;  // candidate slots per ray of the single-pass collect
         std::vector<double> ray_key;  // (channels, step) of the sensor directions in rays
@@ -242,6 +242,7 @@ struct gsim_gpu_context {
             for (int k = 0; k < 2; ++k) { bvh_keys[k].release(); bvh_vals[k].release(); }
             bvh_small.release(); bvh_nodes.release(); bvh_seg.release(); bvh_bounds.release();
             bvh_box.release();
+            bvh_leaf_box.release();
             bvh_wide.release();
             posed.release(); rays.release(); depth.release(); acc.release(); points.release();
             azimuth.release(); rank_elev.release(); seen.release(); ray_all.release();
@@ -1650,6 +1651,7 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
     uint32_t* sm = L.bvh_small.ptr;
     L.bvh_nodes.reserve(5 * nn);  // child 2(n-1), node_parent n-1, leaf_parent n, visits n-1
     L.bvh_box.reserve(6 * nn);
+    L.bvh_leaf_box.reserve(6 * nn);
     L.bvh_wide.reserve(4 * nn);
     L.bvh_seg.reserve(2);
     L.bvh_bounds.reserve(6);
@@ -1681,6 +1683,7 @@ uint64_t bvh_ray_lists(gsim_gpu_context* ctx, LidarArgs& la) {
     b.leaf_parent = L.bvh_nodes.ptr + 3 * nn;
     b.visits = L.bvh_nodes.ptr + 4 * nn;
     b.node_box = L.bvh_box.ptr;
+    b.leaf_box = L.bvh_leaf_box.ptr;
     b.wide = L.bvh_wide.ptr;
     launch_bvh_bounds(b, n_sms, s);
     launch_bvh_morton(b, n_sms, s);

@@ -298,6 +298,8 @@ struct BvhArgs {
     uint32_t* leaf_parent;           // [n]
     uint32_t* visits;                // [n - 1] refit arrivals
     double* node_box;                // [n - 1][6]
+    double* leaf_box;                // [n_leaves][6]: sorted leaf k's double box (refit writes
+                                     // it; the traversal's exact leaf test reads one 48-B row)
     float4* wide;                    // [n - 1][4] traversal nodes (bvh_widen_kernel)
     uint32_t* overflow;              // single-pass collect: largest count over the capacity
 };

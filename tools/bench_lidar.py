@@ -71,11 +71,13 @@ if a.trace:
     dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
     tmax = np.full(a.trace, 100.0)
     ctx.trace_rays(scene, nodes, org, dirs, tmax, 0.5)  # warm-up
-    t0 = time.perf_counter()
-    reps = 5
-    for _ in range(reps):
+    # median of 20 complete calls (wall clock: H2D of the rays, BVH build, traversal, trace, D2H)
+    times = []
+    for _ in range(20):
+        t0 = time.perf_counter()
         hit, _, _ = ctx.trace_rays(scene, nodes, org, dirs, tmax, 0.5)
-    gpu_t = (time.perf_counter() - t0) / reps
+        times.append(time.perf_counter() - t0)
+    gpu_t = float(np.median(times))
     line["trace_rays"] = {"rays": a.trace, "gpu_ms_per_call": round(gpu_t * 1e3, 2),
                           "gpu_rays_per_s": round(a.trace / gpu_t, 1),
                           "candidates_per_ray": round(ctx.stats()["pairs"] / a.trace, 1),
