@@ -223,7 +223,7 @@ struct gsim_gpu_context {
     float frame_valid_alpha = 0.0f;  // render_depth_ring's depth mask (raster epilogue)
     // LiDAR scratch (lidar.cu)
     struct {
-        DevBuf<double> posed, rays, depth, acc, points, azimuth, rank_elev, cand_t, cand_r;
+        DevBuf<double> posed, trace_rec, rays, depth, acc, points, azimuth, rank_elev, cand_t, cand_r;
         DevBuf<uint8_t> seen, ray_all;
         DevBuf<LidarRect> rects;
         DevBuf<uint32_t> all_list, counts, list, hit, ring, rank_channel, cursor, big_list;
@@ -244,7 +244,7 @@ struct gsim_gpu_context {
             bvh_box.release();
             bvh_leaf_box.release();
             bvh_wide.release();
-            posed.release(); rays.release(); depth.release(); acc.release(); points.release();
+            posed.release(); trace_rec.release(); rays.release(); depth.release(); acc.release(); points.release();
             azimuth.release(); rank_elev.release(); seen.release(); ray_all.release();
             cand_t.release(); cand_r.release();
             rects.release(); all_list.release(); counts.release(); list.release(); hit.release();
@@ -1611,6 +1611,7 @@ LidarArgs lidar_pose_stage(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, c
     GSIM_CK(cudaMemcpyAsync(L.segs.ptr, segs.data(), segs.size() * sizeof(DevSegment),
                             cudaMemcpyHostToDevice, ctx->stream));
     L.posed.reserve(std::max<uint64_t>(19 * n, 1));
+    L.trace_rec.reserve(std::max<uint64_t>(20 * n, 2));
     L.seen.reserve(std::max<uint64_t>(n, 1));
     L.rects.reserve(std::max<uint64_t>(n, 1));
     L.all_list.reserve(std::max<uint64_t>(n, 1) + 1);
@@ -1621,6 +1622,7 @@ LidarArgs lidar_pose_stage(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, c
     a.scan = scan ? 1 : 0;
     a.n = n;
     a.posed = L.posed.ptr;
+    a.trace_rec = L.trace_rec.ptr;
     a.seen = L.seen.ptr;
     a.rects = L.rects.ptr;
     a.all_count = L.all_list.ptr;      // [0] = count

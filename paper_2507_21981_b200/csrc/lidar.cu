@@ -41,10 +41,6 @@ constexpr double kTraceAlphaSkip = 1.0 / 255.0;
 constexpr double kTraceCutoff = 1e-4;
 constexpr double kAngleMargin = 1e-7;      // radians added to every angular bound
 
-__device__ __forceinline__ dv3 ld3(const double* p, uint64_t n, uint64_t i) {  // SoA planes
-    return mk3(p[i], p[n + i], p[2 * n + i]);
-}
-
 __device__ __forceinline__ dv3 ldx3(const double* p, uint64_t i) {  // interleaved xyz
     return mk3(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
 }
@@ -71,15 +67,14 @@ __device__ __forceinline__ bool ray_aabb_hit(dv3 lo, dv3 hi, dv3 o, dv3 inv, dou
     return t0 <= t1;
 }
 
-// Peak of primitive i along the ray (trace.cpp:38-49); response 0 when d^T S^-1 d <= 0.
-__device__ __forceinline__ void ray_peak(const LidarArgs& a, uint64_t i, dv3 o, dv3 d, double t_max,
-                                         double& t, double& response) {
-    const uint64_t n = a.n;
-    const dv3 mean = ld3(a.posed, n, i);
-    double ic[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) ic[k] = a.posed[(3 + k) * n + i];
-    const double opacity = a.posed[12 * n + i];
+// Peak of a primitive along the ray (trace.cpp:38-49) from its trace row; response 0 when
+// d^T S^-1 d <= 0.
+__device__ __forceinline__ void ray_peak_row(const double2* R, double opacity, dv3 o, dv3 d,
+                                             double t_max, double& t, double& response) {
+    const double2 r3 = __ldg(R + 3), r4 = __ldg(R + 4), r5 = __ldg(R + 5), r6 = __ldg(R + 6),
+                  r7 = __ldg(R + 7), r8 = __ldg(R + 8);
+    const dv3 mean = mk3(r3.x, r3.y, r4.x);
+    const double ic[9] = {r4.y, r5.x, r5.y, r6.x, r6.y, r7.x, r7.y, r8.x, r8.y};
     const dv3 to_mean = sub3(mean, o);
     const dv3 si_d = matvec(ic, d);
     const double denom = dot3(d, si_d);
@@ -152,6 +147,19 @@ __global__ void __launch_bounds__(256) lidar_pose_kernel(LidarArgs a) {
         P[13 * n + i] = lo.x; P[14 * n + i] = lo.y; P[15 * n + i] = lo.z;
         P[16 * n + i] = hi.x; P[17 * n + i] = hi.y; P[18 * n + i] = hi.z;
         a.seen[i] = seen ? 1 : 0;
+        {
+            double2* R = reinterpret_cast<double2*>(a.trace_rec + 20 * uint64_t(i));
+            R[0] = make_double2(lo.x, lo.y);
+            R[1] = make_double2(lo.z, hi.x);
+            R[2] = make_double2(hi.y, hi.z);
+            R[3] = make_double2(mean.x, mean.y);
+            R[4] = make_double2(mean.z, inv_cov.m[0]);
+            R[5] = make_double2(inv_cov.m[1], inv_cov.m[2]);
+            R[6] = make_double2(inv_cov.m[3], inv_cov.m[4]);
+            R[7] = make_double2(inv_cov.m[5], inv_cov.m[6]);
+            R[8] = make_double2(inv_cov.m[7], inv_cov.m[8]);
+            R[9] = make_double2(f.opacity[i], seen ? 1.0 : 0.0);
+        }
         if (!a.scan) continue;
 
         // Conservative ray rectangle: the box in the sensor frame (AABB of its 8 corners)
@@ -357,12 +365,14 @@ struct RayCands {
 // Candidate j of the ray as (t, response) if its box is hit and alpha >= 1/255 (else false).
 __device__ __forceinline__ bool survivor(const LidarArgs& a, uint32_t i, dv3 o, dv3 d, dv3 inv,
                                          double t_max, double& t, double& resp) {
-    if (!a.seen[i]) return false;
-    const uint64_t n = a.n;
-    const dv3 lo = mk3(a.posed[13 * n + i], a.posed[14 * n + i], a.posed[15 * n + i]);
-    const dv3 hi = mk3(a.posed[16 * n + i], a.posed[17 * n + i], a.posed[18 * n + i]);
+    // the primitive's 160-byte trace row: box first, the rest only for a box hit
+    const double2* R = reinterpret_cast<const double2*>(a.trace_rec + 20 * uint64_t(i));
+    const double2 r0 = __ldg(R), r1 = __ldg(R + 1), r2 = __ldg(R + 2), r9 = __ldg(R + 9);
+    if (!(r9.y != 0.0)) return false;  // not seen
+    const dv3 lo = mk3(r0.x, r0.y, r1.x);
+    const dv3 hi = mk3(r1.y, r2.x, r2.y);
     if (!ray_aabb_hit(lo, hi, o, inv, t_max)) return false;
-    ray_peak(a, i, o, d, t_max, t, resp);
+    ray_peak_row(R, r9.x, o, d, t_max, t, resp);
     // alpha = min(response, 0.99) is skipped below 1/255 (trace.cpp:73): composite-neutral
     return !(resp < kTraceAlphaSkip);
 }
