@@ -241,8 +241,8 @@ struct LidarArgs {
     const uint32_t* list_count;
     uint64_t n;                      // primitives
     double* posed;                   // [19][n]: mean xyz, inv_cov 9, opacity, lo xyz, hi xyz
-    double* trace_rec;               // [n][20]: lo xyz, hi xyz, mean xyz, inv_cov 9, opacity,
-                                     // seen (1.0 / 0.0): one 160-byte row per primitive for the
+    double* trace_rec;               // [n][20]: lo xyz, hi xyz, opacity, seen (1.0 / 0.0) (the
+                                     // first 64 B), mean xyz, inv_cov 9: one 160-byte row for the
                                      // tracer's random candidate reads (the planes serve the
                                      // binning and the BVH)
     uint8_t* seen;                   // [n]

@@ -71,10 +71,10 @@ __device__ __forceinline__ bool ray_aabb_hit(dv3 lo, dv3 hi, dv3 o, dv3 inv, dou
 // d^T S^-1 d <= 0.
 __device__ __forceinline__ void ray_peak_row(const double2* R, double opacity, dv3 o, dv3 d,
                                              double t_max, double& t, double& response) {
-    const double2 r3 = __ldg(R + 3), r4 = __ldg(R + 4), r5 = __ldg(R + 5), r6 = __ldg(R + 6),
-                  r7 = __ldg(R + 7), r8 = __ldg(R + 8);
-    const dv3 mean = mk3(r3.x, r3.y, r4.x);
-    const double ic[9] = {r4.y, r5.x, r5.y, r6.x, r6.y, r7.x, r7.y, r8.x, r8.y};
+    const double2 r4 = __ldg(R + 4), r5 = __ldg(R + 5), r6 = __ldg(R + 6), r7 = __ldg(R + 7),
+                  r8 = __ldg(R + 8), r9 = __ldg(R + 9);
+    const dv3 mean = mk3(r4.x, r4.y, r5.x);
+    const double ic[9] = {r5.y, r6.x, r6.y, r7.x, r7.y, r8.x, r8.y, r9.x, r9.y};
     const dv3 to_mean = sub3(mean, o);
     const dv3 si_d = matvec(ic, d);
     const double denom = dot3(d, si_d);
@@ -152,13 +152,13 @@ __global__ void __launch_bounds__(256) lidar_pose_kernel(LidarArgs a) {
             R[0] = make_double2(lo.x, lo.y);
             R[1] = make_double2(lo.z, hi.x);
             R[2] = make_double2(hi.y, hi.z);
-            R[3] = make_double2(mean.x, mean.y);
-            R[4] = make_double2(mean.z, inv_cov.m[0]);
-            R[5] = make_double2(inv_cov.m[1], inv_cov.m[2]);
-            R[6] = make_double2(inv_cov.m[3], inv_cov.m[4]);
-            R[7] = make_double2(inv_cov.m[5], inv_cov.m[6]);
-            R[8] = make_double2(inv_cov.m[7], inv_cov.m[8]);
-            R[9] = make_double2(f.opacity[i], seen ? 1.0 : 0.0);
+            R[3] = make_double2(f.opacity[i], seen ? 1.0 : 0.0);
+            R[4] = make_double2(mean.x, mean.y);
+            R[5] = make_double2(mean.z, inv_cov.m[0]);
+            R[6] = make_double2(inv_cov.m[1], inv_cov.m[2]);
+            R[7] = make_double2(inv_cov.m[3], inv_cov.m[4]);
+            R[8] = make_double2(inv_cov.m[5], inv_cov.m[6]);
+            R[9] = make_double2(inv_cov.m[7], inv_cov.m[8]);
         }
         if (!a.scan) continue;
 
@@ -367,12 +367,12 @@ __device__ __forceinline__ bool survivor(const LidarArgs& a, uint32_t i, dv3 o, 
                                          double t_max, double& t, double& resp) {
     // the primitive's 160-byte trace row: box first, the rest only for a box hit
     const double2* R = reinterpret_cast<const double2*>(a.trace_rec + 20 * uint64_t(i));
-    const double2 r0 = __ldg(R), r1 = __ldg(R + 1), r2 = __ldg(R + 2), r9 = __ldg(R + 9);
-    if (!(r9.y != 0.0)) return false;  // not seen
+    const double2 r0 = __ldg(R), r1 = __ldg(R + 1), r2 = __ldg(R + 2), r3 = __ldg(R + 3);
+    if (!(r3.y != 0.0)) return false;  // not seen
     const dv3 lo = mk3(r0.x, r0.y, r1.x);
     const dv3 hi = mk3(r1.y, r2.x, r2.y);
     if (!ray_aabb_hit(lo, hi, o, inv, t_max)) return false;
-    ray_peak_row(R, r9.x, o, d, t_max, t, resp);
+    ray_peak_row(R, r3.x, o, d, t_max, t, resp);
     // alpha = min(response, 0.99) is skipped below 1/255 (trace.cpp:73): composite-neutral
     return !(resp < kTraceAlphaSkip);
 }
