@@ -765,7 +765,7 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
 
     // digit histograms per (camera, pass), then the chunk tables (need only the counts)
     BinArgs b = make_bin_args(ctx, p);
-    launch_key_hist(b, n_sms * 2, s);
+    launch_key_hist(b, n_sms * 6, s);
     check_launch();
     launch_chunk_table(b, s);
     check_launch();
