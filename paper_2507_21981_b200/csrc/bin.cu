@@ -483,6 +483,10 @@ __global__ void __launch_bounds__(256) bin_campre_kernel(BinArgs a) {
     if (tid == 0) {
         a.cam_pair_base[a.n_cams] = s_carry;
         a.totals[1] = s_carry;  // P
+        if (a.host_totals) {  // read by the host after the frame's binning event
+            a.host_totals[0] = a.totals[0];
+            a.host_totals[1] = s_carry;
+        }
     }
 }
 

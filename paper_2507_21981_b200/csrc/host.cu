@@ -681,6 +681,10 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p) {
     b.hist = ctx->sort_hist.ptr;
     b.sort_chunk_base = ctx->sort_chunk_base.ptr;
     b.totals = ctx->counts.ptr;
+    ctx->readback.reserve(64);
+    void* host_totals = nullptr;
+    GSIM_CK(cudaHostGetDevicePointer(&host_totals, ctx->readback.ptr, 0));
+    b.host_totals = static_cast<unsigned long long*>(host_totals);
     b.vals_out = ctx->vals.ptr;
     b.capacity = ctx->pair_capacity;
     b.max_tc = int(p.max_tc);
@@ -835,9 +839,9 @@ void run_sort_and_raster(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     launch_bin_campre(b, s);
     check_launch();
     launches += 4;
-    ctx->readback.reserve(64);
-    GSIM_CK(cudaMemcpyAsync(ctx->readback.ptr, ctx->counts.ptr, 2 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s));
+    // (V, P) reach the host through campre's stores into the page-locked readback (no copy
+    // engine operation between the binning and the scatter: a queued copy engine, e.g. behind
+    // another context's image copies, would hold the frame there)
     GSIM_CK(cudaEventRecord(ctx->bin_ev, s));
     record_ev(ctx, kEvBin);
 

@@ -96,6 +96,8 @@ struct BinArgs {
     uint32_t* hist;                  // [C][passes][radix] digit histograms (zeroed per frame)
     uint32_t* sort_chunk_base;       // [C+1] onesweep chunks of passes >= 2 per camera (out)
     unsigned long long* totals;      // [0] V, [1] P
+    unsigned long long* host_totals; // optional: page-locked host copy of totals, stored by
+                                     // campre (no copy-engine operation in the frame's stream)
     uint32_t* vals_out;              // [capacity] record slot of every pair, final order
     uint64_t capacity;
     int max_tc;                      // largest (tiles_x + 1) * (tiles_y + 1) of the batch
