@@ -131,4 +131,7 @@ def main(case: str) -> None:
 
 
 if __name__ == "__main__":
+    import faulthandler
+    # a hang shows where every thread waits (debug_checks.sh kills the case at 900 s)
+    faulthandler.dump_traceback_later(840, exit=True)
     main(sys.argv[1])
