@@ -26,7 +26,6 @@
 #include <string>
 #include <vector>
 
-#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/gsim_gpu.h"
@@ -201,12 +200,10 @@ struct gsim_gpu_context {
     DevBuf<char> query_buf;
     DevBuf<float> enc_src;
     DevBuf<EncodeCam> enc_cams;
-    // host-target renders: camera c's copies start when its tiles are done (copy_stream waits
-    // on cam_done[c] reaching cam_done_expect[c]; the counters only grow, compared cyclically)
+    // host-target renders: camera c's copies start when its tiles are done (the raster runs one
+    // launch per camera; copy_stream waits on the event recorded after camera c's launch)
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t copy_ev = nullptr;
-    DevBuf<uint32_t> cam_done;
-    std::vector<uint32_t> cam_done_expect;
+    std::vector<cudaEvent_t> cam_evs;
     gsim_target* frame_outs = nullptr;   // targets of the camera group in flight (nullptr: none)
     uint8_t* frame_enc_host = nullptr;   // render_encoded: host bytes of the group in flight
     bool copies_stale = false;           // a group was re-run after its copies were issued
@@ -695,10 +692,8 @@ BinArgs make_bin_args(gsim_gpu_context* ctx, const Plan& p) {
     return b;
 }
 
-using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-WaitValueFn wait_value_fn();
-bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out);
-bool queue_camera_copies_enc(gsim_gpu_context* ctx, const Plan& p, const uint8_t* dev, uint32_t bpp);
+void queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out);
+void queue_camera_copies_enc(gsim_gpu_context* ctx, const Plan& p, const uint8_t* dev, uint32_t bpp);
 
 void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster_options& opt,
                          float* out) {
@@ -723,28 +718,36 @@ void launch_raster_stage(gsim_gpu_context* ctx, const Plan& p, const gsim_raster
     rr.exact_cull = ctx->raster_exact_cull;
     rr.bulk_copy = ctx->raster_bulk;
     rr.grid_cap = ctx->raster_ctas > 0 ? ctx->raster_ctas * ctx->num_sms : 0;
-    if (rr.grid_cap > 0 && uint32_t(rr.grid_cap) < p.tiles) {
-        rr.tile_ticket = ctx->zero_block.ptr + kZeroTickets + kRasterTicket;
-        GSIM_CK(cudaMemsetAsync(rr.tile_ticket, 0, sizeof(uint32_t), ctx->stream));
-    }
     rr.valid_alpha = ctx->frame_valid_alpha;
     if (rr.enc.flags && ctx->frame_enc_only) rr.out = nullptr;
-    const bool overlap_enc = ctx->frame_enc_host && rr.enc.flags && wait_value_fn();
-    const bool overlap = (ctx->frame_outs && rr.out && wait_value_fn()) || overlap_enc;
-    if (overlap) {
-        if (ctx->cam_done_expect.size() < p.cams.size()) {
-            // new counters start at zero on both sides (nothing can be waiting on them yet)
-            const size_t n = std::max<size_t>(p.cams.size(), 64);
-            GSIM_CK(cudaStreamSynchronize(ctx->copy_stream));
-            GSIM_CK(cudaStreamSynchronize(ctx->stream));
-            ctx->cam_done.reserve(n);
-            GSIM_CK(cudaMemset(ctx->cam_done.ptr, 0, n * sizeof(uint32_t)));
-            ctx->cam_done_expect.assign(n, 0u);
-        }
-        rr.cam_done = ctx->cam_done.ptr;
+    const bool overlap_enc = ctx->frame_enc_host && rr.enc.flags;
+    const bool overlap = (ctx->frame_outs && rr.out) || overlap_enc;
+    // one launch per camera when host copies overlap the compositing (each camera's copies wait
+    // on the event after its launch: ordinary stream dependencies, no stream memory operations,
+    // which can deadlock through shared hardware queues), else one launch for the batch
+    const size_t n_launch = overlap ? p.cams.size() : 1;
+    while (overlap && ctx->cam_evs.size() < p.cams.size()) {
+        cudaEvent_t e;
+        GSIM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->cam_evs.push_back(e);
     }
-    launch_raster(rr, p.tiles, ctx->stream);
-    check_launch();
+    uint32_t tile = 0;
+    for (size_t k = 0; k < n_launch; ++k) {
+        const uint32_t end = overlap ? tile + uint32_t(p.cams[k].tiles_x) * uint32_t(p.cams[k].tiles_y)
+                                     : uint32_t(p.tiles);
+        rr.tile_begin = tile;
+        if (rr.grid_cap > 0 && uint32_t(rr.grid_cap) < end - tile) {
+            rr.tile_ticket = ctx->zero_block.ptr + kZeroTickets + kRasterTicket;
+            GSIM_CK(cudaMemsetAsync(rr.tile_ticket, 0, sizeof(uint32_t), ctx->stream));
+        } else {
+            rr.tile_ticket = nullptr;
+        }
+        launch_raster(rr, end, ctx->stream);
+        check_launch();
+        if (overlap) GSIM_CK(cudaEventRecord(ctx->cam_evs[k], ctx->stream));
+        tile = end;
+    }
+    ctx->launches_total += n_launch - 1;
     if (overlap_enc)
         queue_camera_copies_enc(ctx, p, rr.enc.dst, encoded_bpp(rr.enc.flags));
     else if (overlap)
@@ -1357,19 +1360,6 @@ gsim_gpu_scene* load_ply(gsim_gpu_context* ctx, const std::string& path) {
     return sc;
 }
 
-// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda link); nullptr when
-// the driver does not offer stream memory operations (copies then follow the whole frame).
-WaitValueFn wait_value_fn() {
-    static const WaitValueFn fn = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return WaitValueFn(nullptr);
-        return reinterpret_cast<WaitValueFn>(f);
-    }();
-    return fn;
-}
 
 // Waits for everything queued on the copy stream and the context stream (a synchronous call's
 // end): cudaStreamSynchronize, or blocking-sync events when the context asks for them.
@@ -1386,20 +1376,14 @@ void wait_frame(gsim_gpu_context* ctx) {
 }
 
 // Per-camera copies of a host-target render, queued right after the raster launch: the copy
-// stream waits for each camera's tile counter, so camera c crosses PCIe while later cameras
+// stream waits on the event after each camera's raster launch, so camera c crosses PCIe while later cameras
 // (and other contexts' frames) are still being composited.
-bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out) {
-    const WaitValueFn wait = wait_value_fn();
-    if (!wait || !ctx->frame_outs) return false;
+void queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out) {
     uint64_t off = 0;
     for (size_t c = 0; c < p.cams.size(); ++c) {
         const DevCamera& cam = p.cams[c];
         const size_t npx = size_t(cam.width) * cam.height;
-        ctx->cam_done_expect[c] += uint32_t(cam.tiles_x) * uint32_t(cam.tiles_y);
-        const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(ctx->cam_done.ptr + c);
-        if (wait(reinterpret_cast<CUstream>(ctx->copy_stream), flag, ctx->cam_done_expect[c],
-                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-            throw CudaError{"cuStreamWaitValue32 failed"};
+        GSIM_CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->cam_evs[c], 0));
         const gsim_target& t = ctx->frame_outs[c];
         const float* base = out + off;
         GSIM_CK(cudaMemcpyAsync(t.rgb, base, 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
@@ -1407,28 +1391,20 @@ bool queue_camera_copies(gsim_gpu_context* ctx, const Plan& p, const float* out)
         GSIM_CK(cudaMemcpyAsync(t.accum_alpha, base + 4 * npx, npx * sizeof(float), cudaMemcpyDeviceToHost, ctx->copy_stream));
         off += 5 * npx;
     }
-    return true;
 }
 
 // The same for render_encoded: camera c's encoded block crosses PCIe once its tiles are done.
-bool queue_camera_copies_enc(gsim_gpu_context* ctx, const Plan& p, const uint8_t* dev, uint32_t bpp) {
-    const WaitValueFn wait = wait_value_fn();
-    if (!wait || !ctx->frame_enc_host) return false;
+void queue_camera_copies_enc(gsim_gpu_context* ctx, const Plan& p, const uint8_t* dev, uint32_t bpp) {
     uint64_t off = 0;
     for (size_t c = 0; c < p.cams.size(); ++c) {
         const DevCamera& cam = p.cams[c];
         const uint64_t bytes = uint64_t(bpp) * uint64_t(cam.width) * uint64_t(cam.height);
-        ctx->cam_done_expect[c] += uint32_t(cam.tiles_x) * uint32_t(cam.tiles_y);
-        const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(ctx->cam_done.ptr + c);
-        if (wait(reinterpret_cast<CUstream>(ctx->copy_stream), flag, ctx->cam_done_expect[c],
-                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-            throw CudaError{"cuStreamWaitValue32 failed"};
+        GSIM_CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->cam_evs[c], 0));
         if (bytes)
             GSIM_CK(cudaMemcpyAsync(ctx->frame_enc_host + off, dev + off, bytes, cudaMemcpyDeviceToHost,
                                     ctx->copy_stream));
         off += bytes;
     }
-    return true;
 }
 
 // D2H of the internal output buffer into host RenderTargets (the drop-in's by-value return).
@@ -1895,7 +1871,6 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     ctx->enc_src.release();
     ctx->enc_cams.release();
     ctx->query_buf.release();
-    ctx->cam_done.release();
     {
         std::lock_guard<std::mutex> lk(ctx->mu);
         for (auto* sc : ctx->scenes) sc->ctx = nullptr;
@@ -1908,7 +1883,7 @@ int gsim_gpu_context_destroy(gsim_gpu_context* ctx) {
     if (ctx->bin_ev) cudaEventDestroy(ctx->bin_ev);
     for (int k = 0; k < 2; ++k)
         if (ctx->wait_ev[k]) cudaEventDestroy(ctx->wait_ev[k]);
-    if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
+    for (cudaEvent_t e : ctx->cam_evs) cudaEventDestroy(e);
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
         cudaStreamDestroy(ctx->copy_stream);
@@ -2304,13 +2279,11 @@ int gsim_gpu_render(gsim_gpu_context* ctx, const gsim_gpu_scene* scene, const gs
         // Asynchronous render with the copies queued behind it: the pair-buffer check is done
         // once at the end (no mid-frame host round trip); on an overflow the tail is re-run
         // and the targets copied again.
-        // Per-camera copies overlap the compositing when the driver has stream memory
-        // operations (queue_camera_copies); otherwise they follow the frame.
-        const bool overlap = ctx->overlap_copies && wait_value_fn() != nullptr;
-        if (overlap && !ctx->copy_stream) {
+        // Per-camera copies overlap the compositing (queue_camera_copies) unless
+        // GSIM_GPU_OVERLAP_COPIES=0; then they follow the frame.
+        const bool overlap = ctx->overlap_copies;
+        if (overlap && !ctx->copy_stream)
             GSIM_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-            GSIM_CK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
-        }
         ctx->copies_stale = false;
         ctx->frame_outs = overlap ? outs : nullptr;
         std::vector<uint64_t> off;
@@ -2466,11 +2439,9 @@ int gsim_gpu_render_encoded(gsim_gpu_context* ctx, const gsim_gpu_scene* scene,
         } reset{ctx};
         ctx->frame_enc = e;
         ctx->frame_enc_only = true;
-        const bool overlap = !out_is_device && ctx->overlap_copies && wait_value_fn() != nullptr;
-        if (overlap && !ctx->copy_stream) {
+        const bool overlap = !out_is_device && ctx->overlap_copies;
+        if (overlap && !ctx->copy_stream)
             GSIM_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-            GSIM_CK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
-        }
         ctx->copies_stale = false;
         ctx->frame_enc_host = overlap ? out : nullptr;
         try {

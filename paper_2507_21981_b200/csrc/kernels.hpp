@@ -122,7 +122,9 @@ struct RasterArgs {
     int batch;                       // records per shared-memory batch: 128 or 256
     int exact_cull;                  // exact ellipse-vs-warp-rectangle test in the compaction
     int bulk_copy;                   // stage records with cp.async.bulk + mbarrier (8x8 rects)
-    uint32_t n_tiles;                // tiles of the launch (set by launch_raster)
+    uint32_t tile_begin;             // first tile of the launch (a camera's tiles, for per-camera
+                                     // launches whose copies start on an event)
+    uint32_t n_tiles;                // one past the last tile of the launch (set by launch_raster)
     int grid_cap;                    // CTAs of the launch (0: one per tile)
     uint32_t* tile_ticket;           // grid_cap > 0: tile counter, zero before the launch
     float valid_alpha;               // depth written as 0 where accum_alpha < valid_alpha
@@ -133,8 +135,6 @@ struct RasterArgs {
     uint64_t n_slots;                // record slots (stale values are clamped to a valid slot)
     EncodeParams enc;                // fused encoding when enc.flags != 0; camera c's block
                                      // starts at enc.dst + out_offset / 5 * encoded_bpp
-    uint32_t* cam_done;              // optional: += 1 per finished tile of camera c (after a
-                                     // system fence), for copies that wait on cuStreamWaitValue32
 };
 
 // Device pose tracks (tracks.cu): records of track k are begin[k] .. begin[k+1]-1.
@@ -185,7 +185,8 @@ void launch_bin_colscan(const BinArgs& a, int grid, cudaStream_t s);
 void launch_bin_tilescan(const BinArgs& a, int grid, cudaStream_t s);
 void launch_bin_campre(const BinArgs& a, cudaStream_t s);
 void launch_bin_scatter(const BinArgs& a, int grid, cudaStream_t s);
-void launch_raster(const RasterArgs& a, uint32_t n_tiles, cudaStream_t stream);
+// Tiles [a.tile_begin, tile_end) of the batch.
+void launch_raster(const RasterArgs& a, uint32_t tile_end, cudaStream_t stream);
 void launch_encode(const EncodeKernelArgs& a, uint32_t n_cams, uint32_t max_pixels,
                    cudaStream_t stream);
 void launch_track_query(const DevTracks& tr, const uint32_t* track, const double* time,

@@ -231,13 +231,12 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     }
     if (kBulk) __syncthreads();  // barriers initialised before any thread arrives
 
-    // One CTA per tile, or (GSIM_GPU_RASTER_CTAS) a capped grid whose CTAs claim tiles in
-    // order from a counter (cameras still finish in order, for the per-camera copies, and the
-    // tail balances).
+    // One CTA per tile of [tile_begin, n_tiles), or (GSIM_GPU_RASTER_CTAS) a capped grid whose
+    // CTAs claim the tiles in order from a counter (the tail balances).
     __shared__ uint32_t s_tile;
-    for (uint32_t g = blockIdx.x;;) {
+    for (uint32_t g = a.tile_begin + blockIdx.x;;) {
         if (a.tile_ticket) {
-            if (tid == 0) s_tile = atomicAdd(a.tile_ticket, 1u);
+            if (tid == 0) s_tile = a.tile_begin + atomicAdd(a.tile_ticket, 1u);
             __syncthreads();
             g = s_tile;
         }
@@ -393,24 +392,16 @@ __global__ void __launch_bounds__(kThreads, kBatch == 128 ? 12 : 8) raster_kerne
     if (tid == 0 && fetched) atomicAdd(a.consumed, (unsigned long long)fetched);
     write_pixel(a, cam, x, y, cr.x, cg.x, cb.x, d.x, acc.x);
     write_pixel(a, cam, x + 1, y, cr.y, cg.y, cb.y, d.y, acc.y);
-    if (a.cam_done) {
-        // The tile's pixels are performed at GPU scope before it is counted: the copy engine
-        // that the counter releases reads this device memory through the same L2 as the
-        // counter's wait, so a GPU-scope fence orders them (a system-scope fence, needed only
-        // for observers outside the GPU, cost 4% of the float e2e rate at config 1).
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) atomicAdd(a.cam_done + cam_idx, 1u);
-    }
     __syncthreads();  // the next tile reuses the record buffers and lists
     if (!a.tile_ticket) break;  // one tile per CTA
     }
 }
 
-void launch_raster(const RasterArgs& a_in, uint32_t n_tiles, cudaStream_t stream) {
-    if (n_tiles == 0) return;
+void launch_raster(const RasterArgs& a_in, uint32_t tile_end, cudaStream_t stream) {
+    if (tile_end <= a_in.tile_begin) return;
     RasterArgs a = a_in;
-    a.n_tiles = n_tiles;
+    a.n_tiles = tile_end;
+    uint32_t n_tiles = tile_end - a.tile_begin;
     const bool small = a.batch == 128;
     // capped grid: the CTAs loop over the tiles (leaves room on every SM for other contexts'
     // kernels); 0 = one CTA per tile

@@ -95,8 +95,8 @@ def test_interleaved_device_frames_equal_sequential(oracle):
 
 
 def test_overlapped_copies_equal_frame_copies(oracle, monkeypatch):
-    """render() copies camera c while later cameras are composited (per-camera tile counters +
-    cuStreamWaitValue32); GSIM_GPU_OVERLAP_COPIES=0 copies after the frame. Same bytes, including
+    """render() copies camera c while later cameras are composited (one raster launch per camera,
+    the copy stream waits on its event); GSIM_GPU_OVERLAP_COPIES=0 copies after the frame. Same bytes, including
     multi-group batches (40 cameras -> several camera groups) and back-to-back frames."""
     field, cams, frames = scene_and_frames(oracle, 3)
     many = []
@@ -142,14 +142,12 @@ def test_pinned_and_pageable_targets_agree(oracle):
 
 
 def test_overlapped_copies_never_stale(oracle):
-    """The per-camera copies start when the camera's tile counter says every tile is composited
-    (raster epilogue: GPU-scope fence, then the counter). Stress that handoff: 4 contexts on 4
+    """The per-camera copies start on the event after the camera's raster launch. Stress that
+    handoff (and, before it used events, a stream-wait-value handoff hung here about once in ten
+    longer runs): 4 contexts on 4
     threads render 24 frames each into page-locked targets reused frame after frame, so a copy
     that overtook a tile's pixel stores would leave the previous frame's pixels in the target.
-    Every frame must equal the same frame rendered alone. (A regression guard: the copy starts
-    microseconds after the counter is seen, far longer than the fence's window; even a build
-    without the fence passed this test, so the fence's scope rests on the L2 argument in
-    raster.cu.)"""
+    Every frame must equal the same frame rendered alone."""
     import torch
     from paper_2507_21981_b200 import RenderTarget
     field, cams, frames = scene_and_frames(oracle, 12)

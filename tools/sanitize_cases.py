@@ -4,8 +4,8 @@ mechanism of the path, run under memcheck / racecheck / synccheck by tools/sanit
     python tools/sanitize_cases.py smoke|copies|contexts|batch|determinism
 
 smoke     __graft_entry__.smoke(): K2, key_hist, onesweep look-back, binning, scatter, raster
-copies    3-camera render into host targets: per-camera tile counters + system fence +
-          cuStreamWaitValue32 copy handoff (raster.cu epilogue, host.cu queue_camera_copies),
+copies    3-camera render into host targets: one raster launch per camera, each camera's copies
+          waiting on its event (host.cu launch_raster_stage / queue_camera_copies),
           then render_encoded (the same handoff for encoded blocks)
 contexts  two contexts rendering concurrently from two host threads (shared device, separate
           streams and workspaces)
