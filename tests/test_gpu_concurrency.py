@@ -181,3 +181,40 @@ def test_overlapped_copies_never_stale(oracle):
         t.join()
     assert not errors, errors
     assert not bad, bad
+
+
+def test_threaded_encoded_renders_equal_single(oracle):
+    """render_encoded from 3 contexts on 3 host threads (each camera's encoded block copied on
+    the event after its raster launch, into pinned and into pageable blobs) gives the bytes of the
+    same frames encoded by one context alone."""
+    import torch
+    from paper_2507_21981_b200 import EncodeOptions
+    field, cams, frames = scene_and_frames(oracle, 6)
+    eo = EncodeOptions()
+    solo = Context(0)
+    s0 = solo.upload(field)
+    want = [solo.render_encoded(s0, nodes, cams, None, eo) for nodes in frames]
+    ctxs = [Context(0) for _ in range(3)]
+    scenes = [c.upload(field) for c in ctxs]
+    nbytes = want[0].size
+    bad, errors = [], []
+
+    def worker(k):
+        try:
+            blob = (torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy() if k % 2 == 0
+                    else np.empty(nbytes, dtype=np.uint8))
+            for rep in range(8):
+                i = (k + rep) % len(frames)
+                got = ctxs[k].render_encoded(scenes[k], frames[i], cams, None, eo, out=blob)
+                if not np.array_equal(got, want[i]):
+                    bad.append((k, rep, i))
+        except Exception as e:  # noqa: BLE001 (reported below)
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert not bad, bad
